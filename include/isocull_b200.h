@@ -1,0 +1,256 @@
+/*
+ * isocull_b200.h — C ABI of the B200-native accelerated PIFu inference path.
+ *
+ * This is the drop-in boundary for the reference's hot path.
+ * The reference (/root/reference/proj/include/isocull) is a header-only C++20
+ * library; its operators take a `FieldOracle` (std::function plugin) and return
+ * results by value.  A std::function cannot run on a GPU, so the field is
+ * described here by data (primitives, feature map, MLP weights) and the
+ * operators run as hand-written sm_100a kernels behind these entry points.
+ *
+ * Every entry point below names the reference interface it replaces.
+ * Conventions that hold for all of them:
+ *   - plain pointers and sizes only; no C++ or torch types cross the ABI;
+ *   - errors never throw: each call returns an ICG_* status and leaves a
+ *     thread-local message readable through icg_last_error();
+ *   - ICG_EINVAL  ≙ std::invalid_argument (reference CLI exit code 2,
+ *                   tools/isocull_cli.cpp:358-364),
+ *     ICG_ERUNTIME ≙ std::runtime_error   (reference CLI exit code 1);
+ *   - calls are synchronous with respect to the host, like the reference
+ *     operators (results are complete when the call returns);
+ *   - one host thread drives one context at a time; distinct contexts (one per
+ *     GPU) may be driven concurrently (reference operators are re-entrant).
+ */
+#ifndef ISOCULL_B200_H
+#define ISOCULL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ICG_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------ */
+#define ICG_OK 0
+#define ICG_ERUNTIME 1 /* runtime_error: CUDA failure, I/O (isocull_cli.cpp:362-364) */
+#define ICG_EINVAL 2   /* invalid_argument: bad config / field (isocull_cli.cpp:358-361) */
+#define ICG_ECAPACITY 3 /* a device work list overflowed its capacity */
+#define ICG_ENODEV 4   /* no CUDA device / extension unusable */
+
+/* ---- limits ------------------------------------------------------------ */
+#define ICG_MAX_LEVELS 16      /* AlgoConfig target_level bound (cells <= 1024, localize.hpp:50) */
+#define ICG_MAX_PRIMS 64
+#define ICG_MAX_TARGET_CELLS 1024 /* validate_config, localize.hpp:50-51 */
+
+/* ---- memory locations for caller-provided buffers ----------------------- */
+#define ICG_MEM_HOST 0
+#define ICG_MEM_DEVICE 1
+
+/* ---- node states: NodeState, grid.hpp:15 -------------------------------- */
+#define ICG_STATE_UNKNOWN 0
+#define ICG_STATE_INTERPOLATED 1
+#define ICG_STATE_EVALUATED 2
+#define ICG_STATE_SHADOW 3
+
+/* ---- analytic scene: SceneSpec / Primitive, scene.hpp:27-103 ------------ */
+#define ICG_PRIM_SPHERE 0
+#define ICG_PRIM_BOX 1
+#define ICG_PRIM_CAPSULE 2
+#define ICG_PRIM_TORUS 3
+
+typedef struct icg_primitive {
+    int32_t kind;             /* ICG_PRIM_* (PrimitiveKind, scene.hpp:25) */
+    int32_t rotated;          /* nonzero: apply inv_rotation to (p - center) */
+    double center[3];         /* sphere / box / torus */
+    double a[3], b[3];        /* capsule segment endpoints, world coordinates */
+    double radius;            /* sphere / capsule */
+    double half[3];           /* box half extents */
+    double major, minor;      /* torus radii (ring in the local xz plane) */
+    double inv_rotation[9];   /* row-major world->local (Primitive::inv_rotation) */
+} icg_primitive;
+
+/* Union-only CSG of primitives (the default tree of parse_scene,
+ * scene.hpp:308-317; every bundled scene and the config-0 capsule figure use
+ * it).  signed_distance = min over primitives (scene.hpp:130-146). */
+typedef struct icg_scene {
+    const icg_primitive* prims;
+    int32_t n_prims;
+    double tau; /* occupancy_from_distance(d, tau) = 1/(1+exp(d/tau)), field.hpp:81 */
+} icg_scene;
+
+/* ---- field descriptor: replaces FieldOracle (field.hpp:22-77) ------------ */
+#define ICG_FIELD_ANALYTIC 0 /* O(P) = 1/(1+exp(sdf(P)/tau)) on device (config 0) */
+#define ICG_FIELD_PIFU 1     /* O(P) = sigmoid(f_O(Phi(P_xy), P_z) - sdf_scale*sdf(P)) (configs 1-4) */
+
+#define ICG_PREC_FP32 0      /* tcgen05 bf16x3 split products, fp32 accumulation (configs 1, 2, 4) */
+#define ICG_PREC_BF16 1      /* tcgen05 bf16 operands, fp32 accumulation (config 3) */
+#define ICG_PREC_FP32_SIMT 2 /* CUDA-core fp32 FFMA path (correctness cross-check) */
+
+typedef struct icg_field {
+    int32_t kind;              /* ICG_FIELD_* */
+    icg_scene scene;           /* analytic field, or the capsule figure biasing the PIFu logit */
+    double sdf_scale;          /* PIFu: logit += -sdf_scale * sdf(P)   (50 in BASELINE configs 1-4) */
+    const float* feature_map;  /* PIFu: C x H x W fp32, channel-major (g_O(I)) */
+    int32_t fmap_c, fmap_h, fmap_w;
+    int32_t fmap_mem;          /* ICG_MEM_HOST (copied H2D inside the call) or ICG_MEM_DEVICE */
+    int32_t precision;         /* ICG_PREC_* */
+} icg_field;
+
+/* ---- MLP weights (f_O / f_T; not in the reference) */
+#define ICG_MLP_GEOMETRY 0 /* 257->1024->512->256->128->1, skip-concat of the 257-d input */
+#define ICG_MLP_TEXTURE 1  /* 513->1024->512->256->128->3, skip-concat of the 513-d input */
+#define ICG_MLP_LAYERS 5
+
+/* weights[l]: fp32 row-major [out_dims[l]][in_dims[l]] where in_dims[l] =
+ * (l==0 ? 0 : out_dims[l-1]) + skip_dim; the previous layer's activations come
+ * first, the skip input last.  biases[l]: fp32 [out_dims[l]].  Host memory. */
+typedef struct icg_mlp_desc {
+    int32_t which;             /* ICG_MLP_* */
+    int32_t n_layers;          /* must be ICG_MLP_LAYERS */
+    int32_t skip_dim;          /* 257 (geometry) or 513 (texture) */
+    int32_t out_dims[ICG_MLP_LAYERS];
+    const float* weights[ICG_MLP_LAYERS];
+    const float* biases[ICG_MLP_LAYERS];
+    float leaky_slope;         /* 0.02 */
+} icg_mlp_desc;
+
+/* ---- algorithm config: AlgoConfig, localize.hpp:36-45 -------------------- */
+#define ICG_VARIANT_BRUTE 0
+#define ICG_VARIANT_PROGRESSIVE 3 /* Variant enum order, localize.hpp:16 */
+
+typedef struct icg_algo_config {
+    int32_t variant;           /* ICG_VARIANT_PROGRESSIVE or ICG_VARIANT_BRUTE */
+    int32_t coarsest_cells;    /* R_0 (>= 2) */
+    int32_t target_level;      /* L; R_L = R_0 * 2^L <= 1024 */
+    int32_t max_conflict_iters;/* 0 = one axis length per level (localize.hpp:339) */
+    int32_t conflict_pass;     /* 0 = ablation (localize.hpp:42, 335-336) */
+} icg_algo_config;
+
+/* ---- extraction result: ExtractionResult, localize.hpp:57-64 ------------- */
+typedef struct icg_extraction {
+    /* caller-provided output buffers; NULL = not requested.  All (R_L+1)^3,
+     * x-fastest (grid.hpp:45-48). */
+    int32_t mem;               /* ICG_MEM_HOST or ICG_MEM_DEVICE for the arrays below */
+    float* values;             /* LevelGrid::values at level L */
+    uint8_t* states;           /* LevelGrid::states (ICG_STATE_*) */
+    uint8_t* binarized;        /* value >= 0.5f (binarized_volume, localize.hpp:154-158) */
+    /* always filled (host scalars) */
+    int32_t cells;             /* R_L */
+    int32_t levels;            /* L + 1 */
+    uint64_t evals_per_level[ICG_MAX_LEVELS];
+    uint64_t total_evals;
+    uint64_t refined_cells_per_level[ICG_MAX_LEVELS]; /* coarse cells of level l-1 whose 8 binarized corners disagree */
+    uint32_t conflict_iters_per_level[ICG_MAX_LEVELS];
+    int32_t conflict_warning;  /* conflict pass hit its bound (localize.hpp:343-346) */
+    double wall_seconds;       /* device time of the whole extraction */
+} icg_extraction;
+
+/* ---- camera: CameraSpec, render.hpp:19-46 -------------------------------- */
+typedef struct icg_camera {
+    double rotation[9];        /* row-major world->view */
+    double translation[3];
+    double scale;              /* weak-perspective x,y scale; 1 = orthographic */
+} icg_camera;
+
+/* ---- rendered image: RenderedImage, render.hpp:50-59 --------------------- */
+typedef struct icg_image {
+    int32_t mem;               /* ICG_MEM_HOST or ICG_MEM_DEVICE for the arrays below */
+    float* depth;              /* W*H view z; -2 where uncovered (render.hpp:72) */
+    float* rgb;                /* W*H*3, clamp01(T(P)) or background */
+    uint8_t* mask;             /* W*H coverage */
+    int32_t* surface_k;        /* W*H first-crossing sample index, -1 where uncovered */
+    /* always filled */
+    uint64_t covered_pixels;
+    uint64_t degenerate_brackets; /* equal-occupancy brackets clamped to the occupied sample */
+    uint64_t grazing_pixels;      /* fractional samples that never reach 0.5 */
+    uint64_t texture_points;      /* texture-MLP evaluations (= covered pixels) */
+    double wall_seconds;
+} icg_image;
+
+/* ======================================================================== */
+/* Context lifecycle                                                         */
+/* ======================================================================== */
+typedef struct icg_context icg_context;
+
+int icg_abi_version(void);
+const char* icg_last_error(void);
+int icg_device_count(int* count);
+int icg_create(int device, icg_context** out);
+int icg_destroy(icg_context* ctx);
+
+/* Weight upload (library-owned device copies; packed for tcgen05 and SIMT). */
+int icg_set_mlp(icg_context* ctx, const icg_mlp_desc* desc);
+
+/* ======================================================================== */
+/* Operators                                                                 */
+/* ======================================================================== */
+
+/* extract(oracle, cfg, workers) -> ExtractionResult (localize.hpp:365-373):
+ * progressive localization (extract_progressive, localize.hpp:315-363) or
+ * dense brute force (extract_brute_force, localize.hpp:181-193).  The final
+ * grid also stays resident in the context for icg_render_localized. */
+int icg_extract(icg_context* ctx, const icg_field* field, const icg_algo_config* cfg,
+                icg_extraction* out);
+
+/* Mesh-free render through the grid localized by the last icg_extract on this
+ * context (north-star renderer, following the
+ * argmax/bracket/depth conventions of render.hpp:140-206 and the texture
+ * lookup of render_view, render.hpp:244-280).  background: 3 floats. */
+int icg_render_localized(icg_context* ctx, const icg_field* field, const icg_camera* camera,
+                         int width, int height, const float* background, icg_image* out);
+
+/* One frame = icg_extract + icg_render_localized in a single call
+ * (BASELINE configs 2-4).  Either output may be NULL. */
+int icg_frame(icg_context* ctx, const icg_field* field, const icg_algo_config* cfg,
+              const icg_camera* camera, int width, int height, const float* background,
+              icg_extraction* ext_out, icg_image* img_out);
+
+/* Direct field evaluation: FieldOracle::occupancy_batch (field.hpp:41-47) and
+ * texture_batch (field.hpp:56-63).  points: n x 3 doubles (NDC).  Outputs are
+ * host or device per `mem`; occupancy as fp32 (the value the grid stores,
+ * localize.hpp:86), rgb as fp32 n x 3 (unclamped sigmoid output). */
+int icg_occupancy_batch(icg_context* ctx, const icg_field* field, const double* points,
+                        size_t n, int mem, float* out);
+int icg_texture_batch(icg_context* ctx, const icg_field* field, const double* points,
+                      size_t n, int mem, float* out_rgb);
+
+/* compare_iou (localize.hpp:377-387) on device or host arrays of n bytes. */
+int icg_compare_iou(icg_context* ctx, const uint8_t* a, const uint8_t* b, size_t n, int mem,
+                    double* iou);
+
+/* ======================================================================== */
+/* Host helpers                                                              */
+/* ======================================================================== */
+
+/* Pinned host buffers for end-to-end (host-buffer) calls. */
+int icg_host_alloc(size_t bytes, void** ptr);
+int icg_host_free(void* ptr);
+int icg_device_alloc(icg_context* ctx, size_t bytes, void** ptr);
+int icg_device_free(icg_context* ctx, void* ptr);
+int icg_memcpy(icg_context* ctx, void* dst, const void* src, size_t bytes, int dst_mem, int src_mem);
+
+/* Seeded synthetic inputs; Rng = mt19937_64 with the
+ * reference's hand-rolled uniform / Box-Muller (random.hpp:16-43). */
+/* 15-capsule stick figure: per capsule a.xyz, b.xyz ~ U[-0.5,0.5], r ~ U[0.03,0.08]. */
+int icg_gen_capsules(uint64_t seed, int n, icg_primitive* out);
+/* n standard normals in generation order. */
+int icg_gen_normals(uint64_t seed, size_t n, float* out);
+/* Kaiming-uniform MLP: per layer W ~ U(-g*sqrt(3/fan_in), +), g = sqrt(2/(1+slope^2)),
+ * then b ~ U(-1/sqrt(fan_in), +).  weights_out / biases_out hold room for
+ * sum(out*in) / sum(out) floats; layer l starts where l-1 ends. */
+int icg_gen_mlp(uint64_t seed, int which, float* weights_out, float* biases_out);
+/* Sizes for icg_gen_mlp and icg_set_mlp: fills out_dims/in_dims and totals. */
+int icg_mlp_shape(int which, int32_t* out_dims, int32_t* in_dims, int32_t* skip_dim,
+                  size_t* n_weights, size_t* n_biases);
+
+/* Camera from angles, CameraSpec::from_angles (render.hpp:36-45). */
+int icg_camera_from_angles(double yaw_deg, double pitch_deg, double dist, double scale,
+                           icg_camera* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISOCULL_B200_H */

@@ -1,0 +1,273 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// A thin extern "C" shim over the UNMODIFIED reference headers
+// (/root/reference/proj/include/isocull/*.hpp, compiled read-only where they
+// lie; nothing is copied into this repo).  Built by oracle/Makefile into
+// oracle/_ref/libisocull_ref.so.  It lets the tests (and bench.py's
+// --impl reference arm) run the reference's own operators:
+//   extract / extract_progressive / extract_brute_force ... localize.hpp:181-373
+//   render_view (view-aligned reference renderer) ........... render.hpp:244-280
+//   grid primitives ......................................... grid.hpp:87-197
+//   Rng ..................................................... random.hpp:16-43
+//   scene JSON loading ...................................... scene.hpp:302-333
+// with the field supplied as a C callback wrapped in the reference's own
+// FieldOracle (field.hpp:22-77), so the reference's call counter and
+// parallel_for drive evaluation exactly as they do in the reference.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "isocull/field.hpp"
+#include "isocull/grid.hpp"
+#include "isocull/localize.hpp"
+#include "isocull/random.hpp"
+#include "isocull/render.hpp"
+#include "isocull/scene.hpp"
+
+#include "../include/isocull_b200.h"
+
+using namespace isocull;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(const std::exception& e, int code) {
+    g_err = e.what();
+    return code;
+}
+}  // namespace
+
+extern "C" {
+
+typedef double (*ref_pt_occ_fn)(void* user, const double* p);
+typedef void (*ref_pt_tex_fn)(void* user, const double* p, double* rgb);
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+static FieldOracle make_oracle(ref_pt_occ_fn occ, ref_pt_tex_fn tex, void* user) {
+    FieldOracle::OccupancyFn o = [occ, user](const Vec3& p) {
+        double q[3] = {p.x, p.y, p.z};
+        return occ(user, q);
+    };
+    FieldOracle::TextureFn t;
+    if (tex)
+        t = [tex, user](const Vec3& p) {
+            double q[3] = {p.x, p.y, p.z}, c[3];
+            tex(user, q, c);
+            return Vec3{c[0], c[1], c[2]};
+        };
+    return FieldOracle(std::move(o), std::move(t));
+}
+
+// extract(oracle, cfg, workers), localize.hpp:365-373
+int ref_extract(ref_pt_occ_fn occ, void* user, int variant, double threshold, int coarsest, int level,
+                int max_conflict_iters, int conflict_pass, int workers, float* values, uint8_t* states,
+                uint8_t* binarized, uint64_t* evals_per_level, uint64_t* total_evals, uint64_t* oracle_calls,
+                int* conflict_warning, double* wall_seconds) {
+    try {
+        FieldOracle oracle = make_oracle(occ, nullptr, user);
+        AlgoConfig cfg;
+        cfg.variant = static_cast<Variant>(variant);
+        cfg.threshold = threshold;
+        cfg.coarsest_cells = coarsest;
+        cfg.target_level = level;
+        cfg.max_conflict_iters = max_conflict_iters;
+        cfg.conflict_pass = conflict_pass != 0;
+        ExtractionResult r = extract(oracle, cfg, workers);
+        if (values) std::memcpy(values, r.grid.values.data(), r.grid.values.size() * sizeof(float));
+        if (states) std::memcpy(states, r.grid.states.data(), r.grid.states.size());
+        if (binarized) std::memcpy(binarized, r.binarized.data(), r.binarized.size());
+        for (std::size_t l = 0; l < r.evals_per_level.size() && l < 16; ++l) evals_per_level[l] = r.evals_per_level[l];
+        *total_evals = r.total_evals;
+        *oracle_calls = oracle.calls();
+        *conflict_warning = r.conflict_warning ? 1 : 0;
+        *wall_seconds = r.wall_seconds;
+        return ICG_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, ICG_EINVAL);
+    } catch (const std::exception& e) {
+        return fail(e, ICG_ERUNTIME);
+    }
+}
+
+// render_view(oracle, camera, cfg, background, workers), render.hpp:244-280
+int ref_render_view(ref_pt_occ_fn occ, ref_pt_tex_fn tex, void* user, double yaw, double pitch, double dist,
+                    double scale, int coarsest, int level, const double* bg, int workers, double* depth,
+                    double* rgb, uint8_t* mask, uint64_t* oracle_calls, int* degenerate, int* grazing,
+                    int* size) {
+    try {
+        FieldOracle oracle = make_oracle(occ, tex, user);
+        AlgoConfig cfg;
+        cfg.variant = Variant::progressive;
+        cfg.coarsest_cells = coarsest;
+        cfg.target_level = level;
+        CameraSpec cam = CameraSpec::from_angles(yaw, pitch, dist, scale);
+        RenderedImage img = render_view(oracle, cam, cfg, Vec3{bg[0], bg[1], bg[2]}, workers);
+        std::size_t n = img.depth.size();
+        if (depth) std::memcpy(depth, img.depth.data(), n * sizeof(double));
+        if (mask) std::memcpy(mask, img.mask.data(), n);
+        if (rgb)
+            for (std::size_t i = 0; i < n; ++i) {
+                rgb[3 * i] = img.rgb[i].x;
+                rgb[3 * i + 1] = img.rgb[i].y;
+                rgb[3 * i + 2] = img.rgb[i].z;
+            }
+        *oracle_calls = img.oracle_calls;
+        *degenerate = img.degenerate_brackets;
+        *grazing = img.grazing_pixels;
+        *size = img.width;
+        return ICG_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, ICG_EINVAL);
+    } catch (const std::exception& e) {
+        return fail(e, ICG_ERUNTIME);
+    }
+}
+
+// CameraSpec::from_angles, render.hpp:36-45
+void ref_camera_from_angles(double yaw, double pitch, double dist, double scale, double* rot9, double* t3) {
+    CameraSpec c = CameraSpec::from_angles(yaw, pitch, dist, scale);
+    for (int i = 0; i < 9; ++i) rot9[i] = c.rotation.m[i];
+    t3[0] = c.translation.x;
+    t3[1] = c.translation.y;
+    t3[2] = c.translation.z;
+}
+
+// ---- scenes (scene.hpp) ----------------------------------------------------
+struct RefScene {
+    SceneSpec spec;
+};
+
+void* ref_scene_load(const char* path) {
+    try {
+        return new RefScene{load_scene(path)};
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void* ref_scene_capsules(const icg_primitive* prims, int n, double tau) {
+    auto* s = new RefScene;
+    for (int i = 0; i < n; ++i) {
+        Primitive p;
+        p.kind = PrimitiveKind::capsule;
+        p.capsule_a = {prims[i].a[0], prims[i].a[1], prims[i].a[2]};
+        p.capsule_b = {prims[i].b[0], prims[i].b[1], prims[i].b[2]};
+        p.radius = prims[i].radius;
+        s->spec.primitives.push_back(p);
+        CsgNode leaf;
+        leaf.prim = i;
+        s->spec.csg.children.push_back(leaf);
+    }
+    s->spec.csg.op = CsgOp::union_op;
+    s->spec.tau = tau;
+    return s;
+}
+
+void ref_scene_free(void* s) { delete static_cast<RefScene*>(s); }
+
+// Exports the (union-only) primitive list in the C ABI layout; returns -1 if
+// the scene uses a non-union CSG tree.
+int ref_scene_export(void* handle, icg_primitive* out, int max, double* tau, int* has_texture) {
+    auto* s = static_cast<RefScene*>(handle);
+    const SceneSpec& sc = s->spec;
+    if (sc.csg.prim >= 0 || sc.csg.op != CsgOp::union_op) return -1;
+    for (const auto& c : sc.csg.children)
+        if (c.prim < 0) return -1;
+    int n = static_cast<int>(sc.primitives.size());
+    if (n > max) return -1;
+    for (int i = 0; i < n; ++i) {
+        const Primitive& p = sc.primitives[i];
+        icg_primitive& o = out[i];
+        std::memset(&o, 0, sizeof(o));
+        o.kind = static_cast<int32_t>(p.kind);
+        o.rotated = p.rotated ? 1 : 0;
+        o.center[0] = p.center.x, o.center[1] = p.center.y, o.center[2] = p.center.z;
+        o.a[0] = p.capsule_a.x, o.a[1] = p.capsule_a.y, o.a[2] = p.capsule_a.z;
+        o.b[0] = p.capsule_b.x, o.b[1] = p.capsule_b.y, o.b[2] = p.capsule_b.z;
+        o.radius = p.radius;
+        o.half[0] = p.half.x, o.half[1] = p.half.y, o.half[2] = p.half.z;
+        o.major = p.major, o.minor = p.minor;
+        for (int k = 0; k < 9; ++k) o.inv_rotation[k] = p.inv_rotation.m[k];
+    }
+    *tau = sc.tau;
+    *has_texture = sc.has_texture() ? 1 : 0;
+    return n;
+}
+
+// FieldOracle-shaped callbacks over a loaded scene (build_oracle, field.hpp:83-91)
+double ref_scene_occ(void* handle, const double* p) {
+    auto* s = static_cast<RefScene*>(handle);
+    return occupancy_from_distance(s->spec.signed_distance(Vec3{p[0], p[1], p[2]}), s->spec.tau);
+}
+
+void ref_scene_tex(void* handle, const double* p, double* rgb) {
+    auto* s = static_cast<RefScene*>(handle);
+    Vec3 c = s->spec.texture_color(Vec3{p[0], p[1], p[2]});
+    rgb[0] = c.x, rgb[1] = c.y, rgb[2] = c.z;
+}
+
+double ref_scene_sdf(void* handle, const double* p) {
+    return static_cast<RefScene*>(handle)->spec.signed_distance(Vec3{p[0], p[1], p[2]});
+}
+
+// ---- grid primitives (grid.hpp) --------------------------------------------
+int ref_upsample(int level, int cells, const float* values, const uint8_t* states, float* out_values,
+                 uint8_t* out_states) {
+    try {
+        LevelGrid g = LevelGrid::make(level, cells);
+        std::memcpy(g.values.data(), values, g.values.size() * sizeof(float));
+        std::memcpy(g.states.data(), states, g.states.size());
+        LevelGrid f = upsample_interpolate(g);
+        std::memcpy(out_values, f.values.data(), f.values.size() * sizeof(float));
+        std::memcpy(out_states, f.states.data(), f.states.size());
+        return ICG_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, ICG_EINVAL);
+    }
+}
+
+void ref_binarize(std::size_t n, const float* in, float* out) {
+    for (std::size_t i = 0; i < n; ++i) out[i] = binarize_value(in[i]);
+}
+
+void ref_boundary_candidates(int cells, const float* values, uint8_t* mask) {
+    LevelGrid g = LevelGrid::make(0, cells, NodeState::evaluated);
+    std::memcpy(g.values.data(), values, g.values.size() * sizeof(float));
+    NodeMask m = boundary_candidates(g);
+    std::memcpy(mask, m.bits.data(), m.bits.size());
+}
+
+void ref_dilate(int nodes, const uint8_t* in, uint8_t* out) {
+    NodeMask m = NodeMask::make(nodes);
+    std::memcpy(m.bits.data(), in, m.bits.size());
+    NodeMask d = dilate_1ring(m);
+    std::memcpy(out, d.bits.data(), d.bits.size());
+}
+
+void ref_argmax_z(int cells, const float* values, float* max_value, int* max_index) {
+    LevelGrid g = LevelGrid::make(0, cells, NodeState::evaluated);
+    std::memcpy(g.values.data(), values, g.values.size() * sizeof(float));
+    ArgmaxZ a = argmax_z(g);
+    std::memcpy(max_value, a.max_value.data(), a.max_value.size() * sizeof(float));
+    std::memcpy(max_index, a.max_index.data(), a.max_index.size() * sizeof(int));
+}
+
+double ref_compare_iou(const uint8_t* a, const uint8_t* b, std::size_t n) {
+    return compare_iou(std::span<const uint8_t>(a, n), std::span<const uint8_t>(b, n));
+}
+
+// ---- Rng (random.hpp) --------------------------------------------------------
+void ref_rng_uniforms(uint64_t seed, std::size_t n, double* out) {
+    Rng r(seed);
+    for (std::size_t i = 0; i < n; ++i) out[i] = r.uniform();
+}
+
+void ref_rng_normals(uint64_t seed, std::size_t n, double* out) {
+    Rng r(seed);
+    for (std::size_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+
+}  // extern "C"

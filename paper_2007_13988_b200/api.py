@@ -1,0 +1,405 @@
+"""Reference-shaped host API over the C ABI (the Python face of the drop-in).
+
+Mirrors the reference's operator surface (/root/reference/proj/include/isocull):
+
+  reference                                   here
+  ------------------------------------------  ------------------------------------------
+  FieldOracle (field.hpp:22-77)               AnalyticField / PifuField (device data)
+  AlgoConfig, validate_config (localize:36)   AlgoConfig (same fields, same errors)
+  ExtractionResult (localize.hpp:57-64)       ExtractionResult
+  extract / extract_progressive /             extract / extract_progressive /
+    extract_brute_force (localize:181-373)      extract_brute_force
+  compare_iou, acceleration_factor            compare_iou, acceleration_factor
+  CameraSpec::from_angles (render.hpp:36)     CameraSpec.from_angles
+  render_view -> RenderedImage (render:244)   render_view -> RenderedImage (first-crossing
+                                                through the localized world grid)
+
+Errors follow the reference: std::invalid_argument -> ValueError,
+std::runtime_error -> RuntimeError.  All work runs in the sm_100a library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import abi
+
+GEO_OUT = (1024, 512, 256, 128, 1)
+TEX_OUT = (1024, 512, 256, 128, 3)
+GEO_SKIP, TEX_SKIP = 257, 513
+
+
+def _check(rc: int) -> None:
+    if rc == abi.ICG_OK:
+        return
+    msg = abi.lib().icg_last_error().decode(errors="replace")
+    if rc == abi.ICG_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"isocull_b200 error {rc}: {msg}")
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+# ---------------------------------------------------------------------------
+# Fields (FieldOracle surrogates)
+# ---------------------------------------------------------------------------
+def capsule_prims(caps: np.ndarray) -> list:
+    """caps: (n, 7) array of a.xyz, b.xyz, r."""
+    out = []
+    for row in np.asarray(caps, dtype=np.float64):
+        p = abi.icg_primitive()
+        p.kind = abi.ICG_PRIM_CAPSULE
+        p.a[:] = row[0:3]
+        p.b[:] = row[3:6]
+        p.radius = row[6]
+        p.inv_rotation[0] = p.inv_rotation[4] = p.inv_rotation[8] = 1.0
+        out.append(p)
+    return out
+
+
+class _Field:
+    def __init__(self):
+        self._prims = None
+        self._fmap = None
+        self.c = abi.icg_field()
+
+    def _set_prims(self, prims: Sequence[abi.icg_primitive], tau: float):
+        arr = (abi.icg_primitive * max(1, len(prims)))(*prims)
+        self._prims = arr
+        self.c.scene.prims = C.cast(arr, C.POINTER(abi.icg_primitive))
+        self.c.scene.n_prims = len(prims)
+        self.c.scene.tau = tau
+
+
+class AnalyticField(_Field):
+    """O(P) = 1/(1+exp(sdf(P)/tau)) over a union of primitives (build_oracle, field.hpp:83-91)."""
+
+    def __init__(self, prims: Sequence[abi.icg_primitive], tau: float):
+        super().__init__()
+        self.c.kind = abi.ICG_FIELD_ANALYTIC
+        self._set_prims(prims, tau)
+
+
+class PifuField(_Field):
+    """O(P) = sigmoid(f_O(Phi(P_xy), P_z) - sdf_scale * sdf(P)) (BASELINE configs 1-4)."""
+
+    def __init__(self, feature_map, capsules: Sequence[abi.icg_primitive], sdf_scale: float = 50.0,
+                 precision: int = abi.ICG_PREC_FP32, device_ptr: Optional[int] = None,
+                 shape: Optional[tuple] = None):
+        super().__init__()
+        self.c.kind = abi.ICG_FIELD_PIFU
+        self._set_prims(capsules, 0.02)
+        self.c.sdf_scale = sdf_scale
+        self.c.precision = precision
+        if device_ptr is not None:
+            ch, hh, ww = shape
+            self.c.feature_map = C.cast(C.c_void_p(device_ptr), abi.f32p)
+            self.c.fmap_mem = abi.ICG_MEM_DEVICE
+        else:
+            fm = np.ascontiguousarray(feature_map, dtype=np.float32)
+            self._fmap = fm
+            ch, hh, ww = fm.shape
+            self.c.feature_map = _ptr(fm, C.c_float)
+            self.c.fmap_mem = abi.ICG_MEM_HOST
+        self.c.fmap_c, self.c.fmap_h, self.c.fmap_w = ch, hh, ww
+
+
+# ---------------------------------------------------------------------------
+# Config / results
+# ---------------------------------------------------------------------------
+@dataclass
+class AlgoConfig:
+    variant: str = "progressive"
+    coarsest_cells: int = 16
+    target_level: int = 3
+    max_conflict_iters: int = 0
+    conflict_pass: bool = True
+
+    def target_cells(self) -> int:
+        return self.coarsest_cells << self.target_level
+
+    def to_c(self) -> abi.icg_algo_config:
+        v = {"progressive": abi.ICG_VARIANT_PROGRESSIVE, "brute": abi.ICG_VARIANT_BRUTE}.get(self.variant)
+        if v is None:
+            raise ValueError(f"unknown variant '{self.variant}'")
+        return abi.icg_algo_config(v, self.coarsest_cells, self.target_level, self.max_conflict_iters,
+                                   1 if self.conflict_pass else 0)
+
+
+@dataclass
+class ExtractionResult:
+    cells: int
+    values: Optional[np.ndarray]
+    states: Optional[np.ndarray]
+    binarized: Optional[np.ndarray]
+    evals_per_level: list
+    total_evals: int
+    refined_cells_per_level: list
+    conflict_iters_per_level: list
+    conflict_warning: bool
+    wall_seconds: float
+
+
+@dataclass
+class CameraSpec:
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    scale: float = 1.0
+
+    @staticmethod
+    def from_angles(yaw_deg: float, pitch_deg: float, dist: float = 0.0, scale: float = 1.0) -> "CameraSpec":
+        cam = abi.icg_camera()
+        _check(abi.lib().icg_camera_from_angles(yaw_deg, pitch_deg, dist, scale, C.byref(cam)))
+        return CameraSpec(np.array(cam.rotation[:]).reshape(3, 3), np.array(cam.translation[:]), cam.scale)
+
+    def to_c(self) -> abi.icg_camera:
+        c = abi.icg_camera()
+        c.rotation[:] = [float(x) for x in np.asarray(self.rotation, dtype=np.float64).reshape(9)]
+        c.translation[:] = [float(x) for x in np.asarray(self.translation, dtype=np.float64).reshape(3)]
+        c.scale = float(self.scale)
+        return c
+
+
+@dataclass
+class RenderedImage:
+    width: int
+    height: int
+    rgb: np.ndarray          # (H, W, 3) float32
+    depth: np.ndarray        # (H, W) float32, -2 where uncovered
+    mask: np.ndarray         # (H, W) uint8
+    surface_k: np.ndarray    # (H, W) int32, -1 where uncovered
+    covered_pixels: int
+    degenerate_brackets: int
+    grazing_pixels: int
+    texture_points: int
+    wall_seconds: float
+
+
+# ---------------------------------------------------------------------------
+# Context and operators
+# ---------------------------------------------------------------------------
+class Context:
+    """One per GPU (icg_create / icg_destroy)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = abi.lib()
+        h = C.c_void_p()
+        _check(self._lib.icg_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self._lib.icg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # weights -----------------------------------------------------------------
+    def set_mlp(self, which: int, weights: Sequence[np.ndarray], biases: Sequence[np.ndarray], slope: float = 0.02):
+        outs = GEO_OUT if which == abi.ICG_MLP_GEOMETRY else TEX_OUT
+        skip = GEO_SKIP if which == abi.ICG_MLP_GEOMETRY else TEX_SKIP
+        d = abi.icg_mlp_desc()
+        d.which, d.n_layers, d.skip_dim = which, 5, skip
+        keep = []
+        for l in range(5):
+            w = np.ascontiguousarray(weights[l], dtype=np.float32)
+            b = np.ascontiguousarray(biases[l], dtype=np.float32)
+            keep += [w, b]
+            d.out_dims[l] = outs[l]
+            d.weights[l] = _ptr(w, C.c_float)
+            d.biases[l] = _ptr(b, C.c_float)
+        d.leaky_slope = slope
+        _check(self._lib.icg_set_mlp(self.h, C.byref(d)))
+
+    # operators -----------------------------------------------------------------
+    def extract(self, fld: _Field, cfg: AlgoConfig, want_grid: bool = True) -> ExtractionResult:
+        n = cfg.target_cells() + 1
+        out = abi.icg_extraction()
+        out.mem = abi.ICG_MEM_HOST
+        vals = sts = binz = None
+        if want_grid and cfg.target_cells() <= 1024:
+            vals = np.empty(n ** 3, np.float32)
+            sts = np.empty(n ** 3, np.uint8)
+            binz = np.empty(n ** 3, np.uint8)
+            out.values, out.states, out.binarized = _ptr(vals, C.c_float), _ptr(sts, C.c_uint8), _ptr(binz, C.c_uint8)
+        cc = cfg.to_c()
+        _check(self._lib.icg_extract(self.h, C.byref(fld.c), C.byref(cc), C.byref(out)))
+        return _extraction(out, cfg, vals, sts, binz)
+
+    def render_localized(self, fld: _Field, camera: CameraSpec, width: int, height: int,
+                         background=(0.0, 0.0, 0.0)) -> RenderedImage:
+        img, bufs = _image_bufs(width, height)
+        bg = np.asarray(background, dtype=np.float32)
+        cam = camera.to_c()
+        _check(self._lib.icg_render_localized(self.h, C.byref(fld.c), C.byref(cam), width, height,
+                                              _ptr(bg, C.c_float), C.byref(img)))
+        return _image(img, width, height, bufs)
+
+    def frame(self, fld: _Field, cfg: AlgoConfig, camera: CameraSpec, width: int, height: int,
+              background=(0.0, 0.0, 0.0), want_grid: bool = False):
+        n = cfg.target_cells() + 1
+        ext = abi.icg_extraction()
+        ext.mem = abi.ICG_MEM_HOST
+        vals = sts = binz = None
+        if want_grid:
+            vals = np.empty(n ** 3, np.float32)
+            sts = np.empty(n ** 3, np.uint8)
+            binz = np.empty(n ** 3, np.uint8)
+            ext.values, ext.states, ext.binarized = _ptr(vals, C.c_float), _ptr(sts, C.c_uint8), _ptr(binz, C.c_uint8)
+        img, bufs = _image_bufs(width, height)
+        bg = np.asarray(background, dtype=np.float32)
+        cam = camera.to_c()
+        cc = cfg.to_c()
+        _check(self._lib.icg_frame(self.h, C.byref(fld.c), C.byref(cc), C.byref(cam), width, height,
+                                   _ptr(bg, C.c_float), C.byref(ext), C.byref(img)))
+        return _extraction(ext, cfg, vals, sts, binz), _image(img, width, height, bufs)
+
+    def occupancy_batch(self, fld: _Field, points: np.ndarray) -> np.ndarray:
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        out = np.empty(len(pts), np.float32)
+        _check(self._lib.icg_occupancy_batch(self.h, C.byref(fld.c), _ptr(pts, C.c_double), len(pts),
+                                             abi.ICG_MEM_HOST, _ptr(out, C.c_float)))
+        return out
+
+    def texture_batch(self, fld: _Field, points: np.ndarray) -> np.ndarray:
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        out = np.empty((len(pts), 3), np.float32)
+        _check(self._lib.icg_texture_batch(self.h, C.byref(fld.c), _ptr(pts, C.c_double), len(pts),
+                                           abi.ICG_MEM_HOST, _ptr(out, C.c_float)))
+        return out
+
+    def compare_iou(self, a: np.ndarray, b: np.ndarray) -> float:
+        return compare_iou(a, b, self)
+
+
+def _extraction(out, cfg, vals, sts, binz) -> ExtractionResult:
+    L = cfg.target_level
+    return ExtractionResult(
+        cells=out.cells, values=vals, states=sts, binarized=binz,
+        evals_per_level=[int(out.evals_per_level[l]) for l in range(L + 1)],
+        total_evals=int(out.total_evals),
+        refined_cells_per_level=[int(out.refined_cells_per_level[l]) for l in range(L + 1)],
+        conflict_iters_per_level=[int(out.conflict_iters_per_level[l]) for l in range(L + 1)],
+        conflict_warning=bool(out.conflict_warning), wall_seconds=out.wall_seconds)
+
+
+def _image_bufs(w, h):
+    img = abi.icg_image()
+    img.mem = abi.ICG_MEM_HOST
+    bufs = dict(depth=np.empty(w * h, np.float32), rgb=np.empty(w * h * 3, np.float32),
+                mask=np.empty(w * h, np.uint8), surface_k=np.empty(w * h, np.int32))
+    img.depth = _ptr(bufs["depth"], C.c_float)
+    img.rgb = _ptr(bufs["rgb"], C.c_float)
+    img.mask = _ptr(bufs["mask"], C.c_uint8)
+    img.surface_k = _ptr(bufs["surface_k"], C.c_int32)
+    return img, bufs
+
+
+def _image(img, w, h, bufs) -> RenderedImage:
+    return RenderedImage(w, h, bufs["rgb"].reshape(h, w, 3), bufs["depth"].reshape(h, w),
+                         bufs["mask"].reshape(h, w), bufs["surface_k"].reshape(h, w), int(img.covered_pixels),
+                         int(img.degenerate_brackets), int(img.grazing_pixels), int(img.texture_points),
+                         img.wall_seconds)
+
+
+def extract(ctx: Context, fld: _Field, cfg: AlgoConfig) -> ExtractionResult:
+    """extract(oracle, cfg, workers), localize.hpp:365-373."""
+    return ctx.extract(fld, cfg)
+
+
+def extract_progressive(ctx: Context, fld: _Field, cfg: AlgoConfig) -> ExtractionResult:
+    cfg = AlgoConfig("progressive", cfg.coarsest_cells, cfg.target_level, cfg.max_conflict_iters, cfg.conflict_pass)
+    return ctx.extract(fld, cfg)
+
+
+def extract_brute_force(ctx: Context, fld: _Field, cfg: AlgoConfig) -> ExtractionResult:
+    cfg = AlgoConfig("brute", cfg.coarsest_cells, cfg.target_level)
+    return ctx.extract(fld, cfg)
+
+
+def render_view(ctx: Context, fld: _Field, camera: CameraSpec, cfg: AlgoConfig, width: int, height: int,
+                background=(0.0, 0.0, 0.0)) -> RenderedImage:
+    """Localize (progressive) then render through the localized grid (one icg_frame call)."""
+    return ctx.frame(fld, cfg, camera, width, height, background)[1]
+
+
+def compare_iou(a: np.ndarray, b: np.ndarray, ctx: Optional[Context] = None) -> float:
+    """compare_iou, localize.hpp:377-387 (dimension mismatch -> ValueError)."""
+    a = np.ascontiguousarray(a, dtype=np.uint8).reshape(-1)
+    b = np.ascontiguousarray(b, dtype=np.uint8).reshape(-1)
+    if a.size != b.size:
+        raise ValueError("compare_iou: dimension mismatch")
+    out = C.c_double()
+    _check(abi.lib().icg_compare_iou(ctx.h if ctx else None, _ptr(a, C.c_uint8), _ptr(b, C.c_uint8), a.size,
+                                     abi.ICG_MEM_HOST, C.byref(out)))
+    return out.value
+
+
+def acceleration_factor(result: ExtractionResult, brute: ExtractionResult) -> float:
+    """acceleration_factor, localize.hpp:389-393."""
+    if result.total_evals == 0 or brute.total_evals == 0:
+        raise ValueError("acceleration_factor: zero evaluation count")
+    return brute.total_evals / result.total_evals
+
+
+# ---------------------------------------------------------------------------
+# Seeded synthetic inputs (host helpers in the library)
+# ---------------------------------------------------------------------------
+def gen_capsules(seed: int, n: int = 15) -> list:
+    arr = (abi.icg_primitive * n)()
+    _check(abi.lib().icg_gen_capsules(seed, n, arr))
+    return list(arr)
+
+
+def capsules_array(prims) -> np.ndarray:
+    return np.array([[*p.a, *p.b, p.radius] for p in prims], dtype=np.float64)
+
+
+def gen_normals(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float32)
+    _check(abi.lib().icg_gen_normals(seed, n, _ptr(out, C.c_float)))
+    return out
+
+
+def gen_feature_map(seed: int, c: int = 256, h: int = 128, w: int = 128) -> np.ndarray:
+    return gen_normals(seed, c * h * w).reshape(c, h, w)
+
+
+def mlp_shape(which: int):
+    outs = (C.c_int32 * 5)()
+    ins = (C.c_int32 * 5)()
+    skip = C.c_int32()
+    nw, nb = C.c_size_t(), C.c_size_t()
+    _check(abi.lib().icg_mlp_shape(which, outs, ins, C.byref(skip), C.byref(nw), C.byref(nb)))
+    return list(outs), list(ins), skip.value, nw.value, nb.value
+
+
+def gen_mlp(seed: int, which: int):
+    """Kaiming-uniform weights (list of [out][in] float32) and biases."""
+    outs, ins, _, nw, nb = mlp_shape(which)
+    w = np.empty(nw, np.float32)
+    b = np.empty(nb, np.float32)
+    _check(abi.lib().icg_gen_mlp(seed, which, _ptr(w, C.c_float), _ptr(b, C.c_float)))
+    ws, bs, wo, bo = [], [], 0, 0
+    for o, i in zip(outs, ins):
+        ws.append(w[wo:wo + o * i].reshape(o, i))
+        bs.append(b[bo:bo + o])
+        wo += o * i
+        bo += o
+    return ws, bs

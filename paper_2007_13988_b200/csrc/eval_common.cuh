@@ -1,0 +1,133 @@
+// eval_common.cuh — shared pieces of every field-evaluation kernel: where the
+// points come from (a level's node list, or explicit points) and what happens
+// to each result (the grid epilogue of evaluate_nodes, localize.hpp:76-90,
+// fused with the conflict test of localize.hpp:341-342).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "icg_internal.h"
+
+namespace icg {
+
+__device__ __forceinline__ unsigned job_count(const EvalJob& j) { return j.count ? *j.count : j.n_static; }
+
+__device__ __forceinline__ uint32_t job_node(const EvalJob& j, unsigned t) { return j.list ? j.list[t] : t; }
+
+__device__ __forceinline__ bool job_is_grid(const EvalJob& j) { return j.points == nullptr; }
+
+// grid.hpp:50-53 node_position, in double, same operation order.
+__device__ __forceinline__ void node_pos_d(uint32_t idx, int cells, double* p) {
+    unsigned n = (unsigned)cells + 1u;
+    unsigned i = idx % n, j = (idx / n) % n, k = idx / (n * n);
+    double r = (double)cells;
+    p[0] = __dadd_rn(-1.0, __ddiv_rn(2.0 * (double)i, r));
+    p[1] = __dadd_rn(-1.0, __ddiv_rn(2.0 * (double)j, r));
+    p[2] = __dsub_rn(1.0, __ddiv_rn(2.0 * (double)k, r));
+}
+
+// The same position in fp32: exact, because node coordinates are dyadic
+// (2i/R with R a power of two <= 1024).
+__device__ __forceinline__ void node_pos_f(uint32_t idx, int cells, float* p) {
+    unsigned n = (unsigned)cells + 1u;
+    unsigned i = idx % n, j = (idx / n) % n, k = idx / (n * n);
+    float r = (float)cells;
+    p[0] = -1.0f + (2.0f * (float)i) / r;
+    p[1] = -1.0f + (2.0f * (float)j) / r;
+    p[2] = 1.0f - (2.0f * (float)k) / r;
+}
+
+__device__ __forceinline__ void job_point_d(const EvalJob& j, unsigned t, double* p) {
+    if (j.points) {
+        p[0] = j.points[3 * (size_t)t];
+        p[1] = j.points[3 * (size_t)t + 1];
+        p[2] = j.points[3 * (size_t)t + 2];
+    } else {
+        node_pos_d(job_node(j, t), j.cells, p);
+    }
+}
+
+// evaluate_nodes write-back (localize.hpp:86-88) + conflict detection
+// (localize.hpp:341-342): bin(oracle value) != bin(tentative value).
+__device__ __forceinline__ void grid_epilogue(const EvalJob& j, uint32_t idx, float v) {
+    j.values[idx] = v;
+    j.states[idx] = ICG_STATE_EVALUATED;
+    if (j.tentbin) {
+        bool tb = (j.tentbin[idx >> 5] >> (idx & 31)) & 1u;
+        bool vb = v >= 0.5f;
+        if (tb != vb) {
+            unsigned pos = atomicAdd(j.conflict_count, 1u);
+            if (pos < j.conflict_cap)
+                j.conflicts[pos] = idx;
+            else
+                *j.overflow = 1u;
+        }
+    }
+}
+
+__device__ __forceinline__ void job_account(const EvalJob& j) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned n = job_count(j);
+        if (j.evals) *j.evals += n;
+        if (j.iters && n > 0) *j.iters += 1u;
+    }
+}
+
+// Union SDF of the analytic scene (scene.hpp:60-103, 130-146) in double,
+// reference operation order; compiled without FMA contraction.
+__device__ __forceinline__ double d_dot3(const double* a, const double* b) {
+    return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[1], b[1])), __dmul_rn(a[2], b[2]));
+}
+
+__device__ __forceinline__ double prim_sdf(const DevPrim& pr, const double* p) {
+    double l[3] = {__dsub_rn(p[0], pr.c[0]), __dsub_rn(p[1], pr.c[1]), __dsub_rn(p[2], pr.c[2])};
+    if (pr.rotated) {
+        const double* m = pr.inv;
+        double r0[3] = {m[0], m[1], m[2]}, r1[3] = {m[3], m[4], m[5]}, r2[3] = {m[6], m[7], m[8]};
+        double l2[3] = {d_dot3(r0, l), d_dot3(r1, l), d_dot3(r2, l)};
+        l[0] = l2[0];
+        l[1] = l2[1];
+        l[2] = l2[2];
+    }
+    switch (pr.kind) {
+        case ICG_PRIM_SPHERE: return __dsub_rn(sqrt(d_dot3(l, l)), pr.radius);
+        case ICG_PRIM_BOX: {
+            double q[3] = {__dsub_rn(fabs(l[0]), pr.half[0]), __dsub_rn(fabs(l[1]), pr.half[1]),
+                           __dsub_rn(fabs(l[2]), pr.half[2])};
+            double qp[3] = {q[0] < 0.0 ? 0.0 : q[0], q[1] < 0.0 ? 0.0 : q[1], q[2] < 0.0 ? 0.0 : q[2]};
+            double m12 = q[1] < q[2] ? q[2] : q[1];
+            double m = q[0] < m12 ? m12 : q[0];
+            double mn = 0.0 < m ? 0.0 : m;
+            return __dadd_rn(sqrt(d_dot3(qp, qp)), mn);
+        }
+        case ICG_PRIM_CAPSULE: {
+            double pa[3] = {__dsub_rn(p[0], pr.a[0]), __dsub_rn(p[1], pr.a[1]), __dsub_rn(p[2], pr.a[2])};
+            double ba[3] = {__dsub_rn(pr.b[0], pr.a[0]), __dsub_rn(pr.b[1], pr.a[1]), __dsub_rn(pr.b[2], pr.a[2])};
+            double den = d_dot3(ba, ba);
+            double h = 0.0;
+            if (den > 0.0) {
+                h = __ddiv_rn(d_dot3(pa, ba), den);
+                h = h < 0.0 ? 0.0 : (h > 1.0 ? 1.0 : h);
+            }
+            double v[3] = {__dsub_rn(pa[0], __dmul_rn(h, ba[0])), __dsub_rn(pa[1], __dmul_rn(h, ba[1])),
+                           __dsub_rn(pa[2], __dmul_rn(h, ba[2]))};
+            return __dsub_rn(sqrt(d_dot3(v, v)), pr.radius);
+        }
+        case ICG_PRIM_TORUS: {
+            double qx = __dsub_rn(sqrt(__dadd_rn(__dmul_rn(l[0], l[0]), __dmul_rn(l[2], l[2]))), pr.major);
+            return __dsub_rn(sqrt(__dadd_rn(__dmul_rn(qx, qx), __dmul_rn(l[1], l[1]))), pr.minor);
+        }
+    }
+    return 1e300;
+}
+
+__device__ __forceinline__ double scene_sdf(const DevScene& s, const double* p) {
+    double acc = 0.0;
+    for (int i = 0; i < s.n_prims; ++i) {
+        double d = prim_sdf(s.prims[i], p);
+        acc = (i == 0) ? d : (d < acc ? d : acc);
+    }
+    return acc;
+}
+
+}  // namespace icg

@@ -1,0 +1,862 @@
+// icg_host.cu — host runtime behind the C ABI (include/isocull_b200.h).
+//
+// One icg_context per GPU: a stream, library-owned weight copies (SIMT and
+// tcgen05 layouts), grow-only device work buffers sized for the finest level,
+// and the grid of the last extraction (for the renderer).  The per-level
+// control flow of extract_progressive (localize.hpp:315-363) is issued as a
+// fixed sequence of kernels that read their work sizes from device counters,
+// so a whole extraction needs one host synchronisation (at the end).  The
+// conflict loop is unrolled `unroll` times per level; if a level still had
+// conflicts after the last unrolled iteration the device raises
+// `unroll_exhausted` and the extraction is replayed with twice the unroll
+// (results are identical; only the launch count changes).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "icg_internal.h"
+
+namespace icg {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+static int einval(const std::string& m) {
+    set_error(m);
+    return ICG_EINVAL;
+}
+
+struct DBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= n) return ICG_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        size_t b = bytes < 256 ? 256 : bytes;
+        ICG_CUDA_TRY(cudaMalloc(&p, b));
+        n = b;
+        return ICG_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace icg
+
+using namespace icg;
+
+struct icg_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    // weights
+    bool has_geo = false, has_tex = false;
+    DBuf geo_wt[5], geo_b[5], tex_wt[5], tex_b[5];
+    SimtMlp geo_simt{}, tex_simt{};
+    DBuf geo_stream, geo_bias, geo_wlast, tex_stream, tex_bias, tex_wlast;
+    TcMlp geo_tc{}, tex_tc{};
+    // field
+    DBuf scene;
+    DevScene* h_scene = nullptr;  // pinned staging
+    DBuf fmap_chw, fmap_hwc;
+    // grids and work lists
+    DBuf vals[2], sts[2];
+    DBuf cbin, mixed, tentbin, sel, queued, block_counts;
+    DBuf list_e0, cf[2], nx[2];
+    DBuf ctr;
+    DevCounters* h_ctr = nullptr;  // pinned
+    DBuf binar, pts, outv;
+    // render
+    DBuf depth, rgb, mask, surfk, spts, spx;
+    // last extraction
+    int last_cells = 0, last_buf = -1;
+    int unroll = 6;
+};
+
+namespace {
+
+size_t nodes3(int cells) {
+    size_t n = (size_t)cells + 1;
+    return n * n * n;
+}
+size_t words(size_t bits) { return (bits + 31) / 32; }
+
+int ensure_grid(icg_context* c, int cells) {
+    size_t N = nodes3(cells);
+    size_t nc = nodes3(cells / 2 > 0 ? cells / 2 : 1);
+    size_t ncell = (size_t)(cells / 2) * (cells / 2) * (cells / 2) + 1;
+    for (int b = 0; b < 2; ++b) {
+        if (int r = c->vals[b].ensure(N * 4)) return r;
+        if (int r = c->sts[b].ensure(N)) return r;
+        if (int r = c->cf[b].ensure(N * 4)) return r;
+        if (int r = c->nx[b].ensure(N * 4)) return r;
+    }
+    if (int r = c->cbin.ensure(words(nc) * 4 + 16)) return r;
+    if (int r = c->mixed.ensure(words(ncell) * 4 + 16)) return r;
+    if (int r = c->tentbin.ensure(words(N) * 4 + 16)) return r;
+    if (int r = c->sel.ensure(words(N) * 4 + 16)) return r;
+    if (int r = c->queued.ensure(words(N) * 4 + 16)) return r;
+    if (int r = c->block_counts.ensure((N / 1024 + 2) * 4)) return r;
+    if (int r = c->list_e0.ensure(N * 4)) return r;
+    return ICG_OK;
+}
+
+int validate_algo(const icg_algo_config* cfg) {
+    // validate_config, localize.hpp:47-55
+    if (!cfg) return einval("config: null");
+    if (cfg->variant != ICG_VARIANT_PROGRESSIVE && cfg->variant != ICG_VARIANT_BRUTE)
+        return einval("config: variant must be progressive or brute");
+    if (cfg->coarsest_cells < 2) return einval("config: coarsest cells must be >= 2");
+    if (cfg->target_level < 0) return einval("config: target level must be >= 0");
+    if (cfg->target_level > 10 || ((long)cfg->coarsest_cells << cfg->target_level) > ICG_MAX_TARGET_CELLS)
+        return einval("config: target resolution exceeds 1024 cells per axis");
+    return ICG_OK;
+}
+
+int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
+    if (!f) return einval("field: null");
+    if (f->kind != ICG_FIELD_ANALYTIC && f->kind != ICG_FIELD_PIFU) return einval("field: unknown kind");
+    const icg_scene& s = f->scene;
+    if (s.n_prims < 0 || s.n_prims > ICG_MAX_PRIMS) return einval("scene: too many primitives");
+    if (f->kind == ICG_FIELD_ANALYTIC) {
+        if (s.n_prims == 0) return einval("scene: no primitives");  // validate_scene, scene.hpp:191
+        if (!(s.tau > 0.0)) return einval("scene: tau must be > 0");
+    }
+    if (s.n_prims && !s.prims) return einval("scene: null primitive array");
+    DevScene* h = c->h_scene;
+    std::memset(h, 0, sizeof(DevScene));
+    for (int i = 0; i < s.n_prims; ++i) {
+        const icg_primitive& p = s.prims[i];
+        if (p.kind < ICG_PRIM_SPHERE || p.kind > ICG_PRIM_TORUS) return einval("scene: unknown primitive kind");
+        DevPrim& d = h->prims[i];
+        d.kind = p.kind;
+        d.rotated = p.rotated ? 1 : 0;
+        for (int k = 0; k < 3; ++k) {
+            d.c[k] = p.center[k];
+            d.a[k] = p.a[k];
+            d.b[k] = p.b[k];
+            d.half[k] = p.half[k];
+        }
+        d.radius = p.radius;
+        d.major = p.major;
+        d.minor = p.minor;
+        for (int k = 0; k < 9; ++k) d.inv[k] = p.inv_rotation[k];
+    }
+    h->n_prims = s.n_prims;
+    h->tau = s.tau;
+    h->sdf_scale = f->sdf_scale;
+    if (int r = c->scene.ensure(sizeof(DevScene))) return r;
+    ICG_CUDA_TRY(cudaMemcpyAsync(c->scene.p, h, sizeof(DevScene), cudaMemcpyHostToDevice, c->stream));
+    fd = FieldDev{};
+    fd.kind = f->kind;
+    fd.precision = f->precision;
+    fd.scene = c->scene.as<DevScene>();
+    if (f->kind == ICG_FIELD_PIFU) {
+        if (!c->has_geo) return einval("field: PIFu field needs geometry MLP weights (icg_set_mlp)");
+        if (f->precision != ICG_PREC_FP32 && f->precision != ICG_PREC_BF16 && f->precision != ICG_PREC_FP32_SIMT)
+            return einval("field: unknown precision");
+        if (f->precision != ICG_PREC_FP32_SIMT && !c->geo_tc.valid)
+            return einval("field: tensor-core weights not packed");
+        if (!f->feature_map) return einval("field: null feature map");
+        if (f->fmap_c != kC) return einval("field: feature map must have 256 channels");
+        if (f->fmap_h < 2 || f->fmap_w < 2) return einval("field: feature map must be at least 2x2");
+        size_t n = (size_t)f->fmap_c * f->fmap_h * f->fmap_w;
+        const float* chw = f->feature_map;
+        if (f->fmap_mem == ICG_MEM_HOST) {
+            if (int r = c->fmap_chw.ensure(n * 4)) return r;
+            ICG_CUDA_TRY(cudaMemcpyAsync(c->fmap_chw.p, f->feature_map, n * 4, cudaMemcpyHostToDevice, c->stream));
+            chw = c->fmap_chw.as<float>();
+        } else if (f->fmap_mem != ICG_MEM_DEVICE) {
+            return einval("field: fmap_mem must be ICG_MEM_HOST or ICG_MEM_DEVICE");
+        }
+        if (int r = c->fmap_hwc.ensure(n * 4)) return r;
+        if (int r = launch_fmap_chw_to_hwc(chw, c->fmap_hwc.as<float>(), f->fmap_c, f->fmap_h, f->fmap_w, c->stream))
+            return r;
+        fd.fmap_hwc = c->fmap_hwc.as<float>();
+        fd.C = f->fmap_c;
+        fd.H = f->fmap_h;
+        fd.W = f->fmap_w;
+    }
+    return ICG_OK;
+}
+
+int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
+    if (fd.kind == ICG_FIELD_ANALYTIC) return launch_analytic_eval(fd, job, max_points, c->stream);
+    if (fd.precision == ICG_PREC_FP32_SIMT) return launch_pifu_simt_eval(fd, c->geo_simt, job, max_points, c->stream);
+    return launch_pifu_tc_eval(fd, c->geo_tc, job, max_points, fd.precision == ICG_PREC_FP32, c->stream);
+}
+
+int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
+    if (fd.precision == ICG_PREC_FP32_SIMT)
+        return launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
+    return launch_pifu_tc_texture(fd, c->geo_tc, c->tex_tc, job, max_points, fd.precision == ICG_PREC_FP32,
+                                  c->stream);
+}
+
+// Issues one whole extraction on the context stream (no host sync).
+int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg, int unroll) {
+    DevCounters* ctr = c->ctr.as<DevCounters>();
+    ICG_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), c->stream));
+    const int L = cfg->target_level;
+    const int RL = cfg->coarsest_cells << L;
+    if (cfg->variant == ICG_VARIANT_BRUTE) {
+        // extract_brute_force, localize.hpp:181-193
+        EvalJob job{};
+        job.cells = RL;
+        job.n_static = (unsigned)nodes3(RL);
+        job.values = c->vals[0].as<float>();
+        job.states = c->sts[0].as<uint8_t>();
+        job.evals = &ctr->evals[L];
+        job.overflow = &ctr->overflow;
+        if (int r = run_eval(c, fd, job, job.n_static)) return r;
+        c->last_buf = 0;
+        c->last_cells = RL;
+        return ICG_OK;
+    }
+    // L0: evaluate_full (localize.hpp:322)
+    int cells = cfg->coarsest_cells;
+    int b = 0;
+    {
+        EvalJob job{};
+        job.cells = cells;
+        job.n_static = (unsigned)nodes3(cells);
+        job.values = c->vals[b].as<float>();
+        job.states = c->sts[b].as<uint8_t>();
+        job.evals = &ctr->evals[0];
+        job.overflow = &ctr->overflow;
+        if (int r = run_eval(c, fd, job, job.n_static)) return r;
+    }
+    for (int l = 1; l <= L; ++l) {
+        const int fcells = 2 * cells;
+        const size_t nf = nodes3(fcells);
+        LevelBufs lb{};
+        lb.cv = c->vals[b].as<float>();
+        lb.cs = c->sts[b].as<uint8_t>();
+        lb.fv = c->vals[b ^ 1].as<float>();
+        lb.fs = c->sts[b ^ 1].as<uint8_t>();
+        lb.cbin = c->cbin.as<uint32_t>();
+        lb.mixed = c->mixed.as<uint32_t>();
+        lb.tentbin = c->tentbin.as<uint32_t>();
+        lb.sel = c->sel.as<uint32_t>();
+        lb.queued = c->queued.as<uint32_t>();
+        lb.block_counts = c->block_counts.as<uint32_t>();
+        lb.list = c->list_e0.as<uint32_t>();
+        lb.rc = cells;
+        if (int r = launch_level_classify(lb, ctr, l, c->stream)) return r;
+        ICG_CUDA_TRY(cudaMemsetAsync(c->queued.p, 0, words(nf) * 4, c->stream));
+        // evaluate E0 (localize.hpp:331-332) with the fused conflict test
+        EvalJob job{};
+        job.list = c->list_e0.as<uint32_t>();
+        job.count = &ctr->list_count;
+        job.cells = fcells;
+        job.values = lb.fv;
+        job.states = lb.fs;
+        job.overflow = &ctr->overflow;
+        if (cfg->conflict_pass) {
+            job.tentbin = lb.tentbin;
+            job.conflicts = c->cf[0].as<uint32_t>();
+            job.conflict_count = &ctr->cf_count[0];
+            job.conflict_cap = (unsigned)nf;
+        }
+        if (int r = run_eval(c, fd, job, (unsigned)nf)) return r;
+        if (cfg->conflict_pass) {
+            int max_iters = cfg->max_conflict_iters > 0 ? cfg->max_conflict_iters : fcells;
+            for (int it = 0; it < unroll; ++it) {
+                int p = it & 1;
+                if (int r = launch_conflict_expand(c->queued.as<uint32_t>(), lb.fs, fcells, c->cf[p].as<uint32_t>(),
+                                                   ctr, it, max_iters, c->nx[p].as<uint32_t>(), (unsigned)nf,
+                                                   c->stream))
+                    return r;
+                EvalJob cj{};
+                cj.list = c->nx[p].as<uint32_t>();
+                cj.count = &ctr->nx_count[p];
+                cj.cells = fcells;
+                cj.values = lb.fv;
+                cj.states = lb.fs;
+                cj.tentbin = lb.tentbin;
+                cj.conflicts = c->cf[p ^ 1].as<uint32_t>();
+                cj.conflict_count = &ctr->cf_count[p ^ 1];
+                cj.conflict_cap = (unsigned)nf;
+                cj.evals = &ctr->evals[l];
+                cj.iters = &ctr->conflict_iters[l];
+                cj.overflow = &ctr->overflow;
+                if (int r = run_eval(c, fd, cj, (unsigned)nf)) return r;
+            }
+            if (int r = launch_unroll_check(ctr, unroll & 1, c->stream)) return r;
+        }
+        b ^= 1;
+        cells = fcells;
+    }
+    c->last_buf = b;
+    c->last_cells = cells;
+    return ICG_OK;
+}
+
+int copy_out(icg_context* c, void* dst, const void* src, size_t bytes, int mem) {
+    if (!dst) return ICG_OK;
+    ICG_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, mem == ICG_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    return ICG_OK;
+}
+
+int finish_extract_outputs(icg_context* c, const icg_algo_config* cfg, icg_extraction* out) {
+    if (!out) return ICG_OK;
+    if (out->mem != ICG_MEM_HOST && out->mem != ICG_MEM_DEVICE) return einval("extraction: bad mem");
+    size_t N = nodes3(c->last_cells);
+    if (int r = copy_out(c, out->values, c->vals[c->last_buf].p, N * 4, out->mem)) return r;
+    if (int r = copy_out(c, out->states, c->sts[c->last_buf].p, N, out->mem)) return r;
+    if (out->binarized) {
+        if (int r = c->binar.ensure(N)) return r;
+        if (int r = launch_binarize(c->vals[c->last_buf].as<float>(), c->binar.as<uint8_t>(), N, c->stream)) return r;
+        if (int r = copy_out(c, out->binarized, c->binar.p, N, out->mem)) return r;
+    }
+    (void)cfg;
+    return ICG_OK;
+}
+
+void fill_extraction_scalars(icg_context* c, const icg_algo_config* cfg, icg_extraction* out, double secs) {
+    if (!out) return;
+    const DevCounters& h = *c->h_ctr;
+    out->cells = c->last_cells;
+    out->levels = cfg->target_level + 1;
+    out->total_evals = 0;
+    for (int l = 0; l < ICG_MAX_LEVELS; ++l) {
+        out->evals_per_level[l] = l <= cfg->target_level ? h.evals[l] : 0;
+        out->refined_cells_per_level[l] = l <= cfg->target_level ? h.refined[l] : 0;
+        out->conflict_iters_per_level[l] = l <= cfg->target_level ? h.conflict_iters[l] : 0;
+        out->total_evals += out->evals_per_level[l];
+    }
+    out->conflict_warning = h.warning ? 1 : 0;
+    out->wall_seconds = secs;
+}
+
+int sync_counters(icg_context* c) {
+    ICG_CUDA_TRY(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return ICG_OK;
+}
+
+int issue_render(icg_context* c, const FieldDev& fd, const icg_camera* cam, int W, int H, const float* bg) {
+    size_t npx = (size_t)W * H;
+    if (int r = c->depth.ensure(npx * 4)) return r;
+    if (int r = c->rgb.ensure(npx * 12)) return r;
+    if (int r = c->mask.ensure(npx)) return r;
+    if (int r = c->surfk.ensure(npx * 4)) return r;
+    if (int r = c->spts.ensure(npx * 24)) return r;
+    if (int r = c->spx.ensure(npx * 4)) return r;
+    DevCounters* ctr = c->ctr.as<DevCounters>();
+    // clear render counters (covered .. surface_count)
+    ICG_CUDA_TRY(cudaMemsetAsync(&ctr->covered, 0, sizeof(DevCounters) - offsetof(DevCounters, covered), c->stream));
+    RenderJob rj{};
+    rj.values = c->vals[c->last_buf].as<float>();
+    rj.cells = c->last_cells;
+    for (int i = 0; i < 9; ++i) rj.rot[i] = cam->rotation[i];
+    for (int i = 0; i < 3; ++i) rj.trans[i] = cam->translation[i];
+    rj.scale = cam->scale;
+    rj.width = W;
+    rj.height = H;
+    for (int i = 0; i < 3; ++i) rj.bg[i] = bg ? bg[i] : 0.0f;
+    rj.depth = c->depth.as<float>();
+    rj.rgb = c->rgb.as<float>();
+    rj.mask = c->mask.as<uint8_t>();
+    rj.surface_k = c->surfk.as<int32_t>();
+    rj.surface_pts = c->spts.as<double>();
+    rj.surface_px = c->spx.as<uint32_t>();
+    rj.ctr = ctr;
+    if (int r = launch_render_first_crossing(rj, c->stream)) return r;
+    if (fd.kind == ICG_FIELD_PIFU && c->has_tex) {
+        EvalJob tj{};
+        tj.points = c->spts.as<double>();
+        tj.count = &ctr->surface_count;
+        tj.out = c->rgb.as<float>();
+        tj.out_pixel = c->spx.as<uint32_t>();
+        tj.out_clamp = 1.0f;
+        if (int r = run_texture(c, fd, tj, (unsigned)npx)) return r;
+    }
+    return ICG_OK;
+}
+
+int finish_render_outputs(icg_context* c, int W, int H, icg_image* out) {
+    if (!out) return ICG_OK;
+    if (out->mem != ICG_MEM_HOST && out->mem != ICG_MEM_DEVICE) return einval("image: bad mem");
+    size_t npx = (size_t)W * H;
+    if (int r = copy_out(c, out->depth, c->depth.p, npx * 4, out->mem)) return r;
+    if (int r = copy_out(c, out->rgb, c->rgb.p, npx * 12, out->mem)) return r;
+    if (int r = copy_out(c, out->mask, c->mask.p, npx, out->mem)) return r;
+    if (int r = copy_out(c, out->surface_k, c->surfk.p, npx * 4, out->mem)) return r;
+    return ICG_OK;
+}
+
+void fill_image_scalars(icg_context* c, icg_image* out, double secs) {
+    if (!out) return;
+    const DevCounters& h = *c->h_ctr;
+    out->covered_pixels = h.covered;
+    out->degenerate_brackets = h.degenerate;
+    out->grazing_pixels = h.grazing;
+    out->texture_points = h.surface_count;
+    out->wall_seconds = secs;
+}
+
+int check_render_args(icg_context* c, const icg_camera* cam, int W, int H) {
+    if (!cam) return einval("render: null camera");
+    if (W < 2 || H < 2 || (size_t)W * H > (size_t)1 << 26) return einval("render: image size out of range");
+    if (!(cam->scale != 0.0)) return einval("render: camera scale must be nonzero");
+    (void)c;
+    return ICG_OK;
+}
+
+float elapsed(icg_context* c) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, c->e0, c->e1);
+    return ms * 1e-3f;
+}
+
+// extraction with the unroll-exhaustion replay
+int do_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg) {
+    for (;;) {
+        if (int r = issue_extract(c, fd, cfg, c->unroll)) return r;
+        if (int r = sync_counters(c)) return r;
+        if (c->h_ctr->overflow) {
+            set_error("extract: device work list overflow");
+            return ICG_ECAPACITY;
+        }
+        if (!c->h_ctr->unroll_exhausted) return ICG_OK;
+        c->unroll *= 2;  // replay with a deeper device-side conflict loop
+        if (c->unroll > 4096) {
+            set_error("extract: conflict loop did not converge");
+            return ICG_ERUNTIME;
+        }
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int icg_abi_version(void) { return ICG_ABI_VERSION; }
+const char* icg_last_error(void) { return g_err.c_str(); }
+
+int icg_device_count(int* count) {
+    if (!count) return einval("null count");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    *count = n;
+    return ICG_OK;
+}
+
+int icg_create(int device, icg_context** out) {
+    if (!out) return einval("null output");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        set_error("no CUDA device");
+        return ICG_ENODEV;
+    }
+    if (device < 0 || device >= n) return einval("device index out of range");
+    ICG_CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    ICG_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        set_error("this build targets sm_100a (B200); device is sm_" + std::to_string(prop.major) +
+                  std::to_string(prop.minor));
+        return ICG_ENODEV;
+    }
+    auto* c = new icg_context();
+    c->device = device;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&c->e0) != cudaSuccess || cudaEventCreate(&c->e1) != cudaSuccess ||
+        cudaMallocHost(&c->h_scene, sizeof(DevScene)) != cudaSuccess ||
+        cudaMallocHost(&c->h_ctr, sizeof(DevCounters)) != cudaSuccess) {
+        set_error("icg_create: CUDA resource allocation failed");
+        delete c;
+        return ICG_ERUNTIME;
+    }
+    if (int r = c->ctr.ensure(sizeof(DevCounters))) {
+        delete c;
+        return r;
+    }
+    *out = c;
+    return ICG_OK;
+}
+
+int icg_destroy(icg_context* c) {
+    if (!c) return ICG_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    DBuf* all[] = {&c->geo_stream, &c->geo_bias, &c->geo_wlast, &c->tex_stream, &c->tex_bias, &c->tex_wlast,
+                   &c->scene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
+                   &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
+                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv,
+                   &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx};
+    for (DBuf* b : all) b->release();
+    for (int l = 0; l < 5; ++l) {
+        c->geo_wt[l].release();
+        c->geo_b[l].release();
+        c->tex_wt[l].release();
+        c->tex_b[l].release();
+    }
+    if (c->h_scene) cudaFreeHost(c->h_scene);
+    if (c->h_ctr) cudaFreeHost(c->h_ctr);
+    if (c->e0) cudaEventDestroy(c->e0);
+    if (c->e1) cudaEventDestroy(c->e1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return ICG_OK;
+}
+
+int icg_mlp_shape(int which, int32_t* out_dims, int32_t* in_dims, int32_t* skip_dim, size_t* n_weights,
+                  size_t* n_biases) {
+    if (which != ICG_MLP_GEOMETRY && which != ICG_MLP_TEXTURE) return einval("mlp: unknown network");
+    const int* outs = which == ICG_MLP_GEOMETRY ? kGeoOut : kTexOut;
+    int skip = which == ICG_MLP_GEOMETRY ? kGeoSkip : kTexSkip;
+    size_t nw = 0, nb = 0;
+    for (int l = 0; l < 5; ++l) {
+        int in = (l ? outs[l - 1] : 0) + skip;
+        if (out_dims) out_dims[l] = outs[l];
+        if (in_dims) in_dims[l] = in;
+        nw += (size_t)outs[l] * in;
+        nb += (size_t)outs[l];
+    }
+    if (skip_dim) *skip_dim = skip;
+    if (n_weights) *n_weights = nw;
+    if (n_biases) *n_biases = nb;
+    return ICG_OK;
+}
+
+int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
+    if (!c || !d) return einval("set_mlp: null argument");
+    if (d->which != ICG_MLP_GEOMETRY && d->which != ICG_MLP_TEXTURE) return einval("set_mlp: unknown network");
+    if (d->n_layers != ICG_MLP_LAYERS) return einval("set_mlp: the PIFu MLPs have 5 layers");
+    int32_t outs[5], ins[5], skip;
+    icg_mlp_shape(d->which, outs, ins, &skip, nullptr, nullptr);
+    if (d->skip_dim != skip) return einval("set_mlp: skip dimension mismatch");
+    for (int l = 0; l < 5; ++l) {
+        if (d->out_dims[l] != outs[l]) return einval("set_mlp: layer width mismatch");
+        if (!d->weights[l] || !d->biases[l]) return einval("set_mlp: null weights");
+    }
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    bool geo = d->which == ICG_MLP_GEOMETRY;
+    DBuf* wt = geo ? c->geo_wt : c->tex_wt;
+    DBuf* bb = geo ? c->geo_b : c->tex_b;
+    SimtMlp& sm = geo ? c->geo_simt : c->tex_simt;
+    std::vector<float> t;
+    for (int l = 0; l < 5; ++l) {
+        int O = outs[l], K = ins[l];
+        t.resize((size_t)O * K);
+        for (int o = 0; o < O; ++o)
+            for (int k = 0; k < K; ++k) t[(size_t)k * O + o] = d->weights[l][(size_t)o * K + k];
+        if (int r = wt[l].ensure(t.size() * 4)) return r;
+        if (int r = bb[l].ensure((size_t)O * 4)) return r;
+        ICG_CUDA_TRY(cudaMemcpy(wt[l].p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+        ICG_CUDA_TRY(cudaMemcpy(bb[l].p, d->biases[l], (size_t)O * 4, cudaMemcpyHostToDevice));
+        sm.wt[l] = wt[l].as<float>();
+        sm.b[l] = bb[l].as<float>();
+        sm.out[l] = O;
+        sm.in[l] = K;
+    }
+    sm.skip = skip;
+    sm.slope = d->leaky_slope;
+    // tcgen05 operand stream (bf16 hi/lo tiles) + fp32 biases + fp32 final layer
+    DBuf& st = geo ? c->geo_stream : c->tex_stream;
+    DBuf& bi = geo ? c->geo_bias : c->tex_bias;
+    DBuf& wl = geo ? c->geo_wlast : c->tex_wlast;
+    TcMlp& tc = geo ? c->geo_tc : c->tex_tc;
+    size_t sb = tc_stream_bytes(d->which);
+    tc.valid = 0;
+    if (sb) {
+        std::vector<uint8_t> hs(sb);
+        std::vector<float> hb(tc_bias_floats(d->which)), hw(tc_wlast_floats(d->which));
+        const float* ws[5];
+        const float* bs[5];
+        for (int l = 0; l < 5; ++l) {
+            ws[l] = d->weights[l];
+            bs[l] = d->biases[l];
+        }
+        if (int r = tc_pack_mlp(d->which, ws, bs, hs.data(), hb.data(), hw.data())) return r;
+        if (int r = st.ensure(sb)) return r;
+        if (int r = bi.ensure(hb.size() * 4)) return r;
+        if (int r = wl.ensure(hw.size() * 4)) return r;
+        ICG_CUDA_TRY(cudaMemcpy(st.p, hs.data(), sb, cudaMemcpyHostToDevice));
+        ICG_CUDA_TRY(cudaMemcpy(bi.p, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice));
+        ICG_CUDA_TRY(cudaMemcpy(wl.p, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice));
+        tc.stream = st.as<uint8_t>();
+        tc.stream_bytes = sb;
+        tc.bias = bi.as<float>();
+        tc.w_last = wl.as<float>();
+        int off = 0;
+        for (int l = 0; l < 5; ++l) {
+            tc.bias_off[l] = off;
+            off += outs[l];
+        }
+        tc.valid = 1;
+    }
+    if (geo)
+        c->has_geo = true;
+    else
+        c->has_tex = true;
+    return ICG_OK;
+}
+
+int icg_extract(icg_context* c, const icg_field* field, const icg_algo_config* cfg, icg_extraction* out) {
+    if (!c) return einval("extract: null context");
+    if (int r = validate_algo(cfg)) return r;
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    FieldDev fd;
+    if (int r = prepare_field(c, field, fd)) return r;
+    if (int r = ensure_grid(c, cfg->coarsest_cells << cfg->target_level)) return r;
+    ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
+    if (int r = do_extract(c, fd, cfg)) return r;
+    ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
+    if (int r = finish_extract_outputs(c, cfg, out)) return r;
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    fill_extraction_scalars(c, cfg, out, elapsed(c));
+    return ICG_OK;
+}
+
+int icg_render_localized(icg_context* c, const icg_field* field, const icg_camera* cam, int W, int H,
+                         const float* bg, icg_image* out) {
+    if (!c) return einval("render: null context");
+    if (c->last_buf < 0) return einval("render: no localized grid on this context (call icg_extract first)");
+    if (int r = check_render_args(c, cam, W, H)) return r;
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    FieldDev fd;
+    if (int r = prepare_field(c, field, fd)) return r;
+    if (fd.kind == ICG_FIELD_PIFU && !c->has_tex) return einval("render: scene has no texture (icg_set_mlp TEXTURE)");
+    ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
+    if (int r = issue_render(c, fd, cam, W, H, bg)) return r;
+    ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
+    if (int r = finish_render_outputs(c, W, H, out)) return r;
+    if (int r = sync_counters(c)) return r;
+    fill_image_scalars(c, out, elapsed(c));
+    return ICG_OK;
+}
+
+int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg, const icg_camera* cam, int W, int H,
+              const float* bg, icg_extraction* ext, icg_image* img) {
+    if (!c) return einval("frame: null context");
+    if (int r = validate_algo(cfg)) return r;
+    if (int r = check_render_args(c, cam, W, H)) return r;
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    FieldDev fd;
+    if (int r = prepare_field(c, field, fd)) return r;
+    if (fd.kind == ICG_FIELD_PIFU && !c->has_tex) return einval("frame: scene has no texture (icg_set_mlp TEXTURE)");
+    if (int r = ensure_grid(c, cfg->coarsest_cells << cfg->target_level)) return r;
+    ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
+    for (;;) {
+        if (int r = issue_extract(c, fd, cfg, c->unroll)) return r;
+        if (int r = issue_render(c, fd, cam, W, H, bg)) return r;
+        ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
+        if (int r = finish_render_outputs(c, W, H, img)) return r;
+        if (int r = sync_counters(c)) return r;
+        if (c->h_ctr->overflow) {
+            set_error("frame: device work list overflow");
+            return ICG_ECAPACITY;
+        }
+        if (!c->h_ctr->unroll_exhausted) break;
+        c->unroll *= 2;
+        if (c->unroll > 4096) {
+            set_error("frame: conflict loop did not converge");
+            return ICG_ERUNTIME;
+        }
+        ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
+    }
+    double secs = elapsed(c);
+    if (ext) {
+        if (int r = finish_extract_outputs(c, cfg, ext)) return r;
+        ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        fill_extraction_scalars(c, cfg, ext, secs);
+    }
+    fill_image_scalars(c, img, secs);
+    return ICG_OK;
+}
+
+static int eval_points(icg_context* c, const icg_field* field, const double* points, size_t n, int mem, float* out,
+                       bool texture) {
+    if (!c || !field) return einval("batch: null argument");
+    if (n == 0) return ICG_OK;  // empty list -> empty list, counter unchanged (SPEC field examples)
+    if (!points || !out) return einval("batch: null buffer");
+    if (mem != ICG_MEM_HOST && mem != ICG_MEM_DEVICE) return einval("batch: bad mem");
+    if (n > (size_t)1 << 31) return einval("batch: too many points");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    FieldDev fd;
+    if (int r = prepare_field(c, field, fd)) return r;
+    if (texture && (fd.kind != ICG_FIELD_PIFU || !c->has_tex)) return einval("FieldOracle: scene has no texture");
+    const double* dpts = points;
+    float* dout = out;
+    size_t ob = n * 4 * (texture ? 3 : 1);
+    if (mem == ICG_MEM_HOST) {
+        if (int r = c->pts.ensure(n * 24)) return r;
+        if (int r = c->outv.ensure(ob)) return r;
+        ICG_CUDA_TRY(cudaMemcpyAsync(c->pts.p, points, n * 24, cudaMemcpyHostToDevice, c->stream));
+        dpts = c->pts.as<double>();
+        dout = c->outv.as<float>();
+    }
+    EvalJob job{};
+    job.points = dpts;
+    job.n_static = (unsigned)n;
+    job.out = dout;
+    int r = texture ? run_texture(c, fd, job, (unsigned)n) : run_eval(c, fd, job, (unsigned)n);
+    if (r) return r;
+    if (mem == ICG_MEM_HOST) ICG_CUDA_TRY(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return ICG_OK;
+}
+
+int icg_occupancy_batch(icg_context* c, const icg_field* f, const double* p, size_t n, int mem, float* out) {
+    return eval_points(c, f, p, n, mem, out, false);
+}
+
+int icg_texture_batch(icg_context* c, const icg_field* f, const double* p, size_t n, int mem, float* out) {
+    return eval_points(c, f, p, n, mem, out, true);
+}
+
+int icg_compare_iou(icg_context* c, const uint8_t* a, const uint8_t* b, size_t n, int mem, double* iou) {
+    if (!iou) return einval("compare_iou: null output");
+    if (n == 0) {
+        *iou = 1.0;
+        return ICG_OK;
+    }
+    if (!a || !b) return einval("compare_iou: null input");
+    if (mem == ICG_MEM_HOST || !c) {
+        uint64_t inter = 0, uni = 0;
+        for (size_t i = 0; i < n; ++i) {
+            bool av = a[i] != 0, bv = b[i] != 0;
+            inter += (av && bv);
+            uni += (av || bv);
+        }
+        *iou = uni ? (double)inter / (double)uni : 1.0;
+        return ICG_OK;
+    }
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    if (int r = c->outv.ensure(16)) return r;
+    ICG_CUDA_TRY(cudaMemsetAsync(c->outv.p, 0, 16, c->stream));
+    if (int r = launch_iou(a, b, n, c->outv.as<unsigned long long>(), c->stream)) return r;
+    unsigned long long iu[2];
+    ICG_CUDA_TRY(cudaMemcpyAsync(iu, c->outv.p, 16, cudaMemcpyDeviceToHost, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *iou = iu[1] ? (double)iu[0] / (double)iu[1] : 1.0;
+    return ICG_OK;
+}
+
+int icg_host_alloc(size_t bytes, void** p) {
+    if (!p) return einval("null output");
+    ICG_CUDA_TRY(cudaMallocHost(p, bytes ? bytes : 1));
+    return ICG_OK;
+}
+int icg_host_free(void* p) {
+    if (p) ICG_CUDA_TRY(cudaFreeHost(p));
+    return ICG_OK;
+}
+int icg_device_alloc(icg_context* c, size_t bytes, void** p) {
+    if (!c || !p) return einval("null argument");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    ICG_CUDA_TRY(cudaMalloc(p, bytes ? bytes : 1));
+    return ICG_OK;
+}
+int icg_device_free(icg_context* c, void* p) {
+    if (!c) return einval("null context");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    if (p) ICG_CUDA_TRY(cudaFree(p));
+    return ICG_OK;
+}
+int icg_memcpy(icg_context* c, void* dst, const void* src, size_t bytes, int dst_mem, int src_mem) {
+    if (!c) return einval("null context");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    cudaMemcpyKind k = dst_mem == ICG_MEM_HOST
+                           ? (src_mem == ICG_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost)
+                           : (src_mem == ICG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice);
+    ICG_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, k, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return ICG_OK;
+}
+
+// ---- seeded inputs: std::mt19937_64 + random.hpp:22-38 transforms ----------
+static double u01(std::mt19937_64& g) { return (double)(g() >> 11) * 0x1.0p-53; }
+static double urange(std::mt19937_64& g, double lo, double hi) { return lo + (hi - lo) * u01(g); }
+static double normal(std::mt19937_64& g) {
+    double a = u01(g);
+    while (a <= 0.0) a = u01(g);
+    double b = u01(g);
+    return std::sqrt(-2.0 * std::log(a)) * std::cos(2.0 * 3.14159265358979323846 * b);
+}
+
+int icg_gen_capsules(uint64_t seed, int n, icg_primitive* out) {
+    if (n < 0 || (n && !out)) return einval("gen_capsules: bad arguments");
+    std::mt19937_64 g(seed);
+    for (int c = 0; c < n; ++c) {
+        std::memset(&out[c], 0, sizeof(icg_primitive));
+        out[c].kind = ICG_PRIM_CAPSULE;
+        for (int d = 0; d < 3; ++d) out[c].a[d] = urange(g, -0.5, 0.5);
+        for (int d = 0; d < 3; ++d) out[c].b[d] = urange(g, -0.5, 0.5);
+        out[c].radius = urange(g, 0.03, 0.08);
+        out[c].inv_rotation[0] = out[c].inv_rotation[4] = out[c].inv_rotation[8] = 1.0;
+    }
+    return ICG_OK;
+}
+
+int icg_gen_normals(uint64_t seed, size_t n, float* out) {
+    if (n && !out) return einval("gen_normals: null output");
+    std::mt19937_64 g(seed);
+    for (size_t i = 0; i < n; ++i) out[i] = (float)normal(g);
+    return ICG_OK;
+}
+
+int icg_gen_mlp(uint64_t seed, int which, float* w, float* b) {
+    int32_t outs[5], ins[5];
+    if (int r = icg_mlp_shape(which, outs, ins, nullptr, nullptr, nullptr)) return r;
+    if (!w || !b) return einval("gen_mlp: null output");
+    const double slope = 0.02, gain = std::sqrt(2.0 / (1.0 + slope * slope));
+    std::mt19937_64 g(seed);
+    size_t wo = 0, bo = 0;
+    for (int l = 0; l < 5; ++l) {
+        double bound = gain * std::sqrt(3.0 / (double)ins[l]);
+        for (size_t i = 0; i < (size_t)outs[l] * ins[l]; ++i) w[wo + i] = (float)urange(g, -bound, bound);
+        double bb = 1.0 / std::sqrt((double)ins[l]);
+        for (int o = 0; o < outs[l]; ++o) b[bo + o] = (float)urange(g, -bb, bb);
+        wo += (size_t)outs[l] * ins[l];
+        bo += (size_t)outs[l];
+    }
+    return ICG_OK;
+}
+
+int icg_camera_from_angles(double yaw_deg, double pitch_deg, double dist, double scale, icg_camera* out) {
+    if (!out) return einval("camera: null output");
+    const double kPi = 3.14159265358979323846;
+    double yaw = std::fmod(yaw_deg, 360.0), pitch = std::fmod(pitch_deg, 360.0);
+    double rx = pitch * kPi / 180.0, ry = yaw * kPi / 180.0;  // deg_to_rad, geom.hpp:11
+    double cx = std::cos(rx), sx = std::sin(rx), cy = std::cos(ry), sy = std::sin(ry);
+    double A[9] = {1, 0, 0, 0, cx, -sx, 0, sx, cx};
+    double B[9] = {cy, 0, sy, 0, 1, 0, -sy, 0, cy};
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0;
+            for (int k = 0; k < 3; ++k) s += A[3 * i + k] * B[3 * k + j];
+            out->rotation[3 * i + j] = s;
+        }
+    out->translation[0] = 0.0;
+    out->translation[1] = 0.0;
+    out->translation[2] = -dist;
+    out->scale = scale;
+    return ICG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+// icg_internal.h — shared declarations of the B200 product library
+// (host runtime in icg_host.cu, kernels in k_*.cu).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/isocull_b200.h"
+
+namespace icg {
+
+// ---------------------------------------------------------------------------
+// Error plumbing: no exceptions cross the C ABI.
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+struct Status {
+    int code = ICG_OK;
+    std::string msg;
+};
+
+#define ICG_CUDA_TRY(expr)                                                                     \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess) {                                                               \
+            ::icg::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+            return ICG_ERUNTIME;                                                               \
+        }                                                                                      \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Device-side counters of one extraction / render (one struct in HBM).
+// ---------------------------------------------------------------------------
+struct DevCounters {
+    unsigned int list_count;          // E0 compaction result
+    unsigned int cf_count[2];         // conflict lists (ping-pong by iteration)
+    unsigned int nx_count[2];         // conflict-neighbour lists (ping-pong)
+    unsigned int warning;             // conflict bound hit
+    unsigned int unroll_exhausted;    // device loop ran out of unrolled iterations
+    unsigned int overflow;            // a work list overflowed
+    unsigned long long evals[ICG_MAX_LEVELS];
+    unsigned long long refined[ICG_MAX_LEVELS];
+    unsigned int conflict_iters[ICG_MAX_LEVELS];
+    unsigned long long covered, degenerate, grazing;
+    unsigned int surface_count;
+    unsigned int pad;
+};
+
+// Analytic scene in constant-friendly form (union of primitives).
+struct DevPrim {
+    int kind, rotated;
+    double c[3], a[3], b[3];
+    double radius, half[3], major, minor, inv[9];
+};
+
+struct DevScene {
+    DevPrim prims[ICG_MAX_PRIMS];
+    int n_prims;
+    double tau;
+    double sdf_scale;
+};
+
+// Fixed PIFu architecture (BASELINE.json configs[1-3]).
+constexpr int kC = 256;           // feature channels
+constexpr int kGeoSkip = 257;     // [Phi(256), z]
+constexpr int kTexSkip = 513;     // [Phi(256), h3(256), z]
+constexpr int kGeoOut[5] = {1024, 512, 256, 128, 1};
+constexpr int kTexOut[5] = {1024, 512, 256, 128, 3};
+
+// Weights of one MLP in the SIMT layout: per layer Wt[K][O] (O contiguous),
+// K = prev_out + skip (prev activations first).
+struct SimtMlp {
+    const float* wt[5];
+    const float* b[5];
+    int out[5];
+    int in[5];
+    int skip;
+    float slope;
+};
+
+// Packed tcgen05 operand stream of one MLP (see k_mlp_tc.cu for the layout).
+struct TcMlp {
+    const uint8_t* stream;    // bf16 hi/lo weight tiles in consumption order
+    size_t stream_bytes;
+    const float* bias;        // concatenated fp32 biases
+    const float* w_last;      // final layer fp32 [out][prev+skip]
+    int bias_off[5];
+    int valid;
+};
+
+// Where the evaluated points come from and where results go.
+struct EvalJob {
+    // source: node list of a level grid, or explicit points
+    const uint32_t* list;         // node indices (nullptr with list_count==nullptr: dense 0..n^3-1)
+    const unsigned int* count;    // device count (nullptr: use n_static)
+    unsigned int n_static;
+    int cells;                    // level R
+    const double* points;         // explicit points (n x 3), when list and count are null
+    // grid epilogue
+    float* values;
+    uint8_t* states;
+    const uint32_t* tentbin;      // conflict detection (nullptr: none)
+    uint32_t* conflicts;
+    unsigned int* conflict_count;
+    unsigned int conflict_cap;
+    unsigned long long* evals;    // += count (block 0)
+    unsigned int* iters;          // += (count > 0) (block 0)
+    unsigned int* overflow;
+    // point epilogue
+    float* out;                   // occupancy per point (or rgb x3 for texture)
+    const uint32_t* out_pixel;    // texture: pixel index per point (out = rgb image)
+    float out_clamp;              // texture: clamp01 when nonzero
+};
+
+struct FieldDev {
+    int kind;                 // ICG_FIELD_*
+    int precision;
+    const DevScene* scene;    // device pointer
+    const float* fmap_hwc;    // H x W x C fp32
+    int C, H, W;
+};
+
+// ---- kernel launchers (k_*.cu) -------------------------------------------
+int launch_analytic_eval(const FieldDev& f, const EvalJob& job, unsigned int max_points, cudaStream_t s);
+int launch_pifu_simt_eval(const FieldDev& f, const SimtMlp& geo, const EvalJob& job,
+                          unsigned int max_points, cudaStream_t s);
+int launch_pifu_simt_texture(const FieldDev& f, const SimtMlp& geo, const SimtMlp& tex,
+                             const EvalJob& job, unsigned int max_points, cudaStream_t s);
+int launch_pifu_tc_eval(const FieldDev& f, const TcMlp& geo, const EvalJob& job, unsigned int max_points,
+                        bool bf16x3, cudaStream_t s);
+int launch_pifu_tc_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const EvalJob& job,
+                           unsigned int max_points, bool bf16x3, cudaStream_t s);
+int launch_fmap_chw_to_hwc(const float* chw, float* hwc, int C, int H, int W, cudaStream_t s);
+
+// grid kernels (k_grid.cu)
+struct LevelBufs {
+    const float* cv;  const uint8_t* cs;   // coarse grid
+    float* fv;        uint8_t* fs;         // fine grid
+    uint32_t* cbin;                         // coarse binarized bits (flat)
+    uint32_t* mixed;                        // coarse cell bits (flat over Rc^3)
+    uint32_t* tentbin;                      // fine bits
+    uint32_t* sel;                          // fine bits (flagged & !evaluated)
+    uint32_t* queued;                       // fine bits
+    uint32_t* block_counts;                 // per 1024-node block
+    uint32_t* list;                         // E0 output
+    int rc;                                 // coarse cells
+};
+int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s);
+int launch_conflict_expand(uint32_t* fine_queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
+                           DevCounters* ctr, int iter, int max_iters, uint32_t* next_list,
+                           unsigned int cap, cudaStream_t s);
+int launch_unroll_check(DevCounters* ctr, int iter_parity, cudaStream_t s);
+int launch_binarize(const float* v, uint8_t* out, size_t n, cudaStream_t s);
+int launch_iou(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* inter_union, cudaStream_t s);
+int launch_fill_states(uint8_t* s, size_t n, uint8_t v, cudaStream_t st);
+
+// render (k_render.cu)
+struct RenderJob {
+    const float* values;
+    int cells;
+    double rot[9], trans[3], scale;
+    int width, height;
+    float bg[3];
+    float* depth;
+    float* rgb;
+    uint8_t* mask;
+    int32_t* surface_k;
+    double* surface_pts;     // world points of covered pixels (compacted)
+    uint32_t* surface_px;    // pixel index per surface point
+    DevCounters* ctr;
+};
+int launch_render_first_crossing(const RenderJob& r, cudaStream_t s);
+
+size_t tc_stream_bytes(int which);
+int tc_pack_mlp(int which, const float* const* w, const float* const* b, uint8_t* host_stream,
+                float* host_bias, float* host_wlast);
+size_t tc_bias_floats(int which);
+size_t tc_wlast_floats(int which);
+
+}  // namespace icg

@@ -1,0 +1,130 @@
+// k_render.cu — mesh-free first-crossing renderer on sm_100a
+// (conventions of render.hpp:140-206 and 264-278).
+//
+// One thread per pixel.  Pixel (col, row) is the view ray x = -1 + 2 col/(W-1),
+// y = 1 - 2 row/(H-1) (row 0 at the top, render.hpp:48-49); sample k sits at
+// view z = 1 - 2k/R (k = 0 nearest, grid.hpp:50-53) and is mapped to the world
+// grid with view_to_world (render.hpp:29-32) in double, rounded once to fp32
+// grid coordinates, then trilinearly interpolated in fp32 in a fixed order.
+// The first sample with value >= 0.5f is the crossing (argmax of the binarised
+// column with the smallest-index tie rule, grid.hpp:173-197); the bracket
+// (k1-1, k1) gives s = clamp((0.5-v0)/(v1-v0), 0, 1) (s = 1 when k1 == 0 or
+// the bracket is degenerate) and depth = 1 - 2(k1-1+s)/R (render.hpp:190-204).
+// Every operation is an explicit round-to-nearest intrinsic, so the CPU oracle
+// (oracle/isocull_oracle.c, -ffp-contract=off) reproduces each crossing index
+// bit-exactly.  Covered pixels append their world surface point to a compact
+// list consumed by the texture MLP.
+#include "eval_common.cuh"
+
+namespace icg {
+
+__device__ __forceinline__ float lerp_rn(float a, float b, float t) {
+    return __fadd_rn(a, __fmul_rn(t, __fsub_rn(b, a)));
+}
+
+__device__ __forceinline__ float sample_grid(const float* __restrict__ V, int R, float gx, float gy, float gk) {
+    float fR = (float)R;
+    if (!(gx >= 0.0f && gx <= fR && gy >= 0.0f && gy <= fR && gk >= 0.0f && gk <= fR)) return 0.0f;
+    int i0 = min((int)floorf(gx), R - 1), j0 = min((int)floorf(gy), R - 1), k0 = min((int)floorf(gk), R - 1);
+    float fx = __fsub_rn(gx, (float)i0), fy = __fsub_rn(gy, (float)j0), fk = __fsub_rn(gk, (float)k0);
+    size_t n = (size_t)R + 1, sj = n, sk = n * n;
+    size_t b = (size_t)i0 + n * ((size_t)j0 + n * (size_t)k0);
+    float c00 = lerp_rn(__ldg(&V[b]), __ldg(&V[b + 1]), fx);
+    float c10 = lerp_rn(__ldg(&V[b + sj]), __ldg(&V[b + sj + 1]), fx);
+    float c01 = lerp_rn(__ldg(&V[b + sk]), __ldg(&V[b + sk + 1]), fx);
+    float c11 = lerp_rn(__ldg(&V[b + sj + sk]), __ldg(&V[b + sj + sk + 1]), fx);
+    float c0 = lerp_rn(c00, c10, fy);
+    float c1 = lerp_rn(c01, c11, fy);
+    return lerp_rn(c0, c1, fk);
+}
+
+// view_to_world, render.hpp:29-32: R^T (v - t), v = (x/scale, y/scale, z)
+__device__ __forceinline__ void view_to_world_d(const RenderJob& r, double x, double y, double z, double* w) {
+    double v0 = __dsub_rn(__ddiv_rn(x, r.scale), r.trans[0]);
+    double v1 = __dsub_rn(__ddiv_rn(y, r.scale), r.trans[1]);
+    double v2 = __dsub_rn(z, r.trans[2]);
+    const double* m = r.rot;
+    w[0] = __dadd_rn(__dadd_rn(__dmul_rn(m[0], v0), __dmul_rn(m[3], v1)), __dmul_rn(m[6], v2));
+    w[1] = __dadd_rn(__dadd_rn(__dmul_rn(m[1], v0), __dmul_rn(m[4], v1)), __dmul_rn(m[7], v2));
+    w[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[2], v0), __dmul_rn(m[5], v1)), __dmul_rn(m[8], v2));
+}
+
+__global__ void __launch_bounds__(256) k_render(RenderJob r) {
+    const int W = r.width, H = r.height, R = r.cells;
+    size_t npx = (size_t)W * H;
+    size_t px = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool covered = false, degenerate = false, grazing = false;
+    if (px < npx) {
+        int col = (int)(px % W), row = (int)(px / W);
+        double vx = __dadd_rn(-1.0, __ddiv_rn(__dmul_rn(2.0, (double)col), (double)(W - 1)));
+        double vy = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)row), (double)(H - 1)));
+        double hr = __dmul_rn(0.5, (double)R);
+        int k1 = -1;
+        float vprev = 0.0f, vhit = 0.0f;
+        for (int k = 0; k <= R; ++k) {
+            double vz = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)k), (double)R));
+            double w[3];
+            view_to_world_d(r, vx, vy, vz, w);
+            float gx = (float)__dmul_rn(__dadd_rn(w[0], 1.0), hr);
+            float gy = (float)__dmul_rn(__dadd_rn(w[1], 1.0), hr);
+            float gk = (float)__dmul_rn(__dsub_rn(1.0, w[2]), hr);
+            float v = sample_grid(r.values, R, gx, gy, gk);
+            if (v >= 0.5f) {
+                k1 = k;
+                vhit = v;
+                break;
+            }
+            if (v > 0.0f && v < 1.0f) grazing = true;
+            vprev = v;
+        }
+        r.rgb[3 * px + 0] = r.bg[0];
+        r.rgb[3 * px + 1] = r.bg[1];
+        r.rgb[3 * px + 2] = r.bg[2];
+        if (k1 < 0) {
+            r.depth[px] = -2.0f;  // kInvalidDepth, render.hpp:72
+            r.mask[px] = 0;
+            if (r.surface_k) r.surface_k[px] = -1;
+        } else {
+            grazing = false;
+            covered = true;
+            double s = 1.0;
+            if (k1 > 0) {
+                double v1 = (double)vhit, v0 = (double)vprev;
+                double denom = __dsub_rn(v1, v0);
+                if (denom > 0.0) {
+                    s = __ddiv_rn(__dsub_rn(0.5, v0), denom);
+                    s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
+                } else {
+                    degenerate = true;
+                }
+            }
+            double depth = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn(__dsub_rn((double)k1, 1.0), s)), (double)R));
+            r.depth[px] = (float)depth;
+            r.mask[px] = 1;
+            if (r.surface_k) r.surface_k[px] = k1;
+            double w[3];
+            view_to_world_d(r, vx, vy, depth, w);
+            unsigned pos = atomicAdd(&r.ctr->surface_count, 1u);
+            r.surface_pts[3 * (size_t)pos + 0] = w[0];
+            r.surface_pts[3 * (size_t)pos + 1] = w[1];
+            r.surface_pts[3 * (size_t)pos + 2] = w[2];
+            r.surface_px[pos] = (uint32_t)px;
+        }
+    }
+    unsigned cb = __ballot_sync(0xffffffffu, covered), db = __ballot_sync(0xffffffffu, degenerate),
+             gb = __ballot_sync(0xffffffffu, grazing);
+    if ((threadIdx.x & 31) == 0) {
+        if (cb) atomicAdd(&r.ctr->covered, (unsigned long long)__popc(cb));
+        if (db) atomicAdd(&r.ctr->degenerate, (unsigned long long)__popc(db));
+        if (gb) atomicAdd(&r.ctr->grazing, (unsigned long long)__popc(gb));
+    }
+}
+
+int launch_render_first_crossing(const RenderJob& r, cudaStream_t s) {
+    size_t npx = (size_t)r.width * r.height;
+    k_render<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(r);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
+}  // namespace icg
