@@ -119,7 +119,7 @@ __device__ __forceinline__ void run_layer(const SimtMlp& m, int l, const float* 
 
 // Final narrow layer (1 or 3 outputs): one warp per (point, output) dot product.
 __device__ __forceinline__ void last_layer(const SimtMlp& m, const float* hin, int hin_stride, const float* skip,
-                                           int skip_stride, float* out /* [TP][O] */) {
+                                           int skip_stride, float* out /* [TP][4] */) {
     const int l = 4, O = m.out[4], Kh = m.out[3], K = Kh + m.skip;
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int job = warp; job < TP * O; job += NT / 32) {
@@ -131,7 +131,7 @@ __device__ __forceinline__ void last_layer(const SimtMlp& m, const float* hin, i
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) out[p * O + c] = acc + m.b[l][c];
+        if (lane == 0) out[p * 4 + c] = acc + m.b[l][c];
     }
 }
 
