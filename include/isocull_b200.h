@@ -222,6 +222,32 @@ int icg_compare_iou(icg_context* ctx, const uint8_t* a, const uint8_t* b, size_t
                     double* iou);
 
 /* ======================================================================== */
+/* Instrumentation (CUDA events on the context stream around every kernel    */
+/* class; counters accumulate until icg_profile_reset).                      */
+/* ======================================================================== */
+typedef struct icg_profile {
+    uint64_t kernel_launches;      /* all library kernel launches (incl. early-exit ones) */
+    uint64_t geo_mlp_launches;     /* geometry-field evaluation launches */
+    uint64_t geo_points;           /* points evaluated by them */
+    double geo_mlp_ms;             /* summed device time of those launches */
+    uint64_t tex_mlp_launches;
+    uint64_t tex_points;
+    double tex_mlp_ms;
+    uint64_t dense_launches;       /* per-level dense passes + compaction + conflict expansion */
+    double dense_ms;
+    uint64_t dense_bytes;          /* algorithmic bytes of the dense passes */
+    uint64_t render_launches;
+    double render_ms;
+    uint64_t render_bytes;
+    double frame_ms;               /* summed device time of whole frames / extractions */
+    uint64_t frames;
+} icg_profile;
+
+int icg_profile_enable(icg_context* ctx, int on);
+int icg_profile_reset(icg_context* ctx);
+int icg_profile_get(icg_context* ctx, icg_profile* out);
+
+/* ======================================================================== */
 /* Host helpers                                                              */
 /* ======================================================================== */
 

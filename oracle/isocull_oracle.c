@@ -275,6 +275,61 @@ static void mlp_block(const orc_mlp* net, const double* skip, int upto, double* 
     *result = (double*)prev;
 }
 
+/* Single-point variants (the FieldOracle per-point shape): 8 output rows at a
+ * time for instruction-level parallelism; each output still accumulates in k
+ * order, so results equal the blocked path bit-for-bit. */
+static void layer_point(const float* W, const float* b, int out_dim, const double* prev, int prev_dim,
+                        const double* skip, int skip_dim, double* out, int leaky, double slope) {
+    int in_dim = prev_dim + skip_dim;
+    int o = 0;
+    for (; o + 8 <= out_dim; o += 8) {
+        double acc[8];
+        const float* wr[8];
+        for (int r = 0; r < 8; ++r) {
+            acc[r] = (double)b[o + r];
+            wr[r] = W + (size_t)(o + r) * in_dim;
+        }
+        for (int k = 0; k < prev_dim; ++k) {
+            double x = prev[k];
+            for (int r = 0; r < 8; ++r) acc[r] += (double)wr[r][k] * x;
+        }
+        for (int k = 0; k < skip_dim; ++k) {
+            double x = skip[k];
+            for (int r = 0; r < 8; ++r) acc[r] += (double)wr[r][prev_dim + k] * x;
+        }
+        for (int r = 0; r < 8; ++r) {
+            double v = acc[r];
+            if (leaky && v < 0.0) v = v * slope;
+            out[o + r] = v;
+        }
+    }
+    for (; o < out_dim; ++o) {
+        double acc = (double)b[o];
+        const float* wr = W + (size_t)o * in_dim;
+        for (int k = 0; k < prev_dim; ++k) acc += (double)wr[k] * prev[k];
+        for (int k = 0; k < skip_dim; ++k) acc += (double)wr[prev_dim + k] * skip[k];
+        if (leaky && acc < 0.0) acc = acc * slope;
+        out[o] = acc;
+    }
+}
+
+static const double* mlp_point(const orc_mlp* net, const double* skip, int upto, double* bufA, double* bufB) {
+    const double* prev = NULL;
+    int prev_dim = 0;
+    double* cur = bufA;
+    double* other = bufB;
+    for (int l = 0; l < upto; ++l) {
+        layer_point(net->w[l], net->b[l], net->out_dims[l], prev, prev_dim, skip, net->skip_dim, cur,
+                    l < net->n_layers - 1, net->slope);
+        prev = cur;
+        prev_dim = net->out_dims[l];
+        double* t = cur;
+        cur = other;
+        other = t;
+    }
+    return prev;
+}
+
 static double sigmoid(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 typedef struct {
@@ -338,7 +393,30 @@ static void pifu_range(void* c, size_t b, size_t e) {
     free(bufB);
 }
 
+static void pifu_one(const orc_pifu* m, const double* P, double* out, int mode) {
+    double gskip[257 + 8], tskip[513 + 8], bufA[1024], bufB[1024];
+    int C = m->C;
+    orc_sample_features(m, P, gskip);
+    gskip[C] = P[2];
+    if (mode == 2) {
+        for (int c = 0; c < C; ++c) tskip[c] = gskip[c];
+        const double* h3 = mlp_point(&m->geo, gskip, 3, bufA, bufB);
+        for (int k = 0; k < m->geo.out_dims[2]; ++k) tskip[C + k] = h3[k];
+        tskip[m->tex.skip_dim - 1] = P[2];
+        const double* o = mlp_point(&m->tex, tskip, m->tex.n_layers, bufA, bufB);
+        for (int ch = 0; ch < 3; ++ch) out[ch] = sigmoid(o[ch]);
+    } else {
+        const double* o = mlp_point(&m->geo, gskip, m->geo.n_layers, bufA, bufB);
+        double logit = o[0] - m->sdf_scale * orc_scene_sdf(m->prims, m->n_prims, P);
+        out[0] = mode == 1 ? logit : sigmoid(logit);
+    }
+}
+
 static void pifu_run(const orc_pifu* m, const double* pts, size_t n, double* out, int threads, int mode) {
+    if (n == 1 && m->C == 256) {
+        pifu_one(m, pts, out, mode);
+        return;
+    }
     pifu_ctx c = {m, pts, n, out, mode};
     if (threads <= 1 || n < 2 * PB) {
         pifu_range(&c, 0, n);

@@ -124,6 +124,9 @@ def ref() -> C.CDLL:
                                         C.c_double, C.c_int, C.c_int, f64p, C.c_int, f64p, f64p, u8p,
                                         C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                         C.POINTER(C.c_int)]
+        lib.ref_occupancy_batch.restype = C.c_uint64
+        lib.ref_occupancy_batch.argtypes = [C.c_void_p, C.c_void_p, f64p, C.c_size_t, C.c_int, f64p]
+        lib.ref_texture_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, f64p, C.c_size_t, C.c_int, f64p]
         lib.ref_camera_from_angles.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, f64p, f64p]
         lib.ref_scene_load.restype = C.c_void_p
         lib.ref_scene_load.argtypes = [C.c_char_p]
@@ -379,6 +382,20 @@ def ref_extract(pt_fn: int, user: int, coarsest: int, level: int, variant: int =
     return dict(values=vals, states=sts, binarized=binz, evals_per_level=[int(evals[l]) for l in range(level + 1)],
                 total_evals=int(total.value), oracle_calls=int(calls.value), conflict_warning=bool(warn.value),
                 wall_seconds=wall.value)
+
+
+def ref_occupancy_batch(pt_fn: int, user: int, pts: np.ndarray, workers: int = 1) -> np.ndarray:
+    pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    out = np.empty(len(pts))
+    ref().ref_occupancy_batch(pt_fn, user, _p(pts, C.c_double), len(pts), workers, _p(out, C.c_double))
+    return out
+
+
+def ref_texture_batch(pt_fn: int, tex_fn: int, user: int, pts: np.ndarray, workers: int = 1) -> np.ndarray:
+    pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    out = np.empty((len(pts), 3))
+    ref().ref_texture_batch(pt_fn, tex_fn, user, _p(pts, C.c_double), len(pts), workers, _p(out, C.c_double))
+    return out
 
 
 class RefScene:

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <exception>
 #include <string>
+#include <vector>
 
 #include "isocull/field.hpp"
 #include "isocull/grid.hpp"
@@ -122,6 +123,32 @@ int ref_render_view(ref_pt_occ_fn occ, ref_pt_tex_fn tex, void* user, double yaw
         return fail(e, ICG_EINVAL);
     } catch (const std::exception& e) {
         return fail(e, ICG_ERUNTIME);
+    }
+}
+
+// FieldOracle::occupancy_batch / texture_batch (field.hpp:41-47, 56-63): the
+// reference's own batched evaluation (parallel_for over `workers` threads,
+// one std::function call per point).  Returns the call counter.
+uint64_t ref_occupancy_batch(ref_pt_occ_fn occ, void* user, const double* pts, std::size_t n, int workers,
+                             double* out) {
+    FieldOracle oracle = make_oracle(occ, nullptr, user);
+    std::vector<Vec3> p(n);
+    for (std::size_t i = 0; i < n; ++i) p[i] = Vec3{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    std::vector<double> v = oracle.occupancy_batch(p, workers);
+    std::memcpy(out, v.data(), n * sizeof(double));
+    return oracle.calls();
+}
+
+void ref_texture_batch(ref_pt_occ_fn occ, ref_pt_tex_fn tex, void* user, const double* pts, std::size_t n,
+                       int workers, double* rgb) {
+    FieldOracle oracle = make_oracle(occ, tex, user);
+    std::vector<Vec3> p(n);
+    for (std::size_t i = 0; i < n; ++i) p[i] = Vec3{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    std::vector<Vec3> v = oracle.texture_batch(p, workers);
+    for (std::size_t i = 0; i < n; ++i) {
+        rgb[3 * i] = v[i].x;
+        rgb[3 * i + 1] = v[i].y;
+        rgb[3 * i + 2] = v[i].z;
     }
 }
 

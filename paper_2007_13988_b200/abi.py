@@ -121,6 +121,26 @@ class icg_image(C.Structure):
     ]
 
 
+class icg_profile(C.Structure):
+    _fields_ = [
+        ("kernel_launches", C.c_uint64),
+        ("geo_mlp_launches", C.c_uint64),
+        ("geo_points", C.c_uint64),
+        ("geo_mlp_ms", C.c_double),
+        ("tex_mlp_launches", C.c_uint64),
+        ("tex_points", C.c_uint64),
+        ("tex_mlp_ms", C.c_double),
+        ("dense_launches", C.c_uint64),
+        ("dense_ms", C.c_double),
+        ("dense_bytes", C.c_uint64),
+        ("render_launches", C.c_uint64),
+        ("render_ms", C.c_double),
+        ("render_bytes", C.c_uint64),
+        ("frame_ms", C.c_double),
+        ("frames", C.c_uint64),
+    ]
+
+
 ctx_p = C.c_void_p
 
 # (name, restype, argtypes) for every symbol the header declares
@@ -140,6 +160,9 @@ SIGNATURES = [
     ("icg_occupancy_batch", C.c_int, [ctx_p, C.POINTER(icg_field), f64p, C.c_size_t, C.c_int, f32p]),
     ("icg_texture_batch", C.c_int, [ctx_p, C.POINTER(icg_field), f64p, C.c_size_t, C.c_int, f32p]),
     ("icg_compare_iou", C.c_int, [ctx_p, u8p, u8p, C.c_size_t, C.c_int, f64p]),
+    ("icg_profile_enable", C.c_int, [ctx_p, C.c_int]),
+    ("icg_profile_reset", C.c_int, [ctx_p]),
+    ("icg_profile_get", C.c_int, [ctx_p, C.POINTER(icg_profile)]),
     ("icg_host_alloc", C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     ("icg_host_free", C.c_int, [C.c_void_p]),
     ("icg_device_alloc", C.c_int, [ctx_p, C.c_size_t, C.POINTER(C.c_void_p)]),

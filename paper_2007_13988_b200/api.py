@@ -287,6 +287,52 @@ class Context:
     def compare_iou(self, a: np.ndarray, b: np.ndarray) -> float:
         return compare_iou(a, b, self)
 
+    # instrumentation ------------------------------------------------------------
+    def profile(self, on: bool = True, reset: bool = True):
+        _check(self._lib.icg_profile_enable(self.h, 1 if on else 0))
+        if reset:
+            _check(self._lib.icg_profile_reset(self.h))
+
+    def profile_get(self) -> dict:
+        p = abi.icg_profile()
+        _check(self._lib.icg_profile_get(self.h, C.byref(p)))
+        return {name: getattr(p, name) for name, _ in abi.icg_profile._fields_}
+
+    # raw buffers (pinned host / device) for end-to-end and device-resident runs
+    def device_alloc(self, nbytes: int) -> int:
+        ptr = C.c_void_p()
+        _check(self._lib.icg_device_alloc(self.h, nbytes, C.byref(ptr)))
+        return ptr.value
+
+    def device_free(self, ptr: int):
+        _check(self._lib.icg_device_free(self.h, C.c_void_p(ptr)))
+
+    def memcpy(self, dst: int, src: int, nbytes: int, dst_mem: int, src_mem: int):
+        _check(self._lib.icg_memcpy(self.h, C.c_void_p(dst), C.c_void_p(src), nbytes, dst_mem, src_mem))
+
+    def frame_raw(self, fld: "_Field", cfg: AlgoConfig, camera: CameraSpec, width: int, height: int,
+                  img: "abi.icg_image", ext: Optional["abi.icg_extraction"] = None, background=(0.0, 0.0, 0.0)):
+        """icg_frame with caller-owned output structs (host or device buffers)."""
+        bg = np.asarray(background, dtype=np.float32)
+        cam = camera.to_c()
+        cc = cfg.to_c()
+        if ext is None:
+            ext = abi.icg_extraction()
+            ext.mem = abi.ICG_MEM_HOST
+        _check(self._lib.icg_frame(self.h, C.byref(fld.c), C.byref(cc), C.byref(cam), width, height,
+                                   _ptr(bg, C.c_float), C.byref(ext), C.byref(img)))
+        return ext, img
+
+
+def host_alloc(nbytes: int) -> int:
+    ptr = C.c_void_p()
+    _check(abi.lib().icg_host_alloc(nbytes, C.byref(ptr)))
+    return ptr.value
+
+
+def host_free(ptr: int):
+    _check(abi.lib().icg_host_free(C.c_void_p(ptr)))
+
 
 def _extraction(out, cfg, vals, sts, binz) -> ExtractionResult:
     L = cfg.target_level

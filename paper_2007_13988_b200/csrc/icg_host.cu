@@ -85,7 +85,19 @@ struct icg_context {
     DBuf depth, rgb, mask, surfk, spts, spx;
     // last extraction
     int last_cells = 0, last_buf = -1;
-    int unroll = 6;
+    // instrumentation
+    struct Mark {
+        int kind;  // 0 geo mlp, 1 tex mlp, 2 dense, 3 render
+        int slot;
+    };
+    bool prof_on = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<Mark> marks;
+    int ev_used = 0;
+    icg_profile prof{};
+    uint64_t launches = 0;
+    // device-side conflict-loop depth per level, adapted from the previous frame
+    int unroll[ICG_MAX_LEVELS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4};
 };
 
 namespace {
@@ -95,6 +107,45 @@ size_t nodes3(int cells) {
     return n * n * n;
 }
 size_t words(size_t bits) { return (bits + 31) / 32; }
+
+// ---- instrumentation ----------------------------------------------------------
+int prof_begin(icg_context* c, int kind) {
+    if (!c->prof_on) return -1;
+    if (c->ev_used + 2 > (int)c->ev_pool.size()) {
+        for (int i = 0; i < 64; ++i) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return -1;
+            c->ev_pool.push_back(e);
+        }
+    }
+    int slot = c->ev_used;
+    c->ev_used += 2;
+    cudaEventRecord(c->ev_pool[slot], c->stream);
+    c->marks.push_back({kind, slot});
+    return slot;
+}
+void prof_end(icg_context* c, int slot) {
+    if (slot >= 0) cudaEventRecord(c->ev_pool[slot + 1], c->stream);
+}
+void prof_discard(icg_context* c) {
+    c->marks.clear();
+    c->ev_used = 0;
+}
+// after a stream sync: fold the recorded intervals into the totals
+void prof_collect(icg_context* c) {
+    if (!c->prof_on) return;
+    for (const auto& m : c->marks) {
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, c->ev_pool[m.slot], c->ev_pool[m.slot + 1]);
+        switch (m.kind) {
+            case 0: c->prof.geo_mlp_ms += ms; c->prof.geo_mlp_launches++; break;
+            case 1: c->prof.tex_mlp_ms += ms; c->prof.tex_mlp_launches++; break;
+            case 2: c->prof.dense_ms += ms; c->prof.dense_launches++; break;
+            case 3: c->prof.render_ms += ms; c->prof.render_launches++; break;
+        }
+    }
+    prof_discard(c);
+}
 
 int ensure_grid(icg_context* c, int cells) {
     size_t N = nodes3(cells);
@@ -187,6 +238,7 @@ int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
         if (int r = c->fmap_hwc.ensure(n * 4)) return r;
         if (int r = launch_fmap_chw_to_hwc(chw, c->fmap_hwc.as<float>(), f->fmap_c, f->fmap_h, f->fmap_w, c->stream))
             return r;
+        c->launches += 1;
         fd.fmap_hwc = c->fmap_hwc.as<float>();
         fd.C = f->fmap_c;
         fd.H = f->fmap_h;
@@ -196,20 +248,35 @@ int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
 }
 
 int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
-    if (fd.kind == ICG_FIELD_ANALYTIC) return launch_analytic_eval(fd, job, max_points, c->stream);
-    if (fd.precision == ICG_PREC_FP32_SIMT) return launch_pifu_simt_eval(fd, c->geo_simt, job, max_points, c->stream);
-    return launch_pifu_tc_eval(fd, c->geo_tc, job, max_points, fd.precision == ICG_PREC_FP32, c->stream);
+    int slot = prof_begin(c, 0);
+    int r;
+    if (fd.kind == ICG_FIELD_ANALYTIC)
+        r = launch_analytic_eval(fd, job, max_points, c->stream);
+    else if (fd.precision == ICG_PREC_FP32_SIMT)
+        r = launch_pifu_simt_eval(fd, c->geo_simt, job, max_points, c->stream);
+    else
+        r = launch_pifu_tc_eval(fd, c->geo_tc, job, max_points, fd.precision == ICG_PREC_FP32, c->stream);
+    prof_end(c, slot);
+    c->launches += 1;
+    return r;
 }
 
 int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
+    int slot = prof_begin(c, 1);
+    int r;
     if (fd.precision == ICG_PREC_FP32_SIMT)
-        return launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
-    return launch_pifu_tc_texture(fd, c->geo_tc, c->tex_tc, job, max_points, fd.precision == ICG_PREC_FP32,
-                                  c->stream);
+        r = launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
+    else
+        r = launch_pifu_tc_texture(fd, c->geo_tc, c->tex_tc, job, max_points, fd.precision == ICG_PREC_FP32,
+                                   c->stream);
+    prof_end(c, slot);
+    c->launches += 1;
+    return r;
 }
 
 // Issues one whole extraction on the context stream (no host sync).
-int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg, int unroll) {
+int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg) {
+    prof_discard(c);
     DevCounters* ctr = c->ctr.as<DevCounters>();
     ICG_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), c->stream));
     const int L = cfg->target_level;
@@ -257,7 +324,13 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
         lb.block_counts = c->block_counts.as<uint32_t>();
         lb.list = c->list_e0.as<uint32_t>();
         lb.rc = cells;
-        if (int r = launch_level_classify(lb, ctr, l, c->stream)) return r;
+        {
+            int slot = prof_begin(c, 2);
+            int r = launch_level_classify(lb, ctr, l, c->stream);
+            prof_end(c, slot);
+            c->launches += 5;
+            if (r) return r;
+        }
         ICG_CUDA_TRY(cudaMemsetAsync(c->queued.p, 0, words(nf) * 4, c->stream));
         // evaluate E0 (localize.hpp:331-332) with the fused conflict test
         EvalJob job{};
@@ -276,12 +349,18 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
         if (int r = run_eval(c, fd, job, (unsigned)nf)) return r;
         if (cfg->conflict_pass) {
             int max_iters = cfg->max_conflict_iters > 0 ? cfg->max_conflict_iters : fcells;
+            const int unroll = c->unroll[l];
             for (int it = 0; it < unroll; ++it) {
                 int p = it & 1;
-                if (int r = launch_conflict_expand(c->queued.as<uint32_t>(), lb.fs, fcells, c->cf[p].as<uint32_t>(),
+                {
+                    int slot = prof_begin(c, 2);
+                    int r = launch_conflict_expand(c->queued.as<uint32_t>(), lb.fs, fcells, c->cf[p].as<uint32_t>(),
                                                    ctr, it, max_iters, c->nx[p].as<uint32_t>(), (unsigned)nf,
-                                                   c->stream))
-                    return r;
+                                                   c->stream);
+                    prof_end(c, slot);
+                    c->launches += 1;
+                    if (r) return r;
+                }
                 EvalJob cj{};
                 cj.list = c->nx[p].as<uint32_t>();
                 cj.count = &ctr->nx_count[p];
@@ -297,7 +376,8 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                 cj.overflow = &ctr->overflow;
                 if (int r = run_eval(c, fd, cj, (unsigned)nf)) return r;
             }
-            if (int r = launch_unroll_check(ctr, unroll & 1, c->stream)) return r;
+            if (int r = launch_unroll_check(ctr, unroll & 1, l, c->stream)) return r;
+            c->launches += 1;
         }
         b ^= 1;
         cells = fcells;
@@ -323,6 +403,7 @@ int finish_extract_outputs(icg_context* c, const icg_algo_config* cfg, icg_extra
     if (out->binarized) {
         if (int r = c->binar.ensure(N)) return r;
         if (int r = launch_binarize(c->vals[c->last_buf].as<float>(), c->binar.as<uint8_t>(), N, c->stream)) return r;
+        c->launches += 1;
         if (int r = copy_out(c, out->binarized, c->binar.p, N, out->mem)) return r;
     }
     (void)cfg;
@@ -378,7 +459,13 @@ int issue_render(icg_context* c, const FieldDev& fd, const icg_camera* cam, int 
     rj.surface_pts = c->spts.as<double>();
     rj.surface_px = c->spx.as<uint32_t>();
     rj.ctr = ctr;
-    if (int r = launch_render_first_crossing(rj, c->stream)) return r;
+    {
+        int slot = prof_begin(c, 3);
+        int r = launch_render_first_crossing(rj, c->stream);
+        prof_end(c, slot);
+        c->launches += 1;
+        if (r) return r;
+    }
     if (fd.kind == ICG_FIELD_PIFU && c->has_tex) {
         EvalJob tj{};
         tj.points = c->spts.as<double>();
@@ -420,24 +507,60 @@ int check_render_args(icg_context* c, const icg_camera* cam, int W, int H) {
     return ICG_OK;
 }
 
+// fold one finished extraction / render into the profile totals
+void prof_extract_done(icg_context* c, const icg_algo_config* cfg) {
+    if (!c->prof_on) return;
+    const DevCounters& h = *c->h_ctr;
+    for (int l = 0; l <= cfg->target_level; ++l) c->prof.geo_points += h.evals[l];
+    if (cfg->variant == ICG_VARIANT_PROGRESSIVE) {
+        for (int l = 1; l <= cfg->target_level; ++l) {
+            // level pass: fine value+state written, coarse read, index list
+            c->prof.dense_bytes += 5 * nodes3(cfg->coarsest_cells << l) + 5 * nodes3(cfg->coarsest_cells << (l - 1)) +
+                                   4 * h.evals[l];
+        }
+    }
+}
+void prof_render_done(icg_context* c, int W, int H) {
+    if (!c->prof_on) return;
+    c->prof.tex_points += c->h_ctr->surface_count;
+    c->prof.render_bytes += 4 * nodes3(c->last_cells) + 17ull * (uint64_t)W * (uint64_t)H;
+}
+
 float elapsed(icg_context* c) {
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, c->e0, c->e1);
     return ms * 1e-3f;
 }
 
-// extraction with the unroll-exhaustion replay
+// After a successful extraction, size each level's device loop to what this
+// frame needed plus a margin; when a level ran out, deepen it and replay.
+bool adapt_unroll(icg_context* c, const icg_algo_config* cfg) {
+    const DevCounters& h = *c->h_ctr;
+    bool replay = false;
+    for (int l = 1; l <= cfg->target_level; ++l) {
+        if (h.unroll_exhausted & (1u << l)) {
+            c->unroll[l] *= 2;
+            replay = true;
+        }
+    }
+    if (!replay)
+        for (int l = 1; l <= cfg->target_level; ++l) {
+            int need = (int)h.conflict_iters[l];
+            c->unroll[l] = need + std::max(2, need / 4);
+        }
+    return replay;
+}
+
 int do_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg) {
-    for (;;) {
-        if (int r = issue_extract(c, fd, cfg, c->unroll)) return r;
+    for (int attempt = 0;; ++attempt) {
+        if (int r = issue_extract(c, fd, cfg)) return r;
         if (int r = sync_counters(c)) return r;
         if (c->h_ctr->overflow) {
             set_error("extract: device work list overflow");
             return ICG_ECAPACITY;
         }
-        if (!c->h_ctr->unroll_exhausted) return ICG_OK;
-        c->unroll *= 2;  // replay with a deeper device-side conflict loop
-        if (c->unroll > 4096) {
+        if (!adapt_unroll(c, cfg)) return ICG_OK;
+        if (attempt > 12) {
             set_error("extract: conflict loop did not converge");
             return ICG_ERUNTIME;
         }
@@ -514,6 +637,7 @@ int icg_destroy(icg_context* c) {
         c->tex_wt[l].release();
         c->tex_b[l].release();
     }
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->h_scene) cudaFreeHost(c->h_scene);
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->e0) cudaEventDestroy(c->e0);
@@ -629,6 +753,12 @@ int icg_extract(icg_context* c, const icg_field* field, const icg_algo_config* c
     if (int r = finish_extract_outputs(c, cfg, out)) return r;
     ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     fill_extraction_scalars(c, cfg, out, elapsed(c));
+    prof_extract_done(c, cfg);
+    prof_collect(c);
+    if (c->prof_on) {
+        c->prof.frame_ms += elapsed(c) * 1e3;
+        c->prof.frames += 1;
+    }
     return ICG_OK;
 }
 
@@ -641,12 +771,15 @@ int icg_render_localized(icg_context* c, const icg_field* field, const icg_camer
     FieldDev fd;
     if (int r = prepare_field(c, field, fd)) return r;
     if (fd.kind == ICG_FIELD_PIFU && !c->has_tex) return einval("render: scene has no texture (icg_set_mlp TEXTURE)");
+    prof_discard(c);
     ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
     if (int r = issue_render(c, fd, cam, W, H, bg)) return r;
     ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
     if (int r = finish_render_outputs(c, W, H, out)) return r;
     if (int r = sync_counters(c)) return r;
     fill_image_scalars(c, out, elapsed(c));
+    prof_render_done(c, W, H);
+    prof_collect(c);
     return ICG_OK;
 }
 
@@ -661,8 +794,8 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
     if (fd.kind == ICG_FIELD_PIFU && !c->has_tex) return einval("frame: scene has no texture (icg_set_mlp TEXTURE)");
     if (int r = ensure_grid(c, cfg->coarsest_cells << cfg->target_level)) return r;
     ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
-    for (;;) {
-        if (int r = issue_extract(c, fd, cfg, c->unroll)) return r;
+    for (int attempt = 0;; ++attempt) {
+        if (int r = issue_extract(c, fd, cfg)) return r;
         if (int r = issue_render(c, fd, cam, W, H, bg)) return r;
         ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
         if (int r = finish_render_outputs(c, W, H, img)) return r;
@@ -671,15 +804,21 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
             set_error("frame: device work list overflow");
             return ICG_ECAPACITY;
         }
-        if (!c->h_ctr->unroll_exhausted) break;
-        c->unroll *= 2;
-        if (c->unroll > 4096) {
+        if (!adapt_unroll(c, cfg)) break;
+        if (attempt > 12) {
             set_error("frame: conflict loop did not converge");
             return ICG_ERUNTIME;
         }
         ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
     }
     double secs = elapsed(c);
+    prof_extract_done(c, cfg);
+    prof_render_done(c, W, H);
+    prof_collect(c);
+    if (c->prof_on) {
+        c->prof.frame_ms += secs * 1e3;
+        c->prof.frames += 1;
+    }
     if (ext) {
         if (int r = finish_extract_outputs(c, cfg, ext)) return r;
         ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -754,6 +893,28 @@ int icg_compare_iou(icg_context* c, const uint8_t* a, const uint8_t* b, size_t n
     ICG_CUDA_TRY(cudaMemcpyAsync(iu, c->outv.p, 16, cudaMemcpyDeviceToHost, c->stream));
     ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     *iou = iu[1] ? (double)iu[0] / (double)iu[1] : 1.0;
+    return ICG_OK;
+}
+
+int icg_profile_enable(icg_context* c, int on) {
+    if (!c) return einval("null context");
+    c->prof_on = on != 0;
+    prof_discard(c);
+    return ICG_OK;
+}
+
+int icg_profile_reset(icg_context* c) {
+    if (!c) return einval("null context");
+    c->prof = icg_profile{};
+    c->launches = 0;
+    prof_discard(c);
+    return ICG_OK;
+}
+
+int icg_profile_get(icg_context* c, icg_profile* out) {
+    if (!c || !out) return einval("null argument");
+    *out = c->prof;
+    out->kernel_launches = c->launches;
     return ICG_OK;
 }
 

@@ -37,7 +37,7 @@ struct DevCounters {
     unsigned int cf_count[2];         // conflict lists (ping-pong by iteration)
     unsigned int nx_count[2];         // conflict-neighbour lists (ping-pong)
     unsigned int warning;             // conflict bound hit
-    unsigned int unroll_exhausted;    // device loop ran out of unrolled iterations
+    unsigned int unroll_exhausted;    // bit l: level l ran out of unrolled conflict iterations
     unsigned int overflow;            // a work list overflowed
     unsigned long long evals[ICG_MAX_LEVELS];
     unsigned long long refined[ICG_MAX_LEVELS];
@@ -150,7 +150,7 @@ int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaS
 int launch_conflict_expand(uint32_t* fine_queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
                            DevCounters* ctr, int iter, int max_iters, uint32_t* next_list,
                            unsigned int cap, cudaStream_t s);
-int launch_unroll_check(DevCounters* ctr, int iter_parity, cudaStream_t s);
+int launch_unroll_check(DevCounters* ctr, int iter_parity, int level, cudaStream_t s);
 int launch_binarize(const float* v, uint8_t* out, size_t n, cudaStream_t s);
 int launch_iou(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* inter_union, cudaStream_t s);
 int launch_fill_states(uint8_t* s, size_t n, uint8_t v, cudaStream_t st);

@@ -12,6 +12,10 @@ namespace icg {
 
 __global__ void __launch_bounds__(256) k_analytic_eval(const DevScene* __restrict__ scene, EvalJob job) {
     __shared__ DevScene s;
+    if (blockIdx.x * blockDim.x >= job_count(job)) {
+        job_account(job);
+        return;
+    }
     for (int i = threadIdx.x; i < (int)(sizeof(DevScene) / 8); i += blockDim.x)
         reinterpret_cast<double*>(&s)[i] = reinterpret_cast<const double*>(scene)[i];
     __syncthreads();

@@ -274,17 +274,17 @@ __global__ void k_conflict_expand(uint32_t* __restrict__ queued, const uint8_t* 
 int launch_conflict_expand(uint32_t* queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
                            DevCounters* ctr, int iter, int max_iters, uint32_t* next_list, unsigned cap,
                            cudaStream_t s) {
-    k_conflict_expand<<<148 * 4, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap);
+    k_conflict_expand<<<148, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }
 
-__global__ void k_unroll_check(DevCounters* ctr, int parity) {
-    if (ctr->cf_count[parity] > 0) ctr->unroll_exhausted = 1;
+__global__ void k_unroll_check(DevCounters* ctr, int parity, int level) {
+    if (ctr->cf_count[parity] > 0) ctr->unroll_exhausted |= 1u << level;
 }
 
-int launch_unroll_check(DevCounters* ctr, int parity, cudaStream_t s) {
-    k_unroll_check<<<1, 1, 0, s>>>(ctr, parity);
+int launch_unroll_check(DevCounters* ctr, int parity, int level, cudaStream_t s) {
+    k_unroll_check<<<1, 1, 0, s>>>(ctr, parity, level);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }

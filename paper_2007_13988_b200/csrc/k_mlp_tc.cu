@@ -228,6 +228,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool texture = P.tiles_b > 0;
     const EvalJob& job = P.job;
+    {
+        // empty work list (e.g. a converged conflict iteration): leave before any setup
+        const unsigned n0 = job_count(job);
+        if (blockIdx.x * NP >= n0) {
+            job_account(job);
+            return;
+        }
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRing; ++s) {

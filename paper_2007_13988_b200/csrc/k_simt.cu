@@ -176,6 +176,10 @@ __global__ void __launch_bounds__(NT, 1) k_pifu_simt_eval(FieldDev f, SimtMlp ge
     extern __shared__ __align__(16) uint8_t smem_raw[];
     SimtSmem& sm = *reinterpret_cast<SimtSmem*>(smem_raw);
     __shared__ DevScene scene;
+    if (blockIdx.x * TP >= job_count(job)) {
+        job_account(job);
+        return;
+    }
     for (int i = threadIdx.x; i < (int)(sizeof(DevScene) / 8); i += blockDim.x)
         reinterpret_cast<double*>(&scene)[i] = reinterpret_cast<const double*>(f.scene)[i];
     __syncthreads();
