@@ -19,7 +19,7 @@ __device__ __forceinline__ bool job_is_grid(const EvalJob& j) { return j.points 
 // grid.hpp:50-53 node_position, in double, same operation order.
 __device__ __forceinline__ void node_pos_d(uint32_t idx, int cells, double* p) {
     unsigned n = (unsigned)cells + 1u;
-    unsigned i = idx % n, j = (idx / n) % n, k = idx / (n * n);
+    unsigned jk = idx / n, i = idx - jk * n, k = jk / n, j = jk - k * n;
     double r = (double)cells;
     p[0] = __dadd_rn(-1.0, __ddiv_rn(2.0 * (double)i, r));
     p[1] = __dadd_rn(-1.0, __ddiv_rn(2.0 * (double)j, r));
@@ -30,7 +30,7 @@ __device__ __forceinline__ void node_pos_d(uint32_t idx, int cells, double* p) {
 // (2i/R with R a power of two <= 1024).
 __device__ __forceinline__ void node_pos_f(uint32_t idx, int cells, float* p) {
     unsigned n = (unsigned)cells + 1u;
-    unsigned i = idx % n, j = (idx / n) % n, k = idx / (n * n);
+    unsigned jk = idx / n, i = idx - jk * n, k = jk / n, j = jk - k * n;
     float r = (float)cells;
     p[0] = -1.0f + (2.0f * (float)i) / r;
     p[1] = -1.0f + (2.0f * (float)j) / r;

@@ -66,10 +66,15 @@ struct icg_context {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     // weights
     bool has_geo = false, has_tex = false;
-    DBuf geo_wt[5], geo_b[5], tex_wt[5], tex_b[5];
+    DBuf geo_wt[5], geo_b[5], tex_wt[5], tex_b[5], geo_wrow[5];
+    const float* geo_rows[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     SimtMlp geo_simt{}, tex_simt{};
     DBuf geo_stream, geo_bias, geo_wlast, tex_stream, tex_bias, tex_wlast;
     TcMlp geo_tc{}, tex_tc{};
+    DBuf geo_pair_stream;
+    alignas(64) unsigned char geo_pair_tmap[128] = {};
+    bool geo_pair = false;
+    bool use_pair = true;
     // field
     DBuf scene;
     DevScene* h_scene = nullptr;  // pinned staging
@@ -80,7 +85,8 @@ struct icg_context {
     DBuf list_e0, cf[2], nx[2];
     DBuf ctr;
     DevCounters* h_ctr = nullptr;  // pinned
-    DBuf binar, pts, outv;
+    DBuf binar, pts, outv, small_scratch;
+    unsigned small_max = 192;  // batches up to this size take the layer-parallel latency path
     // render
     DBuf depth, rgb, mask, surfk, spts, spx;
     // last extraction
@@ -247,15 +253,36 @@ int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
     return ICG_OK;
 }
 
-int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
+// `dependent_chain`: the batch is one link of the serial conflict loop, usually
+// small; it is routed on device between the tensor-core kernel and the
+// layer-parallel latency path by its size.
+int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points,
+             bool dependent_chain = false) {
     int slot = prof_begin(c, 0);
     int r;
-    if (fd.kind == ICG_FIELD_ANALYTIC)
+    if (fd.kind == ICG_FIELD_ANALYTIC) {
         r = launch_analytic_eval(fd, job, max_points, c->stream);
-    else if (fd.precision == ICG_PREC_FP32_SIMT)
+    } else if (fd.precision == ICG_PREC_FP32_SIMT) {
         r = launch_pifu_simt_eval(fd, c->geo_simt, job, max_points, c->stream);
-    else
+    } else if (dependent_chain && c->small_max > 0) {
+        if (int e = c->small_scratch.ensure(small_scratch_bytes(c->small_max))) return e;
+        EvalJob big = job;
+        big.min_count = c->small_max + 1;
+        if (c->geo_pair && c->use_pair)
+            r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap, big, max_points, fd.precision == ICG_PREC_FP32,
+                                      c->stream);
+        else
+            r = launch_pifu_tc_eval(fd, c->geo_tc, big, max_points, fd.precision == ICG_PREC_FP32, c->stream);
+        if (!r)
+            r = launch_small_mlp(fd, c->geo_simt, c->geo_rows, job, c->small_scratch.as<float>(), c->small_max,
+                                 c->small_max, c->stream);
+        c->launches += 1;
+    } else if (c->geo_pair && c->use_pair) {
+        r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap, job, max_points, fd.precision == ICG_PREC_FP32,
+                                  c->stream);
+    } else {
         r = launch_pifu_tc_eval(fd, c->geo_tc, job, max_points, fd.precision == ICG_PREC_FP32, c->stream);
+    }
     prof_end(c, slot);
     c->launches += 1;
     return r;
@@ -374,7 +401,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                 cj.evals = &ctr->evals[l];
                 cj.iters = &ctr->conflict_iters[l];
                 cj.overflow = &ctr->overflow;
-                if (int r = run_eval(c, fd, cj, (unsigned)nf)) return r;
+                if (int r = run_eval(c, fd, cj, (unsigned)nf, true)) return r;
             }
             if (int r = launch_unroll_check(ctr, unroll & 1, l, c->stream)) return r;
             c->launches += 1;
@@ -605,6 +632,8 @@ int icg_create(int device, icg_context** out) {
     }
     auto* c = new icg_context();
     c->device = device;
+    if (const char* e = getenv("ICG_NO_PAIR")) c->use_pair = !(e[0] == '1');
+    if (const char* e = getenv("ICG_SMALL_MAX")) c->small_max = (unsigned)atoi(e);
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->e0) != cudaSuccess || cudaEventCreate(&c->e1) != cudaSuccess ||
         cudaMallocHost(&c->h_scene, sizeof(DevScene)) != cudaSuccess ||
@@ -628,11 +657,12 @@ int icg_destroy(icg_context* c) {
     DBuf* all[] = {&c->geo_stream, &c->geo_bias, &c->geo_wlast, &c->tex_stream, &c->tex_bias, &c->tex_wlast,
                    &c->scene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
-                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv,
+                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->geo_pair_stream,
                    &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx};
     for (DBuf* b : all) b->release();
     for (int l = 0; l < 5; ++l) {
         c->geo_wt[l].release();
+        c->geo_wrow[l].release();
         c->geo_b[l].release();
         c->tex_wt[l].release();
         c->tex_b[l].release();
@@ -692,6 +722,11 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
         if (int r = bb[l].ensure((size_t)O * 4)) return r;
         ICG_CUDA_TRY(cudaMemcpy(wt[l].p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
         ICG_CUDA_TRY(cudaMemcpy(bb[l].p, d->biases[l], (size_t)O * 4, cudaMemcpyHostToDevice));
+        if (geo) {
+            if (int r = c->geo_wrow[l].ensure((size_t)O * K * 4)) return r;
+            ICG_CUDA_TRY(cudaMemcpy(c->geo_wrow[l].p, d->weights[l], (size_t)O * K * 4, cudaMemcpyHostToDevice));
+            c->geo_rows[l] = c->geo_wrow[l].as<float>();
+        }
         sm.wt[l] = wt[l].as<float>();
         sm.b[l] = bb[l].as<float>();
         sm.out[l] = O;
@@ -732,6 +767,17 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
             off += outs[l];
         }
         tc.valid = 1;
+    }
+    if (geo) {
+        size_t pb = pair_stream_bytes();
+        std::vector<uint8_t> ps(pb);
+        const float* ws[5];
+        for (int l = 0; l < 5; ++l) ws[l] = d->weights[l];
+        if (int r = pair_pack_geometry(ws, ps.data())) return r;
+        if (int r = c->geo_pair_stream.ensure(pb)) return r;
+        ICG_CUDA_TRY(cudaMemcpy(c->geo_pair_stream.p, ps.data(), pb, cudaMemcpyHostToDevice));
+        if (int r = pair_make_tmap(c->geo_pair_stream.p, pb, c->geo_pair_tmap)) return r;
+        c->geo_pair = true;
     }
     if (geo)
         c->has_geo = true;
@@ -853,10 +899,18 @@ static int eval_points(icg_context* c, const icg_field* field, const double* poi
     job.points = dpts;
     job.n_static = (unsigned)n;
     job.out = dout;
+    prof_discard(c);
     int r = texture ? run_texture(c, fd, job, (unsigned)n) : run_eval(c, fd, job, (unsigned)n);
     if (r) return r;
     if (mem == ICG_MEM_HOST) ICG_CUDA_TRY(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, c->stream));
     ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->prof_on) {
+        if (texture)
+            c->prof.tex_points += n;
+        else
+            c->prof.geo_points += n;
+        prof_collect(c);
+    }
     return ICG_OK;
 }
 

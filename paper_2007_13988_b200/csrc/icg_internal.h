@@ -107,6 +107,7 @@ struct EvalJob {
     unsigned long long* evals;    // += count (block 0)
     unsigned int* iters;          // += (count > 0) (block 0)
     unsigned int* overflow;
+    unsigned int min_count;       // tensor-core kernel: leave batches below this to the latency path
     // point epilogue
     float* out;                   // occupancy per point (or rgb x3 for texture)
     const uint32_t* out_pixel;    // texture: pixel index per point (out = rgb image)
@@ -131,6 +132,14 @@ int launch_pifu_tc_eval(const FieldDev& f, const TcMlp& geo, const EvalJob& job,
                         bool bf16x3, cudaStream_t s);
 int launch_pifu_tc_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const EvalJob& job,
                            unsigned int max_points, bool bf16x3, cudaStream_t s);
+size_t pair_stream_bytes();
+int pair_pack_geometry(const float* const* w, uint8_t* stream);
+int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out);
+int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
+                          unsigned max_points, bool x3, cudaStream_t s);
+size_t small_scratch_bytes(unsigned cap);
+int launch_small_mlp(const FieldDev& f, const SimtMlp& geo, const float* const* wrow, const EvalJob& job,
+                     float* scratch, unsigned cap, unsigned max_count, cudaStream_t s);
 int launch_fmap_chw_to_hwc(const float* chw, float* hwc, int C, int H, int W, cudaStream_t s);
 
 // grid kernels (k_grid.cu)

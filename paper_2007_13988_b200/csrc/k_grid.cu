@@ -39,19 +39,18 @@ __global__ void k_coarse_bits(const float* __restrict__ cv, size_t n, uint32_t* 
 // ---- coarse cells with mixed binarised corners (refined-cell set) ---------
 __global__ void k_mixed_cells(const uint32_t* __restrict__ cbin, int rc, uint32_t* __restrict__ mixed,
                               unsigned long long* refined) {
-    size_t ncell = (size_t)rc * rc * rc;
-    size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned ncell = (unsigned)rc * rc * rc;
+    const unsigned idx = blockIdx.x * blockDim.x + threadIdx.x;
     bool m = false;
     if (idx < ncell) {
-        int ci = (int)(idx % rc);
-        int cj = (int)((idx / rc) % rc);
-        int ck = (int)(idx / ((size_t)rc * rc));
-        size_t cn = (size_t)rc + 1;
-        size_t base = (size_t)ci + cn * ((size_t)cj + cn * (size_t)ck);
+        const unsigned jk = idx / (unsigned)rc;
+        const unsigned ci = idx - jk * rc, ck = jk / (unsigned)rc, cj = jk - ck * rc;
+        const unsigned cn = rc + 1u;
+        const unsigned base = ci + cn * (cj + cn * ck);
         int ones = 0;
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
-            size_t o = base + (d & 1) + cn * (((d >> 1) & 1) + cn * (d >> 2));
+            unsigned o = base + (d & 1) + cn * (((d >> 1) & 1) + cn * (d >> 2));
             ones += test_bit(cbin, o);
         }
         m = ones != 0 && ones != 8;
@@ -82,20 +81,21 @@ k_fine_classify(const float* __restrict__ cv, const uint8_t* __restrict__ cs, co
                 const uint32_t* __restrict__ mixed, int rc, float* __restrict__ fv, uint8_t* __restrict__ fs,
                 uint32_t* __restrict__ tentbin, uint32_t* __restrict__ sel, uint32_t* __restrict__ block_counts) {
     __shared__ unsigned warp_counts[kClassifyBlock / 32];
-    const int fn = 2 * rc + 1, cn = rc + 1;
-    const size_t nf = (size_t)fn * fn * fn;
-    size_t idx = (size_t)blockIdx.x * kClassifyBlock + threadIdx.x;
+    const unsigned fn = 2u * rc + 1u, cn = rc + 1u;
+    const unsigned nf = fn * fn * fn;
+    const unsigned idx = blockIdx.x * kClassifyBlock + threadIdx.x;
     bool tb = false, s = false;
     if (idx < nf) {
-        int i = (int)(idx % fn);
-        int j = (int)((idx / fn) % fn);
-        int k = (int)(idx / ((size_t)fn * fn));
+        const unsigned jk = idx / fn;
+        int i = (int)(idx - jk * fn);
+        int k = (int)(jk / fn);
+        int j = (int)(jk - (unsigned)k * fn);
         int i0 = i >> 1, i1 = (i + 1) >> 1, j0 = j >> 1, j1 = (j + 1) >> 1, k0 = k >> 1, k1 = (k + 1) >> 1;
         float v;
         uint8_t st;
         if (i0 == i1 && j0 == j1 && k0 == k1) {
             // even node: carry the coarse scalar and state (carry_scalars, localize.hpp:116-119)
-            size_t ci = (size_t)i0 + (size_t)cn * ((size_t)j0 + (size_t)cn * (size_t)k0);
+            unsigned ci = (unsigned)i0 + cn * ((unsigned)j0 + cn * (unsigned)k0);
             v = cv[ci];
             st = cs[ci];
             tb = test_bit(cbin, ci);
@@ -105,7 +105,7 @@ k_fine_classify(const float* __restrict__ cv, const uint8_t* __restrict__ cs, co
             for (int kk = k0; kk <= k1; ++kk)
                 for (int jj = j0; jj <= j1; ++jj)
                     for (int ii = i0; ii <= i1; ++ii) {
-                        ones += test_bit(cbin, (size_t)ii + (size_t)cn * ((size_t)jj + (size_t)cn * (size_t)kk));
+                        ones += test_bit(cbin, (unsigned)ii + cn * ((unsigned)jj + cn * (unsigned)kk));
                         ++cnt;
                     }
             v = (float)ones / (float)cnt;  // exact dyadic; equals (float)(double sum / cnt)
@@ -123,7 +123,7 @@ k_fine_classify(const float* __restrict__ cv, const uint8_t* __restrict__ cs, co
         for (int cz = zl; cz <= zh && !flagged; ++cz)
             for (int cy = yl; cy <= yh && !flagged; ++cy)
                 for (int cx = xl; cx <= xh && !flagged; ++cx)
-                    flagged = test_bit(mixed, (size_t)cx + (size_t)rc * ((size_t)cy + (size_t)rc * (size_t)cz));
+                    flagged = test_bit(mixed, (unsigned)cx + (unsigned)rc * ((unsigned)cy + (unsigned)rc * (unsigned)cz));
         s = flagged && st != ICG_STATE_EVALUATED;  // mask_to_unevaluated_list, localize.hpp:127
     }
     unsigned tbw = __ballot_sync(0xffffffffu, tb);
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kClassifyBlock)
 k_write_list(const uint32_t* __restrict__ sel, size_t nf, const uint32_t* __restrict__ offsets,
              uint32_t* __restrict__ list) {
     __shared__ unsigned warp_off[kClassifyBlock / 32];
-    size_t idx = (size_t)blockIdx.x * kClassifyBlock + threadIdx.x;
+    const size_t idx = (size_t)blockIdx.x * kClassifyBlock + threadIdx.x;
     int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned w = idx < nf ? sel[idx >> 5] : 0u;
     if (idx >= nf) w = 0u;

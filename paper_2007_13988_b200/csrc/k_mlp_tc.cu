@@ -24,6 +24,8 @@
 // owns TMEM), 2..5 = gather + epilogue (128 threads, TMEM lanes 0..127).
 #include <cuda_bf16.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <vector>
@@ -35,10 +37,8 @@ namespace icg {
 
 namespace tc {
 
-constexpr int kRing = 3;                    // weight ring stages
 constexpr uint32_t kTileHalf = 16384;       // one 128 x 64 bf16 tile
 constexpr uint32_t kTileBytes = 2 * kTileHalf;  // hi + lo in the packed stream
-constexpr int kThreads = 192;
 
 // ---------------------------------------------------------------------------
 // The weight-tile schedule.  The packer (host) and the MMA issuer (device)
@@ -146,33 +146,40 @@ int tc_pack_mlp(int which, const float* const* w, const float* const* b, uint8_t
 // ===========================================================================
 namespace tc {
 
+constexpr int kStages = 4;          // weight ring: 4 x 16 KB (one bf16 128x64 tile each)
+constexpr int kEpiWarps = 8;        // gather + epilogue: two warps per TMEM lane quarter
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreadsV2 = 64 + kEpiThreads;
+
 template <int NP>
 struct Smem {
-    // skip operand: KS chunks of [NP rows x 64 bf16], hi block then lo block
-    // (geometry uses 4 chunks, texture 8); h operand: 2 chunks, hi then lo.
+    // skip operand: KS chunks of [NP rows x 64 bf16] (K-major, SW128), hi block
+    // then lo block (geometry 4 chunks, texture 8).  h operand: two buffers of
+    // 2 chunks (hi, lo) so the epilogue of chunk c+1 overlaps the MMAs of c.
     static constexpr uint32_t kChunk = NP * 128;
     static constexpr int kSkipChunks = NP == 64 ? 4 : 8;
     static constexpr uint32_t kSkipHalf = kSkipChunks * kChunk;
     static constexpr uint32_t kHHalf = 2 * kChunk;
+    static constexpr uint32_t kHBuf = 2 * kHHalf;
     static constexpr uint32_t kOffSkip = 0;
     static constexpr uint32_t kOffH = kOffSkip + 2 * kSkipHalf;
-    static constexpr uint32_t kOffRing = kOffH + 2 * kHHalf;
-    static constexpr uint32_t kOffMisc = kOffRing + kRing * kTileBytes;
-    static constexpr uint32_t kTotal = kOffMisc + 10240 + 1024;  // + misc + alignment slack
+    static constexpr uint32_t kOffRing = kOffH + 2 * kHBuf;
+    static constexpr uint32_t kOffMisc = kOffRing + kStages * kTileHalf;
+    static constexpr uint32_t kMisc = 16384;
+    static constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;  // + alignment slack
 };
 
 struct Misc {
-    uint64_t full[kRing], empty[kRing];
-    uint64_t f_ready, h_ready, h_free, l1done[2], d2done, d3done, d4done;
+    uint64_t full[kStages], empty[kStages];
+    uint64_t f_ready, h_ready[2], h_free[2], l1done[2], d2done, d3done, d4done;
     uint32_t tmem_base;
     float z[64];
     float pos[64][3];
     double posd[64][3];
-    float red[4][3][64];  // cross-warp partial sums of the final layer
-    float skipdot[4][3][64];
+    float red[4][3][64];      // final layer: per-quarter partial sums over features
+    float skipdot[8][3][64];  // final layer: skip-input partial dots
 };
-
-static_assert(sizeof(Misc) + 16 <= 10240, "misc smem area too small");
+static_assert(sizeof(Misc) + 16 <= Smem<64>::kMisc, "misc smem area too small");
 
 struct Params {
     FieldDev f;
@@ -186,7 +193,15 @@ struct Params {
     const float* wlast;        // final layer of the network being evaluated
     float slope;
     int x3;                    // bf16x3 split products
+    unsigned long long* trace; // optional per-role wait accounting (CTA 0), see ICG_TC_TRACE
+    int exp;                   // debug experiments: 1 = skip MMAs, 2 = skip weight loads
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -214,13 +229,24 @@ __device__ __forceinline__ float warp_transpose_reduce(float* v) {
     return v[0];
 }
 
+template <int NC>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t* r) {
+    if constexpr (NC == 32)
+        ptx::tmem_ld32(taddr, r);
+    else
+        ptx::tmem_ld16(taddr, r);
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
+
 template <int NP>
-__global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
+__global__ void __launch_bounds__(kThreadsV2, 1) k_mlp_tc(Params P) {
     using S = Smem<NP>;
+    constexpr int NC = NP / 2;  // point columns per epilogue warp
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* skip = smem + S::kOffSkip;
-    uint8_t* hbuf = smem + S::kOffH;
+    uint8_t* hbase = smem + S::kOffH;
     uint8_t* ring = smem + S::kOffRing;
     Misc& ms = *reinterpret_cast<Misc*>(smem + S::kOffMisc);
     __shared__ DevScene scene;
@@ -231,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
     {
         // empty work list (e.g. a converged conflict iteration): leave before any setup
         const unsigned n0 = job_count(job);
+        if (n0 < job.min_count) return;  // small batch: the latency path (k_small.cu) evaluates it
         if (blockIdx.x * NP >= n0) {
             job_account(job);
             return;
@@ -238,15 +265,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
     }
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kRing; ++s) {
+        for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&ms.full[s], 1);
             ptx::mbar_init(&ms.empty[s], 1);
         }
-        ptx::mbar_init(&ms.f_ready, 128);
-        ptx::mbar_init(&ms.h_ready, 128);
-        ptx::mbar_init(&ms.h_free, 1);
-        ptx::mbar_init(&ms.l1done[0], 1);
-        ptx::mbar_init(&ms.l1done[1], 1);
+        ptx::mbar_init(&ms.f_ready, kEpiThreads);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&ms.h_ready[b], kEpiThreads);
+            ptx::mbar_init(&ms.h_free[b], 1);
+            ptx::mbar_init(&ms.l1done[b], 1);
+        }
         ptx::mbar_init(&ms.d2done, 1);
         ptx::mbar_init(&ms.d3done, 1);
         ptx::mbar_init(&ms.d4done, 1);
@@ -264,26 +292,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
 
     const unsigned n = job_count(job);
     const unsigned ntiles = (n + NP - 1) / NP;
-    const uint32_t tile_bytes = P.x3 ? kTileBytes : kTileHalf;
 
     if (warp == 0) {
-        // ===================== weight producer =====================
+        // ===================== weight producer (bulk copies, 16 KB stages) =====================
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
+            const int halves = P.x3 ? 2 : 1;
             for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 for (int seg = 0; seg < 2; ++seg) {
                     const uint8_t* src = seg ? P.stream_b : P.stream_a;
-                    int cnt = seg ? P.tiles_b : P.tiles_a;
-                    for (int i = 0; i < cnt; ++i) {
-                        ptx::mbar_wait(&ms.empty[s], ph ^ 1);
-                        ptx::mbar_arrive_expect_tx(&ms.full[s], tile_bytes);
-                        ptx::bulk_g2s(ring + s * kTileBytes, src + (size_t)i * kTileBytes, tile_bytes, &ms.full[s]);
-                        if (++s == kRing) {
-                            s = 0;
-                            ph ^= 1;
+                    const int cnt = seg ? P.tiles_b : P.tiles_a;
+                    for (int i = 0; i < cnt; ++i)
+                        for (int h = 0; h < halves; ++h) {
+                            ptx::mbar_wait(&ms.empty[s], ph ^ 1);
+                            if (P.exp & 2) {
+                                ptx::mbar_arrive(&ms.full[s]);
+                            } else {
+                                ptx::mbar_arrive_expect_tx(&ms.full[s], kTileHalf);
+                                ptx::bulk_g2s(ring + s * kTileHalf, src + (size_t)i * kTileBytes + h * kTileHalf,
+                                              kTileHalf, &ms.full[s]);
+                            }
+                            if (++s == kStages) {
+                                s = 0;
+                                ph ^= 1;
+                            }
                         }
-                    }
                 }
             }
         }
@@ -292,37 +326,67 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
         if (lane == 0) {
             const uint32_t idesc = ptx::idesc_bf16_f32(128, NP);
             int s = 0;
-            uint32_t ph = 0, fph = 0, hrph = 0;
+            uint32_t ph = 0, fph = 0, hr_ph[2] = {0, 0};
+            int eh = 0;  // h-event counter
             const uint32_t skip_hi = ptx::smem_u32(skip), skip_lo = skip_hi + S::kSkipHalf;
-            const uint32_t h_hi = ptx::smem_u32(hbuf), h_lo = h_hi + S::kHHalf;
+            const uint32_t h0 = ptx::smem_u32(hbase);
             const uint32_t ring0 = ptx::smem_u32(ring);
-            // TMEM columns: D2[m] = m*NP, BUF[b] = 4NP + b*NP (D3[m] reuses BUF), D4 = 6NP
-            auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc) {
-                ptx::mbar_wait(&ms.full[s], ph);
-                ptx::tc_fence_after();
-                const uint32_t a_hi = ring0 + s * kTileBytes, a_lo = a_hi + kTileHalf;
-                const uint64_t ad_hi = ptx::sdesc_sw128(a_hi), ad_lo = ptx::sdesc_sw128(a_lo);
-                const uint64_t bd_hi = ptx::sdesc_sw128(b_hi), bd_lo = ptx::sdesc_sw128(b_lo);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t koff = (uint64_t)(kk * 2);  // +32 bytes per K=16 step
-                    const uint32_t en = (acc || kk > 0) ? 1u : 0u;
-                    ptx::mma_bf16(tmem + dcol, ad_hi + koff, bd_hi + koff, idesc, en);
-                    if (P.x3) {
-                        ptx::mma_bf16(tmem + dcol, ad_hi + koff, bd_lo + koff, idesc, 1u);
-                        ptx::mma_bf16(tmem + dcol, ad_lo + koff, bd_hi + koff, idesc, 1u);
-                    }
+            unsigned long long w_full = 0, w_h = 0, w_f = 0, t_begin = gtime();
+            const bool tr = P.trace && blockIdx.x == 0;
+            auto twait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
+                if (tr) {
+                    unsigned long long t0 = gtime();
+                    ptx::mbar_wait(bar, par);
+                    acc += gtime() - t0;
+                } else {
+                    ptx::mbar_wait(bar, par);
                 }
-                ptx::mma_commit(&ms.empty[s]);
-                if (++s == kRing) {
+            };
+            auto next_stage = [&]() {
+                if (++s == kStages) {
                     s = 0;
                     ph ^= 1;
                 }
             };
-            auto wait_h = [&]() {
-                ptx::mbar_wait(&ms.h_ready, hrph);
-                hrph ^= 1;
+            // TMEM columns: D2[m] = m*NP, BUF[b] = 4NP + b*NP (D3[m] reuses BUF), D4 = 6NP
+            auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc) {
+                const uint64_t bd_hi = ptx::sdesc_sw128(b_hi), bd_lo = ptx::sdesc_sw128(b_lo);
+                twait(&ms.full[s], ph, w_full);
                 ptx::tc_fence_after();
+                const uint64_t ad_hi = ptx::sdesc_sw128(ring0 + s * kTileHalf);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    if (P.exp & 1) break;
+                    const uint64_t koff = (uint64_t)(kk * 2);  // +32 bytes per K=16 step
+                    ptx::mma_bf16(tmem + dcol, ad_hi + koff, bd_hi + koff, idesc, (acc || kk > 0) ? 1u : 0u);
+                    if (P.x3) ptx::mma_bf16(tmem + dcol, ad_hi + koff, bd_lo + koff, idesc, 1u);
+                }
+                ptx::mma_commit(&ms.empty[s]);
+                next_stage();
+                if (P.x3) {
+                    twait(&ms.full[s], ph, w_full);
+                    ptx::tc_fence_after();
+                    const uint64_t ad_lo = ptx::sdesc_sw128(ring0 + s * kTileHalf);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        if (P.exp & 1) break;
+                        const uint64_t koff = (uint64_t)(kk * 2);
+                        ptx::mma_bf16(tmem + dcol, ad_lo + koff, bd_hi + koff, idesc, 1u);
+                    }
+                    ptx::mma_commit(&ms.empty[s]);
+                    next_stage();
+                }
+            };
+            auto wait_h = [&]() -> int {
+                const int b = eh & 1;
+                twait(&ms.h_ready[b], hr_ph[b], w_h);
+                hr_ph[b] ^= 1;
+                ptx::tc_fence_after();
+                return b;
+            };
+            auto done_h = [&](int b) {
+                ptx::mma_commit(&ms.h_free[b]);
+                ++eh;
             };
             // one MLP body: layers 1-3 (+4); skip chunks [0, ks)
             auto body = [&](int ks, bool with_l4) {
@@ -337,11 +401,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
                     for (int j = 0; j < ks; ++j)
                         item(m * NP, skip_hi + j * S::kChunk, skip_lo + j * S::kChunk, j > 0);
                 for (int c = 0; c < 8; ++c) {
-                    wait_h();
+                    const int b = wait_h();
+                    const uint32_t hh = h0 + b * S::kHBuf, hl = hh + S::kHHalf;
                     for (int m = 0; m < 4; ++m)
-                        for (int jj = 0; jj < 2; ++jj)
-                            item(m * NP, h_hi + jj * S::kChunk, h_lo + jj * S::kChunk, true);
-                    ptx::mma_commit(&ms.h_free);
+                        for (int jj = 0; jj < 2; ++jj) item(m * NP, hh + jj * S::kChunk, hl + jj * S::kChunk, true);
+                    done_h(b);
                     if (c + 2 < 8) L1(c + 2);
                 }
                 ptx::mma_commit(&ms.d2done);
@@ -349,33 +413,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
                     for (int j = 0; j < ks; ++j)
                         item(4 * NP + m * NP, skip_hi + j * S::kChunk, skip_lo + j * S::kChunk, j > 0);
                 for (int c = 0; c < 4; ++c) {
-                    wait_h();
+                    const int b = wait_h();
+                    const uint32_t hh = h0 + b * S::kHBuf, hl = hh + S::kHHalf;
                     for (int m = 0; m < 2; ++m)
                         for (int jj = 0; jj < 2; ++jj)
-                            item(4 * NP + m * NP, h_hi + jj * S::kChunk, h_lo + jj * S::kChunk, true);
-                    ptx::mma_commit(&ms.h_free);
+                            item(4 * NP + m * NP, hh + jj * S::kChunk, hl + jj * S::kChunk, true);
+                    done_h(b);
                 }
                 ptx::mma_commit(&ms.d3done);
                 if (with_l4) {
                     for (int j = 0; j < ks; ++j)
                         item(6 * NP, skip_hi + j * S::kChunk, skip_lo + j * S::kChunk, j > 0);
                     for (int c = 0; c < 2; ++c) {
-                        wait_h();
-                        for (int jj = 0; jj < 2; ++jj)
-                            item(6 * NP, h_hi + jj * S::kChunk, h_lo + jj * S::kChunk, true);
-                        ptx::mma_commit(&ms.h_free);
+                        const int b = wait_h();
+                        const uint32_t hh = h0 + b * S::kHBuf, hl = hh + S::kHHalf;
+                        for (int jj = 0; jj < 2; ++jj) item(6 * NP, hh + jj * S::kChunk, hl + jj * S::kChunk, true);
+                        done_h(b);
                     }
                     ptx::mma_commit(&ms.d4done);
                 } else {
                     // prefix mode: h3 goes into skip chunks 4..7 (two events, nothing to consume)
-                    for (int c = 0; c < 2; ++c) {
-                        wait_h();
-                        ptx::mma_commit(&ms.h_free);
-                    }
+                    for (int c = 0; c < 2; ++c) done_h(wait_h());
                 }
             };
             for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                ptx::mbar_wait(&ms.f_ready, fph);
+                twait(&ms.f_ready, fph, w_f);
                 fph ^= 1;
                 ptx::tc_fence_after();
                 if (texture) {
@@ -385,100 +447,116 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
                     body(4, true);
                 }
             }
+            if (tr) {
+                P.trace[0] = gtime() - t_begin;
+                P.trace[1] = w_full;
+                P.trace[2] = w_h;
+                P.trace[3] = w_f;
+            }
         }
     } else {
-        // ===================== gather + epilogue (128 threads) =====================
-        const int et = threadIdx.x - 64;                 // 0..127
-        const int quarter = warp & 3;                    // TMEM lane quarter of this warp
-        const int row = quarter * 32 + lane;             // TMEM lane = output feature within the block
-        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-        uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hfph = 1;
+        // ===================== gather + epilogue (8 warps) =====================
+        const int et = threadIdx.x - 64;              // 0..255
+        const int quarter = warp & 3;                 // TMEM lane quarter of this warp
+        const int colh = (warp - 2) >> 2;             // which half of the point columns
+        const int col0 = colh * NC;
+        const int row = quarter * 32 + lane;          // TMEM lane = output feature within the block
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)col0;
+        uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hf_ph[2] = {1, 1};
+        int ee = 0;  // h-event counter (matches the MMA issuer's)
+        const bool tr = P.trace && blockIdx.x == 0 && threadIdx.x == 64;
+        unsigned long long e_acc = 0, e_hfree = 0, e_gather = 0, e_emit = 0, e_final = 0, e_begin = gtime();
+        auto ewait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc) {
+            if (tr) {
+                unsigned long long t0 = gtime();
+                ptx::mbar_wait(bar, par);
+                acc += gtime() - t0;
+            } else {
+                ptx::mbar_wait(bar, par);
+            }
+        };
         const FieldDev& f = P.f;
+        const bool odd = lane & 1;
+        const uint32_t kk = (uint32_t)(row & 63) & ~1u;
+        const uint32_t rchunk = (uint32_t)(row >> 6) * S::kChunk;
 
-        // write one 128-feature activation chunk (this thread = feature `row`)
-        // from TMEM columns [col, col+NP) to an operand region `dst` (2 chunks of
-        // 64 features, hi block then lo block at +lo_off).
+        // one 128-feature activation chunk: this thread = feature `row`, points
+        // [col0, col0+NC) from TMEM column `col`, into operand region `dst`.
         auto emit_chunk = [&](uint32_t col, const float* bias_blk, int out_dim, int feat0, uint8_t* dst,
                               uint32_t lo_off, bool write_lo) {
             const int o = feat0 + row;
             const float bo = __ldg(&bias_blk[o]);
             const float wz = __ldg(&bias_blk[out_dim + o]);
-            const uint32_t chunk = (uint32_t)(row >> 6) * S::kChunk;
-            const uint32_t kk = (uint32_t)(row & 63) & ~1u;
+            uint32_t r[NC];
+            tmem_ld<NC>(lane_base + col, r);
+            ptx::tmem_ld_wait();
 #pragma unroll
-            for (int half = 0; half < NP / 32; ++half) {
-                uint32_t r[32];
-                ptx::tmem_ld32(lane_base + col + half * 32, r);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int q = 0; q < 32; q += 2) {
-                    const int p = half * 32 + q;
-                    float v0 = __uint_as_float(r[q]) + bo + wz * ms.z[p];
-                    float v1 = __uint_as_float(r[q + 1]) + bo + wz * ms.z[p + 1];
-                    v0 = v0 < 0.0f ? v0 * P.slope : v0;
-                    v1 = v1 < 0.0f ? v1 * P.slope : v1;
-                    // even lane: (p, feats row,row+1); odd lane: (p+1, feats row-1,row)
-                    const bool odd = lane & 1;
-                    float send = odd ? v0 : v1;
-                    float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-                    float a = odd ? recv : v0;   // feature kk   at point pp
-                    float b = odd ? v1 : recv;   // feature kk+1 at point pp
-                    const uint32_t pp = (uint32_t)(p + (odd ? 1 : 0));
-                    __nv_bfloat16 ah = __float2bfloat16_rn(a), bh = __float2bfloat16_rn(b);
-                    const uint32_t off = chunk + sw128(pp, kk);
-                    __nv_bfloat162 hv;
-                    hv.x = ah;
-                    hv.y = bh;
-                    *reinterpret_cast<__nv_bfloat162*>(dst + off) = hv;
-                    if (write_lo) {
-                        *reinterpret_cast<uint32_t*>(dst + lo_off + off) =
-                            pack_bf16(a - __bfloat162float(ah), b - __bfloat162float(bh));
-                    }
+            for (int q = 0; q < NC; q += 2) {
+                const int p = col0 + q;
+                float v0 = __uint_as_float(r[q]) + fmaf(wz, ms.z[p], bo);
+                float v1 = __uint_as_float(r[q + 1]) + fmaf(wz, ms.z[p + 1], bo);
+                v0 = v0 < 0.0f ? v0 * P.slope : v0;
+                v1 = v1 < 0.0f ? v1 * P.slope : v1;
+                // even lane writes (p, feats kk,kk+1); odd lane writes (p+1, feats kk,kk+1)
+                const float send = odd ? v0 : v1;
+                const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+                const float a = odd ? recv : v0;
+                const float b = odd ? v1 : recv;
+                const uint32_t off = rchunk + sw128((uint32_t)(p + (odd ? 1 : 0)), kk);
+                const uint32_t hv = pack_bf16(a, b);
+                *reinterpret_cast<uint32_t*>(dst + off) = hv;
+                if (write_lo) {
+                    const float ah = __uint_as_float(hv << 16), bh = __uint_as_float(hv & 0xFFFF0000u);
+                    *reinterpret_cast<uint32_t*>(dst + lo_off + off) = pack_bf16(a - ah, b - bh);
                 }
             }
         };
 
-        auto h_write_begin = [&]() {
-            ptx::mbar_wait(&ms.h_free, hfph);
-            hfph ^= 1;
+        auto h_begin = [&]() -> int {
+            const int b = ee & 1;
+            ewait(&ms.h_free[b], hf_ph[b], e_hfree);
+            hf_ph[b] ^= 1;
+            return b;
         };
-        auto h_write_end = [&]() {
+        auto h_end = [&](int b) {
             ptx::fence_proxy_async_smem();
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&ms.h_ready);
+            ptx::mbar_arrive(&ms.h_ready[b]);
+            ++ee;
         };
 
-        // epilogue of one body; returns after D3 (prefix) or D4 has been consumed
+        // epilogue of one body; returns after D3 (prefix) or before D4
         auto body_epi = [&](const float* bias, bool prefix) {
             const float* b1 = bias;
             const float* b2 = b1 + 2 * 1024;
             const float* b3 = b2 + 2 * 512;
             for (int c = 0; c < 8; ++c) {
-                ptx::mbar_wait(&ms.l1done[c & 1], l1ph[c & 1]);
+                ewait(&ms.l1done[c & 1], l1ph[c & 1], e_acc);
                 l1ph[c & 1] ^= 1;
                 ptx::tc_fence_after();
-                h_write_begin();
-                emit_chunk(4 * NP + (c & 1) * NP, b1, 1024, c * 128, hbuf, S::kHHalf, P.x3);
-                h_write_end();
+                const int b = h_begin();
+                uint8_t* hb = hbase + b * S::kHBuf;
+                emit_chunk(4 * NP + (c & 1) * NP, b1, 1024, c * 128, hb, S::kHHalf, P.x3);
+                h_end(b);
             }
-            ptx::mbar_wait(&ms.d2done, d2ph);
+            ewait(&ms.d2done, d2ph, e_acc);
             d2ph ^= 1;
             ptx::tc_fence_after();
             for (int m = 0; m < 4; ++m) {
-                h_write_begin();
-                emit_chunk(m * NP, b2, 512, m * 128, hbuf, S::kHHalf, P.x3);
-                h_write_end();
+                const int b = h_begin();
+                emit_chunk(m * NP, b2, 512, m * 128, hbase + b * S::kHBuf, S::kHHalf, P.x3);
+                h_end(b);
             }
-            ptx::mbar_wait(&ms.d3done, d3ph);
+            ewait(&ms.d3done, d3ph, e_acc);
             d3ph ^= 1;
             ptx::tc_fence_after();
             for (int m = 0; m < 2; ++m) {
-                h_write_begin();
+                const int b = h_begin();
                 if (prefix)  // h3 -> skip chunks 4 + 2m, 5 + 2m
                     emit_chunk(4 * NP + m * NP, b3, 256, m * 128, skip + (4 + 2 * m) * S::kChunk, S::kSkipHalf, true);
                 else
-                    emit_chunk(4 * NP + m * NP, b3, 256, m * 128, hbuf, S::kHHalf, P.x3);
-                h_write_end();
+                    emit_chunk(4 * NP + m * NP, b3, 256, m * 128, hbase + b * S::kHBuf, S::kHHalf, P.x3);
+                h_end(b);
             }
         };
 
@@ -486,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
             const unsigned base = t * NP;
             // ---- positions ----
             if (et < NP) {
-                unsigned idx = base + et;
+                const unsigned idx = base + et;
                 double pd[3] = {0.0, 0.0, 0.0};
                 if (idx < n) job_point_d(job, idx, pd);
                 for (int d = 0; d < 3; ++d) {
@@ -495,42 +573,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
                 }
                 ms.z[et] = (float)pd[2];
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            // ---- gather Phi into the skip operand (hi/lo), 2 channels per thread ----
+            epi_bar();
+            // ---- gather Phi into the skip operand (hi/lo): 2 channels x NP/2 points per thread ----
+            unsigned long long tg0 = tr ? gtime() : 0;
             {
-                const int c0 = 2 * et;  // channels c0, c0+1
+                const int c0 = 2 * (et & 127);
+                const int p0 = (et >> 7) * (NP / 2);
                 const uint32_t chunk = (uint32_t)(c0 >> 6) * S::kChunk;
-                const uint32_t kk = (uint32_t)(c0 & 63);
+                const uint32_t ck = (uint32_t)(c0 & 63);
                 const size_t rowW = (size_t)f.W * f.C;
 #pragma unroll 4
-                for (int p = 0; p < NP; ++p) {
+                for (int p = p0; p < p0 + NP / 2; ++p) {
                     float u = (ms.pos[p][0] + 1.0f) * 0.5f * (float)(f.W - 1);
                     float v = (1.0f - ms.pos[p][1]) * 0.5f * (float)(f.H - 1);
                     u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
                     v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
-                    int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
-                    float ax = u - (float)x0, ay = v - (float)y0;
+                    const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
+                    const float ax = u - (float)x0, ay = v - (float)y0;
                     const float* m00 = f.fmap_hwc + ((size_t)y0 * f.W + x0) * (size_t)f.C + c0;
-                    float2 t00 = __ldg(reinterpret_cast<const float2*>(m00));
-                    float2 t10 = __ldg(reinterpret_cast<const float2*>(m00 + f.C));
-                    float2 t01 = __ldg(reinterpret_cast<const float2*>(m00 + rowW));
-                    float2 t11 = __ldg(reinterpret_cast<const float2*>(m00 + rowW + f.C));
-                    float w00 = (1.0f - ax) * (1.0f - ay), w10 = ax * (1.0f - ay), w01 = (1.0f - ax) * ay,
-                          w11 = ax * ay;
-                    float a = w00 * t00.x + w10 * t10.x + w01 * t01.x + w11 * t11.x;
-                    float b = w00 * t00.y + w10 * t10.y + w01 * t01.y + w11 * t11.y;
-                    __nv_bfloat16 ah = __float2bfloat16_rn(a), bh = __float2bfloat16_rn(b);
-                    const uint32_t off = chunk + sw128((uint32_t)p, kk);
-                    __nv_bfloat162 hv;
-                    hv.x = ah;
-                    hv.y = bh;
-                    *reinterpret_cast<__nv_bfloat162*>(skip + off) = hv;
-                    *reinterpret_cast<uint32_t*>(skip + S::kSkipHalf + off) =
-                        pack_bf16(a - __bfloat162float(ah), b - __bfloat162float(bh));
+                    const float2 t00 = __ldg(reinterpret_cast<const float2*>(m00));
+                    const float2 t10 = __ldg(reinterpret_cast<const float2*>(m00 + f.C));
+                    const float2 t01 = __ldg(reinterpret_cast<const float2*>(m00 + rowW));
+                    const float2 t11 = __ldg(reinterpret_cast<const float2*>(m00 + rowW + f.C));
+                    const float w00 = (1.0f - ax) * (1.0f - ay), w10 = ax * (1.0f - ay), w01 = (1.0f - ax) * ay,
+                                w11 = ax * ay;
+                    const float a = w00 * t00.x + w10 * t10.x + w01 * t01.x + w11 * t11.x;
+                    const float b = w00 * t00.y + w10 * t10.y + w01 * t01.y + w11 * t11.y;
+                    const uint32_t off = chunk + sw128((uint32_t)p, ck);
+                    const uint32_t hv = pack_bf16(a, b);
+                    *reinterpret_cast<uint32_t*>(skip + off) = hv;
+                    const float ah = __uint_as_float(hv << 16), bh = __uint_as_float(hv & 0xFFFF0000u);
+                    *reinterpret_cast<uint32_t*>(skip + S::kSkipHalf + off) = pack_bf16(a - ah, b - bh);
                 }
             }
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(&ms.f_ready);
+            if (tr) e_gather += gtime() - tg0;
 
             if (texture) body_epi(P.bias_g, true);
             const float* bias = texture ? P.bias_t : P.bias_g;
@@ -542,37 +620,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
             const int skipdim = texture ? kTexSkip : kGeoSkip;
             const float* b4 = bias + 2 * (1024 + 512 + 256);
             const float* b5 = b4 + 2 * 128;
-            ptx::mbar_wait(&ms.d4done, d4ph);
+            ewait(&ms.d4done, d4ph, e_acc);
+            unsigned long long tf0 = tr ? gtime() : 0;
             d4ph ^= 1;
             ptx::tc_fence_after();
             {
                 const float bo = __ldg(&b4[row]), wz = __ldg(&b4[128 + row]);
-                float w5[3];
-                for (int c = 0; c < nout; ++c) w5[c] = __ldg(&P.wlast[(size_t)c * (K4 + skipdim) + row]);
+                uint32_t r[NC];
+                tmem_ld<NC>(lane_base + 6 * NP, r);
+                ptx::tmem_ld_wait();
+                float h[NC];
 #pragma unroll
-                for (int half = 0; half < NP / 32; ++half) {
-                    uint32_t r[32];
-                    ptx::tmem_ld32(lane_base + 6 * NP + half * 32, r);
-                    ptx::tmem_ld_wait();
-                    float h[32];
+                for (int q = 0; q < NC; ++q) {
+                    float v = __uint_as_float(r[q]) + fmaf(wz, ms.z[col0 + q], bo);
+                    h[q] = v < 0.0f ? v * P.slope : v;
+                }
+                for (int c = 0; c < nout; ++c) {
+                    const float w5 = __ldg(&P.wlast[(size_t)c * (K4 + skipdim) + row]);
+                    float v[32];
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        float v = __uint_as_float(r[q]) + bo + wz * ms.z[half * 32 + q];
-                        h[q] = v < 0.0f ? v * P.slope : v;
-                    }
-                    for (int c = 0; c < nout; ++c) {
-                        float v[32];
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) v[q] = w5[c] * h[q];
-                        float s = warp_transpose_reduce(v);  // lane l: point half*32 + l
-                        ms.red[quarter][c][half * 32 + lane] = s;
-                    }
+                    for (int q = 0; q < 32; ++q) v[q] = q < NC ? w5 * h[q] : 0.0f;
+                    const float sum = warp_transpose_reduce(v);  // lane l: point col0 + l
+                    if (lane < NC) ms.red[quarter][c][col0 + lane] = sum;
                 }
             }
             ptx::tc_fence_before();
-            // skip part of the final layer: sum_j w5s[j] * skip[p][j] (+ z term)
+            // skip part of the final layer: sum_j w5s[j] * skip[p][j] (the z term is added below)
             {
-                const int split = 128 / NP;  // threads per point
+                constexpr int split = kEpiThreads / NP;  // threads per point
                 const int p = et / split, part = et % split;
                 const int nch = (texture ? 512 : 256) / split;
                 for (int c = 0; c < nout; ++c) {
@@ -580,21 +655,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
                     float acc = 0.0f;
                     for (int j = part * nch; j < (part + 1) * nch; j += 2) {
                         const uint32_t off = (uint32_t)(j >> 6) * S::kChunk + sw128((uint32_t)p, (uint32_t)(j & 63));
-                        __nv_bfloat162 hv = *reinterpret_cast<const __nv_bfloat162*>(skip + off);
-                        __nv_bfloat162 lv = *reinterpret_cast<const __nv_bfloat162*>(skip + S::kSkipHalf + off);
-                        float x0 = __bfloat162float(hv.x) + __bfloat162float(lv.x);
-                        float x1 = __bfloat162float(hv.y) + __bfloat162float(lv.y);
+                        const uint32_t hv = *reinterpret_cast<const uint32_t*>(skip + off);
+                        const uint32_t lv = *reinterpret_cast<const uint32_t*>(skip + S::kSkipHalf + off);
+                        const float x0 = __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
+                        const float x1 = __uint_as_float(hv & 0xFFFF0000u) + __uint_as_float(lv & 0xFFFF0000u);
                         acc = fmaf(__ldg(&ws[j]), x0, acc);
                         acc = fmaf(__ldg(&ws[j + 1]), x1, acc);
                     }
                     ms.skipdot[part][c][p] = acc;
                 }
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            epi_bar();
             if (et < NP * nout) {
+                constexpr int split = kEpiThreads / NP;
                 const int p = et % NP, c = et / NP;
                 const unsigned idx = base + p;
-                const int split = 128 / NP;
                 float s = ms.red[0][c][p] + ms.red[1][c][p] + ms.red[2][c][p] + ms.red[3][c][p];
                 for (int q = 0; q < split; ++q) s += ms.skipdot[q][c][p];
                 const float* ws = P.wlast + (size_t)c * (K4 + skipdim) + K4;
@@ -609,9 +684,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
                             job.out[(size_t)idx * 3 + c] = v;
                         }
                     } else {
-                        double sdf = scene_sdf(scene, ms.posd[p]);
-                        float logit = s + (float)(-scene.sdf_scale * sdf);
-                        float v = 1.0f / (1.0f + expf(-logit));
+                        const double sdf = scene_sdf(scene, ms.posd[p]);
+                        const float logit = s + (float)(-scene.sdf_scale * sdf);
+                        const float v = 1.0f / (1.0f + expf(-logit));
                         if (job_is_grid(job))
                             grid_epilogue(job, job_node(job, idx), v);
                         else
@@ -619,7 +694,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
                     }
                 }
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            epi_bar();
+            if (tr) e_final += gtime() - tf0;
+        }
+        if (tr) {
+            P.trace[4] = gtime() - e_begin;
+            P.trace[5] = e_acc;
+            P.trace[6] = e_hfree;
+            P.trace[7] = e_gather;
+            P.trace[8] = e_final;
+            P.trace[9] = ntiles;
         }
     }
     ptx::tc_fence_before();
@@ -632,8 +716,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(Params P) {
 
 }  // namespace tc
 
+static unsigned long long* trace_buffer() {
+    static unsigned long long* buf = nullptr;
+    static int enabled = -1;
+    if (enabled < 0) {
+        const char* e = getenv("ICG_TC_TRACE");
+        enabled = e && e[0] == '1';
+        if (enabled) cudaMallocManaged(&buf, 64 * sizeof(unsigned long long));
+    }
+    return enabled ? buf : nullptr;
+}
+
 template <int NP>
-static int launch_tc(const tc::Params& p, unsigned max_points, cudaStream_t s) {
+static int launch_tc(tc::Params p, unsigned max_points, cudaStream_t s) {
+    p.trace = trace_buffer();
+    {
+        const char* e = getenv("ICG_TC_EXP");
+        p.exp = e ? atoi(e) : 0;
+    }
+    if (p.trace) cudaMemsetAsync(p.trace, 0, 64 * sizeof(unsigned long long), s);
     static bool attr = false;
     const uint32_t smem = tc::Smem<NP>::kTotal;
     if (!attr) {
@@ -643,8 +744,17 @@ static int launch_tc(const tc::Params& p, unsigned max_points, cudaStream_t s) {
     unsigned blocks = (max_points + NP - 1) / NP;
     if (blocks > 148) blocks = 148;
     if (blocks == 0) blocks = 1;
-    tc::k_mlp_tc<NP><<<blocks, tc::kThreads, smem, s>>>(p);
+    tc::k_mlp_tc<NP><<<blocks, tc::kThreadsV2, smem, s>>>(p);
     ICG_CUDA_TRY(cudaGetLastError());
+    if (p.trace) {
+        cudaStreamSynchronize(s);
+        const unsigned long long* t = p.trace;
+        fprintf(stderr,
+                "[tc-trace NP=%d] mma: total %.1f us, wait data %.1f, wait h %.1f, wait f %.1f | epi: total %.1f us, "
+                "wait acc %.1f, wait hfree %.1f, gather %.1f, final %.1f | tiles(cta0) %llu\n",
+                NP, t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3, t[6] * 1e-3,
+                t[7] * 1e-3, t[8] * 1e-3, t[9]);
+    }
     return ICG_OK;
 }
 
