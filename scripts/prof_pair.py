@@ -1,0 +1,12 @@
+"""Two warm-up batches, then one 300k-point geometry batch (pair kernel) for ncu --set full."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2007_13988_b200 import abi, api
+caps = api.gen_capsules(42); fmap = api.gen_feature_map(1000)
+gw, gb = api.gen_mlp(7, 0); tw, tb = api.gen_mlp(8, 1)
+ctx = api.Context(0); ctx.set_mlp(0, gw, gb); ctx.set_mlp(1, tw, tb)
+f = api.PifuField(fmap, caps, 50.0, abi.ICG_PREC_FP32)
+pts = np.random.default_rng(0).uniform(-1, 1, (300000, 3))
+for _ in range(3): ctx.occupancy_batch(f, pts)
+print("ok")
