@@ -86,7 +86,7 @@ struct icg_context {
     DBuf ctr;
     DevCounters* h_ctr = nullptr;  // pinned
     DBuf binar, pts, outv, small_scratch;
-    unsigned small_max = 192;  // batches up to this size take the layer-parallel latency path
+    unsigned small_max = 96;  // batches up to this size take the layer-parallel latency path
     // render
     DBuf depth, rgb, mask, surfk, spts, spx;
     // last extraction

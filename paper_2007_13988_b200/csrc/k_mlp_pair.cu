@@ -76,13 +76,14 @@ constexpr int kItems = 16 + 8 + 32 + 4 + 8 + 4 + 4;  // 76
 
 struct Misc {
     uint64_t full[kStages], empty[kStages];
-    uint64_t f_ready, h_ready, h_free, l1done[2], d2done, d3done, d4done, sd_ready;
+    uint64_t f_ready, h_ready, h_free, l1done[2], d2done, d3done, d4done, sd_ready[2];
     uint32_t tmem_base;
     float z[NP];
     float pos[NP][3];
     double posd[NP][3];
     float red[4][NP];
-    float skipdot[4][NP];
+    float skipdot[2][NP];  // final-layer skip-input dot per point, double-buffered by tile parity
+    float cterm[NP];       // b5 + w5z * z - sdf_scale * sdf(P), per point (leader)
 };
 static_assert(sizeof(Misc) + 16 <= kMisc, "misc smem too small");
 
@@ -164,7 +165,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::mbar_init(&ms.d2done, 1);
         ptx::mbar_init(&ms.d3done, 1);
         ptx::mbar_init(&ms.d4done, 1);
-        ptx::mbar_init(&ms.sd_ready, kEpiThreads);
+        ptx::mbar_init(&ms.sd_ready[0], 64);
+        ptx::mbar_init(&ms.sd_ready[1], 64);
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap);
@@ -181,7 +183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t full0 = ptx::mapa(ptx::smem_u32(&ms.full[0]), 0);
     const uint32_t f_ready0 = ptx::mapa(ptx::smem_u32(&ms.f_ready), 0);
     const uint32_t h_ready0 = ptx::mapa(ptx::smem_u32(&ms.h_ready), 0);
-    const uint32_t sd_ready0 = ptx::mapa(ptx::smem_u32(&ms.sd_ready), 0);
+    const uint32_t sd_ready0 = ptx::mapa(ptx::smem_u32(&ms.sd_ready[0]), 0);
     const uint16_t both = 0x3;
 
     if (warp == 0) {
@@ -317,7 +319,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int colh = (warp - 2) >> 2;  // point half this warp converts = destination CTA
         const int row = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(colh * 64);
-        uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hfph = 1, sdph = 0;
+        uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hfph = 1, sdph[2] = {0, 0};
+        unsigned tile_iter = 0;
         const FieldDev& f = P.f;
         const bool odd = lane & 1;
         // this thread's feature inside a 256-row block, and its K position in the next layer's operand
@@ -385,6 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (unsigned t = pair_id; t < ntiles; t += npairs) {
             const unsigned base = t * NP;
             // ---- positions of all 128 points (every CTA needs z for its epilogue) ----
+            const int tp = (int)(tile_iter & 1u);
             if (et < NP) {
                 const unsigned idx = base + et;
                 double pd[3] = {0.0, 0.0, 0.0};
@@ -394,39 +398,88 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     ms.pos[et][d] = (float)pd[d];
                 }
                 ms.z[et] = (float)pd[2];
+                if (leader)  // constant part of the final logit: b5 + w5z*z - sdf_scale*sdf(P) (fp64 SDF)
+                    ms.cterm[et] = __ldg(&b5[0]) + __ldg(&P.wlast[128 + kGeoSkip - 1]) * (float)pd[2] +
+                                   (float)(-scene.sdf_scale * scene_sdf(scene, pd));
             }
             epi_bar();
             // ---- gather Phi for this CTA's 64 points into its skip operand ----
+            // warp per point (8 points per warp, 2 in flight); lane = 8 consecutive
+            // channels = one 16-byte SW128 chunk of the bf16 operand; the same pass
+            // computes the final layer's skip-input dot product in fp32.
             unsigned long long tg = tr ? gtime() : 0;
             {
-                const int c0 = 2 * (et & 127);
-                const int p0 = (et >> 7) * 32;
+                const int ew = et >> 5;
+                const int c0 = 8 * lane;
                 const uint32_t chunk = (uint32_t)(c0 >> 6) * kChunk;
-                const uint32_t ck = (uint32_t)(c0 & 63);
+                const uint32_t c16 = (uint32_t)((c0 & 63) >> 3);
                 const size_t rowW = (size_t)f.W * f.C;
-#pragma unroll 4
-                for (int pl = p0; pl < p0 + 32; ++pl) {
-                    const int p = (int)rank * 64 + pl;
-                    float u = (ms.pos[p][0] + 1.0f) * 0.5f * (float)(f.W - 1);
-                    float v = (1.0f - ms.pos[p][1]) * 0.5f * (float)(f.H - 1);
-                    u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
-                    v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
-                    const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
-                    const float ax = u - (float)x0, ay = v - (float)y0;
-                    const float* m00 = f.fmap_hwc + ((size_t)y0 * f.W + x0) * (size_t)f.C + c0;
-                    const float2 t00 = __ldg(reinterpret_cast<const float2*>(m00));
-                    const float2 t10 = __ldg(reinterpret_cast<const float2*>(m00 + f.C));
-                    const float2 t01 = __ldg(reinterpret_cast<const float2*>(m00 + rowW));
-                    const float2 t11 = __ldg(reinterpret_cast<const float2*>(m00 + rowW + f.C));
-                    const float w00 = (1.0f - ax) * (1.0f - ay), w10 = ax * (1.0f - ay), w01 = (1.0f - ax) * ay,
-                                w11 = ax * ay;
-                    const float a = w00 * t00.x + w10 * t10.x + w01 * t01.x + w11 * t11.x;
-                    const float b = w00 * t00.y + w10 * t10.y + w01 * t01.y + w11 * t11.y;
-                    const uint32_t off = chunk + sw128((uint32_t)pl, ck);
-                    const uint32_t hv = pack_bf16(a, b);
-                    *reinterpret_cast<uint32_t*>(skip + off) = hv;
-                    const float ah = __uint_as_float(hv << 16), bh = __uint_as_float(hv & 0xFFFF0000u);
-                    *reinterpret_cast<uint32_t*>(skip + kSkipHalf + off) = pack_bf16(a - ah, b - bh);
+                float w5s[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w5s[i] = __ldg(&P.wlast[128 + c0 + i]);
+                for (int it = 0; it < 4; ++it) {
+                    float4 t[2][8];
+                    float wts[2][4];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int p = (int)rank * 64 + ew * 8 + it * 2 + j;
+                        float u = (ms.pos[p][0] + 1.0f) * 0.5f * (float)(f.W - 1);
+                        float v = (1.0f - ms.pos[p][1]) * 0.5f * (float)(f.H - 1);
+                        u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
+                        v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
+                        const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
+                        const float ax = u - (float)x0, ay = v - (float)y0;
+                        wts[j][0] = (1.0f - ax) * (1.0f - ay);
+                        wts[j][1] = ax * (1.0f - ay);
+                        wts[j][2] = (1.0f - ax) * ay;
+                        wts[j][3] = ax * ay;
+                        const float* m00 = f.fmap_hwc + ((size_t)y0 * f.W + x0) * (size_t)f.C + c0;
+                        const float* taps[4] = {m00, m00 + f.C, m00 + rowW, m00 + rowW + f.C};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            t[j][2 * q] = __ldg(reinterpret_cast<const float4*>(taps[q]));
+                            t[j][2 * q + 1] = __ldg(reinterpret_cast<const float4*>(taps[q] + 4));
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int pl = ew * 8 + it * 2 + j;
+                        float val[8];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const float4 a0 = t[j][h], a1 = t[j][2 + h], a2 = t[j][4 + h], a3 = t[j][6 + h];
+                            val[4 * h + 0] = wts[j][0] * a0.x + wts[j][1] * a1.x + wts[j][2] * a2.x + wts[j][3] * a3.x;
+                            val[4 * h + 1] = wts[j][0] * a0.y + wts[j][1] * a1.y + wts[j][2] * a2.y + wts[j][3] * a3.y;
+                            val[4 * h + 2] = wts[j][0] * a0.z + wts[j][1] * a1.z + wts[j][2] * a2.z + wts[j][3] * a3.z;
+                            val[4 * h + 3] = wts[j][0] * a0.w + wts[j][1] * a1.w + wts[j][2] * a2.w + wts[j][3] * a3.w;
+                        }
+                        uint4 hv, lv;
+                        uint32_t* hp = reinterpret_cast<uint32_t*>(&hv);
+                        uint32_t* lp = reinterpret_cast<uint32_t*>(&lv);
+                        float dot = 0.0f;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float a = val[2 * i], b = val[2 * i + 1];
+                            hp[i] = pack_bf16(a, b);
+                            lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                            dot = fmaf(w5s[2 * i], a, dot);
+                            dot = fmaf(w5s[2 * i + 1], b, dot);
+                        }
+                        const uint32_t off = chunk + (uint32_t)pl * 128u + (((c16 ^ (uint32_t)pl) & 7u) << 4);
+                        *reinterpret_cast<uint4*>(skip + off) = hv;
+                        *reinterpret_cast<uint4*>(skip + kSkipHalf + off) = lv;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                        if (lane == 0) {
+                            const int p = (int)rank * 64 + pl;
+                            if (leader) {
+                                ms.skipdot[tp][p] = dot;
+                            } else {
+                                ptx::st_cluster_f32(ptx::mapa(ptx::smem_u32(&ms.skipdot[tp][p]), 0), dot);
+                                ptx::mbar_arrive_cluster(sd_ready0 + 8 * tp);
+                            }
+                        }
+                    }
                 }
             }
             ptx::fence_proxy_async_cluster();
@@ -481,42 +534,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::tc_fence_before();
-            // skip-input part of the final layer for this CTA's own 64 points
-            {
-                const int pl = et >> 2, part = et & 3;
-                const float* ws = P.wlast + 128;
-                float acc = 0.0f;
-                for (int j = part * 64; j < part * 64 + 64; j += 2) {
-                    const uint32_t off = (uint32_t)(j >> 6) * kChunk + sw128((uint32_t)pl, (uint32_t)(j & 63));
-                    const uint32_t hv = *reinterpret_cast<const uint32_t*>(skip + off);
-                    const uint32_t lv = *reinterpret_cast<const uint32_t*>(skip + kSkipHalf + off);
-                    const float x0 = __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
-                    const float x1 = __uint_as_float(hv & 0xFFFF0000u) + __uint_as_float(lv & 0xFFFF0000u);
-                    acc = fmaf(__ldg(&ws[j]), x0, acc);
-                    acc = fmaf(__ldg(&ws[j + 1]), x1, acc);
-                }
-                const int p = (int)rank * 64 + pl;
-                if (leader) {
-                    ms.skipdot[part][p] = acc;
-                } else {
-                    ptx::st_cluster_f32(ptx::mapa(ptx::smem_u32(&ms.skipdot[part][p]), 0), acc);
-                    ptx::mbar_arrive_cluster(sd_ready0);
-                }
-            }
             epi_bar();
             if (leader) {
-                ptx::mbar_wait_cluster(&ms.sd_ready, sdph);
-                sdph ^= 1;
+                ptx::mbar_wait_cluster(&ms.sd_ready[tp], sdph[tp]);
+                sdph[tp] ^= 1;
                 if (et < NP) {
                     const int p = et;
                     const unsigned idx = base + p;
-                    float s = ms.red[0][p] + ms.red[1][p] + ms.red[2][p] + ms.red[3][p];
-                    s += ms.skipdot[0][p] + ms.skipdot[1][p] + ms.skipdot[2][p] + ms.skipdot[3][p];
-                    s += __ldg(&P.wlast[128 + kGeoSkip - 1]) * ms.z[p] + __ldg(&b5[0]);
+                    const float s = ms.red[0][p] + ms.red[1][p] + ms.red[2][p] + ms.red[3][p] + ms.skipdot[tp][p] +
+                                    ms.cterm[p];
                     if (idx < n) {
-                        const double sdf = scene_sdf(scene, ms.posd[p]);
-                        const float logit = s + (float)(-scene.sdf_scale * sdf);
-                        const float vv = 1.0f / (1.0f + expf(-logit));
+                        const float vv = 1.0f / (1.0f + expf(-s));
                         if (job_is_grid(job))
                             grid_epilogue(job, job_node(job, idx), vv);
                         else
@@ -526,6 +554,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             epi_bar();
             if (tr) e_fin += gtime() - tf;
+            ++tile_iter;
         }
         if (tr) {
             P.trace[4] = gtime() - e_begin;

@@ -11,6 +11,9 @@
 // them), so both can be enqueued without a host round-trip.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "eval_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -48,48 +51,64 @@ __device__ __forceinline__ void small_gather(const FieldDev& f, const EvalJob& j
     }
 }
 
-// hout[p][o] = act(b[o] + sum_k W[o][k] * [hin[p], skip[p]][k]); one warp per
-// (o, group of kPG points): lanes split K (lane-strided partial sums, then a
-// fixed xor-tree), so the dependent chain per lane is K/32 and the row-major
-// weight row is read coalesced.
+// hout[p][o] = act(b[o] + sum_k W[o][k] * [hin[p], skip[p]][k]).  One BLOCK
+// per (output o, group of kPG points): the 8 warps take contiguous K slices,
+// lanes stride inside a slice with every load issued before the FMAs, so a
+// layer costs ~one L2 round trip per item round; partial sums combine in
+// shared memory in a fixed order (deterministic, batch-independent).
+constexpr int kSliceMax = 8;  // per-lane elements per slice (K <= 8 warps * 32 lanes * 8)
+
 __device__ __forceinline__ void small_layer(const SimtMlp& m, const float* const* wrow, int l, const float* hin,
-                                            int hin_s, const float* skip, unsigned n, float* hout, int hout_s) {
+                                            int hin_s, const float* skip, unsigned n, float* hout, int hout_s,
+                                            float (*red)[kPG]) {
     const int O = m.out[l], Kh = l ? m.out[l - 1] : 0, Ks = m.skip, K = Kh + Ks;
     const float* __restrict__ W = wrow[l];
     const unsigned groups = (n + kPG - 1) / kPG;
     const unsigned items = groups * (unsigned)O;
-    const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    for (unsigned it = gw; it < items; it += nw) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = kSmallThreads / 32;
+    const int slice = (K + nwarps - 1) / nwarps;
+    const int k0 = warp * slice, k1 = min(K, k0 + slice);
+    for (unsigned it = blockIdx.x; it < items; it += gridDim.x) {
         const int o = (int)(it % (unsigned)O);
         const unsigned p0 = (it / (unsigned)O) * kPG;
         const float* wr = W + (size_t)o * K;
+        float w[kSliceMax], x[kSliceMax][kPG];
+#pragma unroll
+        for (int u = 0; u < kSliceMax; ++u) {
+            const int k = k0 + lane + 32 * u;
+            const bool ok = k < k1;
+            w[u] = ok ? __ldg(&wr[k]) : 0.0f;
+#pragma unroll
+            for (int q = 0; q < kPG; ++q) {
+                const float* src = k < Kh ? hin + (size_t)(p0 + q) * hin_s + k : skip + (size_t)(p0 + q) * kSkipS + (k - Kh);
+                x[u][q] = ok ? *src : 0.0f;
+            }
+        }
         float acc[kPG];
 #pragma unroll
-        for (int q = 0; q < kPG; ++q) acc[q] = 0.0f;
-        for (int k = lane; k < Kh; k += 32) {
-            const float w = __ldg(&wr[k]);
+        for (int q = 0; q < kPG; ++q) {
+            float a = 0.0f;
 #pragma unroll
-            for (int q = 0; q < kPG; ++q) acc[q] = fmaf(w, hin[(size_t)(p0 + q) * hin_s + k], acc[q]);
-        }
-        for (int k = lane; k < Ks; k += 32) {
-            const float w = __ldg(&wr[Kh + k]);
-#pragma unroll
-            for (int q = 0; q < kPG; ++q) acc[q] = fmaf(w, skip[(size_t)(p0 + q) * kSkipS + k], acc[q]);
+            for (int u = 0; u < kSliceMax; ++u) a = fmaf(w[u], x[u][q], a);
+            acc[q] = a;
         }
 #pragma unroll
         for (int q = 0; q < kPG; ++q)
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], s);
-        if (lane < kPG && p0 + lane < n) {
-            float v = acc[0];
+        if (lane == 0)
 #pragma unroll
-            for (int q = 1; q < kPG; ++q)
-                if (lane == q) v = acc[q];
+            for (int q = 0; q < kPG; ++q) red[warp][q] = acc[q];
+        __syncthreads();
+        if (threadIdx.x < kPG && p0 + threadIdx.x < n) {
+            float v = 0.0f;
+            for (int w2 = 0; w2 < nwarps; ++w2) v += red[w2][threadIdx.x];
             v += __ldg(&m.b[l][o]);
             if (v < 0.0f) v *= m.slope;
-            hout[(size_t)(p0 + lane) * hout_s + o] = v;
+            hout[(size_t)(p0 + threadIdx.x) * hout_s + o] = v;
         }
+        __syncthreads();
     }
 }
 
@@ -97,8 +116,15 @@ struct RowWeights {
     const float* w[5];  // row-major [out][in] fp32 copies of the geometry MLP
 };
 
+__device__ __forceinline__ unsigned long long sg_time() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kSmallThreads) k_small_mlp(FieldDev f, SimtMlp geo, RowWeights rw, EvalJob job,
-                                                             float* scratch, unsigned cap, unsigned max_count) {
+                                                             float* scratch, unsigned cap, unsigned max_count,
+                                                             unsigned long long* trace) {
     const unsigned n = job_count(job);
     if (n == 0 || n > max_count || n > cap) return;  // grid-uniform decision
     cg::grid_group grid = cg::this_grid();
@@ -108,16 +134,25 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_mlp(FieldDev f, SimtMlp
     float* hA = skip + (size_t)capr * kSkipS;
     float* hB = hA + (size_t)capr * 1024;
     double* pos = reinterpret_cast<double*>(hB + (size_t)capr * 512);
+    __shared__ float red[kSmallThreads / 32][kPG];
+    const bool tr = trace && blockIdx.x == 0 && threadIdx.x == 0;
+    int ti = 0;
+    if (tr) trace[ti++] = sg_time();
     small_gather(f, job, n, skip, pos);
     grid.sync();
-    small_layer(geo, rw.w, 0, nullptr, 0, skip, n, hA, 1024);
+    if (tr) trace[ti++] = sg_time();
+    small_layer(geo, rw.w, 0, nullptr, 0, skip, n, hA, 1024, red);
     grid.sync();
-    small_layer(geo, rw.w, 1, hA, 1024, skip, n, hB, 512);
+    if (tr) trace[ti++] = sg_time();
+    small_layer(geo, rw.w, 1, hA, 1024, skip, n, hB, 512, red);
     grid.sync();
-    small_layer(geo, rw.w, 2, hB, 512, skip, n, hA, 1024);
+    if (tr) trace[ti++] = sg_time();
+    small_layer(geo, rw.w, 2, hB, 512, skip, n, hA, 1024, red);
     grid.sync();
-    small_layer(geo, rw.w, 3, hA, 1024, skip, n, hB, 512);
+    if (tr) trace[ti++] = sg_time();
+    small_layer(geo, rw.w, 3, hA, 1024, skip, n, hB, 512, red);
     grid.sync();
+    if (tr) trace[ti++] = sg_time();
     // final 385 -> 1 layer: one warp per point, lanes split K, fixed reduction order
     const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -141,6 +176,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_mlp(FieldDev f, SimtMlp
                 job.out[p] = v;
         }
     }
+    if (tr) {
+        trace[ti++] = sg_time();
+        trace[15] = n;
+    }
 }
 
 size_t small_scratch_bytes(unsigned cap) {
@@ -156,7 +195,9 @@ int launch_small_mlp(const FieldDev& f, const SimtMlp& geo, const float* const* 
         ICG_CUDA_TRY(cudaGetDevice(&dev));
         ICG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         ICG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small_mlp, kSmallThreads, 0));
-        grid = sms * (per_sm < 4 ? per_sm : 4);
+        const char* g = getenv("ICG_SMALL_BPS");
+        const int bps = g ? atoi(g) : 4;
+        grid = sms * (per_sm < bps ? per_sm : bps);
         if (grid <= 0) grid = sms;
     }
     FieldDev fa = f;
@@ -164,8 +205,24 @@ int launch_small_mlp(const FieldDev& f, const SimtMlp& geo, const float* const* 
     RowWeights rw;
     for (int l = 0; l < 5; ++l) rw.w[l] = wrow[l];
     EvalJob ja = job;
-    void* args[] = {&fa, &ga, &rw, &ja, &scratch, &cap, &max_count};
+    static unsigned long long* trace = nullptr;
+    static int tron = -1;
+    if (tron < 0) {
+        const char* e = getenv("ICG_TC_TRACE");
+        tron = e && e[0] == '1';
+        if (tron) cudaMallocManaged(&trace, 16 * sizeof(unsigned long long));
+    }
+    unsigned long long* tp = tron ? trace : nullptr;
+    if (tp) cudaMemsetAsync(tp, 0, 16 * 8, s);
+    void* args[] = {&fa, &ga, &rw, &ja, &scratch, &cap, &max_count, &tp};
     ICG_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_small_mlp, grid, kSmallThreads, args, 0, s));
+    if (tp) {
+        cudaStreamSynchronize(s);
+        if (tp[0])
+            fprintf(stderr, "[small-trace] n=%llu gather %.1f L1 %.1f L2 %.1f L3 %.1f L4 %.1f final %.1f us\n", tp[15],
+                    (tp[1] - tp[0]) * 1e-3, (tp[2] - tp[1]) * 1e-3, (tp[3] - tp[2]) * 1e-3, (tp[4] - tp[3]) * 1e-3,
+                    (tp[5] - tp[4]) * 1e-3, (tp[6] - tp[5]) * 1e-3);
+    }
     return ICG_OK;
 }
 
