@@ -71,9 +71,10 @@ struct icg_context {
     SimtMlp geo_simt{}, tex_simt{};
     DBuf geo_stream, geo_bias, geo_wlast, tex_stream, tex_bias, tex_wlast;
     TcMlp geo_tc{}, tex_tc{};
-    DBuf geo_pair_stream;
+    DBuf geo_pair_stream, tex_pair_stream;
     alignas(64) unsigned char geo_pair_tmap[128] = {};
-    bool geo_pair = false;
+    alignas(64) unsigned char tex_pair_tmap[128] = {};
+    bool geo_pair = false, tex_pair = false;
     bool use_pair = true;
     // field
     DBuf scene;
@@ -293,6 +294,9 @@ int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned
     int r;
     if (fd.precision == ICG_PREC_FP32_SIMT)
         r = launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
+    else if (c->geo_pair && c->tex_pair && c->use_pair)
+        r = launch_pifu_pair_texture(fd, c->geo_tc, c->tex_tc, c->geo_pair_tmap, c->tex_pair_tmap, job, max_points,
+                                     fd.precision == ICG_PREC_FP32, c->stream);
     else
         r = launch_pifu_tc_texture(fd, c->geo_tc, c->tex_tc, job, max_points, fd.precision == ICG_PREC_FP32,
                                    c->stream);
@@ -657,7 +661,7 @@ int icg_destroy(icg_context* c) {
     DBuf* all[] = {&c->geo_stream, &c->geo_bias, &c->geo_wlast, &c->tex_stream, &c->tex_bias, &c->tex_wlast,
                    &c->scene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
-                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->geo_pair_stream,
+                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->geo_pair_stream, &c->tex_pair_stream,
                    &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx};
     for (DBuf* b : all) b->release();
     for (int l = 0; l < 5; ++l) {
@@ -768,16 +772,18 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
         }
         tc.valid = 1;
     }
-    if (geo) {
-        size_t pb = pair_stream_bytes();
+    {
+        // CTA-pair operand stream (k_mlp_pair.cu) + its TMA descriptor
+        DBuf& ps_dev = geo ? c->geo_pair_stream : c->tex_pair_stream;
+        const size_t pb = pair_stream_bytes(d->which);
         std::vector<uint8_t> ps(pb);
         const float* ws[5];
         for (int l = 0; l < 5; ++l) ws[l] = d->weights[l];
-        if (int r = pair_pack_geometry(ws, ps.data())) return r;
-        if (int r = c->geo_pair_stream.ensure(pb)) return r;
-        ICG_CUDA_TRY(cudaMemcpy(c->geo_pair_stream.p, ps.data(), pb, cudaMemcpyHostToDevice));
-        if (int r = pair_make_tmap(c->geo_pair_stream.p, pb, c->geo_pair_tmap)) return r;
-        c->geo_pair = true;
+        if (int r = pair_pack(d->which, ws, ps.data())) return r;
+        if (int r = ps_dev.ensure(pb)) return r;
+        ICG_CUDA_TRY(cudaMemcpy(ps_dev.p, ps.data(), pb, cudaMemcpyHostToDevice));
+        if (int r = pair_make_tmap(ps_dev.p, pb, geo ? c->geo_pair_tmap : c->tex_pair_tmap)) return r;
+        (geo ? c->geo_pair : c->tex_pair) = true;
     }
     if (geo)
         c->has_geo = true;

@@ -132,11 +132,14 @@ int launch_pifu_tc_eval(const FieldDev& f, const TcMlp& geo, const EvalJob& job,
                         bool bf16x3, cudaStream_t s);
 int launch_pifu_tc_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const EvalJob& job,
                            unsigned int max_points, bool bf16x3, cudaStream_t s);
-size_t pair_stream_bytes();
-int pair_pack_geometry(const float* const* w, uint8_t* stream);
+size_t pair_stream_bytes(int which);
+int pair_pack(int which, const float* const* w, uint8_t* stream);
 int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out);
 int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
                           unsigned max_points, bool x3, cudaStream_t s);
+int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const void* tmap_geo,
+                             const void* tmap_tex, const EvalJob& job, unsigned max_points, bool x3,
+                             cudaStream_t s);
 size_t small_scratch_bytes(unsigned cap);
 int launch_small_mlp(const FieldDev& f, const SimtMlp& geo, const float* const* wrow, const EvalJob& job,
                      float* scratch, unsigned cap, unsigned max_count, cudaStream_t s);

@@ -1,13 +1,20 @@
-// k_mlp_pair.cu — the PIFu geometry field on CTA PAIRS (tcgen05 cta_group::2).
+// k_mlp_pair.cu — the PIFu geometry and texture fields on CTA PAIRS
+// (tcgen05 cta_group::2).
 //
 // Same fused "weights x activations^T" dataflow as k_mlp_tc.cu, but every MMA
-// is M=256 x N=128 x K=16 executed by two SMs of a TPC: each CTA of the
-// cluster holds 128 of the 256 weight rows (A) and 64 of the 128 points (B)
-// in its shared memory; its TMEM holds its 128 output rows for all 128
-// points.  Per SM this halves the shared-memory operand bytes per FLOP and
-// doubles the tensor work per pipeline stage relative to the single-CTA
-// 128x64 MMA (the single-CTA kernel measured ~25% tensor-pipe activity,
-// bound by per-stage overheads and SMEM operand traffic).
+// is M=256 x N x K=16 executed by the two SMs of a TPC: each CTA of the
+// cluster holds 128 of the 256 weight rows (A) and N/2 of the N points (B) in
+// its shared memory; its TMEM holds its 128 output rows for all N points.  Per
+// SM this halves the shared-memory operand bytes per FLOP and doubles the
+// tensor work per pipeline stage relative to the single-CTA 128xN MMA (the
+// single-CTA kernel measured ~25% tensor-pipe activity, bound by per-stage
+// overheads and SMEM operand traffic).
+//   geometry : N = 128 (64 points per CTA), 257->1024->512->256->128->1
+//   texture  : N = 64 (32 points per CTA; the 513-wide skip input is twice as
+//              large): the geometry prefix (layers 1-3) writes its layer-3
+//              activations h3 straight into the skip operand, then the texture
+//              body 513->1024->512->256->128->3 runs over [Phi, h3, z]
+//              (render.hpp:262-277 evaluates f_T at the surface points).
 //
 //   weights  : both CTAs' producers TMA (2-SM form) their 16 KB half-tile
 //              into their own ring; transaction bytes land on the leader's
@@ -18,8 +25,10 @@
 //              memory of the CTA that owns each point (DSMEM for the peer's).
 //   layer 1  : 4 chunks of 256 features streamed through TMEM into layer 2.
 //   final    : layer 4 is padded to 256 rows (peer half zero); CTA 0 reduces
-//              the 128 -> 1 output for all 128 points on CUDA cores, the peer
-//              contributes its points' skip-input dot products over DSMEM.
+//              the 128 -> 1 (3) outputs for all points on CUDA cores.  The
+//              skip-input part of the final layer is a fp32 dot computed where
+//              the data is produced (Phi during the gather, h3 once it is in
+//              the skip operand); the peer's arrive over DSMEM.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -35,63 +44,86 @@ namespace icg {
 
 namespace pair {
 
-constexpr uint32_t kHalf = 16384;                 // one 128 x 64 bf16 tile
-constexpr int kStages = 4;
+constexpr uint32_t kHalf = 16384;  // one 128 x 64 bf16 tile
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;
-constexpr int NP = 128;                           // points per pair tile (64 per CTA)
-constexpr uint32_t kChunk = 64 * 128;             // 64 point rows x 64 bf16 (SW128)
-constexpr uint32_t kSkipHalf = 4 * kChunk;        // Phi: 4 K-chunks
-constexpr uint32_t kHHalf = 4 * kChunk;           // one 256-feature block: 4 K-chunks
-constexpr uint32_t kOffSkip = 0;
-constexpr uint32_t kOffH = kOffSkip + 2 * kSkipHalf;   // 64 KB
-constexpr uint32_t kOffRing = kOffH + 2 * kHHalf;      // 128 KB
-constexpr uint32_t kOffMisc = kOffRing + kStages * kHalf;  // 192 KB
-constexpr uint32_t kMisc = 16384;
-constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
+constexpr int kMaxNP = 128;
+constexpr int kMaxStages = 6;
 
-// weight-item schedule (pairs): (layer, 256-row block, K column offset)
+template <bool TEX>
+struct Cfg {
+    static constexpr int NPC = TEX ? 32 : 64;        // points per CTA
+    static constexpr int NP = 2 * NPC;               // points per pair tile = MMA N
+    static constexpr int kSkipChunks = TEX ? 8 : 4;  // [Phi] or [Phi, h3] in 64-wide K-chunks
+    static constexpr int kStages = TEX ? 6 : 4;
+    static constexpr uint32_t kChunk = NPC * 128;  // NPC point rows x 64 bf16 (SW128)
+    static constexpr uint32_t kSkipHalf = kSkipChunks * kChunk;
+    static constexpr uint32_t kHHalf = 4 * kChunk;  // one 256-feature block
+    static constexpr uint32_t kOffSkip = 0;
+    static constexpr uint32_t kOffH = kOffSkip + 2 * kSkipHalf;
+    static constexpr uint32_t kOffRing = kOffH + 2 * kHHalf;
+    static constexpr uint32_t kOffMisc = kOffRing + kStages * kHalf;
+    static constexpr uint32_t kMisc = 16384;
+    static constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
+    static constexpr int kOut = TEX ? 3 : 1;
+    static constexpr int kSkipDim = TEX ? kTexSkip : kGeoSkip;
+    static_assert(kStages <= kMaxStages, "stages");
+};
+
+// weight-item schedule of one MLP body: (layer, 256-row block, K column offset).
+// ks = skip K-chunks (4 geometry, 8 texture); the geometry prefix of the texture
+// network is the same schedule without layer 4, i.e. the first items of the
+// geometry stream.
 template <class Emit>
-__host__ __device__ void schedule(Emit&& emit) {
+__host__ __device__ void schedule(int ks, bool with_l4, Emit&& emit) {
     auto L1 = [&](int c) {
-        for (int j = 0; j < 4; ++j) emit(0, c, j * 64);
+        for (int j = 0; j < ks; ++j) emit(0, c, j * 64);
     };
     L1(0);
     L1(1);
     for (int m = 0; m < 2; ++m)
-        for (int j = 0; j < 4; ++j) emit(1, m, 1024 + j * 64);
+        for (int j = 0; j < ks; ++j) emit(1, m, 1024 + j * 64);
     for (int c = 0; c < 4; ++c) {
         for (int m = 0; m < 2; ++m)
             for (int jj = 0; jj < 4; ++jj) emit(1, m, c * 256 + jj * 64);
         if (c + 2 < 4) L1(c + 2);
     }
-    for (int j = 0; j < 4; ++j) emit(2, 0, 512 + j * 64);
+    for (int j = 0; j < ks; ++j) emit(2, 0, 512 + j * 64);
     for (int c = 0; c < 2; ++c)
         for (int jj = 0; jj < 4; ++jj) emit(2, 0, c * 256 + jj * 64);
-    for (int j = 0; j < 4; ++j) emit(3, 0, 256 + j * 64);
-    for (int jj = 0; jj < 4; ++jj) emit(3, 0, jj * 64);
+    if (with_l4) {
+        for (int j = 0; j < ks; ++j) emit(3, 0, 256 + j * 64);
+        for (int jj = 0; jj < 4; ++jj) emit(3, 0, jj * 64);
+    }
 }
-constexpr int kItems = 16 + 8 + 32 + 4 + 8 + 4 + 4;  // 76
+__host__ __device__ constexpr int items(int ks, bool with_l4) {
+    return 4 * ks + 2 * ks + 32 + ks + 8 + (with_l4 ? ks + 4 : 0);
+}
+constexpr int kGeoItems = items(4, true);      // 76
+constexpr int kPrefixItems = items(4, false);  // 68
+constexpr int kTexItems = items(8, true);      // 108
 
 struct Misc {
-    uint64_t full[kStages], empty[kStages];
+    uint64_t full[kMaxStages], empty[kMaxStages];
     uint64_t f_ready, h_ready, h_free, l1done[2], d2done, d3done, d4done, sd_ready[2];
     uint32_t tmem_base;
-    float z[NP];
-    float pos[NP][3];
-    double posd[NP][3];
-    float red[4][NP];
-    float skipdot[2][NP];  // final-layer skip-input dot per point, double-buffered by tile parity
-    float cterm[NP];       // b5 + w5z * z - sdf_scale * sdf(P), per point (leader)
+    float z[kMaxNP];
+    float pos[kMaxNP][3];
+    float red[4][3][kMaxNP];      // final layer: per-lane-quarter partial sums over features
+    float skipdot[2][3][kMaxNP];  // final layer: skip-input dots (leader, all points), by tile parity
+    float sdl[3][kMaxNP / 2];     // texture: this CTA's Phi-part skip dots until h3 is known
+    float cterm[3][kMaxNP];       // b5 + w5z*z (- sdf_scale*sdf for geometry)
 };
-static_assert(sizeof(Misc) + 16 <= kMisc, "misc smem too small");
+static_assert(sizeof(Misc) + 16 <= Cfg<false>::kMisc, "misc smem too small");
 
 struct Params {
     FieldDev f;
     EvalJob job;
-    const float* bias;   // per layer [b, wz] blocks (same layout as the single-CTA stream)
-    const float* wlast;  // final layer [1][128 + 257]
+    const float* bias_g;  // geometry per-layer [b, wz] blocks (same layout as the single-CTA stream)
+    const float* bias_t;  // texture per-layer [b, wz] blocks
+    const float* wlast;   // final layer of the evaluated network, [out][128 + skip]
+    int items_a, items_b;
     float slope;
     int x3;
     unsigned long long* trace;
@@ -129,14 +161,18 @@ __device__ __forceinline__ float warp_transpose_reduce(float* v) {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
 
+template <bool TEX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k_mlp_pair(const __grid_constant__ CUtensorMap tmap, Params P) {
+    k_mlp_pair(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, Params P) {
+    using C = Cfg<TEX>;
+    constexpr int NPC = C::NPC, NP = C::NP, NOUT = C::kOut, kStages = C::kStages;
+    constexpr uint32_t kChunk = C::kChunk, kSkipHalf = C::kSkipHalf, kHHalf = C::kHHalf;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* skip = smem + kOffSkip;
-    uint8_t* hbuf = smem + kOffH;
-    uint8_t* ring = smem + kOffRing;
-    Misc& ms = *reinterpret_cast<Misc*>(smem + kOffMisc);
+    uint8_t* skip = smem + C::kOffSkip;
+    uint8_t* hbuf = smem + C::kOffH;
+    uint8_t* ring = smem + C::kOffRing;
+    Misc& ms = *reinterpret_cast<Misc*>(smem + C::kOffMisc);
     __shared__ DevScene scene;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -165,13 +201,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::mbar_init(&ms.d2done, 1);
         ptx::mbar_init(&ms.d3done, 1);
         ptx::mbar_init(&ms.d4done, 1);
-        ptx::mbar_init(&ms.sd_ready[0], 64);
-        ptx::mbar_init(&ms.sd_ready[1], 64);
+        ptx::mbar_init(&ms.sd_ready[0], NPC);
+        ptx::mbar_init(&ms.sd_ready[1], NPC);
         ptx::fence_mbar_init();
     }
-    if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap);
-    for (int i = threadIdx.x; i < (int)(sizeof(DevScene) / 8); i += blockDim.x)
-        reinterpret_cast<double*>(&scene)[i] = reinterpret_cast<const double*>(P.f.scene)[i];
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmapA);
+        if (TEX) ptx::prefetch_tmap(&tmapB);
+    }
+    if (!TEX)
+        for (int i = threadIdx.x; i < (int)(sizeof(DevScene) / 8); i += blockDim.x)
+            reinterpret_cast<double*>(&scene)[i] = reinterpret_cast<const double*>(P.f.scene)[i];
     if (warp == 1) ptx::tmem_alloc2<512>(&ms.tmem_base);
     ptx::tc_fence_before();
     ptx::cluster_sync();
@@ -194,17 +234,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int parts = P.x3 ? 2 : 1;
             const uint32_t ring0 = ptx::smem_u32(ring);
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
-                for (int i = 0; i < kItems; ++i)
-                    for (int part = 0; part < parts; ++part) {
-                        ptx::mbar_wait(&ms.empty[s], ph ^ 1);
-                        if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kHalf);
-                        const int row0 = ((i * 2 + (int)rank) * 2 + part) * 128;
-                        ptx::tma_load_2d_2sm(ring0 + s * kHalf, &tmap, full0 + s * 8, 0, row0);
-                        if (++s == kStages) {
-                            s = 0;
-                            ph ^= 1;
+                for (int seg = 0; seg < (TEX ? 2 : 1); ++seg) {
+                    const CUtensorMap* tm = seg ? &tmapB : &tmapA;
+                    const int cnt = seg ? P.items_b : P.items_a;
+                    for (int i = 0; i < cnt; ++i)
+                        for (int part = 0; part < parts; ++part) {
+                            ptx::mbar_wait(&ms.empty[s], ph ^ 1);
+                            if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kHalf);
+                            const int row0 = ((i * 2 + (int)rank) * 2 + part) * 128;
+                            ptx::tma_load_2d_2sm(ring0 + s * kHalf, tm, full0 + s * 8, 0, row0);
+                            if (++s == kStages) {
+                                s = 0;
+                                ph ^= 1;
+                            }
                         }
-                    }
+                }
             }
         }
     } else if (warp == 1) {
@@ -224,14 +268,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     ph ^= 1;
                 }
             };
+            auto wait_full = [&]() {
+                const unsigned long long t0 = tr ? gtime() : 0;
+                ptx::mbar_wait(&ms.full[s], ph);
+                if (tr) w_full += gtime() - t0;
+                ptx::tc_fence_after();
+            };
             auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc) {
                 const uint64_t bd_hi = ptx::sdesc_sw128(b_hi), bd_lo = ptx::sdesc_sw128(b_lo);
-                {
-                    unsigned long long t0 = tr ? gtime() : 0;
-                    ptx::mbar_wait(&ms.full[s], ph);
-                    if (tr) w_full += gtime() - t0;
-                }
-                ptx::tc_fence_after();
+                wait_full();
                 const uint64_t ad_hi = ptx::sdesc_sw128(ring0 + s * kHalf);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
@@ -242,12 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mma_commit_pair(&ms.empty[s], both);
                 next_stage();
                 if (P.x3) {
-                    {
-                        unsigned long long t0 = tr ? gtime() : 0;
-                        ptx::mbar_wait(&ms.full[s], ph);
-                        if (tr) w_full += gtime() - t0;
-                    }
-                    ptx::tc_fence_after();
+                    wait_full();
                     const uint64_t ad_lo = ptx::sdesc_sw128(ring0 + s * kHalf);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
@@ -259,7 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             };
             auto wait_h = [&]() {
-                unsigned long long t0 = tr ? gtime() : 0;
+                const unsigned long long t0 = tr ? gtime() : 0;
                 ptx::mbar_wait_cluster(&ms.h_ready, hph);
                 if (tr) w_h += gtime() - t0;
                 hph ^= 1;
@@ -267,43 +307,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             };
             auto skipk = [&](int j) { return skip_hi + j * kChunk; };
             auto skipl = [&](int j) { return skip_lo + j * kChunk; };
-            // TMEM columns: D2[m] = m*128, BUF[b] = 256 + b*128, D3 = BUF[0], D4 = D2[0]
-            for (unsigned t = pair_id; t < ntiles; t += npairs) {
-                {
-                    unsigned long long t0 = tr ? gtime() : 0;
-                    ptx::mbar_wait_cluster(&ms.f_ready, fph);
-                    if (tr) w_f += gtime() - t0;
-                }
-                fph ^= 1;
-                ptx::tc_fence_after();
+            // TMEM columns: D2[m] = m*NP, BUF[b] = 2NP + b*NP, D3 = BUF[0], D4 = D2[0]
+            auto body = [&](int ks, bool with_l4) {
                 auto L1 = [&](int c) {
-                    for (int j = 0; j < 4; ++j) item(256 + (c & 1) * 128, skipk(j), skipl(j), j > 0);
+                    for (int j = 0; j < ks; ++j) item(2 * NP + (c & 1) * NP, skipk(j), skipl(j), j > 0);
                     ptx::mma_commit_pair(&ms.l1done[c & 1], both);
                 };
                 L1(0);
                 L1(1);
                 for (int m = 0; m < 2; ++m)
-                    for (int j = 0; j < 4; ++j) item(m * 128, skipk(j), skipl(j), j > 0);
+                    for (int j = 0; j < ks; ++j) item(m * NP, skipk(j), skipl(j), j > 0);
                 for (int c = 0; c < 4; ++c) {
                     wait_h();
                     for (int m = 0; m < 2; ++m)
-                        for (int jj = 0; jj < 4; ++jj) item(m * 128, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
+                        for (int jj = 0; jj < 4; ++jj) item(m * NP, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
                     ptx::mma_commit_pair(&ms.h_free, both);
                     if (c + 2 < 4) L1(c + 2);
                 }
                 ptx::mma_commit_pair(&ms.d2done, both);
-                for (int j = 0; j < 4; ++j) item(256, skipk(j), skipl(j), j > 0);
+                for (int j = 0; j < ks; ++j) item(2 * NP, skipk(j), skipl(j), j > 0);
                 for (int c = 0; c < 2; ++c) {
                     wait_h();
-                    for (int jj = 0; jj < 4; ++jj) item(256, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
+                    for (int jj = 0; jj < 4; ++jj) item(2 * NP, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
                     ptx::mma_commit_pair(&ms.h_free, both);
                 }
                 ptx::mma_commit_pair(&ms.d3done, both);
-                for (int j = 0; j < 4; ++j) item(0, skipk(j), skipl(j), j > 0);
-                wait_h();
-                for (int jj = 0; jj < 4; ++jj) item(0, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
-                ptx::mma_commit_pair(&ms.h_free, both);
-                ptx::mma_commit_pair(&ms.d4done, both);
+                if (with_l4) {
+                    for (int j = 0; j < ks; ++j) item(0, skipk(j), skipl(j), j > 0);
+                    wait_h();
+                    for (int jj = 0; jj < 4; ++jj) item(0, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
+                    ptx::mma_commit_pair(&ms.h_free, both);
+                    ptx::mma_commit_pair(&ms.d4done, both);
+                } else {
+                    wait_h();  // prefix: h3 is in the skip operands of both CTAs
+                    ptx::mma_commit_pair(&ms.h_free, both);
+                }
+            };
+            for (unsigned t = pair_id; t < ntiles; t += npairs) {
+                {
+                    const unsigned long long t0 = tr ? gtime() : 0;
+                    ptx::mbar_wait_cluster(&ms.f_ready, fph);
+                    if (tr) w_f += gtime() - t0;
+                }
+                fph ^= 1;
+                ptx::tc_fence_after();
+                if (TEX) {
+                    body(4, false);
+                    body(8, true);
+                } else {
+                    body(4, true);
+                }
             }
             if (tr) {
                 P.trace[0] = gtime() - t_begin;
@@ -315,10 +368,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     } else {
         // ===================== gather + epilogue (8 warps, both CTAs) =====================
         const int et = threadIdx.x - 64;
+        const int ew = et >> 5;
         const int quarter = warp & 3;
         const int colh = (warp - 2) >> 2;  // point half this warp converts = destination CTA
         const int row = quarter * 32 + lane;
-        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(colh * 64);
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(colh * NPC);
         uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hfph = 1, sdph[2] = {0, 0};
         unsigned tile_iter = 0;
         const FieldDev& f = P.f;
@@ -328,27 +382,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t kc_off = (feat >> 6) * kChunk;
         const uint32_t kk = (feat & 63u) & ~1u;
         const uint32_t hdst = ptx::mapa(ptx::smem_u32(hbuf), (uint32_t)colh);  // h buffer of the owning CTA
-        const bool tr = P.trace && blockIdx.x == 0 && et == 0;
-        unsigned long long e_acc = 0, e_hf = 0, e_g = 0, e_fin = 0, e_emit = 0, e_begin = gtime();
-        auto ew = [&](uint64_t* bar, uint32_t par) {
-            unsigned long long t0 = tr ? gtime() : 0;
-            ptx::mbar_wait(bar, par);
-            if (tr) e_acc += gtime() - t0;
-        };
+        const uint32_t sdst = ptx::mapa(ptx::smem_u32(skip) + 4 * kChunk, (uint32_t)colh);  // texture: h3 -> skip
 
-        auto emit_block = [&](uint32_t col, const float* bias_blk, int out_dim, int feat0) {
+        // TMEM columns [col, col + NPC) of this thread's lane -> next layer's operand in the owning CTA
+        auto emit_block = [&](uint32_t col, const float* bias_blk, int out_dim, int feat0, uint32_t dst,
+                              uint32_t lo_off, bool write_lo) {
             const int o = feat0 + (int)feat;
             const float bo = __ldg(&bias_blk[o]);
             const float wz = __ldg(&bias_blk[out_dim + o]);
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
+            for (int hf = 0; hf < NPC / 32; ++hf) {
                 uint32_t r[32];
                 ptx::tmem_ld32(lane_base + col + hf * 32, r);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int q = 0; q < 32; q += 2) {
-                    const int pl = hf * 32 + q;          // point within the destination CTA (0..63)
-                    const int p = colh * 64 + pl;        // point within the pair tile
+                    const int pl = hf * 32 + q;    // point within the destination CTA
+                    const int p = colh * NPC + pl;  // point within the pair tile
                     float v0 = __uint_as_float(r[q]) + fmaf(wz, ms.z[p], bo);
                     float v1 = __uint_as_float(r[q + 1]) + fmaf(wz, ms.z[p + 1], bo);
                     v0 = v0 < 0.0f ? v0 * P.slope : v0;
@@ -359,18 +409,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const float b = odd ? v1 : recv;
                     const uint32_t off = kc_off + sw128((uint32_t)(pl + (odd ? 1 : 0)), kk);
                     const uint32_t hv = pack_bf16(a, b);
-                    ptx::st_cluster_u32(hdst + off, hv);
-                    if (P.x3) {
+                    ptx::st_cluster_u32(dst + off, hv);
+                    if (write_lo) {
                         const float ah = __uint_as_float(hv << 16), bh = __uint_as_float(hv & 0xFFFF0000u);
-                        ptx::st_cluster_u32(hdst + kHHalf + off, pack_bf16(a - ah, b - bh));
+                        ptx::st_cluster_u32(dst + lo_off + off, pack_bf16(a - ah, b - bh));
                     }
                 }
             }
         };
         auto h_begin = [&]() {
-            unsigned long long t0 = tr ? gtime() : 0;
             ptx::mbar_wait(&ms.h_free, hfph);
-            if (tr) e_hf += gtime() - t0;
             hfph ^= 1;
         };
         auto h_end = [&]() {
@@ -378,51 +426,84 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             ptx::mbar_arrive_cluster(h_ready0);
         };
+        auto wait_acc = [&](uint64_t* bar, uint32_t& par) {
+            ptx::mbar_wait(bar, par);
+            par ^= 1;
+            ptx::tc_fence_after();
+        };
+        // epilogue of one MLP body (layers 1-3); `after_l1c0` runs once layer-1 chunk 0 is done
+        auto body_epi = [&](const float* bias, bool prefix, auto&& after_l1c0) {
+            const float* b1 = bias;
+            const float* b2 = b1 + 2 * 1024;
+            const float* b3 = b2 + 2 * 512;
+            for (int c = 0; c < 4; ++c) {
+                wait_acc(&ms.l1done[c & 1], l1ph[c & 1]);
+                if (c == 0) after_l1c0();
+                h_begin();
+                emit_block(2 * NP + (c & 1) * NP, b1, 1024, c * 256, hdst, kHHalf, P.x3);
+                h_end();
+            }
+            wait_acc(&ms.d2done, d2ph);
+            for (int m = 0; m < 2; ++m) {
+                h_begin();
+                emit_block(m * NP, b2, 512, m * 256, hdst, kHHalf, P.x3);
+                h_end();
+            }
+            wait_acc(&ms.d3done, d3ph);
+            h_begin();
+            if (prefix)  // h3 -> skip K-chunks 4..7 (lo always: the final skip dot reads hi + lo)
+                emit_block(2 * NP, b3, 256, 0, sdst, kSkipHalf, true);
+            else
+                emit_block(2 * NP, b3, 256, 0, hdst, kHHalf, P.x3);
+            h_end();
+        };
 
-        const float* b1 = P.bias;
-        const float* b2 = b1 + 2 * 1024;
-        const float* b3 = b2 + 2 * 512;
-        const float* b4 = b3 + 2 * 256;
+        const float* bias = TEX ? P.bias_t : P.bias_g;
+        const float* b4 = bias + 2 * (1024 + 512 + 256);
         const float* b5 = b4 + 2 * 128;
+        constexpr int wl_stride = 128 + C::kSkipDim;
 
         for (unsigned t = pair_id; t < ntiles; t += npairs) {
             const unsigned base = t * NP;
-            // ---- positions of all 128 points (every CTA needs z for its epilogue) ----
             const int tp = (int)(tile_iter & 1u);
+            // ---- positions of all points of the pair tile (every CTA needs z for its epilogue) ----
             if (et < NP) {
                 const unsigned idx = base + et;
                 double pd[3] = {0.0, 0.0, 0.0};
                 if (idx < n) job_point_d(job, idx, pd);
-                for (int d = 0; d < 3; ++d) {
-                    ms.posd[et][d] = pd[d];
-                    ms.pos[et][d] = (float)pd[d];
-                }
+                for (int d = 0; d < 3; ++d) ms.pos[et][d] = (float)pd[d];
                 ms.z[et] = (float)pd[2];
-                if (leader)  // constant part of the final logit: b5 + w5z*z - sdf_scale*sdf(P) (fp64 SDF)
-                    ms.cterm[et] = __ldg(&b5[0]) + __ldg(&P.wlast[128 + kGeoSkip - 1]) * (float)pd[2] +
-                                   (float)(-scene.sdf_scale * scene_sdf(scene, pd));
+                if (leader) {
+                    // constant part of the final logits: b5 + w5z*z (- sdf_scale*sdf(P), fp64 SDF, geometry)
+                    float extra = 0.0f;
+                    if (!TEX) extra = (float)(-scene.sdf_scale * scene_sdf(scene, pd));
+                    for (int c = 0; c < NOUT; ++c)
+                        ms.cterm[c][et] = __ldg(&b5[c]) +
+                                          __ldg(&P.wlast[c * wl_stride + wl_stride - 1]) * (float)pd[2] + extra;
+                }
             }
             epi_bar();
-            // ---- gather Phi for this CTA's 64 points into its skip operand ----
-            // warp per point (8 points per warp, 2 in flight); lane = 8 consecutive
-            // channels = one 16-byte SW128 chunk of the bf16 operand; the same pass
-            // computes the final layer's skip-input dot product in fp32.
-            unsigned long long tg = tr ? gtime() : 0;
+            // ---- gather Phi for this CTA's points into its skip operand ----
+            // warp per point (2 in flight); lane = 8 consecutive channels = one 16-byte
+            // SW128 chunk of the bf16 operand; the same pass computes the final
+            // layer's Phi-part skip dot in fp32.
             {
-                const int ew = et >> 5;
                 const int c0 = 8 * lane;
                 const uint32_t chunk = (uint32_t)(c0 >> 6) * kChunk;
                 const uint32_t c16 = (uint32_t)((c0 & 63) >> 3);
                 const size_t rowW = (size_t)f.W * f.C;
-                float w5s[8];
+                float w5s[NOUT][8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) w5s[i] = __ldg(&P.wlast[128 + c0 + i]);
-                for (int it = 0; it < 4; ++it) {
-                    float4 t[2][8];
+                for (int c = 0; c < NOUT; ++c)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) w5s[c][i] = __ldg(&P.wlast[c * wl_stride + 128 + c0 + i]);
+                constexpr int kPerWarp = NPC / kEpiWarps;
+                for (int it = 0; it < kPerWarp / 2; ++it) {
+                    float4 tv[2][8];
                     float wts[2][4];
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
-                        const int p = (int)rank * 64 + ew * 8 + it * 2 + j;
+                        const int p = (int)rank * NPC + ew * kPerWarp + it * 2 + j;
                         float u = (ms.pos[p][0] + 1.0f) * 0.5f * (float)(f.W - 1);
                         float v = (1.0f - ms.pos[p][1]) * 0.5f * (float)(f.H - 1);
                         u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
@@ -437,17 +518,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const float* taps[4] = {m00, m00 + f.C, m00 + rowW, m00 + rowW + f.C};
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            t[j][2 * q] = __ldg(reinterpret_cast<const float4*>(taps[q]));
-                            t[j][2 * q + 1] = __ldg(reinterpret_cast<const float4*>(taps[q] + 4));
+                            tv[j][2 * q] = __ldg(reinterpret_cast<const float4*>(taps[q]));
+                            tv[j][2 * q + 1] = __ldg(reinterpret_cast<const float4*>(taps[q] + 4));
                         }
                     }
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
-                        const int pl = ew * 8 + it * 2 + j;
+                        const int pl = ew * kPerWarp + it * 2 + j;
                         float val[8];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            const float4 a0 = t[j][h], a1 = t[j][2 + h], a2 = t[j][4 + h], a3 = t[j][6 + h];
+                            const float4 a0 = tv[j][h], a1 = tv[j][2 + h], a2 = tv[j][4 + h], a3 = tv[j][6 + h];
                             val[4 * h + 0] = wts[j][0] * a0.x + wts[j][1] * a1.x + wts[j][2] * a2.x + wts[j][3] * a3.x;
                             val[4 * h + 1] = wts[j][0] * a0.y + wts[j][1] * a1.y + wts[j][2] * a2.y + wts[j][3] * a3.y;
                             val[4 * h + 2] = wts[j][0] * a0.z + wts[j][1] * a1.z + wts[j][2] * a2.z + wts[j][3] * a3.z;
@@ -456,27 +537,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         uint4 hv, lv;
                         uint32_t* hp = reinterpret_cast<uint32_t*>(&hv);
                         uint32_t* lp = reinterpret_cast<uint32_t*>(&lv);
-                        float dot = 0.0f;
+                        float dot[NOUT];
+#pragma unroll
+                        for (int c = 0; c < NOUT; ++c) dot[c] = 0.0f;
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
                             const float a = val[2 * i], b = val[2 * i + 1];
                             hp[i] = pack_bf16(a, b);
                             lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
-                            dot = fmaf(w5s[2 * i], a, dot);
-                            dot = fmaf(w5s[2 * i + 1], b, dot);
+#pragma unroll
+                            for (int c = 0; c < NOUT; ++c) {
+                                dot[c] = fmaf(w5s[c][2 * i], a, dot[c]);
+                                dot[c] = fmaf(w5s[c][2 * i + 1], b, dot[c]);
+                            }
                         }
                         const uint32_t off = chunk + (uint32_t)pl * 128u + (((c16 ^ (uint32_t)pl) & 7u) << 4);
                         *reinterpret_cast<uint4*>(skip + off) = hv;
                         *reinterpret_cast<uint4*>(skip + kSkipHalf + off) = lv;
 #pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                        for (int c = 0; c < NOUT; ++c)
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) dot[c] += __shfl_xor_sync(0xffffffffu, dot[c], o);
                         if (lane == 0) {
-                            const int p = (int)rank * 64 + pl;
-                            if (leader) {
-                                ms.skipdot[tp][p] = dot;
+                            if (TEX) {
+#pragma unroll
+                                for (int c = 0; c < NOUT; ++c) ms.sdl[c][pl] = dot[c];
                             } else {
-                                ptx::st_cluster_f32(ptx::mapa(ptx::smem_u32(&ms.skipdot[tp][p]), 0), dot);
-                                ptx::mbar_arrive_cluster(sd_ready0 + 8 * tp);
+                                const int p = (int)rank * NPC + pl;
+                                if (leader) {
+                                    ms.skipdot[tp][0][p] = dot[0];
+                                } else {
+                                    ptx::st_cluster_f32(ptx::mapa(ptx::smem_u32(&ms.skipdot[tp][0][p]), 0), dot[0]);
+                                    ptx::mbar_arrive_cluster(sd_ready0 + 8 * tp);
+                                }
                             }
                         }
                     }
@@ -484,53 +577,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             ptx::fence_proxy_async_cluster();
             ptx::mbar_arrive_cluster(f_ready0);
-            if (tr) e_g += gtime() - tg;
 
-            // ---- layer 1 chunks (256 features each) -> h buffers of both CTAs ----
-            for (int c = 0; c < 4; ++c) {
-                ew(&ms.l1done[c & 1], l1ph[c & 1]);
-                l1ph[c & 1] ^= 1;
-                ptx::tc_fence_after();
-                h_begin();
-                emit_block(256 + (c & 1) * 128, b1, 1024, c * 256);
-                h_end();
+            if (TEX) {
+                body_epi(P.bias_g, true, [] {});
+                // texture body: when its layer-1 chunk 0 is done, h3 (skip chunks 4..7) has been
+                // consumed by the tensor cores, i.e. it is complete in both CTAs -> add the h3
+                // part of the final skip dot for this CTA's points (fp32 from hi + lo)
+                body_epi(P.bias_t, false, [&] {
+                    epi_bar();  // ms.sdl from the gather warps
+                    const int pl = et >> 3, part = et & 7;  // NPC = 32 points x 8 slices of 32 features
+                    float acc[NOUT];
+#pragma unroll
+                    for (int c = 0; c < NOUT; ++c) acc[c] = 0.0f;
+                    for (int j = part * 32; j < part * 32 + 32; j += 2) {
+                        const int k = 256 + j;
+                        const uint32_t off = (uint32_t)(k >> 6) * kChunk + sw128((uint32_t)pl, (uint32_t)(k & 63));
+                        const uint32_t hv = *reinterpret_cast<const uint32_t*>(skip + off);
+                        const uint32_t lv = *reinterpret_cast<const uint32_t*>(skip + kSkipHalf + off);
+                        const float x0 = __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
+                        const float x1 = __uint_as_float(hv & 0xFFFF0000u) + __uint_as_float(lv & 0xFFFF0000u);
+#pragma unroll
+                        for (int c = 0; c < NOUT; ++c) {
+                            acc[c] = fmaf(__ldg(&P.wlast[c * wl_stride + 128 + k]), x0, acc[c]);
+                            acc[c] = fmaf(__ldg(&P.wlast[c * wl_stride + 128 + k + 1]), x1, acc[c]);
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < NOUT; ++c)
+#pragma unroll
+                        for (int o = 1; o < 8; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+                    if (part == 0) {
+                        const int p = (int)rank * NPC + pl;
+#pragma unroll
+                        for (int c = 0; c < NOUT; ++c) {
+                            const float v = acc[c] + ms.sdl[c][pl];
+                            if (leader)
+                                ms.skipdot[tp][c][p] = v;
+                            else
+                                ptx::st_cluster_f32(ptx::mapa(ptx::smem_u32(&ms.skipdot[tp][c][p]), 0), v);
+                        }
+                        if (!leader) ptx::mbar_arrive_cluster(sd_ready0 + 8 * tp);
+                    }
+                });
+            } else {
+                body_epi(P.bias_g, false, [] {});
             }
-            ew(&ms.d2done, d2ph);
-            d2ph ^= 1;
-            ptx::tc_fence_after();
-            for (int m = 0; m < 2; ++m) {
-                h_begin();
-                emit_block(m * 128, b2, 512, m * 256);
-                h_end();
-            }
-            ew(&ms.d3done, d3ph);
-            d3ph ^= 1;
-            ptx::tc_fence_after();
-            h_begin();
-            emit_block(256, b3, 256, 0);
-            h_end();
-            ew(&ms.d4done, d4ph);
-            d4ph ^= 1;
-            ptx::tc_fence_after();
-            unsigned long long tf = tr ? gtime() : 0;
-            // ---- final layer (CTA 0 holds layer-4 rows 0..127 for all 128 points) ----
+            wait_acc(&ms.d4done, d4ph);
+            // ---- final layer (CTA 0 holds layer-4 rows 0..127 for all points) ----
             if (leader) {
                 const float bo = __ldg(&b4[row]), wz = __ldg(&b4[128 + row]);
-                const float w5 = __ldg(&P.wlast[row]);
+                float w5[NOUT];
 #pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
+                for (int c = 0; c < NOUT; ++c) w5[c] = __ldg(&P.wlast[c * wl_stride + row]);
+#pragma unroll
+                for (int hf = 0; hf < NPC / 32; ++hf) {
                     uint32_t r[32];
-                    ptx::tmem_ld32(lane_base + 0 + hf * 32, r);
+                    ptx::tmem_ld32(lane_base + hf * 32, r);
                     ptx::tmem_ld_wait();
-                    float v[32];
+                    float hx[32];
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
-                        float x = __uint_as_float(r[q]) + fmaf(wz, ms.z[colh * 64 + hf * 32 + q], bo);
-                        x = x < 0.0f ? x * P.slope : x;
-                        v[q] = w5 * x;
+                        const float x = __uint_as_float(r[q]) + fmaf(wz, ms.z[colh * NPC + hf * 32 + q], bo);
+                        hx[q] = x < 0.0f ? x * P.slope : x;
                     }
-                    const float sum = warp_transpose_reduce(v);
-                    ms.red[quarter][colh * 64 + hf * 32 + lane] = sum;
+#pragma unroll
+                    for (int c = 0; c < NOUT; ++c) {
+                        float v[32];
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) v[q] = w5[c] * hx[q];
+                        ms.red[quarter][c][colh * NPC + hf * 32 + lane] = warp_transpose_reduce(v);
+                    }
                 }
             }
             ptx::tc_fence_before();
@@ -538,30 +654,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (leader) {
                 ptx::mbar_wait_cluster(&ms.sd_ready[tp], sdph[tp]);
                 sdph[tp] ^= 1;
-                if (et < NP) {
-                    const int p = et;
+                if (et < NP * NOUT) {
+                    const int p = et % NP, c = et / NP;
                     const unsigned idx = base + p;
-                    const float s = ms.red[0][p] + ms.red[1][p] + ms.red[2][p] + ms.red[3][p] + ms.skipdot[tp][p] +
-                                    ms.cterm[p];
+                    const float s = ms.red[0][c][p] + ms.red[1][c][p] + ms.red[2][c][p] + ms.red[3][c][p] +
+                                    ms.skipdot[tp][c][p] + ms.cterm[c][p];
                     if (idx < n) {
-                        const float vv = 1.0f / (1.0f + expf(-s));
-                        if (job_is_grid(job))
-                            grid_epilogue(job, job_node(job, idx), vv);
-                        else
-                            job.out[idx] = vv;
+                        float v = 1.0f / (1.0f + expf(-s));
+                        if (TEX) {
+                            if (job.out_pixel) {
+                                v = fminf(fmaxf(v, 0.0f), 1.0f);  // clamp01, render.hpp:276
+                                job.out[(size_t)job.out_pixel[idx] * 3 + c] = v;
+                            } else {
+                                job.out[(size_t)idx * 3 + c] = v;
+                            }
+                        } else if (job_is_grid(job)) {
+                            grid_epilogue(job, job_node(job, idx), v);
+                        } else {
+                            job.out[idx] = v;
+                        }
                     }
                 }
             }
             epi_bar();
-            if (tr) e_fin += gtime() - tf;
             ++tile_iter;
-        }
-        if (tr) {
-            P.trace[4] = gtime() - e_begin;
-            P.trace[5] = e_acc;
-            P.trace[6] = e_hf;
-            P.trace[7] = e_g;
-            P.trace[8] = e_fin;
         }
     }
     ptx::tc_fence_before();
@@ -575,7 +691,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }  // namespace pair
 
 // ===========================================================================
-// Host side: pair weight stream + tensor map + launch
+// Host side: pair weight streams + tensor maps + launch
 // ===========================================================================
 static inline uint16_t f2bf_p(float f) {
     uint32_t u;
@@ -590,13 +706,17 @@ static inline float bf2f_p(uint16_t h) {
     return f;
 }
 
-size_t pair_stream_bytes() { return (size_t)pair::kItems * 4 * pair::kHalf; }
+size_t pair_stream_bytes(int which) {
+    return (size_t)(which == ICG_MLP_GEOMETRY ? pair::kGeoItems : pair::kTexItems) * 4 * pair::kHalf;
+}
 
 // item i, half h (rows h*128.. of the 256-row block), part (hi/lo): 16 KB SW128 tile
-int pair_pack_geometry(const float* const* w, uint8_t* stream) {
-    const int* outs = kGeoOut;
+int pair_pack(int which, const float* const* w, uint8_t* stream) {
+    const bool geo = which == ICG_MLP_GEOMETRY;
+    const int* outs = geo ? kGeoOut : kTexOut;
+    const int skip = geo ? kGeoSkip : kTexSkip;
     int ins[5];
-    for (int l = 0; l < 5; ++l) ins[l] = (l ? outs[l - 1] : 0) + kGeoSkip;
+    for (int l = 0; l < 5; ++l) ins[l] = (l ? outs[l - 1] : 0) + skip;
     int item = 0;
     auto emit = [&](int l, int m, int col0) {
         for (int h = 0; h < 2; ++h) {
@@ -616,8 +736,8 @@ int pair_pack_geometry(const float* const* w, uint8_t* stream) {
         }
         ++item;
     };
-    pair::schedule(emit);
-    return item == pair::kItems ? ICG_OK : ICG_ERUNTIME;
+    pair::schedule(geo ? 4 : 8, true, emit);
+    return item == (geo ? pair::kGeoItems : pair::kTexItems) ? ICG_OK : ICG_ERUNTIME;
 }
 
 int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-byte CUtensorMap */) {
@@ -647,24 +767,15 @@ int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-b
     return ICG_OK;
 }
 
-int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
-                          unsigned max_points, bool x3, cudaStream_t s) {
+template <bool TEX>
+static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, unsigned max_points, cudaStream_t s) {
+    using C = pair::Cfg<TEX>;
     static bool attr = false;
     if (!attr) {
-        ICG_CUDA_TRY(cudaFuncSetAttribute(pair::k_mlp_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)pair::kTotal));
+        ICG_CUDA_TRY(cudaFuncSetAttribute(pair::k_mlp_pair<TEX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)C::kTotal));
         attr = true;
     }
-    pair::Params p{};
-    p.f = f;
-    p.job = job;
-    p.bias = geo.bias;
-    p.wlast = geo.w_last;
-    p.slope = 0.02f;
-    p.x3 = x3 ? 1 : 0;
-    unsigned pairs = (max_points + pair::NP - 1) / pair::NP;
-    if (pairs > 74) pairs = 74;
-    if (pairs == 0) pairs = 1;
     static unsigned long long* trace = nullptr;
     static int tron = -1;
     if (tron < 0) {
@@ -674,20 +785,50 @@ int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap,
     }
     p.trace = tron ? trace : nullptr;
     if (p.trace) cudaMemsetAsync(p.trace, 0, 64 * 8, s);
-    CUtensorMap tm;
-    std::memcpy(&tm, tmap, sizeof(CUtensorMap));
-    pair::k_mlp_pair<<<2 * pairs, pair::kThreads, pair::kTotal, s>>>(tm, p);
+    unsigned pairs = (max_points + C::NP - 1) / C::NP;
+    if (pairs > 74) pairs = 74;
+    if (pairs == 0) pairs = 1;
+    CUtensorMap ta, tb;
+    std::memcpy(&ta, tmapA, sizeof(CUtensorMap));
+    std::memcpy(&tb, tmapB ? tmapB : tmapA, sizeof(CUtensorMap));
+    pair::k_mlp_pair<TEX><<<2 * pairs, pair::kThreads, C::kTotal, s>>>(ta, tb, p);
     ICG_CUDA_TRY(cudaGetLastError());
     if (p.trace) {
         cudaStreamSynchronize(s);
         const unsigned long long* t = p.trace;
-        fprintf(stderr,
-                "[pair-trace] mma: total %.1f us, wait data %.1f, wait h %.1f, wait f %.1f | epi: total %.1f, wait acc "
-                "%.1f, wait hfree %.1f, gather %.1f, final %.1f\n",
-                t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3, t[6] * 1e-3, t[7] * 1e-3,
-                t[8] * 1e-3);
+        fprintf(stderr, "[pair-trace %s] mma: total %.1f us, wait data %.1f, wait h %.1f, wait f %.1f\n",
+                TEX ? "tex" : "geo", t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3);
     }
     return ICG_OK;
+}
+
+int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
+                          unsigned max_points, bool x3, cudaStream_t s) {
+    pair::Params p{};
+    p.f = f;
+    p.job = job;
+    p.bias_g = geo.bias;
+    p.wlast = geo.w_last;
+    p.items_a = pair::kGeoItems;
+    p.slope = 0.02f;
+    p.x3 = x3 ? 1 : 0;
+    return launch_pair<false>(p, tmap, nullptr, max_points, s);
+}
+
+int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const void* tmap_geo,
+                             const void* tmap_tex, const EvalJob& job, unsigned max_points, bool x3,
+                             cudaStream_t s) {
+    pair::Params p{};
+    p.f = f;
+    p.job = job;
+    p.bias_g = geo.bias;
+    p.bias_t = tex.bias;
+    p.wlast = tex.w_last;
+    p.items_a = pair::kPrefixItems;  // the geometry prefix = the first items of the geometry stream
+    p.items_b = pair::kTexItems;
+    p.slope = 0.02f;
+    p.x3 = x3 ? 1 : 0;
+    return launch_pair<true>(p, tmap_geo, tmap_tex, max_points, s);
 }
 
 }  // namespace icg
