@@ -130,4 +130,32 @@ __device__ __forceinline__ double scene_sdf(const DevScene& s, const double* p) 
     return acc;
 }
 
+// Warp-cooperative scene_sdf: lane i evaluates primitives i, i+32, ...; the
+// union keeps the first minimum in primitive order, exactly as the serial loop
+// (every lane returns the result).
+__device__ __forceinline__ double scene_sdf_warp(const DevScene& s, const double* p) {
+    const int lane = threadIdx.x & 31;
+    double best = 0.0;
+    int bi = 0x7fffffff;
+    for (int i = lane; i < s.n_prims; i += 32) {
+        const double d = prim_sdf(s.prims[i], p);
+        if (bi == 0x7fffffff || d < best) {
+            best = d;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        // a wins if strictly smaller, or equal and earlier in primitive order
+        const bool take = oi != 0x7fffffff && (bi == 0x7fffffff || ob < best || (!(best < ob) && oi < bi));
+        if (take) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    return best;
+}
+
 }  // namespace icg

@@ -86,8 +86,11 @@ struct icg_context {
     DBuf list_e0, cf[2], nx[2];
     DBuf ctr;
     DevCounters* h_ctr = nullptr;  // pinned
-    DBuf binar, pts, outv, small_scratch;
-    unsigned small_max = 96;  // batches up to this size take the layer-parallel latency path
+    DBuf binar, pts, outv, small_scratch, lp_scratch, lp_stream;
+    unsigned small_max = 96;  // ICG_LAT=small: batches up to this size take the SIMT latency kernel
+    unsigned lp_max = 1536;   // batches up to this size take the layer-parallel tensor-core path (k_lp.cu)
+    bool lat_small = false;
+    bool geo_lp = false;
     // render
     DBuf depth, rgb, mask, surfk, spts, spx;
     // last extraction
@@ -265,7 +268,19 @@ int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned ma
         r = launch_analytic_eval(fd, job, max_points, c->stream);
     } else if (fd.precision == ICG_PREC_FP32_SIMT) {
         r = launch_pifu_simt_eval(fd, c->geo_simt, job, max_points, c->stream);
-    } else if (dependent_chain && c->small_max > 0) {
+    } else if (dependent_chain && c->geo_lp && c->lp_max > 0 && !c->lat_small) {
+        // both launched; each exits on device unless the batch size is its own
+        if (int e = c->lp_scratch.ensure(lp_scratch_bytes(c->lp_max))) return e;
+        EvalJob big = job;
+        big.min_count = c->lp_max + 1;
+        const bool x3 = fd.precision == ICG_PREC_FP32;
+        if (c->geo_pair && c->use_pair)
+            r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap, big, max_points, x3, c->stream);
+        else
+            r = launch_pifu_tc_eval(fd, c->geo_tc, big, max_points, x3, c->stream);
+        if (!r) r = launch_lp_eval(fd, c->geo_tc, c->lp_stream.as<uint8_t>(), job, c->lp_scratch.as<uint8_t>(), c->lp_max, x3, c->stream);
+        c->launches += 1;
+    } else if (dependent_chain && c->small_max > 0 && c->lat_small) {
         if (int e = c->small_scratch.ensure(small_scratch_bytes(c->small_max))) return e;
         EvalJob big = job;
         big.min_count = c->small_max + 1;
@@ -638,6 +653,8 @@ int icg_create(int device, icg_context** out) {
     c->device = device;
     if (const char* e = getenv("ICG_NO_PAIR")) c->use_pair = !(e[0] == '1');
     if (const char* e = getenv("ICG_SMALL_MAX")) c->small_max = (unsigned)atoi(e);
+    if (const char* e = getenv("ICG_LP_MAX")) c->lp_max = (unsigned)atoi(e);
+    if (const char* e = getenv("ICG_LAT")) c->lat_small = std::string(e) == "small";
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->e0) != cudaSuccess || cudaEventCreate(&c->e1) != cudaSuccess ||
         cudaMallocHost(&c->h_scene, sizeof(DevScene)) != cudaSuccess ||
@@ -661,7 +678,7 @@ int icg_destroy(icg_context* c) {
     DBuf* all[] = {&c->geo_stream, &c->geo_bias, &c->geo_wlast, &c->tex_stream, &c->tex_bias, &c->tex_wlast,
                    &c->scene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
-                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->geo_pair_stream, &c->tex_pair_stream,
+                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->lp_scratch, &c->lp_stream, &c->geo_pair_stream, &c->tex_pair_stream,
                    &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx};
     for (DBuf* b : all) b->release();
     for (int l = 0; l < 5; ++l) {
@@ -784,6 +801,17 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
         ICG_CUDA_TRY(cudaMemcpy(ps_dev.p, ps.data(), pb, cudaMemcpyHostToDevice));
         if (int r = pair_make_tmap(ps_dev.p, pb, geo ? c->geo_pair_tmap : c->tex_pair_tmap)) return r;
         (geo ? c->geo_pair : c->tex_pair) = true;
+    }
+    if (geo) {
+        // layer-parallel latency path: weight tiles per (layer, row block, K chunk)
+        const size_t lb = lp_stream_bytes();
+        std::vector<uint8_t> ls(lb);
+        const float* ws[5];
+        for (int l = 0; l < 5; ++l) ws[l] = d->weights[l];
+        if (int r = lp_pack_geometry(ws, ls.data())) return r;
+        if (int r = c->lp_stream.ensure(lb)) return r;
+        ICG_CUDA_TRY(cudaMemcpy(c->lp_stream.p, ls.data(), lb, cudaMemcpyHostToDevice));
+        c->geo_lp = true;
     }
     if (geo)
         c->has_geo = true;

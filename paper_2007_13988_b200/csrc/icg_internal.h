@@ -140,6 +140,11 @@ int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap,
 int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const void* tmap_geo,
                              const void* tmap_tex, const EvalJob& job, unsigned max_points, bool x3,
                              cudaStream_t s);
+size_t lp_stream_bytes();
+int lp_pack_geometry(const float* const* w, uint8_t* stream);
+size_t lp_scratch_bytes(unsigned max_count);
+int launch_lp_eval(const FieldDev& f, const TcMlp& geo, const uint8_t* lp_stream, const EvalJob& job, uint8_t* scratch,
+                   unsigned max_count, bool x3, cudaStream_t s);
 size_t small_scratch_bytes(unsigned cap);
 int launch_small_mlp(const FieldDev& f, const SimtMlp& geo, const float* const* wrow, const EvalJob& job,
                      float* scratch, unsigned cap, unsigned max_count, cudaStream_t s);
