@@ -130,6 +130,53 @@ __device__ __forceinline__ double scene_sdf(const DevScene& s, const double* p) 
     return acc;
 }
 
+// fp32 union SDF (same formulas; the PIFu capsule bias is tolerance-bound)
+__device__ __forceinline__ float prim_sdf_f(const FPrim* pr, const float* p) {
+    const int kind = __ldg(&pr->kind);
+    float l[3] = {p[0] - __ldg(&pr->c[0]), p[1] - __ldg(&pr->c[1]), p[2] - __ldg(&pr->c[2])};
+    if (__ldg(&pr->rotated)) {
+        float l2[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            l2[r] = __ldg(&pr->inv[3 * r]) * l[0] + __ldg(&pr->inv[3 * r + 1]) * l[1] + __ldg(&pr->inv[3 * r + 2]) * l[2];
+        l[0] = l2[0];
+        l[1] = l2[1];
+        l[2] = l2[2];
+    }
+    if (kind == ICG_PRIM_CAPSULE) {
+        const float pa[3] = {p[0] - __ldg(&pr->a[0]), p[1] - __ldg(&pr->a[1]), p[2] - __ldg(&pr->a[2])};
+        const float ba[3] = {__ldg(&pr->b[0]) - __ldg(&pr->a[0]), __ldg(&pr->b[1]) - __ldg(&pr->a[1]),
+                             __ldg(&pr->b[2]) - __ldg(&pr->a[2])};
+        const float den = ba[0] * ba[0] + ba[1] * ba[1] + ba[2] * ba[2];
+        float h = 0.0f;
+        if (den > 0.0f) h = fminf(fmaxf((pa[0] * ba[0] + pa[1] * ba[1] + pa[2] * ba[2]) / den, 0.0f), 1.0f);
+        const float v[3] = {pa[0] - h * ba[0], pa[1] - h * ba[1], pa[2] - h * ba[2]};
+        return sqrtf(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]) - __ldg(&pr->radius);
+    }
+    if (kind == ICG_PRIM_SPHERE) return sqrtf(l[0] * l[0] + l[1] * l[1] + l[2] * l[2]) - __ldg(&pr->radius);
+    if (kind == ICG_PRIM_BOX) {
+        const float q[3] = {fabsf(l[0]) - __ldg(&pr->half[0]), fabsf(l[1]) - __ldg(&pr->half[1]),
+                            fabsf(l[2]) - __ldg(&pr->half[2])};
+        const float qp[3] = {fmaxf(q[0], 0.0f), fmaxf(q[1], 0.0f), fmaxf(q[2], 0.0f)};
+        return sqrtf(qp[0] * qp[0] + qp[1] * qp[1] + qp[2] * qp[2]) + fminf(fmaxf(q[0], fmaxf(q[1], q[2])), 0.0f);
+    }
+    if (kind == ICG_PRIM_TORUS) {
+        const float qx = sqrtf(l[0] * l[0] + l[2] * l[2]) - __ldg(&pr->major);
+        return sqrtf(qx * qx + l[1] * l[1]) - __ldg(&pr->minor);
+    }
+    return 1e30f;
+}
+
+__device__ __forceinline__ float scene_sdf_f(const FScene* s, const float* p) {
+    const int n = __ldg(&s->n_prims);
+    float acc = 0.0f;
+    for (int i = 0; i < n; ++i) {
+        const float d = prim_sdf_f(&s->prims[i], p);
+        acc = (i == 0) ? d : fminf(d, acc);
+    }
+    return acc;
+}
+
 // Warp-cooperative scene_sdf: lane i evaluates primitives i, i+32, ...; the
 // union keeps the first minimum in primitive order, exactly as the serial loop
 // (every lane returns the result).

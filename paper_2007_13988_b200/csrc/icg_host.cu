@@ -71,14 +71,17 @@ struct icg_context {
     SimtMlp geo_simt{}, tex_simt{};
     DBuf geo_stream, geo_bias, geo_wlast, tex_stream, tex_bias, tex_wlast;
     TcMlp geo_tc{}, tex_tc{};
-    DBuf geo_pair_stream, tex_pair_stream;
-    alignas(64) unsigned char geo_pair_tmap[128] = {};
-    alignas(64) unsigned char tex_pair_tmap[128] = {};
+    DBuf geo_pair_stream, tex_pair_stream, geo_pair_hi, tex_pair_hi;
+    // TMA descriptors of the pair streams: [0] bf16x3 (hi, lo), [1] bf16 (hi only)
+    alignas(64) unsigned char geo_pair_tmap[2][128] = {};
+    alignas(64) unsigned char tex_pair_tmap[2][128] = {};
     bool geo_pair = false, tex_pair = false;
     bool use_pair = true;
     // field
     DBuf scene;
     DevScene* h_scene = nullptr;  // pinned staging
+    FScene* h_fscene = nullptr;
+    DBuf fscene;
     DBuf fmap_chw, fmap_hwc;
     // grids and work lists
     DBuf vals[2], sts[2];
@@ -223,10 +226,33 @@ int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
     h->sdf_scale = f->sdf_scale;
     if (int r = c->scene.ensure(sizeof(DevScene))) return r;
     ICG_CUDA_TRY(cudaMemcpyAsync(c->scene.p, h, sizeof(DevScene), cudaMemcpyHostToDevice, c->stream));
+    FScene* hf = c->h_fscene;
+    std::memset(hf, 0, sizeof(FScene));
+    for (int i = 0; i < s.n_prims; ++i) {
+        const DevPrim& d = h->prims[i];
+        FPrim& q = hf->prims[i];
+        q.kind = d.kind;
+        q.rotated = d.rotated;
+        for (int k = 0; k < 3; ++k) {
+            q.c[k] = (float)d.c[k];
+            q.a[k] = (float)d.a[k];
+            q.b[k] = (float)d.b[k];
+            q.half[k] = (float)d.half[k];
+        }
+        q.radius = (float)d.radius;
+        q.major = (float)d.major;
+        q.minor = (float)d.minor;
+        for (int k = 0; k < 9; ++k) q.inv[k] = (float)d.inv[k];
+    }
+    hf->n_prims = s.n_prims;
+    hf->sdf_scale = (float)f->sdf_scale;
+    if (int r = c->fscene.ensure(sizeof(FScene))) return r;
+    ICG_CUDA_TRY(cudaMemcpyAsync(c->fscene.p, hf, sizeof(FScene), cudaMemcpyHostToDevice, c->stream));
     fd = FieldDev{};
     fd.kind = f->kind;
     fd.precision = f->precision;
     fd.scene = c->scene.as<DevScene>();
+    fd.fscene = c->fscene.as<FScene>();
     if (f->kind == ICG_FIELD_PIFU) {
         if (!c->has_geo) return einval("field: PIFu field needs geometry MLP weights (icg_set_mlp)");
         if (f->precision != ICG_PREC_FP32 && f->precision != ICG_PREC_BF16 && f->precision != ICG_PREC_FP32_SIMT)
@@ -275,7 +301,7 @@ int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned ma
         big.min_count = c->lp_max + 1;
         const bool x3 = fd.precision == ICG_PREC_FP32;
         if (c->geo_pair && c->use_pair)
-            r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap, big, max_points, x3, c->stream);
+            r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap[x3 ? 0 : 1], big, max_points, x3, c->stream);
         else
             r = launch_pifu_tc_eval(fd, c->geo_tc, big, max_points, x3, c->stream);
         if (!r) r = launch_lp_eval(fd, c->geo_tc, c->lp_stream.as<uint8_t>(), job, c->lp_scratch.as<uint8_t>(), c->lp_max, x3, c->stream);
@@ -285,8 +311,8 @@ int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned ma
         EvalJob big = job;
         big.min_count = c->small_max + 1;
         if (c->geo_pair && c->use_pair)
-            r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap, big, max_points, fd.precision == ICG_PREC_FP32,
-                                      c->stream);
+            r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1], big,
+                                      max_points, fd.precision == ICG_PREC_FP32, c->stream);
         else
             r = launch_pifu_tc_eval(fd, c->geo_tc, big, max_points, fd.precision == ICG_PREC_FP32, c->stream);
         if (!r)
@@ -294,8 +320,8 @@ int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned ma
                                  c->small_max, c->stream);
         c->launches += 1;
     } else if (c->geo_pair && c->use_pair) {
-        r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap, job, max_points, fd.precision == ICG_PREC_FP32,
-                                  c->stream);
+        r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1], job,
+                                  max_points, fd.precision == ICG_PREC_FP32, c->stream);
     } else {
         r = launch_pifu_tc_eval(fd, c->geo_tc, job, max_points, fd.precision == ICG_PREC_FP32, c->stream);
     }
@@ -310,7 +336,8 @@ int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned
     if (fd.precision == ICG_PREC_FP32_SIMT)
         r = launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
     else if (c->geo_pair && c->tex_pair && c->use_pair)
-        r = launch_pifu_pair_texture(fd, c->geo_tc, c->tex_tc, c->geo_pair_tmap, c->tex_pair_tmap, job, max_points,
+        r = launch_pifu_pair_texture(fd, c->geo_tc, c->tex_tc, c->geo_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1],
+                                     c->tex_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1], job, max_points,
                                      fd.precision == ICG_PREC_FP32, c->stream);
     else
         r = launch_pifu_tc_texture(fd, c->geo_tc, c->tex_tc, job, max_points, fd.precision == ICG_PREC_FP32,
@@ -658,6 +685,7 @@ int icg_create(int device, icg_context** out) {
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->e0) != cudaSuccess || cudaEventCreate(&c->e1) != cudaSuccess ||
         cudaMallocHost(&c->h_scene, sizeof(DevScene)) != cudaSuccess ||
+        cudaMallocHost(&c->h_fscene, sizeof(FScene)) != cudaSuccess ||
         cudaMallocHost(&c->h_ctr, sizeof(DevCounters)) != cudaSuccess) {
         set_error("icg_create: CUDA resource allocation failed");
         delete c;
@@ -676,9 +704,9 @@ int icg_destroy(icg_context* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     DBuf* all[] = {&c->geo_stream, &c->geo_bias, &c->geo_wlast, &c->tex_stream, &c->tex_bias, &c->tex_wlast,
-                   &c->scene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
+                   &c->scene, &c->fscene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
-                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->lp_scratch, &c->lp_stream, &c->geo_pair_stream, &c->tex_pair_stream,
+                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->lp_scratch, &c->lp_stream, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi,
                    &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx};
     for (DBuf* b : all) b->release();
     for (int l = 0; l < 5; ++l) {
@@ -690,6 +718,7 @@ int icg_destroy(icg_context* c) {
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->h_scene) cudaFreeHost(c->h_scene);
+    if (c->h_fscene) cudaFreeHost(c->h_fscene);
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->e0) cudaEventDestroy(c->e0);
     if (c->e1) cudaEventDestroy(c->e1);
@@ -790,16 +819,21 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
         tc.valid = 1;
     }
     {
-        // CTA-pair operand stream (k_mlp_pair.cu) + its TMA descriptor
-        DBuf& ps_dev = geo ? c->geo_pair_stream : c->tex_pair_stream;
-        const size_t pb = pair_stream_bytes(d->which);
-        std::vector<uint8_t> ps(pb);
+        // CTA-pair operand streams (k_mlp_pair.cu) + their TMA descriptors
+        DBuf& px = geo ? c->geo_pair_stream : c->tex_pair_stream;
+        DBuf& ph = geo ? c->geo_pair_hi : c->tex_pair_hi;
+        const size_t bx = pair_stream_bytes(d->which, true), bh = pair_stream_bytes(d->which, false);
+        std::vector<uint8_t> sx(bx), sh(bh);
         const float* ws[5];
         for (int l = 0; l < 5; ++l) ws[l] = d->weights[l];
-        if (int r = pair_pack(d->which, ws, ps.data())) return r;
-        if (int r = ps_dev.ensure(pb)) return r;
-        ICG_CUDA_TRY(cudaMemcpy(ps_dev.p, ps.data(), pb, cudaMemcpyHostToDevice));
-        if (int r = pair_make_tmap(ps_dev.p, pb, geo ? c->geo_pair_tmap : c->tex_pair_tmap)) return r;
+        if (int r = pair_pack(d->which, ws, sx.data(), sh.data())) return r;
+        if (int r = px.ensure(bx)) return r;
+        if (int r = ph.ensure(bh)) return r;
+        ICG_CUDA_TRY(cudaMemcpy(px.p, sx.data(), bx, cudaMemcpyHostToDevice));
+        ICG_CUDA_TRY(cudaMemcpy(ph.p, sh.data(), bh, cudaMemcpyHostToDevice));
+        unsigned char (*tm)[128] = geo ? c->geo_pair_tmap : c->tex_pair_tmap;
+        if (int r = pair_make_tmap(px.p, bx, tm[0])) return r;
+        if (int r = pair_make_tmap(ph.p, bh, tm[1])) return r;
         (geo ? c->geo_pair : c->tex_pair) = true;
     }
     if (geo) {

@@ -54,6 +54,19 @@ struct DevPrim {
     double radius, half[3], major, minor, inv[9];
 };
 
+// fp32 mirror of the scene for the PIFu capsule bias inside the MLP kernels
+// (tolerance-bound; the exact fp64 form above serves the analytic field)
+struct FPrim {
+    int kind, rotated;
+    float c[3], a[3], b[3];
+    float radius, half[3], major, minor, inv[9];
+};
+struct FScene {
+    FPrim prims[ICG_MAX_PRIMS];
+    int n_prims;
+    float sdf_scale;
+};
+
 struct DevScene {
     DevPrim prims[ICG_MAX_PRIMS];
     int n_prims;
@@ -118,6 +131,7 @@ struct FieldDev {
     int kind;                 // ICG_FIELD_*
     int precision;
     const DevScene* scene;    // device pointer
+    const FScene* fscene;     // device pointer, fp32 mirror
     const float* fmap_hwc;    // H x W x C fp32
     int C, H, W;
 };
@@ -132,8 +146,8 @@ int launch_pifu_tc_eval(const FieldDev& f, const TcMlp& geo, const EvalJob& job,
                         bool bf16x3, cudaStream_t s);
 int launch_pifu_tc_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const EvalJob& job,
                            unsigned int max_points, bool bf16x3, cudaStream_t s);
-size_t pair_stream_bytes(int which);
-int pair_pack(int which, const float* const* w, uint8_t* stream);
+size_t pair_stream_bytes(int which, bool x3);
+int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi);
 int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out);
 int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
                           unsigned max_points, bool x3, cudaStream_t s);

@@ -44,7 +44,8 @@ namespace icg {
 
 namespace pair {
 
-constexpr uint32_t kHalf = 16384;  // one 128 x 64 bf16 tile
+constexpr uint32_t kHalf = 16384;   // one 128 x 64 bf16 tile
+constexpr uint32_t kStage = 32768;  // one TMA box: (hi, lo) of one item (bf16x3) or hi of two items (bf16)
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;
@@ -56,14 +57,14 @@ struct Cfg {
     static constexpr int NPC = TEX ? 32 : 64;        // points per CTA
     static constexpr int NP = 2 * NPC;               // points per pair tile = MMA N
     static constexpr int kSkipChunks = TEX ? 8 : 4;  // [Phi] or [Phi, h3] in 64-wide K-chunks
-    static constexpr int kStages = TEX ? 6 : 4;
+    static constexpr int kStages = TEX ? 3 : 2;  // 32 KB stages (per-copy TMA cost is size-independent)
     static constexpr uint32_t kChunk = NPC * 128;  // NPC point rows x 64 bf16 (SW128)
     static constexpr uint32_t kSkipHalf = kSkipChunks * kChunk;
     static constexpr uint32_t kHHalf = 4 * kChunk;  // one 256-feature block
     static constexpr uint32_t kOffSkip = 0;
     static constexpr uint32_t kOffH = kOffSkip + 2 * kSkipHalf;
     static constexpr uint32_t kOffRing = kOffH + 2 * kHHalf;
-    static constexpr uint32_t kOffMisc = kOffRing + kStages * kHalf;
+    static constexpr uint32_t kOffMisc = kOffRing + kStages * kStage;
     static constexpr uint32_t kMisc = 16384;
     static constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
     static constexpr int kOut = TEX ? 3 : 1;
@@ -123,7 +124,8 @@ struct Params {
     const float* bias_g;  // geometry per-layer [b, wz] blocks (same layout as the single-CTA stream)
     const float* bias_t;  // texture per-layer [b, wz] blocks
     const float* wlast;   // final layer of the evaluated network, [out][128 + skip]
-    int items_a, items_b;
+    int items_a, items_b;  // items used from stream A / B
+    int total_a, total_b;  // items in stream A / B (per-rank segment length)
     float slope;
     int x3;
     unsigned long long* trace;
@@ -173,7 +175,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* hbuf = smem + C::kOffH;
     uint8_t* ring = smem + C::kOffRing;
     Misc& ms = *reinterpret_cast<Misc*>(smem + C::kOffMisc);
-    __shared__ DevScene scene;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_rank();
@@ -209,9 +210,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmapA);
         if (TEX) ptx::prefetch_tmap(&tmapB);
     }
-    if (!TEX)
-        for (int i = threadIdx.x; i < (int)(sizeof(DevScene) / 8); i += blockDim.x)
-            reinterpret_cast<double*>(&scene)[i] = reinterpret_cast<const double*>(P.f.scene)[i];
     if (warp == 1) ptx::tmem_alloc2<512>(&ms.tmem_base);
     ptx::tc_fence_before();
     ptx::cluster_sync();
@@ -231,23 +229,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            const int parts = P.x3 ? 2 : 1;
+            const int per_stage = P.x3 ? 1 : 2;  // items per 32 KB box
             const uint32_t ring0 = ptx::smem_u32(ring);
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
                 for (int seg = 0; seg < (TEX ? 2 : 1); ++seg) {
                     const CUtensorMap* tm = seg ? &tmapB : &tmapA;
                     const int cnt = seg ? P.items_b : P.items_a;
-                    for (int i = 0; i < cnt; ++i)
-                        for (int part = 0; part < parts; ++part) {
-                            ptx::mbar_wait(&ms.empty[s], ph ^ 1);
-                            if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kHalf);
-                            const int row0 = ((i * 2 + (int)rank) * 2 + part) * 128;
-                            ptx::tma_load_2d_2sm(ring0 + s * kHalf, tm, full0 + s * 8, 0, row0);
-                            if (++s == kStages) {
-                                s = 0;
-                                ph ^= 1;
-                            }
+                    const int total = seg ? P.total_b : P.total_a;
+                    for (int i = 0; i < cnt; i += per_stage) {
+                        ptx::mbar_wait(&ms.empty[s], ph ^ 1);
+                        if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kStage);
+                        // stream layout [rank][item][hi, lo] (x3) or [rank][item][hi] (bf16), 128-row tiles
+                        const int row0 = ((int)rank * total + i) * (P.x3 ? 256 : 128);
+                        ptx::tma_load_2d_2sm(ring0 + s * kStage, tm, full0 + s * 8, 0, row0);
+                        if (++s == kStages) {
+                            s = 0;
+                            ph ^= 1;
                         }
+                    }
                 }
             }
         }
@@ -274,28 +273,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (tr) w_full += gtime() - t0;
                 ptx::tc_fence_after();
             };
+            int sub = 0;  // bf16: which of the two items of the current box
             auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc) {
                 const uint64_t bd_hi = ptx::sdesc_sw128(b_hi), bd_lo = ptx::sdesc_sw128(b_lo);
-                wait_full();
-                const uint64_t ad_hi = ptx::sdesc_sw128(ring0 + s * kHalf);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t koff = (uint64_t)(kk * 2);
-                    ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_hi + koff, idesc, (acc || kk > 0) ? 1u : 0u);
-                    if (P.x3) ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_lo + koff, idesc, 1u);
-                }
-                ptx::mma_commit_pair(&ms.empty[s], both);
-                next_stage();
                 if (P.x3) {
                     wait_full();
-                    const uint64_t ad_lo = ptx::sdesc_sw128(ring0 + s * kHalf);
+                    const uint64_t ad_hi = ptx::sdesc_sw128(ring0 + s * kStage);
+                    const uint64_t ad_lo = ptx::sdesc_sw128(ring0 + s * kStage + kHalf);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t koff = (uint64_t)(kk * 2);
+                        ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_hi + koff, idesc, (acc || kk > 0) ? 1u : 0u);
+                        ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_lo + koff, idesc, 1u);
                         ptx::mma_bf16_pair(tmem + dcol, ad_lo + koff, bd_hi + koff, idesc, 1u);
                     }
                     ptx::mma_commit_pair(&ms.empty[s], both);
                     next_stage();
+                } else {
+                    if (sub == 0) wait_full();
+                    const uint64_t ad = ptx::sdesc_sw128(ring0 + s * kStage + sub * kHalf);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t koff = (uint64_t)(kk * 2);
+                        ptx::mma_bf16_pair(tmem + dcol, ad + koff, bd_hi + koff, idesc, (acc || kk > 0) ? 1u : 0u);
+                    }
+                    if (sub == 1) {
+                        ptx::mma_commit_pair(&ms.empty[s], both);
+                        next_stage();
+                    }
+                    sub ^= 1;
                 }
             };
             auto wait_h = [&]() {
@@ -473,14 +479,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (idx < n) job_point_d(job, idx, pd);
                 for (int d = 0; d < 3; ++d) ms.pos[et][d] = (float)pd[d];
                 ms.z[et] = (float)pd[2];
-                if (leader) {
-                    // constant part of the final logits: b5 + w5z*z (- sdf_scale*sdf(P), fp64 SDF, geometry)
-                    float extra = 0.0f;
-                    if (!TEX) extra = (float)(-scene.sdf_scale * scene_sdf(scene, pd));
-                    for (int c = 0; c < NOUT; ++c)
-                        ms.cterm[c][et] = __ldg(&b5[c]) +
-                                          __ldg(&P.wlast[c * wl_stride + wl_stride - 1]) * (float)pd[2] + extra;
-                }
             }
             epi_bar();
             // ---- gather Phi for this CTA's points into its skip operand ----
@@ -577,6 +575,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             ptx::fence_proxy_async_cluster();
             ptx::mbar_arrive_cluster(f_ready0);
+            // constant part of the final logits, b5 + w5z*z (- sdf_scale*sdf(P) for geometry), off the
+            // MMA critical path: the tensor cores are busy with layer 1 now
+            if (leader && et < NP) {
+                float extra = 0.0f;
+                if (!TEX) extra = -__ldg(&f.fscene->sdf_scale) * scene_sdf_f(f.fscene, ms.pos[et]);
+                for (int c = 0; c < NOUT; ++c)
+                    ms.cterm[c][et] = __ldg(&b5[c]) + __ldg(&P.wlast[c * wl_stride + wl_stride - 1]) * ms.z[et] + extra;
+            }
 
             if (TEX) {
                 body_epi(P.bias_g, true, [] {});
@@ -706,22 +712,25 @@ static inline float bf2f_p(uint16_t h) {
     return f;
 }
 
-size_t pair_stream_bytes(int which) {
-    return (size_t)(which == ICG_MLP_GEOMETRY ? pair::kGeoItems : pair::kTexItems) * 4 * pair::kHalf;
+// x3 stream: [rank][item][hi, lo] 16 KB tiles; hi stream (bf16 mode): [rank][item][hi]
+size_t pair_stream_bytes(int which, bool x3) {
+    return (size_t)(which == ICG_MLP_GEOMETRY ? pair::kGeoItems : pair::kTexItems) * (x3 ? 4 : 2) * pair::kHalf;
 }
 
-// item i, half h (rows h*128.. of the 256-row block), part (hi/lo): 16 KB SW128 tile
-int pair_pack(int which, const float* const* w, uint8_t* stream) {
+// item i, rank r (rows r*128.. of the 256-row block), part (hi/lo): 16 KB SW128 tile
+int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi) {
     const bool geo = which == ICG_MLP_GEOMETRY;
     const int* outs = geo ? kGeoOut : kTexOut;
     const int skip = geo ? kGeoSkip : kTexSkip;
+    const int nitems = geo ? pair::kGeoItems : pair::kTexItems;
     int ins[5];
     for (int l = 0; l < 5; ++l) ins[l] = (l ? outs[l - 1] : 0) + skip;
     int item = 0;
     auto emit = [&](int l, int m, int col0) {
         for (int h = 0; h < 2; ++h) {
-            uint8_t* hi = stream + ((size_t)(item * 2 + h) * 2 + 0) * pair::kHalf;
-            uint8_t* lo = stream + ((size_t)(item * 2 + h) * 2 + 1) * pair::kHalf;
+            uint8_t* hi = stream_x3 + ((size_t)(h * nitems + item) * 2 + 0) * pair::kHalf;
+            uint8_t* lo = stream_x3 + ((size_t)(h * nitems + item) * 2 + 1) * pair::kHalf;
+            uint8_t* h2 = stream_hi + (size_t)(h * nitems + item) * pair::kHalf;
             for (int r = 0; r < 128; ++r) {
                 const int o = m * 256 + h * 128 + r;
                 for (int k = 0; k < 64; ++k) {
@@ -731,13 +740,14 @@ int pair_pack(int which, const float* const* w, uint8_t* stream) {
                     size_t off = (size_t)r * 128 + (size_t)(((k >> 3) ^ (r & 7)) << 4) + (size_t)(k & 7) * 2;
                     std::memcpy(hi + off, &a, 2);
                     std::memcpy(lo + off, &b, 2);
+                    std::memcpy(h2 + off, &a, 2);
                 }
             }
         }
         ++item;
     };
     pair::schedule(geo ? 4 : 8, true, emit);
-    return item == (geo ? pair::kGeoItems : pair::kTexItems) ? ICG_OK : ICG_ERUNTIME;
+    return item == nitems ? ICG_OK : ICG_ERUNTIME;
 }
 
 int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-byte CUtensorMap */) {
@@ -754,7 +764,7 @@ int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-b
     }
     cuuint64_t dims[2] = {128, (cuuint64_t)(bytes / 128)};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {128, 128};
+    cuuint32_t box[2] = {128, 256};  // one 32 KB stage
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
                         const_cast<void*>(dev_stream), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -810,6 +820,7 @@ int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap,
     p.bias_g = geo.bias;
     p.wlast = geo.w_last;
     p.items_a = pair::kGeoItems;
+    p.total_a = pair::kGeoItems;
     p.slope = 0.02f;
     p.x3 = x3 ? 1 : 0;
     return launch_pair<false>(p, tmap, nullptr, max_points, s);
@@ -826,6 +837,8 @@ int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& t
     p.wlast = tex.w_last;
     p.items_a = pair::kPrefixItems;  // the geometry prefix = the first items of the geometry stream
     p.items_b = pair::kTexItems;
+    p.total_a = pair::kGeoItems;
+    p.total_b = pair::kTexItems;
     p.slope = 0.02f;
     p.x3 = x3 ? 1 : 0;
     return launch_pair<true>(p, tmap_geo, tmap_tex, max_points, s);
