@@ -65,7 +65,7 @@ struct Cfg {
     static constexpr uint32_t kOffH = kOffSkip + 2 * kSkipHalf;
     static constexpr uint32_t kOffRing = kOffH + 2 * kHHalf;
     static constexpr uint32_t kOffMisc = kOffRing + kStages * kStage;
-    static constexpr uint32_t kMisc = 16384;
+    static constexpr uint32_t kMisc = 20480;
     static constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
     static constexpr int kOut = TEX ? 3 : 1;
     static constexpr int kSkipDim = TEX ? kTexSkip : kGeoSkip;
@@ -107,10 +107,10 @@ constexpr int kTexItems = items(8, true);      // 108
 
 struct Misc {
     uint64_t full[kMaxStages], empty[kMaxStages];
-    uint64_t f_ready, h_ready, h_free, l1done[2], d2done, d3done, d4done, sd_ready[2];
+    uint64_t f_ready, h_ready, h_free, l1done[2], d2done, d3done, d4done, sd_ready[2], skip_free, d4_free;
     uint32_t tmem_base;
-    float z[kMaxNP];
-    float pos[kMaxNP][3];
+    float z[2][kMaxNP];       // by tile parity (the next tile is gathered before this one's final layer)
+    float pos[2][kMaxNP][3];
     float red[4][3][kMaxNP];      // final layer: per-lane-quarter partial sums over features
     float skipdot[2][3][kMaxNP];  // final layer: skip-input dots (leader, all points), by tile parity
     float sdl[3][kMaxNP / 2];     // texture: this CTA's Phi-part skip dots until h3 is known
@@ -161,6 +161,63 @@ __device__ __forceinline__ float warp_transpose_reduce(float* v) {
     return v[0];
 }
 
+// 8x8 transpose inside each 8-lane group: lane i of a group holds one feature (8g + i) for 32
+// points; afterwards it holds all 8 features of the group, as bf16 hi (and lo) 16-byte rows, for
+// points 8u + i (u = 0..3).  Three butterfly rounds swap point-index bits with lane bits.
+template <bool LO>
+__device__ __forceinline__ void transpose8_bf16(const float* v, uint4* hi, uint4* lo) {
+    const int lane = threadIdx.x & 31;
+    const bool i0 = lane & 1, i1 = lane & 2, i2 = lane & 4;
+    // round 0 (fp32): keep points q with q0 == i0; pack the two features as bf16x2 (lower feature first)
+    uint32_t wh[16], wl[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const float keep = i0 ? v[2 * m + 1] : v[2 * m];
+        const float send = i0 ? v[2 * m] : v[2 * m + 1];
+        const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+        const float a = i0 ? recv : keep, b = i0 ? keep : recv;
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+        wh[m] = *reinterpret_cast<uint32_t*>(&h2);
+        if (LO) {
+            __nv_bfloat162 l2 =
+                __floats2bfloat162_rn(a - __uint_as_float(wh[m] << 16), b - __uint_as_float(wh[m] & 0xFFFF0000u));
+            wl[m] = *reinterpret_cast<uint32_t*>(&l2);
+        }
+    }
+    // round 1: words m (point 2m + i0); keep m with m0 == i1 -> 2 words (features 0-3 of the half-group)
+    uint32_t xh[8][2], xl[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t kh = i1 ? wh[2 * j + 1] : wh[2 * j], sh = i1 ? wh[2 * j] : wh[2 * j + 1];
+        const uint32_t rh = __shfl_xor_sync(0xffffffffu, sh, 2);
+        xh[j][0] = i1 ? rh : kh;
+        xh[j][1] = i1 ? kh : rh;
+        if (LO) {
+            const uint32_t kl = i1 ? wl[2 * j + 1] : wl[2 * j], sl = i1 ? wl[2 * j] : wl[2 * j + 1];
+            const uint32_t rl = __shfl_xor_sync(0xffffffffu, sl, 2);
+            xl[j][0] = i1 ? rl : kl;
+            xl[j][1] = i1 ? kl : rl;
+        }
+    }
+    // round 2: words j (point 4j + 2 i1 + i0); keep j with j0 == i2 -> 4 words = 8 features
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        uint32_t k0 = i2 ? xh[2 * u + 1][0] : xh[2 * u][0], k1 = i2 ? xh[2 * u + 1][1] : xh[2 * u][1];
+        uint32_t s0 = i2 ? xh[2 * u][0] : xh[2 * u + 1][0], s1 = i2 ? xh[2 * u][1] : xh[2 * u + 1][1];
+        uint32_t r0 = __shfl_xor_sync(0xffffffffu, s0, 4), r1 = __shfl_xor_sync(0xffffffffu, s1, 4);
+        hi[u] = i2 ? make_uint4(r0, r1, k0, k1) : make_uint4(k0, k1, r0, r1);
+        if (LO) {
+            k0 = i2 ? xl[2 * u + 1][0] : xl[2 * u][0];
+            k1 = i2 ? xl[2 * u + 1][1] : xl[2 * u][1];
+            s0 = i2 ? xl[2 * u][0] : xl[2 * u + 1][0];
+            s1 = i2 ? xl[2 * u][1] : xl[2 * u + 1][1];
+            r0 = __shfl_xor_sync(0xffffffffu, s0, 4);
+            r1 = __shfl_xor_sync(0xffffffffu, s1, 4);
+            lo[u] = i2 ? make_uint4(r0, r1, k0, k1) : make_uint4(k0, k1, r0, r1);
+        }
+    }
+}
+
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
 
 template <bool TEX>
@@ -204,6 +261,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::mbar_init(&ms.d4done, 1);
         ptx::mbar_init(&ms.sd_ready[0], NPC);
         ptx::mbar_init(&ms.sd_ready[1], NPC);
+        ptx::mbar_init(&ms.skip_free, 1);
+        ptx::mbar_init(&ms.d4_free, kEpiThreads);
         ptx::fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -314,13 +373,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             auto skipk = [&](int j) { return skip_hi + j * kChunk; };
             auto skipl = [&](int j) { return skip_lo + j * kChunk; };
             // TMEM columns: D2[m] = m*NP, BUF[b] = 2NP + b*NP, D3 = BUF[0], D4 = D2[0]
-            auto body = [&](int ks, bool with_l4) {
+            uint32_t d4fph = 0;
+            auto body = [&](int ks, bool with_l4, bool wait_d4) {
                 auto L1 = [&](int c) {
                     for (int j = 0; j < ks; ++j) item(2 * NP + (c & 1) * NP, skipk(j), skipl(j), j > 0);
                     ptx::mma_commit_pair(&ms.l1done[c & 1], both);
                 };
                 L1(0);
                 L1(1);
+                if (wait_d4) {  // D2[0] doubles as the previous tile's D4: its final layer must have read it
+                    ptx::mbar_wait(&ms.d4_free, d4fph);
+                    d4fph ^= 1;
+                    ptx::tc_fence_after();
+                }
                 for (int m = 0; m < 2; ++m)
                     for (int j = 0; j < ks; ++j) item(m * NP, skipk(j), skipl(j), j > 0);
                 for (int c = 0; c < 4; ++c) {
@@ -340,6 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mma_commit_pair(&ms.d3done, both);
                 if (with_l4) {
                     for (int j = 0; j < ks; ++j) item(0, skipk(j), skipl(j), j > 0);
+                    ptx::mma_commit_pair(&ms.skip_free, both);  // last reader of the skip operand
                     wait_h();
                     for (int jj = 0; jj < 4; ++jj) item(0, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
                     ptx::mma_commit_pair(&ms.h_free, both);
@@ -357,11 +423,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 fph ^= 1;
                 ptx::tc_fence_after();
+                const bool later = t != pair_id;
                 if (TEX) {
-                    body(4, false);
-                    body(8, true);
+                    body(4, false, later);
+                    body(8, true, false);
                 } else {
-                    body(4, true);
+                    body(4, true, later);
                 }
             }
             if (tr) {
@@ -379,63 +446,89 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int colh = (warp - 2) >> 2;  // point half this warp converts = destination CTA
         const int row = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(colh * NPC);
-        uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hfph = 1, sdph[2] = {0, 0};
+        uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hfph = 1, sdph[2] = {0, 0}, sfph = 0;
         unsigned tile_iter = 0;
+        const float* zc = ms.z[0];  // z of the tile being converted
         const FieldDev& f = P.f;
         const bool odd = lane & 1;
         // this thread's feature inside a 256-row block, and its K position in the next layer's operand
         const uint32_t feat = rank * 128u + (uint32_t)row;
         const uint32_t kc_off = (feat >> 6) * kChunk;
-        const uint32_t kk = (feat & 63u) & ~1u;
+        const uint32_t c16 = (feat & 63u) >> 3;  // 16-byte chunk of this lane group's 8 features
         const uint32_t hdst = ptx::mapa(ptx::smem_u32(hbuf), (uint32_t)colh);  // h buffer of the owning CTA
         const uint32_t sdst = ptx::mapa(ptx::smem_u32(skip) + 4 * kChunk, (uint32_t)colh);  // texture: h3 -> skip
 
+        const bool etr = P.trace && blockIdx.x == 0 && et == 0;
+        unsigned long long e_acc = 0, e_hf = 0, e_emit = 0, e_t0 = 0, e_begin = gtime();
+        unsigned long long e_cyc[3] = {0, 0, 0};
         // TMEM columns [col, col + NPC) of this thread's lane -> next layer's operand in the owning CTA
         auto emit_block = [&](uint32_t col, const float* bias_blk, int out_dim, int feat0, uint32_t dst,
                               uint32_t lo_off, bool write_lo) {
             const int o = feat0 + (int)feat;
             const float bo = __ldg(&bias_blk[o]);
             const float wz = __ldg(&bias_blk[out_dim + o]);
+            unsigned long long c0 = etr ? clock64() : 0;
 #pragma unroll
             for (int hf = 0; hf < NPC / 32; ++hf) {
                 uint32_t r[32];
                 ptx::tmem_ld32(lane_base + col + hf * 32, r);
                 ptx::tmem_ld_wait();
+                if (etr) {
+                    const unsigned long long c1 = clock64();
+                    e_cyc[0] += c1 - c0;
+                    c0 = c1;
+                }
+                float v[32];
 #pragma unroll
-                for (int q = 0; q < 32; q += 2) {
-                    const int pl = hf * 32 + q;    // point within the destination CTA
-                    const int p = colh * NPC + pl;  // point within the pair tile
-                    float v0 = __uint_as_float(r[q]) + fmaf(wz, ms.z[p], bo);
-                    float v1 = __uint_as_float(r[q + 1]) + fmaf(wz, ms.z[p + 1], bo);
-                    v0 = v0 < 0.0f ? v0 * P.slope : v0;
-                    v1 = v1 < 0.0f ? v1 * P.slope : v1;
-                    const float send = odd ? v0 : v1;
-                    const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-                    const float a = odd ? recv : v0;
-                    const float b = odd ? v1 : recv;
-                    const uint32_t off = kc_off + sw128((uint32_t)(pl + (odd ? 1 : 0)), kk);
-                    const uint32_t hv = pack_bf16(a, b);
-                    ptx::st_cluster_u32(dst + off, hv);
-                    if (write_lo) {
-                        const float ah = __uint_as_float(hv << 16), bh = __uint_as_float(hv & 0xFFFF0000u);
-                        ptx::st_cluster_u32(dst + lo_off + off, pack_bf16(a - ah, b - bh));
-                    }
+                for (int q = 0; q < 32; ++q) {
+                    const float x = __uint_as_float(r[q]) + fmaf(wz, zc[colh * NPC + hf * 32 + q], bo);
+                    v[q] = x < 0.0f ? x * P.slope : x;
+                }
+                // rows (points) 8u + (lane & 7) of this hf block, 16-byte chunk of this lane group's 8 features
+                uint4 hv[4], lv[4];
+                if (write_lo)
+                    transpose8_bf16<true>(v, hv, lv);
+                else
+                    transpose8_bf16<false>(v, hv, lv);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t pl = (uint32_t)(hf * 32 + 8 * u + (lane & 7));
+                    const uint32_t off = kc_off + pl * 128u + (((c16 ^ pl) & 7u) << 4);
+                    ptx::st_cluster_v4(dst + off, hv[u]);
+                    if (write_lo) ptx::st_cluster_v4(dst + lo_off + off, lv[u]);
+                }
+                if (etr) {
+                    const unsigned long long c1 = clock64();
+                    e_cyc[1] += c1 - c0;
+                    c0 = c1;
                 }
             }
         };
         auto h_begin = [&]() {
+            const unsigned long long t0 = etr ? gtime() : 0;
             ptx::mbar_wait(&ms.h_free, hfph);
             hfph ^= 1;
+            if (etr) {
+                e_t0 = gtime();
+                e_hf += e_t0 - t0;
+            }
         };
         auto h_end = [&]() {
+            const unsigned long long c0 = etr ? clock64() : 0;
             ptx::fence_proxy_async_cluster();
             ptx::tc_fence_before();
             ptx::mbar_arrive_cluster(h_ready0);
+            if (etr) {
+                e_cyc[2] += clock64() - c0;
+                e_emit += gtime() - e_t0;
+            }
         };
         auto wait_acc = [&](uint64_t* bar, uint32_t& par) {
+            const unsigned long long t0 = etr ? gtime() : 0;
             ptx::mbar_wait(bar, par);
             par ^= 1;
             ptx::tc_fence_after();
+            if (etr) e_acc += gtime() - t0;
         };
         // epilogue of one MLP body (layers 1-3); `after_l1c0` runs once layer-1 chunk 0 is done
         auto body_epi = [&](const float* bias, bool prefix, auto&& after_l1c0) {
@@ -469,16 +562,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float* b5 = b4 + 2 * 128;
         constexpr int wl_stride = 128 + C::kSkipDim;
 
-        for (unsigned t = pair_id; t < ntiles; t += npairs) {
-            const unsigned base = t * NP;
-            const int tp = (int)(tile_iter & 1u);
+        // positions + Phi gather of pair tile tg into the skip operand (parity gb buffers)
+        auto gather_tile = [&](unsigned tg, int gb) {
             // ---- positions of all points of the pair tile (every CTA needs z for its epilogue) ----
             if (et < NP) {
-                const unsigned idx = base + et;
+                const unsigned idx = tg * NP + et;
                 double pd[3] = {0.0, 0.0, 0.0};
                 if (idx < n) job_point_d(job, idx, pd);
-                for (int d = 0; d < 3; ++d) ms.pos[et][d] = (float)pd[d];
-                ms.z[et] = (float)pd[2];
+                for (int d = 0; d < 3; ++d) ms.pos[gb][et][d] = (float)pd[d];
+                ms.z[gb][et] = (float)pd[2];
             }
             epi_bar();
             // ---- gather Phi for this CTA's points into its skip operand ----
@@ -502,8 +594,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         const int p = (int)rank * NPC + ew * kPerWarp + it * 2 + j;
-                        float u = (ms.pos[p][0] + 1.0f) * 0.5f * (float)(f.W - 1);
-                        float v = (1.0f - ms.pos[p][1]) * 0.5f * (float)(f.H - 1);
+                        float u = (ms.pos[gb][p][0] + 1.0f) * 0.5f * (float)(f.W - 1);
+                        float v = (1.0f - ms.pos[gb][p][1]) * 0.5f * (float)(f.H - 1);
                         u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
                         v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
                         const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
@@ -563,10 +655,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             } else {
                                 const int p = (int)rank * NPC + pl;
                                 if (leader) {
-                                    ms.skipdot[tp][0][p] = dot[0];
+                                    ms.skipdot[gb][0][p] = dot[0];
                                 } else {
-                                    ptx::st_cluster_f32(ptx::mapa(ptx::smem_u32(&ms.skipdot[tp][0][p]), 0), dot[0]);
-                                    ptx::mbar_arrive_cluster(sd_ready0 + 8 * tp);
+                                    ptx::st_cluster_f32(ptx::mapa(ptx::smem_u32(&ms.skipdot[gb][0][p]), 0), dot[0]);
+                                    ptx::mbar_arrive_cluster(sd_ready0 + 8 * gb);
                                 }
                             }
                         }
@@ -575,13 +667,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             ptx::fence_proxy_async_cluster();
             ptx::mbar_arrive_cluster(f_ready0);
+        };
+
+        gather_tile(pair_id, 0);
+        for (unsigned t = pair_id; t < ntiles; t += npairs) {
+            const unsigned base = t * NP;
+            const int tp = (int)(tile_iter & 1u);
+            zc = ms.z[tp];
             // constant part of the final logits, b5 + w5z*z (- sdf_scale*sdf(P) for geometry), off the
             // MMA critical path: the tensor cores are busy with layer 1 now
             if (leader && et < NP) {
                 float extra = 0.0f;
-                if (!TEX) extra = -__ldg(&f.fscene->sdf_scale) * scene_sdf_f(f.fscene, ms.pos[et]);
+                if (!TEX) extra = -__ldg(&f.fscene->sdf_scale) * scene_sdf_f(f.fscene, ms.pos[tp][et]);
                 for (int c = 0; c < NOUT; ++c)
-                    ms.cterm[c][et] = __ldg(&b5[c]) + __ldg(&P.wlast[c * wl_stride + wl_stride - 1]) * ms.z[et] + extra;
+                    ms.cterm[c][et] = __ldg(&b5[c]) + __ldg(&P.wlast[c * wl_stride + wl_stride - 1]) * ms.z[tp][et] + extra;
             }
 
             if (TEX) {
@@ -628,6 +727,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             } else {
                 body_epi(P.bias_g, false, [] {});
             }
+            // the next tile's gather overlaps this tile's last MMAs and final layer
+            if (t + npairs < ntiles) {
+                ptx::mbar_wait(&ms.skip_free, sfph);
+                sfph ^= 1;
+                gather_tile(t + npairs, tp ^ 1);
+            }
             wait_acc(&ms.d4done, d4ph);
             // ---- final layer (CTA 0 holds layer-4 rows 0..127 for all points) ----
             if (leader) {
@@ -643,7 +748,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     float hx[32];
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
-                        const float x = __uint_as_float(r[q]) + fmaf(wz, ms.z[colh * NPC + hf * 32 + q], bo);
+                        const float x = __uint_as_float(r[q]) + fmaf(wz, zc[colh * NPC + hf * 32 + q], bo);
                         hx[q] = x < 0.0f ? x * P.slope : x;
                     }
 #pragma unroll
@@ -681,9 +786,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+                ptx::mbar_arrive(&ms.d4_free);  // D4 and this tile's skip dots consumed
             }
             epi_bar();
             ++tile_iter;
+        }
+        if (etr) {
+            P.trace[4] = gtime() - e_begin;
+            P.trace[5] = e_acc;
+            P.trace[6] = e_hf;
+            P.trace[7] = e_emit;
+            P.trace[8] = e_cyc[0];
+            P.trace[9] = e_cyc[1];
+            P.trace[10] = e_cyc[2];
         }
     }
     ptx::tc_fence_before();
@@ -806,8 +921,12 @@ static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, uns
     if (p.trace) {
         cudaStreamSynchronize(s);
         const unsigned long long* t = p.trace;
-        fprintf(stderr, "[pair-trace %s] mma: total %.1f us, wait data %.1f, wait h %.1f, wait f %.1f\n",
-                TEX ? "tex" : "geo", t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3);
+        fprintf(stderr,
+                "[pair-trace %s] mma: total %.1f us, wait data %.1f, wait h %.1f, wait f %.1f | epi: total %.1f, wait acc "
+                "%.1f, wait hfree %.1f, emit %.1f\n",
+                TEX ? "tex" : "geo", t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3,
+                t[6] * 1e-3, t[7] * 1e-3);
+        fprintf(stderr, "    epi cycles: tmem-ld %llu, convert+store %llu, fence+arrive %llu\n", t[8], t[9], t[10]);
     }
     return ICG_OK;
 }
