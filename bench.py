@@ -287,17 +287,13 @@ def main():
     def flush_l2():
         ctx.memcpy(flush_b, flush_a, 320 << 20, abi.ICG_MEM_DEVICE, abi.ICG_MEM_DEVICE)
 
+    from paper_2007_13988_b200 import shard
+
     def barrier():
-        if dist:
-            dist.barrier()
+        shard.barrier()
 
     def allmax(x: float) -> float:
-        if not dist:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return shard.allmax(x, device=f"cuda:{local_rank}" if dist else None)
 
     # ---- warm-up ----
     for s in range(args.warmup):
@@ -344,7 +340,7 @@ def main():
     achieved = prof["geo_points"] * GEO_FLOP_PER_POINT / geo_s / 1e12 if geo_s > 0 else 0.0
     peak_t = pk.get("bf16_tflops_sustained", 1385.7)
     executed_mult = 3 if prec_name == "fp32" else 1
-    roofline = {"bound": "tensor", "kernel": "k_mlp_tc<64> (fused geometry MLP)", "achieved": achieved,
+    roofline = {"bound": "tensor", "kernel": "geometry MLP: k_mlp_pair<0> (CTA-pair tcgen05) + k_lp (latency path), all launches", "achieved": achieved,
                 "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t, "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" + (" (fallback)" if pk.get("fallback") else ""),
                 "algorithmic_flop_per_point": GEO_FLOP_PER_POINT,
