@@ -117,6 +117,9 @@ def ref() -> C.CDLL:
             raise ImportError(f"reference shim not built: {REF_PATH}")
         lib = C.CDLL(REF_PATH)
         lib.ref_last_error.restype = C.c_char_p
+        lib.ref_write_ppm.argtypes = [C.c_char_p, C.c_int, C.c_int, f64p]
+        lib.ref_write_float_map.argtypes = [C.c_char_p, C.c_int, C.c_int, f64p]
+        lib.ref_dump_grid.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_float)]
         lib.ref_extract.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.c_int, f32p, u8p, u8p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                     C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_double)]

@@ -10,6 +10,7 @@
 //   grid primitives ......................................... grid.hpp:87-197
 //   Rng ..................................................... random.hpp:16-43
 //   scene JSON loading ...................................... scene.hpp:302-333
+//   output formats (PPM, float map, grid dump) .............. image.hpp:18-48, grid.hpp:199-222
 // with the field supplied as a C callback wrapped in the reference's own
 // FieldOracle (field.hpp:22-77), so the reference's call counter and
 // parallel_for drive evaluation exactly as they do in the reference.
@@ -21,6 +22,7 @@
 
 #include "isocull/field.hpp"
 #include "isocull/grid.hpp"
+#include "isocull/image.hpp"
 #include "isocull/localize.hpp"
 #include "isocull/random.hpp"
 #include "isocull/render.hpp"
@@ -295,6 +297,42 @@ void ref_rng_uniforms(uint64_t seed, std::size_t n, double* out) {
 void ref_rng_normals(uint64_t seed, std::size_t n, double* out) {
     Rng r(seed);
     for (std::size_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+
+// ---- output formats (image.hpp, grid.hpp) ----------------------------------------
+int ref_write_ppm(const char* path, int w, int h, const double* rgb) {
+    try {
+        std::vector<Vec3> px((std::size_t)w * h);
+        for (std::size_t i = 0; i < px.size(); ++i) px[i] = Vec3{rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+        write_ppm(path, w, h, px);
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, ICG_EINVAL);
+    } catch (const std::exception& e) {
+        return fail(e, ICG_ERUNTIME);
+    }
+}
+
+int ref_write_float_map(const char* path, int w, int h, const double* values) {
+    try {
+        write_float_map(path, w, h, std::span<const double>(values, (std::size_t)w * h));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, ICG_EINVAL);
+    } catch (const std::exception& e) {
+        return fail(e, ICG_ERUNTIME);
+    }
+}
+
+int ref_dump_grid(const char* path, int level, int cells, const float* values) {
+    try {
+        LevelGrid g = LevelGrid::make(level, cells, NodeState::evaluated);
+        std::memcpy(g.values.data(), values, g.values.size() * sizeof(float));
+        dump_grid(g, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, ICG_ERUNTIME);
+    }
 }
 
 }  // extern "C"

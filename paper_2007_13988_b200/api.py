@@ -405,6 +405,55 @@ def acceleration_factor(result: ExtractionResult, brute: ExtractionResult) -> fl
 
 
 # ---------------------------------------------------------------------------
+# Output formats (image.hpp:18-48, grid.hpp:199-222), byte-identical
+# ---------------------------------------------------------------------------
+def write_ppm(path: str, width: int, height: int, rgb) -> None:
+    """Binary P6, 8-bit; byte = lround(255 * clamp(v, 0, 1)) (image.hpp:18-33)."""
+    a = np.asarray(rgb, dtype=np.float64).reshape(-1)
+    if a.size != 3 * width * height:
+        raise ValueError("write_ppm: buffer size mismatch")
+    x = 255.0 * np.clip(a, 0.0, 1.0)
+    b = np.floor(x + 0.5).astype(np.uint8)  # lround for non-negative values (half away from zero)
+    with open(path, "wb") as f:
+        f.write(f"P6\n{width} {height}\n255\n".encode())
+        f.write(b.tobytes())
+
+
+def write_float_map(path: str, width: int, height: int, values) -> None:
+    """int32 width, height, then float32 values, little-endian (image.hpp:37-48)."""
+    a = np.asarray(values, dtype=np.float64).reshape(-1)
+    if a.size != width * height:
+        raise ValueError("write_float_map: buffer size mismatch")
+    with open(path, "wb") as f:
+        f.write(np.array([width, height], dtype="<i4").tobytes())
+        f.write(a.astype("<f4").tobytes())
+
+
+def dump_grid(path: str, level: int, cells: int, values) -> None:
+    """int32 level, int32 R, then float32 node values x-fastest (grid.hpp:199-209)."""
+    a = np.asarray(values, dtype=np.float32).reshape(-1)
+    if a.size != (cells + 1) ** 3:
+        raise ValueError("dump_grid: value count does not match (R+1)^3")
+    with open(path, "wb") as f:
+        f.write(np.array([level, cells], dtype="<i4").tobytes())
+        f.write(a.astype("<f4").tobytes())
+
+
+def load_grid_dump(path: str):
+    """Inverse of dump_grid (grid.hpp:211-222): returns (level, cells, values)."""
+    with open(path, "rb") as f:
+        hdr = f.read(8)
+        if len(hdr) < 8:
+            raise RuntimeError(f"load_grid_dump: short header in {path}")
+        level, cells = (int(v) for v in np.frombuffer(hdr, dtype="<i4"))
+        n = (cells + 1) ** 3
+        data = f.read(4 * n)
+        if len(data) < 4 * n:
+            raise RuntimeError(f"load_grid_dump: short data in {path}")
+    return level, cells, np.frombuffer(data, dtype="<f4").copy()
+
+
+# ---------------------------------------------------------------------------
 # Seeded synthetic inputs (host helpers in the library)
 # ---------------------------------------------------------------------------
 def gen_capsules(seed: int, n: int = 15) -> list:

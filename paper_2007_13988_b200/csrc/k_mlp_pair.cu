@@ -86,8 +86,8 @@ __host__ __device__ void schedule(int ks, bool with_l4, Emit&& emit) {
     for (int m = 0; m < 2; ++m)
         for (int j = 0; j < ks; ++j) emit(1, m, 1024 + j * 64);
     for (int c = 0; c < 4; ++c) {
-        for (int m = 0; m < 2; ++m)
-            for (int jj = 0; jj < 4; ++jj) emit(1, m, c * 256 + jj * 64);
+        for (int jj = 0; jj < 4; ++jj)  // jj-major: h halves (K chunks 0-1 / 2-3) are released in turn
+            for (int m = 0; m < 2; ++m) emit(1, m, c * 256 + jj * 64);
         if (c + 2 < 4) L1(c + 2);
     }
     for (int j = 0; j < ks; ++j) emit(2, 0, 512 + j * 64);
@@ -107,7 +107,7 @@ constexpr int kTexItems = items(8, true);      // 108
 
 struct Misc {
     uint64_t full[kMaxStages], empty[kMaxStages];
-    uint64_t f_ready, h_ready, h_free, l1done[2], d2done, d3done, d4done, sd_ready[2], skip_free, d4_free;
+    uint64_t f_ready, h_ready[2], h_free[2], l1done[2], d2done, d3done, d4done, sd_ready[2], skip_free, d4_free;
     uint32_t tmem_base;
     float z[2][kMaxNP];       // by tile parity (the next tile is gathered before this one's final layer)
     float pos[2][kMaxNP][3];
@@ -252,8 +252,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&ms.empty[s], 1);
         }
         ptx::mbar_init(&ms.f_ready, 2 * kEpiThreads);
-        ptx::mbar_init(&ms.h_ready, 2 * kEpiThreads);
-        ptx::mbar_init(&ms.h_free, 1);
+        // h buffer halves: K chunks 0-1 (features 0-127) are written by CTA 0, chunks 2-3 by CTA 1
+        ptx::mbar_init(&ms.h_ready[0], kEpiThreads);
+        ptx::mbar_init(&ms.h_ready[1], kEpiThreads);
+        ptx::mbar_init(&ms.h_free[0], 1);
+        ptx::mbar_init(&ms.h_free[1], 1);
         ptx::mbar_init(&ms.l1done[0], 1);
         ptx::mbar_init(&ms.l1done[1], 1);
         ptx::mbar_init(&ms.d2done, 1);
@@ -279,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // leader-CTA addresses of the barriers that receive cross-CTA traffic
     const uint32_t full0 = ptx::mapa(ptx::smem_u32(&ms.full[0]), 0);
     const uint32_t f_ready0 = ptx::mapa(ptx::smem_u32(&ms.f_ready), 0);
-    const uint32_t h_ready0 = ptx::mapa(ptx::smem_u32(&ms.h_ready), 0);
+    const uint32_t h_ready0 = ptx::mapa(ptx::smem_u32(&ms.h_ready[rank]), 0);  // this CTA's half
     const uint32_t sd_ready0 = ptx::mapa(ptx::smem_u32(&ms.sd_ready[0]), 0);
     const uint16_t both = 0x3;
 
@@ -314,7 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (leader && lane == 0) {
             const uint32_t idesc = ptx::idesc_bf16_f32(256, NP);
             int s = 0;
-            uint32_t ph = 0, fph = 0, hph = 0;
+            uint32_t ph = 0, fph = 0, hph[2] = {0, 0};
             const uint32_t skip_hi = ptx::smem_u32(skip), skip_lo = skip_hi + kSkipHalf;
             const uint32_t h_hi = ptx::smem_u32(hbuf), h_lo = h_hi + kHHalf;
             const uint32_t ring0 = ptx::smem_u32(ring);
@@ -363,12 +366,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     sub ^= 1;
                 }
             };
-            auto wait_h = [&]() {
+            auto wait_h = [&](int half) {
                 const unsigned long long t0 = tr ? gtime() : 0;
-                ptx::mbar_wait_cluster(&ms.h_ready, hph);
+                ptx::mbar_wait_cluster(&ms.h_ready[half], hph[half]);
                 if (tr) w_h += gtime() - t0;
-                hph ^= 1;
+                hph[half] ^= 1;
                 ptx::tc_fence_after();
+            };
+            // consume one h block (4 K chunks) for `nm` 256-row blocks, half by half
+            auto h_block = [&](int nm, uint32_t dcol0) {
+                for (int half = 0; half < 2; ++half) {
+                    wait_h(half);
+                    for (int jj = 2 * half; jj < 2 * half + 2; ++jj)
+                        for (int m = 0; m < nm; ++m)
+                            item(dcol0 + m * NP, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
+                    ptx::mma_commit_pair(&ms.h_free[half], both);
+                }
             };
             auto skipk = [&](int j) { return skip_hi + j * kChunk; };
             auto skipl = [&](int j) { return skip_lo + j * kChunk; };
@@ -389,30 +402,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int m = 0; m < 2; ++m)
                     for (int j = 0; j < ks; ++j) item(m * NP, skipk(j), skipl(j), j > 0);
                 for (int c = 0; c < 4; ++c) {
-                    wait_h();
-                    for (int m = 0; m < 2; ++m)
-                        for (int jj = 0; jj < 4; ++jj) item(m * NP, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
-                    ptx::mma_commit_pair(&ms.h_free, both);
+                    h_block(2, 0);
                     if (c + 2 < 4) L1(c + 2);
                 }
                 ptx::mma_commit_pair(&ms.d2done, both);
                 for (int j = 0; j < ks; ++j) item(2 * NP, skipk(j), skipl(j), j > 0);
-                for (int c = 0; c < 2; ++c) {
-                    wait_h();
-                    for (int jj = 0; jj < 4; ++jj) item(2 * NP, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
-                    ptx::mma_commit_pair(&ms.h_free, both);
-                }
+                for (int c = 0; c < 2; ++c) h_block(1, 2 * NP);
                 ptx::mma_commit_pair(&ms.d3done, both);
                 if (with_l4) {
                     for (int j = 0; j < ks; ++j) item(0, skipk(j), skipl(j), j > 0);
                     ptx::mma_commit_pair(&ms.skip_free, both);  // last reader of the skip operand
-                    wait_h();
-                    for (int jj = 0; jj < 4; ++jj) item(0, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
-                    ptx::mma_commit_pair(&ms.h_free, both);
+                    h_block(1, 0);
                     ptx::mma_commit_pair(&ms.d4done, both);
                 } else {
-                    wait_h();  // prefix: h3 is in the skip operands of both CTAs
-                    ptx::mma_commit_pair(&ms.h_free, both);
+                    // prefix: h3 is in the skip operands of both CTAs
+                    for (int half = 0; half < 2; ++half) {
+                        wait_h(half);
+                        ptx::mma_commit_pair(&ms.h_free[half], both);
+                    }
                 }
             };
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
@@ -506,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         };
         auto h_begin = [&]() {
             const unsigned long long t0 = etr ? gtime() : 0;
-            ptx::mbar_wait(&ms.h_free, hfph);
+            ptx::mbar_wait(&ms.h_free[rank], hfph);
             hfph ^= 1;
             if (etr) {
                 e_t0 = gtime();
