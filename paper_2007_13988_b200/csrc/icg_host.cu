@@ -175,7 +175,8 @@ int ensure_grid(icg_context* c, int cells) {
     if (int r = c->tentbin.ensure(words(N) * 4 + 16)) return r;
     if (int r = c->sel.ensure(words(N) * 4 + 16)) return r;
     if (int r = c->queued.ensure(words(N) * 4 + 16)) return r;
-    if (int r = c->block_counts.ensure((N / 1024 + 2) * 4)) return r;
+    const size_t fn = (size_t)cells + 1;  // row counts (fn^2) + per-1024 group sums
+    if (int r = c->block_counts.ensure((fn * fn + fn * fn / 1024 + 64) * 4)) return r;
     if (int r = c->list_e0.ensure(N * 4)) return r;
     return ICG_OK;
 }

@@ -20,6 +20,8 @@
 // reference by tests/test_gpu_parity.py.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "icg_internal.h"
 
 namespace icg {
@@ -62,8 +64,15 @@ __global__ void k_mixed_cells(const uint32_t* __restrict__ cbin, int rc, uint32_
     }
 }
 
-// ---- fine pass: tent / carry / tentbin / selection + block counts ---------
-constexpr int kClassifyBlock = 1024;
+// ---- fine pass: one WARP per fine row (j, k) ----------------------------------
+// The row's parent information is staged per warp in shared memory as aligned
+// bit rows: the (1, 2 or 4) coarse binarised rows (jj, kk) it interpolates
+// from, and the OR of the (1..4) adjacent rows of mixed coarse cells.  A node
+// then costs a handful of shared-memory bit tests; all index math is 32-bit.
+// Values/states are stored coalesced along x; the flat tentbin / sel words
+// (rows are not word-aligned) are merged with atomicOr (buffers cleared first).
+constexpr int kFineThreads = 256;
+constexpr int kRowWords = 17;  // >= (cn + 32) / 32 for cn <= 513
 
 __device__ __forceinline__ void adjacent_cells(int i, int rc, int& lo, int& hi) {
     if (i & 1) {
@@ -76,76 +85,122 @@ __device__ __forceinline__ void adjacent_cells(int i, int rc, int& lo, int& hi) 
     }
 }
 
-__global__ void __launch_bounds__(kClassifyBlock)
-k_fine_classify(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const uint32_t* __restrict__ cbin,
-                const uint32_t* __restrict__ mixed, int rc, float* __restrict__ fv, uint8_t* __restrict__ fs,
-                uint32_t* __restrict__ tentbin, uint32_t* __restrict__ sel, uint32_t* __restrict__ block_counts) {
-    __shared__ unsigned warp_counts[kClassifyBlock / 32];
-    const unsigned fn = 2u * rc + 1u, cn = rc + 1u;
-    const unsigned nf = fn * fn * fn;
-    const unsigned idx = blockIdx.x * kClassifyBlock + threadIdx.x;
-    bool tb = false, s = false;
-    if (idx < nf) {
-        const unsigned jk = idx / fn;
-        int i = (int)(idx - jk * fn);
-        int k = (int)(jk / fn);
-        int j = (int)(jk - (unsigned)k * fn);
-        int i0 = i >> 1, i1 = (i + 1) >> 1, j0 = j >> 1, j1 = (j + 1) >> 1, k0 = k >> 1, k1 = (k + 1) >> 1;
-        float v;
-        uint8_t st;
-        if (i0 == i1 && j0 == j1 && k0 == k1) {
-            // even node: carry the coarse scalar and state (carry_scalars, localize.hpp:116-119)
-            unsigned ci = (unsigned)i0 + cn * ((unsigned)j0 + cn * (unsigned)k0);
-            v = cv[ci];
-            st = cs[ci];
-            tb = test_bit(cbin, ci);
-        } else {
-            // mean of the binarised parents (upsample_interpolate, grid.hpp:106-115)
-            int ones = 0, cnt = 0;
-            for (int kk = k0; kk <= k1; ++kk)
-                for (int jj = j0; jj <= j1; ++jj)
-                    for (int ii = i0; ii <= i1; ++ii) {
-                        ones += test_bit(cbin, (unsigned)ii + cn * ((unsigned)jj + cn * (unsigned)kk));
-                        ++cnt;
-                    }
-            v = (float)ones / (float)cnt;  // exact dyadic; equals (float)(double sum / cnt)
-            st = ICG_STATE_INTERPOLATED;
-            tb = 2 * ones >= cnt;          // tent >= 0.5f
-        }
-        fv[idx] = v;
-        fs[idx] = st;
-        // dilate_1ring(boundary_candidates(tent)) via adjacent mixed coarse cells
-        int xl, xh, yl, yh, zl, zh;
-        adjacent_cells(i, rc, xl, xh);
+// word w of the bit row starting at flat bit `base` of g
+__device__ __forceinline__ uint32_t row_word(const uint32_t* __restrict__ g, uint32_t base, int w) {
+    const uint32_t b = base + 32u * (uint32_t)w, q = b >> 5, r = b & 31u;
+    const uint32_t lo = __ldg(&g[q]);
+    return r ? __funnelshift_r(lo, __ldg(&g[q + 1]), r) : lo;
+}
+
+__device__ __forceinline__ uint32_t sbit(const uint32_t* row, int i) { return (row[i >> 5] >> (i & 31)) & 1u; }
+
+__global__ void __launch_bounds__(kFineThreads)
+k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const uint32_t* __restrict__ cbin,
+            const uint32_t* __restrict__ mixed, int rc, float* __restrict__ fv, uint8_t* __restrict__ fs,
+            uint32_t* __restrict__ tentbin, uint32_t* __restrict__ sel) {
+    __shared__ uint32_t prow[kFineThreads / 32][4][kRowWords];
+    __shared__ uint32_t mrow[kFineThreads / 32][kRowWords];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int fn = 2 * rc + 1, cn = rc + 1;
+    const uint32_t nrows_total = (uint32_t)fn * (uint32_t)fn;
+    const int cwords = (cn + 31) >> 5, mwords = (rc + 31) >> 5;
+    uint32_t(*pr)[kRowWords] = prow[wl];
+    uint32_t* mr = mrow[wl];
+    for (uint32_t row = blockIdx.x * (kFineThreads / 32) + wl; row < nrows_total; row += gridDim.x * (kFineThreads / 32)) {
+        const int k = (int)(row / (uint32_t)fn), j = (int)(row - (uint32_t)k * fn);
+        const int j0 = j >> 1, j1 = (j + 1) >> 1, k0 = k >> 1, k1 = (k + 1) >> 1;
+        const int nj = 1 + (j1 != j0), nk = 1 + (k1 != k0), npr = nj * nk;
+        int yl, yh, zl, zh;
         adjacent_cells(j, rc, yl, yh);
         adjacent_cells(k, rc, zl, zh);
-        bool flagged = false;
-        for (int cz = zl; cz <= zh && !flagged; ++cz)
-            for (int cy = yl; cy <= yh && !flagged; ++cy)
-                for (int cx = xl; cx <= xh && !flagged; ++cx)
-                    flagged = test_bit(mixed, (unsigned)cx + (unsigned)rc * ((unsigned)cy + (unsigned)rc * (unsigned)cz));
-        s = flagged && st != ICG_STATE_EVALUATED;  // mask_to_unevaluated_list, localize.hpp:127
-    }
-    unsigned tbw = __ballot_sync(0xffffffffu, tb);
-    unsigned sw = __ballot_sync(0xffffffffu, s);
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        if (idx < nf) {
-            tentbin[idx >> 5] = tbw;
-            sel[idx >> 5] = sw;
+        __syncwarp();
+        // stage: parent rows r = (jj - j0) + nj * (kk - k0), and the OR of the adjacent mixed rows
+        for (int t = lane; t < 4 * cwords; t += 32) {
+            const int r = t / cwords, w = t - r * cwords;
+            if (r < npr) {
+                const int jj = j0 + r % nj, kk = k0 + r / nj;
+                pr[r][w] = row_word(cbin, (uint32_t)cn * ((uint32_t)jj + (uint32_t)cn * (uint32_t)kk), w);
+            }
         }
-        warp_counts[warp] = __popc(sw);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        unsigned c = warp_counts[lane];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) block_counts[blockIdx.x] = c;
+        if (lane < mwords) {
+            uint32_t m = 0;
+            for (int cz = zl; cz <= zh; ++cz)
+                for (int cy = yl; cy <= yh; ++cy)
+                    m |= row_word(mixed, (uint32_t)rc * ((uint32_t)cy + (uint32_t)rc * (uint32_t)cz), lane);
+            mr[lane] = m;
+        }
+        __syncwarp();
+        const uint32_t rowbase = row * (uint32_t)fn;
+        const bool even_jk = !((j | k) & 1);
+        const uint32_t cbase = (uint32_t)cn * ((uint32_t)j0 + (uint32_t)cn * (uint32_t)k0);
+        for (int i0w = 0; i0w < fn; i0w += 32) {
+            const int i = i0w + lane;
+            bool tb = false, sl = false;
+            if (i < fn) {
+                const int i0 = i >> 1, i1 = (i + 1) >> 1;
+                float v;
+                uint8_t st;
+                if (even_jk && !(i & 1)) {
+                    // even node: carry the coarse scalar and state (carry_scalars, localize.hpp:116-119)
+                    v = cv[cbase + i0];
+                    st = cs[cbase + i0];
+                    tb = sbit(pr[0], i0);
+                } else {
+                    // mean of the binarised parents (upsample_interpolate, grid.hpp:106-115): exact dyadic
+                    int ones = 0;
+                    for (int r = 0; r < npr; ++r) ones += sbit(pr[r], i0) + (i1 != i0 ? sbit(pr[r], i1) : 0);
+                    const int cnt = npr * (1 + (i1 != i0));  // 1, 2, 4 or 8: the quotient is exact
+                    v = (float)ones * __int_as_float((127 - (31 - __clz(cnt))) << 23);
+                    st = ICG_STATE_INTERPOLATED;
+                    tb = 2 * ones >= cnt;  // tent >= 0.5f
+                }
+                fv[rowbase + i] = v;
+                fs[rowbase + i] = st;
+                int xl, xh;
+                adjacent_cells(i, rc, xl, xh);
+                const bool flagged = sbit(mr, xl) | sbit(mr, xh);  // dilate_1ring(boundary_candidates)
+                sl = flagged && st != ICG_STATE_EVALUATED;          // mask_to_unevaluated_list
+            }
+            const unsigned tbw = __ballot_sync(0xffffffffu, tb), sw = __ballot_sync(0xffffffffu, sl);
+            if (lane == 0) {
+                const uint32_t first = rowbase + (uint32_t)i0w, sh = first & 31u, w = first >> 5;
+                if (tbw) {
+                    atomicOr(&tentbin[w], tbw << sh);
+                    if (sh && (tbw >> (32 - sh))) atomicOr(&tentbin[w + 1], tbw >> (32 - sh));
+                }
+                if (sw) {
+                    atomicOr(&sel[w], sw << sh);
+                    if (sh && (sw >> (32 - sh))) atomicOr(&sel[w + 1], sw >> (32 - sh));
+                }
+            }
+        }
     }
 }
 
-// ---- exclusive scan of block counts (single block) ------------------------
+// per-CTA selection counts over the word partition used by k_write_words
+constexpr int kWordsPerCta = 2048;
+constexpr int kWriteThreads = 1024;
+
+__global__ void __launch_bounds__(kWriteThreads)
+k_count_words(const uint32_t* __restrict__ sel, unsigned nwords, uint32_t* __restrict__ counts) {
+    __shared__ unsigned warp_counts[kWriteThreads / 32];
+    unsigned c = 0;
+    for (unsigned w = blockIdx.x * kWordsPerCta + threadIdx.x; w < min(nwords, (blockIdx.x + 1) * kWordsPerCta);
+         w += kWriteThreads)
+        c += __popc(__ldg(&sel[w]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) warp_counts[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned v = warp_counts[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) counts[blockIdx.x] = v;
+    }
+}
+
+// ---- exclusive scan of the per-CTA counts (single block) -----------------------
 __global__ void __launch_bounds__(1024)
 k_scan_blocks(uint32_t* __restrict__ counts, unsigned nblocks, DevCounters* ctr, int level) {
     __shared__ unsigned warp_sums[32];
@@ -191,43 +246,72 @@ k_scan_blocks(uint32_t* __restrict__ counts, unsigned nblocks, DevCounters* ctr,
     }
 }
 
-// ---- write the ascending E0 list -----------------------------------------
-__global__ void __launch_bounds__(kClassifyBlock)
-k_write_list(const uint32_t* __restrict__ sel, size_t nf, const uint32_t* __restrict__ offsets,
-             uint32_t* __restrict__ list) {
-    __shared__ unsigned warp_off[kClassifyBlock / 32];
-    const size_t idx = (size_t)blockIdx.x * kClassifyBlock + threadIdx.x;
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned w = idx < nf ? sel[idx >> 5] : 0u;
-    if (idx >= nf) w = 0u;
-    if (lane == 0) warp_off[warp] = __popc(w);
+// ---- write the ascending E0 list: same CTA/word partition as k_fine_words -------
+__global__ void __launch_bounds__(kWriteThreads)
+k_write_words(const uint32_t* __restrict__ sel, unsigned long long nwords, const uint32_t* __restrict__ offsets,
+              uint32_t* __restrict__ list) {
+    __shared__ unsigned warp_sums[kWriteThreads / 32];
+    const unsigned long long wbeg = (unsigned long long)blockIdx.x * kWordsPerCta;
+    const int per = kWordsPerCta / kWriteThreads;  // consecutive words per thread
+    const unsigned long long w0 = wbeg + (unsigned long long)threadIdx.x * per;
+    uint32_t wv[kWordsPerCta / kWriteThreads];
+    unsigned c = 0;
+#pragma unroll
+    for (int q = 0; q < per; ++q) {
+        wv[q] = w0 + q < nwords ? __ldg(&sel[w0 + q]) : 0u;
+        c += __popc(wv[q]);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        unsigned c = warp_off[lane], x = c;
+        const unsigned w = warp_sums[lane];
+        unsigned ws = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const unsigned y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += y;
         }
-        warp_off[lane] = x - c;
+        warp_sums[lane] = ws - w;
     }
     __syncthreads();
-    if (idx < nf && ((w >> lane) & 1u)) {
-        unsigned pos = offsets[blockIdx.x] + warp_off[warp] + __popc(w & ((1u << lane) - 1u));
-        list[pos] = (uint32_t)idx;
+    unsigned pos = offsets[blockIdx.x] + warp_sums[warp] + x - c;
+#pragma unroll
+    for (int q = 0; q < per; ++q) {
+        uint32_t m = wv[q];
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            list[pos++] = (uint32_t)((w0 + q) * 32 + b);
+        }
     }
 }
 
 int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s) {
     const int rc = b.rc, cn = rc + 1, fn = 2 * rc + 1;
+    if (cn + 32 > 32 * kRowWords) {
+        set_error("level classify: grid too large");
+        return ICG_ERUNTIME;
+    }
     size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
+    const unsigned nwords = (unsigned)((nf + 31) / 32);
+    const unsigned nblocks = (nwords + kWordsPerCta - 1) / kWordsPerCta;
     k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
     k_mixed_cells<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(b.cbin, rc, b.mixed, &ctr->refined[level]);
-    unsigned nblocks = (unsigned)((nf + kClassifyBlock - 1) / kClassifyBlock);
-    k_fine_classify<<<nblocks, kClassifyBlock, 0, s>>>(b.cv, b.cs, b.cbin, b.mixed, rc, b.fv, b.fs, b.tentbin, b.sel,
-                                                       b.block_counts);
+    ICG_CUDA_TRY(cudaMemsetAsync(b.tentbin, 0, ((size_t)nwords + 1) * 4, s));
+    ICG_CUDA_TRY(cudaMemsetAsync(b.sel, 0, ((size_t)nwords + 1) * 4, s));
+    const unsigned rows = (unsigned)fn * fn;
+    const unsigned fine_blocks = std::min<unsigned>((rows + kFineThreads / 32 - 1) / (kFineThreads / 32), 148u * 8u);
+    k_fine_rows<<<fine_blocks, kFineThreads, 0, s>>>(b.cv, b.cs, b.cbin, b.mixed, rc, b.fv, b.fs, b.tentbin, b.sel);
+    k_count_words<<<nblocks, kWriteThreads, 0, s>>>(b.sel, nwords, b.block_counts);
     k_scan_blocks<<<1, 1024, 0, s>>>(b.block_counts, nblocks, ctr, level);
-    k_write_list<<<nblocks, kClassifyBlock, 0, s>>>(b.sel, nf, b.block_counts, b.list);
+    k_write_words<<<nblocks, kWriteThreads, 0, s>>>(b.sel, nwords, b.block_counts, b.list);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }

@@ -14,6 +14,13 @@
 // (oracle/isocull_oracle.c, -ffp-contract=off) reproduces each crossing index
 // bit-exactly.  Covered pixels append their world surface point to a compact
 // list consumed by the texture MLP.
+//
+// Speed without changing a single rounding: the per-pixel parts of
+// view_to_world (x/scale, y/scale and the first two products of each row) and
+// the view depth of every sample (1 - 2k/R, a shared table) are computed once,
+// and a warp walks one ray 32 samples at a time (coalesced corner loads).
+#include <algorithm>
+
 #include "eval_common.cuh"
 
 namespace icg {
@@ -49,80 +56,121 @@ __device__ __forceinline__ void view_to_world_d(const RenderJob& r, double x, do
     w[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[2], v0), __dmul_rn(m[5], v1)), __dmul_rn(m[8], v2));
 }
 
-__global__ void __launch_bounds__(256) k_render(RenderJob r) {
+constexpr int kMaxRenderCells = 1024;
+constexpr int kRenderThreads = 256;
+
+// One WARP per pixel ray: lane l evaluates sample k = kb + l of the current
+// 32-sample chunk.  Consecutive samples sit one cell apart along the ray, so
+// the lanes' corner loads are spatially coherent (fully coalesced when the ray
+// runs along the x-fastest memory axis, as for yaw 90).  The first crossing is
+// the lowest lane whose value is >= 0.5f (ballot); every value is computed with
+// the same operations as the per-thread formulation, so results are unchanged.
+__global__ void __launch_bounds__(kRenderThreads) k_render(RenderJob r) {
+    __shared__ double vz_tab[kMaxRenderCells + 1];
     const int W = r.width, H = r.height, R = r.cells;
-    size_t npx = (size_t)W * H;
-    size_t px = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool covered = false, degenerate = false, grazing = false;
-    if (px < npx) {
-        int col = (int)(px % W), row = (int)(px / W);
-        double vx = __dadd_rn(-1.0, __ddiv_rn(__dmul_rn(2.0, (double)col), (double)(W - 1)));
-        double vy = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)row), (double)(H - 1)));
-        double hr = __dmul_rn(0.5, (double)R);
+    for (int k = threadIdx.x; k <= R; k += blockDim.x)
+        vz_tab[k] = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)k), (double)R));
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const size_t npx = (size_t)W * H;
+    const size_t nwarps = (size_t)gridDim.x * (kRenderThreads / 32);
+    unsigned long long n_cov = 0, n_deg = 0, n_graz = 0;
+    const double* m = r.rot;
+    const double hr = __dmul_rn(0.5, (double)R);
+    const float fR = (float)R;
+    for (size_t px = (size_t)blockIdx.x * (kRenderThreads / 32) + (threadIdx.x >> 5); px < npx; px += nwarps) {
+        const int col = (int)(px % W), row = (int)(px / W);
+        const double vx = __dadd_rn(-1.0, __ddiv_rn(__dmul_rn(2.0, (double)col), (double)(W - 1)));
+        const double vy = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)row), (double)(H - 1)));
+        // view_to_world (render.hpp:29-32) with the per-pixel terms hoisted (same operations, same order)
+        const double v0 = __dsub_rn(__ddiv_rn(vx, r.scale), r.trans[0]);
+        const double v1 = __dsub_rn(__ddiv_rn(vy, r.scale), r.trans[1]);
+        const double c0 = __dadd_rn(__dmul_rn(m[0], v0), __dmul_rn(m[3], v1));
+        const double c1 = __dadd_rn(__dmul_rn(m[1], v0), __dmul_rn(m[4], v1));
+        const double c2 = __dadd_rn(__dmul_rn(m[2], v0), __dmul_rn(m[5], v1));
         int k1 = -1;
-        float vprev = 0.0f, vhit = 0.0f;
-        for (int k = 0; k <= R; ++k) {
-            double vz = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)k), (double)R));
-            double w[3];
-            view_to_world_d(r, vx, vy, vz, w);
-            float gx = (float)__dmul_rn(__dadd_rn(w[0], 1.0), hr);
-            float gy = (float)__dmul_rn(__dadd_rn(w[1], 1.0), hr);
-            float gk = (float)__dmul_rn(__dsub_rn(1.0, w[2]), hr);
-            float v = sample_grid(r.values, R, gx, gy, gk);
-            if (v >= 0.5f) {
-                k1 = k;
-                vhit = v;
+        float vprev = 0.0f, vhit = 0.0f, last = 0.0f;
+        bool grazing = false;
+        for (int kb = 0; kb <= R; kb += 32) {
+            const int k = kb + lane;
+            float v = 0.0f;
+            if (k <= R) {
+                const double v2 = __dsub_rn(vz_tab[k], r.trans[2]);
+                const double w0 = __dadd_rn(c0, __dmul_rn(m[6], v2));
+                const double w1 = __dadd_rn(c1, __dmul_rn(m[7], v2));
+                const double w2 = __dadd_rn(c2, __dmul_rn(m[8], v2));
+                const float gx = (float)__dmul_rn(__dadd_rn(w0, 1.0), hr);
+                const float gy = (float)__dmul_rn(__dadd_rn(w1, 1.0), hr);
+                const float gk = (float)__dmul_rn(__dsub_rn(1.0, w2), hr);
+                v = sample_grid(r.values, R, gx, gy, gk);
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, k <= R && v >= 0.5f);
+            const int first = hit ? __ffs(hit) - 1 : 32;
+            // samples before the crossing: grazing (0 < v < 1), render.hpp:180-188
+            grazing |= __ballot_sync(0xffffffffu, lane < first && k <= R && v > 0.0f && v < 1.0f) != 0u;
+            const float prev_in_chunk = __shfl_up_sync(0xffffffffu, v, 1);
+            if (hit) {
+                k1 = kb + first;
+                vhit = __shfl_sync(0xffffffffu, v, first);
+                const float pv = __shfl_sync(0xffffffffu, prev_in_chunk, first);
+                vprev = first > 0 ? pv : last;
                 break;
             }
-            if (v > 0.0f && v < 1.0f) grazing = true;
-            vprev = v;
+            last = __shfl_sync(0xffffffffu, v, 31);
         }
-        r.rgb[3 * px + 0] = r.bg[0];
-        r.rgb[3 * px + 1] = r.bg[1];
-        r.rgb[3 * px + 2] = r.bg[2];
-        if (k1 < 0) {
-            r.depth[px] = -2.0f;  // kInvalidDepth, render.hpp:72
-            r.mask[px] = 0;
-            if (r.surface_k) r.surface_k[px] = -1;
-        } else {
-            grazing = false;
-            covered = true;
-            double s = 1.0;
-            if (k1 > 0) {
-                double v1 = (double)vhit, v0 = (double)vprev;
-                double denom = __dsub_rn(v1, v0);
-                if (denom > 0.0) {
-                    s = __ddiv_rn(__dsub_rn(0.5, v0), denom);
-                    s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
-                } else {
-                    degenerate = true;
+        if (lane == 0) {
+            r.rgb[3 * px + 0] = r.bg[0];
+            r.rgb[3 * px + 1] = r.bg[1];
+            r.rgb[3 * px + 2] = r.bg[2];
+            if (k1 < 0) {
+                r.depth[px] = -2.0f;  // kInvalidDepth, render.hpp:72
+                r.mask[px] = 0;
+                if (r.surface_k) r.surface_k[px] = -1;
+                n_graz += grazing ? 1 : 0;
+            } else {
+                ++n_cov;
+                double s = 1.0;
+                if (k1 > 0) {
+                    double v1d = (double)vhit, v0d = (double)vprev;
+                    double denom = __dsub_rn(v1d, v0d);
+                    if (denom > 0.0) {
+                        s = __ddiv_rn(__dsub_rn(0.5, v0d), denom);
+                        s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
+                    } else {
+                        ++n_deg;
+                    }
                 }
+                double depth =
+                    __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn(__dsub_rn((double)k1, 1.0), s)), (double)R));
+                r.depth[px] = (float)depth;
+                r.mask[px] = 1;
+                if (r.surface_k) r.surface_k[px] = k1;
+                double w[3];
+                view_to_world_d(r, vx, vy, depth, w);
+                unsigned pos = atomicAdd(&r.ctr->surface_count, 1u);
+                r.surface_pts[3 * (size_t)pos + 0] = w[0];
+                r.surface_pts[3 * (size_t)pos + 1] = w[1];
+                r.surface_pts[3 * (size_t)pos + 2] = w[2];
+                r.surface_px[pos] = (uint32_t)px;
             }
-            double depth = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn(__dsub_rn((double)k1, 1.0), s)), (double)R));
-            r.depth[px] = (float)depth;
-            r.mask[px] = 1;
-            if (r.surface_k) r.surface_k[px] = k1;
-            double w[3];
-            view_to_world_d(r, vx, vy, depth, w);
-            unsigned pos = atomicAdd(&r.ctr->surface_count, 1u);
-            r.surface_pts[3 * (size_t)pos + 0] = w[0];
-            r.surface_pts[3 * (size_t)pos + 1] = w[1];
-            r.surface_pts[3 * (size_t)pos + 2] = w[2];
-            r.surface_px[pos] = (uint32_t)px;
         }
     }
-    unsigned cb = __ballot_sync(0xffffffffu, covered), db = __ballot_sync(0xffffffffu, degenerate),
-             gb = __ballot_sync(0xffffffffu, grazing);
-    if ((threadIdx.x & 31) == 0) {
-        if (cb) atomicAdd(&r.ctr->covered, (unsigned long long)__popc(cb));
-        if (db) atomicAdd(&r.ctr->degenerate, (unsigned long long)__popc(db));
-        if (gb) atomicAdd(&r.ctr->grazing, (unsigned long long)__popc(gb));
+    (void)fR;
+    if (lane == 0) {
+        if (n_cov) atomicAdd(&r.ctr->covered, n_cov);
+        if (n_deg) atomicAdd(&r.ctr->degenerate, n_deg);
+        if (n_graz) atomicAdd(&r.ctr->grazing, n_graz);
     }
 }
 
 int launch_render_first_crossing(const RenderJob& r, cudaStream_t s) {
-    size_t npx = (size_t)r.width * r.height;
-    k_render<<<(unsigned)((npx + 255) / 256), 256, 0, s>>>(r);
+    if (r.cells > kMaxRenderCells) {
+        set_error("render: grid larger than 1024 cells");
+        return ICG_EINVAL;
+    }
+    const size_t npx = (size_t)r.width * r.height;
+    const size_t blocks = std::min<size_t>((npx + kRenderThreads / 32 - 1) / (kRenderThreads / 32), 148 * 16);
+    k_render<<<(unsigned)blocks, kRenderThreads, 0, s>>>(r);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }
