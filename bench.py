@@ -65,12 +65,17 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        # nvidia-smi needs a moment before its first row: do not start timing blind
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 10 and self.proc.poll() is None:
+            time.sleep(0.05)
+        self.rows.clear()
 
     def _read(self):
         for line in self.proc.stdout:
@@ -204,7 +209,7 @@ def workload_config(cfg_name: str, args) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
@@ -298,8 +303,7 @@ def main():
     # ---- warm-up ----
     for s in range(args.warmup):
         ctx.frame_raw(fields_dev[s % nF], cfg, cam, res, res, img_struct(dout, abi.ICG_MEM_DEVICE))
-    # ---- timed: device-resident inputs and outputs ----
-    ctx.profile(True, reset=True)
+    # ---- timed: device-resident inputs and outputs (no per-kernel events inside) ----
     barrier()
     cvd = [d for d in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if d.strip().isdigit()]
     clocks = ClockSampler(int(cvd[local_rank]) if local_rank < len(cvd) else local_rank)
@@ -315,11 +319,18 @@ def main():
         lat.append(img.wall_seconds * 1e3)
     wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
-    prof = ctx.profile_get()
-    ctx.profile(False, reset=False)
     barrier()
     dev_max = allmax(dev_total)
     value = world * args.steps / dev_max
+
+    # ---- per-kernel breakdown: a separate pass over the same frames with CUDA events
+    # around every launch (the events themselves cost a little, so `value` is not taken here) ----
+    ctx.profile(True, reset=True)
+    for s in range(min(args.steps, 20)):
+        flush_l2()
+        ctx.frame_raw(fields_dev[(s + args.warmup) % nF], cfg, cam, res, res, img_struct(dout, abi.ICG_MEM_DEVICE))
+    prof = ctx.profile_get()
+    ctx.profile(False, reset=False)
 
     # ---- e2e: pinned host inputs/outputs through the C ABI, host wall clock ----
     e2e = None
@@ -377,7 +388,7 @@ def main():
                            frame_latency_ms={"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99))},
                            evals_per_frame=int(prof["geo_points"] / max(1, prof["frames"]))),
             "e2e": e2e, "roofline": roofline, "secondary": secondary, "cpu_baseline": cpu_baseline,
-            "gpu_launches": int(prof["kernel_launches"]), "clocks": clk,
+            "gpu_launches": int(round(prof["kernel_launches"] / max(1, prof["frames"]) * args.steps)), "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     if dist:

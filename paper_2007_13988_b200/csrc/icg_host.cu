@@ -76,6 +76,11 @@ struct icg_context {
     alignas(64) unsigned char geo_pair_tmap[2][128] = {};
     alignas(64) unsigned char tex_pair_tmap[2][128] = {};
     bool geo_pair = false, tex_pair = false;
+    // column-factored geometry field (FACT / COLS streams, [part][x3 ? 0 : 1])
+    DBuf geo_fact_stream[2][2];
+    alignas(64) unsigned char geo_fact_tmap[2][2][128] = {};
+    bool geo_fact = false, use_fact = true;
+    DBuf colrec, cmap, collist, colcnt, sorted;
     bool use_pair = true;
     // field
     DBuf scene;
@@ -120,6 +125,7 @@ size_t nodes3(int cells) {
     return n * n * n;
 }
 size_t words(size_t bits) { return (bits + 31) / 32; }
+bool job_is_grid_host(const EvalJob& j) { return j.points == nullptr && j.values != nullptr; }
 
 // ---- instrumentation ----------------------------------------------------------
 int prof_begin(icg_context* c, int kind) {
@@ -284,11 +290,68 @@ int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
     return ICG_OK;
 }
 
+bool fact_ok(const icg_context* c, const FieldDev& fd) {
+    return fd.kind == ICG_FIELD_PIFU && (fd.precision == ICG_PREC_FP32 || fd.precision == ICG_PREC_BF16) &&
+           c->geo_pair && c->use_pair && c->geo_fact && c->use_fact;
+}
+
+// Column-factored evaluation of a grid job (a level's node list, or all nodes of a dense grid):
+// the orthographic projection gives every node of a column (i, j) the same Phi, so the Phi part
+// of every layer is computed once per distinct column (COLS pass, k_mlp_pair.cu) and the per-node
+// pass (FACT) only runs the hidden-input parts of layers 2-4.
+int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
+    const int xi = fd.precision == ICG_PREC_FP32 ? 0 : 1;
+    const size_t n1 = (size_t)job.cells + 1, plane = n1 * n1;
+    if (int r = c->colrec.ensure(plane * kColRecord * sizeof(float))) return r;
+    if (int r = c->cmap.ensure(plane * sizeof(int))) return r;
+    if (int r = c->collist.ensure(plane * sizeof(uint32_t))) return r;
+    if (int r = c->colcnt.ensure(plane * sizeof(uint32_t))) return r;
+    if (int r = c->sorted.ensure(nodes3(job.cells) * sizeof(uint32_t))) return r;
+    DevCounters* ctr = c->ctr.as<DevCounters>();
+    int slot = prof_begin(c, 0);
+    EvalJob cj{};
+    cj.cells = job.cells;
+    const int* cm = nullptr;
+    unsigned max_cols = (unsigned)plane;
+    EvalJob pj = job;  // the per-node job, its list in column order (a tile spans few column records)
+    pj.list = c->sorted.as<uint32_t>();
+    if (job.list) {
+        ICG_CUDA_TRY(cudaMemsetAsync(c->cmap.p, 0xFF, plane * sizeof(int), c->stream));
+        ICG_CUDA_TRY(cudaMemsetAsync(&ctr->ncols, 0, sizeof(unsigned), c->stream));
+        if (int r = launch_col_claim(job.list, job.count, job.cells, c->cmap.as<int>(), c->collist.as<uint32_t>(),
+                                     ctr, max_points, c->stream))
+            return r;
+        if (int r = launch_sort_by_column(job.list, job.count, job.cells, c->cmap.as<int>(), c->colcnt.as<uint32_t>(),
+                                          ctr, c->sorted.as<uint32_t>(), max_points, c->stream))
+            return r;
+        cj.list = c->collist.as<uint32_t>();
+        cj.count = &ctr->ncols;
+        cm = c->cmap.as<int>();
+        if (max_points < max_cols) max_cols = max_points;
+        c->launches += 4;
+    } else {
+        // dense grid (job.n_static = all nodes): every column, record = column index
+        if (job.n_static != nodes3(job.cells)) return einval("factored field: dense job must cover the grid");
+        cj.n_static = (unsigned)plane;
+        if (int r = launch_dense_column_list(job.cells, c->sorted.as<uint32_t>(), c->stream)) return r;
+        c->launches += 1;
+    }
+    if (int r = launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][xi], cj, c->colrec.as<float>(), max_cols,
+                                      xi == 0, c->stream))
+        return r;
+    int r = launch_pifu_pair_fact(fd, c->geo_tc, c->geo_fact_tmap[0][xi], pj, c->colrec.as<float>(), cm, max_points,
+                                  xi == 0, c->stream);
+    prof_end(c, slot);
+    c->launches += 2;
+    return r;
+}
+
 // `dependent_chain`: the batch is one link of the serial conflict loop, usually
 // small; it is routed on device between the tensor-core kernel and the
 // layer-parallel latency path by its size.
 int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points,
              bool dependent_chain = false) {
+    if (!dependent_chain && job_is_grid_host(job) && fact_ok(c, fd)) return run_eval_fact(c, fd, job, max_points);
     int slot = prof_begin(c, 0);
     int r;
     if (fd.kind == ICG_FIELD_ANALYTIC) {
@@ -680,6 +743,7 @@ int icg_create(int device, icg_context** out) {
     auto* c = new icg_context();
     c->device = device;
     if (const char* e = getenv("ICG_NO_PAIR")) c->use_pair = !(e[0] == '1');
+    if (const char* e = getenv("ICG_NO_FACT")) c->use_fact = !(e[0] == '1');
     if (const char* e = getenv("ICG_SMALL_MAX")) c->small_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_LP_MAX")) c->lp_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_LAT")) c->lat_small = std::string(e) == "small";
@@ -708,7 +772,9 @@ int icg_destroy(icg_context* c) {
                    &c->scene, &c->fscene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
                    &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->lp_scratch, &c->lp_stream, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi,
-                   &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx};
+                   &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx, &c->colrec, &c->cmap, &c->collist, &c->colcnt, &c->sorted,
+                   &c->geo_fact_stream[0][0], &c->geo_fact_stream[0][1], &c->geo_fact_stream[1][0],
+                   &c->geo_fact_stream[1][1]};
     for (DBuf* b : all) b->release();
     for (int l = 0; l < 5; ++l) {
         c->geo_wt[l].release();
@@ -836,6 +902,23 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
         if (int r = pair_make_tmap(px.p, bx, tm[0])) return r;
         if (int r = pair_make_tmap(ph.p, bh, tm[1])) return r;
         (geo ? c->geo_pair : c->tex_pair) = true;
+    }
+    if (geo) {
+        // column-factored streams: part 0 = hidden-input items of layers 2-4, part 1 = Phi items
+        const float* ws[5];
+        for (int l = 0; l < 5; ++l) ws[l] = d->weights[l];
+        for (int part = 0; part < 2; ++part) {
+            const size_t bx = pair_fact_stream_bytes(part, true), bh = pair_fact_stream_bytes(part, false);
+            std::vector<uint8_t> sx(bx), sh(bh);
+            if (int r = pair_pack_factored(ws, part, sx.data(), sh.data())) return r;
+            if (int r = c->geo_fact_stream[part][0].ensure(bx)) return r;
+            if (int r = c->geo_fact_stream[part][1].ensure(bh)) return r;
+            ICG_CUDA_TRY(cudaMemcpy(c->geo_fact_stream[part][0].p, sx.data(), bx, cudaMemcpyHostToDevice));
+            ICG_CUDA_TRY(cudaMemcpy(c->geo_fact_stream[part][1].p, sh.data(), bh, cudaMemcpyHostToDevice));
+            if (int r = pair_make_tmap(c->geo_fact_stream[part][0].p, bx, c->geo_fact_tmap[part][0])) return r;
+            if (int r = pair_make_tmap(c->geo_fact_stream[part][1].p, bh, c->geo_fact_tmap[part][1])) return r;
+        }
+        c->geo_fact = true;
     }
     if (geo) {
         // layer-parallel latency path: weight tiles per (layer, row block, K chunk)

@@ -44,7 +44,7 @@ struct DevCounters {
     unsigned int conflict_iters[ICG_MAX_LEVELS];
     unsigned long long covered, degenerate, grazing;
     unsigned int surface_count;
-    unsigned int pad;
+    unsigned int ncols;               // column-factored field: distinct columns of the current batch
 };
 
 // Analytic scene in constant-friendly form (union of primitives).
@@ -149,6 +149,15 @@ int launch_pifu_tc_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex
 size_t pair_stream_bytes(int which, bool x3);
 int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi);
 int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out);
+// column-factored geometry field (k_mlp_pair.cu, modes COLS / FACT): part 0 = FACT stream
+// (hidden-input items of layers 2-4), part 1 = COLS stream (Phi items of layers 1-4)
+constexpr int kColRecord = 1936;  // floats per column record
+size_t pair_fact_stream_bytes(int part, bool x3);
+int pair_pack_factored(const float* const* w, int part, uint8_t* stream_x3, uint8_t* stream_hi);
+int launch_pifu_pair_cols(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& cols, float* records,
+                          unsigned max_cols, bool x3, cudaStream_t s);
+int launch_pifu_pair_fact(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
+                          const float* records, const int* cmap, unsigned max_points, bool x3, cudaStream_t s);
 int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
                           unsigned max_points, bool x3, cudaStream_t s);
 int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const void* tmap_geo,
@@ -182,6 +191,16 @@ int launch_conflict_expand(uint32_t* fine_queued, const uint8_t* fs, int fcells,
                            DevCounters* ctr, int iter, int max_iters, uint32_t* next_list,
                            unsigned int cap, cudaStream_t s);
 int launch_unroll_check(DevCounters* ctr, int iter_parity, int level, cudaStream_t s);
+// column-factored field: give every distinct column (i + n j) of a node list a record slot
+// (cmap[col] = slot, collist[slot] = col, ctr->ncols = number of slots); cmap must be all -1
+int launch_col_claim(const uint32_t* list, const unsigned* count, int cells, int* cmap, uint32_t* collist,
+                     DevCounters* ctr, unsigned max_points, cudaStream_t s);
+// counting sort of a node list by column record (so a point tile spans few columns); cnt holds
+// one u32 per possible column and is cleared here
+int launch_sort_by_column(const uint32_t* list, const unsigned* count, int cells, const int* cmap, uint32_t* cnt,
+                          DevCounters* ctr, uint32_t* sorted, unsigned max_points, cudaStream_t s);
+// node list of a dense (cells+1)^3 grid in column order: t -> node (t / n1) + plane * (t % n1)
+int launch_dense_column_list(int cells, uint32_t* list, cudaStream_t s);
 int launch_binarize(const float* v, uint8_t* out, size_t n, cudaStream_t s);
 int launch_iou(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* inter_union, cudaStream_t s);
 int launch_fill_states(uint8_t* s, size_t n, uint8_t v, cudaStream_t st);

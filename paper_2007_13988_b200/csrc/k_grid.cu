@@ -363,6 +363,113 @@ int launch_conflict_expand(uint32_t* queued, const uint8_t* fs, int fcells, cons
     return ICG_OK;
 }
 
+// ---- column claim (column-factored PIFu field) ------------------------------
+// Slot order depends on atomic timing, but a column's record is a function of the column
+// alone, so every node value is independent of it.
+__global__ void k_col_claim(const uint32_t* __restrict__ list, const unsigned* __restrict__ count, int cells,
+                            int* __restrict__ cmap, uint32_t* __restrict__ collist, DevCounters* ctr) {
+    const unsigned n = *count;
+    const uint32_t n1 = (uint32_t)cells + 1u, plane = n1 * n1;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const uint32_t col = list[t] % plane;
+        if (cmap[col] != -1) continue;  // cheap pre-check; the CAS decides
+        if (atomicCAS(&cmap[col], -1, -2) == -1) {
+            const unsigned slot = atomicAdd(&ctr->ncols, 1u);
+            collist[slot] = col;
+            cmap[col] = (int)slot;
+        }
+    }
+}
+
+int launch_col_claim(const uint32_t* list, const unsigned* count, int cells, int* cmap, uint32_t* collist,
+                     DevCounters* ctr, unsigned max_points, cudaStream_t s) {
+    const unsigned blocks = std::min<unsigned>((max_points + 255) / 256, 148u * 8u);
+    k_col_claim<<<blocks ? blocks : 1, 256, 0, s>>>(list, count, cells, cmap, collist, ctr);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
+__global__ void k_slot_count(const uint32_t* __restrict__ list, const unsigned* __restrict__ count, int cells,
+                             const int* __restrict__ cmap, uint32_t* __restrict__ cnt) {
+    const unsigned n = *count;
+    const uint32_t n1 = (uint32_t)cells + 1u, plane = n1 * n1;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        atomicAdd(&cnt[cmap[list[t] % plane]], 1u);
+}
+
+// exclusive scan of cnt[0 .. *ncols) in place (one block)
+__global__ void __launch_bounds__(1024) k_scan_slots(uint32_t* __restrict__ cnt, const unsigned* __restrict__ ncols) {
+    __shared__ unsigned warp_sums[32];
+    __shared__ unsigned carry;
+    const unsigned n = *ncols;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (unsigned base = 0; base < n; base += 1024) {
+        const unsigned idx = base + threadIdx.x;
+        const unsigned v = idx < n ? cnt[idx] : 0u;
+        unsigned x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            const unsigned w = warp_sums[lane];
+            unsigned ws = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, ws, o);
+                if (lane >= o) ws += y;
+            }
+            warp_sums[lane] = ws - w;
+        }
+        __syncthreads();
+        if (idx < n) cnt[idx] = carry + warp_sums[warp] + x - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += warp_sums[31] + x;
+        __syncthreads();
+    }
+}
+
+__global__ void k_slot_scatter(const uint32_t* __restrict__ list, const unsigned* __restrict__ count, int cells,
+                               const int* __restrict__ cmap, uint32_t* __restrict__ off, uint32_t* __restrict__ sorted) {
+    const unsigned n = *count;
+    const uint32_t n1 = (uint32_t)cells + 1u, plane = n1 * n1;
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const uint32_t node = list[t];
+        sorted[atomicAdd(&off[cmap[node % plane]], 1u)] = node;
+    }
+}
+
+int launch_sort_by_column(const uint32_t* list, const unsigned* count, int cells, const int* cmap, uint32_t* cnt,
+                          DevCounters* ctr, uint32_t* sorted, unsigned max_points, cudaStream_t s) {
+    const size_t plane = ((size_t)cells + 1) * ((size_t)cells + 1);
+    ICG_CUDA_TRY(cudaMemsetAsync(cnt, 0, plane * 4, s));
+    const unsigned blocks = std::max(1u, std::min<unsigned>((max_points + 255) / 256, 148u * 8u));
+    k_slot_count<<<blocks, 256, 0, s>>>(list, count, cells, cmap, cnt);
+    k_scan_slots<<<1, 1024, 0, s>>>(cnt, &ctr->ncols);
+    k_slot_scatter<<<blocks, 256, 0, s>>>(list, count, cells, cmap, cnt, sorted);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
+__global__ void k_dense_column_list(int cells, uint32_t* __restrict__ list) {
+    const uint32_t n1 = (uint32_t)cells + 1u, plane = n1 * n1, total = plane * n1;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x)
+        list[t] = t / n1 + plane * (t % n1);
+}
+
+int launch_dense_column_list(int cells, uint32_t* list, cudaStream_t s) {
+    const size_t total = ((size_t)cells + 1) * ((size_t)cells + 1) * ((size_t)cells + 1);
+    const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 148 * 16);
+    k_dense_column_list<<<blocks, 256, 0, s>>>(cells, list);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
 __global__ void k_unroll_check(DevCounters* ctr, int parity, int level) {
     if (ctr->cf_count[parity] > 0) ctr->unroll_exhausted |= 1u << level;
 }

@@ -46,28 +46,54 @@ namespace pair {
 
 constexpr uint32_t kHalf = 16384;   // one 128 x 64 bf16 tile
 constexpr uint32_t kStage = 32768;  // one TMA box: (hi, lo) of one item (bf16x3) or hi of two items (bf16)
-constexpr int kEpiWarps = 8;
-constexpr int kEpiThreads = 32 * kEpiWarps;
-constexpr int kThreads = 64 + kEpiThreads;
+constexpr int kEpiWarpsMax = 16;
 constexpr int kMaxNP = 128;
 constexpr int kMaxStages = 6;
 
-template <bool TEX>
+// Kernel modes.
+//   GEO  : geometry field, full network per point (257-wide skip operand gathered per point)
+//   TEX  : texture field at surface points (geometry prefix + texture body)
+//   COLS : column pass of the column-factored geometry field: for a list of grid COLUMNS (i,j)
+//          computes the Phi-part of every layer's pre-activation, S = W_Phi . Phi(x_i, y_j), and
+//          the Phi-part of the output dot, into a fp32 record per column (kSRow floats)
+//   FACT : column-factored geometry field: under the orthographic projection every node of a
+//          column shares Phi, so layer 1 is act(S1[col] + w1z z + b1) (no MMA) and layers 2-4
+//          only multiply the hidden part: W_h . h + S_l[col]
+enum { kModeGeo = 0, kModeTex = 1, kModeCols = 2, kModeFact = 3 };
+constexpr int kSRow = 1936;    // floats per column record: [1024 | 512 | 256 | 128 | final Phi dot | pad]
+constexpr int kSFinal = 1920;  // offset of the final layer's Phi dot
+__host__ __device__ constexpr int kSOffL(int l) { return l == 0 ? 0 : l == 1 ? 1024 : l == 2 ? 1536 : 1792; }
+
+template <int MODE>
 struct Cfg {
+    static constexpr bool TEX = MODE == kModeTex;
     static constexpr int NPC = TEX ? 32 : 64;        // points per CTA
     static constexpr int NP = 2 * NPC;               // points per pair tile = MMA N
-    static constexpr int kSkipChunks = TEX ? 8 : 4;  // [Phi] or [Phi, h3] in 64-wide K-chunks
-    static constexpr int kStages = TEX ? 3 : 2;  // 32 KB stages (per-copy TMA cost is size-independent)
+    // [Phi] or [Phi, h3] in 64-wide K-chunks (none for FACT: Phi enters through the column records)
+    static constexpr int kSkipChunks = TEX ? 8 : (MODE == kModeFact ? 0 : 4);
+    static constexpr int kHBufs = MODE == kModeFact ? 2 : (MODE == kModeCols ? 0 : 1);  // h operand buffers
+    // 32 KB stages (per-copy TMA cost is size-independent)
+    static constexpr int kStages = TEX ? 3 : (MODE == kModeCols ? 4 : 2);
     static constexpr uint32_t kChunk = NPC * 128;  // NPC point rows x 64 bf16 (SW128)
     static constexpr uint32_t kSkipHalf = kSkipChunks * kChunk;
     static constexpr uint32_t kHHalf = 4 * kChunk;  // one 256-feature block
     static constexpr uint32_t kOffSkip = 0;
     static constexpr uint32_t kOffH = kOffSkip + 2 * kSkipHalf;
-    static constexpr uint32_t kOffRing = kOffH + 2 * kHHalf;
+    static constexpr uint32_t kOffRing = kOffH + kHBufs * 2 * kHHalf;
     static constexpr uint32_t kOffMisc = kOffRing + kStages * kStage;
-    static constexpr uint32_t kMisc = 20480;
+    static constexpr uint32_t kMisc = 24576;
     static constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
     static constexpr int kOut = TEX ? 3 : 1;
+    // epilogue warps: 8 = 4 TMEM lane quarters x 2 point halves; FACT (no transposes, fewer
+    // registers) uses 16 = 4 quarters x 4 point quarters to hide the per-block latency chain
+    static constexpr int kEpiWarps = 8;
+    static constexpr int kEpiThreads = 32 * kEpiWarps;
+    static constexpr int kThreads = 64 + kEpiThreads;
+    static constexpr int kHF = (NPC / 32) / (kEpiWarps / 8);  // 32-point chunks per epilogue thread
+    // one CTA per SM: the register file split over the CTA's warps, allocated in groups of 4
+    // warps, per thread a multiple of 8
+    static constexpr int kWarpsAlloc = ((kThreads / 32) + 3) / 4 * 4;
+    static constexpr int kMaxReg = (65536 / (kWarpsAlloc * 32)) / 8 * 8;
     static constexpr int kSkipDim = TEX ? kTexSkip : kGeoSkip;
     static_assert(kStages <= kMaxStages, "stages");
 };
@@ -105,18 +131,51 @@ constexpr int kGeoItems = items(4, true);      // 76
 constexpr int kPrefixItems = items(4, false);  // 68
 constexpr int kTexItems = items(8, true);      // 108
 
+// FACT stream: only the hidden-input items of layers 2-4, in the order the MMA issuer consumes
+// them (h1 chunk c: K chunks jj, row blocks m; then h2 blocks for layer 3; then h3 for layer 4)
+template <class Emit>
+__host__ __device__ void schedule_fact(Emit&& emit) {
+    for (int c = 0; c < 4; ++c)
+        for (int jj = 0; jj < 4; ++jj)
+            for (int m = 0; m < 2; ++m) emit(1, m, c * 256 + jj * 64);
+    for (int c = 0; c < 2; ++c)
+        for (int jj = 0; jj < 4; ++jj) emit(2, 0, c * 256 + jj * 64);
+    for (int jj = 0; jj < 4; ++jj) emit(3, 0, jj * 64);
+}
+constexpr int kFactItems = 44;
+// COLS stream: the Phi items (K = skip columns 0..255) of every 256-row block of layers 1-4
+template <class Emit>
+__host__ __device__ void schedule_cols(Emit&& emit) {
+    const int prev[4] = {0, 1024, 512, 256};
+    const int blocks[4] = {4, 2, 1, 1};
+    for (int l = 0; l < 4; ++l)
+        for (int m = 0; m < blocks[l]; ++m)
+            for (int j = 0; j < 4; ++j) emit(l, m, prev[l] + j * 64);
+}
+constexpr int kColsItems = 32;
+constexpr int kColsBlocks = 8;
+
 struct Misc {
     uint64_t full[kMaxStages], empty[kMaxStages];
-    uint64_t f_ready, h_ready[2], h_free[2], l1done[2], d2done, d3done, d4done, sd_ready[2], skip_free, d4_free;
+    uint64_t f_ready, h_ready[2][2], h_free[2][2], l1done[2], d2done, d3done, d4done, sd_ready[2], skip_free, d4_free;
+    uint64_t accb[4], acc_free[4];  // COLS: accumulator ring
     uint32_t tmem_base;
+    int slot[2][kMaxNP];  // FACT: column record of each point of the tile (by tile parity)
+    // FACT: per 32-point chunk of a (column-sorted) tile: first / last record, mask of the points
+    // on the last record, and whether those two records are all the chunk uses
+    int cfirst[2][kMaxNP / 32], clast[2][kMaxNP / 32];
+    uint32_t cmask[2][kMaxNP / 32], cok[2][kMaxNP / 32];
     float z[2][kMaxNP];       // by tile parity (the next tile is gathered before this one's final layer)
     float pos[2][kMaxNP][3];
     float red[4][3][kMaxNP];      // final layer: per-lane-quarter partial sums over features
     float skipdot[2][3][kMaxNP];  // final layer: skip-input dots (leader, all points), by tile parity
     float sdl[3][kMaxNP / 2];     // texture: this CTA's Phi-part skip dots until h3 is known
-    float cterm[3][kMaxNP];       // b5 + w5z*z (- sdf_scale*sdf for geometry)
+    float cterm[3][kMaxNP];       // b5 + w5z*z (- sdf_scale*sdf for geometry); FACT: [tile parity][point]
+    // the bias scene as capsules (a, b - a, |b - a|^2, r), when every primitive is a capsule
+    float caps[ICG_MAX_PRIMS][8];
+    int ncaps;  // -1: not all capsules (use the general fp32 scene path)
 };
-static_assert(sizeof(Misc) + 16 <= Cfg<false>::kMisc, "misc smem too small");
+static_assert(sizeof(Misc) + 16 <= Cfg<kModeGeo>::kMisc, "misc smem too small");
 
 struct Params {
     FieldDev f;
@@ -129,6 +188,9 @@ struct Params {
     float slope;
     int x3;
     unsigned long long* trace;
+    float* s_out;        // COLS: column records, kSRow floats per list entry
+    const float* s_in;   // FACT: column records
+    const int* cmap;     // FACT: column (i + n j) -> record index (nullptr: the column index itself)
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -218,12 +280,16 @@ __device__ __forceinline__ void transpose8_bf16(const float* v, uint4* hi, uint4
     }
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
+template <int N>
+__device__ __forceinline__ void epi_bar_n() { asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory"); }
 
-template <bool TEX>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
     k_mlp_pair(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB, Params P) {
-    using C = Cfg<TEX>;
+    using C = Cfg<MODE>;
+    constexpr int kEpiWarps = C::kEpiWarps, kEpiThreads = C::kEpiThreads, kHF = C::kHF;
+    auto epi_bar = [] { epi_bar_n<C::kEpiThreads>(); };
+    constexpr bool TEX = MODE == kModeTex, COLS = MODE == kModeCols, FACT = MODE == kModeFact;
     constexpr int NPC = C::NPC, NP = C::NP, NOUT = C::kOut, kStages = C::kStages;
     constexpr uint32_t kChunk = C::kChunk, kSkipHalf = C::kSkipHalf, kHHalf = C::kHHalf;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -251,12 +317,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&ms.full[s], 1);
             ptx::mbar_init(&ms.empty[s], 1);
         }
-        ptx::mbar_init(&ms.f_ready, 2 * kEpiThreads);
+        ptx::mbar_init(&ms.f_ready, 2 * kEpiWarps);  // one arrival per epilogue warp (after __syncwarp)
         // h buffer halves: K chunks 0-1 (features 0-127) are written by CTA 0, chunks 2-3 by CTA 1
-        ptx::mbar_init(&ms.h_ready[0], kEpiThreads);
-        ptx::mbar_init(&ms.h_ready[1], kEpiThreads);
-        ptx::mbar_init(&ms.h_free[0], 1);
-        ptx::mbar_init(&ms.h_free[1], 1);
+        for (int b = 0; b < 2; ++b)
+            for (int h = 0; h < 2; ++h) {
+                ptx::mbar_init(&ms.h_ready[b][h], kEpiWarps);
+                ptx::mbar_init(&ms.h_free[b][h], 1);
+            }
+        for (int a = 0; a < 4; ++a) {
+            ptx::mbar_init(&ms.accb[a], 1);
+            ptx::mbar_init(&ms.acc_free[a], 2 * kEpiThreads);
+        }
         ptx::mbar_init(&ms.l1done[0], 1);
         ptx::mbar_init(&ms.l1done[1], 1);
         ptx::mbar_init(&ms.d2done, 1);
@@ -278,11 +349,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = ms.tmem_base;
     job_account(job);
+    if constexpr (MODE == kModeFact) {
+        // the capsule figure of the -sdf_scale * sdf bias in shared memory (read by every tile)
+        if (threadIdx.x >= 64) {
+            const int i = threadIdx.x - 64;
+            const int np = __ldg(&P.f.fscene->n_prims);
+            if (i < np) {
+                const FPrim* pr = &P.f.fscene->prims[i];
+                const float a0 = __ldg(&pr->a[0]), a1 = __ldg(&pr->a[1]), a2 = __ldg(&pr->a[2]);
+                const float b0 = __ldg(&pr->b[0]) - a0, b1 = __ldg(&pr->b[1]) - a1, b2 = __ldg(&pr->b[2]) - a2;
+                ms.caps[i][0] = a0;
+                ms.caps[i][1] = a1;
+                ms.caps[i][2] = a2;
+                ms.caps[i][3] = b0;
+                ms.caps[i][4] = b1;
+                ms.caps[i][5] = b2;
+                ms.caps[i][6] = b0 * b0 + b1 * b1 + b2 * b2;
+                ms.caps[i][7] = __ldg(&pr->radius);
+            }
+            if (i == 0) {
+                bool all = np <= ICG_MAX_PRIMS;
+                for (int k = 0; k < np && all; ++k)
+                    all = __ldg(&P.f.fscene->prims[k].kind) == ICG_PRIM_CAPSULE && !__ldg(&P.f.fscene->prims[k].rotated);
+                ms.ncaps = all ? np : -1;
+            }
+            epi_bar_n<C::kEpiThreads>();
+        }
+    }
 
     // leader-CTA addresses of the barriers that receive cross-CTA traffic
     const uint32_t full0 = ptx::mapa(ptx::smem_u32(&ms.full[0]), 0);
     const uint32_t f_ready0 = ptx::mapa(ptx::smem_u32(&ms.f_ready), 0);
-    const uint32_t h_ready0 = ptx::mapa(ptx::smem_u32(&ms.h_ready[rank]), 0);  // this CTA's half
+    // this CTA's half of h buffer b: h_ready0 + 16 * b
+    const uint32_t h_ready0 = ptx::mapa(ptx::smem_u32(&ms.h_ready[0][rank]), 0);
+    const uint32_t acc_free0 = ptx::mapa(ptx::smem_u32(&ms.acc_free[0]), 0);
     const uint32_t sd_ready0 = ptx::mapa(ptx::smem_u32(&ms.sd_ready[0]), 0);
     const uint16_t both = 0x3;
 
@@ -336,8 +436,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
             };
             int sub = 0;  // bf16: which of the two items of the current box
-            auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc) {
-                const uint64_t bd_hi = ptx::sdesc_sw128(b_hi), bd_lo = ptx::sdesc_sw128(b_lo);
+            // B operand (point activations): K-major (gathered skip operand) or MN-major (h
+            // blocks written one feature per thread, FACT); A (weights) is always K-major
+            const uint32_t idesc_mn = idesc | (1u << 16);
+            auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc, bool mn = false) {
+                const uint64_t bd_hi = mn ? ptx::sdesc_sw128_mn(b_hi) : ptx::sdesc_sw128(b_hi);
+                const uint64_t bd_lo = mn ? ptx::sdesc_sw128_mn(b_lo) : ptx::sdesc_sw128(b_lo);
+                const uint32_t id = mn ? idesc_mn : idesc;
                 if (P.x3) {
                     wait_full();
                     const uint64_t ad_hi = ptx::sdesc_sw128(ring0 + s * kStage);
@@ -345,9 +450,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t koff = (uint64_t)(kk * 2);
-                        ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_hi + koff, idesc, (acc || kk > 0) ? 1u : 0u);
-                        ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_lo + koff, idesc, 1u);
-                        ptx::mma_bf16_pair(tmem + dcol, ad_lo + koff, bd_hi + koff, idesc, 1u);
+                        const uint64_t kb = mn ? (uint64_t)(kk * 128) : koff;  // 16 k = 16 rows of 128 B (MN)
+                        ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_hi + kb, id, (acc || kk > 0) ? 1u : 0u);
+                        ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_lo + kb, id, 1u);
+                        ptx::mma_bf16_pair(tmem + dcol, ad_lo + koff, bd_hi + kb, id, 1u);
                     }
                     ptx::mma_commit_pair(&ms.empty[s], both);
                     next_stage();
@@ -357,7 +463,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t koff = (uint64_t)(kk * 2);
-                        ptx::mma_bf16_pair(tmem + dcol, ad + koff, bd_hi + koff, idesc, (acc || kk > 0) ? 1u : 0u);
+                        const uint64_t kb = mn ? (uint64_t)(kk * 128) : koff;
+                        ptx::mma_bf16_pair(tmem + dcol, ad + koff, bd_hi + kb, id, (acc || kk > 0) ? 1u : 0u);
                     }
                     if (sub == 1) {
                         ptx::mma_commit_pair(&ms.empty[s], both);
@@ -366,27 +473,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     sub ^= 1;
                 }
             };
-            auto wait_h = [&](int half) {
-                const unsigned long long t0 = tr ? gtime() : 0;
-                ptx::mbar_wait_cluster(&ms.h_ready[half], hph[half]);
-                if (tr) w_h += gtime() - t0;
-                hph[half] ^= 1;
-                ptx::tc_fence_after();
+            uint32_t hph_bits = 0;  // parity of h_ready[buf][half] at bit 2 buf + half (no local array)
+            int nev = 0;  // trace: event log of block 0 (times at [64..320), codes at [320..576))
+            auto ev = [&](int code) {
+                if (tr && nev < 256) {
+                    P.trace[64 + nev] = gtime();
+                    P.trace[320 + nev] = (unsigned long long)code;
+                    ++nev;
+                }
             };
-            // consume one h block (4 K chunks) for `nm` 256-row blocks, half by half
-            auto h_block = [&](int nm, uint32_t dcol0) {
+            auto wait_h = [&](int buf, int half) {
+                ev(100 + 10 * buf + half);
+                const unsigned long long t0 = tr ? gtime() : 0;
+                const uint32_t bit = (uint32_t)(2 * buf + half);
+                ptx::mbar_wait_cluster(&ms.h_ready[buf][half], (hph_bits >> bit) & 1u);
+                if (tr) w_h += gtime() - t0;
+                hph_bits ^= 1u << bit;
+                ptx::tc_fence_after();
+                ev(200 + 10 * buf + half);
+            };
+            (void)hph;
+            // consume one h block (4 K chunks) of buffer `buf` for `nm` 256-row blocks, half by half;
+            // `first`: the block starts the accumulation (FACT: no skip items precede it)
+            auto h_block = [&](int nm, uint32_t dcol0, int buf = 0, bool first = false) {
+                const uint32_t bh = h_hi + (uint32_t)buf * 2 * kHHalf, bl = bh + kHHalf;
                 for (int half = 0; half < 2; ++half) {
-                    wait_h(half);
+                    wait_h(buf, half);
                     for (int jj = 2 * half; jj < 2 * half + 2; ++jj)
                         for (int m = 0; m < nm; ++m)
-                            item(dcol0 + m * NP, h_hi + jj * kChunk, h_lo + jj * kChunk, true);
-                    ptx::mma_commit_pair(&ms.h_free[half], both);
+                            item(dcol0 + m * NP, bh + jj * kChunk, bl + jj * kChunk, !(first && jj == 0), FACT);
+                    ptx::mma_commit_pair(&ms.h_free[buf][half], both);
                 }
             };
             auto skipk = [&](int j) { return skip_hi + j * kChunk; };
             auto skipl = [&](int j) { return skip_lo + j * kChunk; };
             // TMEM columns: D2[m] = m*NP, BUF[b] = 2NP + b*NP, D3 = BUF[0], D4 = D2[0]
             uint32_t d4fph = 0;
+            uint32_t cblk = 0, hblk = 0;  // COLS accumulator blocks / FACT h blocks issued so far
             auto body = [&](int ks, bool with_l4, bool wait_d4) {
                 auto L1 = [&](int c) {
                     for (int j = 0; j < ks; ++j) item(2 * NP + (c & 1) * NP, skipk(j), skipl(j), j > 0);
@@ -417,8 +540,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 } else {
                     // prefix: h3 is in the skip operands of both CTAs
                     for (int half = 0; half < 2; ++half) {
-                        wait_h(half);
-                        ptx::mma_commit_pair(&ms.h_free[half], both);
+                        wait_h(0, half);
+                        ptx::mma_commit_pair(&ms.h_free[0][half], both);
                     }
                 }
             };
@@ -431,9 +554,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 fph ^= 1;
                 ptx::tc_fence_after();
                 const bool later = t != pair_id;
-                if (TEX) {
+                if constexpr (TEX) {
                     body(4, false, later);
                     body(8, true, false);
+                } else if constexpr (COLS) {
+                    // 8 blocks of 256 rows, each K = 256 (the Phi channels), through a ring of 4 accumulators
+                    for (int b = 0; b < kColsBlocks; ++b) {
+                        const int a = (int)(cblk & 3u);
+                        ptx::mbar_wait(&ms.acc_free[a], ((cblk >> 2) & 1u) ^ 1u);
+                        ptx::tc_fence_after();
+                        for (int j = 0; j < 4; ++j) item((uint32_t)a * NP, skipk(j), skipl(j), j > 0);
+                        ptx::mma_commit_pair(&ms.accb[a], both);
+                        ++cblk;
+                    }
+                    ptx::mma_commit_pair(&ms.skip_free, both);
+                } else if constexpr (FACT) {
+                    // TMEM: D2[m] = m*NP, D3 = 2NP, D4 = 3NP; h blocks alternate between two buffers
+                    for (int c = 0; c < 4; ++c) h_block(2, 0, (int)(hblk++ & 1u), c == 0);
+                    ptx::mma_commit_pair(&ms.d2done, both);
+                    ev(302);
+                    for (int c = 0; c < 2; ++c) h_block(1, 2 * NP, (int)(hblk++ & 1u), c == 0);
+                    ptx::mma_commit_pair(&ms.d3done, both);
+                    ev(303);
+                    h_block(1, 3 * NP, (int)(hblk++ & 1u), true);
+                    ptx::mma_commit_pair(&ms.d4done, both);
+                    ev(304);
                 } else {
                     body(4, true, later);
                 }
@@ -450,12 +595,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int et = threadIdx.x - 64;
         const int ew = et >> 5;
         const int quarter = warp & 3;
-        const int colh = (warp - 2) >> 2;  // point half this warp converts = destination CTA
+        const int colq = (warp - 2) >> 2;
+        const int colh = colq / (kEpiWarps / 8);  // point half this warp converts = destination CTA
+        const int hf0 = (colq % (kEpiWarps / 8)) * kHF;  // its first 32-point chunk inside that half
         const int row = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(colh * NPC);
-        uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hfph = 1, sdph[2] = {0, 0}, sfph = 0;
+        uint32_t l1ph[2] = {0, 0}, d2ph = 0, d3ph = 0, d4ph = 0, hfph = 1, sdph_bits = 0, sfph = 0;
         unsigned tile_iter = 0;
         const float* zc = ms.z[0];  // z of the tile being converted
+        const int* slc = ms.slot[0];  // FACT: column records of the tile being converted
+        int ms_tile_parity = 0;       // FACT: parity of that tile (chunk record info)
+        uint32_t hfph_bits = 3u;      // h_free parity per h buffer (bit buf)
+        uint32_t hbe = 0;             // FACT: h blocks emitted so far (buffer = hbe & 1)
         const FieldDev& f = P.f;
         const bool odd = lane & 1;
         // this thread's feature inside a 256-row block, and its K position in the next layer's operand
@@ -466,20 +617,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t sdst = ptx::mapa(ptx::smem_u32(skip) + 4 * kChunk, (uint32_t)colh);  // texture: h3 -> skip
 
         const bool etr = P.trace && blockIdx.x == 0 && et == 0;
+        int nee = 0;  // trace: epilogue event log (times at [576..832), codes at [832..1088))
+        auto eev = [&](int code) {
+            if (etr && nee < 256) {
+                P.trace[576 + nee] = gtime();
+                P.trace[832 + nee] = (unsigned long long)code;
+                ++nee;
+            }
+        };
         unsigned long long e_acc = 0, e_hf = 0, e_emit = 0, e_t0 = 0, e_begin = gtime();
         unsigned long long e_cyc[3] = {0, 0, 0};
         // TMEM columns [col, col + NPC) of this thread's lane -> next layer's operand in the owning CTA
-        auto emit_block = [&](uint32_t col, const float* bias_blk, int out_dim, int feat0, uint32_t dst,
-                              uint32_t lo_off, bool write_lo) {
+        // soff >= 0 (FACT): add the column-record term S[slot(p)][soff + o]; from_tmem == false
+        // (FACT layer 1): there is no accumulator, the pre-activation is the column term alone
+        // FACT: a block's global operands (bias, z weight, the two column-record terms of each
+        // 32-point chunk), loaded one block ahead so their latency overlaps the previous block
+        struct Pre {
+            float bo, wz, sA[kHF], sB[kHF];
+        };
+        auto fact_pre = [&](const float* bias_blk, int out_dim, int feat0, int soff, int cp) {
+            Pre q;
             const int o = feat0 + (int)feat;
-            const float bo = __ldg(&bias_blk[o]);
-            const float wz = __ldg(&bias_blk[out_dim + o]);
+            q.bo = __ldg(&bias_blk[o]);
+            q.wz = __ldg(&bias_blk[out_dim + o]);
+#pragma unroll
+            for (int hi = 0; hi < kHF; ++hi) {
+                const int c = colh * (NPC / 32) + hf0 + hi;
+                q.sA[hi] = __ldg(P.s_in + soff + o + (size_t)ms.cfirst[cp][c] * kSRow);
+                q.sB[hi] = __ldg(P.s_in + soff + o + (size_t)ms.clast[cp][c] * kSRow);
+            }
+            return q;
+        };
+        auto emit_block = [&](uint32_t col, const float* bias_blk, int out_dim, int feat0, uint32_t dst,
+                              uint32_t lo_off, bool write_lo, int soff = -1, bool from_tmem = true,
+                              const Pre* pre = nullptr) {
+            const int o = feat0 + (int)feat;
+            const float bo = FACT ? pre->bo : __ldg(&bias_blk[o]);
+            const float wz = FACT ? pre->wz : __ldg(&bias_blk[out_dim + o]);
+            float sA[kHF], sB[kHF];
+            uint32_t smask[kHF], sok[kHF];
+            if constexpr (FACT) {
+                const int cp = ms_tile_parity;
+#pragma unroll
+                for (int hi = 0; hi < kHF; ++hi) {
+                    const int c = colh * (NPC / 32) + hf0 + hi;
+                    sok[hi] = ms.cok[cp][c];
+                    smask[hi] = ms.cmask[cp][c];
+                    sA[hi] = pre->sA[hi];
+                    sB[hi] = pre->sB[hi];
+                }
+            }
             unsigned long long c0 = etr ? clock64() : 0;
 #pragma unroll
-            for (int hf = 0; hf < NPC / 32; ++hf) {
+            for (int hi = 0; hi < kHF; ++hi) {
+                const int hf = hf0 + hi;
                 uint32_t r[32];
-                ptx::tmem_ld32(lane_base + col + hf * 32, r);
-                ptx::tmem_ld_wait();
+                if constexpr (FACT) {
+                    const float* sbase = P.s_in + soff + o;
+                    const int* sl = slc + colh * NPC + hf * 32;
+                    if (from_tmem) ptx::tmem_ld32(lane_base + col + hf * 32, r);
+                    // points are sorted by column record: a 32-point chunk uses one or two records
+                    if (sok[hi]) {
+                        if (from_tmem) ptx::tmem_ld_wait();
+                        const uint32_t m = smask[hi];
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) {
+                            const float sq = (m >> q) & 1u ? sB[hi] : sA[hi];
+                            r[q] = __float_as_uint((from_tmem ? __uint_as_float(r[q]) : 0.0f) + sq);
+                        }
+                    } else {  // three or more records in the chunk (rare): one load per point
+                        if (from_tmem) ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int q = 0; q < 32; ++q)
+                            r[q] = __float_as_uint((from_tmem ? __uint_as_float(r[q]) : 0.0f) +
+                                                   __ldg(sbase + (size_t)sl[q] * kSRow));
+                    }
+                } else {
+                    ptx::tmem_ld32(lane_base + col + hf * 32, r);
+                    ptx::tmem_ld_wait();
+                }
                 if (etr) {
                     const unsigned long long c1 = clock64();
                     e_cyc[0] += c1 - c0;
@@ -490,6 +706,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int q = 0; q < 32; ++q) {
                     const float x = __uint_as_float(r[q]) + fmaf(wz, zc[colh * NPC + hf * 32 + q], bo);
                     v[q] = x < 0.0f ? x * P.slope : x;
+                }
+                if constexpr (FACT) {
+                    // MN-major operand: this thread's feature is one 128-byte row (64 points) of its
+                    // K-chunk; points hf*32 + 8u .. +7 are the 16-byte chunk hf*4 + u (swizzled by row)
+                    const uint32_t fr = feat & 63u;
+                    const uint32_t rbase = (feat >> 6) * kChunk + fr * 128u;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        uint4 hv, lv;
+                        uint32_t* hp = reinterpret_cast<uint32_t*>(&hv);
+                        uint32_t* lp = reinterpret_cast<uint32_t*>(&lv);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float a = v[8 * u + 2 * i], b = v[8 * u + 2 * i + 1];
+                            hp[i] = pack_bf16(a, b);
+                            lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                        }
+                        const uint32_t off = rbase + ((((uint32_t)(hf * 4 + u)) ^ (fr & 7u)) << 4);
+                        ptx::st_cluster_v4(dst + off, hv);
+                        if (write_lo) ptx::st_cluster_v4(dst + lo_off + off, lv);
+                    }
+                    continue;
                 }
                 // rows (points) 8u + (lane & 7) of this hf block, 16-byte chunk of this lane group's 8 features
                 uint4 hv[4], lv[4];
@@ -511,28 +749,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
         };
-        auto h_begin = [&]() {
+        auto h_begin = [&](int buf = 0) {
             const unsigned long long t0 = etr ? gtime() : 0;
-            ptx::mbar_wait(&ms.h_free[rank], hfph);
-            hfph ^= 1;
+            ptx::mbar_wait(&ms.h_free[buf][rank], (hfph_bits >> buf) & 1u);
+            hfph_bits ^= 1u << buf;
+            (void)hfph;
             if (etr) {
                 e_t0 = gtime();
                 e_hf += e_t0 - t0;
             }
         };
-        auto h_end = [&]() {
+        auto h_end = [&](int buf = 0) {
             const unsigned long long c0 = etr ? clock64() : 0;
+            // every lane makes its own stores visible to the async proxy; after the warp
+            // barrier one lane arrives for the warp (256 remote arrivals per block would serialise)
             ptx::fence_proxy_async_cluster();
             ptx::tc_fence_before();
-            ptx::mbar_arrive_cluster(h_ready0);
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(h_ready0 + 16u * (uint32_t)buf);
             if (etr) {
                 e_cyc[2] += clock64() - c0;
                 e_emit += gtime() - e_t0;
             }
         };
         auto wait_acc = [&](uint64_t* bar, uint32_t& par) {
+            eev(400);
             const unsigned long long t0 = etr ? gtime() : 0;
             ptx::mbar_wait(bar, par);
+            eev(401);
             par ^= 1;
             ptx::tc_fence_after();
             if (etr) e_acc += gtime() - t0;
@@ -575,11 +819,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (et < NP) {
                 const unsigned idx = tg * NP + et;
                 double pd[3] = {0.0, 0.0, 0.0};
-                if (idx < n) job_point_d(job, idx, pd);
+                if constexpr (COLS) {
+                    // list entry = a column i + n j of the level grid; its node at k = 0 gives (x, y)
+                    if (idx < n) node_pos_d(job_node(job, idx), job.cells, pd);
+                } else {
+                    if (idx < n) job_point_d(job, idx, pd);
+                }
+                if constexpr (FACT) {
+                    int sl = 0;
+                    if (idx < n) {
+                        const uint32_t n1 = (uint32_t)job.cells + 1u, col = job_node(job, idx) % (n1 * n1);
+                        sl = P.cmap ? __ldg(&P.cmap[col]) : (int)col;
+                    }
+                    ms.slot[gb][et] = sl;
+                }
                 for (int d = 0; d < 3; ++d) ms.pos[gb][et][d] = (float)pd[d];
                 ms.z[gb][et] = (float)pd[2];
             }
             epi_bar();
+            if constexpr (FACT) {
+                // no Phi operand: the final layer's Phi dot is part of the column record
+                if (leader && et < NP) ms.skipdot[gb][0][et] = __ldg(&P.s_in[(size_t)ms.slot[gb][et] * kSRow + kSFinal]);
+                if (et < NP) {  // one warp per 32-point chunk
+                    const int c = et >> 5, sv = ms.slot[gb][et];
+                    const int first = __shfl_sync(0xffffffffu, sv, 0), last = __shfl_sync(0xffffffffu, sv, 31);
+                    const uint32_t m = __ballot_sync(0xffffffffu, sv == last);
+                    const uint32_t ok = __all_sync(0xffffffffu, sv == first || sv == last);
+                    if (lane == 0) {
+                        ms.cfirst[gb][c] = first;
+                        ms.clast[gb][c] = last;
+                        ms.cmask[gb][c] = m;
+                        ms.cok[gb][c] = ok;
+                    }
+                }
+                epi_bar();
+            } else
             // ---- gather Phi for this CTA's points into its skip operand ----
             // warp per point (2 in flight); lane = 8 consecutive channels = one 16-byte
             // SW128 chunk of the bf16 operand; the same pass computes the final
@@ -656,7 +930,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int o = 16; o > 0; o >>= 1) dot[c] += __shfl_xor_sync(0xffffffffu, dot[c], o);
                         if (lane == 0) {
-                            if (TEX) {
+                            if constexpr (COLS) {
+                                const unsigned gi = tg * NP + rank * NPC + (unsigned)pl;
+                                if (gi < n) P.s_out[(size_t)gi * kSRow + kSFinal] = dot[0];
+                            } else if (TEX) {
 #pragma unroll
                                 for (int c = 0; c < NOUT; ++c) ms.sdl[c][pl] = dot[c];
                             } else {
@@ -673,9 +950,239 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::fence_proxy_async_cluster();
-            ptx::mbar_arrive_cluster(f_ready0);
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(f_ready0);
         };
 
+        // ---- final layer (CTA 0 holds layer-4 rows 0..127 for all points) ----
+        auto final_layer = [&](unsigned t, int tp) {
+            const unsigned base = t * NP;
+            if (leader) {
+                const float bo = __ldg(&b4[row]), wz = __ldg(&b4[128 + row]);
+                float w5[NOUT];
+#pragma unroll
+                for (int c = 0; c < NOUT; ++c) w5[c] = __ldg(&P.wlast[c * wl_stride + row]);
+#pragma unroll
+                for (int hi = 0; hi < kHF; ++hi) {
+                const int hf = hf0 + hi;
+                    uint32_t r[32];
+                    float s4a = 0.0f, s4b = 0.0f;
+                    uint32_t s4m = 0, s4ok = 1;
+                    if (FACT) {
+                        const int c = colh * (NPC / 32) + hf;
+                        s4ok = ms.cok[tp][c];
+                        s4m = ms.cmask[tp][c];
+                        s4a = __ldg(&P.s_in[(size_t)ms.cfirst[tp][c] * kSRow + kSOffL(3) + row]);
+                        s4b = __ldg(&P.s_in[(size_t)ms.clast[tp][c] * kSRow + kSOffL(3) + row]);
+                    }
+                    ptx::tmem_ld32(lane_base + (FACT ? 3 * NP : 0) + hf * 32, r);
+                    ptx::tmem_ld_wait();
+                    float hx[32];
+#pragma unroll
+                    if (FACT && !s4ok) {  // three or more records in the chunk (rare)
+#pragma unroll 4
+                        for (int q = 0; q < 32; ++q)
+                            r[q] = __float_as_uint(__uint_as_float(r[q]) +
+                                                   __ldg(&P.s_in[(size_t)slc[colh * NPC + hf * 32 + q] * kSRow + kSOffL(3) + row]));
+                    }
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const float acc4 =
+                            FACT && s4ok ? __uint_as_float(r[q]) + ((s4m >> q) & 1u ? s4b : s4a) : __uint_as_float(r[q]);
+                        const float x = acc4 + fmaf(wz, zc[colh * NPC + hf * 32 + q], bo);
+                        hx[q] = x < 0.0f ? x * P.slope : x;
+                    }
+                    if constexpr (NOUT == 1) {  // in place: fewer live registers
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) hx[q] *= w5[0];
+                        ms.red[quarter][0][colh * NPC + hf * 32 + lane] = warp_transpose_reduce(hx);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < NOUT; ++c) {
+                            float v[32];
+#pragma unroll
+                            for (int q = 0; q < 32; ++q) v[q] = w5[c] * hx[q];
+                            ms.red[quarter][c][colh * NPC + hf * 32 + lane] = warp_transpose_reduce(v);
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            epi_bar();
+            if (leader) {
+                if (!FACT) {  // FACT: the leader read every point's Phi dot from the column records
+                    ptx::mbar_wait_cluster(&ms.sd_ready[tp], (sdph_bits >> tp) & 1u);
+                    sdph_bits ^= 1u << tp;
+                }
+                if (et < NP * NOUT) {
+                    const int p = et % NP, c = et / NP;
+                    const unsigned idx = base + p;
+                    const float s = ms.red[0][c][p] + ms.red[1][c][p] + ms.red[2][c][p] + ms.red[3][c][p] +
+                                    ms.skipdot[tp][c][p] + ms.cterm[FACT ? tp : c][p];
+                    if (idx < n) {
+                        float v = 1.0f / (1.0f + expf(-s));
+                        if (TEX) {
+                            if (job.out_pixel) {
+                                v = fminf(fmaxf(v, 0.0f), 1.0f);  // clamp01, render.hpp:276
+                                job.out[(size_t)job.out_pixel[idx] * 3 + c] = v;
+                            } else {
+                                job.out[(size_t)idx * 3 + c] = v;
+                            }
+                        } else if (job_is_grid(job)) {
+                            grid_epilogue(job, job_node(job, idx), v);
+                        } else {
+                            job.out[idx] = v;
+                        }
+                    }
+                }
+                if (!FACT) ptx::mbar_arrive(&ms.d4_free);  // D4 and this tile's skip dots consumed
+            }
+            epi_bar();
+        };
+
+        if constexpr (COLS) {
+            // ---- column pass: drain each 256-row block of S = W_Phi . Phi into the column records ----
+            uint32_t cb = 0;
+            gather_tile(pair_id, 0);
+            for (unsigned t = pair_id; t < ntiles; t += npairs) {
+                const int tp = (int)(tile_iter & 1u);
+                for (int b = 0; b < kColsBlocks; ++b) {
+                    const int a = (int)(cb & 3u);
+                    ptx::mbar_wait(&ms.accb[a], (cb >> 2) & 1u);
+                    ptx::tc_fence_after();
+                    // block b: layer-1 blocks 0-3, layer-2 blocks 0-1, layer 3, layer 4 (128 rows)
+                    const int roff = b < 4 ? b * 256 : (b < 6 ? 1024 + (b - 4) * 256 : (b == 6 ? 1536 : 1792));
+                    const bool valid = b < 7 || feat < 128u;
+#pragma unroll
+                    for (int hi = 0; hi < kHF; ++hi) {
+                const int hf = hf0 + hi;
+                        uint32_t r[32];
+                        ptx::tmem_ld32(lane_base + (uint32_t)a * NP + hf * 32, r);
+                        ptx::tmem_ld_wait();
+                        if (valid) {
+#pragma unroll
+                            for (int q = 0; q < 32; ++q) {
+                                const unsigned gi = t * NP + (unsigned)(colh * NPC + hf * 32 + q);
+                                if (gi < n) P.s_out[(size_t)gi * kSRow + roff + feat] = __uint_as_float(r[q]);
+                            }
+                        }
+                    }
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive_cluster(acc_free0 + 8u * (uint32_t)a);
+                    ++cb;
+                }
+                if (t + npairs < ntiles) {
+                    ptx::mbar_wait(&ms.skip_free, sfph);
+                    sfph ^= 1;
+                    gather_tile(t + npairs, tp ^ 1);
+                }
+                ++tile_iter;
+            }
+        } else if constexpr (FACT) {
+            const float* b1 = P.bias_g;
+            const float* b2 = b1 + 2 * 1024;
+            const float* b3 = b2 + 2 * 512;
+            auto emit_h = [&](uint32_t col, const float* bb, int od, int f0, int soff, bool tm, const Pre& pre) {
+                const int buf = (int)(hbe++ & 1u);
+                eev(500 + buf);
+                h_begin(buf);
+                eev(510 + buf);
+                emit_block(col, bb, od, f0, hdst + (uint32_t)buf * 2u * kHHalf, kHHalf, P.x3, soff, tm, &pre);
+                eev(520 + buf);
+                h_end(buf);
+                eev(530 + buf);
+            };
+            auto step_pre = [&](int kk, int cp) {
+                const int l = kk < 4 ? 0 : (kk < 6 ? 1 : 2);
+                const int blk = kk < 4 ? kk : (kk < 6 ? kk - 4 : 0);
+                return fact_pre(l == 0 ? b1 : (l == 1 ? b2 : b3), 1024 >> l, blk * 256, kSOffL(l), cp);
+            };
+            // -sdf_scale * sdf(P) + b5 + w5z z of the tile's points (parity gb): two threads per point
+            // split the capsules (same per-capsule arithmetic as scene_sdf_f)
+            auto fact_cterm = [&](int gb) {
+                const int p = et >> 1, h = et & 1;
+                const float* P3 = ms.pos[gb][p];
+                float d = 3.0e38f;
+                const int nc = ms.ncaps;
+                if (nc >= 0) {
+                    for (int i = h; i < nc; i += 2) {
+                        const float* c = ms.caps[i];
+                        const float pa0 = P3[0] - c[0], pa1 = P3[1] - c[1], pa2 = P3[2] - c[2];
+                        float hh = 0.0f;
+                        if (c[6] > 0.0f) hh = fminf(fmaxf((pa0 * c[3] + pa1 * c[4] + pa2 * c[5]) / c[6], 0.0f), 1.0f);
+                        const float v0 = pa0 - hh * c[3], v1 = pa1 - hh * c[4], v2 = pa2 - hh * c[5];
+                        d = fminf(d, sqrtf(v0 * v0 + v1 * v1 + v2 * v2) - c[7]);
+                    }
+                    d = fminf(d, __shfl_xor_sync(0xffffffffu, d, 1));
+                    if (nc == 0) d = 0.0f;
+                } else if (h == 0) {
+                    d = scene_sdf_f(f.fscene, P3);
+                }
+                if (h == 0 && p < NP)
+                    ms.cterm[gb][p] = __ldg(&b5[0]) + __ldg(&P.wlast[wl_stride - 1]) * ms.z[gb][p] -
+                                      __ldg(&f.fscene->sdf_scale) * d;
+            };
+            // Per tile t the epilogue emits layer-1 chunks 2-3 of t; then, while the tensor cores
+            // finish layer 2 of t, the final layer of t-1 and the gather of t+1; then layers 2-3 of t
+            // and layer-1 chunks 0-1 of t+1 (so layer 2 of t+1 follows layer 4 of t at once).
+            // One emit site: the epilogue is large and inlining it per step costs registers.
+            const float* b_of[3] = {b1, b2, b3};
+            (void)b_of;
+            auto run_steps = [&](int k0, int k1, int cp) {
+                Pre cur = step_pre(k0, cp);
+#pragma unroll 1
+                for (int k = k0; k < k1; ++k) {
+                    Pre nxt = cur;
+                    if (k + 1 < k1) nxt = step_pre(k + 1, cp);  // in flight during this block
+                    if (k == 4) wait_acc(&ms.d2done, d2ph);
+                    if (k == 6) wait_acc(&ms.d3done, d3ph);
+                    const int l = k < 4 ? 0 : (k < 6 ? 1 : 2);
+                    const int blk = k < 4 ? k : (k < 6 ? k - 4 : 0);
+                    emit_h(l == 0 ? 0u : (uint32_t)(l == 1 ? blk : 2) * NP, l == 0 ? b1 : (l == 1 ? b2 : b3),
+                           1024 >> l, blk * 256, kSOffL(l), l > 0, cur);
+                    cur = nxt;
+                }
+            };
+            auto set_tile = [&](int gb) {
+                zc = ms.z[gb];
+                slc = ms.slot[gb];
+                ms_tile_parity = gb;
+            };
+            gather_tile(pair_id, 0);
+            fact_cterm(0);
+            set_tile(0);
+            run_steps(0, 2, 0);
+            for (unsigned t = pair_id; t < ntiles; t += npairs) {
+                const int tp = (int)(tile_iter & 1u);
+                const bool has_next = t + npairs < ntiles;
+                set_tile(tp);
+                run_steps(2, 4, tp);
+                if (t != pair_id) {  // the previous tile's final layer (its D4 is long done)
+                    set_tile(tp ^ 1);
+                    wait_acc(&ms.d4done, d4ph);
+                    eev(600);
+                    final_layer(t - npairs, tp ^ 1);
+                    eev(601);
+                }
+                if (has_next) {
+                    gather_tile(t + npairs, tp ^ 1);
+                    fact_cterm(tp ^ 1);
+                }
+                set_tile(tp);
+                run_steps(4, 7, tp);
+                if (has_next) {
+                    set_tile(tp ^ 1);
+                    run_steps(0, 2, tp ^ 1);
+                }
+                ++tile_iter;
+            }
+            {  // the last tile's final layer
+                const int tp = (int)((tile_iter - 1u) & 1u);
+                set_tile(tp);
+                wait_acc(&ms.d4done, d4ph);
+                final_layer(pair_id + (tile_iter - 1u) * npairs, tp);
+            }
+        } else {
         gather_tile(pair_id, 0);
         for (unsigned t = pair_id; t < ntiles; t += npairs) {
             const unsigned base = t * NP;
@@ -741,63 +1248,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 gather_tile(t + npairs, tp ^ 1);
             }
             wait_acc(&ms.d4done, d4ph);
-            // ---- final layer (CTA 0 holds layer-4 rows 0..127 for all points) ----
-            if (leader) {
-                const float bo = __ldg(&b4[row]), wz = __ldg(&b4[128 + row]);
-                float w5[NOUT];
-#pragma unroll
-                for (int c = 0; c < NOUT; ++c) w5[c] = __ldg(&P.wlast[c * wl_stride + row]);
-#pragma unroll
-                for (int hf = 0; hf < NPC / 32; ++hf) {
-                    uint32_t r[32];
-                    ptx::tmem_ld32(lane_base + hf * 32, r);
-                    ptx::tmem_ld_wait();
-                    float hx[32];
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        const float x = __uint_as_float(r[q]) + fmaf(wz, zc[colh * NPC + hf * 32 + q], bo);
-                        hx[q] = x < 0.0f ? x * P.slope : x;
-                    }
-#pragma unroll
-                    for (int c = 0; c < NOUT; ++c) {
-                        float v[32];
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) v[q] = w5[c] * hx[q];
-                        ms.red[quarter][c][colh * NPC + hf * 32 + lane] = warp_transpose_reduce(v);
-                    }
-                }
-            }
-            ptx::tc_fence_before();
-            epi_bar();
-            if (leader) {
-                ptx::mbar_wait_cluster(&ms.sd_ready[tp], sdph[tp]);
-                sdph[tp] ^= 1;
-                if (et < NP * NOUT) {
-                    const int p = et % NP, c = et / NP;
-                    const unsigned idx = base + p;
-                    const float s = ms.red[0][c][p] + ms.red[1][c][p] + ms.red[2][c][p] + ms.red[3][c][p] +
-                                    ms.skipdot[tp][c][p] + ms.cterm[c][p];
-                    if (idx < n) {
-                        float v = 1.0f / (1.0f + expf(-s));
-                        if (TEX) {
-                            if (job.out_pixel) {
-                                v = fminf(fmaxf(v, 0.0f), 1.0f);  // clamp01, render.hpp:276
-                                job.out[(size_t)job.out_pixel[idx] * 3 + c] = v;
-                            } else {
-                                job.out[(size_t)idx * 3 + c] = v;
-                            }
-                        } else if (job_is_grid(job)) {
-                            grid_epilogue(job, job_node(job, idx), v);
-                        } else {
-                            job.out[idx] = v;
-                        }
-                    }
-                }
-                ptx::mbar_arrive(&ms.d4_free);  // D4 and this tile's skip dots consumed
-            }
-            epi_bar();
+            final_layer(t, tp);
             ++tile_iter;
         }
+        }  // GEO / TEX
         if (etr) {
             P.trace[4] = gtime() - e_begin;
             P.trace[5] = e_acc;
@@ -840,11 +1294,13 @@ size_t pair_stream_bytes(int which, bool x3) {
 }
 
 // item i, rank r (rows r*128.. of the 256-row block), part (hi/lo): 16 KB SW128 tile
-int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi) {
+// sched: 0 = full network (pair::schedule), 1 = FACT items, 2 = COLS items (geometry only)
+static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi) {
     const bool geo = which == ICG_MLP_GEOMETRY;
     const int* outs = geo ? kGeoOut : kTexOut;
     const int skip = geo ? kGeoSkip : kTexSkip;
-    const int nitems = geo ? pair::kGeoItems : pair::kTexItems;
+    const int nitems = sched == 1 ? pair::kFactItems
+                                  : sched == 2 ? pair::kColsItems : (geo ? pair::kGeoItems : pair::kTexItems);
     int ins[5];
     for (int l = 0; l < 5; ++l) ins[l] = (l ? outs[l - 1] : 0) + skip;
     int item = 0;
@@ -868,8 +1324,25 @@ int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* str
         }
         ++item;
     };
-    pair::schedule(geo ? 4 : 8, true, emit);
+    if (sched == 1)
+        pair::schedule_fact(emit);
+    else if (sched == 2)
+        pair::schedule_cols(emit);
+    else
+        pair::schedule(geo ? 4 : 8, true, emit);
     return item == nitems ? ICG_OK : ICG_ERUNTIME;
+}
+
+int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi) {
+    return pair_pack_sched(which, 0, w, stream_x3, stream_hi);
+}
+
+size_t pair_fact_stream_bytes(int part, bool x3) {
+    return (size_t)(part == 0 ? pair::kFactItems : pair::kColsItems) * (x3 ? 4 : 2) * pair::kHalf;
+}
+
+int pair_pack_factored(const float* const* w, int part, uint8_t* stream_x3, uint8_t* stream_hi) {
+    return pair_pack_sched(ICG_MLP_GEOMETRY, part == 0 ? 1 : 2, w, stream_x3, stream_hi);
 }
 
 int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-byte CUtensorMap */) {
@@ -899,12 +1372,13 @@ int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-b
     return ICG_OK;
 }
 
-template <bool TEX>
+template <int MODE>
 static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, unsigned max_points, cudaStream_t s) {
-    using C = pair::Cfg<TEX>;
+    using C = pair::Cfg<MODE>;
+    constexpr bool TEX = MODE == pair::kModeTex;
     static bool attr = false;
     if (!attr) {
-        ICG_CUDA_TRY(cudaFuncSetAttribute(pair::k_mlp_pair<TEX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        ICG_CUDA_TRY(cudaFuncSetAttribute(pair::k_mlp_pair<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)C::kTotal));
         attr = true;
     }
@@ -913,17 +1387,17 @@ static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, uns
     if (tron < 0) {
         const char* e = getenv("ICG_TC_TRACE");
         tron = e && e[0] == '1';
-        if (tron) cudaMallocManaged(&trace, 64 * sizeof(unsigned long long));
+        if (tron) cudaMallocManaged(&trace, 2048 * sizeof(unsigned long long));
     }
     p.trace = tron ? trace : nullptr;
-    if (p.trace) cudaMemsetAsync(p.trace, 0, 64 * 8, s);
+    if (p.trace) cudaMemsetAsync(p.trace, 0, 2048 * 8, s);
     unsigned pairs = (max_points + C::NP - 1) / C::NP;
     if (pairs > 74) pairs = 74;
     if (pairs == 0) pairs = 1;
     CUtensorMap ta, tb;
     std::memcpy(&ta, tmapA, sizeof(CUtensorMap));
     std::memcpy(&tb, tmapB ? tmapB : tmapA, sizeof(CUtensorMap));
-    pair::k_mlp_pair<TEX><<<2 * pairs, pair::kThreads, C::kTotal, s>>>(ta, tb, p);
+    pair::k_mlp_pair<MODE><<<2 * pairs, C::kThreads, C::kTotal, s>>>(ta, tb, p);
     ICG_CUDA_TRY(cudaGetLastError());
     if (p.trace) {
         cudaStreamSynchronize(s);
@@ -931,9 +1405,28 @@ static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, uns
         fprintf(stderr,
                 "[pair-trace %s] mma: total %.1f us, wait data %.1f, wait h %.1f, wait f %.1f | epi: total %.1f, wait acc "
                 "%.1f, wait hfree %.1f, emit %.1f\n",
-                TEX ? "tex" : "geo", t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3,
+                TEX ? "tex" : (MODE == pair::kModeGeo ? "geo" : (MODE == pair::kModeCols ? "cols" : "fact")), t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3,
                 t[6] * 1e-3, t[7] * 1e-3);
         fprintf(stderr, "    epi cycles: tmem-ld %llu, convert+store %llu, fence+arrive %llu\n", t[8], t[9], t[10]);
+        if (getenv("ICG_TC_EVENTS") && (t[64] || t[576])) {
+            // merged event log of block 0: MMA (m) and epilogue thread 0 (e), us from the first event
+            unsigned long long t0 = ~0ull;
+            for (int i = 0; i < 256; ++i) {
+                if (t[64 + i] && t[64 + i] < t0) t0 = t[64 + i];
+                if (t[576 + i] && t[576 + i] < t0) t0 = t[576 + i];
+            }
+            int a = 0, b = 0;
+            while ((a < 256 && t[64 + a]) || (b < 256 && t[576 + b])) {
+                const bool ta = a < 256 && t[64 + a], tb = b < 256 && t[576 + b];
+                if (ta && (!tb || t[64 + a] <= t[576 + b])) {
+                    fprintf(stderr, "  m %8.2f %llu\n", (t[64 + a] - t0) * 1e-3, t[320 + a]);
+                    ++a;
+                } else {
+                    fprintf(stderr, "  e %8.2f %llu\n", (t[576 + b] - t0) * 1e-3, t[832 + b]);
+                    ++b;
+                }
+            }
+        }
     }
     return ICG_OK;
 }
@@ -949,7 +1442,38 @@ int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap,
     p.total_a = pair::kGeoItems;
     p.slope = 0.02f;
     p.x3 = x3 ? 1 : 0;
-    return launch_pair<false>(p, tmap, nullptr, max_points, s);
+    return launch_pair<pair::kModeGeo>(p, tmap, nullptr, max_points, s);
+}
+
+int launch_pifu_pair_cols(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& cols, float* records,
+                          unsigned max_cols, bool x3, cudaStream_t s) {
+    pair::Params p{};
+    p.f = f;
+    p.job = cols;
+    p.bias_g = geo.bias;
+    p.wlast = geo.w_last;
+    p.items_a = pair::kColsItems;
+    p.total_a = pair::kColsItems;
+    p.slope = 0.02f;
+    p.x3 = x3 ? 1 : 0;
+    p.s_out = records;
+    return launch_pair<pair::kModeCols>(p, tmap, nullptr, max_cols, s);
+}
+
+int launch_pifu_pair_fact(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
+                          const float* records, const int* cmap, unsigned max_points, bool x3, cudaStream_t s) {
+    pair::Params p{};
+    p.f = f;
+    p.job = job;
+    p.bias_g = geo.bias;
+    p.wlast = geo.w_last;
+    p.items_a = pair::kFactItems;
+    p.total_a = pair::kFactItems;
+    p.slope = 0.02f;
+    p.x3 = x3 ? 1 : 0;
+    p.s_in = records;
+    p.cmap = cmap;
+    return launch_pair<pair::kModeFact>(p, tmap, nullptr, max_points, s);
 }
 
 int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const void* tmap_geo,
@@ -967,7 +1491,7 @@ int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& t
     p.total_b = pair::kTexItems;
     p.slope = 0.02f;
     p.x3 = x3 ? 1 : 0;
-    return launch_pair<true>(p, tmap_geo, tmap_tex, max_points, s);
+    return launch_pair<pair::kModeTex>(p, tmap_geo, tmap_tex, max_points, s);
 }
 
 }  // namespace icg

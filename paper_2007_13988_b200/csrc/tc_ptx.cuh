@@ -131,6 +131,20 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr) {
     return d;
 }
 
+// MN-major, 128-byte swizzle (canonical ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-byte units):
+// each 128-byte row holds 64 consecutive M/N elements of ONE k; 8 k-rows form a 1 KB swizzle
+// atom (16-byte chunks XORed with k % 8); atoms stacked along k at SBO = 1024 B.  Used for
+// operands written one k (feature) per thread, where a K-major layout would need a transpose.
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)(8192u >> 4) << 16;   // LBO: next 64-element group along M/N (unused for N <= 64)
+    d |= (uint64_t)(1024u >> 4) << 32;   // SBO: next 8 k-rows
+    d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    return d;
+}
+
 // Instruction descriptor: kind::f16, A = B = bf16, D = f32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
     return (1u << 4)            // D format f32

@@ -255,3 +255,21 @@ def test_config2_full_size_properties(gpu_ctx, pifu_inputs):
     i, j, k = idx % n, (idx // n) % n, idx // (n * n)
     pts = np.stack([-1 + 2 * i / 256.0, -1 + 2 * j / 256.0, 1 - 2 * k / 256.0], 1)
     assert np.abs(ext.values[idx] - m.occupancy(pts)).max() <= OCC_TOL_FP32
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("yaw,pitch", [(0, 0), (30, 20), (135, -40), (90, 0), (270, 75)])
+def test_render_general_cameras_exact(gpu_ctx, pifu_inputs, yaw, pitch):
+    """Empty-space skipping in the ray pass must not change a single crossing,
+    depth bit, or the grazing / degenerate counters, for oblique rays too."""
+    f = _pifu(gpu_ctx, pifu_inputs, abi.ICG_PREC_FP32)
+    cfg = api.AlgoConfig("progressive", 16, 3)
+    cam = api.CameraSpec.from_angles(yaw, pitch)
+    W, H = 200, 150
+    ext, img = gpu_ctx.frame(f, cfg, cam, W, H, want_grid=True)
+    r = O.render_first_crossing(ext.values, 128, O.camera_from_angles(yaw, pitch), W, H)
+    assert np.array_equal(img.mask, r["mask"])
+    assert np.array_equal(img.surface_k, r["surface_k"])
+    assert np.array_equal(img.depth, r["depth"])
+    assert img.covered_pixels == r["covered"] and img.degenerate_brackets == r["degenerate"]
+    assert img.grazing_pixels == r["grazing"]
