@@ -80,7 +80,9 @@ struct icg_context {
     DBuf geo_fact_stream[2][2];
     alignas(64) unsigned char geo_fact_tmap[2][2][128] = {};
     bool geo_fact = false, use_fact = true;
-    DBuf colrec, cmap, collist, colcnt, sorted;
+    DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
+    bool use_tail = true;
+    unsigned tail_max = 100;  // conflict batches up to this size start the persistent tail kernel
     bool use_pair = true;
     // field
     DBuf scene;
@@ -411,6 +413,38 @@ int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned
     return r;
 }
 
+int issue_tail(icg_context* c, const FieldDev& fd, const LevelBufs& lb, int level, int fcells, int it, int max_iters,
+               unsigned nf) {
+    const unsigned cap_pts = 4096, cap_new = 4096;
+    const size_t plane = ((size_t)fcells + 1) * ((size_t)fcells + 1);
+    if (int r = c->tail_scratch.ensure(tail_scratch_bytes(cap_pts, cap_new, (unsigned)plane))) return r;
+    TailParams tp{};
+    tp.f = fd;
+    tp.cells = fcells;
+    tp.level = level;
+    tp.it0 = it;
+    tp.max_iters = max_iters;
+    tp.cap = nf;
+    tp.max_start = c->tail_max;
+    tp.fv = lb.fv;
+    tp.fs = lb.fs;
+    tp.tentbin = lb.tentbin;
+    tp.queued = c->queued.as<uint32_t>();
+    for (int b = 0; b < 2; ++b) {
+        tp.cf[b] = c->cf[b].as<uint32_t>();
+        tp.nx[b] = c->nx[b].as<uint32_t>();
+    }
+    tp.ctr = c->ctr.as<DevCounters>();
+    tp.colrec = c->colrec.as<float>();
+    tp.cmap = c->cmap.as<int>();
+    tp.collist = c->collist.as<uint32_t>();
+    for (int l = 0; l < 4; ++l) tp.w[l] = c->geo_rows[l];
+    tp.bias = c->geo_tc.bias;
+    tp.wlast = c->geo_tc.w_last;
+    tp.slope = 0.02f;
+    return launch_tail(tp, c->tail_scratch.as<uint8_t>(), cap_pts, cap_new, (unsigned)plane, c->stream);
+}
+
 // Issues one whole extraction on the context stream (no host sync).
 int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg) {
     prof_discard(c);
@@ -511,7 +545,28 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                 cj.evals = &ctr->evals[l];
                 cj.iters = &ctr->conflict_iters[l];
                 cj.overflow = &ctr->overflow;
-                if (int r = run_eval(c, fd, cj, (unsigned)nf, true)) return r;
+                if (fact_ok(c, fd) && c->use_tail && c->geo_pair) {
+                    // large batches: the CTA-pair kernel; the first small one starts the persistent tail,
+                    // which finishes the level's chain (k_tail.cu)
+                    // (mid-size batches: 64-point pair tiles, twice as many pairs busy per wave)
+                    const unsigned mid_max = 74u * 64u;
+                    EvalJob big = cj, mid = cj;
+                    big.min_count = std::max(c->tail_max, mid_max) + 1;
+                    mid.min_count = c->tail_max + 1;
+                    mid.max_count = mid_max;
+                    int slot = prof_begin(c, 0);
+                    const bool x3 = fd.precision == ICG_PREC_FP32;
+                    const void* tm = c->geo_pair_tmap[x3 ? 0 : 1];
+                    int r = launch_pifu_pair_eval(fd, c->geo_tc, tm, big, (unsigned)nf, x3, c->stream);
+                    if (!r && c->tail_max < mid_max)
+                        r = launch_pifu_pair_eval_small(fd, c->geo_tc, tm, mid, mid_max, x3, c->stream);
+                    if (!r) r = issue_tail(c, fd, lb, l, fcells, it, max_iters, (unsigned)nf);
+                    prof_end(c, slot);
+                    c->launches += 3;
+                    if (r) return r;
+                } else if (int r = run_eval(c, fd, cj, (unsigned)nf, true)) {
+                    return r;
+                }
             }
             if (int r = launch_unroll_check(ctr, unroll & 1, l, c->stream)) return r;
             c->launches += 1;
@@ -682,8 +737,13 @@ bool adapt_unroll(icg_context* c, const icg_algo_config* cfg) {
     }
     if (!replay)
         for (int l = 1; l <= cfg->target_level; ++l) {
-            int need = (int)h.conflict_iters[l];
-            c->unroll[l] = need + std::max(2, need / 4);
+            // host-side iterations: up to the one where the persistent tail took over
+            // (once started, the tail finishes the level: a margin of one iteration covers frames
+            // whose chain hands over one iteration later)
+            if (h.tail_start[l])
+                c->unroll[l] = (int)h.tail_start[l] + 1;
+            else
+                c->unroll[l] = (int)h.conflict_iters[l] + std::max(2, (int)h.conflict_iters[l] / 4);
         }
     return replay;
 }
@@ -744,6 +804,8 @@ int icg_create(int device, icg_context** out) {
     c->device = device;
     if (const char* e = getenv("ICG_NO_PAIR")) c->use_pair = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_FACT")) c->use_fact = !(e[0] == '1');
+    if (const char* e = getenv("ICG_NO_TAIL")) c->use_tail = !(e[0] == '1');
+    if (const char* e = getenv("ICG_TAIL_MAX")) c->tail_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_SMALL_MAX")) c->small_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_LP_MAX")) c->lp_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_LAT")) c->lat_small = std::string(e) == "small";
@@ -772,7 +834,7 @@ int icg_destroy(icg_context* c) {
                    &c->scene, &c->fscene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
                    &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->lp_scratch, &c->lp_stream, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi,
-                   &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx, &c->colrec, &c->cmap, &c->collist, &c->colcnt, &c->sorted,
+                   &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx, &c->colrec, &c->cmap, &c->collist, &c->colcnt, &c->sorted, &c->tail_scratch,
                    &c->geo_fact_stream[0][0], &c->geo_fact_stream[0][1], &c->geo_fact_stream[1][0],
                    &c->geo_fact_stream[1][1]};
     for (DBuf* b : all) b->release();

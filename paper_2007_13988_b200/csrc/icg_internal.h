@@ -42,9 +42,11 @@ struct DevCounters {
     unsigned long long evals[ICG_MAX_LEVELS];
     unsigned long long refined[ICG_MAX_LEVELS];
     unsigned int conflict_iters[ICG_MAX_LEVELS];
+    unsigned int ncols;               // column-factored field: distinct columns of the current batch
+    unsigned int tail_start[ICG_MAX_LEVELS];  // 1 + host iteration at which k_tail took over (0: never)
+    // render counters (cleared per render: everything from `covered` to the end)
     unsigned long long covered, degenerate, grazing;
     unsigned int surface_count;
-    unsigned int ncols;               // column-factored field: distinct columns of the current batch
 };
 
 // Analytic scene in constant-friendly form (union of primitives).
@@ -121,6 +123,7 @@ struct EvalJob {
     unsigned int* iters;          // += (count > 0) (block 0)
     unsigned int* overflow;
     unsigned int min_count;       // tensor-core kernel: leave batches below this to the latency path
+    unsigned int max_count;       // ... and above this (nonzero) to the large-tile kernel
     // point epilogue
     float* out;                   // occupancy per point (or rgb x3 for texture)
     const uint32_t* out_pixel;    // texture: pixel index per point (out = rgb image)
@@ -156,6 +159,9 @@ size_t pair_fact_stream_bytes(int part, bool x3);
 int pair_pack_factored(const float* const* w, int part, uint8_t* stream_x3, uint8_t* stream_hi);
 int launch_pifu_pair_cols(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& cols, float* records,
                           unsigned max_cols, bool x3, cudaStream_t s);
+// geometry field with 64-point pair tiles (twice the pairs busy on mid-size batches)
+int launch_pifu_pair_eval_small(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
+                                unsigned max_points, bool x3, cudaStream_t s);
 int launch_pifu_pair_fact(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
                           const float* records, const int* cmap, unsigned max_points, bool x3, cudaStream_t s);
 int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
@@ -191,6 +197,36 @@ int launch_conflict_expand(uint32_t* fine_queued, const uint8_t* fs, int fcells,
                            DevCounters* ctr, int iter, int max_iters, uint32_t* next_list,
                            unsigned int cap, cudaStream_t s);
 int launch_unroll_check(DevCounters* ctr, int iter_parity, int level, cudaStream_t s);
+// persistent conflict-loop tail (k_tail.cu)
+struct TailParams {
+    FieldDev f;
+    int cells, level, it0, max_iters;
+    unsigned cap, max_start;
+    float* fv;
+    uint8_t* fs;
+    const uint32_t* tentbin;
+    uint32_t* queued;
+    uint32_t* cf[2];
+    uint32_t* nx[2];
+    DevCounters* ctr;
+    float* colrec;
+    int* cmap;
+    uint32_t* collist;
+    const float* w[4];      // geometry layers 1-4, row-major [out][in] fp32
+    const float* bias;      // tc layout: per layer [b, wz], then b5
+    const float* wlast;     // final layer [128 + 257]
+    float slope;
+    // scratch (launch_tail carves it)
+    float *h1, *h2, *h3, *h4, *pz, *phi;
+    int* pslot;
+    unsigned *newcols, *nnew;
+    unsigned cap_pts, cap_new;
+    unsigned long long* trace;  // ICG_TAIL_TRACE=1: phase times of block 0
+};
+size_t tail_smem_bytes();
+size_t tail_scratch_bytes(unsigned cap_pts, unsigned cap_new, unsigned max_cols);
+int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_new, unsigned max_cols, cudaStream_t s);
+
 // column-factored field: give every distinct column (i + n j) of a node list a record slot
 // (cmap[col] = slot, collist[slot] = col, ctr->ncols = number of slots); cmap must be all -1
 int launch_col_claim(const uint32_t* list, const unsigned* count, int cells, int* cmap, uint32_t* collist,

@@ -59,7 +59,7 @@ constexpr int kMaxStages = 6;
 //   FACT : column-factored geometry field: under the orthographic projection every node of a
 //          column shares Phi, so layer 1 is act(S1[col] + w1z z + b1) (no MMA) and layers 2-4
 //          only multiply the hidden part: W_h . h + S_l[col]
-enum { kModeGeo = 0, kModeTex = 1, kModeCols = 2, kModeFact = 3 };
+enum { kModeGeo = 0, kModeTex = 1, kModeCols = 2, kModeFact = 3, kModeGeo64 = 4 };
 constexpr int kSRow = 1936;    // floats per column record: [1024 | 512 | 256 | 128 | final Phi dot | pad]
 constexpr int kSFinal = 1920;  // offset of the final layer's Phi dot
 __host__ __device__ constexpr int kSOffL(int l) { return l == 0 ? 0 : l == 1 ? 1024 : l == 2 ? 1536 : 1792; }
@@ -67,13 +67,13 @@ __host__ __device__ constexpr int kSOffL(int l) { return l == 0 ? 0 : l == 1 ? 1
 template <int MODE>
 struct Cfg {
     static constexpr bool TEX = MODE == kModeTex;
-    static constexpr int NPC = TEX ? 32 : 64;        // points per CTA
+    static constexpr int NPC = (TEX || MODE == kModeGeo64) ? 32 : 64;  // points per CTA
     static constexpr int NP = 2 * NPC;               // points per pair tile = MMA N
     // [Phi] or [Phi, h3] in 64-wide K-chunks (none for FACT: Phi enters through the column records)
     static constexpr int kSkipChunks = TEX ? 8 : (MODE == kModeFact ? 0 : 4);
     static constexpr int kHBufs = MODE == kModeFact ? 2 : (MODE == kModeCols ? 0 : 1);  // h operand buffers
     // 32 KB stages (per-copy TMA cost is size-independent)
-    static constexpr int kStages = TEX ? 3 : (MODE == kModeCols ? 4 : 2);
+    static constexpr int kStages = TEX ? 3 : ((MODE == kModeCols || MODE == kModeGeo64) ? 4 : 2);
     static constexpr uint32_t kChunk = NPC * 128;  // NPC point rows x 64 bf16 (SW128)
     static constexpr uint32_t kSkipHalf = kSkipChunks * kChunk;
     static constexpr uint32_t kHHalf = 4 * kChunk;  // one 256-feature block
@@ -305,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
     const EvalJob& job = P.job;
     const unsigned pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const unsigned n = job_count(job);
-    if (n < job.min_count) return;  // small batch: latency path
+    if (n < job.min_count || (job.max_count && n > job.max_count)) return;  // not this kernel's size class
     if (pair_id * NP >= n) {        // both CTAs of the pair take the same decision
         job_account(job);
         return;
@@ -1443,6 +1443,20 @@ int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap,
     p.slope = 0.02f;
     p.x3 = x3 ? 1 : 0;
     return launch_pair<pair::kModeGeo>(p, tmap, nullptr, max_points, s);
+}
+
+int launch_pifu_pair_eval_small(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
+                                unsigned max_points, bool x3, cudaStream_t s) {
+    pair::Params p{};
+    p.f = f;
+    p.job = job;
+    p.bias_g = geo.bias;
+    p.wlast = geo.w_last;
+    p.items_a = pair::kGeoItems;
+    p.total_a = pair::kGeoItems;
+    p.slope = 0.02f;
+    p.x3 = x3 ? 1 : 0;
+    return launch_pair<pair::kModeGeo64>(p, tmap, nullptr, max_points, s);
 }
 
 int launch_pifu_pair_cols(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& cols, float* records,
