@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 GEO_FLOP_PER_POINT = 2363906
+FACT_MMA_FLOP_PER_POINT = 2 * (512 * 1024 + 256 * 512 + 128 * 256)  # hidden parts of layers 2-4
 TEX_FLOP_PER_POINT = 3350022 + 2231808
 METRIC = "frames/sec (256^3 recon + 512² render) at 1/2/4/8 B200; MLP points/sec vs TC peak"
 
@@ -198,8 +199,9 @@ def workload_config(cfg_name: str, args) -> dict:
                         f"feature map {c}x{h}x{w}, {res}x{res} first-crossing render yaw 90 + texture MLP; "
                         "frames sharded round-robin over GPUs (configs[4] pattern)",
             "precision": prec if args.precision is None else args.precision,
-            "frames_per_gpu_resident": args.frames, "l2": "flushed between frames (320 MB device copy); "
-                                                          "inputs cycle over distinct feature maps",
+            "frames_in_flight_per_gpu": args.streams,
+            "feature_maps_per_stream": args.frames, "l2": "flushed before every frame (320 MB device copy on "
+                                                          "the frame's stream); inputs cycle over distinct feature maps",
             "parallelism": f"frame-sharded x{args.gpus}, no per-frame collective"}
 
 
@@ -214,7 +216,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="config2", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "bf16", "simt"])
-    ap.add_argument("--frames", type=int, default=8, help="distinct device-resident feature maps per GPU")
+    ap.add_argument("--frames", type=int, default=4, help="distinct device-resident feature maps per stream")
+    ap.add_argument("--l2", default="flush", choices=["flush", "cycle"],
+                    help="flush: 320 MB device copy before every frame; cycle: no flush, the distinct "
+                         "feature maps cycled over (streams x frames x 16.8 MB) exceed the 126 MB L2")
+    ap.add_argument("--streams", type=int, default=3,
+                    help="frames in flight per GPU (one context + stream + host thread each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -244,38 +251,12 @@ def main():
         prec_name = args.precision
     prec = {"fp32": abi.ICG_PREC_FP32, "bf16": abi.ICG_PREC_BF16, "simt": abi.ICG_PREC_FP32_SIMT}[prec_name]
     caps, gw, gb, tw, tb = make_inputs(cfg_name)
-    ctx = api.Context(local_rank)
-    ctx.set_mlp(abi.ICG_MLP_GEOMETRY, gw, gb)
-    ctx.set_mlp(abi.ICG_MLP_TEXTURE, tw, tb)
+    S = max(1, args.streams)
     cfg = api.AlgoConfig("progressive", r0, lv)
     cam = api.CameraSpec.from_angles(90, 0)
     fbytes = C_ * H_ * W_ * 4
     npx = res * res
-
-    # distinct feature maps: pinned host copies (e2e) and device-resident copies (value)
-    nF = args.frames
-    host_maps, dev_maps = [], []
-    for i in range(nF):
-        fm = api.gen_feature_map(fmap_seed(rank, i), C_, H_, W_)
-        hp = api.host_alloc(fbytes)
-        np.ctypeslib.as_array((np.ctypeslib.ctypes.c_float * fm.size).from_address(hp))[:] = fm.reshape(-1)
-        dp = ctx.device_alloc(fbytes)
-        ctx.memcpy(dp, hp, fbytes, abi.ICG_MEM_DEVICE, abi.ICG_MEM_HOST)
-        host_maps.append(hp)
-        dev_maps.append(dp)
-    fields_dev = [api.PifuField(None, caps, 50.0, prec, device_ptr=dp, shape=(C_, H_, W_)) for dp in dev_maps]
-    fields_host = []
-    for hp in host_maps:
-        f = api.PifuField(None, caps, 50.0, prec, device_ptr=hp, shape=(C_, H_, W_))
-        f.c.fmap_mem = abi.ICG_MEM_HOST
-        fields_host.append(f)
-
-    # device-resident outputs for `value`; pinned host outputs for `e2e`
     import ctypes as C
-    dout = {k: ctx.device_alloc(b) for k, b in (("depth", npx * 4), ("rgb", npx * 12), ("mask", npx),
-                                                 ("sk", npx * 4))}
-    hout = {k: api.host_alloc(b) for k, b in (("depth", npx * 4), ("rgb", npx * 12), ("mask", npx),
-                                               ("sk", npx * 4))}
 
     def img_struct(bufs, mem):
         img = abi.icg_image()
@@ -286,12 +267,50 @@ def main():
         img.surface_k = C.cast(C.c_void_p(bufs["sk"]), abi.i32p)
         return img
 
-    flush_a = ctx.device_alloc(320 << 20)
-    flush_b = ctx.device_alloc(320 << 20)
+    class Lane:
+        """One context (stream) of this GPU: its own frames in flight, driven by one host thread."""
 
-    def flush_l2():
-        ctx.memcpy(flush_b, flush_a, 320 << 20, abi.ICG_MEM_DEVICE, abi.ICG_MEM_DEVICE)
+        def __init__(self, s):
+            self.ctx = api.Context(local_rank)
+            self.ctx.set_mlp(abi.ICG_MLP_GEOMETRY, gw, gb)
+            self.ctx.set_mlp(abi.ICG_MLP_TEXTURE, tw, tb)
+            self.host_maps, self.dev_maps = [], []
+            for i in range(args.frames):
+                fm = api.gen_feature_map(fmap_seed(rank, s * args.frames + i), C_, H_, W_)
+                hp = api.host_alloc(fbytes)
+                np.ctypeslib.as_array((np.ctypeslib.ctypes.c_float * fm.size).from_address(hp))[:] = fm.reshape(-1)
+                dp = self.ctx.device_alloc(fbytes)
+                self.ctx.memcpy(dp, hp, fbytes, abi.ICG_MEM_DEVICE, abi.ICG_MEM_HOST)
+                self.host_maps.append(hp)
+                self.dev_maps.append(dp)
+            self.fields_dev = [api.PifuField(None, caps, 50.0, prec, device_ptr=dp, shape=(C_, H_, W_))
+                               for dp in self.dev_maps]
+            self.fields_host = []
+            for hp in self.host_maps:
+                f = api.PifuField(None, caps, 50.0, prec, device_ptr=hp, shape=(C_, H_, W_))
+                f.c.fmap_mem = abi.ICG_MEM_HOST
+                self.fields_host.append(f)
+            sizes = (("depth", npx * 4), ("rgb", npx * 12), ("mask", npx), ("sk", npx * 4))
+            self.dout = img_struct({k: self.ctx.device_alloc(b) for k, b in sizes}, abi.ICG_MEM_DEVICE)
+            self.hout = img_struct({k: api.host_alloc(b) for k, b in sizes}, abi.ICG_MEM_HOST)
+            self.flush_a = self.ctx.device_alloc(320 << 20)
+            self.flush_b = self.ctx.device_alloc(320 << 20)
+            self.lat = []
+            self.k = 0
 
+        def flush_l2(self):
+            self.ctx.memcpy(self.flush_b, self.flush_a, 320 << 20, abi.ICG_MEM_DEVICE, abi.ICG_MEM_DEVICE)
+
+        def frame(self, host=False, flush=True):
+            if flush and args.l2 == "flush":
+                self.flush_l2()
+            f = (self.fields_host if host else self.fields_dev)[self.k % args.frames]
+            self.k += 1
+            ext, img = self.ctx.frame_raw(f, cfg, cam, res, res, self.hout if host else self.dout)
+            self.lat.append(img.wall_seconds * 1e3)
+
+    lanes = [Lane(s) for s in range(S)]
+    ctxs = [ln.ctx for ln in lanes]
     from paper_2007_13988_b200 import shard
 
     def barrier():
@@ -300,65 +319,93 @@ def main():
     def allmax(x: float) -> float:
         return shard.allmax(x, device=f"cuda:{local_rank}" if dist else None)
 
-    # ---- warm-up ----
-    for s in range(args.warmup):
-        ctx.frame_raw(fields_dev[s % nF], cfg, cam, res, res, img_struct(dout, abi.ICG_MEM_DEVICE))
-    # ---- timed: device-resident inputs and outputs (no per-kernel events inside) ----
+    def run_frames(nframes: int, host: bool) -> float:
+        """nframes frames round-robin over the lanes (one host thread per lane); returns the
+        device-timed span (CUDA events: common start event, last stream's end event), ms."""
+        counts = [nframes // S + (1 if i < nframes % S else 0) for i in range(S)]
+        api.span_begin(ctxs)
+        ths = [threading.Thread(target=lambda ln=ln, c=c: [ln.frame(host) for _ in range(c)])
+               for ln, c in zip(lanes, counts)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return api.span_end(ctxs)
+
+    # ---- warm-up (every lane) ----
+    for ln in lanes:
+        for _ in range(args.warmup):
+            ln.frame()
+    # ---- single-frame latency: one lane, frames back to back (device time per frame) ----
+    lat_lane = lanes[0]
+    lat_lane.lat = []
+    for _ in range(min(args.steps, 30)):
+        lat_lane.frame()
+    single_lat = list(lat_lane.lat)
+    # ---- timed: S frames in flight, device-resident inputs and outputs ----
+    for ln in lanes:
+        ln.lat = []
     barrier()
     cvd = [d for d in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if d.strip().isdigit()]
     clocks = ClockSampler(int(cvd[local_rank]) if local_rank < len(cvd) else local_rank)
     clocks.start()
-    dev_total = 0.0
-    lat = []
     t_wall0 = time.perf_counter()
-    for s in range(args.steps):
-        flush_l2()
-        ext, img = ctx.frame_raw(fields_dev[(s + args.warmup) % nF], cfg, cam, res, res,
-                                 img_struct(dout, abi.ICG_MEM_DEVICE))
-        dev_total += img.wall_seconds
-        lat.append(img.wall_seconds * 1e3)
+    span_ms = run_frames(args.steps, host=False)
     wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
+    lat = sum((ln.lat for ln in lanes), [])
     barrier()
-    dev_max = allmax(dev_total)
+    dev_max = allmax(span_ms / 1e3)
     value = world * args.steps / dev_max
 
-    # ---- per-kernel breakdown: a separate pass over the same frames with CUDA events
-    # around every launch (the events themselves cost a little, so `value` is not taken here) ----
+    # ---- per-kernel breakdown: a separate single-lane pass with CUDA events around every launch
+    # (the events themselves cost a little, so `value` is not taken here) ----
+    ctx = lat_lane.ctx
     ctx.profile(True, reset=True)
-    for s in range(min(args.steps, 20)):
-        flush_l2()
-        ctx.frame_raw(fields_dev[(s + args.warmup) % nF], cfg, cam, res, res, img_struct(dout, abi.ICG_MEM_DEVICE))
+    for _ in range(min(args.steps, 20)):
+        lat_lane.frame()
     prof = ctx.profile_get()
     ctx.profile(False, reset=False)
 
-    # ---- e2e: pinned host inputs/outputs through the C ABI, host wall clock ----
+    # ---- e2e: pinned host inputs/outputs through the C ABI (H2D + D2H inside every call) ----
     e2e = None
     if not args.no_e2e:
-        for s in range(2):
-            ctx.frame_raw(fields_host[s % nF], cfg, cam, res, res, img_struct(hout, abi.ICG_MEM_HOST))
+        for ln in lanes:
+            for _ in range(2):
+                ln.frame(host=True, flush=False)
         barrier()
-        t0 = time.perf_counter()
-        for s in range(args.steps):
-            ctx.frame_raw(fields_host[s % nF], cfg, cam, res, res, img_struct(hout, abi.ICG_MEM_HOST))
-        e2e_t = allmax(time.perf_counter() - t0)
+        e2e_ms = run_frames(args.steps, host=True)
+        e2e_t = allmax(e2e_ms / 1e3)
         e2e = {"value": world * args.steps / e2e_t, "unit": "frames/s", "h2d_bytes_per_step": fbytes,
                "d2h_bytes_per_step": npx * (4 + 12 + 1 + 4)}
 
-    # ---- roofline of the dominant kernel (fused geometry MLP) ----
+    # ---- roofline of the dominant kernel: the column-factored geometry field on the bulk batches ----
     pk = peaks()
-    geo_s = prof["geo_mlp_ms"] / 1e3
-    achieved = prof["geo_points"] * GEO_FLOP_PER_POINT / geo_s / 1e12 if geo_s > 0 else 0.0
     peak_t = pk.get("bf16_tflops_sustained", 1385.7)
-    executed_mult = 3 if prec_name == "fp32" else 1
-    roofline = {"bound": "tensor", "kernel": "geometry MLP: k_mlp_pair<0> (CTA-pair tcgen05) + k_lp (latency path), all launches", "achieved": achieved,
-                "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t, "traffic": None,
+    fact_s = prof["fact_ms"] / 1e3
+    fact_pts = prof["fact_points"]
+    # algorithmic (dense-equivalent) work per evaluated point, SURVEY.md §8(d); executed MMA work of
+    # the factored pass: layers 2-4 hidden parts (688,128 MAC/point) x3 for bf16x3
+    exec_mult = 3 if prec_name == "fp32" else 1
+    achieved = fact_pts * GEO_FLOP_PER_POINT / fact_s / 1e12 if fact_s > 0 else 0.0
+    executed = fact_pts * FACT_MMA_FLOP_PER_POINT * exec_mult / fact_s / 1e12 if fact_s > 0 else 0.0
+    roofline = {"bound": "tensor",
+                "kernel": "geometry field, bulk batches (dense level 0 + each level's E0 list): column pass "
+                          "k_mlp_pair<COLS> + factored pass k_mlp_pair<FACT> (CTA-pair tcgen05), incl. list sorting",
+                "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
+                "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" + (" (fallback)" if pk.get("fallback") else ""),
                 "algorithmic_flop_per_point": GEO_FLOP_PER_POINT,
-                "executed_tflops": achieved * executed_mult,
-                "launches": prof["geo_mlp_launches"], "avg_launch_ms": prof["geo_mlp_ms"] / max(1, prof["geo_mlp_launches"]),
-                "points": prof["geo_points"]}
+                "achieved_note": "dense-equivalent algorithmic FLOP (SURVEY §8(d)); the factored pass executes fewer",
+                "executed_tflops": executed, "executed_frac": executed / peak_t,
+                "executed_flop_per_point": FACT_MMA_FLOP_PER_POINT * exec_mult,
+                "launches": prof["fact_launches"], "points": fact_pts,
+                "avg_launch_ms": prof["fact_ms"] / max(1, prof["fact_launches"])}
     secondary = {
+        "conflict_chain": {"points": prof["chain_points"], "ms": prof["chain_ms"], "launches": prof["chain_launches"]},
+        "geometry_all": {"points": prof["geo_points"], "ms": prof["geo_mlp_ms"],
+                         "mlp_points_per_s": prof["geo_points"] / max(1e-9, prof["geo_mlp_ms"] / 1e3),
+                         "achieved_tflops": prof["geo_points"] * GEO_FLOP_PER_POINT / max(1e-9, prof["geo_mlp_ms"] / 1e3) / 1e12},
         "texture_mlp": {"points": prof["tex_points"], "ms": prof["tex_mlp_ms"],
                         "achieved_tflops": prof["tex_points"] * TEX_FLOP_PER_POINT / max(1e-9, prof["tex_mlp_ms"] / 1e3) / 1e12},
         "dense_passes": {"bytes": prof["dense_bytes"], "ms": prof["dense_ms"],
@@ -366,7 +413,7 @@ def main():
                          "peak_gbs": pk.get("hbm_gbs")},
         "render": {"bytes": prof["render_bytes"], "ms": prof["render_ms"],
                    "achieved_gbs": prof["render_bytes"] / max(1e-9, prof["render_ms"] / 1e3) / 1e9},
-        "mlp_points_per_s": prof["geo_points"] / max(1e-9, geo_s),
+        "profiled_frames": prof["frames"], "profiled_frame_ms": prof["frame_ms"] / max(1, prof["frames"]),
     }
 
     cpu_baseline = None
@@ -385,10 +432,15 @@ def main():
             "dtype": "bf16x3 (fp32-accurate)" if prec_name == "fp32" else prec_name,
             "data": "synthetic (seeded N(0,1) feature maps, Kaiming-uniform weights, 15-capsule sdf bias)",
             "config": dict(workload_config(cfg_name, args), wall_ms_per_step=1e3 * wall / args.steps,
-                           frame_latency_ms={"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99))},
+                           frame_latency_ms={"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+                                             "note": f"device time of one frame with {S} frames in flight"},
+                           single_frame_latency_ms={"p50": float(np.percentile(single_lat, 50)),
+                                                    "p99": float(np.percentile(single_lat, 99)),
+                                                    "note": "one frame at a time on one stream"},
                            evals_per_frame=int(prof["geo_points"] / max(1, prof["frames"]))),
             "e2e": e2e, "roofline": roofline, "secondary": secondary, "cpu_baseline": cpu_baseline,
             "gpu_launches": int(round(prof["kernel_launches"] / max(1, prof["frames"]) * args.steps)), "clocks": clk,
+            "streams": S,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -241,11 +241,26 @@ typedef struct icg_profile {
     uint64_t render_bytes;
     double frame_ms;               /* summed device time of whole frames / extractions */
     uint64_t frames;
+    /* breakdown of the geometry launches above (column-factored PIFu field):  */
+    uint64_t fact_launches;        /* bulk batches (dense L0 + each level's E0): column pass + factored pass */
+    uint64_t fact_points;
+    double fact_ms;
+    uint64_t chain_launches;       /* conflict-loop batches (CTA-pair kernels + persistent tail) */
+    uint64_t chain_points;
+    double chain_ms;
 } icg_profile;
 
 int icg_profile_enable(icg_context* ctx, int on);
 int icg_profile_reset(icg_context* ctx);
 int icg_profile_get(icg_context* ctx, icg_profile* out);
+
+/* Device-timed span over n contexts of ONE device (several frames in flight,
+ * one host thread per context).  icg_span_begin records a start event on
+ * ctxs[0]'s stream and makes every context's stream wait for it;
+ * icg_span_end records an end event on every stream, waits, and returns the
+ * milliseconds from the start event to the last stream's end event. */
+int icg_span_begin(icg_context* const* ctxs, int n);
+int icg_span_end(icg_context* const* ctxs, int n, float* ms);
 
 /* ======================================================================== */
 /* Host helpers                                                              */

@@ -138,6 +138,12 @@ class icg_profile(C.Structure):
         ("render_bytes", C.c_uint64),
         ("frame_ms", C.c_double),
         ("frames", C.c_uint64),
+        ("fact_launches", C.c_uint64),
+        ("fact_points", C.c_uint64),
+        ("fact_ms", C.c_double),
+        ("chain_launches", C.c_uint64),
+        ("chain_points", C.c_uint64),
+        ("chain_ms", C.c_double),
     ]
 
 
@@ -163,6 +169,8 @@ SIGNATURES = [
     ("icg_profile_enable", C.c_int, [ctx_p, C.c_int]),
     ("icg_profile_reset", C.c_int, [ctx_p]),
     ("icg_profile_get", C.c_int, [ctx_p, C.POINTER(icg_profile)]),
+    ("icg_span_begin", C.c_int, [C.POINTER(ctx_p), C.c_int]),
+    ("icg_span_end", C.c_int, [C.POINTER(ctx_p), C.c_int, C.POINTER(C.c_float)]),
     ("icg_host_alloc", C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     ("icg_host_free", C.c_int, [C.c_void_p]),
     ("icg_device_alloc", C.c_int, [ctx_p, C.c_size_t, C.POINTER(C.c_void_p)]),

@@ -324,6 +324,20 @@ class Context:
         return ext, img
 
 
+def span_begin(ctxs) -> None:
+    """Start a device-timed span over contexts of one device (see icg_span_begin)."""
+    arr = (abi.ctx_p * len(ctxs))(*[c.h for c in ctxs])
+    _check(abi.lib().icg_span_begin(arr, len(ctxs)))
+
+
+def span_end(ctxs) -> float:
+    """Milliseconds from span_begin to the last context's completion (icg_span_end)."""
+    arr = (abi.ctx_p * len(ctxs))(*[c.h for c in ctxs])
+    ms = C.c_float()
+    _check(abi.lib().icg_span_end(arr, len(ctxs), C.byref(ms)))
+    return ms.value
+
+
 def host_alloc(nbytes: int) -> int:
     ptr = C.c_void_p()
     _check(abi.lib().icg_host_alloc(nbytes, C.byref(ptr)))

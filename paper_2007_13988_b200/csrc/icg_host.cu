@@ -64,6 +64,21 @@ struct icg_context {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t span_start = nullptr, span_end = nullptr;  // icg_span_begin / icg_span_end
+    // CUDA graph of one frame's device work (icg_frame), keyed by everything its launches capture
+    struct FrameKey {
+        icg_algo_config cfg;
+        icg_camera cam;
+        int W, H, kind, precision, img_mem;
+        float bg[3];
+        void* img_ptr[4];
+        int unroll[ICG_MAX_LEVELS];
+        bool operator==(const FrameKey& o) const { return std::memcmp(this, &o, sizeof(FrameKey)) == 0; }
+    };
+    FrameKey graph_key{}, warm_key{};
+    bool graph_valid = false, warm_valid = false, use_graph = true;
+    cudaGraphExec_t graph_exec = nullptr;
+    uint64_t graph_launches = 0;
     // weights
     bool has_geo = false, has_tex = false;
     DBuf geo_wt[5], geo_b[5], tex_wt[5], tex_b[5], geo_wrow[5];
@@ -80,6 +95,7 @@ struct icg_context {
     DBuf geo_fact_stream[2][2];
     alignas(64) unsigned char geo_fact_tmap[2][2][128] = {};
     bool geo_fact = false, use_fact = true;
+    bool fact_used = false;  // the last extraction ran its bulk batches column-factored
     DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
     bool use_tail = true;
     unsigned tail_max = 100;  // conflict batches up to this size start the persistent tail kernel
@@ -118,6 +134,7 @@ struct icg_context {
     uint64_t launches = 0;
     // device-side conflict-loop depth per level, adapted from the previous frame
     int unroll[ICG_MAX_LEVELS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4};
+    int unroll_seen[ICG_MAX_LEVELS] = {};  // deepest adapted depth so far (grow-only)
 };
 
 namespace {
@@ -160,6 +177,14 @@ void prof_collect(icg_context* c) {
         cudaEventElapsedTime(&ms, c->ev_pool[m.slot], c->ev_pool[m.slot + 1]);
         switch (m.kind) {
             case 0: c->prof.geo_mlp_ms += ms; c->prof.geo_mlp_launches++; break;
+            case 4:  // column-factored bulk batch (also a geometry launch)
+                c->prof.geo_mlp_ms += ms; c->prof.geo_mlp_launches++;
+                c->prof.fact_ms += ms; c->prof.fact_launches++;
+                break;
+            case 5:  // conflict-loop batch on the pair kernels + tail
+                c->prof.geo_mlp_ms += ms; c->prof.geo_mlp_launches++;
+                c->prof.chain_ms += ms; c->prof.chain_launches++;
+                break;
             case 1: c->prof.tex_mlp_ms += ms; c->prof.tex_mlp_launches++; break;
             case 2: c->prof.dense_ms += ms; c->prof.dense_launches++; break;
             case 3: c->prof.render_ms += ms; c->prof.render_launches++; break;
@@ -310,7 +335,8 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
     if (int r = c->colcnt.ensure(plane * sizeof(uint32_t))) return r;
     if (int r = c->sorted.ensure(nodes3(job.cells) * sizeof(uint32_t))) return r;
     DevCounters* ctr = c->ctr.as<DevCounters>();
-    int slot = prof_begin(c, 0);
+    int slot = prof_begin(c, 4);
+    c->fact_used = true;
     EvalJob cj{};
     cj.cells = job.cells;
     const int* cm = nullptr;
@@ -448,6 +474,7 @@ int issue_tail(icg_context* c, const FieldDev& fd, const LevelBufs& lb, int leve
 // Issues one whole extraction on the context stream (no host sync).
 int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg) {
     prof_discard(c);
+    c->fact_used = false;
     DevCounters* ctr = c->ctr.as<DevCounters>();
     ICG_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), c->stream));
     const int L = cfg->target_level;
@@ -554,7 +581,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                     big.min_count = std::max(c->tail_max, mid_max) + 1;
                     mid.min_count = c->tail_max + 1;
                     mid.max_count = mid_max;
-                    int slot = prof_begin(c, 0);
+                    int slot = prof_begin(c, 5);
                     const bool x3 = fd.precision == ICG_PREC_FP32;
                     const void* tm = c->geo_pair_tmap[x3 ? 0 : 1];
                     int r = launch_pifu_pair_eval(fd, c->geo_tc, tm, big, (unsigned)nf, x3, c->stream);
@@ -704,6 +731,13 @@ void prof_extract_done(icg_context* c, const icg_algo_config* cfg) {
     if (!c->prof_on) return;
     const DevCounters& h = *c->h_ctr;
     for (int l = 0; l <= cfg->target_level; ++l) c->prof.geo_points += h.evals[l];
+    if (c->fact_used && cfg->variant == ICG_VARIANT_PROGRESSIVE) {
+        c->prof.fact_points += h.evals[0];
+        for (int l = 1; l <= cfg->target_level; ++l) {
+            c->prof.fact_points += h.e0[l];
+            c->prof.chain_points += h.evals[l] - h.e0[l];
+        }
+    }
     if (cfg->variant == ICG_VARIANT_PROGRESSIVE) {
         for (int l = 1; l <= cfg->target_level; ++l) {
             // level pass: fine value+state written, coarse read, index list
@@ -740,10 +774,12 @@ bool adapt_unroll(icg_context* c, const icg_algo_config* cfg) {
             // host-side iterations: up to the one where the persistent tail took over
             // (once started, the tail finishes the level: a margin of one iteration covers frames
             // whose chain hands over one iteration later)
-            if (h.tail_start[l])
-                c->unroll[l] = (int)h.tail_start[l] + 1;
-            else
-                c->unroll[l] = (int)h.conflict_iters[l] + std::max(2, (int)h.conflict_iters[l] / 4);
+            // grow-only: frames of a stream differ a little, and a stable depth keeps the frame's
+            // CUDA graph valid (a shallower depth would only save a few early-exit launches)
+            int need = h.tail_start[l] ? (int)h.tail_start[l] + 1
+                                       : (int)h.conflict_iters[l] + std::max(2, (int)h.conflict_iters[l] / 4);
+            c->unroll[l] = std::max(c->unroll_seen[l], need);
+            c->unroll_seen[l] = c->unroll[l];
         }
     return replay;
 }
@@ -805,6 +841,8 @@ int icg_create(int device, icg_context** out) {
     if (const char* e = getenv("ICG_NO_PAIR")) c->use_pair = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_FACT")) c->use_fact = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_TAIL")) c->use_tail = !(e[0] == '1');
+    if (const char* e = getenv("ICG_NO_GRAPH")) c->use_graph = !(e[0] == '1');
+    if (getenv("ICG_TC_TRACE") || getenv("ICG_TAIL_TRACE")) c->use_graph = false;  // traces synchronise
     if (const char* e = getenv("ICG_TAIL_MAX")) c->tail_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_SMALL_MAX")) c->small_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_LP_MAX")) c->lp_max = (unsigned)atoi(e);
@@ -851,6 +889,9 @@ int icg_destroy(icg_context* c) {
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->e0) cudaEventDestroy(c->e0);
     if (c->e1) cudaEventDestroy(c->e1);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    if (c->span_start) cudaEventDestroy(c->span_start);
+    if (c->span_end) cudaEventDestroy(c->span_end);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return ICG_OK;
@@ -1053,13 +1094,92 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
     if (int r = prepare_field(c, field, fd)) return r;
     if (fd.kind == ICG_FIELD_PIFU && !c->has_tex) return einval("frame: scene has no texture (icg_set_mlp TEXTURE)");
     if (int r = ensure_grid(c, cfg->coarsest_cells << cfg->target_level)) return r;
-    ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
-    for (int attempt = 0;; ++attempt) {
+    // the frame's device work: extraction, render + texture, output copies, counters back to the host
+    auto body = [&]() -> int {
         if (int r = issue_extract(c, fd, cfg)) return r;
         if (int r = issue_render(c, fd, cam, W, H, bg)) return r;
-        ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
         if (int r = finish_render_outputs(c, W, H, img)) return r;
-        if (int r = sync_counters(c)) return r;
+        ICG_CUDA_TRY(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->stream));
+        return ICG_OK;
+    };
+    ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
+    for (int attempt = 0;; ++attempt) {
+        // Replayed as a CUDA graph once the same frame shape has run eagerly (allocations done):
+        // one launch instead of ~150, no host work between dependent kernels.
+        icg_context::FrameKey key{};
+        key.cfg = *cfg;
+        key.cam = *cam;
+        key.W = W;
+        key.H = H;
+        key.kind = fd.kind;
+        key.precision = fd.precision;
+        for (int i = 0; i < 3; ++i) key.bg[i] = bg ? bg[i] : 0.0f;
+        if (img) {
+            key.img_mem = img->mem;
+            key.img_ptr[0] = img->depth;
+            key.img_ptr[1] = img->rgb;
+            key.img_ptr[2] = img->mask;
+            key.img_ptr[3] = img->surface_k;
+        }
+        std::memcpy(key.unroll, c->unroll, sizeof(key.unroll));
+        const bool graphs = c->use_graph && !c->prof_on;
+        bool ran = false;
+        if (getenv("ICG_GRAPH_DEBUG") && c->warm_valid && !(c->warm_key == key)) {
+            const icg_context::FrameKey& w = c->warm_key;
+            fprintf(stderr, "[icg] frame key differs: cfg %d cam %d WH %d kind %d img %d bg %d unroll %d\n",
+                    std::memcmp(&w.cfg, &key.cfg, sizeof(key.cfg)) != 0, std::memcmp(&w.cam, &key.cam, sizeof(key.cam)) != 0,
+                    w.W != key.W || w.H != key.H, w.kind != key.kind || w.precision != key.precision,
+                    std::memcmp(w.img_ptr, key.img_ptr, sizeof(key.img_ptr)) != 0 || w.img_mem != key.img_mem,
+                    std::memcmp(w.bg, key.bg, sizeof(key.bg)) != 0, std::memcmp(w.unroll, key.unroll, sizeof(key.unroll)) != 0);
+        }
+        if (graphs && c->graph_valid && c->graph_key == key) {
+            ICG_CUDA_TRY(cudaGraphLaunch(c->graph_exec, c->stream));
+            c->launches += c->graph_launches;
+            ran = true;
+        } else if (graphs && c->warm_valid && c->warm_key == key) {
+            const uint64_t l0 = c->launches;
+            cudaGraph_t g = nullptr;
+            int r = ICG_OK;
+            if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                r = ICG_ERUNTIME;
+            } else {
+                r = body();
+                cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+                if (e != cudaSuccess) r = r ? r : ICG_ERUNTIME;
+            }
+            cudaGetLastError();
+            if (r == ICG_OK && g) {
+                if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+                c->graph_exec = nullptr;
+                if (cudaGraphInstantiate(&c->graph_exec, g, 0) == cudaSuccess) {
+                    c->graph_key = key;
+                    c->graph_valid = true;
+                    c->graph_launches = c->launches - l0;
+                    if (getenv("ICG_GRAPH_DEBUG")) fprintf(stderr, "[icg] frame graph captured: %llu launches\n",
+                                                           (unsigned long long)c->graph_launches);
+                    ICG_CUDA_TRY(cudaGraphLaunch(c->graph_exec, c->stream));
+                    ran = true;
+                } else {
+                    c->graph_exec = nullptr;
+                }
+            }
+            if (g) cudaGraphDestroy(g);
+            if (!ran) {  // capture not possible: stay eager on this context
+                if (getenv("ICG_GRAPH_DEBUG"))
+                    fprintf(stderr, "[icg] frame graph capture failed (%d: %s); staying eager\n", r, g_err.c_str());
+                cudaGetLastError();
+                c->use_graph = false;
+                c->graph_valid = false;
+                c->launches = l0;
+            }
+        }
+        if (!ran) {
+            if (int r = body()) return r;
+            c->warm_key = key;
+            c->warm_valid = true;
+        }
+        ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
+        ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
         if (c->h_ctr->overflow) {
             set_error("frame: device work list overflow");
             return ICG_ECAPACITY;
@@ -1161,6 +1281,38 @@ int icg_compare_iou(icg_context* c, const uint8_t* a, const uint8_t* b, size_t n
     ICG_CUDA_TRY(cudaMemcpyAsync(iu, c->outv.p, 16, cudaMemcpyDeviceToHost, c->stream));
     ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     *iou = iu[1] ? (double)iu[0] / (double)iu[1] : 1.0;
+    return ICG_OK;
+}
+
+int icg_span_begin(icg_context* const* ctxs, int n) {
+    if (!ctxs || n < 1 || !ctxs[0]) return einval("span: no contexts");
+    icg_context* c0 = ctxs[0];
+    ICG_CUDA_TRY(cudaSetDevice(c0->device));
+    if (!c0->span_start) ICG_CUDA_TRY(cudaEventCreate(&c0->span_start));
+    ICG_CUDA_TRY(cudaEventRecord(c0->span_start, c0->stream));
+    for (int i = 1; i < n; ++i) {
+        if (!ctxs[i] || ctxs[i]->device != c0->device) return einval("span: contexts must share a device");
+        ICG_CUDA_TRY(cudaStreamWaitEvent(ctxs[i]->stream, c0->span_start, 0));
+    }
+    return ICG_OK;
+}
+
+int icg_span_end(icg_context* const* ctxs, int n, float* ms) {
+    if (!ctxs || n < 1 || !ctxs[0] || !ms) return einval("span: bad arguments");
+    icg_context* c0 = ctxs[0];
+    if (!c0->span_start) return einval("span: icg_span_begin was not called");
+    ICG_CUDA_TRY(cudaSetDevice(c0->device));
+    float best = 0.0f;
+    for (int i = 0; i < n; ++i) {
+        icg_context* c = ctxs[i];
+        if (!c->span_end) ICG_CUDA_TRY(cudaEventCreate(&c->span_end));
+        ICG_CUDA_TRY(cudaEventRecord(c->span_end, c->stream));
+        ICG_CUDA_TRY(cudaEventSynchronize(c->span_end));
+        float t = 0.0f;
+        ICG_CUDA_TRY(cudaEventElapsedTime(&t, c0->span_start, c->span_end));
+        if (t > best) best = t;
+    }
+    *ms = best;
     return ICG_OK;
 }
 

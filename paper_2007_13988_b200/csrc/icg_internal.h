@@ -43,6 +43,7 @@ struct DevCounters {
     unsigned long long refined[ICG_MAX_LEVELS];
     unsigned int conflict_iters[ICG_MAX_LEVELS];
     unsigned int ncols;               // column-factored field: distinct columns of the current batch
+    unsigned int e0[ICG_MAX_LEVELS];  // size of each level's E0 list (the bulk batch)
     unsigned int tail_start[ICG_MAX_LEVELS];  // 1 + host iteration at which k_tail took over (0: never)
     // render counters (cleared per render: everything from `covered` to the end)
     unsigned long long covered, degenerate, grazing;

@@ -238,6 +238,7 @@ k_scan_blocks(uint32_t* __restrict__ counts, unsigned nblocks, DevCounters* ctr,
     }
     if (threadIdx.x == 0) {
         ctr->list_count = carry;
+        ctr->e0[level] = carry;
         ctr->evals[level] += carry;
         ctr->cf_count[0] = 0;
         ctr->cf_count[1] = 0;
