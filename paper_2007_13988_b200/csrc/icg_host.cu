@@ -575,7 +575,8 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                 if (fact_ok(c, fd) && c->use_tail && c->geo_pair) {
                     // large batches: the CTA-pair kernel; the first small one starts the persistent tail,
                     // which finishes the level's chain (k_tail.cu)
-                    // (mid-size batches: 64-point pair tiles, twice as many pairs busy per wave)
+                    // (mid-size batches: 64-point pair tiles, twice as many pairs busy per wave; the
+                    // column-factored pass has a longer single-tile latency, so it is kept for bulk batches)
                     const unsigned mid_max = 74u * 64u;
                     EvalJob big = cj, mid = cj;
                     big.min_count = std::max(c->tail_max, mid_max) + 1;

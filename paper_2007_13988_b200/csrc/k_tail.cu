@@ -44,7 +44,10 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kRec = 1936;  // column record floats (k_mlp_pair.cu kSRow)
 // A small grid: every activation is read by every CTA (rows are partitioned), so fewer, fatter
 // CTAs keep that broadcast cheap; 32 CTAs hold all resident weights in shared memory.
-constexpr int kG = 148;
+#ifndef ICG_TAIL_CTAS
+#define ICG_TAIL_CTAS 148
+#endif
+constexpr int kG = ICG_TAIL_CTAS;
 constexpr int kMaxOwn2 = (512 + kG - 1) / kG, kMaxOwn3 = (256 + kG - 1) / kG, kMaxOwn4 = (128 + kG - 1) / kG;
 constexpr int kSRows = 1921;  // Phi rows of a record: 1024 + 512 + 256 + 128 + final dot
 constexpr int kMaxOwnS = (kSRows + kG - 1) / kG;
@@ -405,7 +408,7 @@ int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_n
         }
         grid = tail::kG;
         if (sms < tail::kG) {
-            set_error("k_tail: needs 148 SMs");
+            set_error("k_tail: not enough SMs");
             return ICG_ERUNTIME;
         }
         attr = true;

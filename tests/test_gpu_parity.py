@@ -273,3 +273,99 @@ def test_render_general_cameras_exact(gpu_ctx, pifu_inputs, yaw, pitch):
     assert np.array_equal(img.depth, r["depth"])
     assert img.covered_pixels == r["covered"] and img.degenerate_brackets == r["degenerate"]
     assert img.grazing_pixels == r["grazing"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("max_iters", [1, 2, 5])
+def test_pifu_conflict_bound_replay(gpu_ctx, pifu_inputs, max_iters):
+    """A conflict-iteration bound (AlgoConfig.max_conflict_iters, localize.hpp:343-346) cuts the
+    loop wherever it is running -- CTA-pair kernels or the persistent tail -- exactly where the
+    reference cuts it; the warning flag agrees."""
+    f = _pifu(gpu_ctx, pifu_inputs, abi.ICG_PREC_FP32)
+    coarsest, level = 16, 3
+    g = gpu_ctx.extract(f, api.AlgoConfig("progressive", coarsest, level, max_conflict_iters=max_iters))
+    rp = O.Replay(g.values, g.states, coarsest << level)
+    if O.ref_available():
+        r = O.ref_extract(rp.pt_fn, rp.user, coarsest, level, max_conflict_iters=max_iters)
+    else:
+        r = O.extract_progressive(rp, coarsest, level, max_conflict_iters=max_iters)
+    assert rp.c.misses == 0
+    assert r["evals_per_level"] == g.evals_per_level
+    assert np.array_equal(r["states"], g.states)
+    assert np.array_equal(r["values"], g.values)
+    assert r["conflict_warning"] == g.conflict_warning
+
+
+@pytest.mark.gpu
+def test_frame_graph_replay_identical(gpu_ctx, pifu_inputs):
+    """Frames of the same shape run eagerly, then warm, then are captured as a CUDA graph and
+    replayed (fixed pinned output buffers keep the shape): every output bit is identical."""
+    import ctypes as C
+    f = _pifu(gpu_ctx, pifu_inputs, abi.ICG_PREC_FP32)
+    cfg = api.AlgoConfig("progressive", 16, 3)
+    cam = api.CameraSpec.from_angles(90, 0)
+    W, H = 128, 96
+    npx = W * H
+    sizes = {"depth": npx * 4, "rgb": npx * 12, "mask": npx, "sk": npx * 4}
+    ptrs = {k: api.host_alloc(b) for k, b in sizes.items()}
+    img = abi.icg_image()
+    img.mem = abi.ICG_MEM_HOST
+    img.depth = C.cast(C.c_void_p(ptrs["depth"]), abi.f32p)
+    img.rgb = C.cast(C.c_void_p(ptrs["rgb"]), abi.f32p)
+    img.mask = C.cast(C.c_void_p(ptrs["mask"]), abi.u8p)
+    img.surface_k = C.cast(C.c_void_p(ptrs["sk"]), abi.i32p)
+
+    def view(k, dt, n):
+        return np.ctypeslib.as_array((C.c_uint8 * (n * np.dtype(dt).itemsize)).from_address(ptrs[k])).view(dt).copy()
+
+    outs = []
+    for _ in range(5):
+        ext, im = gpu_ctx.frame_raw(f, cfg, cam, W, H, img)
+        outs.append((list(ext.evals_per_level[:4]), im.covered_pixels, im.grazing_pixels,
+                     view("rgb", np.float32, npx * 3), view("depth", np.float32, npx), view("sk", np.int32, npx)))
+    for o in outs[1:]:
+        assert o[0] == outs[0][0] and o[1] == outs[0][1] and o[2] == outs[0][2]
+        for a, b in zip(o[3:], outs[0][3:]):
+            assert np.array_equal(a, b)
+    for p_ in ptrs.values():
+        api.host_free(p_)
+
+
+@pytest.mark.gpu
+def test_concurrent_contexts_match_serial(pifu_inputs):
+    """Distinct contexts driven from concurrent host threads (several frames in flight on one
+    GPU, as bench.py does) give exactly the results of running the frames one at a time."""
+    import threading
+    inp = pifu_inputs
+    cfg = api.AlgoConfig("progressive", 16, 3)
+    cam = api.CameraSpec.from_angles(90, 0)
+    fmaps = [inp["fmap"], np.ascontiguousarray(inp["fmap"][:, ::-1, :]), np.ascontiguousarray(inp["fmap"] * 0.5)]
+    ctxs = []
+    for _ in fmaps:
+        c = api.Context(0)
+        c.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+        c.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+        ctxs.append(c)
+    serial = []
+    for c, fm in zip(ctxs, fmaps):
+        serial.append(c.frame(api.PifuField(fm, inp["caps"], 50.0, abi.ICG_PREC_FP32), cfg, cam, 96, 96,
+                              want_grid=True))
+    results = [None] * len(ctxs)
+
+    def run(k):
+        out = None
+        for _ in range(3):
+            out = ctxs[k].frame(api.PifuField(fmaps[k], inp["caps"], 50.0, abi.ICG_PREC_FP32), cfg, cam, 96, 96,
+                                want_grid=True)
+        results[k] = out
+
+    ths = [threading.Thread(target=run, args=(k,)) for k in range(len(ctxs))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for (es, is_), (ec, ic) in zip(serial, results):
+        assert np.array_equal(es.values, ec.values) and np.array_equal(es.states, ec.states)
+        assert np.array_equal(is_.rgb, ic.rgb) and np.array_equal(is_.surface_k, ic.surface_k)
+    for c in ctxs:
+        c.close()
