@@ -90,6 +90,8 @@ struct icg_context {
     // TMA descriptors of the pair streams: [0] bf16x3 (hi, lo), [1] bf16 (hi only)
     alignas(64) unsigned char geo_pair_tmap[2][128] = {};
     alignas(64) unsigned char tex_pair_tmap[2][128] = {};
+    DBuf geo_pair_f16, geo_pair_f16_hi;  // geometry stream with fp16 skip items (texture kernel prefix)
+    alignas(64) unsigned char geo_pair_f16_tmap[2][128] = {};
     bool geo_pair = false, tex_pair = false;
     // column-factored geometry field (FACT / COLS streams, [part][x3 ? 0 : 1])
     DBuf geo_fact_stream[2][2];
@@ -428,7 +430,7 @@ int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned
     if (fd.precision == ICG_PREC_FP32_SIMT)
         r = launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
     else if (c->geo_pair && c->tex_pair && c->use_pair)
-        r = launch_pifu_pair_texture(fd, c->geo_tc, c->tex_tc, c->geo_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1],
+        r = launch_pifu_pair_texture(fd, c->geo_tc, c->tex_tc, c->geo_pair_f16_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1],
                                      c->tex_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1], job, max_points,
                                      fd.precision == ICG_PREC_FP32, c->stream);
     else
@@ -872,7 +874,7 @@ int icg_destroy(icg_context* c) {
     DBuf* all[] = {&c->geo_stream, &c->geo_bias, &c->geo_wlast, &c->tex_stream, &c->tex_bias, &c->tex_wlast,
                    &c->scene, &c->fscene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
-                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->lp_scratch, &c->lp_stream, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi,
+                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->lp_scratch, &c->lp_stream, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi, &c->geo_pair_f16, &c->geo_pair_f16_hi,
                    &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx, &c->colrec, &c->cmap, &c->collist, &c->colcnt, &c->sorted, &c->tail_scratch,
                    &c->geo_fact_stream[0][0], &c->geo_fact_stream[0][1], &c->geo_fact_stream[1][0],
                    &c->geo_fact_stream[1][1]};
@@ -997,7 +999,8 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
         std::vector<uint8_t> sx(bx), sh(bh);
         const float* ws[5];
         for (int l = 0; l < 5; ++l) ws[l] = d->weights[l];
-        if (int r = pair_pack(d->which, ws, sx.data(), sh.data())) return r;
+        // (the texture stream carries fp16 skip items: the texture kernel's skip operand is fp16)
+        if (int r = pair_pack(d->which, ws, sx.data(), sh.data(), !geo)) return r;
         if (int r = px.ensure(bx)) return r;
         if (int r = ph.ensure(bh)) return r;
         ICG_CUDA_TRY(cudaMemcpy(px.p, sx.data(), bx, cudaMemcpyHostToDevice));
@@ -1005,6 +1008,15 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
         unsigned char (*tm)[128] = geo ? c->geo_pair_tmap : c->tex_pair_tmap;
         if (int r = pair_make_tmap(px.p, bx, tm[0])) return r;
         if (int r = pair_make_tmap(ph.p, bh, tm[1])) return r;
+        if (geo) {  // the geometry prefix of the texture kernel: same items, fp16 skip items
+            if (int r = pair_pack(d->which, ws, sx.data(), sh.data(), true)) return r;
+            if (int r = c->geo_pair_f16.ensure(bx)) return r;
+            if (int r = c->geo_pair_f16_hi.ensure(bh)) return r;
+            ICG_CUDA_TRY(cudaMemcpy(c->geo_pair_f16.p, sx.data(), bx, cudaMemcpyHostToDevice));
+            ICG_CUDA_TRY(cudaMemcpy(c->geo_pair_f16_hi.p, sh.data(), bh, cudaMemcpyHostToDevice));
+            if (int r = pair_make_tmap(c->geo_pair_f16.p, bx, c->geo_pair_f16_tmap[0])) return r;
+            if (int r = pair_make_tmap(c->geo_pair_f16_hi.p, bh, c->geo_pair_f16_tmap[1])) return r;
+        }
         (geo ? c->geo_pair : c->tex_pair) = true;
     }
     if (geo) {

@@ -31,6 +31,7 @@
 //              the skip operand); the peer's arrive over DSMEM.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -67,18 +68,23 @@ __host__ __device__ constexpr int kSOffL(int l) { return l == 0 ? 0 : l == 1 ? 1
 template <int MODE>
 struct Cfg {
     static constexpr bool TEX = MODE == kModeTex;
-    static constexpr int NPC = (TEX || MODE == kModeGeo64) ? 32 : 64;  // points per CTA
+    static constexpr int NPC = MODE == kModeGeo64 ? 32 : 64;  // points per CTA
     static constexpr int NP = 2 * NPC;               // points per pair tile = MMA N
     // [Phi] or [Phi, h3] in 64-wide K-chunks (none for FACT: Phi enters through the column records)
     static constexpr int kSkipChunks = TEX ? 8 : (MODE == kModeFact ? 0 : 4);
     static constexpr int kHBufs = MODE == kModeFact ? 2 : (MODE == kModeCols ? 0 : 1);  // h operand buffers
     // 32 KB stages (per-copy TMA cost is size-independent)
-    static constexpr int kStages = TEX ? 3 : ((MODE == kModeCols || MODE == kModeGeo64) ? 4 : 2);
+    static constexpr int kStages = (MODE == kModeCols || MODE == kModeGeo64) ? 4 : 2;
+    // TEX: the skip operand [Phi, h3] is ONE fp16 copy (its weights fp16 hi + lo): 10 more mantissa
+    // bits than a bf16 copy keep colours within 1e-3 (max 1.9e-4 simulated) and free the shared
+    // memory of a lo copy, so the texture tile is 128 points like the geometry one
+    static constexpr bool kF16Skip = TEX;
+    static constexpr int kSkipCopies = kF16Skip ? 1 : 2;
     static constexpr uint32_t kChunk = NPC * 128;  // NPC point rows x 64 bf16 (SW128)
     static constexpr uint32_t kSkipHalf = kSkipChunks * kChunk;
     static constexpr uint32_t kHHalf = 4 * kChunk;  // one 256-feature block
     static constexpr uint32_t kOffSkip = 0;
-    static constexpr uint32_t kOffH = kOffSkip + 2 * kSkipHalf;
+    static constexpr uint32_t kOffH = kOffSkip + kSkipCopies * kSkipHalf;
     static constexpr uint32_t kOffRing = kOffH + kHBufs * 2 * kHHalf;
     static constexpr uint32_t kOffMisc = kOffRing + kStages * kStage;
     static constexpr uint32_t kMisc = 24576;
@@ -226,7 +232,7 @@ __device__ __forceinline__ float warp_transpose_reduce(float* v) {
 // 8x8 transpose inside each 8-lane group: lane i of a group holds one feature (8g + i) for 32
 // points; afterwards it holds all 8 features of the group, as bf16 hi (and lo) 16-byte rows, for
 // points 8u + i (u = 0..3).  Three butterfly rounds swap point-index bits with lane bits.
-template <bool LO>
+template <bool LO, bool F16 = false>
 __device__ __forceinline__ void transpose8_bf16(const float* v, uint4* hi, uint4* lo) {
     const int lane = threadIdx.x & 31;
     const bool i0 = lane & 1, i1 = lane & 2, i2 = lane & 4;
@@ -238,9 +244,14 @@ __device__ __forceinline__ void transpose8_bf16(const float* v, uint4* hi, uint4
         const float send = i0 ? v[2 * m] : v[2 * m + 1];
         const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
         const float a = i0 ? recv : keep, b = i0 ? keep : recv;
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-        wh[m] = *reinterpret_cast<uint32_t*>(&h2);
-        if (LO) {
+        if (F16) {
+            __half2 f2 = __floats2half2_rn(a, b);
+            wh[m] = *reinterpret_cast<uint32_t*>(&f2);
+        } else {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+            wh[m] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        if (LO && !F16) {
             __nv_bfloat162 l2 =
                 __floats2bfloat162_rn(a - __uint_as_float(wh[m] << 16), b - __uint_as_float(wh[m] & 0xFFFF0000u));
             wl[m] = *reinterpret_cast<uint32_t*>(&l2);
@@ -439,10 +450,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             // B operand (point activations): K-major (gathered skip operand) or MN-major (h
             // blocks written one feature per thread, FACT); A (weights) is always K-major
             const uint32_t idesc_mn = idesc | (1u << 16);
-            auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc, bool mn = false) {
+            const uint32_t idesc_f16 = idesc & ~((7u << 7) | (7u << 10));  // A, B fp16 (fp32 accumulate)
+            // f16: a skip item of the TEX kernel: fp16 weights (hi, lo) x the single fp16 operand
+            auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc, bool mn = false, bool f16 = false) {
                 const uint64_t bd_hi = mn ? ptx::sdesc_sw128_mn(b_hi) : ptx::sdesc_sw128(b_hi);
                 const uint64_t bd_lo = mn ? ptx::sdesc_sw128_mn(b_lo) : ptx::sdesc_sw128(b_lo);
-                const uint32_t id = mn ? idesc_mn : idesc;
+                const uint32_t id = f16 ? idesc_f16 : (mn ? idesc_mn : idesc);
                 if (P.x3) {
                     wait_full();
                     const uint64_t ad_hi = ptx::sdesc_sw128(ring0 + s * kStage);
@@ -452,7 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                         const uint64_t koff = (uint64_t)(kk * 2);
                         const uint64_t kb = mn ? (uint64_t)(kk * 128) : koff;  // 16 k = 16 rows of 128 B (MN)
                         ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_hi + kb, id, (acc || kk > 0) ? 1u : 0u);
-                        ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_lo + kb, id, 1u);
+                        if (!f16) ptx::mma_bf16_pair(tmem + dcol, ad_hi + koff, bd_lo + kb, id, 1u);
                         ptx::mma_bf16_pair(tmem + dcol, ad_lo + koff, bd_hi + kb, id, 1u);
                     }
                     ptx::mma_commit_pair(&ms.empty[s], both);
@@ -512,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             uint32_t cblk = 0, hblk = 0;  // COLS accumulator blocks / FACT h blocks issued so far
             auto body = [&](int ks, bool with_l4, bool wait_d4) {
                 auto L1 = [&](int c) {
-                    for (int j = 0; j < ks; ++j) item(2 * NP + (c & 1) * NP, skipk(j), skipl(j), j > 0);
+                    for (int j = 0; j < ks; ++j) item(2 * NP + (c & 1) * NP, skipk(j), skipl(j), j > 0, false, C::kF16Skip);
                     ptx::mma_commit_pair(&ms.l1done[c & 1], both);
                 };
                 L1(0);
@@ -523,17 +536,17 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     ptx::tc_fence_after();
                 }
                 for (int m = 0; m < 2; ++m)
-                    for (int j = 0; j < ks; ++j) item(m * NP, skipk(j), skipl(j), j > 0);
+                    for (int j = 0; j < ks; ++j) item(m * NP, skipk(j), skipl(j), j > 0, false, C::kF16Skip);
                 for (int c = 0; c < 4; ++c) {
                     h_block(2, 0);
                     if (c + 2 < 4) L1(c + 2);
                 }
                 ptx::mma_commit_pair(&ms.d2done, both);
-                for (int j = 0; j < ks; ++j) item(2 * NP, skipk(j), skipl(j), j > 0);
+                for (int j = 0; j < ks; ++j) item(2 * NP, skipk(j), skipl(j), j > 0, false, C::kF16Skip);
                 for (int c = 0; c < 2; ++c) h_block(1, 2 * NP);
                 ptx::mma_commit_pair(&ms.d3done, both);
                 if (with_l4) {
-                    for (int j = 0; j < ks; ++j) item(0, skipk(j), skipl(j), j > 0);
+                    for (int j = 0; j < ks; ++j) item(0, skipk(j), skipl(j), j > 0, false, C::kF16Skip);
                     ptx::mma_commit_pair(&ms.skip_free, both);  // last reader of the skip operand
                     h_block(1, 0);
                     ptx::mma_commit_pair(&ms.d4done, both);
@@ -650,7 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
         };
         auto emit_block = [&](uint32_t col, const float* bias_blk, int out_dim, int feat0, uint32_t dst,
                               uint32_t lo_off, bool write_lo, int soff = -1, bool from_tmem = true,
-                              const Pre* pre = nullptr) {
+                              const Pre* pre = nullptr, bool f16 = false) {
             const int o = feat0 + (int)feat;
             const float bo = FACT ? pre->bo : __ldg(&bias_blk[o]);
             const float wz = FACT ? pre->wz : __ldg(&bias_blk[out_dim + o]);
@@ -731,7 +744,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 }
                 // rows (points) 8u + (lane & 7) of this hf block, 16-byte chunk of this lane group's 8 features
                 uint4 hv[4], lv[4];
-                if (write_lo)
+                if (f16)
+                    transpose8_bf16<false, true>(v, hv, lv);
+                else if (write_lo)
                     transpose8_bf16<true>(v, hv, lv);
                 else
                     transpose8_bf16<false>(v, hv, lv);
@@ -801,8 +816,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             }
             wait_acc(&ms.d3done, d3ph);
             h_begin();
-            if (prefix)  // h3 -> skip K-chunks 4..7 (lo always: the final skip dot reads hi + lo)
-                emit_block(2 * NP, b3, 256, 0, sdst, kSkipHalf, true);
+            if (prefix)  // h3 -> skip K-chunks 4..7 (TEX: the single fp16 skip copy)
+                emit_block(2 * NP, b3, 256, 0, sdst, kSkipHalf, !C::kF16Skip, -1, true, nullptr, C::kF16Skip);
             else
                 emit_block(2 * NP, b3, 256, 0, hdst, kHHalf, P.x3);
             h_end();
@@ -914,8 +929,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
                             const float a = val[2 * i], b = val[2 * i + 1];
-                            hp[i] = pack_bf16(a, b);
-                            lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                            if constexpr (C::kF16Skip) {
+                                __half2 f2 = __floats2half2_rn(a, b);
+                                hp[i] = *reinterpret_cast<uint32_t*>(&f2);
+                                lp[i] = 0u;
+                            } else {
+                                hp[i] = pack_bf16(a, b);
+                                lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                            }
 #pragma unroll
                             for (int c = 0; c < NOUT; ++c) {
                                 dot[c] = fmaf(w5s[c][2 * i], a, dot[c]);
@@ -924,7 +945,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                         }
                         const uint32_t off = chunk + (uint32_t)pl * 128u + (((c16 ^ (uint32_t)pl) & 7u) << 4);
                         *reinterpret_cast<uint4*>(skip + off) = hv;
-                        *reinterpret_cast<uint4*>(skip + kSkipHalf + off) = lv;
+                        if constexpr (!C::kF16Skip) *reinterpret_cast<uint4*>(skip + kSkipHalf + off) = lv;
 #pragma unroll
                         for (int c = 0; c < NOUT; ++c)
 #pragma unroll
@@ -1014,8 +1035,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     ptx::mbar_wait_cluster(&ms.sd_ready[tp], (sdph_bits >> tp) & 1u);
                     sdph_bits ^= 1u << tp;
                 }
-                if (et < NP * NOUT) {
-                    const int p = et % NP, c = et / NP;
+                for (int e = et; e < NP * NOUT; e += kEpiThreads) {  // (texture: 384 outputs, 256 threads)
+                    const int p = e % NP, c = e / NP;
                     const unsigned idx = base + p;
                     const float s = ms.red[0][c][p] + ms.red[1][c][p] + ms.red[2][c][p] + ms.red[3][c][p] +
                                     ms.skipdot[tp][c][p] + ms.cterm[FACT ? tp : c][p];
@@ -1204,17 +1225,26 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 // part of the final skip dot for this CTA's points (fp32 from hi + lo)
                 body_epi(P.bias_t, false, [&] {
                     epi_bar();  // ms.sdl from the gather warps
-                    const int pl = et >> 3, part = et & 7;  // NPC = 32 points x 8 slices of 32 features
+                    // NPC points x kSl slices of 256 / kSl features (h3 = skip K 256..511, fp16)
+                    constexpr int kSl = kEpiThreads / NPC, kSF = 256 / kSl;
+                    const int pl = et / kSl, part = et % kSl;
                     float acc[NOUT];
 #pragma unroll
                     for (int c = 0; c < NOUT; ++c) acc[c] = 0.0f;
-                    for (int j = part * 32; j < part * 32 + 32; j += 2) {
+                    for (int j = part * kSF; j < part * kSF + kSF; j += 2) {
                         const int k = 256 + j;
                         const uint32_t off = (uint32_t)(k >> 6) * kChunk + sw128((uint32_t)pl, (uint32_t)(k & 63));
                         const uint32_t hv = *reinterpret_cast<const uint32_t*>(skip + off);
-                        const uint32_t lv = *reinterpret_cast<const uint32_t*>(skip + kSkipHalf + off);
-                        const float x0 = __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
-                        const float x1 = __uint_as_float(hv & 0xFFFF0000u) + __uint_as_float(lv & 0xFFFF0000u);
+                        float x0, x1;
+                        if constexpr (C::kF16Skip) {
+                            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hv));
+                            x0 = f.x;
+                            x1 = f.y;
+                        } else {
+                            const uint32_t lv = *reinterpret_cast<const uint32_t*>(skip + kSkipHalf + off);
+                            x0 = __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
+                            x1 = __uint_as_float(hv & 0xFFFF0000u) + __uint_as_float(lv & 0xFFFF0000u);
+                        }
 #pragma unroll
                         for (int c = 0; c < NOUT; ++c) {
                             acc[c] = fmaf(__ldg(&P.wlast[c * wl_stride + 128 + k]), x0, acc[c]);
@@ -1224,7 +1254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
 #pragma unroll
                     for (int c = 0; c < NOUT; ++c)
 #pragma unroll
-                        for (int o = 1; o < 8; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+                        for (int o = 1; o < kSl; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
                     if (part == 0) {
                         const int p = (int)rank * NPC + pl;
 #pragma unroll
@@ -1295,7 +1325,10 @@ size_t pair_stream_bytes(int which, bool x3) {
 
 // item i, rank r (rows r*128.. of the 256-row block), part (hi/lo): 16 KB SW128 tile
 // sched: 0 = full network (pair::schedule), 1 = FACT items, 2 = COLS items (geometry only)
-static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi) {
+// f16skip: items over the skip input (K columns >= the hidden width) as fp16 hi / lo (the TEX
+// kernel's single fp16 skip operand); everything else bf16 hi / lo
+static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi,
+                           bool f16skip = false) {
     const bool geo = which == ICG_MLP_GEOMETRY;
     const int* outs = geo ? kGeoOut : kTexOut;
     const int skip = geo ? kGeoSkip : kTexSkip;
@@ -1305,6 +1338,7 @@ static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t*
     for (int l = 0; l < 5; ++l) ins[l] = (l ? outs[l - 1] : 0) + skip;
     int item = 0;
     auto emit = [&](int l, int m, int col0) {
+        const bool f16 = f16skip && col0 >= (l ? outs[l - 1] : 0);
         for (int h = 0; h < 2; ++h) {
             uint8_t* hi = stream_x3 + ((size_t)(h * nitems + item) * 2 + 0) * pair::kHalf;
             uint8_t* lo = stream_x3 + ((size_t)(h * nitems + item) * 2 + 1) * pair::kHalf;
@@ -1313,8 +1347,16 @@ static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t*
                 const int o = m * 256 + h * 128 + r;
                 for (int k = 0; k < 64; ++k) {
                     float v = o < outs[l] ? w[l][(size_t)o * ins[l] + col0 + k] : 0.0f;
-                    uint16_t a = f2bf_p(v);
-                    uint16_t b = f2bf_p(v - bf2f_p(a));
+                    uint16_t a, b;
+                    if (f16) {
+                        const __half ha = __float2half_rn(v);
+                        const __half hb = __float2half_rn(v - __half2float(ha));
+                        std::memcpy(&a, &ha, 2);
+                        std::memcpy(&b, &hb, 2);
+                    } else {
+                        a = f2bf_p(v);
+                        b = f2bf_p(v - bf2f_p(a));
+                    }
                     size_t off = (size_t)r * 128 + (size_t)(((k >> 3) ^ (r & 7)) << 4) + (size_t)(k & 7) * 2;
                     std::memcpy(hi + off, &a, 2);
                     std::memcpy(lo + off, &b, 2);
@@ -1333,8 +1375,8 @@ static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t*
     return item == nitems ? ICG_OK : ICG_ERUNTIME;
 }
 
-int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi) {
-    return pair_pack_sched(which, 0, w, stream_x3, stream_hi);
+int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi, bool f16skip) {
+    return pair_pack_sched(which, 0, w, stream_x3, stream_hi, f16skip);
 }
 
 size_t pair_fact_stream_bytes(int part, bool x3) {
