@@ -100,7 +100,7 @@ struct icg_context {
     bool fact_used = false;  // the last extraction ran its bulk batches column-factored
     DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
     bool use_tail = true;
-    unsigned tail_max = 100;  // conflict batches up to this size start the persistent tail kernel
+    unsigned tail_max = 128;  // conflict batches up to this size start the persistent tail kernel
     bool use_pair = true;
     // field
     DBuf scene;

@@ -61,7 +61,7 @@ struct Smem {
     float w4[kMaxOwn4][256];
     float wphi[kMaxOwnS][256];
     float wlast[128];
-    alignas(16) float stage[kPB * 1024];  // activations of kPB points (layer input)
+    alignas(16) float stage[2][kPB * 1024];  // activations of kPB points (layer input), double-buffered
 };
 
 __device__ __forceinline__ float leaky(float x, float s) { return x < 0.0f ? x * s : x; }
@@ -244,20 +244,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
             // all in flight), then a warp computes (owned row, point) dot products from it.
             auto layer = [&](const float* hin, int K, const float* wrows, int nown, int rows, int soff,
                              const float* bl, float* hout) {
-                for (unsigned pb = 0; pb < nc; pb += kPB) {
+                // double-buffered: the next block's copies are in flight while this one is computed
+                auto issue = [&](unsigned pb, int buf) {
                     const unsigned np = min((unsigned)kPB, nc - pb);
                     const float4* src = reinterpret_cast<const float4*>(hin + (size_t)pb * K);
-                    float4* dst = reinterpret_cast<float4*>(sm.stage);
+                    float4* dst = reinterpret_cast<float4*>(sm.stage[buf]);
                     const unsigned nv = np * (unsigned)K / 4u;
-                    // asynchronous 16-byte copies (L2 only): every load of the block in flight at once
-                    for (unsigned e = tid; e < nv; e += kThreads) {
+                    for (unsigned e = tid; e < nv; e += kThreads) {  // 16-byte copies, L2 only
                         const uint32_t d = (uint32_t)__cvta_generic_to_shared(&dst[e]);
                         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(&src[e]) : "memory");
                     }
-                    asm volatile("cp.async.wait_all;" ::: "memory");
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                };
+                issue(0, 0);
+                int b = 0;
+                for (unsigned pb = 0; pb < nc; pb += kPB, ++b) {
+                    const unsigned np = min((unsigned)kPB, nc - pb);
+                    if (pb + kPB < nc) {
+                        issue(pb + kPB, (b + 1) & 1);
+                        asm volatile("cp.async.wait_group 1;" ::: "memory");
+                    } else {
+                        asm volatile("cp.async.wait_group 0;" ::: "memory");
+                    }
                     __syncthreads();
+                    const float* stage = sm.stage[b & 1];
                     for (unsigned t = warp; t < np; t += kWarps) {
-                        const float* h = sm.stage + (size_t)t * K;
+                        const float* h = stage + (size_t)t * K;
+                        const unsigned tt = pb + t;
+                        // this point's per-row epilogue operands (lane a < nown: row a), loaded before
+                        // the dot so their latency overlaps it
+                        const int r_l = cta + lane * G;
+                        float pre_s = 0.0f, pre_b = 0.0f, pre_w = 0.0f, z = 0.0f;
+                        {
+                            const int slot = __ldcg(&P.pslot[tt]);
+                            z = __ldcg(&P.pz[tt]);
+                            if (lane < nown && r_l < rows) {
+                                pre_s = __ldcg(&P.colrec[(size_t)slot * kRec + soff + r_l]);
+                                pre_b = __ldg(&bl[r_l]);
+                                pre_w = __ldg(&bl[rows + r_l]);
+                            }
+                        }
                         float acc[kMaxOwn2];
 #pragma unroll
                         for (int a = 0; a < kMaxOwn2; ++a) acc[a] = 0.0f;
@@ -269,20 +295,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
                             for (int a = 0; a < kMaxOwn2; ++a)
                                 if (a < nown) acc[a] = fmaf(wrows[(size_t)a * K + k], x, acc[a]);
                         }
-                        const unsigned tt = pb + t;
-                        const int slot = __ldcg(&P.pslot[tt]);
-                        const float z = __ldcg(&P.pz[tt]);
+                        float mine = 0.0f;
 #pragma unroll
                         for (int a = 0; a < kMaxOwn2; ++a) {
                             if (a >= nown) break;
                             const float sum = warp_sum(acc[a]);
-                            const int r = cta + a * G;
-                            if (lane == 0 && r < rows)
-                                hout[(size_t)tt * rows + r] =
-                                    leaky(sum + __ldcg(&P.colrec[(size_t)slot * kRec + soff + r]) +
-                                              fmaf(__ldg(&bl[rows + r]), z, __ldg(&bl[r])),
-                                          slope);
+                            if (lane == a) mine = sum;
                         }
+                        if (lane < nown && r_l < rows)
+                            hout[(size_t)tt * rows + r_l] = leaky(mine + pre_s + fmaf(pre_w, z, pre_b), slope);
                     }
                     __syncthreads();
                 }
