@@ -389,11 +389,20 @@ def main():
     exec_mult = 3 if prec_name == "fp32" else 1
     achieved = fact_pts * GEO_FLOP_PER_POINT / fact_s / 1e12 if fact_s > 0 else 0.0
     executed = fact_pts * FACT_MMA_FLOP_PER_POINT * exec_mult / fact_s / 1e12 if fact_s > 0 else 0.0
+    traffic, traffic_note = None, None
+    try:  # DRAM bytes of the factored pass's level-3 launch, from the committed ncu --set full capture
+        rec = json.load(open(os.path.join(ROOT, "profiles", "r01b_ncu_full_fact_L3.json")))[0]
+        mb = lambda v: float(v.split()[0]) * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}[v.split()[1]]
+        traffic = (mb(rec["dram__bytes_read.sum"]) + mb(rec["dram__bytes_write.sum"])) * 1e6
+        traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum of the level-3 FACT launch (280 k points, "
+                        "profiles/r01b_ncu_full_fact_L3.json): weights, column records and lists, L2-resident at 92 %")
+    except Exception:
+        pass
     roofline = {"bound": "tensor",
                 "kernel": "geometry field, bulk batches (dense level 0 + each level's E0 list): column pass "
                           "k_mlp_pair<COLS> + factored pass k_mlp_pair<FACT> (CTA-pair tcgen05), incl. list sorting",
                 "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
-                "traffic": None,
+                "traffic": traffic, "traffic_note": traffic_note,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" + (" (fallback)" if pk.get("fallback") else ""),
                 "algorithmic_flop_per_point": GEO_FLOP_PER_POINT,
                 "achieved_note": "dense-equivalent algorithmic FLOP (SURVEY §8(d)); the factored pass executes fewer",
