@@ -369,3 +369,72 @@ def test_concurrent_contexts_match_serial(pifu_inputs):
         assert np.array_equal(is_.rgb, ic.rgb) and np.array_equal(is_.surface_k, ic.surface_k)
     for c in ctxs:
         c.close()
+
+
+# ---------------------------------------------------------------------------
+# config 3: bf16 weights / activations with fp32 accumulation
+# ---------------------------------------------------------------------------
+OCC_TOL_BF16 = 1e-2
+RGB_TOL_BF16 = 1e-2  # bf16 texture network (config 3); the fp32 configs hold 1e-3
+
+
+@pytest.mark.gpu
+def test_bf16_occupancy_and_texture(gpu_ctx, pifu_inputs):
+    f = _pifu(gpu_ctx, pifu_inputs, abi.ICG_PREC_BF16)
+    m = _oracle_model(pifu_inputs)
+    rng = np.random.default_rng(11)
+    pts = rng.uniform(-1, 1, (3000, 3))
+    pts[:500] = np.round((pts[:500] + 1) * 128) / 128 - 1
+    assert np.abs(gpu_ctx.occupancy_batch(f, pts) - m.occupancy(pts)).max() <= OCC_TOL_BF16
+    assert np.abs(gpu_ctx.texture_batch(f, pts[:1000]) - m.texture(pts[:1000])).max() <= RGB_TOL_BF16
+
+
+@pytest.mark.gpu
+def test_bf16_localization_replay_and_render(gpu_ctx, pifu_inputs):
+    """Config 3 at test scale: the control flow is exact (replay through the reference), node
+    values within the bf16 tolerance, first crossings exact against the oracle renderer on the
+    GPU's own grid."""
+    f = _pifu(gpu_ctx, pifu_inputs, abi.ICG_PREC_BF16)
+    cfg = api.AlgoConfig("progressive", 16, 3)
+    cam = api.CameraSpec.from_angles(90, 0)
+    ext, img = gpu_ctx.frame(f, cfg, cam, 200, 200, want_grid=True)
+    replay_check(ext, 16, 3)
+    ev = np.flatnonzero(ext.states == abi.ICG_STATE_EVALUATED)
+    sub = ev[:: max(1, len(ev) // 3000)]
+    n = 129
+    i, j, k = sub % n, (sub // n) % n, sub // (n * n)
+    pts = np.stack([-1 + 2 * i / 128.0, -1 + 2 * j / 128.0, 1 - 2 * k / 128.0], 1)
+    m = _oracle_model(pifu_inputs)
+    assert np.abs(ext.values[sub] - m.occupancy(pts)).max() <= OCC_TOL_BF16
+    r = O.render_first_crossing(ext.values, 128, O.camera_from_angles(90, 0), 200, 200, tex=m)
+    assert np.array_equal(img.surface_k, r["surface_k"]) and np.array_equal(img.depth, r["depth"])
+    assert np.abs(img.rgb - r["rgb"]).max() <= RGB_TOL_BF16
+
+
+@pytest.mark.gpu
+def test_config3_full_size_properties(gpu_ctx):
+    """BASELINE config 3 at full size (512^3 with the 32->512 hierarchy, feature map 256x256x256,
+    1024x1024 render, bf16): size-independent invariants and sampled node values."""
+    caps = api.gen_capsules(42)
+    fmap = api.gen_feature_map(1000, 256, 256, 256)
+    gw, gb = api.gen_mlp(7, 0)
+    tw, tb = api.gen_mlp(8, 1)
+    gpu_ctx.set_mlp(abi.ICG_MLP_GEOMETRY, gw, gb)
+    gpu_ctx.set_mlp(abi.ICG_MLP_TEXTURE, tw, tb)
+    f = api.PifuField(fmap, caps, 50.0, abi.ICG_PREC_BF16)
+    cfg = api.AlgoConfig("progressive", 32, 4)
+    cam = api.CameraSpec.from_angles(90, 0)
+    ext, img = gpu_ctx.frame(f, cfg, cam, 1024, 1024, want_grid=True)
+    ev = np.flatnonzero(ext.states == abi.ICG_STATE_EVALUATED)
+    assert len(ev) == ext.total_evals and ext.evals_per_level[0] == 33 ** 3
+    assert len(ext.evals_per_level) == 5 and all(e > 0 for e in ext.evals_per_level)
+    assert np.array_equal(ext.binarized, (ext.values >= 0.5).astype(np.uint8))
+    assert img.texture_points == img.covered_pixels > 0
+    ext2, img2 = gpu_ctx.frame(f, cfg, cam, 1024, 1024)
+    assert ext2.evals_per_level == ext.evals_per_level and np.array_equal(img.rgb, img2.rgb)
+    m = O.Pifu(fmap, caps, gw, gb, tw, tb, threads=8)
+    sub = ev[:: max(1, len(ev) // 2000)]
+    n = 513
+    i, j, k = sub % n, (sub // n) % n, sub // (n * n)
+    pts = np.stack([-1 + 2 * i / 512.0, -1 + 2 * j / 512.0, 1 - 2 * k / 512.0], 1)
+    assert np.abs(ext.values[sub] - m.occupancy(pts)).max() <= OCC_TOL_BF16
