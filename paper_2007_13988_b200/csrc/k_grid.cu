@@ -98,29 +98,36 @@ __global__ void __launch_bounds__(kFineThreads)
 k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const uint32_t* __restrict__ cbin,
             const uint32_t* __restrict__ mixed, int rc, float* __restrict__ fv, uint8_t* __restrict__ fs,
             uint32_t* __restrict__ tentbin, uint32_t* __restrict__ sel) {
-    __shared__ uint32_t prow[kFineThreads / 32][4][kRowWords];
+    // per warp: the parent rows' binarised bits summed per coarse node, as 3 bit planes
+    // (count = p0 + 2 p1 + 4 p2, count <= 4), and the OR of the adjacent mixed-cell rows
+    __shared__ uint32_t plane[kFineThreads / 32][3][kRowWords];
     __shared__ uint32_t mrow[kFineThreads / 32][kRowWords];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int fn = 2 * rc + 1, cn = rc + 1;
     const uint32_t nrows_total = (uint32_t)fn * (uint32_t)fn;
     const int cwords = (cn + 31) >> 5, mwords = (rc + 31) >> 5;
-    uint32_t(*pr)[kRowWords] = prow[wl];
+    uint32_t(*pl)[kRowWords] = plane[wl];
     uint32_t* mr = mrow[wl];
     for (uint32_t row = blockIdx.x * (kFineThreads / 32) + wl; row < nrows_total; row += gridDim.x * (kFineThreads / 32)) {
         const int k = (int)(row / (uint32_t)fn), j = (int)(row - (uint32_t)k * fn);
         const int j0 = j >> 1, j1 = (j + 1) >> 1, k0 = k >> 1, k1 = (k + 1) >> 1;
-        const int nj = 1 + (j1 != j0), nk = 1 + (k1 != k0), npr = nj * nk;
+        const bool jy = j1 != j0, kz = k1 != k0;
+        const int lgr = (int)jy + (int)kz;  // log2 of the parent rows (1, 2 or 4)
         int yl, yh, zl, zh;
         adjacent_cells(j, rc, yl, yh);
         adjacent_cells(k, rc, zl, zh);
         __syncwarp();
-        // stage: parent rows r = (jj - j0) + nj * (kk - k0), and the OR of the adjacent mixed rows
-        for (int t = lane; t < 4 * cwords; t += 32) {
-            const int r = t / cwords, w = t - r * cwords;
-            if (r < npr) {
-                const int jj = j0 + r % nj, kk = k0 + r / nj;
-                pr[r][w] = row_word(cbin, (uint32_t)cn * ((uint32_t)jj + (uint32_t)cn * (uint32_t)kk), w);
-            }
+        if (lane < cwords) {
+            // bit-sliced sum of the (1, 2 or 4) parent bit rows (upsample_interpolate, grid.hpp:106-115)
+            const uint32_t a = row_word(cbin, (uint32_t)cn * ((uint32_t)j0 + (uint32_t)cn * (uint32_t)k0), lane);
+            const uint32_t b = jy ? row_word(cbin, (uint32_t)cn * ((uint32_t)j1 + (uint32_t)cn * (uint32_t)k0), lane) : 0u;
+            const uint32_t c = kz ? row_word(cbin, (uint32_t)cn * ((uint32_t)j0 + (uint32_t)cn * (uint32_t)k1), lane) : 0u;
+            const uint32_t d = (jy && kz) ? row_word(cbin, (uint32_t)cn * ((uint32_t)j1 + (uint32_t)cn * (uint32_t)k1), lane) : 0u;
+            const uint32_t ab0 = a ^ b, ab1 = a & b, cd0 = c ^ d, cd1 = c & d;
+            const uint32_t carry = ab0 & cd0, t = ab1 ^ cd1;
+            pl[0][lane] = ab0 ^ cd0;
+            pl[1][lane] = t ^ carry;
+            pl[2][lane] = (ab1 & cd1) | (t & carry);
         }
         if (lane < mwords) {
             uint32_t m = 0;
@@ -133,26 +140,29 @@ k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const 
         const uint32_t rowbase = row * (uint32_t)fn;
         const bool even_jk = !((j | k) & 1);
         const uint32_t cbase = (uint32_t)cn * ((uint32_t)j0 + (uint32_t)cn * (uint32_t)k0);
+        auto count = [&](int x) -> int {
+            const int w = x >> 5, sh = x & 31;
+            return (int)((pl[0][w] >> sh) & 1u) + 2 * (int)((pl[1][w] >> sh) & 1u) + 4 * (int)((pl[2][w] >> sh) & 1u);
+        };
         for (int i0w = 0; i0w < fn; i0w += 32) {
             const int i = i0w + lane;
             bool tb = false, sl = false;
             if (i < fn) {
-                const int i0 = i >> 1, i1 = (i + 1) >> 1;
+                const int odd = i & 1, x0 = i >> 1;
+                const int ones = count(x0) + (odd ? count(x0 + 1) : 0);
                 float v;
                 uint8_t st;
-                if (even_jk && !(i & 1)) {
+                if (even_jk && !odd) {
                     // even node: carry the coarse scalar and state (carry_scalars, localize.hpp:116-119)
-                    v = cv[cbase + i0];
-                    st = cs[cbase + i0];
-                    tb = sbit(pr[0], i0);
+                    v = __ldg(&cv[cbase + x0]);
+                    st = __ldg(&cs[cbase + x0]);
+                    tb = ones != 0;  // its tentative value is the binarised coarse value
                 } else {
-                    // mean of the binarised parents (upsample_interpolate, grid.hpp:106-115): exact dyadic
-                    int ones = 0;
-                    for (int r = 0; r < npr; ++r) ones += sbit(pr[r], i0) + (i1 != i0 ? sbit(pr[r], i1) : 0);
-                    const int cnt = npr * (1 + (i1 != i0));  // 1, 2, 4 or 8: the quotient is exact
-                    v = (float)ones * __int_as_float((127 - (31 - __clz(cnt))) << 23);
+                    // mean of the binarised parents: exact dyadic ones / 2^lg
+                    const int lg = lgr + odd;
+                    v = (float)ones * __int_as_float((127 - lg) << 23);
                     st = ICG_STATE_INTERPOLATED;
-                    tb = 2 * ones >= cnt;  // tent >= 0.5f
+                    tb = 2 * ones >= (1 << lg);  // tent >= 0.5f
                 }
                 fv[rowbase + i] = v;
                 fs[rowbase + i] = st;
