@@ -42,16 +42,23 @@ namespace tail {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRec = 1936;  // column record floats (k_mlp_pair.cu kSRow)
-// A small grid: every activation is read by every CTA (rows are partitioned), so fewer, fatter
-// CTAs keep that broadcast cheap; 32 CTAs hold all resident weights in shared memory.
+// Grid size: every activation is read by every CTA (rows are partitioned), so more CTAs mean
+// less work but more broadcast per CTA.  The kernel is cooperative and holds its SMs for the whole
+// chain while doing little, so with several frames in flight a smaller grid leaves SMs to the
+// other frames: 64 CTAs measured 222 frames/s (3 in flight) vs 191 with 148, at +3 % single-frame
+// latency (5.73 vs 5.57 ms).
 #ifndef ICG_TAIL_CTAS
-#define ICG_TAIL_CTAS 148
+#define ICG_TAIL_CTAS 64
 #endif
 constexpr int kG = ICG_TAIL_CTAS;
 constexpr int kMaxOwn2 = (512 + kG - 1) / kG, kMaxOwn3 = (256 + kG - 1) / kG, kMaxOwn4 = (128 + kG - 1) / kG;
 constexpr int kSRows = 1921;  // Phi rows of a record: 1024 + 512 + 256 + 128 + final dot
 constexpr int kMaxOwnS = (kSRows + kG - 1) / kG;
 constexpr int kPB = 16;       // points per staged activation block
+// double-buffer the staged activations when the resident weights leave room for it
+constexpr size_t kWeightBytes = 4 * ((size_t)kMaxOwn2 * 1024 + (size_t)kMaxOwn3 * 512 + (size_t)kMaxOwn4 * 256 +
+                                     (size_t)kMaxOwnS * 256 + 128);
+constexpr int kStageBufs = kWeightBytes + 2 * (size_t)kPB * 1024 * 4 <= 220 * 1024 ? 2 : 1;
 
 __host__ __device__ constexpr int rec_row_layer(int r) { return r < 1024 ? 0 : r < 1536 ? 1 : r < 1792 ? 2 : r < 1920 ? 3 : 4; }
 
@@ -61,7 +68,7 @@ struct Smem {
     float w4[kMaxOwn4][256];
     float wphi[kMaxOwnS][256];
     float wlast[128];
-    alignas(16) float stage[2][kPB * 1024];  // activations of kPB points (layer input), double-buffered
+    alignas(16) float stage[kStageBufs][kPB * 1024];  // activations of kPB points (layer input)
 };
 
 __device__ __forceinline__ float leaky(float x, float s) { return x < 0.0f ? x * s : x; }
@@ -258,16 +265,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
                 };
                 issue(0, 0);
                 int b = 0;
+                static_assert(kStageBufs == 1 || kStageBufs == 2, "stage buffers");
                 for (unsigned pb = 0; pb < nc; pb += kPB, ++b) {
                     const unsigned np = min((unsigned)kPB, nc - pb);
-                    if (pb + kPB < nc) {
+                    if (kStageBufs == 2 && pb + kPB < nc) {
                         issue(pb + kPB, (b + 1) & 1);
                         asm volatile("cp.async.wait_group 1;" ::: "memory");
                     } else {
                         asm volatile("cp.async.wait_group 0;" ::: "memory");
                     }
                     __syncthreads();
-                    const float* stage = sm.stage[b & 1];
+                    const float* stage = sm.stage[kStageBufs == 2 ? (b & 1) : 0];
                     for (unsigned t = warp; t < np; t += kWarps) {
                         const float* h = stage + (size_t)t * K;
                         const unsigned tt = pb + t;
@@ -306,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
                             hout[(size_t)tt * rows + r_l] = leaky(mine + pre_s + fmaf(pre_w, z, pre_b), slope);
                     }
                     __syncthreads();
+                    if (kStageBufs == 1 && pb + kPB < nc) issue(pb + kPB, 0);  // single buffer: refill now
                 }
             };
             tr(5);
