@@ -91,19 +91,78 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(RenderJob r) {
         int k1 = -1;
         float vprev = 0.0f, vhit = 0.0f, last = 0.0f;
         bool grazing = false;
-        for (int kb = 0; kb <= R; kb += 32) {
-            const int k = kb + lane;
+        // Rays that run along grid x (the yaw-90 view): every grid coordinate of a sample is a
+        // monotone function of k (each step a correctly rounded op with fixed operands), so if gy
+        // and gk agree at k = 0 and k = R they are the SAME for every sample.  Those rays hoist
+        // the y/z part of the coordinates and of the trilinear setup out of the sample loop, and a
+        // sample with fx == 0 skips its x+1 corners (lerp_rn(a, b, 0) == a exactly for finite
+        // values).  Every arithmetic result is unchanged.
+        float gyc = 0.0f, gkc = 0.0f;
+        if (lane < 2) {
+            const double v2 = __dsub_rn(vz_tab[lane == 0 ? 0 : R], r.trans[2]);
+            gyc = (float)__dmul_rn(__dadd_rn(__dadd_rn(c1, __dmul_rn(m[7], v2)), 1.0), hr);
+            gkc = (float)__dmul_rn(__dsub_rn(1.0, __dadd_rn(c2, __dmul_rn(m[8], v2))), hr);
+        }
+        const float gy_a = __shfl_sync(0xffffffffu, gyc, 0), gy_b = __shfl_sync(0xffffffffu, gyc, 1);
+        const float gk_a = __shfl_sync(0xffffffffu, gkc, 0), gk_b = __shfl_sync(0xffffffffu, gkc, 1);
+        const bool xray = gy_a == gy_b && gk_a == gk_b;
+        const bool yz_in = gy_a >= 0.0f && gy_a <= fR && gk_a >= 0.0f && gk_a <= fR;
+        const int j0 = min((int)floorf(gy_a), R - 1), kk0 = min((int)floorf(gk_a), R - 1);
+        const float fy = __fsub_rn(gy_a, (float)j0), fk = __fsub_rn(gk_a, (float)kk0);
+        const size_t nn = (size_t)R + 1;
+        const size_t byz = nn * ((size_t)j0 + nn * (size_t)kk0);
+        auto sample_at = [&](int k) -> float {
             float v = 0.0f;
             if (k <= R) {
                 const double v2 = __dsub_rn(vz_tab[k], r.trans[2]);
                 const double w0 = __dadd_rn(c0, __dmul_rn(m[6], v2));
-                const double w1 = __dadd_rn(c1, __dmul_rn(m[7], v2));
-                const double w2 = __dadd_rn(c2, __dmul_rn(m[8], v2));
                 const float gx = (float)__dmul_rn(__dadd_rn(w0, 1.0), hr);
-                const float gy = (float)__dmul_rn(__dadd_rn(w1, 1.0), hr);
-                const float gk = (float)__dmul_rn(__dsub_rn(1.0, w2), hr);
-                v = sample_grid(r.values, R, gx, gy, gk);
+                if (xray) {
+                    if (yz_in && gx >= 0.0f && gx <= fR) {
+                        const int i0 = min((int)floorf(gx), R - 1);
+                        const float fx = __fsub_rn(gx, (float)i0);
+                        const float* V = r.values + byz + (size_t)i0;
+                        const size_t sj = nn, sk = nn * nn;
+                        float c00, c10, c01, c11;
+                        if (fx == 0.0f) {
+                            c00 = __ldg(&V[0]);
+                            c10 = __ldg(&V[sj]);
+                            c01 = __ldg(&V[sk]);
+                            c11 = __ldg(&V[sj + sk]);
+                        } else {
+                            c00 = lerp_rn(__ldg(&V[0]), __ldg(&V[1]), fx);
+                            c10 = lerp_rn(__ldg(&V[sj]), __ldg(&V[sj + 1]), fx);
+                            c01 = lerp_rn(__ldg(&V[sk]), __ldg(&V[sk + 1]), fx);
+                            c11 = lerp_rn(__ldg(&V[sj + sk]), __ldg(&V[sj + sk + 1]), fx);
+                        }
+                        const float cy0 = lerp_rn(c00, c10, fy);
+                        const float cy1 = lerp_rn(c01, c11, fy);
+                        v = lerp_rn(cy0, cy1, fk);
+                    }
+                } else {
+                    const double w1 = __dadd_rn(c1, __dmul_rn(m[7], v2));
+                    const double w2 = __dadd_rn(c2, __dmul_rn(m[8], v2));
+                    const float gy = (float)__dmul_rn(__dadd_rn(w1, 1.0), hr);
+                    const float gk = (float)__dmul_rn(__dsub_rn(1.0, w2), hr);
+                    v = sample_grid(r.values, R, gx, gy, gk);
+                }
             }
+            return v;
+        };
+        // kBatch 32-sample chunks per iteration (measured: batching chunks so more corner loads are
+        // in flight costs more in registers and discarded samples than it hides; 1 is fastest)
+        constexpr int kBatch = 1;
+        for (int kb2 = 0; kb2 <= R; kb2 += 32 * kBatch) {
+            float vv[kBatch];
+#pragma unroll
+            for (int h = 0; h < kBatch; ++h) vv[h] = kb2 + 32 * h <= R ? sample_at(kb2 + 32 * h + lane) : 0.0f;
+            bool done = false;
+#pragma unroll
+            for (int h = 0; h < kBatch; ++h) {
+            const int kb = kb2 + 32 * h;
+            if (done || kb > R) break;
+            const int k = kb + lane;
+            const float v = vv[h];
             const unsigned hit = __ballot_sync(0xffffffffu, k <= R && v >= 0.5f);
             const int first = hit ? __ffs(hit) - 1 : 32;
             // samples before the crossing: grazing (0 < v < 1), render.hpp:180-188
@@ -114,9 +173,12 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(RenderJob r) {
                 vhit = __shfl_sync(0xffffffffu, v, first);
                 const float pv = __shfl_sync(0xffffffffu, prev_in_chunk, first);
                 vprev = first > 0 ? pv : last;
+                done = true;
                 break;
             }
             last = __shfl_sync(0xffffffffu, v, 31);
+            }
+            if (done) break;
         }
         if (lane == 0) {
             r.rgb[3 * px + 0] = r.bg[0];
