@@ -65,7 +65,7 @@ constexpr int kRenderThreads = 256;
 // runs along the x-fastest memory axis, as for yaw 90).  The first crossing is
 // the lowest lane whose value is >= 0.5f (ballot); every value is computed with
 // the same operations as the per-thread formulation, so results are unchanged.
-__global__ void __launch_bounds__(kRenderThreads) k_render(RenderJob r) {
+__global__ void __launch_bounds__(kRenderThreads, 6) k_render(RenderJob r) {
     __shared__ double vz_tab[kMaxRenderCells + 1];
     const int W = r.width, H = r.height, R = r.cells;
     for (int k = threadIdx.x; k <= R; k += blockDim.x)
