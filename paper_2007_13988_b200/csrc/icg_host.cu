@@ -73,6 +73,8 @@ struct icg_context {
         float bg[3];
         void* img_ptr[4];
         int unroll[ICG_MAX_LEVELS];
+        uint8_t pred[ICG_MAX_LEVELS][kPredIters];
+        uint8_t pred_valid[ICG_MAX_LEVELS];
         bool operator==(const FrameKey& o) const { return std::memcmp(this, &o, sizeof(FrameKey)) == 0; }
     };
     FrameKey graph_key{}, warm_key{};
@@ -137,6 +139,10 @@ struct icg_context {
     // device-side conflict-loop depth per level, adapted from the previous frame
     int unroll[ICG_MAX_LEVELS] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4};
     int unroll_seen[ICG_MAX_LEVELS] = {};  // deepest adapted depth so far (grow-only)
+    // conflict-loop size classes per level and host iteration (union over frames; invalid: all)
+    uint8_t pred[ICG_MAX_LEVELS][kPredIters] = {};
+    bool pred_valid[ICG_MAX_LEVELS] = {};
+    bool pred_all[ICG_MAX_LEVELS] = {};  // the last frame mispredicted this level: launch everything
 };
 
 namespace {
@@ -550,13 +556,23 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
         if (cfg->conflict_pass) {
             int max_iters = cfg->max_conflict_iters > 0 ? cfg->max_conflict_iters : fcells;
             const int unroll = c->unroll[l];
+            // size-class prediction: only the evaluators the previous frames needed at each
+            // iteration are enqueued; a batch that meets none raises `mispredict` (checked on
+            // device by the next expansion) and the frame is replayed with all of them
+            const bool chain_pred = fact_ok(c, fd) && c->use_tail && c->geo_pair;
+            const unsigned mid_max = 74u * 64u;
+            int prev_mask = -1;
             for (int it = 0; it < unroll; ++it) {
                 int p = it & 1;
+                const int pm =
+                    (chain_pred && c->pred_valid[l] && !c->pred_all[l] && it < kPredIters) ? c->pred[l][it] : 7;
                 {
                     int slot = prof_begin(c, 2);
-                    int r = launch_conflict_expand(c->queued.as<uint32_t>(), lb.fs, fcells, c->cf[p].as<uint32_t>(),
-                                                   ctr, it, max_iters, c->nx[p].as<uint32_t>(), (unsigned)nf,
-                                                   c->stream);
+                    ChainClasses cc{c->tail_max, mid_max, l, chain_pred ? prev_mask : -1};
+                    int r = launch_conflict_expand_cls(c->queued.as<uint32_t>(), lb.fs, fcells,
+                                                       c->cf[p].as<uint32_t>(), ctr, it, max_iters,
+                                                       c->nx[p].as<uint32_t>(), (unsigned)nf, cc, c->stream);
+                    prev_mask = pm;
                     prof_end(c, slot);
                     c->launches += 1;
                     if (r) return r;
@@ -574,12 +590,11 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                 cj.evals = &ctr->evals[l];
                 cj.iters = &ctr->conflict_iters[l];
                 cj.overflow = &ctr->overflow;
-                if (fact_ok(c, fd) && c->use_tail && c->geo_pair) {
+                if (chain_pred) {
                     // large batches: the CTA-pair kernel; the first small one starts the persistent tail,
                     // which finishes the level's chain (k_tail.cu)
                     // (mid-size batches: 64-point pair tiles, twice as many pairs busy per wave; the
                     // column-factored pass has a longer single-tile latency, so it is kept for bulk batches)
-                    const unsigned mid_max = 74u * 64u;
                     EvalJob big = cj, mid = cj;
                     big.min_count = std::max(c->tail_max, mid_max) + 1;
                     mid.min_count = c->tail_max + 1;
@@ -587,18 +602,30 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                     int slot = prof_begin(c, 5);
                     const bool x3 = fd.precision == ICG_PREC_FP32;
                     const void* tm = c->geo_pair_tmap[x3 ? 0 : 1];
-                    int r = launch_pifu_pair_eval(fd, c->geo_tc, tm, big, (unsigned)nf, x3, c->stream);
-                    if (!r && c->tail_max < mid_max)
+                    int r = ICG_OK;
+                    if (pm & 1) {
+                        r = launch_pifu_pair_eval(fd, c->geo_tc, tm, big, (unsigned)nf, x3, c->stream);
+                        c->launches += 1;
+                    }
+                    if (!r && (pm & 2) && c->tail_max < mid_max) {
                         r = launch_pifu_pair_eval_small(fd, c->geo_tc, tm, mid, mid_max, x3, c->stream);
-                    if (!r) r = issue_tail(c, fd, lb, l, fcells, it, max_iters, (unsigned)nf);
+                        c->launches += 1;
+                    }
+                    if (!r && (pm & 4)) {
+                        r = issue_tail(c, fd, lb, l, fcells, it, max_iters, (unsigned)nf);
+                        c->launches += 1;
+                    }
                     prof_end(c, slot);
-                    c->launches += 3;
                     if (r) return r;
                 } else if (int r = run_eval(c, fd, cj, (unsigned)nf, true)) {
                     return r;
                 }
             }
-            if (int r = launch_unroll_check(ctr, unroll & 1, l, c->stream)) return r;
+            {
+                ChainClasses cc{c->tail_max, mid_max, l, chain_pred ? prev_mask : -1};
+                if (int r = launch_unroll_check_cls(ctr, unroll & 1, l, cc, chain_pred ? unroll - 1 : -1, c->stream))
+                    return r;
+            }
             c->launches += 1;
         }
         b ^= 1;
@@ -766,6 +793,11 @@ float elapsed(icg_context* c) {
 bool adapt_unroll(icg_context* c, const icg_algo_config* cfg) {
     const DevCounters& h = *c->h_ctr;
     bool replay = false;
+    if (h.mispredict) {  // a conflict batch met no launched evaluator: all evaluators for that level
+        for (int l = 1; l <= cfg->target_level; ++l)
+            if (h.mispredict & (1u << l)) c->pred_all[l] = true;  // replay with every evaluator
+        return true;
+    }
     for (int l = 1; l <= cfg->target_level; ++l) {
         if (h.unroll_exhausted & (1u << l)) {
             c->unroll[l] *= 2;
@@ -783,6 +815,11 @@ bool adapt_unroll(icg_context* c, const icg_algo_config* cfg) {
                                        : (int)h.conflict_iters[l] + std::max(2, (int)h.conflict_iters[l] / 4);
             c->unroll[l] = std::max(c->unroll_seen[l], need);
             c->unroll_seen[l] = c->unroll[l];
+            // size classes: the first clean frame sets them, later ones only add (grow-only)
+            for (int it = 0; it < kPredIters; ++it)
+                c->pred[l][it] = c->pred_valid[l] ? (uint8_t)(c->pred[l][it] | h.cls[l][it]) : h.cls[l][it];
+            c->pred_valid[l] = true;
+            c->pred_all[l] = false;
         }
     return replay;
 }
@@ -1135,6 +1172,8 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
             key.img_ptr[3] = img->surface_k;
         }
         std::memcpy(key.unroll, c->unroll, sizeof(key.unroll));
+        std::memcpy(key.pred, c->pred, sizeof(key.pred));
+        for (int l = 0; l < ICG_MAX_LEVELS; ++l) key.pred_valid[l] = (uint8_t)(c->pred_valid[l] | (c->pred_all[l] << 1));
         const bool graphs = c->use_graph && !c->prof_on;
         bool ran = false;
         if (getenv("ICG_GRAPH_DEBUG") && c->warm_valid && !(c->warm_key == key)) {

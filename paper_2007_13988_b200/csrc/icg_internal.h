@@ -32,6 +32,7 @@ struct Status {
 // ---------------------------------------------------------------------------
 // Device-side counters of one extraction / render (one struct in HBM).
 // ---------------------------------------------------------------------------
+constexpr int kPredIters = 48;  // conflict-loop iterations with size-class prediction
 struct DevCounters {
     unsigned int list_count;          // E0 compaction result
     unsigned int cf_count[2];         // conflict lists (ping-pong by iteration)
@@ -45,6 +46,10 @@ struct DevCounters {
     unsigned int ncols;               // column-factored field: distinct columns of the current batch
     unsigned int e0[ICG_MAX_LEVELS];  // size of each level's E0 list (the bulk batch)
     unsigned int tail_start[ICG_MAX_LEVELS];  // 1 + host iteration at which k_tail took over (0: never)
+    // conflict-loop size classes (1: 128-point pair tiles, 2: 64-point pair tiles, 4: tail) seen per
+    // level and host iteration, and the levels where a batch met no launched evaluator
+    uint8_t cls[ICG_MAX_LEVELS][kPredIters];
+    unsigned int mispredict;
     // render counters (cleared per render: everything from `covered` to the end)
     unsigned long long covered, degenerate, grazing;
     unsigned int surface_count;
@@ -195,6 +200,17 @@ struct LevelBufs {
     int rc;                                 // coarse cells
 };
 int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s);
+// size classes of a conflict batch: which evaluator takes n nodes (0: empty)
+struct ChainClasses {
+    unsigned tail_max, mid_max;
+    int level;
+    int prev_mask;  // classes launched for the previous iteration (-1: no check)
+};
+int launch_conflict_expand_cls(uint32_t* fine_queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
+                               DevCounters* ctr, int iter, int max_iters, uint32_t* next_list, unsigned cap,
+                               const ChainClasses& cc, cudaStream_t s);
+int launch_unroll_check_cls(DevCounters* ctr, int iter_parity, int level, const ChainClasses& cc, int last_iter,
+                            cudaStream_t s);
 int launch_conflict_expand(uint32_t* fine_queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
                            DevCounters* ctr, int iter, int max_iters, uint32_t* next_list,
                            unsigned int cap, cudaStream_t s);

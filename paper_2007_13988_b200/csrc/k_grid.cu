@@ -330,12 +330,25 @@ int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaS
 // ---- conflict expansion (localize.hpp:338-353, 160-177) --------------------
 // Iteration `iter` reads conflicts cf[iter&1], writes neighbours to next_list /
 // nx[iter&1], and clears the buffers iteration iter+1 will fill.
+__device__ __forceinline__ int chain_class(unsigned n, const ChainClasses& cc) {
+    return n == 0 ? 0 : (n > cc.mid_max ? 1 : (n > cc.tail_max ? 2 : 4));
+}
+// the batch of host iteration `it` (count n) must have met one of the launched evaluators
+__device__ __forceinline__ void check_class(DevCounters* ctr, const ChainClasses& cc, int it, unsigned n) {
+    if (cc.prev_mask < 0) return;
+    const int c = chain_class(n, cc);
+    if (c == 0) return;  // empty, or evaluated by the tail (which clears the counts when done)
+    if (!(c & cc.prev_mask)) ctr->mispredict |= 1u << cc.level;
+    if (it >= 0 && it < kPredIters && c != 4) ctr->cls[cc.level][it] |= (uint8_t)c;
+}
+
 __global__ void k_conflict_expand(uint32_t* __restrict__ queued, const uint8_t* __restrict__ fs, int fcells,
                                   const uint32_t* __restrict__ conflicts, DevCounters* ctr, int iter, int max_iters,
-                                  uint32_t* __restrict__ next_list, unsigned cap) {
+                                  uint32_t* __restrict__ next_list, unsigned cap, ChainClasses cc) {
     const int p = iter & 1;
     unsigned ncf = ctr->cf_count[p];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (iter > 0) check_class(ctr, cc, iter - 1, ctr->nx_count[p ^ 1]);
         ctr->cf_count[p ^ 1] = 0;
         ctr->nx_count[p ^ 1] = 0;
         if (ncf > 0 && iter >= max_iters) ctr->warning = 1;  // localize.hpp:343-346
@@ -369,7 +382,16 @@ __global__ void k_conflict_expand(uint32_t* __restrict__ queued, const uint8_t* 
 int launch_conflict_expand(uint32_t* queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
                            DevCounters* ctr, int iter, int max_iters, uint32_t* next_list, unsigned cap,
                            cudaStream_t s) {
-    k_conflict_expand<<<148, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap);
+    ChainClasses cc{0, 0, 0, -1};
+    k_conflict_expand<<<148, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap, cc);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
+int launch_conflict_expand_cls(uint32_t* queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
+                               DevCounters* ctr, int iter, int max_iters, uint32_t* next_list, unsigned cap,
+                               const ChainClasses& cc, cudaStream_t s) {
+    k_conflict_expand<<<148, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap, cc);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }
@@ -481,12 +503,21 @@ int launch_dense_column_list(int cells, uint32_t* list, cudaStream_t s) {
     return ICG_OK;
 }
 
-__global__ void k_unroll_check(DevCounters* ctr, int parity, int level) {
+__global__ void k_unroll_check(DevCounters* ctr, int parity, int level, ChainClasses cc, int last_iter) {
     if (ctr->cf_count[parity] > 0) ctr->unroll_exhausted |= 1u << level;
+    if (last_iter >= 0) check_class(ctr, cc, last_iter, ctr->nx_count[last_iter & 1]);
+}
+
+int launch_unroll_check_cls(DevCounters* ctr, int parity, int level, const ChainClasses& cc, int last_iter,
+                            cudaStream_t s) {
+    k_unroll_check<<<1, 1, 0, s>>>(ctr, parity, level, cc, last_iter);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
 }
 
 int launch_unroll_check(DevCounters* ctr, int parity, int level, cudaStream_t s) {
-    k_unroll_check<<<1, 1, 0, s>>>(ctr, parity, level);
+    ChainClasses cc{0, 0, level, -1};
+    k_unroll_check<<<1, 1, 0, s>>>(ctr, parity, level, cc, -1);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }

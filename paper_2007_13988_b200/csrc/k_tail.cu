@@ -86,7 +86,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
         if (n0 == 0 || n0 > P.max_start) return;
     }
     cg::grid_group grid = cg::this_grid();
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->tail_start[P.level] = (unsigned)P.it0 + 1u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr->tail_start[P.level] = (unsigned)P.it0 + 1u;
+        if (P.it0 < kPredIters) ctr->cls[P.level][P.it0] |= 4u;
+    }
     int ntr = 0;  // trace (block 0): (tag, globaltimer) pairs
     auto tr = [&](unsigned tag) {
         if (P.trace && blockIdx.x == 0 && threadIdx.x == 0 && ntr < 1000) {
