@@ -438,3 +438,35 @@ def test_config3_full_size_properties(gpu_ctx):
     i, j, k = sub % n, (sub // n) % n, sub // (n * n)
     pts = np.stack([-1 + 2 * i / 512.0, -1 + 2 * j / 512.0, 1 - 2 * k / 512.0], 1)
     assert np.abs(ext.values[sub] - m.occupancy(pts)).max() <= OCC_TOL_BF16
+
+
+@pytest.mark.gpu
+def test_chain_prediction_alternating_inputs(pifu_inputs):
+    """One context alternates between feature maps whose conflict chains differ (size classes
+    per iteration, tail hand-over): every frame equals the same frame on a fresh context, i.e.
+    mispredicted evaluator sets are caught on device and replayed."""
+    inp = pifu_inputs
+    cfg = api.AlgoConfig("progressive", 32, 3)
+    cam = api.CameraSpec.from_angles(90, 0)
+    fmaps = [api.gen_feature_map(2000 + s) for s in range(3)]
+
+    def ctx_new():
+        c = api.Context(0)
+        c.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+        c.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+        return c
+
+    ref = []
+    for fm in fmaps:
+        c = ctx_new()
+        e, i = c.frame(api.PifuField(fm, inp["caps"], 50.0, abi.ICG_PREC_FP32), cfg, cam, 128, 128, want_grid=True)
+        ref.append((e.evals_per_level, e.values.copy(), i.surface_k.copy()))
+        c.close()
+    c = ctx_new()
+    for rep in range(3):
+        for s, fm in enumerate(fmaps):
+            e, i = c.frame(api.PifuField(fm, inp["caps"], 50.0, abi.ICG_PREC_FP32), cfg, cam, 128, 128,
+                           want_grid=True)
+            assert e.evals_per_level == ref[s][0]
+            assert np.array_equal(e.values, ref[s][1]) and np.array_equal(i.surface_k, ref[s][2])
+    c.close()
