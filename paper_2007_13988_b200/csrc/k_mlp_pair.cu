@@ -94,7 +94,10 @@ struct Cfg {
     // registers) uses 16 = 4 quarters x 4 point quarters to hide the per-block latency chain
     static constexpr int kEpiWarps = 8;
     static constexpr int kEpiThreads = 32 * kEpiWarps;
-    static constexpr int kThreads = 64 + kEpiThreads;
+    // FACT: two auxiliary warps gather the next tiles (positions, column records, sdf bias) so the
+    // epilogue warps only convert and emit h blocks (their work bounds the FACT tile time)
+    static constexpr int kAuxWarps = MODE == kModeFact ? 2 : 0;
+    static constexpr int kThreads = 64 + kEpiThreads + 32 * kAuxWarps;
     static constexpr int kHF = (NPC / 32) / (kEpiWarps / 8);  // 32-point chunks per epilogue thread
     // one CTA per SM: the register file split over the CTA's warps, allocated in groups of 4
     // warps, per thread a multiple of 8
@@ -165,6 +168,7 @@ struct Misc {
     uint64_t full[kMaxStages], empty[kMaxStages];
     uint64_t f_ready, h_ready[2][2], h_free[2][2], l1done[2], d2done, d3done, d4done, sd_ready[2], skip_free, d4_free;
     uint64_t accb[4], acc_free[4];  // COLS: accumulator ring
+    uint64_t g_ready[2], fin_done[2];  // FACT: tile gathered (aux -> epilogue), final layer done (-> aux)
     uint32_t tmem_base;
     int slot[2][kMaxNP];  // FACT: column record of each point of the tile (by tile parity)
     // FACT: per 32-point chunk of a (column-sorted) tile: first / last record, mask of the points
@@ -339,6 +343,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             ptx::mbar_init(&ms.accb[a], 1);
             ptx::mbar_init(&ms.acc_free[a], 2 * kEpiThreads);
         }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&ms.g_ready[b], C::kAuxWarps > 0 ? C::kAuxWarps : 1);
+            ptx::mbar_init(&ms.fin_done[b], kEpiWarps);
+        }
         ptx::mbar_init(&ms.l1done[0], 1);
         ptx::mbar_init(&ms.l1done[1], 1);
         ptx::mbar_init(&ms.d2done, 1);
@@ -354,15 +362,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
         ptx::prefetch_tmap(&tmapA);
         if (TEX) ptx::prefetch_tmap(&tmapB);
     }
-    if (warp == 1) ptx::tmem_alloc2<512>(&ms.tmem_base);
-    ptx::tc_fence_before();
-    ptx::cluster_sync();
-    ptx::tc_fence_after();
-    const uint32_t tmem = ms.tmem_base;
-    job_account(job);
+    // (loaded before the start-up cluster barrier, which publishes it to every warp)
     if constexpr (MODE == kModeFact) {
         // the capsule figure of the -sdf_scale * sdf bias in shared memory (read by every tile)
-        if (threadIdx.x >= 64) {
+        if (threadIdx.x >= 64 && threadIdx.x < 64 + kEpiThreads) {
             const int i = threadIdx.x - 64;
             const int np = __ldg(&P.f.fscene->n_prims);
             if (i < np) {
@@ -384,9 +387,15 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     all = __ldg(&P.f.fscene->prims[k].kind) == ICG_PRIM_CAPSULE && !__ldg(&P.f.fscene->prims[k].rotated);
                 ms.ncaps = all ? np : -1;
             }
-            epi_bar_n<C::kEpiThreads>();
         }
     }
+    if (warp == 1) ptx::tmem_alloc2<512>(&ms.tmem_base);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = ms.tmem_base;
+    job_account(job);
+
 
     // leader-CTA addresses of the barriers that receive cross-CTA traffic
     const uint32_t full0 = ptx::mapa(ptx::smem_u32(&ms.full[0]), 0);
@@ -404,6 +413,30 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             uint32_t ph = 0;
             const int per_stage = P.x3 ? 1 : 2;  // items per 32 KB box
             const uint32_t ring0 = ptx::smem_u32(ring);
+            if constexpr (FACT) {
+                // the MMA's consumption order, software-pipelined across tiles (see the issuer):
+                // A(0) B(0) C(0) | A(1) D(0) B(1) C(1) | ... | D(last), where A/B = layer-2 items of
+                // h1 chunks 0-1 / 2-3, C = layer 3, D = layer 4 (item ranges of the FACT stream)
+                auto load_range = [&](int i0, int i1) {
+                    for (int i = i0; i < i1; i += per_stage) {
+                        ptx::mbar_wait(&ms.empty[s], ph ^ 1);
+                        if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kStage);
+                        const int row0 = ((int)rank * P.total_a + i) * (P.x3 ? 256 : 128);
+                        ptx::tma_load_2d_2sm(ring0 + s * kStage, &tmapA, full0 + s * 8, 0, row0);
+                        if (++s == kStages) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+                };
+                for (unsigned t = pair_id; t < ntiles; t += npairs) {
+                    load_range(0, 16);                   // A(t)
+                    if (t != pair_id) load_range(40, 44);  // D(t-1)
+                    load_range(16, 32);                  // B(t)
+                    load_range(32, 40);                  // C(t)
+                }
+                load_range(40, 44);  // D(last)
+            } else
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
                 for (int seg = 0; seg < (TEX ? 2 : 1); ++seg) {
                     const CUtensorMap* tm = seg ? &tmapB : &tmapA;
@@ -559,7 +592,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 }
             };
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
-                {
+                if constexpr (!FACT) {  // FACT: operands arrive through the h buffers only
                     const unsigned long long t0 = tr ? gtime() : 0;
                     ptx::mbar_wait_cluster(&ms.f_ready, fph);
                     if (tr) w_f += gtime() - t0;
@@ -582,16 +615,27 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     }
                     ptx::mma_commit_pair(&ms.skip_free, both);
                 } else if constexpr (FACT) {
-                    // TMEM: D2[m] = m*NP, D3 = 2NP, D4 = 3NP; h blocks alternate between two buffers
-                    for (int c = 0; c < 4; ++c) h_block(2, 0, (int)(hblk++ & 1u), c == 0);
+                    // TMEM: D2[m] = m*NP, D3 = 2NP, D4 = 3NP; h blocks alternate between two buffers.
+                    // Software-pipelined across tiles: the previous tile's layer 4 runs after this
+                    // tile's first two layer-2 chunks, so the tensor cores have work while the
+                    // epilogue emits the previous tile's layer-3 output (h3).
+                    for (int c = 0; c < 2; ++c) h_block(2, 0, (int)(hblk++ & 1u), c == 0);  // A(t)
+                    if (later) {                                                               // D(t-1)
+                        h_block(1, 3 * NP, (int)(hblk++ & 1u), true);
+                        ptx::mma_commit_pair(&ms.d4done, both);
+                        ev(304);
+                    }
+                    for (int c = 2; c < 4; ++c) h_block(2, 0, (int)(hblk++ & 1u), false);  // B(t)
                     ptx::mma_commit_pair(&ms.d2done, both);
                     ev(302);
-                    for (int c = 0; c < 2; ++c) h_block(1, 2 * NP, (int)(hblk++ & 1u), c == 0);
+                    for (int c = 0; c < 2; ++c) h_block(1, 2 * NP, (int)(hblk++ & 1u), c == 0);  // C(t)
                     ptx::mma_commit_pair(&ms.d3done, both);
                     ev(303);
-                    h_block(1, 3 * NP, (int)(hblk++ & 1u), true);
-                    ptx::mma_commit_pair(&ms.d4done, both);
-                    ev(304);
+                    if (t + npairs >= ntiles) {  // D(last)
+                        h_block(1, 3 * NP, (int)(hblk++ & 1u), true);
+                        ptx::mma_commit_pair(&ms.d4done, both);
+                        ev(304);
+                    }
                 } else {
                     body(4, true, later);
                 }
@@ -602,6 +646,77 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 P.trace[2] = w_h;
                 P.trace[3] = w_f;
             }
+        }
+    } else if (C::kAuxWarps > 0 && warp >= 2 + kEpiWarps) {
+        // ===================== FACT auxiliary warps: gather tiles ahead =====================
+        const int at = (int)threadIdx.x - (64 + kEpiThreads);
+        constexpr int kAT = 32 * C::kAuxWarps;
+        const int aw = at >> 5;
+        auto aux_bar = [] { asm volatile("bar.sync 2, %0;" ::"n"(32 * C::kAuxWarps) : "memory"); };
+        const float* b5 = P.bias_g + 2 * (1024 + 512 + 256 + 128);
+        constexpr int wls = 128 + kGeoSkip;
+        uint32_t fph_bits = 0;
+        unsigned tl = 0;
+        for (unsigned t = pair_id; t < ntiles; t += npairs, ++tl) {
+            const int gb = (int)(tl & 1u);
+            if (tl >= 2) {  // the epilogue's final layer of tile tl-2 is done with these buffers
+                ptx::mbar_wait(&ms.fin_done[gb], (fph_bits >> gb) & 1u);
+                fph_bits ^= 1u << gb;
+            }
+            // positions, column records
+            for (int p = at; p < NP; p += kAT) {
+                const unsigned idx = t * NP + (unsigned)p;
+                double pd[3] = {0.0, 0.0, 0.0};
+                int sl = 0;
+                if (idx < n) {
+                    job_point_d(job, idx, pd);
+                    const uint32_t n1 = (uint32_t)job.cells + 1u, col = job_node(job, idx) % (n1 * n1);
+                    sl = P.cmap ? __ldg(&P.cmap[col]) : (int)col;
+                }
+                ms.slot[gb][p] = sl;
+                for (int d = 0; d < 3; ++d) ms.pos[gb][p][d] = (float)pd[d];
+                ms.z[gb][p] = (float)pd[2];
+            }
+            aux_bar();
+            // per 32-point chunk: first / last record and which points use the last one
+            for (int c = aw; c < NP / 32; c += C::kAuxWarps) {
+                const int sv = ms.slot[gb][32 * c + lane];
+                const int first = __shfl_sync(0xffffffffu, sv, 0), last = __shfl_sync(0xffffffffu, sv, 31);
+                const uint32_t m = __ballot_sync(0xffffffffu, sv == last);
+                const uint32_t ok = __all_sync(0xffffffffu, sv == first || sv == last);
+                if (lane == 0) {
+                    ms.cfirst[gb][c] = first;
+                    ms.clast[gb][c] = last;
+                    ms.cmask[gb][c] = m;
+                    ms.cok[gb][c] = ok;
+                }
+            }
+            if (leader) {  // the final layer's Phi dot and constant term (-sdf_scale sdf + b5 + w5z z)
+                for (int p = at; p < NP; p += kAT) {
+                    ms.skipdot[gb][0][p] = __ldg(&P.s_in[(size_t)ms.slot[gb][p] * kSRow + kSFinal]);
+                    const float* P3 = ms.pos[gb][p];
+                    float d = 3.0e38f;
+                    const int nc = ms.ncaps;
+                    if (nc >= 0) {
+                        for (int i = 0; i < nc; ++i) {
+                            const float* c = ms.caps[i];
+                            const float pa0 = P3[0] - c[0], pa1 = P3[1] - c[1], pa2 = P3[2] - c[2];
+                            float hh = 0.0f;
+                            if (c[6] > 0.0f) hh = fminf(fmaxf((pa0 * c[3] + pa1 * c[4] + pa2 * c[5]) / c[6], 0.0f), 1.0f);
+                            const float v0 = pa0 - hh * c[3], v1 = pa1 - hh * c[4], v2 = pa2 - hh * c[5];
+                            d = fminf(d, sqrtf(v0 * v0 + v1 * v1 + v2 * v2) - c[7]);
+                        }
+                        if (nc == 0) d = 0.0f;
+                    } else {
+                        d = scene_sdf_f(P.f.fscene, P3);
+                    }
+                    ms.cterm[gb][p] = __ldg(&b5[0]) + __ldg(&P.wlast[wls - 1]) * ms.z[gb][p] -
+                                      __ldg(&P.f.fscene->sdf_scale) * d;
+                }
+            }
+            aux_bar();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&ms.g_ready[gb]);
         }
     } else {
         // ===================== gather + epilogue (8 warps, both CTAs) =====================
@@ -1144,8 +1259,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                                       __ldg(&f.fscene->sdf_scale) * d;
             };
             // Per tile t the epilogue emits layer-1 chunks 2-3 of t; then, while the tensor cores
-            // finish layer 2 of t, the final layer of t-1 and the gather of t+1; then layers 2-3 of t
-            // and layer-1 chunks 0-1 of t+1 (so layer 2 of t+1 follows layer 4 of t at once).
+            // finish layer 2 of t, the final layer of t-1 and the gather of t+1; then h2 of t, the
+            // layer-1 chunks 0-1 of t+1 and h3 of t -- the order the issuer consumes them in
+            // (A(t+1) before D(t), so the tensor cores work while h3 is converted).
             // One emit site: the epilogue is large and inlining it per step costs registers.
             const float* b_of[3] = {b1, b2, b3};
             (void)b_of;
@@ -1169,8 +1285,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 slc = ms.slot[gb];
                 ms_tile_parity = gb;
             };
-            gather_tile(pair_id, 0);
-            fact_cterm(0);
+            // tiles are gathered ahead by the auxiliary warps (g_ready per parity buffer)
+            uint32_t gph_bits = 0;
+            auto wait_g = [&](int gb) {
+                ptx::mbar_wait(&ms.g_ready[gb], (gph_bits >> gb) & 1u);
+                gph_bits ^= 1u << gb;
+            };
+            (void)fact_cterm;
+            wait_g(0);
             set_tile(0);
             run_steps(0, 2, 0);
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
@@ -1184,17 +1306,18 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     eev(600);
                     final_layer(t - npairs, tp ^ 1);
                     eev(601);
-                }
-                if (has_next) {
-                    gather_tile(t + npairs, tp ^ 1);
-                    fact_cterm(tp ^ 1);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&ms.fin_done[tp ^ 1]);  // its buffers may be refilled
                 }
                 set_tile(tp);
-                run_steps(4, 7, tp);
-                if (has_next) {
+                run_steps(4, 6, tp);  // h2 of t
+                if (has_next) {       // the next tile's first layer-1 chunks, before h3 of t: the MMA
+                    wait_g(tp ^ 1);    // runs layer 2 of t+1 while h3 is converted (issuer order)
                     set_tile(tp ^ 1);
                     run_steps(0, 2, tp ^ 1);
                 }
+                set_tile(tp);
+                run_steps(6, 7, tp);  // h3 of t
                 ++tile_iter;
             }
             {  // the last tile's final layer
