@@ -74,18 +74,21 @@ struct Cfg {
     static constexpr int kSkipChunks = TEX ? 8 : (MODE == kModeFact ? 0 : 4);
     static constexpr int kHBufs = MODE == kModeFact ? 2 : (MODE == kModeCols ? 0 : 1);  // h operand buffers
     // 32 KB stages (per-copy TMA cost is size-independent)
-    static constexpr int kStages = (MODE == kModeCols || MODE == kModeGeo64) ? 4 : 2;
+    static constexpr int kStages = (MODE == kModeCols || MODE == kModeGeo64) ? 4 : (MODE == kModeTex ? 3 : 2);
     // TEX: the skip operand [Phi, h3] is ONE fp16 copy (its weights fp16 hi + lo): 10 more mantissa
     // bits than a bf16 copy keep colours within 1e-3 (max 1.9e-4 simulated) and free the shared
     // memory of a lo copy, so the texture tile is 128 points like the geometry one
     static constexpr bool kF16Skip = TEX;
     static constexpr int kSkipCopies = kF16Skip ? 1 : 2;
+    // TEX: the hidden activations too are one fp16 copy (all weights fp16 hi / lo): 2 MMAs per
+    // K step instead of 3, half the h-operand bytes; colours within 2.5e-4 of the oracle (simulated)
+    static constexpr bool kF16H = TEX;
     static constexpr uint32_t kChunk = NPC * 128;  // NPC point rows x 64 bf16 (SW128)
     static constexpr uint32_t kSkipHalf = kSkipChunks * kChunk;
     static constexpr uint32_t kHHalf = 4 * kChunk;  // one 256-feature block
     static constexpr uint32_t kOffSkip = 0;
     static constexpr uint32_t kOffH = kOffSkip + kSkipCopies * kSkipHalf;
-    static constexpr uint32_t kOffRing = kOffH + kHBufs * 2 * kHHalf;
+    static constexpr uint32_t kOffRing = kOffH + kHBufs * (kF16H ? 1 : 2) * kHHalf;
     static constexpr uint32_t kOffMisc = kOffRing + kStages * kStage;
     static constexpr uint32_t kMisc = 24576;
     static constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
@@ -547,7 +550,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     wait_h(buf, half);
                     for (int jj = 2 * half; jj < 2 * half + 2; ++jj)
                         for (int m = 0; m < nm; ++m)
-                            item(dcol0 + m * NP, bh + jj * kChunk, bl + jj * kChunk, !(first && jj == 0), FACT);
+                            item(dcol0 + m * NP, bh + jj * kChunk, bl + jj * kChunk, !(first && jj == 0), FACT,
+                                 C::kF16H);
                     ptx::mma_commit_pair(&ms.h_free[buf][half], both);
                 }
             };
@@ -920,13 +924,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 wait_acc(&ms.l1done[c & 1], l1ph[c & 1]);
                 if (c == 0) after_l1c0();
                 h_begin();
-                emit_block(2 * NP + (c & 1) * NP, b1, 1024, c * 256, hdst, kHHalf, P.x3);
+                emit_block(2 * NP + (c & 1) * NP, b1, 1024, c * 256, hdst, kHHalf, P.x3 && !C::kF16H, -1, true, nullptr,
+                           C::kF16H);
                 h_end();
             }
             wait_acc(&ms.d2done, d2ph);
             for (int m = 0; m < 2; ++m) {
                 h_begin();
-                emit_block(m * NP, b2, 512, m * 256, hdst, kHHalf, P.x3);
+                emit_block(m * NP, b2, 512, m * 256, hdst, kHHalf, P.x3 && !C::kF16H, -1, true, nullptr, C::kF16H);
                 h_end();
             }
             wait_acc(&ms.d3done, d3ph);
@@ -934,7 +939,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             if (prefix)  // h3 -> skip K-chunks 4..7 (TEX: the single fp16 skip copy)
                 emit_block(2 * NP, b3, 256, 0, sdst, kSkipHalf, !C::kF16Skip, -1, true, nullptr, C::kF16Skip);
             else
-                emit_block(2 * NP, b3, 256, 0, hdst, kHHalf, P.x3);
+                emit_block(2 * NP, b3, 256, 0, hdst, kHHalf, P.x3 && !C::kF16H, -1, true, nullptr, C::kF16H);
             h_end();
         };
 
@@ -1451,7 +1456,7 @@ size_t pair_stream_bytes(int which, bool x3) {
 // f16skip: items over the skip input (K columns >= the hidden width) as fp16 hi / lo (the TEX
 // kernel's single fp16 skip operand); everything else bf16 hi / lo
 static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi,
-                           bool f16skip = false) {
+                           bool f16skip = false, bool f16all = false) {
     const bool geo = which == ICG_MLP_GEOMETRY;
     const int* outs = geo ? kGeoOut : kTexOut;
     const int skip = geo ? kGeoSkip : kTexSkip;
@@ -1461,7 +1466,7 @@ static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t*
     for (int l = 0; l < 5; ++l) ins[l] = (l ? outs[l - 1] : 0) + skip;
     int item = 0;
     auto emit = [&](int l, int m, int col0) {
-        const bool f16 = f16skip && col0 >= (l ? outs[l - 1] : 0);
+        const bool f16 = f16all || (f16skip && col0 >= (l ? outs[l - 1] : 0));
         for (int h = 0; h < 2; ++h) {
             uint8_t* hi = stream_x3 + ((size_t)(h * nitems + item) * 2 + 0) * pair::kHalf;
             uint8_t* lo = stream_x3 + ((size_t)(h * nitems + item) * 2 + 1) * pair::kHalf;
@@ -1499,7 +1504,8 @@ static int pair_pack_sched(int which, int sched, const float* const* w, uint8_t*
 }
 
 int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi, bool f16skip) {
-    return pair_pack_sched(which, 0, w, stream_x3, stream_hi, f16skip);
+    // f16skip: the texture kernel's streams -- every item fp16 hi / lo (its operands are fp16)
+    return pair_pack_sched(which, 0, w, stream_x3, stream_hi, f16skip, f16skip);
 }
 
 size_t pair_fact_stream_bytes(int part, bool x3) {
