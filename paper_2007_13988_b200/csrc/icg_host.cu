@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <atomic>
 #include <cstring>
 #include <random>
 #include <string>
@@ -75,12 +76,17 @@ struct icg_context {
         int unroll[ICG_MAX_LEVELS];
         uint8_t pred[ICG_MAX_LEVELS][kPredIters];
         uint8_t pred_valid[ICG_MAX_LEVELS];
+        uint8_t tail_wide;
         bool operator==(const FrameKey& o) const { return std::memcmp(this, &o, sizeof(FrameKey)) == 0; }
     };
-    FrameKey graph_key{}, warm_key{};
-    bool graph_valid = false, warm_valid = false, use_graph = true;
-    cudaGraphExec_t graph_exec = nullptr;
-    uint64_t graph_launches = 0;
+    // one slot per tail width, so a context alternating between alone / shared frames keeps both graphs
+    struct GraphSlot {
+        FrameKey graph_key{}, warm_key{};
+        bool graph_valid = false, warm_valid = false;
+        cudaGraphExec_t graph_exec = nullptr;
+        uint64_t graph_launches = 0;
+    } gslot[2];
+    bool use_graph = true;
     // weights
     bool has_geo = false, has_tex = false;
     DBuf geo_wt[5], geo_b[5], tex_wt[5], tex_b[5], geo_wrow[5];
@@ -102,6 +108,7 @@ struct icg_context {
     bool fact_used = false;  // the last extraction ran its bulk batches column-factored
     DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
     bool use_tail = true;
+    bool tail_wide = true;  // this frame is alone on its device: the tail kernel takes every SM
     unsigned tail_max = 128;  // conflict batches up to this size start the persistent tail kernel
     bool use_pair = true;
     // field
@@ -152,6 +159,16 @@ size_t nodes3(int cells) {
     return n * n * n;
 }
 size_t words(size_t bits) { return (bits + 31) / 32; }
+
+// frames in flight per device (contexts driven from concurrent host threads): a frame alone on
+// its device lets latency-bound kernels (the conflict-loop tail) take every SM
+std::atomic<int> g_inflight[64];
+struct InflightGuard {
+    int dev;
+    bool alone;
+    explicit InflightGuard(int d) : dev(d & 63) { alone = g_inflight[dev].fetch_add(1) == 0; }
+    ~InflightGuard() { g_inflight[dev].fetch_sub(1); }
+};
 bool job_is_grid_host(const EvalJob& j) { return j.points == nullptr && j.values != nullptr; }
 
 // ---- instrumentation ----------------------------------------------------------
@@ -476,7 +493,7 @@ int issue_tail(icg_context* c, const FieldDev& fd, const LevelBufs& lb, int leve
     tp.bias = c->geo_tc.bias;
     tp.wlast = c->geo_tc.w_last;
     tp.slope = 0.02f;
-    return launch_tail(tp, c->tail_scratch.as<uint8_t>(), cap_pts, cap_new, (unsigned)plane, c->stream);
+    return launch_tail(tp, c->tail_scratch.as<uint8_t>(), cap_pts, cap_new, (unsigned)plane, c->stream, c->tail_wide);
 }
 
 // Issues one whole extraction on the context stream (no host sync).
@@ -929,7 +946,8 @@ int icg_destroy(icg_context* c) {
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->e0) cudaEventDestroy(c->e0);
     if (c->e1) cudaEventDestroy(c->e1);
-    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    for (auto& gs : c->gslot)
+        if (gs.graph_exec) cudaGraphExecDestroy(gs.graph_exec);
     if (c->span_start) cudaEventDestroy(c->span_start);
     if (c->span_end) cudaEventDestroy(c->span_end);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -1098,6 +1116,8 @@ int icg_extract(icg_context* c, const icg_field* field, const icg_algo_config* c
     FieldDev fd;
     if (int r = prepare_field(c, field, fd)) return r;
     if (int r = ensure_grid(c, cfg->coarsest_cells << cfg->target_level)) return r;
+    InflightGuard inflight(c->device);
+    c->tail_wide = inflight.alone;
     ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
     if (int r = do_extract(c, fd, cfg)) return r;
     ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
@@ -1144,6 +1164,8 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
     if (int r = prepare_field(c, field, fd)) return r;
     if (fd.kind == ICG_FIELD_PIFU && !c->has_tex) return einval("frame: scene has no texture (icg_set_mlp TEXTURE)");
     if (int r = ensure_grid(c, cfg->coarsest_cells << cfg->target_level)) return r;
+    InflightGuard inflight(c->device);
+    c->tail_wide = inflight.alone;
     // the frame's device work: extraction, render + texture, output copies, counters back to the host
     auto body = [&]() -> int {
         if (int r = issue_extract(c, fd, cfg)) return r;
@@ -1172,23 +1194,25 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
             key.img_ptr[3] = img->surface_k;
         }
         std::memcpy(key.unroll, c->unroll, sizeof(key.unroll));
+        key.tail_wide = c->tail_wide ? 1 : 0;
+        icg_context::GraphSlot& gs = c->gslot[key.tail_wide];
         std::memcpy(key.pred, c->pred, sizeof(key.pred));
         for (int l = 0; l < ICG_MAX_LEVELS; ++l) key.pred_valid[l] = (uint8_t)(c->pred_valid[l] | (c->pred_all[l] << 1));
         const bool graphs = c->use_graph && !c->prof_on;
         bool ran = false;
-        if (getenv("ICG_GRAPH_DEBUG") && c->warm_valid && !(c->warm_key == key)) {
-            const icg_context::FrameKey& w = c->warm_key;
+        if (getenv("ICG_GRAPH_DEBUG") && gs.warm_valid && !(gs.warm_key == key)) {
+            const icg_context::FrameKey& w = gs.warm_key;
             fprintf(stderr, "[icg] frame key differs: cfg %d cam %d WH %d kind %d img %d bg %d unroll %d\n",
                     std::memcmp(&w.cfg, &key.cfg, sizeof(key.cfg)) != 0, std::memcmp(&w.cam, &key.cam, sizeof(key.cam)) != 0,
                     w.W != key.W || w.H != key.H, w.kind != key.kind || w.precision != key.precision,
                     std::memcmp(w.img_ptr, key.img_ptr, sizeof(key.img_ptr)) != 0 || w.img_mem != key.img_mem,
                     std::memcmp(w.bg, key.bg, sizeof(key.bg)) != 0, std::memcmp(w.unroll, key.unroll, sizeof(key.unroll)) != 0);
         }
-        if (graphs && c->graph_valid && c->graph_key == key) {
-            ICG_CUDA_TRY(cudaGraphLaunch(c->graph_exec, c->stream));
-            c->launches += c->graph_launches;
+        if (graphs && gs.graph_valid && gs.graph_key == key) {
+            ICG_CUDA_TRY(cudaGraphLaunch(gs.graph_exec, c->stream));
+            c->launches += gs.graph_launches;
             ran = true;
-        } else if (graphs && c->warm_valid && c->warm_key == key) {
+        } else if (graphs && gs.warm_valid && gs.warm_key == key) {
             const uint64_t l0 = c->launches;
             cudaGraph_t g = nullptr;
             int r = ICG_OK;
@@ -1201,18 +1225,18 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
             }
             cudaGetLastError();
             if (r == ICG_OK && g) {
-                if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
-                c->graph_exec = nullptr;
-                if (cudaGraphInstantiate(&c->graph_exec, g, 0) == cudaSuccess) {
-                    c->graph_key = key;
-                    c->graph_valid = true;
-                    c->graph_launches = c->launches - l0;
+                if (gs.graph_exec) cudaGraphExecDestroy(gs.graph_exec);
+                gs.graph_exec = nullptr;
+                if (cudaGraphInstantiate(&gs.graph_exec, g, 0) == cudaSuccess) {
+                    gs.graph_key = key;
+                    gs.graph_valid = true;
+                    gs.graph_launches = c->launches - l0;
                     if (getenv("ICG_GRAPH_DEBUG")) fprintf(stderr, "[icg] frame graph captured: %llu launches\n",
-                                                           (unsigned long long)c->graph_launches);
-                    ICG_CUDA_TRY(cudaGraphLaunch(c->graph_exec, c->stream));
+                                                           (unsigned long long)gs.graph_launches);
+                    ICG_CUDA_TRY(cudaGraphLaunch(gs.graph_exec, c->stream));
                     ran = true;
                 } else {
-                    c->graph_exec = nullptr;
+                    gs.graph_exec = nullptr;
                 }
             }
             if (g) cudaGraphDestroy(g);
@@ -1221,14 +1245,14 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
                     fprintf(stderr, "[icg] frame graph capture failed (%d: %s); staying eager\n", r, g_err.c_str());
                 cudaGetLastError();
                 c->use_graph = false;
-                c->graph_valid = false;
+                gs.graph_valid = false;
                 c->launches = l0;
             }
         }
         if (!ran) {
             if (int r = body()) return r;
-            c->warm_key = key;
-            c->warm_valid = true;
+            gs.warm_key = key;
+            gs.warm_valid = true;
         }
         ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
         ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));

@@ -243,7 +243,8 @@ struct TailParams {
 };
 size_t tail_smem_bytes();
 size_t tail_scratch_bytes(unsigned cap_pts, unsigned cap_new, unsigned max_cols);
-int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_new, unsigned max_cols, cudaStream_t s);
+int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_new, unsigned max_cols, cudaStream_t s,
+                bool wide);
 
 // column-factored field: give every distinct column (i + n j) of a node list a record slot
 // (cmap[col] = slot, collist[slot] = col, ctr->ncols = number of slots); cmap must be all -1

@@ -44,32 +44,31 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kRec = 1936;  // column record floats (k_mlp_pair.cu kSRow)
 // Grid size: every activation is read by every CTA (rows are partitioned), so more CTAs mean
 // less work but more broadcast per CTA.  The kernel is cooperative and holds its SMs for the whole
-// chain while doing little, so with several frames in flight a smaller grid leaves SMs to the
-// other frames: 64 CTAs measured 222 frames/s (3 in flight) vs 191 with 148, at +3 % single-frame
-// latency (5.73 vs 5.57 ms).
-#ifndef ICG_TAIL_CTAS
-#define ICG_TAIL_CTAS 64
-#endif
-constexpr int kG = ICG_TAIL_CTAS;
-constexpr int kMaxOwn2 = (512 + kG - 1) / kG, kMaxOwn3 = (256 + kG - 1) / kG, kMaxOwn4 = (128 + kG - 1) / kG;
+// chain while doing little: with other frames in flight on the device a 64-CTA grid leaves SMs to
+// them (222 vs 191 frames/s with 3 in flight), while a frame alone on the device takes the
+// 148-CTA grid (lower latency).  Both are instantiated; launch_tail picks.
 constexpr int kSRows = 1921;  // Phi rows of a record: 1024 + 512 + 256 + 128 + final dot
-constexpr int kMaxOwnS = (kSRows + kG - 1) / kG;
 constexpr int kPB = 16;       // points per staged activation block
-// double-buffer the staged activations when the resident weights leave room for it
-constexpr size_t kWeightBytes = 4 * ((size_t)kMaxOwn2 * 1024 + (size_t)kMaxOwn3 * 512 + (size_t)kMaxOwn4 * 256 +
-                                     (size_t)kMaxOwnS * 256 + 128);
-constexpr int kStageBufs = kWeightBytes + 2 * (size_t)kPB * 1024 * 4 <= 220 * 1024 ? 2 : 1;
+
+template <int G>
+struct TailCfg {
+    static constexpr int kMaxOwn2 = (512 + G - 1) / G, kMaxOwn3 = (256 + G - 1) / G, kMaxOwn4 = (128 + G - 1) / G;
+    static constexpr int kMaxOwnS = (kSRows + G - 1) / G;
+    // double-buffer the staged activations when the resident weights leave room for it
+    static constexpr size_t kWeightBytes =
+        4 * ((size_t)kMaxOwn2 * 1024 + (size_t)kMaxOwn3 * 512 + (size_t)kMaxOwn4 * 256 + (size_t)kMaxOwnS * 256 + 128);
+    static constexpr int kStageBufs = kWeightBytes + 2 * (size_t)kPB * 1024 * 4 <= 220 * 1024 ? 2 : 1;
+    struct Smem {
+        float w2[kMaxOwn2][1024];
+        float w3[kMaxOwn3][512];
+        float w4[kMaxOwn4][256];
+        float wphi[kMaxOwnS][256];
+        float wlast[128];
+        alignas(16) float stage[kStageBufs][kPB * 1024];  // activations of kPB points (layer input)
+    };
+};
 
 __host__ __device__ constexpr int rec_row_layer(int r) { return r < 1024 ? 0 : r < 1536 ? 1 : r < 1792 ? 2 : r < 1920 ? 3 : 4; }
-
-struct Smem {
-    float w2[kMaxOwn2][1024];
-    float w3[kMaxOwn3][512];
-    float w4[kMaxOwn4][256];
-    float wphi[kMaxOwnS][256];
-    float wlast[128];
-    alignas(16) float stage[kStageBufs][kPB * 1024];  // activations of kPB points (layer input)
-};
 
 __device__ __forceinline__ float leaky(float x, float s) { return x < 0.0f ? x * s : x; }
 
@@ -79,7 +78,12 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+template <int kG>
 __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
+    using TC = TailCfg<kG>;
+    using Smem = typename TC::Smem;
+    constexpr int kMaxOwn2 = TC::kMaxOwn2, kMaxOwn3 = TC::kMaxOwn3, kMaxOwn4 = TC::kMaxOwn4, kMaxOwnS = TC::kMaxOwnS;
+    constexpr int kStageBufs = TC::kStageBufs;
     DevCounters* ctr = P.ctr;
     {  // grid-uniform start decision: the batch of host iteration it0 is nx[it0 & 1]
         const unsigned n0 = ctr->nx_count[P.it0 & 1];
@@ -417,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
 
 }  // namespace tail
 
-size_t tail_smem_bytes() { return sizeof(tail::Smem); }
+size_t tail_smem_bytes() { return sizeof(tail::TailCfg<148>::Smem); }
 
 // scratch: per-point activations for cap_pts points, Phi of cap_new columns, the new-column list
 // (up to max_cols entries: every column of the level)
@@ -425,25 +429,29 @@ size_t tail_scratch_bytes(unsigned cap_pts, unsigned cap_new, unsigned max_cols)
     return (size_t)cap_pts * (1024 + 512 + 256 + 128 + 2) * 4 + (size_t)cap_new * kC * 4 + (size_t)max_cols * 4 + 256;
 }
 
-int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_new, unsigned max_cols, cudaStream_t s) {
+template <int G>
+static int tail_setup(int sms) {
+    const size_t smem = sizeof(typename tail::TailCfg<G>::Smem);
+    ICG_CUDA_TRY(cudaFuncSetAttribute(tail::k_tail<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    ICG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tail::k_tail<G>, tail::kThreads, smem));
+    if (per < 1 || sms < G) {
+        set_error("k_tail: does not fit the device");
+        return ICG_ERUNTIME;
+    }
+    return ICG_OK;
+}
+
+// wide: the frame is alone on the device (148-CTA grid, lower latency); otherwise 64 CTAs
+int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_new, unsigned max_cols, cudaStream_t s,
+                bool wide) {
     static bool attr = false;
-    static int grid = 0;
-    const size_t smem = sizeof(tail::Smem);
     if (!attr) {
-        ICG_CUDA_TRY(cudaFuncSetAttribute(tail::k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int dev = 0, sms = 0, per = 0;
+        int dev = 0, sms = 0;
         ICG_CUDA_TRY(cudaGetDevice(&dev));
         ICG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        ICG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tail::k_tail, tail::kThreads, smem));
-        if (per < 1) {
-            set_error("k_tail: does not fit on an SM");
-            return ICG_ERUNTIME;
-        }
-        grid = tail::kG;
-        if (sms < tail::kG) {
-            set_error("k_tail: not enough SMs");
-            return ICG_ERUNTIME;
-        }
+        if (int r = tail_setup<64>(sms)) return r;
+        if (int r = tail_setup<148>(sms)) return r;
         attr = true;
     }
     uint8_t* q = scratch;
@@ -476,7 +484,12 @@ int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_n
     p.trace = tron ? trace : nullptr;
     if (p.trace) cudaMemsetAsync(p.trace, 0, 2000 * 8, s);
     void* args[] = {&p};
-    ICG_CUDA_TRY(cudaLaunchCooperativeKernel((void*)tail::k_tail, grid, tail::kThreads, args, smem, s));
+    if (wide)
+        ICG_CUDA_TRY(cudaLaunchCooperativeKernel((void*)tail::k_tail<148>, 148, tail::kThreads, args,
+                                                 sizeof(tail::TailCfg<148>::Smem), s));
+    else
+        ICG_CUDA_TRY(cudaLaunchCooperativeKernel((void*)tail::k_tail<64>, 64, tail::kThreads, args,
+                                                 sizeof(tail::TailCfg<64>::Smem), s));
     if (p.trace) {
         cudaStreamSynchronize(s);
         if (trace[1]) {
