@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libisocull_b200.so")
+LIB_PATH = os.environ.get("ICG_LIB") or os.path.join(HERE, "libisocull_b200.so")  # ICG_LIB: dev builds
 
 # ---- constants (include/isocull_b200.h) ----------------------------------
 ICG_OK, ICG_ERUNTIME, ICG_EINVAL, ICG_ECAPACITY, ICG_ENODEV = 0, 1, 2, 3, 4

@@ -108,6 +108,7 @@ struct icg_context {
     bool fact_used = false;  // the last extraction ran its bulk batches column-factored
     DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
     bool use_tail = true;
+    bool chain_trace = false;  // ICG_CHAIN_TRACE=1
     bool tail_wide = true;  // this frame is alone on its device: the tail kernel takes every SM
     unsigned tail_max = 128;  // conflict batches up to this size start the persistent tail kernel
     bool use_pair = true;
@@ -634,6 +635,13 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                     }
                     prof_end(c, slot);
                     if (r) return r;
+                    if (c->chain_trace) {  // dev aid: batch size of every iteration (synchronises)
+                        DevCounters h;
+                        cudaStreamSynchronize(c->stream);
+                        cudaMemcpy(&h, ctr, sizeof(h), cudaMemcpyDeviceToHost);
+                        fprintf(stderr, "[chain] level %d it %d batch %u tail_start %u\n", l, it, h.nx_count[p],
+                                h.tail_start[l]);
+                    }
                 } else if (int r = run_eval(c, fd, cj, (unsigned)nf, true)) {
                     return r;
                 }
@@ -900,6 +908,10 @@ int icg_create(int device, icg_context** out) {
     if (const char* e = getenv("ICG_NO_TAIL")) c->use_tail = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_GRAPH")) c->use_graph = !(e[0] == '1');
     if (getenv("ICG_TC_TRACE") || getenv("ICG_TAIL_TRACE")) c->use_graph = false;  // traces synchronise
+    if (getenv("ICG_CHAIN_TRACE")) {
+        c->chain_trace = true;
+        c->use_graph = false;
+    }
     if (const char* e = getenv("ICG_TAIL_MAX")) c->tail_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_SMALL_MAX")) c->small_max = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_LP_MAX")) c->lp_max = (unsigned)atoi(e);

@@ -745,8 +745,18 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
         const uint32_t feat = rank * 128u + (uint32_t)row;
         const uint32_t kc_off = (feat >> 6) * kChunk;
         const uint32_t c16 = (feat & 63u) >> 3;  // 16-byte chunk of this lane group's 8 features
-        const uint32_t hdst = ptx::mapa(ptx::smem_u32(hbuf), (uint32_t)colh);  // h buffer of the owning CTA
-        const uint32_t sdst = ptx::mapa(ptx::smem_u32(skip) + 4 * kChunk, (uint32_t)colh);  // texture: h3 -> skip
+        // h buffer of the owning CTA: warps converting this CTA's own points store locally (plain
+        // st.shared, CTA-scope proxy fence), the others through DSMEM (cluster-scope fence)
+        const bool local_dst = (uint32_t)colh == rank;
+        const uint32_t hdst = local_dst ? ptx::smem_u32(hbuf) : ptx::mapa(ptx::smem_u32(hbuf), (uint32_t)colh);
+        const uint32_t sdst = local_dst ? ptx::smem_u32(skip) + 4 * kChunk
+                                        : ptx::mapa(ptx::smem_u32(skip) + 4 * kChunk, (uint32_t)colh);  // texture: h3 -> skip
+        auto st_h = [local_dst](uint32_t a, uint4 v) {
+            if (local_dst)
+                ptx::st_shared_v4(a, v);
+            else
+                ptx::st_cluster_v4(a, v);
+        };
 
         const bool etr = P.trace && blockIdx.x == 0 && et == 0;
         int nee = 0;  // trace: epilogue event log (times at [576..832), codes at [832..1088))
@@ -856,8 +866,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                             lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
                         }
                         const uint32_t off = rbase + ((((uint32_t)(hf * 4 + u)) ^ (fr & 7u)) << 4);
-                        ptx::st_cluster_v4(dst + off, hv);
-                        if (write_lo) ptx::st_cluster_v4(dst + lo_off + off, lv);
+                        st_h(dst + off, hv);
+                        if (write_lo) st_h(dst + lo_off + off, lv);
                     }
                     continue;
                 }
@@ -873,8 +883,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t pl = (uint32_t)(hf * 32 + 8 * u + (lane & 7));
                     const uint32_t off = kc_off + pl * 128u + (((c16 ^ pl) & 7u) << 4);
-                    ptx::st_cluster_v4(dst + off, hv[u]);
-                    if (write_lo) ptx::st_cluster_v4(dst + lo_off + off, lv[u]);
+                    st_h(dst + off, hv[u]);
+                    if (write_lo) st_h(dst + lo_off + off, lv[u]);
                 }
                 if (etr) {
                     const unsigned long long c1 = clock64();
@@ -897,7 +907,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             const unsigned long long c0 = etr ? clock64() : 0;
             // every lane makes its own stores visible to the async proxy; after the warp
             // barrier one lane arrives for the warp (256 remote arrivals per block would serialise)
-            ptx::fence_proxy_async_cluster();
+            if (local_dst)
+                ptx::fence_proxy_async_smem();
+            else
+                ptx::fence_proxy_async_cluster();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(h_ready0 + 16u * (uint32_t)buf);
@@ -1090,7 +1103,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     }
                 }
             }
-            ptx::fence_proxy_async_cluster();
+            ptx::fence_proxy_async_smem();  // the skip operand is this CTA's own shared memory
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(f_ready0);
         };
@@ -1576,7 +1589,7 @@ static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, uns
         fprintf(stderr,
                 "[pair-trace %s] mma: total %.1f us, wait data %.1f, wait h %.1f, wait f %.1f | epi: total %.1f, wait acc "
                 "%.1f, wait hfree %.1f, emit %.1f\n",
-                TEX ? "tex" : (MODE == pair::kModeGeo ? "geo" : (MODE == pair::kModeCols ? "cols" : "fact")), t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3,
+                TEX ? "tex" : (MODE == pair::kModeGeo ? "geo" : (MODE == pair::kModeCols ? "cols" : (MODE == pair::kModeGeo64 ? "geo64" : "fact"))), t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3,
                 t[6] * 1e-3, t[7] * 1e-3);
         fprintf(stderr, "    epi cycles: tmem-ld %llu, convert+store %llu, fence+arrive %llu\n", t[8], t[9], t[10]);
         if (getenv("ICG_TC_EVENTS") && (t[64] || t[576])) {
