@@ -24,7 +24,8 @@ struct Status {
     do {                                                                                       \
         cudaError_t _e = (expr);                                                               \
         if (_e != cudaSuccess) {                                                               \
-            ::icg::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+            ::icg::set_error(std::string(#expr) + " (" + __FILE__ + ":" + std::to_string(__LINE__) + "): " + \
+                             cudaGetErrorString(_e));                                            \
             return ICG_ERUNTIME;                                                               \
         }                                                                                      \
     } while (0)

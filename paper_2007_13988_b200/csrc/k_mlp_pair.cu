@@ -1582,7 +1582,10 @@ static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, uns
     std::memcpy(&ta, tmapA, sizeof(CUtensorMap));
     std::memcpy(&tb, tmapB ? tmapB : tmapA, sizeof(CUtensorMap));
     pair::k_mlp_pair<MODE><<<2 * pairs, C::kThreads, C::kTotal, s>>>(ta, tb, p);
-    ICG_CUDA_TRY(cudaGetLastError());
+    if (const cudaError_t e = cudaGetLastError()) {
+        set_error("k_mlp_pair<" + std::to_string(MODE) + ">: " + cudaGetErrorString(e));
+        return ICG_ERUNTIME;
+    }
     if (p.trace) {
         cudaStreamSynchronize(s);
         const unsigned long long* t = p.trace;
