@@ -107,6 +107,8 @@ struct icg_context {
     bool geo_fact = false, use_fact = true;
     bool fact_used = false;  // the last extraction ran its bulk batches column-factored
     DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
+    DBuf xext;  // render: nonzero extent of every grid x-line
+    bool use_xext = true;  // ICG_NO_XEXT=1: rays along grid x walk every sample
     bool use_tail = true;
     bool chain_trace = false;  // ICG_CHAIN_TRACE=1
     bool tail_wide = true;  // this frame is alone on its device: the tail kernel takes every SM
@@ -735,6 +737,14 @@ int issue_render(icg_context* c, const FieldDev& fd, const icg_camera* cam, int 
     rj.ctr = ctr;
     {
         int slot = prof_begin(c, 3);
+        // rays along world x (the view direction R^T e_z has no y / z part): empty-space skipping
+        if (c->use_xext && std::fabs(cam->rotation[7]) < 1e-9 && std::fabs(cam->rotation[8]) < 1e-9) {
+            const size_t lines = ((size_t)rj.cells + 1) * ((size_t)rj.cells + 1);
+            if (int r = c->xext.ensure(lines * sizeof(int2))) return r;
+            if (int r = launch_xline_extents(rj.values, rj.cells, c->xext.as<int2>(), c->stream)) return r;
+            rj.xext = c->xext.as<int2>();
+            c->launches += 1;
+        }
         int r = launch_render_first_crossing(rj, c->stream);
         prof_end(c, slot);
         c->launches += 1;
@@ -908,6 +918,7 @@ int icg_create(int device, icg_context** out) {
     if (const char* e = getenv("ICG_NO_TAIL")) c->use_tail = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_GRAPH")) c->use_graph = !(e[0] == '1');
     if (getenv("ICG_TC_TRACE") || getenv("ICG_TAIL_TRACE")) c->use_graph = false;  // traces synchronise
+    if (const char* e = getenv("ICG_NO_XEXT")) c->use_xext = !(e[0] == '1');
     if (getenv("ICG_CHAIN_TRACE")) {
         c->chain_trace = true;
         c->use_graph = false;

@@ -275,8 +275,11 @@ struct RenderJob {
     double* surface_pts;     // world points of covered pixels (compacted)
     uint32_t* surface_px;    // pixel index per surface point
     DevCounters* ctr;
+    const int2* xext;        // per grid x-line (j, k): first / last i with a nonzero value (nullptr: none)
 };
 int launch_render_first_crossing(const RenderJob& r, cudaStream_t s);
+// extents of the nonzero values along every x-line of the (R+1)^3 grid (render empty-space skipping)
+int launch_xline_extents(const float* values, int cells, int2* ext, cudaStream_t s);
 
 size_t tc_stream_bytes(int which);
 int tc_pack_mlp(int which, const float* const* w, const float* const* b, uint8_t* host_stream,

@@ -19,6 +19,10 @@
 // view_to_world (x/scale, y/scale and the first two products of each row) and
 // the view depth of every sample (1 - 2k/R, a shared table) are computed once,
 // and a warp walks one ray 32 samples at a time (coalesced corner loads).
+// Rays along grid x (the yaw-90 view) skip empty space exactly: a sample whose
+// cell corners are all 0.0f interpolates to exactly 0 (no crossing, not
+// grazing), so only the samples whose cell meets the nonzero extent of the 4
+// x-lines around the ray (k_xline_extents) are evaluated.
 #include <algorithm>
 
 #include "eval_common.cuh"
@@ -111,6 +115,35 @@ __global__ void __launch_bounds__(kRenderThreads, 6) k_render(RenderJob r) {
         const float fy = __fsub_rn(gy_a, (float)j0), fk = __fsub_rn(gk_a, (float)kk0);
         const size_t nn = (size_t)R + 1;
         const size_t byz = nn * ((size_t)j0 + nn * (size_t)kk0);
+        // samples [k_lo, k_hi] may be nonzero; outside it every sample is exactly 0
+        int k_lo = 0, k_hi = R;
+        if (xray && r.xext) {
+            if (!yz_in) {
+                k_hi = -1;
+            } else {
+                const int2 e00 = __ldg(&r.xext[(size_t)j0 + nn * (size_t)kk0]);
+                const int2 e10 = __ldg(&r.xext[(size_t)j0 + 1 + nn * (size_t)kk0]);
+                const int2 e01 = __ldg(&r.xext[(size_t)j0 + nn * (size_t)(kk0 + 1)]);
+                const int2 e11 = __ldg(&r.xext[(size_t)j0 + 1 + nn * (size_t)(kk0 + 1)]);
+                const int lo = min(min(e00.x, e10.x), min(e01.x, e11.x));
+                const int hi = max(max(e00.y, e10.y), max(e01.y, e11.y));
+                if (lo > hi) {
+                    k_hi = -1;  // all four lines are zero: the ray misses
+                } else {
+                    // gx(k) = A + B k up to roundings (sample_at); cells lo-1 .. hi <=> gx in [lo-1, hi+1]
+                    const double B = -m[6];
+                    if (fabs(B) > 0.25) {
+                        const double A = (c0 + m[6] * (1.0 - r.trans[2]) + 1.0) * hr;
+                        const double ka = ((double)(lo - 1) - A) / B, kb = ((double)(hi + 1) - A) / B;
+                        const double kmin = fmin(ka, kb), kmax = fmax(ka, kb);
+                        k_lo = kmin < 0.0 ? 0 : (kmin > (double)R ? R + 1 : (int)floor(kmin) - 2);
+                        k_hi = kmax > (double)R ? R : (kmax < 0.0 ? -1 : (int)ceil(kmax) + 2);
+                        k_lo = max(k_lo, 0);
+                        k_hi = min(k_hi, R);
+                    }
+                }
+            }
+        }
         auto sample_at = [&](int k) -> float {
             float v = 0.0f;
             if (k <= R) {
@@ -152,15 +185,16 @@ __global__ void __launch_bounds__(kRenderThreads, 6) k_render(RenderJob r) {
         // kBatch 32-sample chunks per iteration (measured: batching chunks so more corner loads are
         // in flight costs more in registers and discarded samples than it hides; 1 is fastest)
         constexpr int kBatch = 1;
-        for (int kb2 = 0; kb2 <= R; kb2 += 32 * kBatch) {
+        for (int kb2 = k_lo; kb2 <= k_hi; kb2 += 32 * kBatch) {
             float vv[kBatch];
 #pragma unroll
-            for (int h = 0; h < kBatch; ++h) vv[h] = kb2 + 32 * h <= R ? sample_at(kb2 + 32 * h + lane) : 0.0f;
+            for (int h = 0; h < kBatch; ++h)
+                vv[h] = kb2 + 32 * h + lane <= k_hi ? sample_at(kb2 + 32 * h + lane) : 0.0f;
             bool done = false;
 #pragma unroll
             for (int h = 0; h < kBatch; ++h) {
             const int kb = kb2 + 32 * h;
-            if (done || kb > R) break;
+            if (done || kb > k_hi) break;
             const int k = kb + lane;
             const float v = vv[h];
             const unsigned hit = __ballot_sync(0xffffffffu, k <= R && v >= 0.5f);
@@ -223,6 +257,35 @@ __global__ void __launch_bounds__(kRenderThreads, 6) k_render(RenderJob r) {
         if (n_deg) atomicAdd(&r.ctr->degenerate, n_deg);
         if (n_graz) atomicAdd(&r.ctr->grazing, n_graz);
     }
+}
+
+// one warp per x-line (j, k): first and last i with values[i + n (j + n k)] != 0 ({n, -1} if none)
+__global__ void __launch_bounds__(256) k_xline_extents(const float* __restrict__ V, int R, int2* __restrict__ ext) {
+    const int n = R + 1;
+    const size_t lines = (size_t)n * n;
+    const int lane = threadIdx.x & 31;
+    for (size_t L = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; L < lines;
+         L += ((size_t)gridDim.x * blockDim.x) >> 5) {
+        const float* row = V + L * (size_t)n;
+        int first = n, last = -1;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            const int i = i0 + lane;
+            const unsigned nz = __ballot_sync(0xffffffffu, i < n && __ldg(&row[i]) != 0.0f);
+            if (nz) {
+                if (first == n) first = i0 + __ffs(nz) - 1;
+                last = i0 + 31 - __clz(nz);
+            }
+        }
+        if (lane == 0) ext[L] = make_int2(first, last);
+    }
+}
+
+int launch_xline_extents(const float* values, int cells, int2* ext, cudaStream_t s) {
+    const size_t lines = ((size_t)cells + 1) * ((size_t)cells + 1);
+    const unsigned blocks = (unsigned)std::min<size_t>((lines + 7) / 8, 148 * 16);
+    k_xline_extents<<<blocks, 256, 0, s>>>(values, cells, ext);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
 }
 
 int launch_render_first_crossing(const RenderJob& r, cudaStream_t s) {

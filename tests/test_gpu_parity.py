@@ -470,3 +470,28 @@ def test_chain_prediction_alternating_inputs(pifu_inputs):
             assert e.evals_per_level == ref[s][0]
             assert np.array_equal(e.values, ref[s][1]) and np.array_equal(i.surface_k, ref[s][2])
     c.close()
+
+
+@pytest.mark.gpu
+def test_render_empty_space_skip_identical(pifu_inputs, monkeypatch):
+    """Rays along grid x skip the samples whose cell corners are all exactly zero (per-x-line
+    nonzero extents): every output bit and counter equals the walk over all samples."""
+    inp = pifu_inputs
+    cfg = api.AlgoConfig("progressive", 32, 3)
+    cams = [api.CameraSpec.from_angles(90, 0), api.CameraSpec.from_angles(-90, 0, dist=0.3, scale=1.3),
+            api.CameraSpec.from_angles(90, 0, scale=0.7)]
+    outs = {}
+    for skip in (True, False):
+        monkeypatch.setenv("ICG_NO_XEXT", "0" if skip else "1")
+        c = api.Context(0)
+        c.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+        c.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+        f = api.PifuField(inp["fmap"], inp["caps"], 50.0, abi.ICG_PREC_FP32)
+        outs[skip] = [c.frame(f, cfg, cam, 300, 200)[1] for cam in cams]
+        c.close()
+    for a, b in zip(outs[True], outs[False]):
+        assert a.covered_pixels > 0
+        assert (a.covered_pixels, a.degenerate_brackets, a.grazing_pixels, a.texture_points) == \
+            (b.covered_pixels, b.degenerate_brackets, b.grazing_pixels, b.texture_points)
+        for x, y in ((a.depth, b.depth), (a.rgb, b.rgb), (a.mask, b.mask), (a.surface_k, b.surface_k)):
+            assert np.array_equal(x, y)
