@@ -108,6 +108,7 @@ struct icg_context {
     bool fact_used = false;  // the last extraction ran its bulk batches column-factored
     DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
     DBuf xext;  // render: nonzero extent of every grid x-line
+    DBuf rtab;  // render: per-column / per-row / per-sample view_to_world terms
     bool use_xext = true;  // ICG_NO_XEXT=1: rays along grid x walk every sample
     bool use_tail = true;
     bool chain_trace = false;  // ICG_CHAIN_TRACE=1
@@ -735,6 +736,8 @@ int issue_render(icg_context* c, const FieldDev& fd, const icg_camera* cam, int 
     rj.surface_pts = c->spts.as<double>();
     rj.surface_px = c->spx.as<uint32_t>();
     rj.ctr = ctr;
+    if (int r = c->rtab.ensure(render_tab_doubles(W, H, rj.cells) * sizeof(double))) return r;
+    rj.tab = c->rtab.as<double>();
     {
         int slot = prof_begin(c, 3);
         // rays along world x (the view direction R^T e_z has no y / z part): empty-space skipping
@@ -747,7 +750,7 @@ int issue_render(icg_context* c, const FieldDev& fd, const icg_camera* cam, int 
         }
         int r = launch_render_first_crossing(rj, c->stream);
         prof_end(c, slot);
-        c->launches += 1;
+        c->launches += 2;
         if (r) return r;
     }
     if (fd.kind == ICG_FIELD_PIFU && c->has_tex) {

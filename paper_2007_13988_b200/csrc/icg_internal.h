@@ -276,7 +276,9 @@ struct RenderJob {
     uint32_t* surface_px;    // pixel index per surface point
     DevCounters* ctr;
     const int2* xext;        // per grid x-line (j, k): first / last i with a nonzero value (nullptr: none)
+    double* tab;             // scratch of render_tab_doubles(W, H, R) doubles (k_render_setup)
 };
+inline size_t render_tab_doubles(int W, int H, int R) { return (size_t)W + H + 3 * ((size_t)R + 1); }
 int launch_render_first_crossing(const RenderJob& r, cudaStream_t s);
 // extents of the nonzero values along every x-line of the (R+1)^3 grid (render empty-space skipping)
 int launch_xline_extents(const float* values, int cells, int2* ext, cudaStream_t s);

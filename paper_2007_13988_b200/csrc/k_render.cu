@@ -49,73 +49,85 @@ __device__ __forceinline__ float sample_grid(const float* __restrict__ V, int R,
     return lerp_rn(c0, c1, fk);
 }
 
-// view_to_world, render.hpp:29-32: R^T (v - t), v = (x/scale, y/scale, z)
-__device__ __forceinline__ void view_to_world_d(const RenderJob& r, double x, double y, double z, double* w) {
-    double v0 = __dsub_rn(__ddiv_rn(x, r.scale), r.trans[0]);
-    double v1 = __dsub_rn(__ddiv_rn(y, r.scale), r.trans[1]);
-    double v2 = __dsub_rn(z, r.trans[2]);
-    const double* m = r.rot;
-    w[0] = __dadd_rn(__dadd_rn(__dmul_rn(m[0], v0), __dmul_rn(m[3], v1)), __dmul_rn(m[6], v2));
-    w[1] = __dadd_rn(__dadd_rn(__dmul_rn(m[1], v0), __dmul_rn(m[4], v1)), __dmul_rn(m[7], v2));
-    w[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[2], v0), __dmul_rn(m[5], v1)), __dmul_rn(m[8], v2));
-}
-
 constexpr int kMaxRenderCells = 1024;
 constexpr int kRenderThreads = 256;
 
-// One WARP per pixel ray: lane l evaluates sample k = kb + l of the current
-// 32-sample chunk.  Consecutive samples sit one cell apart along the ray, so
-// the lanes' corner loads are spatially coherent (fully coalesced when the ray
-// runs along the x-fastest memory axis, as for yaw 90).  The first crossing is
-// the lowest lane whose value is >= 0.5f (ballot); every value is computed with
-// the same operations as the per-thread formulation, so results are unchanged.
-__global__ void __launch_bounds__(kRenderThreads, 6) k_render(RenderJob r) {
-    __shared__ double vz_tab[kMaxRenderCells + 1];
+// The ray-independent double terms of view_to_world, each computed once per frame with the
+// operations (and roundings) of the per-sample formulation:
+//   tab[col]             = vx(col)/scale - t0     (v0 of render.hpp:29-32)
+//   tab[W + row]         = vy(row)/scale - t1     (v1)
+//   tab[W + H + 3k + a]  = m[6 + a] * (vz(k) - t2) (the view-depth products of sample k)
+__global__ void k_render_setup(RenderJob r) {
     const int W = r.width, H = r.height, R = r.cells;
-    for (int k = threadIdx.x; k <= R; k += blockDim.x)
-        vz_tab[k] = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)k), (double)R));
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < W) {
+        const double vx = __dadd_rn(-1.0, __ddiv_rn(__dmul_rn(2.0, (double)t), (double)(W - 1)));
+        r.tab[t] = __dsub_rn(__ddiv_rn(vx, r.scale), r.trans[0]);
+    } else if (t < W + H) {
+        const double vy = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)(t - W)), (double)(H - 1)));
+        r.tab[t] = __dsub_rn(__ddiv_rn(vy, r.scale), r.trans[1]);
+    } else if (t < W + H + R + 1) {
+        const int k = t - W - H;
+        const double vz = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)k), (double)R));
+        const double v2 = __dsub_rn(vz, r.trans[2]);
+        for (int a = 0; a < 3; ++a) r.tab[W + H + 3 * k + a] = __dmul_rn(r.rot[6 + a], v2);
+    }
+}
+
+// A warp renders 32 consecutive pixels.  Per-pixel work is lane-parallel (lane p owns
+// pixel base + p): the view_to_world terms, the x-ray test and the empty-space
+// window, then the output writes and the surface-point append (one atomic per
+// warp).  Each ray is then walked by the whole warp: lane l evaluates sample
+// k = kb + l of the current 32-sample chunk, so consecutive samples (one cell
+// apart along the ray) make coalesced corner loads, and the first crossing is
+// the lowest lane whose value is >= 0.5f (ballot).  Every value is computed
+// with the same operations as the per-sample formulation.
+__global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderJob r) {
+    __shared__ double mv_tab[3][kMaxRenderCells + 1];  // m[6 + a] * (vz(k) - t2)
+    const int W = r.width, H = r.height, R = r.cells;
+    for (int e = threadIdx.x; e < 3 * (R + 1); e += blockDim.x) mv_tab[e % 3][e / 3] = r.tab[W + H + e];
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const size_t npx = (size_t)W * H;
-    const size_t nwarps = (size_t)gridDim.x * (kRenderThreads / 32);
+    const unsigned npx = (unsigned)W * (unsigned)H;
+    const unsigned nwarps = gridDim.x * (kRenderThreads / 32);
     unsigned long long n_cov = 0, n_deg = 0, n_graz = 0;
     const double* m = r.rot;
     const double hr = __dmul_rn(0.5, (double)R);
     const float fR = (float)R;
-    for (size_t px = (size_t)blockIdx.x * (kRenderThreads / 32) + (threadIdx.x >> 5); px < npx; px += nwarps) {
-        const int col = (int)(px % W), row = (int)(px / W);
-        const double vx = __dadd_rn(-1.0, __ddiv_rn(__dmul_rn(2.0, (double)col), (double)(W - 1)));
-        const double vy = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, (double)row), (double)(H - 1)));
+    const size_t nn = (size_t)R + 1;
+    // gx(k) = A + B k up to roundings: the empty-space window is estimated with B's inverse
+    const double B = -m[6];
+    const bool xwin = r.xext && fabs(B) > 0.25;
+    const double invB = xwin ? 1.0 / B : 0.0;
+    for (unsigned base = (blockIdx.x * (kRenderThreads / 32) + (threadIdx.x >> 5)) * 32u; base < npx;
+         base += nwarps * 32u) {
+        // ---------------- per-pixel setup, lane-parallel ----------------
+        const unsigned px = base + (unsigned)lane;
+        const bool valid = px < npx;
+        const unsigned pxc = valid ? px : npx - 1;
+        const unsigned row = pxc / (unsigned)W, col = pxc - row * (unsigned)W;
         // view_to_world (render.hpp:29-32) with the per-pixel terms hoisted (same operations, same order)
-        const double v0 = __dsub_rn(__ddiv_rn(vx, r.scale), r.trans[0]);
-        const double v1 = __dsub_rn(__ddiv_rn(vy, r.scale), r.trans[1]);
+        const double v0 = __ldg(&r.tab[col]);
+        const double v1 = __ldg(&r.tab[W + row]);
         const double c0 = __dadd_rn(__dmul_rn(m[0], v0), __dmul_rn(m[3], v1));
         const double c1 = __dadd_rn(__dmul_rn(m[1], v0), __dmul_rn(m[4], v1));
         const double c2 = __dadd_rn(__dmul_rn(m[2], v0), __dmul_rn(m[5], v1));
-        int k1 = -1;
-        float vprev = 0.0f, vhit = 0.0f, last = 0.0f;
-        bool grazing = false;
         // Rays that run along grid x (the yaw-90 view): every grid coordinate of a sample is a
         // monotone function of k (each step a correctly rounded op with fixed operands), so if gy
         // and gk agree at k = 0 and k = R they are the SAME for every sample.  Those rays hoist
         // the y/z part of the coordinates and of the trilinear setup out of the sample loop, and a
         // sample with fx == 0 skips its x+1 corners (lerp_rn(a, b, 0) == a exactly for finite
         // values).  Every arithmetic result is unchanged.
-        float gyc = 0.0f, gkc = 0.0f;
-        if (lane < 2) {
-            const double v2 = __dsub_rn(vz_tab[lane == 0 ? 0 : R], r.trans[2]);
-            gyc = (float)__dmul_rn(__dadd_rn(__dadd_rn(c1, __dmul_rn(m[7], v2)), 1.0), hr);
-            gkc = (float)__dmul_rn(__dsub_rn(1.0, __dadd_rn(c2, __dmul_rn(m[8], v2))), hr);
-        }
-        const float gy_a = __shfl_sync(0xffffffffu, gyc, 0), gy_b = __shfl_sync(0xffffffffu, gyc, 1);
-        const float gk_a = __shfl_sync(0xffffffffu, gkc, 0), gk_b = __shfl_sync(0xffffffffu, gkc, 1);
+        const float gy_a = (float)__dmul_rn(__dadd_rn(__dadd_rn(c1, mv_tab[1][0]), 1.0), hr);
+        const float gy_b = (float)__dmul_rn(__dadd_rn(__dadd_rn(c1, mv_tab[1][R]), 1.0), hr);
+        const float gk_a = (float)__dmul_rn(__dsub_rn(1.0, __dadd_rn(c2, mv_tab[2][0])), hr);
+        const float gk_b = (float)__dmul_rn(__dsub_rn(1.0, __dadd_rn(c2, mv_tab[2][R])), hr);
         const bool xray = gy_a == gy_b && gk_a == gk_b;
         const bool yz_in = gy_a >= 0.0f && gy_a <= fR && gk_a >= 0.0f && gk_a <= fR;
-        const int j0 = min((int)floorf(gy_a), R - 1), kk0 = min((int)floorf(gk_a), R - 1);
+        const int j0 = min(max((int)floorf(gy_a), 0), R - 1), kk0 = min(max((int)floorf(gk_a), 0), R - 1);
         const float fy = __fsub_rn(gy_a, (float)j0), fk = __fsub_rn(gk_a, (float)kk0);
-        const size_t nn = (size_t)R + 1;
-        const size_t byz = nn * ((size_t)j0 + nn * (size_t)kk0);
-        // samples [k_lo, k_hi] may be nonzero; outside it every sample is exactly 0
+        // samples [k_lo, k_hi] may be nonzero; outside it every sample is exactly 0: a sample whose
+        // cell corners are all 0.0f interpolates to exactly 0 (no crossing, not grazing)
         int k_lo = 0, k_hi = R;
         if (xray && r.xext) {
             if (!yz_in) {
@@ -129,29 +141,41 @@ __global__ void __launch_bounds__(kRenderThreads, 6) k_render(RenderJob r) {
                 const int hi = max(max(e00.y, e10.y), max(e01.y, e11.y));
                 if (lo > hi) {
                     k_hi = -1;  // all four lines are zero: the ray misses
-                } else {
-                    // gx(k) = A + B k up to roundings (sample_at); cells lo-1 .. hi <=> gx in [lo-1, hi+1]
-                    const double B = -m[6];
-                    if (fabs(B) > 0.25) {
-                        const double A = (c0 + m[6] * (1.0 - r.trans[2]) + 1.0) * hr;
-                        const double ka = ((double)(lo - 1) - A) / B, kb = ((double)(hi + 1) - A) / B;
-                        const double kmin = fmin(ka, kb), kmax = fmax(ka, kb);
-                        k_lo = kmin < 0.0 ? 0 : (kmin > (double)R ? R + 1 : (int)floor(kmin) - 2);
-                        k_hi = kmax > (double)R ? R : (kmax < 0.0 ? -1 : (int)ceil(kmax) + 2);
-                        k_lo = max(k_lo, 0);
-                        k_hi = min(k_hi, R);
-                    }
+                } else if (xwin) {
+                    // cells lo-1 .. hi <=> gx in [lo-1, hi+1]; 2 samples of margin for the roundings
+                    const double A = (c0 + m[6] * (1.0 - r.trans[2]) + 1.0) * hr;
+                    const double ka = ((double)(lo - 1) - A) * invB, kb = ((double)(hi + 1) - A) * invB;
+                    const double kmin = fmin(ka, kb), kmax = fmax(ka, kb);
+                    k_lo = kmin < 0.0 ? 0 : (kmin > (double)R ? R + 1 : (int)floor(kmin) - 2);
+                    k_hi = kmax > (double)R ? R : (kmax < 0.0 ? -1 : (int)ceil(kmax) + 2);
+                    k_lo = max(k_lo, 0);
+                    k_hi = min(k_hi, R);
                 }
             }
         }
-        auto sample_at = [&](int k) -> float {
-            float v = 0.0f;
-            if (k <= R) {
-                const double v2 = __dsub_rn(vz_tab[k], r.trans[2]);
-                const double w0 = __dadd_rn(c0, __dmul_rn(m[6], v2));
+        // ---------------- the rays, one at a time across the warp ----------------
+        int my_k1 = -1;
+        float my_vhit = 0.0f, my_vprev = 0.0f;
+        bool my_graz = false;
+        unsigned todo = __ballot_sync(0xffffffffu, valid && k_lo <= k_hi);
+        while (todo) {
+            const int p = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const double pc0 = __shfl_sync(0xffffffffu, c0, p);
+            const double pc1 = __shfl_sync(0xffffffffu, c1, p);
+            const double pc2 = __shfl_sync(0xffffffffu, c2, p);
+            const bool pxray = __shfl_sync(0xffffffffu, (int)xray, p) != 0;
+            const bool pyz_in = __shfl_sync(0xffffffffu, (int)yz_in, p) != 0;
+            const int pj0 = __shfl_sync(0xffffffffu, j0, p), pkk0 = __shfl_sync(0xffffffffu, kk0, p);
+            const float pfy = __shfl_sync(0xffffffffu, fy, p), pfk = __shfl_sync(0xffffffffu, fk, p);
+            const int plo = __shfl_sync(0xffffffffu, k_lo, p), phi = __shfl_sync(0xffffffffu, k_hi, p);
+            const size_t byz = nn * ((size_t)pj0 + nn * (size_t)pkk0);
+            auto sample_at = [&](int k) -> float {
+                float v = 0.0f;
+                const double w0 = __dadd_rn(pc0, mv_tab[0][k]);
                 const float gx = (float)__dmul_rn(__dadd_rn(w0, 1.0), hr);
-                if (xray) {
-                    if (yz_in && gx >= 0.0f && gx <= fR) {
+                if (pxray) {
+                    if (pyz_in && gx >= 0.0f && gx <= fR) {
                         const int i0 = min((int)floorf(gx), R - 1);
                         const float fx = __fsub_rn(gx, (float)i0);
                         const float* V = r.values + byz + (size_t)i0;
@@ -168,90 +192,97 @@ __global__ void __launch_bounds__(kRenderThreads, 6) k_render(RenderJob r) {
                             c01 = lerp_rn(__ldg(&V[sk]), __ldg(&V[sk + 1]), fx);
                             c11 = lerp_rn(__ldg(&V[sj + sk]), __ldg(&V[sj + sk + 1]), fx);
                         }
-                        const float cy0 = lerp_rn(c00, c10, fy);
-                        const float cy1 = lerp_rn(c01, c11, fy);
-                        v = lerp_rn(cy0, cy1, fk);
+                        const float cy0 = lerp_rn(c00, c10, pfy);
+                        const float cy1 = lerp_rn(c01, c11, pfy);
+                        v = lerp_rn(cy0, cy1, pfk);
                     }
                 } else {
-                    const double w1 = __dadd_rn(c1, __dmul_rn(m[7], v2));
-                    const double w2 = __dadd_rn(c2, __dmul_rn(m[8], v2));
+                    const double w1 = __dadd_rn(pc1, mv_tab[1][k]);
+                    const double w2 = __dadd_rn(pc2, mv_tab[2][k]);
                     const float gy = (float)__dmul_rn(__dadd_rn(w1, 1.0), hr);
                     const float gk = (float)__dmul_rn(__dsub_rn(1.0, w2), hr);
                     v = sample_grid(r.values, R, gx, gy, gk);
                 }
+                return v;
+            };
+            int k1 = -1;
+            float vprev = 0.0f, vhit = 0.0f, last = 0.0f;  // the sample before k_lo is exactly 0
+            bool grazing = false;
+            for (int kb = plo; kb <= phi; kb += 32) {
+                const int k = kb + lane;
+                const float v = k <= phi ? sample_at(k) : 0.0f;
+                const unsigned hit = __ballot_sync(0xffffffffu, k <= phi && v >= 0.5f);
+                const int first = hit ? __ffs(hit) - 1 : 32;
+                // samples before the crossing: grazing (0 < v < 1), render.hpp:180-188
+                grazing |= __ballot_sync(0xffffffffu, lane < first && k <= phi && v > 0.0f && v < 1.0f) != 0u;
+                const float prev_in_chunk = __shfl_up_sync(0xffffffffu, v, 1);
+                if (hit) {
+                    k1 = kb + first;
+                    vhit = __shfl_sync(0xffffffffu, v, first);
+                    const float pv = __shfl_sync(0xffffffffu, prev_in_chunk, first);
+                    vprev = first > 0 ? pv : last;
+                    break;
+                }
+                last = __shfl_sync(0xffffffffu, v, 31);
             }
-            return v;
-        };
-        // kBatch 32-sample chunks per iteration (measured: batching chunks so more corner loads are
-        // in flight costs more in registers and discarded samples than it hides; 1 is fastest)
-        constexpr int kBatch = 1;
-        for (int kb2 = k_lo; kb2 <= k_hi; kb2 += 32 * kBatch) {
-            float vv[kBatch];
-#pragma unroll
-            for (int h = 0; h < kBatch; ++h)
-                vv[h] = kb2 + 32 * h + lane <= k_hi ? sample_at(kb2 + 32 * h + lane) : 0.0f;
-            bool done = false;
-#pragma unroll
-            for (int h = 0; h < kBatch; ++h) {
-            const int kb = kb2 + 32 * h;
-            if (done || kb > k_hi) break;
-            const int k = kb + lane;
-            const float v = vv[h];
-            const unsigned hit = __ballot_sync(0xffffffffu, k <= R && v >= 0.5f);
-            const int first = hit ? __ffs(hit) - 1 : 32;
-            // samples before the crossing: grazing (0 < v < 1), render.hpp:180-188
-            grazing |= __ballot_sync(0xffffffffu, lane < first && k <= R && v > 0.0f && v < 1.0f) != 0u;
-            const float prev_in_chunk = __shfl_up_sync(0xffffffffu, v, 1);
-            if (hit) {
-                k1 = kb + first;
-                vhit = __shfl_sync(0xffffffffu, v, first);
-                const float pv = __shfl_sync(0xffffffffu, prev_in_chunk, first);
-                vprev = first > 0 ? pv : last;
-                done = true;
-                break;
+            if (lane == p) {
+                my_k1 = k1;
+                my_vhit = vhit;
+                my_vprev = vprev;
+                my_graz = grazing;
             }
-            last = __shfl_sync(0xffffffffu, v, 31);
-            }
-            if (done) break;
         }
-        if (lane == 0) {
-            r.rgb[3 * px + 0] = r.bg[0];
-            r.rgb[3 * px + 1] = r.bg[1];
-            r.rgb[3 * px + 2] = r.bg[2];
-            if (k1 < 0) {
+        // ---------------- outputs, lane-parallel ----------------
+        const bool cov = valid && my_k1 >= 0;
+        const unsigned covm = __ballot_sync(0xffffffffu, cov);
+        unsigned pos0 = 0;
+        if (covm) {  // the warp's surface points take one contiguous range of the compact list
+            if (lane == 0) pos0 = atomicAdd(&r.ctr->surface_count, (unsigned)__popc(covm));
+            pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+        }
+        if (valid) {
+            r.rgb[3 * (size_t)px + 0] = r.bg[0];
+            r.rgb[3 * (size_t)px + 1] = r.bg[1];
+            r.rgb[3 * (size_t)px + 2] = r.bg[2];
+            if (!cov) {
                 r.depth[px] = -2.0f;  // kInvalidDepth, render.hpp:72
                 r.mask[px] = 0;
                 if (r.surface_k) r.surface_k[px] = -1;
-                n_graz += grazing ? 1 : 0;
+                n_graz += my_graz ? 1 : 0;
             } else {
                 ++n_cov;
-                double s = 1.0;
-                if (k1 > 0) {
-                    double v1d = (double)vhit, v0d = (double)vprev;
-                    double denom = __dsub_rn(v1d, v0d);
+                double sv = 1.0;
+                if (my_k1 > 0) {
+                    const double v1d = (double)my_vhit, v0d = (double)my_vprev;
+                    const double denom = __dsub_rn(v1d, v0d);
                     if (denom > 0.0) {
-                        s = __ddiv_rn(__dsub_rn(0.5, v0d), denom);
-                        s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
+                        sv = __ddiv_rn(__dsub_rn(0.5, v0d), denom);
+                        sv = sv < 0.0 ? 0.0 : (sv > 1.0 ? 1.0 : sv);
                     } else {
                         ++n_deg;
                     }
                 }
-                double depth =
-                    __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn(__dsub_rn((double)k1, 1.0), s)), (double)R));
+                const double depth =
+                    __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn(__dsub_rn((double)my_k1, 1.0), sv)), (double)R));
                 r.depth[px] = (float)depth;
                 r.mask[px] = 1;
-                if (r.surface_k) r.surface_k[px] = k1;
-                double w[3];
-                view_to_world_d(r, vx, vy, depth, w);
-                unsigned pos = atomicAdd(&r.ctr->surface_count, 1u);
-                r.surface_pts[3 * (size_t)pos + 0] = w[0];
-                r.surface_pts[3 * (size_t)pos + 1] = w[1];
-                r.surface_pts[3 * (size_t)pos + 2] = w[2];
-                r.surface_px[pos] = (uint32_t)px;
+                if (r.surface_k) r.surface_k[px] = my_k1;
+                // view_to_world(vx, vy, depth) = c + m[6..8] (depth - t2): the hoisted terms again
+                const double v2 = __dsub_rn(depth, r.trans[2]);
+                const unsigned pos = pos0 + (unsigned)__popc(covm & ((1u << lane) - 1u));
+                r.surface_pts[3 * (size_t)pos + 0] = __dadd_rn(c0, __dmul_rn(m[6], v2));
+                r.surface_pts[3 * (size_t)pos + 1] = __dadd_rn(c1, __dmul_rn(m[7], v2));
+                r.surface_pts[3 * (size_t)pos + 2] = __dadd_rn(c2, __dmul_rn(m[8], v2));
+                r.surface_px[pos] = px;
             }
         }
     }
-    (void)fR;
+    // block-level counter totals
+    for (int o = 16; o > 0; o >>= 1) {
+        n_cov += __shfl_xor_sync(0xffffffffu, n_cov, o);
+        n_deg += __shfl_xor_sync(0xffffffffu, n_deg, o);
+        n_graz += __shfl_xor_sync(0xffffffffu, n_graz, o);
+    }
     if (lane == 0) {
         if (n_cov) atomicAdd(&r.ctr->covered, n_cov);
         if (n_deg) atomicAdd(&r.ctr->degenerate, n_deg);
@@ -268,12 +299,21 @@ __global__ void __launch_bounds__(256) k_xline_extents(const float* __restrict__
          L += ((size_t)gridDim.x * blockDim.x) >> 5) {
         const float* row = V + L * (size_t)n;
         int first = n, last = -1;
-        for (int i0 = 0; i0 < n; i0 += 32) {
-            const int i = i0 + lane;
-            const unsigned nz = __ballot_sync(0xffffffffu, i < n && __ldg(&row[i]) != 0.0f);
-            if (nz) {
-                if (first == n) first = i0 + __ffs(nz) - 1;
-                last = i0 + 31 - __clz(nz);
+        for (int g0 = 0; g0 < n; g0 += 32 * 8) {  // 8 chunks of 32 in flight per lane
+            float v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int i = g0 + 32 * c + lane;
+                v[c] = i < n ? __ldg(&row[i]) : 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const unsigned nz = __ballot_sync(0xffffffffu, v[c] != 0.0f);
+                if (nz) {
+                    const int i0 = g0 + 32 * c;
+                    if (first == n) first = i0 + __ffs(nz) - 1;
+                    last = i0 + 31 - __clz(nz);
+                }
             }
         }
         if (lane == 0) ext[L] = make_int2(first, last);
@@ -294,7 +334,14 @@ int launch_render_first_crossing(const RenderJob& r, cudaStream_t s) {
         return ICG_EINVAL;
     }
     const size_t npx = (size_t)r.width * r.height;
-    const size_t blocks = std::min<size_t>((npx + kRenderThreads / 32 - 1) / (kRenderThreads / 32), 148 * 16);
+    if (npx >= (1ull << 32)) {
+        set_error("render: too many pixels");
+        return ICG_EINVAL;
+    }
+    const int nt = r.width + r.height + r.cells + 1;
+    k_render_setup<<<(nt + 255) / 256, 256, 0, s>>>(r);
+    const size_t warps = (npx + 31) / 32;  // 32 pixels per warp
+    const size_t blocks = std::min<size_t>((warps + kRenderThreads / 32 - 1) / (kRenderThreads / 32), 148 * 4);
     k_render<<<(unsigned)blocks, kRenderThreads, 0, s>>>(r);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
