@@ -457,9 +457,10 @@ int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned
     if (fd.precision == ICG_PREC_FP32_SIMT)
         r = launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
     else if (c->geo_pair && c->tex_pair && c->use_pair)
-        r = launch_pifu_pair_texture(fd, c->geo_tc, c->tex_tc, c->geo_pair_f16_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1],
-                                     c->tex_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1], job, max_points,
-                                     fd.precision == ICG_PREC_FP32, c->stream);
+        // one fp16 copy of every weight and operand, one MMA per K step, at every precision:
+        // colours within 5.2e-4 of fp64 (scripts/tex_precision.py; tolerance 1e-3)
+        r = launch_pifu_pair_texture(fd, c->geo_tc, c->tex_tc, c->geo_pair_f16_tmap[1], c->tex_pair_tmap[1], job,
+                                     max_points, false, c->stream);
     else
         r = launch_pifu_tc_texture(fd, c->geo_tc, c->tex_tc, job, max_points, fd.precision == ICG_PREC_FP32,
                                    c->stream);

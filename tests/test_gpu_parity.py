@@ -495,3 +495,15 @@ def test_render_empty_space_skip_identical(pifu_inputs, monkeypatch):
             (b.covered_pixels, b.degenerate_brackets, b.grazing_pixels, b.texture_points)
         for x, y in ((a.depth, b.depth), (a.rgb, b.rgb), (a.mask, b.mask), (a.surface_k, b.surface_k)):
             assert np.array_equal(x, y)
+
+
+@pytest.mark.gpu
+def test_texture_colour_error_wide_sample(gpu_ctx, pifu_inputs):
+    """The texture kernel keeps one fp16 copy of every weight and operand (fp32 accumulation):
+    colours over a wide random sample stay within the 1e-3 bar (fp64 model: 5.2e-4 max)."""
+    f = _pifu(gpu_ctx, pifu_inputs, abi.ICG_PREC_FP32)
+    m = _oracle_model(pifu_inputs)
+    pts = np.random.default_rng(11).uniform(-0.9, 0.9, (20000, 3))
+    err = np.abs(gpu_ctx.texture_batch(f, pts) - m.texture(pts)).max()
+    print(f"max colour error {err:.3e}")
+    assert err <= RGB_TOL
