@@ -308,6 +308,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
     constexpr int kEpiWarps = C::kEpiWarps, kEpiThreads = C::kEpiThreads, kHF = C::kHF;
     auto epi_bar = [] { epi_bar_n<C::kEpiThreads>(); };
     constexpr bool TEX = MODE == kModeTex, COLS = MODE == kModeCols, FACT = MODE == kModeFact;
+    // h operands (and TEX's h3 skip chunks) MN-major: one 128-byte row per feature, written
+    // without register transposes (b_major = MN in the instruction descriptor)
+    constexpr bool kMnH = FACT || TEX;
     constexpr int NPC = C::NPC, NP = C::NP, NOUT = C::kOut, kStages = C::kStages;
     constexpr uint32_t kChunk = C::kChunk, kSkipHalf = C::kSkipHalf, kHHalf = C::kHHalf;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -491,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             auto item = [&](uint32_t dcol, uint32_t b_hi, uint32_t b_lo, bool acc, bool mn = false, bool f16 = false) {
                 const uint64_t bd_hi = mn ? ptx::sdesc_sw128_mn(b_hi) : ptx::sdesc_sw128(b_hi);
                 const uint64_t bd_lo = mn ? ptx::sdesc_sw128_mn(b_lo) : ptx::sdesc_sw128(b_lo);
-                const uint32_t id = f16 ? idesc_f16 : (mn ? idesc_mn : idesc);
+                const uint32_t id = (f16 ? idesc_f16 : idesc) | (mn ? (1u << 16) : 0u);
                 if (P.x3) {
                     wait_full();
                     const uint64_t ad_hi = ptx::sdesc_sw128(ring0 + s * kStage);
@@ -550,19 +553,20 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     wait_h(buf, half);
                     for (int jj = 2 * half; jj < 2 * half + 2; ++jj)
                         for (int m = 0; m < nm; ++m)
-                            item(dcol0 + m * NP, bh + jj * kChunk, bl + jj * kChunk, !(first && jj == 0), FACT,
+                            item(dcol0 + m * NP, bh + jj * kChunk, bl + jj * kChunk, !(first && jj == 0), kMnH,
                                  C::kF16H);
                     ptx::mma_commit_pair(&ms.h_free[buf][half], both);
                 }
             };
             auto skipk = [&](int j) { return skip_hi + j * kChunk; };
+            auto skipmn = [&](int j) { return TEX && j >= 4; };  // TEX: [Phi K-major | h3 MN-major]
             auto skipl = [&](int j) { return skip_lo + j * kChunk; };
             // TMEM columns: D2[m] = m*NP, BUF[b] = 2NP + b*NP, D3 = BUF[0], D4 = D2[0]
             uint32_t d4fph = 0;
             uint32_t cblk = 0, hblk = 0;  // COLS accumulator blocks / FACT h blocks issued so far
             auto body = [&](int ks, bool with_l4, bool wait_d4) {
                 auto L1 = [&](int c) {
-                    for (int j = 0; j < ks; ++j) item(2 * NP + (c & 1) * NP, skipk(j), skipl(j), j > 0, false, C::kF16Skip);
+                    for (int j = 0; j < ks; ++j) item(2 * NP + (c & 1) * NP, skipk(j), skipl(j), j > 0, skipmn(j), C::kF16Skip);
                     ptx::mma_commit_pair(&ms.l1done[c & 1], both);
                 };
                 L1(0);
@@ -573,17 +577,17 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     ptx::tc_fence_after();
                 }
                 for (int m = 0; m < 2; ++m)
-                    for (int j = 0; j < ks; ++j) item(m * NP, skipk(j), skipl(j), j > 0, false, C::kF16Skip);
+                    for (int j = 0; j < ks; ++j) item(m * NP, skipk(j), skipl(j), j > 0, skipmn(j), C::kF16Skip);
                 for (int c = 0; c < 4; ++c) {
                     h_block(2, 0);
                     if (c + 2 < 4) L1(c + 2);
                 }
                 ptx::mma_commit_pair(&ms.d2done, both);
-                for (int j = 0; j < ks; ++j) item(2 * NP, skipk(j), skipl(j), j > 0, false, C::kF16Skip);
+                for (int j = 0; j < ks; ++j) item(2 * NP, skipk(j), skipl(j), j > 0, skipmn(j), C::kF16Skip);
                 for (int c = 0; c < 2; ++c) h_block(1, 2 * NP);
                 ptx::mma_commit_pair(&ms.d3done, both);
                 if (with_l4) {
-                    for (int j = 0; j < ks; ++j) item(0, skipk(j), skipl(j), j > 0, false, C::kF16Skip);
+                    for (int j = 0; j < ks; ++j) item(0, skipk(j), skipl(j), j > 0, skipmn(j), C::kF16Skip);
                     ptx::mma_commit_pair(&ms.skip_free, both);  // last reader of the skip operand
                     h_block(1, 0);
                     ptx::mma_commit_pair(&ms.d4done, both);
@@ -849,7 +853,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     const float x = __uint_as_float(r[q]) + fmaf(wz, zc[colh * NPC + hf * 32 + q], bo);
                     v[q] = x < 0.0f ? x * P.slope : x;
                 }
-                if constexpr (FACT) {
+                if constexpr (kMnH) {
                     // MN-major operand: this thread's feature is one 128-byte row (64 points) of its
                     // K-chunk; points hf*32 + 8u .. +7 are the 16-byte chunk hf*4 + u (swizzled by row)
                     const uint32_t fr = feat & 63u;
@@ -862,8 +866,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
                             const float a = v[8 * u + 2 * i], b = v[8 * u + 2 * i + 1];
-                            hp[i] = pack_bf16(a, b);
-                            lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                            if (f16) {
+                                __half2 f2 = __floats2half2_rn(a, b);
+                                hp[i] = *reinterpret_cast<uint32_t*>(&f2);
+                                lp[i] = 0u;
+                            } else {
+                                hp[i] = pack_bf16(a, b);
+                                lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                            }
                         }
                         const uint32_t off = rbase + ((((uint32_t)(hf * 4 + u)) ^ (fr & 7u)) << 4);
                         st_h(dst + off, hv);
@@ -1374,9 +1384,17 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     for (int c = 0; c < NOUT; ++c) acc[c] = 0.0f;
                     for (int j = part * kSF; j < part * kSF + kSF; j += 2) {
                         const int k = 256 + j;
+                        float x0, x1;
+                        if constexpr (kMnH) {
+                            // MN-major h3 chunk: feature row fr, point pl at 16-byte chunk pl / 8 (swizzled)
+                            const uint32_t fr = (uint32_t)(k & 63), cb = (uint32_t)(k >> 6) * kChunk + ((uint32_t)pl & 7u) * 2u;
+                            const uint32_t o0 = cb + fr * 128u + (((((uint32_t)pl >> 3) ^ fr) & 7u) << 4);
+                            const uint32_t o1 = cb + (fr + 1u) * 128u + (((((uint32_t)pl >> 3) ^ (fr + 1u)) & 7u) << 4);
+                            x0 = __half2float(*reinterpret_cast<const __half*>(skip + o0));
+                            x1 = __half2float(*reinterpret_cast<const __half*>(skip + o1));
+                        } else {
                         const uint32_t off = (uint32_t)(k >> 6) * kChunk + sw128((uint32_t)pl, (uint32_t)(k & 63));
                         const uint32_t hv = *reinterpret_cast<const uint32_t*>(skip + off);
-                        float x0, x1;
                         if constexpr (C::kF16Skip) {
                             const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hv));
                             x0 = f.x;
@@ -1385,6 +1403,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                             const uint32_t lv = *reinterpret_cast<const uint32_t*>(skip + kSkipHalf + off);
                             x0 = __uint_as_float(hv << 16) + __uint_as_float(lv << 16);
                             x1 = __uint_as_float(hv & 0xFFFF0000u) + __uint_as_float(lv & 0xFFFF0000u);
+                        }
                         }
 #pragma unroll
                         for (int c = 0; c < NOUT; ++c) {
