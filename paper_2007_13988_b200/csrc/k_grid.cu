@@ -430,18 +430,32 @@ __global__ void k_slot_count(const uint32_t* __restrict__ list, const unsigned* 
         atomicAdd(&cnt[cmap[list[t] % plane]], 1u);
 }
 
-// exclusive scan of cnt[0 .. *ncols) in place (one block)
+// exclusive scan of cnt[0 .. *ncols) in place (one block; each thread scans 8 consecutive
+// entries of an 8 K pass staged in shared memory with coalesced loads and stores)
 __global__ void __launch_bounds__(1024) k_scan_slots(uint32_t* __restrict__ cnt, const unsigned* __restrict__ ncols) {
+    constexpr int kPer = 8;
     __shared__ unsigned warp_sums[32];
     __shared__ unsigned carry;
+    __shared__ unsigned stage[1024 * kPer];  // coalesced loads, scanned per thread from shared memory
     const unsigned n = *ncols;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (unsigned base = 0; base < n; base += 1024) {
-        const unsigned idx = base + threadIdx.x;
-        const unsigned v = idx < n ? cnt[idx] : 0u;
-        unsigned x = v;
+    for (unsigned base = 0; base < n; base += 1024u * kPer) {
+        const unsigned i0 = base + threadIdx.x * kPer;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const unsigned i = base + q * 1024u + threadIdx.x;
+            stage[q * 1024 + threadIdx.x] = i < n ? cnt[i] : 0u;
+        }
+        __syncthreads();
+        unsigned v[kPer], sum = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            v[q] = stage[threadIdx.x * kPer + q];
+            sum += v[q];
+        }
+        unsigned x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
@@ -460,9 +474,20 @@ __global__ void __launch_bounds__(1024) k_scan_slots(uint32_t* __restrict__ cnt,
             warp_sums[lane] = ws - w;
         }
         __syncthreads();
-        if (idx < n) cnt[idx] = carry + warp_sums[warp] + x - v;
+        unsigned run = carry + warp_sums[warp] + x - sum;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            stage[threadIdx.x * kPer + q] = run;
+            run += v[q];
+        }
         __syncthreads();
-        if (threadIdx.x == 1023) carry += warp_sums[31] + x;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const unsigned i = base + q * 1024u + threadIdx.x;
+            if (i < n) cnt[i] = stage[q * 1024 + threadIdx.x];
+        }
+        (void)i0;
+        if (threadIdx.x == 1023) carry = run;
         __syncthreads();
     }
 }
