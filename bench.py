@@ -220,7 +220,7 @@ def main():
     ap.add_argument("--l2", default="flush", choices=["flush", "cycle"],
                     help="flush: 320 MB device copy before every frame; cycle: no flush, the distinct "
                          "feature maps cycled over (streams x frames x 16.8 MB) exceed the 126 MB L2")
-    ap.add_argument("--streams", type=int, default=3,
+    ap.add_argument("--streams", type=int, default=4,
                     help="frames in flight per GPU (one context + stream + host thread each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
