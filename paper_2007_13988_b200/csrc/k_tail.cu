@@ -230,10 +230,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
             }
             grid.sync();
         }
-        if (m > 0) {
-            grid.sync();  // everyone has read *P.nnew
-            if (gtid == 0) *P.nnew = 0u;
-        }
+        // every CTA read *P.nnew before the record phase's barriers; the claims that count it
+        // again come after this iteration's layer barriers
+        if (m > 0 && gtid == 0) *P.nnew = 0u;
         // ---- process the batch in chunks of the scratch capacity ----
         for (unsigned base = 0; base < n; base += P.cap_pts) {
             const unsigned nc = min(P.cap_pts, n - base);
@@ -377,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
         // ---- expand for iteration it + 1 (k_conflict_expand with p = (it + 1) & 1) ----
         const int p = q ^ 1;
         const unsigned ncf = __ldcg(&ctr->cf_count[p]);
-        grid.sync();  // everyone has read the counts before they are reset
+        // the counters reset here (cf / nx of parity q) were last read before earlier barriers
         if (gtid == 0) {
             ctr->cf_count[p ^ 1] = 0;
             ctr->nx_count[p ^ 1] = 0;
