@@ -112,6 +112,7 @@ struct icg_context {
     bool use_xext = true;  // ICG_NO_XEXT=1: rays along grid x walk every sample
     bool use_tail = true;
     bool chain_trace = false;  // ICG_CHAIN_TRACE=1
+    bool use_fact2 = true;     // bulk factored pass with swapped operands (k_fact2.cu); ICG_FACT2=0: k_mlp_pair<FACT>
     bool tail_wide = true;  // this frame is alone on its device: the tail kernel takes every SM
     unsigned tail_max = 128;  // conflict batches up to this size start the persistent tail kernel
     bool use_pair = true;
@@ -396,8 +397,11 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
     if (int r = launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][xi], cj, c->colrec.as<float>(), max_cols,
                                       xi == 0, c->stream))
         return r;
-    int r = launch_pifu_pair_fact(fd, c->geo_tc, c->geo_fact_tmap[0][xi], pj, c->colrec.as<float>(), cm, max_points,
-                                  xi == 0, c->stream);
+    int r = (c->use_fact2 && xi == 0)
+                ? launch_pifu_fact2(fd, c->geo_tc, c->geo_fact_tmap[0][0], pj, c->colrec.as<float>(), cm, max_points,
+                                    c->stream)
+                : launch_pifu_pair_fact(fd, c->geo_tc, c->geo_fact_tmap[0][xi], pj, c->colrec.as<float>(), cm,
+                                        max_points, xi == 0, c->stream);
     prof_end(c, slot);
     c->launches += 2;
     return r;
@@ -922,6 +926,7 @@ int icg_create(int device, icg_context** out) {
     if (const char* e = getenv("ICG_NO_TAIL")) c->use_tail = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_GRAPH")) c->use_graph = !(e[0] == '1');
     if (getenv("ICG_TC_TRACE") || getenv("ICG_TAIL_TRACE")) c->use_graph = false;  // traces synchronise
+    if (const char* e = getenv("ICG_FACT2")) c->use_fact2 = e[0] == '1';
     if (const char* e = getenv("ICG_NO_XEXT")) c->use_xext = !(e[0] == '1');
     if (getenv("ICG_CHAIN_TRACE")) {
         c->chain_trace = true;

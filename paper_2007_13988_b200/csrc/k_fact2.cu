@@ -1,0 +1,462 @@
+// k_fact2.cu — column-factored geometry field, bulk batches, with the operands swapped:
+// A = the point tile's activations, B = the weight tiles.
+//
+// Same arithmetic as k_mlp_pair<FACT> (localize.hpp:76-90 evaluation of
+// a node list): layer 1 = act(S1[col] + w1z z + b1) from the column record, layers 2-4 =
+// act(W_h . h + S_l[col] + w_lz z + b_l) with W_h on the tensor cores (bf16x3), output =
+// sigmoid(w5 . h4 + S5[col] + b5 + w5z z - sdf_scale sdf).  What changes is the MMA shape:
+//
+//   tcgen05.mma.cta_group::2, M = 256 POINTS (128 per CTA), N = 256 output features,
+//   A = activations, K-major, each CTA's own 128 points in its own shared memory,
+//   B = weight tile, K-major, 128 of the 256 feature rows per CTA (the FACT stream as is),
+//   D = TMEM, lane = point, column = feature.
+//
+// Consequences (the reasons for the swap):
+//   * an epilogue thread owns one point (its TMEM lane) and reads that point's features, so the
+//     next layer's operand is written by the CTA that owns the point: no DSMEM exchange, no
+//     register transposes, and the final 128 -> 1 layer is an in-thread dot product;
+//   * N = 256 instead of 128: per MMA the shared-memory port reads 4 KB of A + 4 KB of B per CTA
+//     for 2x the MACs (scripts/mma_bench.cu: pair M256 N128 87 clk, N256 152 clk per MMA).
+//
+// TMEM (512 columns x 128 lanes per CTA): layer 2's D2 fills it (512 features); D3 reuses
+// columns 0-255 once h2 chunks 0-3 are read, D4 (N = 256, upper half zero weights) columns
+// 256-511.  The next tile's layer 2 starts when the final layer has read D4.
+//
+// Activation chunks (64 K x 128 points, bf16 hi + lo = 32 KB) stream through a ring of 4 slots:
+// 16 h1 chunks (from the records), 8 h2 chunks (from D2), 4 h3 chunks (from D3) per tile.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "eval_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace icg {
+
+namespace fact2 {
+
+constexpr uint32_t kHalf = 16384;                   // 128 x 64 bf16 tile
+constexpr uint32_t kStage = 32768;                  // weight item: (hi, lo) of 128 rows x 64 K
+constexpr int kStages = 2;                          // weight ring
+constexpr int kA = 4;                               // activation chunk ring
+constexpr uint32_t kAChunk = 32768;                 // 128 points x 64 K, hi then lo
+constexpr int kEpiWarps = 8;                        // 4 TMEM lane quarters x 2 column halves
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 64 + kEpiThreads;
+constexpr int NPC = 128;                            // points per CTA
+constexpr int NP = 256;                             // points per pair tile
+constexpr int kSRow = 1936;
+constexpr int kSFinal = 1920;
+constexpr int kItems = 44;                          // FACT stream: L2 (kc, m) 32, L3 8, L4 4
+constexpr uint32_t kOffRing = 0;
+constexpr uint32_t kOffA = kOffRing + kStages * kStage;
+constexpr uint32_t kOffMisc = kOffA + kA * kAChunk;
+constexpr uint32_t kMisc = 8192;
+constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
+static_assert(kTotal <= 232448, "shared memory");
+
+struct Misc {
+    uint64_t full[kStages], empty[kStages];
+    uint64_t a_ready[kA], a_free[kA];
+    uint64_t d2done, d3done, d4done, tm_free;
+    uint32_t tmem_base;
+    int ncaps;
+    float caps[16][8];
+    int slot[NPC];
+    float z[NPC], cterm[NPC], sfinal[NPC];
+    float red[NPC];
+};
+static_assert(sizeof(Misc) <= kMisc, "misc");
+
+struct Params {
+    FieldDev f;
+    EvalJob job;
+    const float* bias;   // [b, wz] per layer (tc layout), then b5
+    const float* wlast;  // [128 + 257]: w5 hidden part, Phi part, z
+    const float* s_in;   // column records
+    const int* cmap;     // column -> record
+    float slope;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_fact2(const __grid_constant__ CUtensorMap tmapW, Params P) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring = smem + kOffRing;
+    uint8_t* abuf = smem + kOffA;
+    Misc& ms = *reinterpret_cast<Misc*>(smem + kOffMisc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_rank();
+    const bool leader = rank == 0;
+    const EvalJob& job = P.job;
+    const unsigned pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const unsigned n = job_count(job);
+    if (n < job.min_count || (job.max_count && n > job.max_count)) return;
+    if (pair_id * NP >= n) {
+        job_account(job);
+        return;
+    }
+    const unsigned ntiles = (n + NP - 1) / NP;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&ms.full[s], 1);
+            ptx::mbar_init(&ms.empty[s], 1);
+        }
+        for (int a = 0; a < kA; ++a) {
+            ptx::mbar_init(&ms.a_ready[a], 2 * kEpiWarps);  // every epilogue warp of both CTAs
+            ptx::mbar_init(&ms.a_free[a], 1);
+        }
+        ptx::mbar_init(&ms.d2done, 1);
+        ptx::mbar_init(&ms.d3done, 1);
+        ptx::mbar_init(&ms.d4done, 1);
+        ptx::mbar_init(&ms.tm_free, 2 * kEpiWarps);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmapW);
+    if (threadIdx.x >= 64 && threadIdx.x < 64 + 32) {  // capsule figure of the sdf bias
+        const int i = threadIdx.x - 64;
+        const int np = __ldg(&P.f.fscene->n_prims);
+        if (i < np && i < 16) {
+            const FPrim* pr = &P.f.fscene->prims[i];
+            const float a0 = __ldg(&pr->a[0]), a1 = __ldg(&pr->a[1]), a2 = __ldg(&pr->a[2]);
+            const float b0 = __ldg(&pr->b[0]) - a0, b1 = __ldg(&pr->b[1]) - a1, b2 = __ldg(&pr->b[2]) - a2;
+            ms.caps[i][0] = a0;
+            ms.caps[i][1] = a1;
+            ms.caps[i][2] = a2;
+            ms.caps[i][3] = b0;
+            ms.caps[i][4] = b1;
+            ms.caps[i][5] = b2;
+            ms.caps[i][6] = b0 * b0 + b1 * b1 + b2 * b2;
+            ms.caps[i][7] = __ldg(&pr->radius);
+        }
+        if (i == 0) {
+            bool all = np <= 16;
+            for (int k = 0; k < np && all; ++k)
+                all = __ldg(&P.f.fscene->prims[k].kind) == ICG_PRIM_CAPSULE && !__ldg(&P.f.fscene->prims[k].rotated);
+            ms.ncaps = all ? np : -1;
+        }
+    }
+    if (warp == 1) ptx::tmem_alloc2<512>(&ms.tmem_base);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = ms.tmem_base;
+    job_account(job);
+
+    const uint32_t full0 = ptx::mapa(ptx::smem_u32(&ms.full[0]), 0);
+    const uint32_t a_ready0 = ptx::mapa(ptx::smem_u32(&ms.a_ready[0]), 0);
+    const uint32_t tm_free0 = ptx::mapa(ptx::smem_u32(&ms.tm_free), 0);
+    const uint16_t both = 0x3;
+
+    if (warp == 0) {
+        // ===================== weight producer (both CTAs) =====================
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t ring0 = ptx::smem_u32(ring);
+            for (unsigned t = pair_id; t < ntiles; t += npairs) {
+                for (int i = 0; i < kItems; ++i) {
+                    ptx::mbar_wait(&ms.empty[s], ph ^ 1);
+                    if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kStage);
+                    const int row0 = ((int)rank * kItems + i) * 256;  // stream [rank][item][hi, lo]
+                    ptx::tma_load_2d_2sm(ring0 + s * kStage, &tmapW, full0 + s * 8, 0, row0);
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader only) =====================
+        if (leader && lane == 0) {
+            const uint32_t idesc = ptx::idesc_bf16_f32(256, 256);
+            const uint32_t ring0 = ptx::smem_u32(ring), a0 = ptx::smem_u32(abuf);
+            int s = 0;
+            uint32_t ph = 0;
+            uint32_t ac = 0;  // activation chunks consumed
+            uint32_t tfph = 0;
+            auto wait_chunk = [&](uint32_t c) {
+                ptx::mbar_wait_cluster(&ms.a_ready[c % kA], (c / kA) & 1u);
+                ptx::tc_fence_after();
+            };
+            // one weight item (4 K steps) against activation chunk c into D columns dcol
+            auto item = [&](uint32_t c, uint32_t dcol, bool first) {
+                ptx::mbar_wait(&ms.full[s], ph);
+                ptx::tc_fence_after();
+                const uint32_t ab = a0 + (c % kA) * kAChunk;
+                const uint64_t ah = ptx::sdesc_sw128(ab), al = ptx::sdesc_sw128(ab + kHalf);
+                const uint64_t bh = ptx::sdesc_sw128(ring0 + s * kStage), bl = ptx::sdesc_sw128(ring0 + s * kStage + kHalf);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t ko = (uint64_t)(kk * 2);
+                    ptx::mma_bf16_pair(tmem + dcol, ah + ko, bh + ko, idesc, (first && kk == 0) ? 0u : 1u);
+                    ptx::mma_bf16_pair(tmem + dcol, ah + ko, bl + ko, idesc, 1u);
+                    ptx::mma_bf16_pair(tmem + dcol, al + ko, bh + ko, idesc, 1u);
+                }
+                ptx::mma_commit_pair(&ms.empty[s], both);
+                if (++s == kStages) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            };
+            for (unsigned t = pair_id; t < ntiles; t += npairs) {
+                if (t != pair_id) {  // the previous tile's final layer has read D4 (and h3 read D3)
+                    ptx::mbar_wait_cluster(&ms.tm_free, tfph);
+                    tfph ^= 1;
+                    ptx::tc_fence_after();
+                }
+                // layer 2: 16 h1 chunks x 2 feature halves into D2 (columns 0-511)
+                for (int kc = 0; kc < 16; ++kc) {
+                    wait_chunk(ac);
+                    item(ac, 0, kc == 0);
+                    item(ac, 256, kc == 0);
+                    ptx::mma_commit_pair(&ms.a_free[ac % kA], both);
+                    ++ac;
+                }
+                ptx::mma_commit_pair(&ms.d2done, both);
+                // layer 3 into D3 = columns 0-255: its first MMA needs h2 chunks 0-3 (D2 columns
+                // 0-255) read, i.e. all four of them emitted
+                for (uint32_t c = ac; c < ac + 4; ++c) wait_chunk(c);
+                for (int kc = 0; kc < 8; ++kc) {
+                    if (kc >= 4) wait_chunk(ac);
+                    item(ac, 0, kc == 0);
+                    ptx::mma_commit_pair(&ms.a_free[ac % kA], both);
+                    ++ac;
+                }
+                ptx::mma_commit_pair(&ms.d3done, both);
+                // layer 4 into D4 = columns 256-511 (D2's upper half was read as h2 chunks 4-7)
+                for (int kc = 0; kc < 4; ++kc) {
+                    wait_chunk(ac);
+                    item(ac, 256, kc == 0);
+                    ptx::mma_commit_pair(&ms.a_free[ac % kA], both);
+                    ++ac;
+                }
+                ptx::mma_commit_pair(&ms.d4done, both);
+            }
+        }
+    } else {
+        // ===================== epilogue: thread = (point row, column half) =====================
+        const int et = threadIdx.x - 64;
+        const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int row = quarter * 32 + lane;  // this CTA's point = TMEM lane
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t arow = ptx::smem_u32(abuf) + (uint32_t)row * 128u;
+        const uint32_t sw = (uint32_t)row & 7u;
+        auto epi_bar = [] { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); };
+        const float* b1 = P.bias;
+        const float* b2 = b1 + 2 * 1024;
+        const float* b3 = b2 + 2 * 512;
+        const float* b4 = b3 + 2 * 256;
+        const float* b5 = b4 + 2 * 128;
+        const float w5z = __ldg(&P.wlast[128 + kGeoSkip - 1]);
+        uint32_t ac = 0, d2ph = 0, d3ph = 0, d4ph = 0;
+        // 32 activations of this thread (features f0 .. f0+31 of chunk c) -> chunk slot, hi and lo
+        auto store_chunk = [&](const float* v) {
+            const uint32_t base = arow + (ac % kA) * kAChunk;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint4 hv, lv;
+                uint32_t* hp = reinterpret_cast<uint32_t*>(&hv);
+                uint32_t* lp = reinterpret_cast<uint32_t*>(&lv);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float a = v[8 * j + 2 * i], b = v[8 * j + 2 * i + 1];
+                    hp[i] = pack_bf16(a, b);
+                    lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                }
+                const uint32_t off = ((((uint32_t)(half * 4 + j)) ^ sw) << 4);
+                ptx::st_shared_v4(base + off, hv);
+                ptx::st_shared_v4(base + kHalf + off, lv);
+            }
+        };
+        auto begin_chunk = [&]() { ptx::mbar_wait(&ms.a_free[ac % kA], ((ac / kA) & 1u) ^ 1u); };
+        auto end_chunk = [&]() {
+            ptx::fence_proxy_async_smem();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(a_ready0 + 8u * (ac % kA));
+            ++ac;
+        };
+        auto wait_d = [&](uint64_t* bar, uint32_t& par) {
+            ptx::mbar_wait(bar, par);
+            par ^= 1;
+            ptx::tc_fence_after();
+        };
+        for (unsigned t = pair_id; t < ntiles; t += npairs) {
+            const unsigned idx = t * NP + rank * NPC + (unsigned)row;
+            const bool valid = idx < n;
+            // ---- the tile's points: record slot, z, final-layer constant (half 0 threads) ----
+            if (half == 0) {
+                double pd[3] = {0.0, 0.0, 0.0};
+                int sl = 0;
+                if (valid) {
+                    job_point_d(job, idx, pd);
+                    const uint32_t n1 = (uint32_t)job.cells + 1u, col = job_node(job, idx) % (n1 * n1);
+                    sl = P.cmap ? __ldg(&P.cmap[col]) : (int)col;
+                }
+                const float p3[3] = {(float)pd[0], (float)pd[1], (float)pd[2]};
+                float d = 3.0e38f;
+                const int nc = ms.ncaps;
+                if (nc >= 0) {
+                    for (int i = 0; i < nc; ++i) {
+                        const float* c = ms.caps[i];
+                        const float pa0 = p3[0] - c[0], pa1 = p3[1] - c[1], pa2 = p3[2] - c[2];
+                        float hh = 0.0f;
+                        if (c[6] > 0.0f) hh = fminf(fmaxf((pa0 * c[3] + pa1 * c[4] + pa2 * c[5]) / c[6], 0.0f), 1.0f);
+                        const float v0 = pa0 - hh * c[3], v1 = pa1 - hh * c[4], v2 = pa2 - hh * c[5];
+                        d = fminf(d, sqrtf(v0 * v0 + v1 * v1 + v2 * v2) - c[7]);
+                    }
+                    if (nc == 0) d = 0.0f;
+                } else {
+                    d = scene_sdf_f(P.f.fscene, p3);
+                }
+                ms.slot[row] = sl;
+                ms.z[row] = p3[2];
+                ms.cterm[row] = __ldg(&b5[0]) + w5z * p3[2] - __ldg(&P.f.fscene->sdf_scale) * d;
+                ms.sfinal[row] = __ldg(&P.s_in[(size_t)sl * kSRow + kSFinal]);
+            }
+            epi_bar();
+            const float z = ms.z[row];
+            const float* rec = P.s_in + (size_t)ms.slot[row] * kSRow;
+            // ---- layer 1 (no MMA): 16 chunks of act(S1 + w1z z + b1) ----
+            for (int kc = 0; kc < 16; ++kc) {
+                const int f0 = kc * 64 + half * 32;
+                float v[32];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 s4 = __ldg(reinterpret_cast<const float4*>(rec + f0) + q);
+                    v[4 * q + 0] = s4.x;
+                    v[4 * q + 1] = s4.y;
+                    v[4 * q + 2] = s4.z;
+                    v[4 * q + 3] = s4.w;
+                }
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const float x = v[q] + fmaf(__ldg(&b1[1024 + f0 + q]), z, __ldg(&b1[f0 + q]));
+                    v[q] = x < 0.0f ? x * P.slope : x;
+                }
+                begin_chunk();
+                store_chunk(v);
+                end_chunk();
+            }
+            // ---- hidden layers 2, 3: drain D into the next layer's chunks ----
+            auto drain = [&](int nchunks, uint32_t col0, const float* bl, int od, int soff) {
+                for (int c = 0; c < nchunks; ++c) {
+                    const int f0 = c * 64 + half * 32;
+                    uint32_t r[32];
+                    ptx::tmem_ld32(lane_base + col0 + (uint32_t)f0, r);
+                    float v[32];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 s4 = __ldg(reinterpret_cast<const float4*>(rec + soff + f0) + q);
+                        v[4 * q + 0] = s4.x;
+                        v[4 * q + 1] = s4.y;
+                        v[4 * q + 2] = s4.z;
+                        v[4 * q + 3] = s4.w;
+                    }
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const float x = (__uint_as_float(r[q]) + v[q]) + fmaf(__ldg(&bl[od + f0 + q]), z, __ldg(&bl[f0 + q]));
+                        v[q] = x < 0.0f ? x * P.slope : x;
+                    }
+                    begin_chunk();
+                    store_chunk(v);
+                    end_chunk();
+                }
+            };
+            wait_d(&ms.d2done, d2ph);
+            drain(8, 0, b2, 512, 1024);
+            wait_d(&ms.d3done, d3ph);
+            drain(4, 0, b3, 256, 1536);
+            // ---- layer 4 + output: this thread's 64 of the 128 layer-4 features, dot with w5 ----
+            wait_d(&ms.d4done, d4ph);
+            float part = 0.0f;
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+                const int f0 = half * 64 + c * 32;
+                uint32_t r[32];
+                ptx::tmem_ld32(lane_base + 256u + (uint32_t)f0, r);
+                float v[32];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 s4 = __ldg(reinterpret_cast<const float4*>(rec + 1792 + f0) + q);
+                    v[4 * q + 0] = s4.x;
+                    v[4 * q + 1] = s4.y;
+                    v[4 * q + 2] = s4.z;
+                    v[4 * q + 3] = s4.w;
+                }
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const float x = (__uint_as_float(r[q]) + v[q]) + fmaf(__ldg(&b4[128 + f0 + q]), z, __ldg(&b4[f0 + q]));
+                    const float h = x < 0.0f ? x * P.slope : x;
+                    part = fmaf(__ldg(&P.wlast[f0 + q]), h, part);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(tm_free0);  // D3 / D4 are free for the next tile
+            if (half == 1) ms.red[row] = part;
+            epi_bar();
+            if (half == 0 && valid) {
+                const float s = part + ms.red[row] + ms.sfinal[row] + ms.cterm[row];
+                const float v = 1.0f / (1.0f + expf(-s));
+                if (job_is_grid(job))
+                    grid_epilogue(job, job_node(job, idx), v);
+                else
+                    job.out[idx] = v;
+            }
+            epi_bar();
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc2<512>(tmem);
+    }
+}
+
+}  // namespace fact2
+
+int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job, const float* records,
+                      const int* cmap, unsigned max_points, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        ICG_CUDA_TRY(cudaFuncSetAttribute(fact2::k_fact2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fact2::kTotal));
+        attr = true;
+    }
+    fact2::Params p{};
+    p.f = f;
+    p.job = job;
+    p.bias = geo.bias;
+    p.wlast = geo.w_last;
+    p.s_in = records;
+    p.cmap = cmap;
+    p.slope = 0.02f;
+    unsigned pairs = (max_points + fact2::NP - 1) / fact2::NP;
+    if (pairs > 74) pairs = 74;
+    if (pairs == 0) pairs = 1;
+    CUtensorMap tm;
+    std::memcpy(&tm, tmap, sizeof(CUtensorMap));
+    fact2::k_fact2<<<2 * pairs, fact2::kThreads, fact2::kTotal, s>>>(tm, p);
+    if (const cudaError_t e = cudaGetLastError()) {
+        set_error(std::string("k_fact2: ") + cudaGetErrorString(e));
+        return ICG_ERUNTIME;
+    }
+    return ICG_OK;
+}
+
+}  // namespace icg

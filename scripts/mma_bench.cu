@@ -107,6 +107,7 @@ int main() {
     run<64, false, 16>("cta1 M128 N64  x16/commit");
     run<128, false, 16>("cta1 M128 N128 x16/commit");
     run<256, false, 16>("cta1 M128 N256 x16/commit");
+    run<32, true, 16>("pair M256 N32  x16/commit");
     run<64, true, 16>("pair M256 N64  x16/commit");
     run<128, true, 4>("pair M256 N128 x4/commit");
     run<128, true, 16>("pair M256 N128 x16/commit");
