@@ -400,7 +400,8 @@ def main():
         pass
     roofline = {"bound": "tensor",
                 "kernel": "geometry field, bulk batches (dense level 0 + each level's E0 list): column pass "
-                          "k_mlp_pair<COLS> + factored pass k_mlp_pair<FACT> (CTA-pair tcgen05), incl. list sorting",
+                          "k_mlp_pair<COLS> + factored pass k_fact2 (CTA-pair tcgen05, M = 256 points x N = 256 "
+                          "features), incl. list sorting",
                 "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
                 "traffic": traffic, "traffic_note": traffic_note,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" + (" (fallback)" if pk.get("fallback") else ""),

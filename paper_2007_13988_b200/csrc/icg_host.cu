@@ -104,6 +104,7 @@ struct icg_context {
     // column-factored geometry field (FACT / COLS streams, [part][x3 ? 0 : 1])
     DBuf geo_fact_stream[2][2];
     alignas(64) unsigned char geo_fact_tmap[2][2][128] = {};
+    alignas(64) unsigned char geo_fact2_tmap[128] = {};  // the FACT x3 stream in 16 KB (hi / lo) boxes
     bool geo_fact = false, use_fact = true;
     bool fact_used = false;  // the last extraction ran its bulk batches column-factored
     DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
@@ -398,7 +399,7 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
                                       xi == 0, c->stream))
         return r;
     int r = (c->use_fact2 && xi == 0)
-                ? launch_pifu_fact2(fd, c->geo_tc, c->geo_fact_tmap[0][0], pj, c->colrec.as<float>(), cm, max_points,
+                ? launch_pifu_fact2(fd, c->geo_tc, c->geo_fact2_tmap, pj, c->colrec.as<float>(), cm, max_points,
                                     c->stream)
                 : launch_pifu_pair_fact(fd, c->geo_tc, c->geo_fact_tmap[0][xi], pj, c->colrec.as<float>(), cm,
                                         max_points, xi == 0, c->stream);
@@ -1120,6 +1121,8 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
             ICG_CUDA_TRY(cudaMemcpy(c->geo_fact_stream[part][1].p, sh.data(), bh, cudaMemcpyHostToDevice));
             if (int r = pair_make_tmap(c->geo_fact_stream[part][0].p, bx, c->geo_fact_tmap[part][0])) return r;
             if (int r = pair_make_tmap(c->geo_fact_stream[part][1].p, bh, c->geo_fact_tmap[part][1])) return r;
+            if (part == 0)
+                if (int r = pair_make_tmap(c->geo_fact_stream[0][0].p, bx, c->geo_fact2_tmap, 128)) return r;
         }
         c->geo_fact = true;
     }

@@ -159,7 +159,7 @@ int launch_pifu_tc_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex
 size_t pair_stream_bytes(int which, bool x3);
 // f16skip: skip-input items as fp16 hi/lo (the texture kernel's streams, geometry prefix included)
 int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi, bool f16skip = false);
-int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out);
+int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out, unsigned box_rows = 256);
 // column-factored geometry field (k_mlp_pair.cu, modes COLS / FACT): part 0 = FACT stream
 // (hidden-input items of layers 2-4), part 1 = COLS stream (Phi items of layers 1-4)
 constexpr int kColRecord = 1936;  // floats per column record

@@ -39,11 +39,16 @@ namespace icg {
 namespace fact2 {
 
 constexpr uint32_t kHalf = 16384;                   // 128 x 64 bf16 tile
-constexpr uint32_t kStage = 32768;                  // weight item: (hi, lo) of 128 rows x 64 K
-constexpr int kStages = 2;                          // weight ring
+constexpr uint32_t kStage = 16384;                  // half a weight item: hi or lo of 128 rows x 64 K
+constexpr int kStages = 5;                          // weight ring (80 KB in flight)
 constexpr int kA = 4;                               // activation chunk ring
 constexpr uint32_t kAChunk = 32768;                 // 128 points x 64 K, hi then lo
-constexpr int kEpiWarps = 8;                        // 4 TMEM lane quarters x 2 column halves
+#ifndef FACT2_CQ
+#define FACT2_CQ 4
+#endif
+constexpr int kCQ = FACT2_CQ;                       // column groups per TMEM lane quarter
+constexpr int kFW = 64 / kCQ;                       // features per thread of a 64-feature chunk
+constexpr int kEpiWarps = 4 * kCQ;                  // 4 TMEM lane quarters x kCQ column groups
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;
 constexpr int NPC = 128;                            // points per CTA
@@ -54,7 +59,7 @@ constexpr int kItems = 44;                          // FACT stream: L2 (kc, m) 3
 constexpr uint32_t kOffRing = 0;
 constexpr uint32_t kOffA = kOffRing + kStages * kStage;
 constexpr uint32_t kOffMisc = kOffA + kA * kAChunk;
-constexpr uint32_t kMisc = 8192;
+constexpr uint32_t kMisc = 12288;
 constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
 static_assert(kTotal <= 232448, "shared memory");
 
@@ -65,9 +70,11 @@ struct Misc {
     uint32_t tmem_base;
     int ncaps;
     float caps[16][8];
-    int slot[NPC];
-    float z[NPC], cterm[NPC], sfinal[NPC];
-    float red[NPC];
+    float dmin[2][kCQ][NPC];  // capsule distance, split over the column groups (tile parity)
+    float ppos[2][NPC][3];  // the tile's point positions (tile parity)
+    int pslot[2][NPC];
+    float sfinal[2][NPC];   // the record's output-layer term (tile parity)
+    float red[kCQ][NPC];
 };
 static_assert(sizeof(Misc) <= kMisc, "misc");
 
@@ -79,7 +86,14 @@ struct Params {
     const float* s_in;   // column records
     const int* cmap;     // column -> record
     float slope;
+    unsigned long long* trace;  // optional wait accounting of CTA 0 (ICG_TC_TRACE=1)
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -164,10 +178,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t ph = 0;
             const uint32_t ring0 = ptx::smem_u32(ring);
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
-                for (int i = 0; i < kItems; ++i) {
+                for (int i = 0; i < 2 * kItems; ++i) {  // stream [rank][item][hi, lo], 128 rows each
                     ptx::mbar_wait(&ms.empty[s], ph ^ 1);
                     if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kStage);
-                    const int row0 = ((int)rank * kItems + i) * 256;  // stream [rank][item][hi, lo]
+                    const int row0 = ((int)rank * kItems) * 256 + i * 128;
                     ptx::tma_load_2d_2sm(ring0 + s * kStage, &tmapW, full0 + s * 8, 0, row0);
                     if (++s == kStages) {
                         s = 0;
@@ -185,33 +199,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t ph = 0;
             uint32_t ac = 0;  // activation chunks consumed
             uint32_t tfph = 0;
+            const bool tr = P.trace && blockIdx.x == 0;
+            unsigned long long w_chunk = 0, w_full = 0, w_tm = 0, t_begin = gtime();
             auto wait_chunk = [&](uint32_t c) {
+                const unsigned long long t0 = tr ? gtime() : 0;
                 ptx::mbar_wait_cluster(&ms.a_ready[c % kA], (c / kA) & 1u);
+                if (tr) w_chunk += gtime() - t0;
                 ptx::tc_fence_after();
             };
             // one weight item (4 K steps) against activation chunk c into D columns dcol
-            auto item = [&](uint32_t c, uint32_t dcol, bool first) {
-                ptx::mbar_wait(&ms.full[s], ph);
-                ptx::tc_fence_after();
-                const uint32_t ab = a0 + (c % kA) * kAChunk;
-                const uint64_t ah = ptx::sdesc_sw128(ab), al = ptx::sdesc_sw128(ab + kHalf);
-                const uint64_t bh = ptx::sdesc_sw128(ring0 + s * kStage), bl = ptx::sdesc_sw128(ring0 + s * kStage + kHalf);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t ko = (uint64_t)(kk * 2);
-                    ptx::mma_bf16_pair(tmem + dcol, ah + ko, bh + ko, idesc, (first && kk == 0) ? 0u : 1u);
-                    ptx::mma_bf16_pair(tmem + dcol, ah + ko, bl + ko, idesc, 1u);
-                    ptx::mma_bf16_pair(tmem + dcol, al + ko, bh + ko, idesc, 1u);
-                }
+            auto next_stage = [&]() {
                 ptx::mma_commit_pair(&ms.empty[s], both);
                 if (++s == kStages) {
                     s = 0;
                     ph ^= 1;
                 }
             };
+            auto wait_stage = [&]() {
+                const unsigned long long t0 = tr ? gtime() : 0;
+                ptx::mbar_wait(&ms.full[s], ph);
+                if (tr) w_full += gtime() - t0;
+                ptx::tc_fence_after();
+            };
+            // one weight item (4 K steps) against activation chunk c into D columns dcol: the weights'
+            // hi stage (x act hi, x act lo), then their lo stage (x act hi)
+            auto item = [&](uint32_t c, uint32_t dcol, bool first) {
+                const uint32_t ab = a0 + (c % kA) * kAChunk;
+                const uint64_t ah = ptx::sdesc_sw128(ab), al = ptx::sdesc_sw128(ab + kHalf);
+                wait_stage();
+                const uint64_t bh = ptx::sdesc_sw128(ring0 + s * kStage);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t ko = (uint64_t)(kk * 2);
+                    ptx::mma_bf16_pair(tmem + dcol, ah + ko, bh + ko, idesc, (first && kk == 0) ? 0u : 1u);
+                    ptx::mma_bf16_pair(tmem + dcol, al + ko, bh + ko, idesc, 1u);
+                }
+                next_stage();
+                wait_stage();
+                const uint64_t bl = ptx::sdesc_sw128(ring0 + s * kStage);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t ko = (uint64_t)(kk * 2);
+                    ptx::mma_bf16_pair(tmem + dcol, ah + ko, bl + ko, idesc, 1u);
+                }
+                next_stage();
+            };
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
                 if (t != pair_id) {  // the previous tile's final layer has read D4 (and h3 read D3)
+                    const unsigned long long t0 = tr ? gtime() : 0;
                     ptx::mbar_wait_cluster(&ms.tm_free, tfph);
+                    if (tr) w_tm += gtime() - t0;
                     tfph ^= 1;
                     ptx::tc_fence_after();
                 }
@@ -243,12 +280,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 ptx::mma_commit_pair(&ms.d4done, both);
             }
+            if (tr) {
+                P.trace[0] = gtime() - t_begin;
+                P.trace[1] = w_chunk;
+                P.trace[2] = w_full;
+                P.trace[3] = w_tm;
+            }
         }
     } else {
-        // ===================== epilogue: thread = (point row, column half) =====================
+        // ===================== epilogue: thread = (point row, column group) =====================
         const int et = threadIdx.x - 64;
         const int quarter = warp & 3;
-        const int half = (warp - 2) >> 2;
+        const int cq = (warp - 2) >> 2;  // column group
         const int row = quarter * 32 + lane;  // this CTA's point = TMEM lane
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const uint32_t arow = ptx::smem_u32(abuf) + (uint32_t)row * 128u;
@@ -261,11 +304,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float* b5 = b4 + 2 * 128;
         const float w5z = __ldg(&P.wlast[128 + kGeoSkip - 1]);
         uint32_t ac = 0, d2ph = 0, d3ph = 0, d4ph = 0;
-        // 32 activations of this thread (features f0 .. f0+31 of chunk c) -> chunk slot, hi and lo
-        auto store_chunk = [&](const float* v) {
-            const uint32_t base = arow + (ac % kA) * kAChunk;
+        const bool etr = P.trace && blockIdx.x == 0 && et == 0;
+        unsigned long long e_free = 0, e_d = 0, e_prep = 0, e_h1 = 0, e_fin = 0, e_begin = gtime();
+        // kFW activations of this thread (features cq kFW .. of the chunk) -> chunk slot, hi and lo
+        auto store_chunk = [&](const float* v, uint32_t a) {
+            const uint32_t base = arow + (a % kA) * kAChunk;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < kFW / 8; ++j) {
                 uint4 hv, lv;
                 uint32_t* hp = reinterpret_cast<uint32_t*>(&hv);
                 uint32_t* lp = reinterpret_cast<uint32_t*>(&lv);
@@ -275,150 +320,226 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     hp[i] = pack_bf16(a, b);
                     lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
                 }
-                const uint32_t off = ((((uint32_t)(half * 4 + j)) ^ sw) << 4);
+                const uint32_t off = ((((uint32_t)(cq * (kFW / 8) + j)) ^ sw) << 4);
                 ptx::st_shared_v4(base + off, hv);
                 ptx::st_shared_v4(base + kHalf + off, lv);
             }
         };
-        auto begin_chunk = [&]() { ptx::mbar_wait(&ms.a_free[ac % kA], ((ac / kA) & 1u) ^ 1u); };
-        auto end_chunk = [&]() {
+        auto begin_chunk = [&](uint32_t a) {
+            const unsigned long long t0 = etr ? gtime() : 0;
+            ptx::mbar_wait(&ms.a_free[a % kA], ((a / kA) & 1u) ^ 1u);
+            if (etr) e_free += gtime() - t0;
+        };
+        // publish chunks ac .. ac+cnt-1: ONE proxy fence for all of this thread's stores (the fence
+        // waits for them to land, so it is paid per batch, not per chunk)
+        auto end_chunks = [&](int cnt) {
             ptx::fence_proxy_async_smem();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(a_ready0 + 8u * (ac % kA));
-            ++ac;
+            if (lane == 0)
+                for (int i = 0; i < cnt; ++i) ptx::mbar_arrive_cluster(a_ready0 + 8u * ((ac + i) % kA));
+            ac += cnt;
         };
         auto wait_d = [&](uint64_t* bar, uint32_t& par) {
+            const unsigned long long t0 = etr ? gtime() : 0;
             ptx::mbar_wait(bar, par);
+            if (etr) e_d += gtime() - t0;
             par ^= 1;
             ptx::tc_fence_after();
         };
-        for (unsigned t = pair_id; t < ntiles; t += npairs) {
-            const unsigned idx = t * NP + rank * NPC + (unsigned)row;
-            const bool valid = idx < n;
-            // ---- the tile's points: record slot, z, final-layer constant (half 0 threads) ----
-            if (half == 0) {
+        // kFW consecutive floats at p (16-byte aligned) into v as float4 loads
+        auto loadw = [](const float* p, float* v) {
+#pragma unroll
+            for (int q = 0; q < kFW / 4; ++q) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(p) + q);
+                v[4 * q + 0] = x.x;
+                v[4 * q + 1] = x.y;
+                v[4 * q + 2] = x.z;
+                v[4 * q + 3] = x.w;
+            }
+        };
+        // per-thread state of a tile's point (both column halves compute it; the capsule distance
+        // is split between them and combined by the final layer)
+        struct Pt {
+            const float* rec;
+            float z;
+            unsigned idx;
+            bool valid;
+        };
+        auto prep = [&](unsigned tg, int pb) {
+            Pt q;
+            q.idx = tg * NP + rank * NPC + (unsigned)row;
+            q.valid = q.idx < n;
+            if (cq == 0) {  // position (fp64 node -> NDC, as the reference) and record slot
                 double pd[3] = {0.0, 0.0, 0.0};
                 int sl = 0;
-                if (valid) {
-                    job_point_d(job, idx, pd);
-                    const uint32_t n1 = (uint32_t)job.cells + 1u, col = job_node(job, idx) % (n1 * n1);
+                if (q.valid) {
+                    job_point_d(job, q.idx, pd);
+                    const uint32_t n1 = (uint32_t)job.cells + 1u, col = job_node(job, q.idx) % (n1 * n1);
                     sl = P.cmap ? __ldg(&P.cmap[col]) : (int)col;
                 }
-                const float p3[3] = {(float)pd[0], (float)pd[1], (float)pd[2]};
-                float d = 3.0e38f;
-                const int nc = ms.ncaps;
-                if (nc >= 0) {
-                    for (int i = 0; i < nc; ++i) {
-                        const float* c = ms.caps[i];
-                        const float pa0 = p3[0] - c[0], pa1 = p3[1] - c[1], pa2 = p3[2] - c[2];
-                        float hh = 0.0f;
-                        if (c[6] > 0.0f) hh = fminf(fmaxf((pa0 * c[3] + pa1 * c[4] + pa2 * c[5]) / c[6], 0.0f), 1.0f);
-                        const float v0 = pa0 - hh * c[3], v1 = pa1 - hh * c[4], v2 = pa2 - hh * c[5];
-                        d = fminf(d, sqrtf(v0 * v0 + v1 * v1 + v2 * v2) - c[7]);
-                    }
-                    if (nc == 0) d = 0.0f;
-                } else {
-                    d = scene_sdf_f(P.f.fscene, p3);
-                }
-                ms.slot[row] = sl;
-                ms.z[row] = p3[2];
-                ms.cterm[row] = __ldg(&b5[0]) + w5z * p3[2] - __ldg(&P.f.fscene->sdf_scale) * d;
-                ms.sfinal[row] = __ldg(&P.s_in[(size_t)sl * kSRow + kSFinal]);
+                ms.ppos[pb][row][0] = (float)pd[0];
+                ms.ppos[pb][row][1] = (float)pd[1];
+                ms.ppos[pb][row][2] = (float)pd[2];
+                ms.pslot[pb][row] = sl;
+                ms.sfinal[pb][row] = __ldg(P.s_in + (size_t)sl * kSRow + kSFinal);
             }
             epi_bar();
-            const float z = ms.z[row];
-            const float* rec = P.s_in + (size_t)ms.slot[row] * kSRow;
-            // ---- layer 1 (no MMA): 16 chunks of act(S1 + w1z z + b1) ----
-            for (int kc = 0; kc < 16; ++kc) {
-                const int f0 = kc * 64 + half * 32;
-                float v[32];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 s4 = __ldg(reinterpret_cast<const float4*>(rec + f0) + q);
-                    v[4 * q + 0] = s4.x;
-                    v[4 * q + 1] = s4.y;
-                    v[4 * q + 2] = s4.z;
-                    v[4 * q + 3] = s4.w;
+            const float p3[3] = {ms.ppos[pb][row][0], ms.ppos[pb][row][1], ms.ppos[pb][row][2]};
+            const int sl = ms.pslot[pb][row];
+            float d = 3.0e38f;
+            const int nc = ms.ncaps;
+            if (nc >= 0) {
+                for (int i = cq; i < nc; i += kCQ) {
+                    const float* c = ms.caps[i];
+                    const float pa0 = p3[0] - c[0], pa1 = p3[1] - c[1], pa2 = p3[2] - c[2];
+                    float hh = 0.0f;
+                    if (c[6] > 0.0f) hh = fminf(fmaxf((pa0 * c[3] + pa1 * c[4] + pa2 * c[5]) / c[6], 0.0f), 1.0f);
+                    const float v0 = pa0 - hh * c[3], v1 = pa1 - hh * c[4], v2 = pa2 - hh * c[5];
+                    d = fminf(d, sqrtf(v0 * v0 + v1 * v1 + v2 * v2) - c[7]);
                 }
-#pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const float x = v[q] + fmaf(__ldg(&b1[1024 + f0 + q]), z, __ldg(&b1[f0 + q]));
-                    v[q] = x < 0.0f ? x * P.slope : x;
-                }
-                begin_chunk();
-                store_chunk(v);
-                end_chunk();
+                if (nc == 0) d = 0.0f;
+            } else if (cq == 0) {
+                d = scene_sdf_f(P.f.fscene, p3);
             }
-            // ---- hidden layers 2, 3: drain D into the next layer's chunks ----
-            auto drain = [&](int nchunks, uint32_t col0, const float* bl, int od, int soff) {
-                for (int c = 0; c < nchunks; ++c) {
-                    const int f0 = c * 64 + half * 32;
-                    uint32_t r[32];
-                    ptx::tmem_ld32(lane_base + col0 + (uint32_t)f0, r);
-                    float v[32];
+            ms.dmin[pb][cq][row] = d;
+            q.z = p3[2];
+            q.rec = P.s_in + (size_t)sl * kSRow;
+            return q;
+        };
+        // layer 1 (no MMA): chunks [c0, c1) of act(S1 + w1z z + b1)
+        // layer 1 in pairs of chunks [c0, c1) (c1 - c0 even)
+        auto emit_h1 = [&](const Pt& q, int c0, int c1) {
+            for (int kc = c0; kc < c1; kc += 2) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const float4 s4 = __ldg(reinterpret_cast<const float4*>(rec + soff + f0) + q);
-                        v[4 * q + 0] = s4.x;
-                        v[4 * q + 1] = s4.y;
-                        v[4 * q + 2] = s4.z;
-                        v[4 * q + 3] = s4.w;
-                    }
-                    ptx::tmem_ld_wait();
+                for (int u = 0; u < 2; ++u) {
+                    const int f0 = (kc + u) * 64 + cq * kFW;
+                    float v[kFW], bb[kFW], wz[kFW];
+                    loadw(q.rec + f0, v);
+                    loadw(b1 + f0, bb);
+                    loadw(b1 + 1024 + f0, wz);
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        const float x = (__uint_as_float(r[q]) + v[q]) + fmaf(__ldg(&bl[od + f0 + q]), z, __ldg(&bl[f0 + q]));
-                        v[q] = x < 0.0f ? x * P.slope : x;
+                    for (int i = 0; i < kFW; ++i) {
+                        const float x = v[i] + fmaf(wz[i], q.z, bb[i]);
+                        v[i] = x < 0.0f ? x * P.slope : x;
                     }
-                    begin_chunk();
-                    store_chunk(v);
-                    end_chunk();
+                    begin_chunk(ac + u);
+                    store_chunk(v, ac + u);
                 }
-            };
-            wait_d(&ms.d2done, d2ph);
-            drain(8, 0, b2, 512, 1024);
-            wait_d(&ms.d3done, d3ph);
-            drain(4, 0, b3, 256, 1536);
-            // ---- layer 4 + output: this thread's 64 of the 128 layer-4 features, dot with w5 ----
-            wait_d(&ms.d4done, d4ph);
-            float part = 0.0f;
+                end_chunks(2);
+            }
+        };
+        // hidden layers 2, 3: drain D (columns col0 + feature) into the next layer's chunks
+        auto drain = [&](const Pt& q, int nchunks, uint32_t col0, const float* bl, int od, int soff) {
+            for (int c2 = 0; c2 < nchunks; c2 += 2) {
 #pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
-                const int f0 = half * 64 + c * 32;
-                uint32_t r[32];
-                ptx::tmem_ld32(lane_base + 256u + (uint32_t)f0, r);
-                float v[32];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 s4 = __ldg(reinterpret_cast<const float4*>(rec + 1792 + f0) + q);
-                    v[4 * q + 0] = s4.x;
-                    v[4 * q + 1] = s4.y;
-                    v[4 * q + 2] = s4.z;
-                    v[4 * q + 3] = s4.w;
-                }
+              for (int u = 0; u < 2; ++u) {
+                const int c = c2 + u;
+                const int f0 = c * 64 + cq * kFW;
+                uint32_t r[kFW];
+                if constexpr (kFW == 32)
+                    ptx::tmem_ld32(lane_base + col0 + (uint32_t)f0, r);
+                else
+                    ptx::tmem_ld16(lane_base + col0 + (uint32_t)f0, r);
+                float v[kFW], bb[kFW], wz[kFW];
+                loadw(q.rec + soff + f0, v);
+                loadw(bl + f0, bb);
+                loadw(bl + od + f0, wz);
                 ptx::tmem_ld_wait();
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const float x = (__uint_as_float(r[q]) + v[q]) + fmaf(__ldg(&b4[128 + f0 + q]), z, __ldg(&b4[f0 + q]));
+                for (int i = 0; i < kFW; ++i) {
+                    const float x = (__uint_as_float(r[i]) + v[i]) + fmaf(wz[i], q.z, bb[i]);
+                    v[i] = x < 0.0f ? x * P.slope : x;
+                }
+                begin_chunk(ac + u);
+                store_chunk(v, ac + u);
+              }
+              end_chunks(2);
+            }
+        };
+        // layer 4 + output: this thread's 64 of the 128 layer-4 features, dot with w5
+        auto final_layer = [&](const Pt& q, int pb) {
+            float part = 0.0f;
+            constexpr int kFin = 128 / kCQ;  // layer-4 features of this thread
+#pragma unroll 1
+            for (int c = 0; c < kFin / kFW; ++c) {
+                const int f0 = cq * kFin + c * kFW;
+                uint32_t r[kFW];
+                if constexpr (kFW == 32)
+                    ptx::tmem_ld32(lane_base + 256u + (uint32_t)f0, r);
+                else
+                    ptx::tmem_ld16(lane_base + 256u + (uint32_t)f0, r);
+                float v[kFW], bb[kFW], wz[kFW];
+                loadw(q.rec + 1792 + f0, v);
+                loadw(b4 + f0, bb);
+                loadw(b4 + 128 + f0, wz);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < kFW; ++i) {
+                    const float x = (__uint_as_float(r[i]) + v[i]) + fmaf(wz[i], q.z, bb[i]);
                     const float h = x < 0.0f ? x * P.slope : x;
-                    part = fmaf(__ldg(&P.wlast[f0 + q]), h, part);
+                    part = fmaf(__ldg(&P.wlast[f0 + i]), h, part);
                 }
             }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(tm_free0);  // D3 / D4 are free for the next tile
-            if (half == 1) ms.red[row] = part;
+            ms.red[cq][row] = part;
             epi_bar();
-            if (half == 0 && valid) {
-                const float s = part + ms.red[row] + ms.sfinal[row] + ms.cterm[row];
+            if (cq == 0 && q.valid) {
+                float d = ms.dmin[pb][0][row], sum = part;
+#pragma unroll
+                for (int g = 1; g < kCQ; ++g) {
+                    d = fminf(d, ms.dmin[pb][g][row]);
+                    sum += ms.red[g][row];
+                }
+                const float cterm = __ldg(&b5[0]) + w5z * q.z - __ldg(&P.f.fscene->sdf_scale) * d;
+                const float s = sum + ms.sfinal[pb][row] + cterm;
                 const float v = 1.0f / (1.0f + expf(-s));
                 if (job_is_grid(job))
-                    grid_epilogue(job, job_node(job, idx), v);
+                    grid_epilogue(job, job_node(job, q.idx), v);
                 else
-                    job.out[idx] = v;
+                    job.out[q.idx] = v;
             }
             epi_bar();
+        };
+        // Per tile t: h1(t) 4-15, prep(t+1), h2(t), h3(t), h1(t+1) 0-3, final(t): the next tile's first
+        // layer-1 chunks are ready when its layer 2 may start (after final(t) has read D4).
+        int pb = 0;
+        unsigned long long tq = etr ? gtime() : 0;
+        Pt cur = prep(pair_id, 0);
+        if (etr) e_prep += gtime() - tq;
+        emit_h1(cur, 0, 4);
+        for (unsigned t = pair_id; t < ntiles; t += npairs) {
+            const bool has_next = t + npairs < ntiles;
+            tq = etr ? gtime() : 0;
+            emit_h1(cur, 4, 16);
+            if (etr) e_h1 += gtime() - tq;
+            Pt nxt = cur;
+            tq = etr ? gtime() : 0;
+            if (has_next) nxt = prep(t + npairs, pb ^ 1);
+            if (etr) e_prep += gtime() - tq;
+            wait_d(&ms.d2done, d2ph);
+            drain(cur, 8, 0, b2, 512, 1024);
+            wait_d(&ms.d3done, d3ph);
+            drain(cur, 4, 0, b3, 256, 1536);
+            tq = etr ? gtime() : 0;
+            if (has_next) emit_h1(nxt, 0, 4);
+            if (etr) e_h1 += gtime() - tq;
+            wait_d(&ms.d4done, d4ph);
+            tq = etr ? gtime() : 0;
+            final_layer(cur, pb);
+            if (etr) e_fin += gtime() - tq;
+            cur = nxt;
+            pb ^= 1;
+        }
+        if (etr) {
+            P.trace[4] = gtime() - e_begin;
+            P.trace[5] = e_free;
+            P.trace[6] = e_d;
+            P.trace[7] = e_prep;
+            P.trace[8] = e_h1;
+            P.trace[9] = e_fin;
         }
     }
     ptx::tc_fence_before();
@@ -451,10 +572,28 @@ int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, con
     if (pairs == 0) pairs = 1;
     CUtensorMap tm;
     std::memcpy(&tm, tmap, sizeof(CUtensorMap));
+    static unsigned long long* trace = nullptr;
+    static int tron = -1;
+    if (tron < 0) {
+        const char* e = getenv("ICG_TC_TRACE");
+        tron = e && e[0] == '1';
+        if (tron) cudaMallocManaged(&trace, 64 * sizeof(unsigned long long));
+    }
+    p.trace = tron ? trace : nullptr;
+    if (p.trace) cudaMemsetAsync(p.trace, 0, 64 * 8, s);
     fact2::k_fact2<<<2 * pairs, fact2::kThreads, fact2::kTotal, s>>>(tm, p);
     if (const cudaError_t e = cudaGetLastError()) {
         set_error(std::string("k_fact2: ") + cudaGetErrorString(e));
         return ICG_ERUNTIME;
+    }
+    if (p.trace) {
+        cudaStreamSynchronize(s);
+        const unsigned long long* t = p.trace;
+        fprintf(stderr,
+                "[fact2-trace] mma: total %.1f us, wait chunk %.1f, wait weights %.1f, wait tmem %.1f | epi: total %.1f, "
+                "wait slot %.1f, wait acc %.1f, prep %.1f, h1 %.1f, final %.1f\n",
+                t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3, t[6] * 1e-3, t[7] * 1e-3,
+                t[8] * 1e-3, t[9] * 1e-3);
     }
     return ICG_OK;
 }

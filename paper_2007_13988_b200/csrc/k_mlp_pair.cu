@@ -1548,7 +1548,7 @@ int pair_pack_factored(const float* const* w, int part, uint8_t* stream_x3, uint
     return pair_pack_sched(ICG_MLP_GEOMETRY, part == 0 ? 1 : 2, w, stream_x3, stream_hi);
 }
 
-int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-byte CUtensorMap */) {
+int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-byte CUtensorMap */, unsigned box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -1562,7 +1562,7 @@ int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-b
     }
     cuuint64_t dims[2] = {128, (cuuint64_t)(bytes / 128)};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {128, 256};  // one 32 KB stage
+    cuuint32_t box[2] = {128, box_rows};  // one stage: 256 rows = 32 KB (hi + lo of an item)
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
                         const_cast<void*>(dev_stream), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
