@@ -113,6 +113,7 @@ struct icg_context {
     bool use_xext = true;  // ICG_NO_XEXT=1: rays along grid x walk every sample
     bool use_tail = true;
     bool chain_trace = false;  // ICG_CHAIN_TRACE=1
+    bool chain_fact = true;    // large conflict-loop batches column-factored (ICG_CHAIN_FACT=0: CTA-pair GEO)
     bool use_fact2 = true;     // bulk factored pass with swapped operands (k_fact2.cu); ICG_FACT2=0: k_mlp_pair<FACT>
     bool tail_wide = true;  // this frame is alone on its device: the tail kernel takes every SM
     unsigned tail_max = 128;  // conflict batches up to this size start the persistent tail kernel
@@ -408,6 +409,37 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
     return r;
 }
 
+// A large conflict-loop batch (size class 1) through the column-factored kernels: the level's
+// column records persist from its E0 pass, so only columns the batch adds are claimed and
+// recorded (COLS over the record window [ncols_base, ncols)), then the batch is sorted by record
+// and evaluated by k_fact2.  Every launch is sized by device counts; the claim and k_fact2 exit on
+// device unless the batch is their class (job.min_count).
+int run_chain_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
+    const size_t n1 = (size_t)job.cells + 1, plane = n1 * n1;
+    DevCounters* ctr = c->ctr.as<DevCounters>();
+    if (int r = launch_col_claim(job.list, job.count, job.cells, c->cmap.as<int>(), c->collist.as<uint32_t>(), ctr,
+                                 max_points, c->stream, job.min_count))
+        return r;
+    if (int r = launch_sort_by_column(job.list, job.count, job.cells, c->cmap.as<int>(), c->colcnt.as<uint32_t>(), ctr,
+                                      c->sorted.as<uint32_t>(), max_points, c->stream, job.min_count))
+        return r;
+    EvalJob cj{};
+    cj.cells = job.cells;
+    cj.list = c->collist.as<uint32_t>();
+    cj.count = &ctr->ncols;
+    cj.base = &ctr->ncols_base;
+    const unsigned max_cols = (unsigned)std::min<size_t>(plane, max_points);
+    if (int r = launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][0], cj, c->colrec.as<float>(), max_cols, true,
+                                      c->stream))
+        return r;
+    EvalJob pj = job;
+    pj.list = c->sorted.as<uint32_t>();
+    int r = launch_pifu_fact2(fd, c->geo_tc, c->geo_fact2_tmap, pj, c->colrec.as<float>(), c->cmap.as<int>(), max_points,
+                              c->stream);
+    c->launches += 6;
+    return r;
+}
+
 // `dependent_chain`: the batch is one link of the serial conflict loop, usually
 // small; it is routed on device between the tensor-core kernel and the
 // layer-parallel latency path by its size.
@@ -588,14 +620,17 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
             // device by the next expansion) and the frame is replayed with all of them
             const bool chain_pred = fact_ok(c, fd) && c->use_tail && c->geo_pair;
             const unsigned mid_max = 74u * 64u;
+            // batches beyond one wave of 128-point pair tiles: column-factored (k_fact2, 256-point tiles)
+            const bool x3c = fd.precision == ICG_PREC_FP32;
+            const unsigned big_max = (c->chain_fact && c->use_fact2 && x3c) ? 74u * 128u : 0u;
             int prev_mask = -1;
             for (int it = 0; it < unroll; ++it) {
                 int p = it & 1;
                 const int pm =
-                    (chain_pred && c->pred_valid[l] && !c->pred_all[l] && it < kPredIters) ? c->pred[l][it] : 7;
+                    (chain_pred && c->pred_valid[l] && !c->pred_all[l] && it < kPredIters) ? c->pred[l][it] : 15;
                 {
                     int slot = prof_begin(c, 2);
-                    ChainClasses cc{c->tail_max, mid_max, l, chain_pred ? prev_mask : -1};
+                    ChainClasses cc{c->tail_max, mid_max, l, chain_pred ? prev_mask : -1, big_max};
                     int r = launch_conflict_expand_cls(c->queued.as<uint32_t>(), lb.fs, fcells,
                                                        c->cf[p].as<uint32_t>(), ctr, it, max_iters,
                                                        c->nx[p].as<uint32_t>(), (unsigned)nf, cc, c->stream);
@@ -622,15 +657,18 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                     // which finishes the level's chain (k_tail.cu)
                     // (mid-size batches: 64-point pair tiles, twice as many pairs busy per wave; the
                     // column-factored pass has a longer single-tile latency, so it is kept for bulk batches)
-                    EvalJob big = cj, mid = cj;
+                    EvalJob huge = cj, big = cj, mid = cj;
+                    huge.min_count = big_max + 1;
                     big.min_count = std::max(c->tail_max, mid_max) + 1;
+                    big.max_count = big_max;
                     mid.min_count = c->tail_max + 1;
                     mid.max_count = mid_max;
                     int slot = prof_begin(c, 5);
-                    const bool x3 = fd.precision == ICG_PREC_FP32;
+                    const bool x3 = x3c;
                     const void* tm = c->geo_pair_tmap[x3 ? 0 : 1];
                     int r = ICG_OK;
-                    if (pm & 1) {
+                    if ((pm & 8) && big_max) r = run_chain_fact(c, fd, huge, (unsigned)nf);
+                    if (!r && (pm & 1)) {
                         r = launch_pifu_pair_eval(fd, c->geo_tc, tm, big, (unsigned)nf, x3, c->stream);
                         c->launches += 1;
                     }
@@ -656,7 +694,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                 }
             }
             {
-                ChainClasses cc{c->tail_max, mid_max, l, chain_pred ? prev_mask : -1};
+                ChainClasses cc{c->tail_max, mid_max, l, chain_pred ? prev_mask : -1, big_max};
                 if (int r = launch_unroll_check_cls(ctr, unroll & 1, l, cc, chain_pred ? unroll - 1 : -1, c->stream))
                     return r;
             }
@@ -928,6 +966,7 @@ int icg_create(int device, icg_context** out) {
     if (const char* e = getenv("ICG_NO_GRAPH")) c->use_graph = !(e[0] == '1');
     if (getenv("ICG_TC_TRACE") || getenv("ICG_TAIL_TRACE")) c->use_graph = false;  // traces synchronise
     if (const char* e = getenv("ICG_FACT2")) c->use_fact2 = e[0] == '1';
+    if (const char* e = getenv("ICG_CHAIN_FACT")) c->chain_fact = e[0] == '1';
     if (const char* e = getenv("ICG_NO_XEXT")) c->use_xext = !(e[0] == '1');
     if (getenv("ICG_CHAIN_TRACE")) {
         c->chain_trace = true;

@@ -45,6 +45,7 @@ struct DevCounters {
     unsigned long long refined[ICG_MAX_LEVELS];
     unsigned int conflict_iters[ICG_MAX_LEVELS];
     unsigned int ncols;               // column-factored field: distinct columns of the current batch
+    unsigned int ncols_base;          // ncols before the current conflict-loop batch claimed its columns
     unsigned int e0[ICG_MAX_LEVELS];  // size of each level's E0 list (the bulk batch)
     unsigned int tail_start[ICG_MAX_LEVELS];  // 1 + host iteration at which k_tail took over (0: never)
     // conflict-loop size classes (1: 128-point pair tiles, 2: 64-point pair tiles, 4: tail) seen per
@@ -131,6 +132,7 @@ struct EvalJob {
     unsigned int* overflow;
     unsigned int min_count;       // tensor-core kernel: leave batches below this to the latency path
     unsigned int max_count;       // ... and above this (nonzero) to the large-tile kernel
+    const unsigned int* base;     // k_mlp_pair COLS: list window start read on device (nullptr: 0), entries [*base, *count)
     // point epilogue
     float* out;                   // occupancy per point (or rgb x3 for texture)
     const uint32_t* out_pixel;    // texture: pixel index per point (out = rgb image)
@@ -208,7 +210,8 @@ int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaS
 struct ChainClasses {
     unsigned tail_max, mid_max;
     int level;
-    int prev_mask;  // classes launched for the previous iteration (-1: no check)
+    int prev_mask;     // classes launched for the previous iteration (-1: no check)
+    unsigned big_max;  // above this: the column-factored class 8 (0: no such class)
 };
 int launch_conflict_expand_cls(uint32_t* fine_queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
                                DevCounters* ctr, int iter, int max_iters, uint32_t* next_list, unsigned cap,
@@ -253,11 +256,12 @@ int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_n
 // column-factored field: give every distinct column (i + n j) of a node list a record slot
 // (cmap[col] = slot, collist[slot] = col, ctr->ncols = number of slots); cmap must be all -1
 int launch_col_claim(const uint32_t* list, const unsigned* count, int cells, int* cmap, uint32_t* collist,
-                     DevCounters* ctr, unsigned max_points, cudaStream_t s);
+                     DevCounters* ctr, unsigned max_points, cudaStream_t s, unsigned min_count = 0);
 // counting sort of a node list by column record (so a point tile spans few columns); cnt holds
 // one u32 per possible column and is cleared here
 int launch_sort_by_column(const uint32_t* list, const unsigned* count, int cells, const int* cmap, uint32_t* cnt,
-                          DevCounters* ctr, uint32_t* sorted, unsigned max_points, cudaStream_t s);
+                          DevCounters* ctr, uint32_t* sorted, unsigned max_points, cudaStream_t s,
+                          unsigned min_count = 0);
 // node list of a dense (cells+1)^3 grid in column order: t -> node (t / n1) + plane * (t % n1)
 int launch_dense_column_list(int cells, uint32_t* list, cudaStream_t s);
 int launch_binarize(const float* v, uint8_t* out, size_t n, cudaStream_t s);

@@ -331,7 +331,7 @@ int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaS
 // Iteration `iter` reads conflicts cf[iter&1], writes neighbours to next_list /
 // nx[iter&1], and clears the buffers iteration iter+1 will fill.
 __device__ __forceinline__ int chain_class(unsigned n, const ChainClasses& cc) {
-    return n == 0 ? 0 : (n > cc.mid_max ? 1 : (n > cc.tail_max ? 2 : 4));
+    return n == 0 ? 0 : ((cc.big_max && n > cc.big_max) ? 8 : (n > cc.mid_max ? 1 : (n > cc.tail_max ? 2 : 4)));
 }
 // the batch of host iteration `it` (count n) must have met one of the launched evaluators
 __device__ __forceinline__ void check_class(DevCounters* ctr, const ChainClasses& cc, int it, unsigned n) {
@@ -349,6 +349,7 @@ __global__ void k_conflict_expand(uint32_t* __restrict__ queued, const uint8_t* 
     unsigned ncf = ctr->cf_count[p];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (iter > 0) check_class(ctr, cc, iter - 1, ctr->nx_count[p ^ 1]);
+        ctr->ncols_base = ctr->ncols;  // the column records this iteration's batch may add start here
         ctr->cf_count[p ^ 1] = 0;
         ctr->nx_count[p ^ 1] = 0;
         if (ncf > 0 && iter >= max_iters) ctr->warning = 1;  // localize.hpp:343-346
@@ -400,8 +401,13 @@ int launch_conflict_expand_cls(uint32_t* queued, const uint8_t* fs, int fcells, 
 // Slot order depends on atomic timing, but a column's record is a function of the column
 // alone, so every node value is independent of it.
 __global__ void k_col_claim(const uint32_t* __restrict__ list, const unsigned* __restrict__ count, int cells,
-                            int* __restrict__ cmap, uint32_t* __restrict__ collist, DevCounters* ctr) {
+                            int* __restrict__ cmap, uint32_t* __restrict__ collist, DevCounters* ctr,
+                            unsigned min_count) {
     const unsigned n = *count;
+    // a conflict-loop batch claims columns only when it is the factored kernels' size class: which
+    // kernel records a column (tensor-core COLS or the tail's CUDA-core pass) must not depend on
+    // which evaluators the frame enqueued
+    if (n < min_count) return;
     const uint32_t n1 = (uint32_t)cells + 1u, plane = n1 * n1;
     for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const uint32_t col = list[t] % plane;
@@ -415,16 +421,17 @@ __global__ void k_col_claim(const uint32_t* __restrict__ list, const unsigned* _
 }
 
 int launch_col_claim(const uint32_t* list, const unsigned* count, int cells, int* cmap, uint32_t* collist,
-                     DevCounters* ctr, unsigned max_points, cudaStream_t s) {
+                     DevCounters* ctr, unsigned max_points, cudaStream_t s, unsigned min_count) {
     const unsigned blocks = std::min<unsigned>((max_points + 255) / 256, 148u * 8u);
-    k_col_claim<<<blocks ? blocks : 1, 256, 0, s>>>(list, count, cells, cmap, collist, ctr);
+    k_col_claim<<<blocks ? blocks : 1, 256, 0, s>>>(list, count, cells, cmap, collist, ctr, min_count);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }
 
 __global__ void k_slot_count(const uint32_t* __restrict__ list, const unsigned* __restrict__ count, int cells,
-                             const int* __restrict__ cmap, uint32_t* __restrict__ cnt) {
+                             const int* __restrict__ cmap, uint32_t* __restrict__ cnt, unsigned min_count) {
     const unsigned n = *count;
+    if (n < min_count) return;  // below the size class its columns were not claimed
     const uint32_t n1 = (uint32_t)cells + 1u, plane = n1 * n1;
     for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
         atomicAdd(&cnt[cmap[list[t] % plane]], 1u);
@@ -493,8 +500,10 @@ __global__ void __launch_bounds__(1024) k_scan_slots(uint32_t* __restrict__ cnt,
 }
 
 __global__ void k_slot_scatter(const uint32_t* __restrict__ list, const unsigned* __restrict__ count, int cells,
-                               const int* __restrict__ cmap, uint32_t* __restrict__ off, uint32_t* __restrict__ sorted) {
+                               const int* __restrict__ cmap, uint32_t* __restrict__ off, uint32_t* __restrict__ sorted,
+                               unsigned min_count) {
     const unsigned n = *count;
+    if (n < min_count) return;
     const uint32_t n1 = (uint32_t)cells + 1u, plane = n1 * n1;
     for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const uint32_t node = list[t];
@@ -503,13 +512,13 @@ __global__ void k_slot_scatter(const uint32_t* __restrict__ list, const unsigned
 }
 
 int launch_sort_by_column(const uint32_t* list, const unsigned* count, int cells, const int* cmap, uint32_t* cnt,
-                          DevCounters* ctr, uint32_t* sorted, unsigned max_points, cudaStream_t s) {
+                          DevCounters* ctr, uint32_t* sorted, unsigned max_points, cudaStream_t s, unsigned min_count) {
     const size_t plane = ((size_t)cells + 1) * ((size_t)cells + 1);
     ICG_CUDA_TRY(cudaMemsetAsync(cnt, 0, plane * 4, s));
     const unsigned blocks = std::max(1u, std::min<unsigned>((max_points + 255) / 256, 148u * 8u));
-    k_slot_count<<<blocks, 256, 0, s>>>(list, count, cells, cmap, cnt);
+    k_slot_count<<<blocks, 256, 0, s>>>(list, count, cells, cmap, cnt, min_count);
     k_scan_slots<<<1, 1024, 0, s>>>(cnt, &ctr->ncols);
-    k_slot_scatter<<<blocks, 256, 0, s>>>(list, count, cells, cmap, cnt, sorted);
+    k_slot_scatter<<<blocks, 256, 0, s>>>(list, count, cells, cmap, cnt, sorted, min_count);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }

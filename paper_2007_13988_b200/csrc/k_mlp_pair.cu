@@ -325,7 +325,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
     const bool leader = rank == 0;
     const EvalJob& job = P.job;
     const unsigned pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    const unsigned n = job_count(job);
+    // COLS: the job may be a window [*base, *count) of the column list (records of new columns only)
+    const unsigned jbase = (COLS && job.base) ? *job.base : 0u;
+    const unsigned n = job_count(job) - jbase;
+    float* const s_out = COLS ? P.s_out + (size_t)jbase * kSRow : nullptr;  // record of entry gi: row jbase + gi
     if (n < job.min_count || (job.max_count && n > job.max_count)) return;  // not this kernel's size class
     if (pair_id * NP >= n) {        // both CTAs of the pair take the same decision
         job_account(job);
@@ -979,7 +982,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 double pd[3] = {0.0, 0.0, 0.0};
                 if constexpr (COLS) {
                     // list entry = a column i + n j of the level grid; its node at k = 0 gives (x, y)
-                    if (idx < n) node_pos_d(job_node(job, idx), job.cells, pd);
+                    if (idx < n) node_pos_d(job_node(job, jbase + idx), job.cells, pd);
                 } else {
                     if (idx < n) job_point_d(job, idx, pd);
                 }
@@ -1096,7 +1099,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                         if (lane == 0) {
                             if constexpr (COLS) {
                                 const unsigned gi = tg * NP + rank * NPC + (unsigned)pl;
-                                if (gi < n) P.s_out[(size_t)gi * kSRow + kSFinal] = dot[0];
+                                if (gi < n) s_out[(size_t)gi * kSRow + kSFinal] = dot[0];
                             } else if (TEX) {
 #pragma unroll
                                 for (int c = 0; c < NOUT; ++c) ms.sdl[c][pl] = dot[c];
@@ -1227,7 +1230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
 #pragma unroll
                             for (int q = 0; q < 32; ++q) {
                                 const unsigned gi = t * NP + (unsigned)(colh * NPC + hf * 32 + q);
-                                if (gi < n) P.s_out[(size_t)gi * kSRow + roff + feat] = __uint_as_float(r[q]);
+                                if (gi < n) s_out[(size_t)gi * kSRow + roff + feat] = __uint_as_float(r[q]);
                             }
                         }
                     }
