@@ -391,11 +391,11 @@ def main():
     executed = fact_pts * FACT_MMA_FLOP_PER_POINT * exec_mult / fact_s / 1e12 if fact_s > 0 else 0.0
     traffic, traffic_note = None, None
     try:  # DRAM bytes of the factored pass's level-3 launch, from the committed ncu --set full capture
-        rec = json.load(open(os.path.join(ROOT, "profiles", "r01d_ncu_full_fact_L3.json")))[0]
+        rec = json.load(open(os.path.join(ROOT, "profiles", "r01e_ncu_full_fact2_L3.json")))[0]
         mb = lambda v: float(v.split()[0]) * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}[v.split()[1]]
         traffic = (mb(rec["dram__bytes_read.sum"]) + mb(rec["dram__bytes_write.sum"])) * 1e6
-        traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum of the level-3 FACT launch (280 k points, "
-                        "profiles/r01d_ncu_full_fact_L3.json): weights, column records and lists, L2-resident at 92 %")
+        traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum of the level-3 k_fact2 launch (280 k points, "
+                        "profiles/r01e_ncu_full_fact2_L3.json): weights, column records and lists, L2-resident at 92 %")
     except Exception:
         pass
     roofline = {"bound": "tensor",
