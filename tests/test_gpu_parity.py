@@ -507,3 +507,35 @@ def test_texture_colour_error_wide_sample(gpu_ctx, pifu_inputs):
     err = np.abs(gpu_ctx.texture_batch(f, pts) - m.texture(pts)).max()
     print(f"max colour error {err:.3e}")
     assert err <= RGB_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chain_fact", ["1", "0"])
+def test_points_in_m_factored_pass_matches(pifu_inputs, monkeypatch, chain_fact):
+    """config 2 (256^3) through the points-in-M factored kernel (k_fact2, also taking the level-3
+    conflict batches above 9472 nodes when chain_fact=1) against k_mlp_pair<FACT> and the
+    full-network chain kernels: identical evaluated sets, states and counts, values within 1e-5,
+    and both within the oracle bar on a sample."""
+    inp = pifu_inputs
+    cfg = api.AlgoConfig("progressive", 32, 3)
+    out = {}
+    for f2 in ("1", "0"):
+        monkeypatch.setenv("ICG_FACT2", f2)
+        monkeypatch.setenv("ICG_CHAIN_FACT", chain_fact)
+        c = api.Context(0)
+        c.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+        c.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+        f = api.PifuField(inp["fmap"], inp["caps"], 50.0, abi.ICG_PREC_FP32)
+        out[f2] = c.extract(f, cfg)
+        c.close()
+    a, b = out["1"], out["0"]
+    assert a.total_evals == b.total_evals and list(a.evals_per_level) == list(b.evals_per_level)
+    assert list(a.conflict_iters_per_level) == list(b.conflict_iters_per_level)
+    assert np.array_equal(a.states, b.states)
+    assert np.abs(a.values - b.values).max() <= 1e-5
+    m = _oracle_model(inp)
+    idx = np.flatnonzero(a.states == abi.ICG_STATE_EVALUATED)[::1499]
+    n = 257
+    i, j, k = idx % n, (idx // n) % n, idx // (n * n)
+    pts = np.stack([-1 + 2 * i / 256.0, -1 + 2 * j / 256.0, 1 - 2 * k / 256.0], 1)
+    assert np.abs(a.values[idx] - m.occupancy(pts)).max() <= OCC_TOL_FP32
