@@ -245,17 +245,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 next_stage();
             };
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
-                if (t != pair_id) {  // the previous tile's final layer has read D4 (and h3 read D3)
-                    const unsigned long long t0 = tr ? gtime() : 0;
-                    ptx::mbar_wait_cluster(&ms.tm_free, tfph);
-                    if (tr) w_tm += gtime() - t0;
-                    tfph ^= 1;
-                    ptx::tc_fence_after();
-                }
-                // layer 2: 16 h1 chunks x 2 feature halves into D2 (columns 0-511)
+                // layer 2: 16 h1 chunks x 2 feature halves into D2 (columns 0-511).  Columns 0-255
+                // (the previous tile's D3) are free once its h3 chunks were emitted, so the first
+                // item goes ahead; columns 256-511 (its D4) wait for the output layer to read them.
                 for (int kc = 0; kc < 16; ++kc) {
                     wait_chunk(ac);
                     item(ac, 0, kc == 0);
+                    if (kc == 0 && t != pair_id) {
+                        const unsigned long long t0 = tr ? gtime() : 0;
+                        ptx::mbar_wait_cluster(&ms.tm_free, tfph);
+                        if (tr) w_tm += gtime() - t0;
+                        tfph ^= 1;
+                        ptx::tc_fence_after();
+                    }
                     item(ac, 256, kc == 0);
                     ptx::mma_commit_pair(&ms.a_free[ac % kA], both);
                     ++ac;
