@@ -368,23 +368,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             unsigned idx;
             bool valid;
         };
-        auto prep = [&](unsigned tg, int pb) {
+        // the node index and record slot of this thread's point of tile tg, loaded ahead of prep()
+        struct Pre {
+            uint32_t node;
+            int slot;
+        };
+        auto preload = [&](unsigned tg) {
+            Pre r{0u, 0};
+            const unsigned idx = tg * NP + rank * NPC + (unsigned)row;
+            if (cq == 0 && idx < n) {
+                r.node = job_node(job, idx);
+                const uint32_t n1 = (uint32_t)job.cells + 1u, col = r.node % (n1 * n1);
+                r.slot = P.cmap ? __ldg(&P.cmap[col]) : (int)col;
+            }
+            return r;
+        };
+        auto prep = [&](unsigned tg, int pb, const Pre& pr) {
             Pt q;
             q.idx = tg * NP + rank * NPC + (unsigned)row;
             q.valid = q.idx < n;
             if (cq == 0) {  // position (fp64 node -> NDC, as the reference) and record slot
                 double pd[3] = {0.0, 0.0, 0.0};
-                int sl = 0;
-                if (q.valid) {
-                    job_point_d(job, q.idx, pd);
-                    const uint32_t n1 = (uint32_t)job.cells + 1u, col = job_node(job, q.idx) % (n1 * n1);
-                    sl = P.cmap ? __ldg(&P.cmap[col]) : (int)col;
-                }
+                if (q.valid) node_pos_d(pr.node, job.cells, pd);
                 ms.ppos[pb][row][0] = (float)pd[0];
                 ms.ppos[pb][row][1] = (float)pd[1];
                 ms.ppos[pb][row][2] = (float)pd[2];
-                ms.pslot[pb][row] = sl;
-                ms.sfinal[pb][row] = __ldg(P.s_in + (size_t)sl * kSRow + kSFinal);
+                ms.pslot[pb][row] = pr.slot;
             }
             epi_bar();
             const float p3[3] = {ms.ppos[pb][row][0], ms.ppos[pb][row][1], ms.ppos[pb][row][2]};
@@ -496,7 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     sum += ms.red[g][row];
                 }
                 const float cterm = __ldg(&b5[0]) + w5z * q.z - __ldg(&P.f.fscene->sdf_scale) * d;
-                const float s = sum + ms.sfinal[pb][row] + cterm;
+                const float s = sum + __ldg(q.rec + kSFinal) + cterm;
                 const float v = 1.0f / (1.0f + expf(-s));
                 if (job_is_grid(job))
                     grid_epilogue(job, job_node(job, q.idx), v);
@@ -509,17 +518,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // layer-1 chunks are ready when its layer 2 may start (after final(t) has read D4).
         int pb = 0;
         unsigned long long tq = etr ? gtime() : 0;
-        Pt cur = prep(pair_id, 0);
+        Pt cur = prep(pair_id, 0, preload(pair_id));
         if (etr) e_prep += gtime() - tq;
         emit_h1(cur, 0, 4);
         for (unsigned t = pair_id; t < ntiles; t += npairs) {
             const bool has_next = t + npairs < ntiles;
+            const Pre pre_next = has_next ? preload(t + npairs) : Pre{0u, 0};  // in flight during h1
             tq = etr ? gtime() : 0;
             emit_h1(cur, 4, 16);
             if (etr) e_h1 += gtime() - tq;
             Pt nxt = cur;
             tq = etr ? gtime() : 0;
-            if (has_next) nxt = prep(t + npairs, pb ^ 1);
+            if (has_next) nxt = prep(t + npairs, pb ^ 1, pre_next);
             if (etr) e_prep += gtime() - tq;
             wait_d(&ms.d2done, d2ph);
             drain(cur, 8, 0, b2, 512, 1024);
