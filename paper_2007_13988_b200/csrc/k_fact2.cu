@@ -420,8 +420,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         };
         // layer 1 (no MMA): chunks [c0, c1) of act(S1 + w1z z + b1)
         // layer 1 in pairs of chunks [c0, c1) (c1 - c0 even)
+        auto prefetch_l1 = [](const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); };
         auto emit_h1 = [&](const Pt& q, int c0, int c1) {
             for (int kc = c0; kc < c1; kc += 2) {
+                // the record terms and biases the drains of layers 2-4 read, into L1 ahead of time
+                // (pair kc: h2 chunk kc/2; pairs 0-3 also h3 chunk kc/2, pair 4 the layer-4 slice)
+                {
+                    const int c = kc >> 1, fo = cq * kFW;
+                    prefetch_l1(q.rec + 1024 + c * 64 + fo);
+                    prefetch_l1(b2 + c * 64 + fo);
+                    prefetch_l1(b2 + 512 + c * 64 + fo);
+                    if (c < 4) {
+                        prefetch_l1(q.rec + 1536 + c * 64 + fo);
+                        prefetch_l1(b3 + c * 64 + fo);
+                        prefetch_l1(b3 + 256 + c * 64 + fo);
+                    } else if (c == 4) {
+                        prefetch_l1(q.rec + 1792 + cq * (128 / kCQ));
+                        prefetch_l1(b4 + cq * (128 / kCQ));
+                        prefetch_l1(b4 + 128 + cq * (128 / kCQ));
+                    }
+                }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                     const int f0 = (kc + u) * 64 + cq * kFW;
