@@ -66,7 +66,7 @@ static_assert(kTotal <= 232448, "shared memory");
 struct Misc {
     uint64_t full[kStages], empty[kStages];
     uint64_t a_ready[kA], a_free[kA];
-    uint64_t d2done, d3done, d4done, tm_free;
+    uint64_t d2a, d2done, d3done, d4done, tm_free;  // d2a: D2 columns 0-255 final
     uint32_t tmem_base;
     int ncaps;
     float caps[16][8];
@@ -129,6 +129,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&ms.a_ready[a], 2 * kEpiWarps);  // every epilogue warp of both CTAs
             ptx::mbar_init(&ms.a_free[a], 1);
         }
+        ptx::mbar_init(&ms.d2a, 1);
         ptx::mbar_init(&ms.d2done, 1);
         ptx::mbar_init(&ms.d3done, 1);
         ptx::mbar_init(&ms.d4done, 1);
@@ -251,6 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int kc = 0; kc < 16; ++kc) {
                     wait_chunk(ac);
                     item(ac, 0, kc == 0);
+                    if (kc == 15) ptx::mma_commit_pair(&ms.d2a, both);  // h2 chunks 0-3 may be drained
                     if (kc == 0 && t != pair_id) {
                         const unsigned long long t0 = tr ? gtime() : 0;
                         ptx::mbar_wait_cluster(&ms.tm_free, tfph);
@@ -305,7 +307,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float* b4 = b3 + 2 * 256;
         const float* b5 = b4 + 2 * 128;
         const float w5z = __ldg(&P.wlast[128 + kGeoSkip - 1]);
-        uint32_t ac = 0, d2ph = 0, d3ph = 0, d4ph = 0;
+        uint32_t ac = 0, d2aph = 0, d2ph = 0, d3ph = 0, d4ph = 0;
         const bool etr = P.trace && blockIdx.x == 0 && et == 0;
         unsigned long long e_free = 0, e_d = 0, e_prep = 0, e_h1 = 0, e_fin = 0, e_begin = gtime();
         // kFW activations of this thread (features cq kFW .. of the chunk) -> chunk slot, hi and lo
@@ -459,8 +461,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         };
         // hidden layers 2, 3: drain D (columns col0 + feature) into the next layer's chunks
-        auto drain = [&](const Pt& q, int nchunks, uint32_t col0, const float* bl, int od, int soff) {
-            for (int c2 = 0; c2 < nchunks; c2 += 2) {
+        auto drain = [&](const Pt& q, int cbeg, int cend, uint32_t col0, const float* bl, int od, int soff) {
+            for (int c2 = cbeg; c2 < cend; c2 += 2) {
 #pragma unroll 1
               for (int u = 0; u < 2; ++u) {
                 const int c = c2 + u;
@@ -549,10 +551,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tq = etr ? gtime() : 0;
             if (has_next) nxt = prep(t + npairs, pb ^ 1, pre_next);
             if (etr) e_prep += gtime() - tq;
+            wait_d(&ms.d2a, d2aph);
+            drain(cur, 0, 4, 0, b2, 512, 1024);
             wait_d(&ms.d2done, d2ph);
-            drain(cur, 8, 0, b2, 512, 1024);
+            drain(cur, 4, 8, 0, b2, 512, 1024);
             wait_d(&ms.d3done, d3ph);
-            drain(cur, 4, 0, b3, 256, 1536);
+            drain(cur, 0, 4, 0, b3, 256, 1536);
             tq = etr ? gtime() : 0;
             if (has_next) emit_h1(nxt, 0, 4);
             if (etr) e_h1 += gtime() - tq;
