@@ -114,6 +114,7 @@ struct icg_context {
     bool use_tail = true;
     bool chain_trace = false;  // ICG_CHAIN_TRACE=1
     bool chain_fact = true;    // large conflict-loop batches column-factored (ICG_CHAIN_FACT=0: CTA-pair GEO)
+    unsigned chain_fact_min = 74u * 128u;  // ... above this many nodes (ICG_CHAIN_FACT_MIN)
     bool use_fact2 = true;     // bulk factored pass with swapped operands (k_fact2.cu); ICG_FACT2=0: k_mlp_pair<FACT>
     bool tail_wide = true;  // this frame is alone on its device: the tail kernel takes every SM
     unsigned tail_max = 128;  // conflict batches up to this size start the persistent tail kernel
@@ -622,7 +623,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
             const unsigned mid_max = 74u * 64u;
             // batches beyond one wave of 128-point pair tiles: column-factored (k_fact2, 256-point tiles)
             const bool x3c = fd.precision == ICG_PREC_FP32;
-            const unsigned big_max = (c->chain_fact && c->use_fact2 && x3c) ? 74u * 128u : 0u;
+            const unsigned big_max = (c->chain_fact && c->use_fact2 && x3c) ? c->chain_fact_min : 0u;
             int prev_mask = -1;
             for (int it = 0; it < unroll; ++it) {
                 int p = it & 1;
@@ -967,6 +968,7 @@ int icg_create(int device, icg_context** out) {
     if (getenv("ICG_TC_TRACE") || getenv("ICG_TAIL_TRACE")) c->use_graph = false;  // traces synchronise
     if (const char* e = getenv("ICG_FACT2")) c->use_fact2 = e[0] == '1';
     if (const char* e = getenv("ICG_CHAIN_FACT")) c->chain_fact = e[0] == '1';
+    if (const char* e = getenv("ICG_CHAIN_FACT_MIN")) c->chain_fact_min = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_NO_XEXT")) c->use_xext = !(e[0] == '1');
     if (getenv("ICG_CHAIN_TRACE")) {
         c->chain_trace = true;
