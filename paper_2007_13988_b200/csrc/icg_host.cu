@@ -33,11 +33,16 @@ static int einval(const std::string& m) {
     return ICG_EINVAL;
 }
 
+// Bumped by every device (re)allocation of a work buffer: a captured frame graph bakes the
+// buffer addresses into its launches, so it is only replayed while this is unchanged.
+static std::atomic<unsigned long long> g_alloc_gen{0};
+
 struct DBuf {
     void* p = nullptr;
     size_t n = 0;
     int ensure(size_t bytes) {
         if (bytes <= n) return ICG_OK;
+        g_alloc_gen.fetch_add(1, std::memory_order_relaxed);
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
@@ -70,6 +75,8 @@ struct icg_context {
     struct FrameKey {
         icg_algo_config cfg;
         icg_camera cam;
+        unsigned long long alloc_gen;  // no work buffer moved since the capture (g_alloc_gen)
+        int fmap_c, fmap_h, fmap_w;    // feature-map shape baked into the field kernels' parameters
         int W, H, kind, precision, img_mem;
         float bg[3];
         void* img_ptr[4];
@@ -92,7 +99,7 @@ struct icg_context {
     DBuf geo_wt[5], geo_b[5], tex_wt[5], tex_b[5], geo_wrow[5];
     const float* geo_rows[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     SimtMlp geo_simt{}, tex_simt{};
-    DBuf geo_stream, geo_bias, geo_wlast, tex_stream, tex_bias, tex_wlast;
+    DBuf geo_bias, geo_wlast, tex_bias, tex_wlast;
     TcMlp geo_tc{}, tex_tc{};
     DBuf geo_pair_stream, tex_pair_stream, geo_pair_hi, tex_pair_hi;
     // TMA descriptors of the pair streams: [0] bf16x3 (hi, lo), [1] bf16 (hi only)
@@ -118,7 +125,6 @@ struct icg_context {
     bool use_fact2 = true;     // bulk factored pass with swapped operands (k_fact2.cu); ICG_FACT2=0: k_mlp_pair<FACT>
     bool tail_wide = true;  // this frame is alone on its device: the tail kernel takes every SM
     unsigned tail_max = 128;  // conflict batches up to this size start the persistent tail kernel
-    bool use_pair = true;
     // field
     DBuf scene;
     DevScene* h_scene = nullptr;  // pinned staging
@@ -131,11 +137,7 @@ struct icg_context {
     DBuf list_e0, cf[2], nx[2];
     DBuf ctr;
     DevCounters* h_ctr = nullptr;  // pinned
-    DBuf binar, pts, outv, small_scratch, lp_scratch, lp_stream;
-    unsigned small_max = 96;  // ICG_LAT=small: batches up to this size take the SIMT latency kernel
-    unsigned lp_max = 1536;   // batches up to this size take the layer-parallel tensor-core path (k_lp.cu)
-    bool lat_small = false;
-    bool geo_lp = false;
+    DBuf binar, pts, outv;
     // render
     DBuf depth, rgb, mask, surfk, spts, spx;
     // last extraction
@@ -352,7 +354,7 @@ int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
 
 bool fact_ok(const icg_context* c, const FieldDev& fd) {
     return fd.kind == ICG_FIELD_PIFU && (fd.precision == ICG_PREC_FP32 || fd.precision == ICG_PREC_BF16) &&
-           c->geo_pair && c->use_pair && c->geo_fact && c->use_fact;
+           c->geo_pair && c->geo_fact && c->use_fact;
 }
 
 // Column-factored evaluation of a grid job (a level's node list, or all nodes of a dense grid):
@@ -453,36 +455,9 @@ int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned ma
         r = launch_analytic_eval(fd, job, max_points, c->stream);
     } else if (fd.precision == ICG_PREC_FP32_SIMT) {
         r = launch_pifu_simt_eval(fd, c->geo_simt, job, max_points, c->stream);
-    } else if (dependent_chain && c->geo_lp && c->lp_max > 0 && !c->lat_small) {
-        // both launched; each exits on device unless the batch size is its own
-        if (int e = c->lp_scratch.ensure(lp_scratch_bytes(c->lp_max))) return e;
-        EvalJob big = job;
-        big.min_count = c->lp_max + 1;
-        const bool x3 = fd.precision == ICG_PREC_FP32;
-        if (c->geo_pair && c->use_pair)
-            r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap[x3 ? 0 : 1], big, max_points, x3, c->stream);
-        else
-            r = launch_pifu_tc_eval(fd, c->geo_tc, big, max_points, x3, c->stream);
-        if (!r) r = launch_lp_eval(fd, c->geo_tc, c->lp_stream.as<uint8_t>(), job, c->lp_scratch.as<uint8_t>(), c->lp_max, x3, c->stream);
-        c->launches += 1;
-    } else if (dependent_chain && c->small_max > 0 && c->lat_small) {
-        if (int e = c->small_scratch.ensure(small_scratch_bytes(c->small_max))) return e;
-        EvalJob big = job;
-        big.min_count = c->small_max + 1;
-        if (c->geo_pair && c->use_pair)
-            r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1], big,
-                                      max_points, fd.precision == ICG_PREC_FP32, c->stream);
-        else
-            r = launch_pifu_tc_eval(fd, c->geo_tc, big, max_points, fd.precision == ICG_PREC_FP32, c->stream);
-        if (!r)
-            r = launch_small_mlp(fd, c->geo_simt, c->geo_rows, job, c->small_scratch.as<float>(), c->small_max,
-                                 c->small_max, c->stream);
-        c->launches += 1;
-    } else if (c->geo_pair && c->use_pair) {
+    } else {
         r = launch_pifu_pair_eval(fd, c->geo_tc, c->geo_pair_tmap[fd.precision == ICG_PREC_FP32 ? 0 : 1], job,
                                   max_points, fd.precision == ICG_PREC_FP32, c->stream);
-    } else {
-        r = launch_pifu_tc_eval(fd, c->geo_tc, job, max_points, fd.precision == ICG_PREC_FP32, c->stream);
     }
     prof_end(c, slot);
     c->launches += 1;
@@ -494,14 +469,11 @@ int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned
     int r;
     if (fd.precision == ICG_PREC_FP32_SIMT)
         r = launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
-    else if (c->geo_pair && c->tex_pair && c->use_pair)
+    else
         // one fp16 copy of every weight and operand, one MMA per K step, at every precision:
         // colours within 5.2e-4 of fp64 (scripts/tex_precision.py; tolerance 1e-3)
         r = launch_pifu_pair_texture(fd, c->geo_tc, c->tex_tc, c->geo_pair_f16_tmap[1], c->tex_pair_tmap[1], job,
                                      max_points, false, c->stream);
-    else
-        r = launch_pifu_tc_texture(fd, c->geo_tc, c->tex_tc, job, max_points, fd.precision == ICG_PREC_FP32,
-                                   c->stream);
     prof_end(c, slot);
     c->launches += 1;
     return r;
@@ -961,7 +933,6 @@ int icg_create(int device, icg_context** out) {
     }
     auto* c = new icg_context();
     c->device = device;
-    if (const char* e = getenv("ICG_NO_PAIR")) c->use_pair = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_FACT")) c->use_fact = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_TAIL")) c->use_tail = !(e[0] == '1');
     if (const char* e = getenv("ICG_NO_GRAPH")) c->use_graph = !(e[0] == '1');
@@ -975,9 +946,6 @@ int icg_create(int device, icg_context** out) {
         c->use_graph = false;
     }
     if (const char* e = getenv("ICG_TAIL_MAX")) c->tail_max = (unsigned)atoi(e);
-    if (const char* e = getenv("ICG_SMALL_MAX")) c->small_max = (unsigned)atoi(e);
-    if (const char* e = getenv("ICG_LP_MAX")) c->lp_max = (unsigned)atoi(e);
-    if (const char* e = getenv("ICG_LAT")) c->lat_small = std::string(e) == "small";
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->e0) != cudaSuccess || cudaEventCreate(&c->e1) != cudaSuccess ||
         cudaMallocHost(&c->h_scene, sizeof(DevScene)) != cudaSuccess ||
@@ -999,10 +967,10 @@ int icg_destroy(icg_context* c) {
     if (!c) return ICG_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    DBuf* all[] = {&c->geo_stream, &c->geo_bias, &c->geo_wlast, &c->tex_stream, &c->tex_bias, &c->tex_wlast,
+    DBuf* all[] = {&c->geo_bias, &c->geo_wlast, &c->tex_bias, &c->tex_wlast,
                    &c->scene, &c->fscene, &c->fmap_chw, &c->fmap_hwc, &c->vals[0], &c->vals[1], &c->sts[0], &c->sts[1],
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
-                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->small_scratch, &c->lp_scratch, &c->lp_stream, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi, &c->geo_pair_f16, &c->geo_pair_f16_hi,
+                   &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi, &c->geo_pair_f16, &c->geo_pair_f16_hi,
                    &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx, &c->colrec, &c->cmap, &c->collist, &c->colcnt, &c->sorted, &c->tail_scratch,
                    &c->geo_fact_stream[0][0], &c->geo_fact_stream[0][1], &c->geo_fact_stream[1][0],
                    &c->geo_fact_stream[1][1]};
@@ -1086,15 +1054,12 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
     }
     sm.skip = skip;
     sm.slope = d->leaky_slope;
-    // tcgen05 operand stream (bf16 hi/lo tiles) + fp32 biases + fp32 final layer
-    DBuf& st = geo ? c->geo_stream : c->tex_stream;
+    // fp32 epilogue operands of the tensor-core kernels: biases + z-weight columns, final layer
     DBuf& bi = geo ? c->geo_bias : c->tex_bias;
     DBuf& wl = geo ? c->geo_wlast : c->tex_wlast;
     TcMlp& tc = geo ? c->geo_tc : c->tex_tc;
-    size_t sb = tc_stream_bytes(d->which);
     tc.valid = 0;
-    if (sb) {
-        std::vector<uint8_t> hs(sb);
+    {
         std::vector<float> hb(tc_bias_floats(d->which)), hw(tc_wlast_floats(d->which));
         const float* ws[5];
         const float* bs[5];
@@ -1102,15 +1067,11 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
             ws[l] = d->weights[l];
             bs[l] = d->biases[l];
         }
-        if (int r = tc_pack_mlp(d->which, ws, bs, hs.data(), hb.data(), hw.data())) return r;
-        if (int r = st.ensure(sb)) return r;
+        if (int r = tc_pack_epilogue(d->which, ws, bs, hb.data(), hw.data())) return r;
         if (int r = bi.ensure(hb.size() * 4)) return r;
         if (int r = wl.ensure(hw.size() * 4)) return r;
-        ICG_CUDA_TRY(cudaMemcpy(st.p, hs.data(), sb, cudaMemcpyHostToDevice));
         ICG_CUDA_TRY(cudaMemcpy(bi.p, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice));
         ICG_CUDA_TRY(cudaMemcpy(wl.p, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice));
-        tc.stream = st.as<uint8_t>();
-        tc.stream_bytes = sb;
         tc.bias = bi.as<float>();
         tc.w_last = wl.as<float>();
         int off = 0;
@@ -1166,17 +1127,6 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
                 if (int r = pair_make_tmap(c->geo_fact_stream[0][0].p, bx, c->geo_fact2_tmap, 128)) return r;
         }
         c->geo_fact = true;
-    }
-    if (geo) {
-        // layer-parallel latency path: weight tiles per (layer, row block, K chunk)
-        const size_t lb = lp_stream_bytes();
-        std::vector<uint8_t> ls(lb);
-        const float* ws[5];
-        for (int l = 0; l < 5; ++l) ws[l] = d->weights[l];
-        if (int r = lp_pack_geometry(ws, ls.data())) return r;
-        if (int r = c->lp_stream.ensure(lb)) return r;
-        ICG_CUDA_TRY(cudaMemcpy(c->lp_stream.p, ls.data(), lb, cudaMemcpyHostToDevice));
-        c->geo_lp = true;
     }
     if (geo)
         c->has_geo = true;
@@ -1261,6 +1211,10 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
         key.H = H;
         key.kind = fd.kind;
         key.precision = fd.precision;
+        key.alloc_gen = g_alloc_gen.load(std::memory_order_relaxed);
+        key.fmap_c = fd.C;
+        key.fmap_h = fd.H;
+        key.fmap_w = fd.W;
         for (int i = 0; i < 3; ++i) key.bg[i] = bg ? bg[i] : 0.0f;
         if (img) {
             key.img_mem = img->mem;
@@ -1287,6 +1241,10 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
         if (graphs && gs.graph_valid && gs.graph_key == key) {
             ICG_CUDA_TRY(cudaGraphLaunch(gs.graph_exec, c->stream));
             c->launches += gs.graph_launches;
+            // the host-side bookkeeping body() would have done (issue_extract's final grid)
+            c->last_cells = cfg->coarsest_cells << cfg->target_level;
+            c->last_buf = cfg->variant == ICG_VARIANT_BRUTE ? 0 : (cfg->target_level & 1);
+            c->fact_used = fact_ok(c, fd);
             ran = true;
         } else if (graphs && gs.warm_valid && gs.warm_key == key) {
             const uint64_t l0 = c->launches;
@@ -1415,7 +1373,9 @@ int icg_compare_iou(icg_context* c, const uint8_t* a, const uint8_t* b, size_t n
         return ICG_OK;
     }
     if (!a || !b) return einval("compare_iou: null input");
-    if (mem == ICG_MEM_HOST || !c) {
+    if (mem != ICG_MEM_HOST && mem != ICG_MEM_DEVICE) return einval("compare_iou: mem must be ICG_MEM_HOST or ICG_MEM_DEVICE");
+    if (mem == ICG_MEM_DEVICE && !c) return einval("compare_iou: device arrays need a context");
+    if (mem == ICG_MEM_HOST) {
         uint64_t inter = 0, uni = 0;
         for (size_t i = 0; i < n; ++i) {
             bool av = a[i] != 0, bv = b[i] != 0;
@@ -1513,6 +1473,10 @@ int icg_device_free(icg_context* c, void* p) {
 }
 int icg_memcpy(icg_context* c, void* dst, const void* src, size_t bytes, int dst_mem, int src_mem) {
     if (!c) return einval("null context");
+    if ((dst_mem != ICG_MEM_HOST && dst_mem != ICG_MEM_DEVICE) || (src_mem != ICG_MEM_HOST && src_mem != ICG_MEM_DEVICE))
+        return einval("memcpy: mem must be ICG_MEM_HOST or ICG_MEM_DEVICE");
+    if (bytes == 0) return ICG_OK;
+    if (!dst || !src) return einval("memcpy: null pointer");
     ICG_CUDA_TRY(cudaSetDevice(c->device));
     cudaMemcpyKind k = dst_mem == ICG_MEM_HOST
                            ? (src_mem == ICG_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost)

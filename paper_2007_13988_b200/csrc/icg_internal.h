@@ -5,11 +5,33 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
 #include <string>
 
 #include "../../include/isocull_b200.h"
 
 namespace icg {
+
+// Once-per-device initialisation (cudaFuncSetAttribute and friends are per device, and several
+// host threads may drive contexts on several devices at once): `run(f)` calls f() the first time
+// it is reached on the current device, under a lock; a failure is not recorded as done.
+struct PerDeviceOnce {
+    std::atomic<unsigned long long> done{0};
+    std::mutex m;
+    template <class F>
+    int run(F&& f) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return ICG_ERUNTIME;
+        const unsigned long long bit = 1ull << (dev & 63);
+        if (done.load(std::memory_order_acquire) & bit) return ICG_OK;
+        std::lock_guard<std::mutex> g(m);
+        if (done.load(std::memory_order_relaxed) & bit) return ICG_OK;
+        int r = f();
+        if (r == ICG_OK) done.fetch_or(bit, std::memory_order_release);
+        return r;
+    }
+};
 
 // ---------------------------------------------------------------------------
 // Error plumbing: no exceptions cross the C ABI.
@@ -102,10 +124,8 @@ struct SimtMlp {
     float slope;
 };
 
-// Packed tcgen05 operand stream of one MLP (see k_mlp_tc.cu for the layout).
+// fp32 epilogue operands of one MLP shared by the tensor-core kernels (mlp_pack.cu).
 struct TcMlp {
-    const uint8_t* stream;    // bf16 hi/lo weight tiles in consumption order
-    size_t stream_bytes;
     const float* bias;        // concatenated fp32 biases
     const float* w_last;      // final layer fp32 [out][prev+skip]
     int bias_off[5];
@@ -154,10 +174,6 @@ int launch_pifu_simt_eval(const FieldDev& f, const SimtMlp& geo, const EvalJob& 
                           unsigned int max_points, cudaStream_t s);
 int launch_pifu_simt_texture(const FieldDev& f, const SimtMlp& geo, const SimtMlp& tex,
                              const EvalJob& job, unsigned int max_points, cudaStream_t s);
-int launch_pifu_tc_eval(const FieldDev& f, const TcMlp& geo, const EvalJob& job, unsigned int max_points,
-                        bool bf16x3, cudaStream_t s);
-int launch_pifu_tc_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const EvalJob& job,
-                           unsigned int max_points, bool bf16x3, cudaStream_t s);
 size_t pair_stream_bytes(int which, bool x3);
 // f16skip: skip-input items as fp16 hi/lo (the texture kernel's streams, geometry prefix included)
 int pair_pack(int which, const float* const* w, uint8_t* stream_x3, uint8_t* stream_hi, bool f16skip = false);
@@ -182,14 +198,6 @@ int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap,
 int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& tex, const void* tmap_geo,
                              const void* tmap_tex, const EvalJob& job, unsigned max_points, bool x3,
                              cudaStream_t s);
-size_t lp_stream_bytes();
-int lp_pack_geometry(const float* const* w, uint8_t* stream);
-size_t lp_scratch_bytes(unsigned max_count);
-int launch_lp_eval(const FieldDev& f, const TcMlp& geo, const uint8_t* lp_stream, const EvalJob& job, uint8_t* scratch,
-                   unsigned max_count, bool x3, cudaStream_t s);
-size_t small_scratch_bytes(unsigned cap);
-int launch_small_mlp(const FieldDev& f, const SimtMlp& geo, const float* const* wrow, const EvalJob& job,
-                     float* scratch, unsigned cap, unsigned max_count, cudaStream_t s);
 int launch_fmap_chw_to_hwc(const float* chw, float* hwc, int C, int H, int W, cudaStream_t s);
 
 // grid kernels (k_grid.cu)
@@ -290,9 +298,7 @@ int launch_render_first_crossing(const RenderJob& r, cudaStream_t s);
 // extents of the nonzero values along every x-line of the (R+1)^3 grid (render empty-space skipping)
 int launch_xline_extents(const float* values, int cells, int2* ext, cudaStream_t s);
 
-size_t tc_stream_bytes(int which);
-int tc_pack_mlp(int which, const float* const* w, const float* const* b, uint8_t* host_stream,
-                float* host_bias, float* host_wlast);
+int tc_pack_epilogue(int which, const float* const* w, const float* const* b, float* host_bias, float* host_wlast);
 size_t tc_bias_floats(int which);
 size_t tc_wlast_floats(int which);
 

@@ -588,11 +588,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job, const float* records,
                       const int* cmap, unsigned max_points, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        ICG_CUDA_TRY(cudaFuncSetAttribute(fact2::k_fact2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fact2::kTotal));
-        attr = true;
-    }
+    static PerDeviceOnce once;
+    if (int r = once.run([] {
+            ICG_CUDA_TRY(cudaFuncSetAttribute(fact2::k_fact2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)fact2::kTotal));
+            return ICG_OK;
+        }))
+        return r;
     fact2::Params p{};
     p.f = f;
     p.job = job;

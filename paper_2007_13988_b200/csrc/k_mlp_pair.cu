@@ -1,14 +1,14 @@
 // k_mlp_pair.cu — the PIFu geometry and texture fields on CTA PAIRS
 // (tcgen05 cta_group::2).
 //
-// Same fused "weights x activations^T" dataflow as k_mlp_tc.cu, but every MMA
-// is M=256 x N x K=16 executed by the two SMs of a TPC: each CTA of the
-// cluster holds 128 of the 256 weight rows (A) and N/2 of the N points (B) in
-// its shared memory; its TMEM holds its 128 output rows for all N points.  Per
-// SM this halves the shared-memory operand bytes per FLOP and doubles the
-// tensor work per pipeline stage relative to the single-CTA 128xN MMA (the
-// single-CTA kernel measured ~25% tensor-pipe activity, bound by per-stage
-// overheads and SMEM operand traffic).
+// A fused "weights x activations^T" dataflow: every MMA is M=256 x N x K=16
+// executed by the two SMs of a TPC: each CTA of the cluster holds 128 of the
+// 256 weight rows (A) and N/2 of the N points (B) in its shared memory; its
+// TMEM holds its 128 output rows for all N points.  Per SM this halves the
+// shared-memory operand bytes per FLOP and doubles the tensor work per
+// pipeline stage relative to a single-CTA 128xN MMA (a round-1 single-CTA
+// kernel measured ~25% tensor-pipe activity, bound by per-stage overheads and
+// SMEM operand traffic; it was removed in round 2).
 //   geometry : N = 128 (64 points per CTA), 257->1024->512->256->128->1
 //   texture  : N = 64 (32 points per CTA; the 513-wide skip input is twice as
 //              large): the geometry prefix (layers 1-3) writes its layer-3
@@ -1582,12 +1582,13 @@ template <int MODE>
 static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, unsigned max_points, cudaStream_t s) {
     using C = pair::Cfg<MODE>;
     constexpr bool TEX = MODE == pair::kModeTex;
-    static bool attr = false;
-    if (!attr) {
-        ICG_CUDA_TRY(cudaFuncSetAttribute(pair::k_mlp_pair<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)C::kTotal));
-        attr = true;
-    }
+    static PerDeviceOnce once;
+    if (int r = once.run([] {
+            ICG_CUDA_TRY(cudaFuncSetAttribute(pair::k_mlp_pair<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)C::kTotal));
+            return ICG_OK;
+        }))
+        return r;
     static unsigned long long* trace = nullptr;
     static int tron = -1;
     if (tron < 0) {

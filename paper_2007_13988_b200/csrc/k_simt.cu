@@ -265,12 +265,13 @@ __global__ void __launch_bounds__(NT, 1) k_pifu_simt_texture(FieldDev f, SimtMlp
 
 int launch_pifu_simt_eval(const FieldDev& f, const SimtMlp& geo, const EvalJob& job, unsigned int max_points,
                           cudaStream_t s) {
-    static bool attr = false;
-    size_t smem = sizeof(SimtSmem);
-    if (!attr) {
-        ICG_CUDA_TRY(cudaFuncSetAttribute(k_pifu_simt_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    static PerDeviceOnce once;
+    const size_t smem = sizeof(SimtSmem);
+    if (int r = once.run([&] {
+            ICG_CUDA_TRY(cudaFuncSetAttribute(k_pifu_simt_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            return ICG_OK;
+        }))
+        return r;
     unsigned blocks = (max_points + TP - 1) / TP;
     if (blocks > 148) blocks = 148;
     if (blocks == 0) blocks = 1;
@@ -281,12 +282,13 @@ int launch_pifu_simt_eval(const FieldDev& f, const SimtMlp& geo, const EvalJob& 
 
 int launch_pifu_simt_texture(const FieldDev& f, const SimtMlp& geo, const SimtMlp& tex, const EvalJob& job,
                              unsigned int max_points, cudaStream_t s) {
-    static bool attr = false;
-    size_t smem = sizeof(SimtTexSmem);
-    if (!attr) {
-        ICG_CUDA_TRY(cudaFuncSetAttribute(k_pifu_simt_texture, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    static PerDeviceOnce once;
+    const size_t smem = sizeof(SimtTexSmem);
+    if (int r = once.run([&] {
+            ICG_CUDA_TRY(cudaFuncSetAttribute(k_pifu_simt_texture, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            return ICG_OK;
+        }))
+        return r;
     unsigned blocks = (max_points + TP - 1) / TP;
     if (blocks > 148) blocks = 148;
     if (blocks == 0) blocks = 1;

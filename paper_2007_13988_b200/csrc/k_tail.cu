@@ -444,15 +444,15 @@ static int tail_setup(int sms) {
 // wide: the frame is alone on the device (148-CTA grid, lower latency); otherwise 64 CTAs
 int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_new, unsigned max_cols, cudaStream_t s,
                 bool wide) {
-    static bool attr = false;
-    if (!attr) {
-        int dev = 0, sms = 0;
-        ICG_CUDA_TRY(cudaGetDevice(&dev));
-        ICG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (int r = tail_setup<64>(sms)) return r;
-        if (int r = tail_setup<148>(sms)) return r;
-        attr = true;
-    }
+    static PerDeviceOnce once;
+    if (int r = once.run([] {
+            int dev = 0, sms = 0;
+            ICG_CUDA_TRY(cudaGetDevice(&dev));
+            ICG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            if (int e = tail_setup<64>(sms)) return e;
+            return tail_setup<148>(sms);
+        }))
+        return r;
     uint8_t* q = scratch;
     p.h1 = reinterpret_cast<float*>(q);
     q += (size_t)cap_pts * 1024 * 4;
