@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ICG_ABI_VERSION 1
+#define ICG_ABI_VERSION 2
 
 /* ---- status codes ------------------------------------------------------ */
 #define ICG_OK 0
@@ -127,6 +127,8 @@ typedef struct icg_algo_config {
     int32_t target_level;      /* L; R_L = R_0 * 2^L <= 1024 */
     int32_t max_conflict_iters;/* 0 = one axis length per level (localize.hpp:339) */
     int32_t conflict_pass;     /* 0 = ablation (localize.hpp:42, 335-336) */
+    int32_t keep_level_sets;   /* nonzero: keep every level's refined-cell and evaluated-node sets
+                                  on the context for icg_level_set (one extra bitset pass per level) */
 } icg_algo_config;
 
 /* ---- extraction result: ExtractionResult, localize.hpp:57-64 ------------- */
@@ -194,6 +196,23 @@ int icg_set_mlp(icg_context* ctx, const icg_mlp_desc* desc);
  * grid also stays resident in the context for icg_render_localized. */
 int icg_extract(icg_context* ctx, const icg_field* field, const icg_algo_config* cfg,
                 icg_extraction* out);
+
+/* Per-level sets of the last extraction / frame on this context that ran with
+ * cfg.keep_level_sets (the reference keeps them
+ * implicitly: the `to_eval` / conflict-neighbour lists of localize.hpp:331-353
+ * and the cells binarize+upsample refine, grid.hpp:133-140):
+ *   ICG_SET_EVALUATED_NODES: node indices i + n(j + n k) of the level-l grid
+ *     (n = R_l + 1) whose occupancy was evaluated at level l (level 0: every
+ *     node; the E0 list and every conflict-loop batch of localize.hpp:331-353);
+ *   ICG_SET_REFINED_CELLS: level l >= 1: cell indices ci + Rc(cj + Rc ck) of
+ *     the level-(l-1) grid (Rc = R_{l-1}) whose 8 binarized corners disagree
+ *     (the cells the level refines); level 0: empty.
+ * Sets are returned as ascending u32 lists.  *count is always set; out may be
+ * NULL (count only); capacity < count returns ICG_ECAPACITY. */
+#define ICG_SET_EVALUATED_NODES 0
+#define ICG_SET_REFINED_CELLS 1
+int icg_level_set(icg_context* ctx, int level, int which, int mem, uint32_t* out, size_t capacity,
+                  size_t* count);
 
 /* Mesh-free render through the grid localized by the last icg_extract on this
  * context (north-star renderer, following the

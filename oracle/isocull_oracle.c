@@ -639,6 +639,17 @@ static void vpush(vec_sz* v, size_t x) {
     v->v[v->n++] = x;
 }
 
+/* record the level of every node of a level-l list in the final-grid eval_level map */
+static void mark_level(orc_extract_out* out, int l, int target_level, int cells, const size_t* list, size_t n) {
+    if (!out->eval_level) return;
+    const size_t nn = (size_t)cells + 1, fn = ((size_t)cells << (target_level - l)) + 1;
+    const int sh = target_level - l;
+    for (size_t t = 0; t < n; ++t) {
+        size_t idx = list[t], i = idx % nn, j = (idx / nn) % nn, k = idx / (nn * nn);
+        out->eval_level[(i << sh) + fn * ((j << sh) + fn * (k << sh))] = (uint8_t)l;
+    }
+}
+
 int orc_extract_progressive(orc_occ_batch_fn occ, void* user, int coarsest_cells, int target_level,
                             int max_conflict_iters, int conflict_pass, orc_extract_out* out) {
     /* validate_config, localize.hpp:47-55 */
@@ -655,6 +666,14 @@ int orc_extract_progressive(orc_occ_batch_fn occ, void* user, int coarsest_cells
     uint8_t* gs = (uint8_t*)malloc(count);
     memset(gs, ICG_STATE_UNKNOWN, count);
     out->evals_per_level[0] = evaluate_full(occ, user, cells, gv, gs);
+    if (out->eval_level) {
+        size_t fnodes = ((size_t)coarsest_cells << target_level) + 1;
+        memset(out->eval_level, 0xFF, fnodes * fnodes * fnodes);
+        size_t* all = (size_t*)malloc(sizeof(size_t) * count);
+        for (size_t i = 0; i < count; ++i) all[i] = i;
+        mark_level(out, 0, target_level, cells, all, count);
+        free(all);
+    }
 
     for (int l = 1; l <= target_level; ++l) {
         int cc = cells, cn = cc + 1;
@@ -669,6 +688,8 @@ int orc_extract_progressive(orc_occ_batch_fn occ, void* user, int coarsest_cells
                     for (int d = 0; d < 8; ++d)
                         ones += gv[gidx(cn, i + (d & 1), j + ((d >> 1) & 1), k + (d >> 2))] >= 0.5f;
                     refined += (ones != 0 && ones != 8);
+                    if (out->refined_cells[l])
+                        out->refined_cells[l][(size_t)i + (size_t)cc * ((size_t)j + (size_t)cc * k)] = ones != 0 && ones != 8;
                 }
         out->refined_cells_per_level[l] = refined;
         /* bin = binarize(grid); tent = upsample_interpolate(bin) */
@@ -699,6 +720,7 @@ int orc_extract_progressive(orc_occ_batch_fn occ, void* user, int coarsest_cells
         for (size_t i = 0; i < fcount; ++i)
             if (flagged[i] && fs[i] != ICG_STATE_EVALUATED) vpush(&to_eval, i);
         out->evals_per_level[l] += evaluate_nodes(occ, user, fcells, fv, fs, to_eval.v, to_eval.n);
+        mark_level(out, l, target_level, fcells, to_eval.v, to_eval.n);
         /* conflict pass, localize.hpp:333-354 */
         uint8_t* queued = (uint8_t*)calloc(fcount, 1);
         vec_sz newly = {0};
@@ -743,6 +765,7 @@ int orc_extract_progressive(orc_occ_batch_fn occ, void* user, int coarsest_cells
                 break;
             }
             out->evals_per_level[l] += evaluate_nodes(occ, user, fcells, fv, fs, next.v, next.n);
+            mark_level(out, l, target_level, fcells, next.v, next.n);
             out->conflict_iters_per_level[l] += 1;
             free(newly.v);
             newly = next;

@@ -134,6 +134,13 @@ typedef struct orc_extract_out {
     uint32_t conflict_iters_per_level[16];
     int conflict_warning;
     double wall_seconds;
+    /* optional per-level sets (NULL = not requested):
+     * eval_level: (R_L+1)^3 bytes over the FINAL grid; the level at which the node at that
+     *   position was evaluated (each physical node is evaluated at most once), 0xFF = never;
+     * refined_cells[l], l >= 1: R_{l-1}^3 bytes over the level-(l-1) cells, 1 = the cell's 8
+     *   binarized corners disagree (the cells level l refines). */
+    uint8_t* eval_level;
+    uint8_t* refined_cells[16];
 } orc_extract_out;
 
 int orc_extract_progressive(orc_occ_batch_fn occ, void* user, int coarsest_cells,

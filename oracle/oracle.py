@@ -18,8 +18,27 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORC_PATH = os.path.join(HERE, "liborc.so")
 REF_PATH = os.path.join(HERE, "_ref", "libisocull_ref.so")
 
-# struct layouts shared with the product ABI header (plain data types only)
-from paper_2007_13988_b200.abi import icg_camera, icg_primitive  # noqa: E402
+
+# Plain-data struct layouts of include/isocull_b200.h (the C oracle includes that header for its
+# types; nothing of the product package is imported here).
+class icg_primitive(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("rotated", C.c_int32), ("center", C.c_double * 3), ("a", C.c_double * 3),
+                ("b", C.c_double * 3), ("radius", C.c_double), ("half", C.c_double * 3), ("major", C.c_double),
+                ("minor", C.c_double), ("inv_rotation", C.c_double * 9)]
+
+
+class icg_camera(C.Structure):
+    _fields_ = [("rotation", C.c_double * 9), ("translation", C.c_double * 3), ("scale", C.c_double)]
+
+
+def _as(cls, obj):
+    """obj as an instance of the oracle's struct `cls` (the product's ctypes structs have the
+    same layout: copied by value)."""
+    if isinstance(obj, cls):
+        return obj
+    if C.sizeof(type(obj)) != C.sizeof(cls):
+        raise TypeError(f"{type(obj).__name__} does not have the layout of {cls.__name__}")
+    return cls.from_buffer_copy(bytes(obj))
 
 f32p = C.POINTER(C.c_float)
 f64p = C.POINTER(C.c_double)
@@ -60,7 +79,7 @@ class orc_extract_out(C.Structure):
     _fields_ = [("values", f32p), ("states", u8p), ("binarized", u8p), ("evals_per_level", C.c_uint64 * 16),
                 ("total_evals", C.c_uint64), ("refined_cells_per_level", C.c_uint64 * 16),
                 ("conflict_iters_per_level", C.c_uint32 * 16), ("conflict_warning", C.c_int),
-                ("wall_seconds", C.c_double)]
+                ("wall_seconds", C.c_double), ("eval_level", u8p), ("refined_cells", u8p * 16)]
 
 
 class orc_render_out(C.Structure):
@@ -162,7 +181,7 @@ def fnptr(lib: C.CDLL, name: str) -> int:
 # Fields
 # ---------------------------------------------------------------------------
 def prim_array(prims):
-    arr = (icg_primitive * max(1, len(prims)))(*prims)
+    arr = (icg_primitive * max(1, len(prims)))(*[_as(icg_primitive, p) for p in prims])
     return arr
 
 
@@ -283,13 +302,39 @@ def _result(o, L, vals, sts, binz):
                 conflict_warning=bool(o.conflict_warning), wall_seconds=o.wall_seconds)
 
 
-def extract_progressive(fld, coarsest: int, level: int, max_conflict_iters: int = 0, conflict_pass: bool = True):
+def extract_progressive(fld, coarsest: int, level: int, max_conflict_iters: int = 0, conflict_pass: bool = True,
+                        level_sets: bool = False):
+    """level_sets: also return r["evaluated_sets"][l] (ascending node indices of the level-l grid
+    evaluated at level l) and r["refined_sets"][l] (ascending cell indices of the level-(l-1) grid
+    whose binarized corners disagree; empty at l = 0)."""
     o, vals, sts, binz = _new_out(coarsest << level)
+    keep = []
+    if level_sets:
+        n = (coarsest << level) + 1
+        ev = np.empty(n ** 3, np.uint8)
+        o.eval_level = _p(ev, C.c_uint8)
+        keep.append(ev)
+        for l in range(1, level + 1):
+            rc_ = coarsest << (l - 1)
+            a = np.zeros(rc_ ** 3, np.uint8)
+            o.refined_cells[l] = _p(a, C.c_uint8)
+            keep.append(a)
     rc = orc().orc_extract_progressive(fld.batch_fn, fld.user, coarsest, level, max_conflict_iters,
                                        1 if conflict_pass else 0, C.byref(o))
     if rc:
         raise ValueError("orc_extract_progressive: invalid config")
-    return _result(o, level, vals, sts, binz)
+    r = _result(o, level, vals, sts, binz)
+    if level_sets:
+        n = (coarsest << level) + 1
+        r["evaluated_sets"] = []
+        for l in range(level + 1):
+            f = np.flatnonzero(ev == l)
+            s = level - l
+            nl = (coarsest << l) + 1
+            i, j, k = (f % n) >> s, ((f // n) % n) >> s, (f // (n * n)) >> s
+            r["evaluated_sets"].append((i + nl * (j + nl * k)).astype(np.uint32))
+        r["refined_sets"] = [np.zeros(0, np.uint32)] + [np.flatnonzero(a).astype(np.uint32) for a in keep[1:]]
+    return r
 
 
 def extract_brute(fld, coarsest: int, level: int):
@@ -321,6 +366,7 @@ def render_first_crossing(values: np.ndarray, cells: int, cam: icg_camera, width
         out.surface_pts = _p(spts, C.c_double)
     bg = np.asarray(background, np.float32)
     v = np.ascontiguousarray(values, np.float32)
+    cam = _as(icg_camera, cam)
     rc = orc().orc_render_first_crossing(_p(v, C.c_float), cells, C.byref(cam), width, height, _p(bg, C.c_float),
                                          tex.tex_fn if tex else None, tex.user if tex else None, C.byref(out))
     if rc:
@@ -343,6 +389,14 @@ def gen_capsules(seed: int, n: int = 15):
     arr = (icg_primitive * n)()
     orc().orc_gen_capsules(seed, n, arr)
     return list(arr)
+
+
+def gen_feature_map(seed: int, c: int = 256, h: int = 128, w: int = 128) -> np.ndarray:
+    """C x H x W float32 map of Rng(seed) normals in generation order (the product's
+    icg_gen_normals draws the same sequence)."""
+    out = np.empty(c * h * w)
+    orc().orc_rng_normals(seed, out.size, _p(out, C.c_double))
+    return out.astype(np.float32).reshape(c, h, w)
 
 
 def gen_mlp(seed: int, which: int):

@@ -23,6 +23,8 @@ ICG_PREC_FP32, ICG_PREC_BF16, ICG_PREC_FP32_SIMT = 0, 1, 2
 ICG_MLP_GEOMETRY, ICG_MLP_TEXTURE = 0, 1
 ICG_MLP_LAYERS = 5
 ICG_VARIANT_BRUTE, ICG_VARIANT_PROGRESSIVE = 0, 3
+ICG_SET_EVALUATED_NODES, ICG_SET_REFINED_CELLS = 0, 1
+ICG_ABI_VERSION = 2
 
 f32p = C.POINTER(C.c_float)
 u8p = C.POINTER(C.c_uint8)
@@ -82,6 +84,7 @@ class icg_algo_config(C.Structure):
         ("target_level", C.c_int32),
         ("max_conflict_iters", C.c_int32),
         ("conflict_pass", C.c_int32),
+        ("keep_level_sets", C.c_int32),
     ]
 
 
@@ -163,6 +166,8 @@ SIGNATURES = [
     ("icg_frame", C.c_int,
      [ctx_p, C.POINTER(icg_field), C.POINTER(icg_algo_config), C.POINTER(icg_camera), C.c_int, C.c_int, f32p,
       C.POINTER(icg_extraction), C.POINTER(icg_image)]),
+    ("icg_level_set", C.c_int,
+     [ctx_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint32), C.c_size_t, C.POINTER(C.c_size_t)]),
     ("icg_occupancy_batch", C.c_int, [ctx_p, C.POINTER(icg_field), f64p, C.c_size_t, C.c_int, f32p]),
     ("icg_texture_batch", C.c_int, [ctx_p, C.POINTER(icg_field), f64p, C.c_size_t, C.c_int, f32p]),
     ("icg_compare_iou", C.c_int, [ctx_p, u8p, u8p, C.c_size_t, C.c_int, f64p]),

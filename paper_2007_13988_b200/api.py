@@ -119,6 +119,7 @@ class AlgoConfig:
     target_level: int = 3
     max_conflict_iters: int = 0
     conflict_pass: bool = True
+    keep_level_sets: bool = False  # keep per-level refined-cell / evaluated-node sets (Context.level_set)
 
     def target_cells(self) -> int:
         return self.coarsest_cells << self.target_level
@@ -128,7 +129,7 @@ class AlgoConfig:
         if v is None:
             raise ValueError(f"unknown variant '{self.variant}'")
         return abi.icg_algo_config(v, self.coarsest_cells, self.target_level, self.max_conflict_iters,
-                                   1 if self.conflict_pass else 0)
+                                   1 if self.conflict_pass else 0, 1 if self.keep_level_sets else 0)
 
 
 @dataclass
@@ -270,6 +271,21 @@ class Context:
                                    _ptr(bg, C.c_float), C.byref(ext), C.byref(img)))
         return _extraction(ext, cfg, vals, sts, binz), _image(img, width, height, bufs)
 
+    def level_set(self, level: int, which: str) -> np.ndarray:
+        """Ascending u32 list of a per-level set of the last extraction that ran with
+        keep_level_sets: which = "evaluated" (node indices of the level-l grid evaluated at level l)
+        or "refined" (cell indices of the level-(l-1) grid whose 8 binarized corners disagree)."""
+        w = {"evaluated": abi.ICG_SET_EVALUATED_NODES, "refined": abi.ICG_SET_REFINED_CELLS}.get(which)
+        if w is None:
+            raise ValueError(f"unknown level set '{which}'")
+        n = C.c_size_t()
+        _check(self._lib.icg_level_set(self.h, level, w, abi.ICG_MEM_HOST, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.uint32)
+        if n.value:
+            _check(self._lib.icg_level_set(self.h, level, w, abi.ICG_MEM_HOST, _ptr(out, C.c_uint32), n.value,
+                                           C.byref(n)))
+        return out
+
     def occupancy_batch(self, fld: _Field, points: np.ndarray) -> np.ndarray:
         pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
         out = np.empty(len(pts), np.float32)
@@ -384,7 +400,8 @@ def extract(ctx: Context, fld: _Field, cfg: AlgoConfig) -> ExtractionResult:
 
 
 def extract_progressive(ctx: Context, fld: _Field, cfg: AlgoConfig) -> ExtractionResult:
-    cfg = AlgoConfig("progressive", cfg.coarsest_cells, cfg.target_level, cfg.max_conflict_iters, cfg.conflict_pass)
+    cfg = AlgoConfig("progressive", cfg.coarsest_cells, cfg.target_level, cfg.max_conflict_iters, cfg.conflict_pass,
+                     cfg.keep_level_sets)
     return ctx.extract(fld, cfg)
 
 

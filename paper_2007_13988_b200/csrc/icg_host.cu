@@ -142,6 +142,12 @@ struct icg_context {
     DBuf depth, rgb, mask, surfk, spts, spx;
     // last extraction
     int last_cells = 0, last_buf = -1;
+    // per-level sets kept by an extraction with cfg.keep_level_sets (icg_level_set):
+    // [0][l] nodes evaluated at level l, [1][l] refined cells of level l (bitsets)
+    DBuf lvl_bits[2][ICG_MAX_LEVELS];
+    bool kept_valid = false;
+    icg_algo_config kept_cfg{};
+    DBuf set_scratch, set_list, set_total, set_bits;
     // instrumentation
     struct Mark {
         int kind;  // 0 geo mlp, 1 tex mlp, 2 dense, 3 render
@@ -673,6 +679,16 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
             }
             c->launches += 1;
         }
+        if (cfg->keep_level_sets) {
+            const size_t ncell = (size_t)cells * cells * cells;
+            if (int r = c->lvl_bits[0][l].ensure(words(nf) * 4 + 16)) return r;
+            if (int r = c->lvl_bits[1][l].ensure(words(ncell) * 4 + 16)) return r;
+            if (int r = launch_level_eval_bits(lb.fs, lb.cs, cells, c->lvl_bits[0][l].as<uint32_t>(), c->stream))
+                return r;
+            ICG_CUDA_TRY(cudaMemcpyAsync(c->lvl_bits[1][l].p, c->mixed.p, words(ncell) * 4, cudaMemcpyDeviceToDevice,
+                                         c->stream));
+            c->launches += 1;
+        }
         b ^= 1;
         cells = fcells;
     }
@@ -972,9 +988,12 @@ int icg_destroy(icg_context* c) {
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
                    &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi, &c->geo_pair_f16, &c->geo_pair_f16_hi,
                    &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx, &c->colrec, &c->cmap, &c->collist, &c->colcnt, &c->sorted, &c->tail_scratch,
+                   &c->set_scratch, &c->set_list, &c->set_total, &c->set_bits,
                    &c->geo_fact_stream[0][0], &c->geo_fact_stream[0][1], &c->geo_fact_stream[1][0],
                    &c->geo_fact_stream[1][1]};
     for (DBuf* b : all) b->release();
+    for (auto& lv : c->lvl_bits)
+        for (DBuf& b : lv) b.release();
     for (int l = 0; l < 5; ++l) {
         c->geo_wt[l].release();
         c->geo_wrow[l].release();
@@ -1150,12 +1169,71 @@ int icg_extract(icg_context* c, const icg_field* field, const icg_algo_config* c
     if (int r = finish_extract_outputs(c, cfg, out)) return r;
     ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     fill_extraction_scalars(c, cfg, out, elapsed(c));
+    c->kept_valid = cfg->keep_level_sets != 0;
+    c->kept_cfg = *cfg;
     prof_extract_done(c, cfg);
     prof_collect(c);
     if (c->prof_on) {
         c->prof.frame_ms += elapsed(c) * 1e3;
         c->prof.frames += 1;
     }
+    return ICG_OK;
+}
+
+int icg_level_set(icg_context* c, int level, int which, int mem, uint32_t* out, size_t cap, size_t* count) {
+    if (!c || !count) return einval("level_set: null argument");
+    *count = 0;
+    if (which != ICG_SET_EVALUATED_NODES && which != ICG_SET_REFINED_CELLS) return einval("level_set: unknown set");
+    if (mem != ICG_MEM_HOST && mem != ICG_MEM_DEVICE) return einval("level_set: mem must be ICG_MEM_HOST or ICG_MEM_DEVICE");
+    if (!c->kept_valid)
+        return einval("level_set: the last extraction on this context did not run with keep_level_sets");
+    const icg_algo_config& k = c->kept_cfg;
+    if (level < 0 || level > k.target_level) return einval("level_set: level out of range");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    const int cells = k.coarsest_cells << level;
+    const uint32_t* bits = nullptr;
+    size_t nbits = 0;
+    const bool brute = k.variant == ICG_VARIANT_BRUTE;
+    if (which == ICG_SET_REFINED_CELLS) {
+        if (level == 0 || brute) return ICG_OK;  // no refinement: empty
+        nbits = (size_t)(cells / 2) * (cells / 2) * (cells / 2);
+        bits = c->lvl_bits[1][level].as<uint32_t>();
+    } else if (brute ? level == k.target_level : level == 0) {
+        nbits = nodes3(cells);  // dense evaluation: every node
+        if (int r = c->set_bits.ensure(words(nbits) * 4 + 16)) return r;
+        if (int r = launch_all_bits(c->set_bits.as<uint32_t>(), nbits, c->stream)) return r;
+        bits = c->set_bits.as<uint32_t>();
+    } else if (brute) {
+        return ICG_OK;  // brute force evaluates only the target level
+    } else {
+        nbits = nodes3(cells);
+        bits = c->lvl_bits[0][level].as<uint32_t>();
+    }
+    if (int r = c->set_scratch.ensure(bits_to_list_scratch_words(nbits) * 4)) return r;
+    if (int r = c->set_total.ensure(16)) return r;
+    if (int r = launch_bits_to_list(bits, nbits, c->set_scratch.as<uint32_t>(), nullptr, c->set_total.as<unsigned>(),
+                                    c->stream))
+        return r;
+    unsigned total = 0;
+    ICG_CUDA_TRY(cudaMemcpyAsync(&total, c->set_total.p, 4, cudaMemcpyDeviceToHost, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    *count = total;
+    if (!out || total == 0) return ICG_OK;
+    if (cap < total) {
+        set_error("level_set: capacity " + std::to_string(cap) + " < " + std::to_string(total) + " entries");
+        return ICG_ECAPACITY;
+    }
+    uint32_t* dst = out;
+    if (mem == ICG_MEM_HOST) {
+        if (int r = c->set_list.ensure((size_t)total * 4)) return r;
+        dst = c->set_list.as<uint32_t>();
+    }
+    if (int r = launch_bits_to_list(bits, nbits, c->set_scratch.as<uint32_t>(), dst, c->set_total.as<unsigned>(),
+                                    c->stream))
+        return r;
+    if (mem == ICG_MEM_HOST)
+        ICG_CUDA_TRY(cudaMemcpyAsync(out, dst, (size_t)total * 4, cudaMemcpyDeviceToHost, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     return ICG_OK;
 }
 
@@ -1302,6 +1380,8 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
         ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
     }
     double secs = elapsed(c);
+    c->kept_valid = cfg->keep_level_sets != 0;
+    c->kept_cfg = *cfg;
     prof_extract_done(c, cfg);
     prof_render_done(c, W, H);
     prof_collect(c);

@@ -273,6 +273,13 @@ int launch_sort_by_column(const uint32_t* list, const unsigned* count, int cells
 // node list of a dense (cells+1)^3 grid in column order: t -> node (t / n1) + plane * (t % n1)
 int launch_dense_column_list(int cells, uint32_t* list, cudaStream_t s);
 int launch_binarize(const float* v, uint8_t* out, size_t n, cudaStream_t s);
+// per-level sets (icg_level_set): nodes evaluated during a level (fine states vs the coarse states
+// the even nodes carried), every bit set, and the ascending list of a bitset's set bits
+int launch_level_eval_bits(const uint8_t* fs, const uint8_t* cs, int rc, uint32_t* bits, cudaStream_t s);
+int launch_all_bits(uint32_t* bits, size_t nbits, cudaStream_t s);
+size_t bits_to_list_scratch_words(size_t nbits);
+int launch_bits_to_list(const uint32_t* bits, size_t nbits, uint32_t* scratch, uint32_t* list, unsigned* total,
+                        cudaStream_t s);
 int launch_iou(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* inter_union, cudaStream_t s);
 int launch_fill_states(uint8_t* s, size_t n, uint8_t v, cudaStream_t st);
 

@@ -211,8 +211,8 @@ k_count_words(const uint32_t* __restrict__ sel, unsigned nwords, uint32_t* __res
 }
 
 // ---- exclusive scan of the per-CTA counts (single block) -----------------------
-__global__ void __launch_bounds__(1024)
-k_scan_blocks(uint32_t* __restrict__ counts, unsigned nblocks, DevCounters* ctr, int level) {
+// in place; returns the total (valid in every thread)
+__device__ unsigned scan_block_counts(uint32_t* __restrict__ counts, unsigned nblocks) {
     __shared__ unsigned warp_sums[32];
     __shared__ unsigned carry;
     if (threadIdx.x == 0) carry = 0;
@@ -246,15 +246,26 @@ k_scan_blocks(uint32_t* __restrict__ counts, unsigned nblocks, DevCounters* ctr,
         if (threadIdx.x == 1023) carry = excl + v;
         __syncthreads();
     }
+    return carry;
+}
+
+__global__ void __launch_bounds__(1024)
+k_scan_blocks(uint32_t* __restrict__ counts, unsigned nblocks, DevCounters* ctr, int level) {
+    const unsigned total = scan_block_counts(counts, nblocks);
     if (threadIdx.x == 0) {
-        ctr->list_count = carry;
-        ctr->e0[level] = carry;
-        ctr->evals[level] += carry;
+        ctr->list_count = total;
+        ctr->e0[level] = total;
+        ctr->evals[level] += total;
         ctr->cf_count[0] = 0;
         ctr->cf_count[1] = 0;
         ctr->nx_count[0] = 0;
         ctr->nx_count[1] = 0;
     }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_total(uint32_t* __restrict__ counts, unsigned nblocks, unsigned* total) {
+    const unsigned t = scan_block_counts(counts, nblocks);
+    if (threadIdx.x == 0) *total = t;
 }
 
 // ---- write the ascending E0 list: same CTA/word partition as k_fine_words -------
@@ -533,6 +544,69 @@ int launch_dense_column_list(int cells, uint32_t* list, cudaStream_t s) {
     const size_t total = ((size_t)cells + 1) * ((size_t)cells + 1) * ((size_t)cells + 1);
     const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 148 * 16);
     k_dense_column_list<<<blocks, 256, 0, s>>>(cells, list);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
+// ---- per-level sets kept for icg_level_set -------------
+// nodes of the fine grid evaluated during this level: evaluated now, and not an even node that
+// carried an evaluated coarse state (carry_scalars, localize.hpp:110-122)
+__global__ void k_level_eval_bits(const uint8_t* __restrict__ fs, const uint8_t* __restrict__ cs, int rc,
+                                  uint32_t* __restrict__ bits) {
+    const unsigned fn = 2u * rc + 1u, cn = rc + 1u;
+    const unsigned long long nf = (unsigned long long)fn * fn * fn;
+    const unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool b = false;
+    if (idx < nf) {
+        b = fs[idx] == ICG_STATE_EVALUATED;
+        if (b) {
+            const unsigned jk = (unsigned)(idx / fn), i = (unsigned)(idx - (unsigned long long)jk * fn);
+            const unsigned k = jk / fn, j = jk - k * fn;
+            if (!((i | j | k) & 1u)) b = cs[(i >> 1) + cn * ((j >> 1) + (unsigned long long)cn * (k >> 1))] != ICG_STATE_EVALUATED;
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, b);
+    if ((threadIdx.x & 31) == 0 && idx < nf) bits[idx >> 5] = m;
+}
+
+int launch_level_eval_bits(const uint8_t* fs, const uint8_t* cs, int rc, uint32_t* bits, cudaStream_t s) {
+    const size_t fn = 2 * (size_t)rc + 1, nf = fn * fn * fn;
+    k_level_eval_bits<<<(unsigned)((nf + 255) / 256), 256, 0, s>>>(fs, cs, rc, bits);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
+// every bit of a flat bitset of nbits bits set (the dense level-0 / brute-force evaluation)
+__global__ void k_all_bits(uint32_t* __restrict__ bits, unsigned long long nbits) {
+    const unsigned long long w = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x, nw = (nbits + 31) / 32;
+    if (w < nw) bits[w] = (w + 1) * 32 <= nbits ? 0xffffffffu : (1u << (nbits & 31)) - 1u;
+}
+
+int launch_all_bits(uint32_t* bits, size_t nbits, cudaStream_t s) {
+    const size_t nw = (nbits + 31) / 32;
+    k_all_bits<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(bits, nbits);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
+size_t bits_to_list_scratch_words(size_t nbits) {
+    const size_t nw = (nbits + 31) / 32;
+    return (nw + kWordsPerCta - 1) / kWordsPerCta + 2;
+}
+
+// ascending list of the set bits of a flat bitset (count / scan / ordered write, the E0 compaction);
+// *total (device) = number of set bits; list must hold them all
+int launch_bits_to_list(const uint32_t* bits, size_t nbits, uint32_t* scratch, uint32_t* list, unsigned* total,
+                        cudaStream_t s) {
+    const unsigned nwords = (unsigned)((nbits + 31) / 32);
+    const unsigned nblocks = (nwords + kWordsPerCta - 1) / kWordsPerCta;
+    if (nblocks == 0) {
+        ICG_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(unsigned), s));
+        return ICG_OK;
+    }
+    k_count_words<<<nblocks, kWriteThreads, 0, s>>>(bits, nwords, scratch);
+    k_scan_total<<<1, 1024, 0, s>>>(scratch, nblocks, total);
+    if (list) k_write_words<<<nblocks, kWriteThreads, 0, s>>>(bits, nwords, scratch, list);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }

@@ -30,10 +30,10 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_struct_sizes():
     lib = abi.lib()
-    assert lib.icg_abi_version() == 1
+    assert lib.icg_abi_version() == abi.ICG_ABI_VERSION == 2
     # spot-check layouts against the C compiler's view
     assert C.sizeof(abi.icg_primitive) == 8 + 8 * 24
-    assert C.sizeof(abi.icg_algo_config) == 20
+    assert C.sizeof(abi.icg_algo_config) == 24
     assert C.sizeof(abi.icg_camera) == 13 * 8
 
 
@@ -66,3 +66,18 @@ def test_config_validation_errors_without_gpu():
                                    api.ExtractionResult(0, None, None, None, [], 100, [], [], False, 0.0)) == 10.0
     with pytest.raises(ValueError):
         api.compare_iou(np.zeros(3, np.uint8), np.zeros(4, np.uint8))
+
+
+def test_argument_validation_without_gpu():
+    lib = abi.lib()
+    a = np.ones(8, np.uint8)
+    out = C.c_double()
+    p = a.ctypes.data_as(abi.u8p)
+    # device arrays need a context (no host dereference of device pointers); unknown mem is rejected
+    assert lib.icg_compare_iou(None, p, p, 8, abi.ICG_MEM_DEVICE, C.byref(out)) == abi.ICG_EINVAL
+    assert lib.icg_compare_iou(None, p, p, 8, 7, C.byref(out)) == abi.ICG_EINVAL
+    assert lib.icg_compare_iou(None, p, p, 8, abi.ICG_MEM_HOST, C.byref(out)) == abi.ICG_OK and out.value == 1.0
+    n = C.c_size_t(5)
+    assert lib.icg_level_set(None, 0, abi.ICG_SET_EVALUATED_NODES, abi.ICG_MEM_HOST, None, 0,
+                             C.byref(n)) == abi.ICG_EINVAL
+    assert lib.icg_memcpy(None, None, None, 0, 0, 0) == abi.ICG_EINVAL

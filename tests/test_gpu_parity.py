@@ -539,3 +539,71 @@ def test_points_in_m_factored_pass_matches(pifu_inputs, monkeypatch, chain_fact)
     i, j, k = idx % n, (idx // n) % n, idx // (n * n)
     pts = np.stack([-1 + 2 * i / 256.0, -1 + 2 * j / 256.0, 1 - 2 * k / 256.0], 1)
     assert np.abs(a.values[idx] - m.occupancy(pts)).max() <= OCC_TOL_FP32
+
+
+@pytest.mark.gpu
+def test_level_sets_config0_match_oracle(gpu_ctx):
+    """icg_level_set: per-level refined-cell and evaluated-node sets of the
+    config-0 extraction equal the oracle's (which records them while localizing), for the
+    progressive and the brute-force variants, host and device outputs."""
+    caps = api.gen_capsules(42)
+    f = api.AnalyticField(caps, 0.02)
+    g = gpu_ctx.extract(f, api.AlgoConfig("progressive", 32, 3, keep_level_sets=True))
+    o = O.extract_progressive(O.Analytic(caps, 0.02, threads=8), 32, 3, level_sets=True)
+    for l in range(4):
+        ev = gpu_ctx.level_set(l, "evaluated")
+        rf = gpu_ctx.level_set(l, "refined")
+        assert np.array_equal(ev, o["evaluated_sets"][l]), l
+        assert np.array_equal(rf, o["refined_sets"][l]), l
+        assert len(ev) == g.evals_per_level[l] and len(rf) == g.refined_cells_per_level[l]
+    # capacity handling and device output through the raw ABI
+    import ctypes as C
+    n = C.c_size_t()
+    lib = abi.lib()
+    small = np.empty(4, np.uint32)
+    assert lib.icg_level_set(gpu_ctx.h, 3, abi.ICG_SET_EVALUATED_NODES, abi.ICG_MEM_HOST,
+                             small.ctypes.data_as(C.POINTER(C.c_uint32)), 4, C.byref(n)) == abi.ICG_ECAPACITY
+    assert n.value == g.evals_per_level[3]
+    dptr = gpu_ctx.device_alloc(4 * n.value)
+    assert lib.icg_level_set(gpu_ctx.h, 3, abi.ICG_SET_EVALUATED_NODES, abi.ICG_MEM_DEVICE,
+                             C.cast(C.c_void_p(dptr), C.POINTER(C.c_uint32)), n.value, C.byref(n)) == abi.ICG_OK
+    back = np.empty(n.value, np.uint32)
+    gpu_ctx.memcpy(back.ctypes.data, dptr, 4 * n.value, abi.ICG_MEM_HOST, abi.ICG_MEM_DEVICE)
+    gpu_ctx.device_free(dptr)
+    assert np.array_equal(back, o["evaluated_sets"][3])
+    # brute force: every node at the target level, nothing refined
+    gpu_ctx.extract(f, api.AlgoConfig("brute", 8, 2, keep_level_sets=True))
+    assert np.array_equal(gpu_ctx.level_set(2, "evaluated"), np.arange(33 ** 3, dtype=np.uint32))
+    assert len(gpu_ctx.level_set(2, "refined")) == 0 and len(gpu_ctx.level_set(0, "evaluated")) == 0
+    # an extraction without keep_level_sets drops them
+    gpu_ctx.extract(f, api.AlgoConfig("progressive", 8, 2))
+    with pytest.raises(ValueError):
+        gpu_ctx.level_set(1, "evaluated")
+
+
+@pytest.mark.gpu
+def test_frame_graph_survives_shape_changes(pifu_inputs):
+    """A captured frame graph must not be replayed after the context's work buffers moved
+    (a larger grid / image / feature map in between): frame(A) x3 (graph captured), then a larger
+    frame B and a larger extraction, then frame(A) again — every output equals a fresh context's."""
+    inp = pifu_inputs
+    ctx = api.Context(0)
+    ctx.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+    ctx.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+    fa = api.PifuField(inp["fmap"][:, :64, :64], inp["caps"], 50.0, abi.ICG_PREC_FP32)
+    fb = api.PifuField(inp["fmap"], inp["caps"], 50.0, abi.ICG_PREC_FP32)
+    cam = api.CameraSpec.from_angles(90, 0)
+    ca, cb = api.AlgoConfig("progressive", 16, 2), api.AlgoConfig("progressive", 16, 3)
+    first = [ctx.frame(fa, ca, cam, 64, 64, want_grid=True) for _ in range(3)][-1]
+    ctx.frame(fb, cb, cam, 256, 256)
+    ctx.extract(fb, api.AlgoConfig("progressive", 32, 3))
+    again = [ctx.frame(fa, ca, cam, 64, 64, want_grid=True) for _ in range(3)]
+    ctx.close()
+    with api.Context(0) as fresh:
+        fresh.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+        fresh.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+        ref = fresh.frame(fa, ca, cam, 64, 64, want_grid=True)
+    for ext, img in [first] + again:
+        assert ext.cells == 64
+        assert np.array_equal(ext.values, ref[0].values) and np.array_equal(ext.states, ref[0].states)
+        assert np.array_equal(img.rgb, ref[1].rgb) and np.array_equal(img.surface_k, ref[1].surface_k)
