@@ -9,6 +9,7 @@
 
 #include <math.h>
 #include <pthread.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
@@ -759,10 +760,29 @@ int orc_extract_progressive(orc_occ_batch_fn occ, void* user, int coarsest_cells
                             vpush(&next, nb);
                         }
             }
+            const uint64_t conflicts_n_dump = conflicts.n;
+            if (getenv("ORC_CHAIN_DUMP")) {
+                FILE* df = fopen(getenv("ORC_CHAIN_DUMP"), "ab");
+                if (df) {
+                    uint64_t hdr[4] = {(uint64_t)l, (uint64_t)iter | (1ull << 32), conflicts.n, 0};
+                    fwrite(hdr, 8, 4, df);
+                    fwrite(conflicts.v, sizeof(size_t), conflicts.n, df);
+                    fclose(df);
+                }
+            }
             free(conflicts.v);
             if (next.n == 0) {
                 free(next.v);
                 break;
+            }
+            if (getenv("ORC_CHAIN_DUMP")) {  /* dev aid: per-iteration conflict / next lists */
+                FILE* df = fopen(getenv("ORC_CHAIN_DUMP"), "ab");
+                if (df) {
+                    uint64_t hdr[4] = {(uint64_t)l, (uint64_t)iter, conflicts_n_dump, next.n};
+                    fwrite(hdr, 8, 4, df);
+                    fwrite(next.v, sizeof(size_t), next.n, df);
+                    fclose(df);
+                }
             }
             out->evals_per_level[l] += evaluate_nodes(occ, user, fcells, fv, fs, next.v, next.n);
             mark_level(out, l, target_level, fcells, next.v, next.n);

@@ -111,7 +111,7 @@ struct icg_context {
     // column-factored geometry field (FACT / COLS streams, [part][x3 ? 0 : 1])
     DBuf geo_fact_stream[2][2];
     alignas(64) unsigned char geo_fact_tmap[2][2][128] = {};
-    alignas(64) unsigned char geo_fact2_tmap[128] = {};  // the FACT x3 stream in 16 KB (hi / lo) boxes
+    alignas(64) unsigned char geo_fact2_tmap[2][128] = {};  // k_fact2: the FACT [x3, hi] streams in 16 KB boxes
     bool geo_fact = false, use_fact = true;
     bool fact_used = false;  // the last extraction ran its bulk batches column-factored
     DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
@@ -408,9 +408,9 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
     if (int r = launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][xi], cj, c->colrec.as<float>(), max_cols,
                                       xi == 0, c->stream))
         return r;
-    int r = (c->use_fact2 && xi == 0)
-                ? launch_pifu_fact2(fd, c->geo_tc, c->geo_fact2_tmap, pj, c->colrec.as<float>(), cm, max_points,
-                                    c->stream)
+    int r = c->use_fact2
+                ? launch_pifu_fact2(fd, c->geo_tc, c->geo_fact2_tmap[xi], pj, c->colrec.as<float>(), cm, max_points,
+                                    xi == 0, c->stream)
                 : launch_pifu_pair_fact(fd, c->geo_tc, c->geo_fact_tmap[0][xi], pj, c->colrec.as<float>(), cm,
                                         max_points, xi == 0, c->stream);
     prof_end(c, slot);
@@ -424,6 +424,7 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
 // and evaluated by k_fact2.  Every launch is sized by device counts; the claim and k_fact2 exit on
 // device unless the batch is their class (job.min_count).
 int run_chain_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
+    const int xi = fd.precision == ICG_PREC_FP32 ? 0 : 1;
     const size_t n1 = (size_t)job.cells + 1, plane = n1 * n1;
     DevCounters* ctr = c->ctr.as<DevCounters>();
     if (int r = launch_col_claim(job.list, job.count, job.cells, c->cmap.as<int>(), c->collist.as<uint32_t>(), ctr,
@@ -438,13 +439,13 @@ int run_chain_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsig
     cj.count = &ctr->ncols;
     cj.base = &ctr->ncols_base;
     const unsigned max_cols = (unsigned)std::min<size_t>(plane, max_points);
-    if (int r = launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][0], cj, c->colrec.as<float>(), max_cols, true,
-                                      c->stream))
+    if (int r = launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][xi], cj, c->colrec.as<float>(), max_cols,
+                                      xi == 0, c->stream))
         return r;
     EvalJob pj = job;
     pj.list = c->sorted.as<uint32_t>();
-    int r = launch_pifu_fact2(fd, c->geo_tc, c->geo_fact2_tmap, pj, c->colrec.as<float>(), c->cmap.as<int>(), max_points,
-                              c->stream);
+    int r = launch_pifu_fact2(fd, c->geo_tc, c->geo_fact2_tmap[xi], pj, c->colrec.as<float>(), c->cmap.as<int>(),
+                              max_points, xi == 0, c->stream);
     c->launches += 6;
     return r;
 }
@@ -601,7 +602,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
             const unsigned mid_max = 74u * 64u;
             // batches beyond one wave of 128-point pair tiles: column-factored (k_fact2, 256-point tiles)
             const bool x3c = fd.precision == ICG_PREC_FP32;
-            const unsigned big_max = (c->chain_fact && c->use_fact2 && x3c) ? c->chain_fact_min : 0u;
+            const unsigned big_max = (c->chain_fact && c->use_fact2) ? c->chain_fact_min : 0u;
             int prev_mask = -1;
             for (int it = 0; it < unroll; ++it) {
                 int p = it & 1;
@@ -1142,8 +1143,10 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
             ICG_CUDA_TRY(cudaMemcpy(c->geo_fact_stream[part][1].p, sh.data(), bh, cudaMemcpyHostToDevice));
             if (int r = pair_make_tmap(c->geo_fact_stream[part][0].p, bx, c->geo_fact_tmap[part][0])) return r;
             if (int r = pair_make_tmap(c->geo_fact_stream[part][1].p, bh, c->geo_fact_tmap[part][1])) return r;
-            if (part == 0)
-                if (int r = pair_make_tmap(c->geo_fact_stream[0][0].p, bx, c->geo_fact2_tmap, 128)) return r;
+            if (part == 0) {
+                if (int r = pair_make_tmap(c->geo_fact_stream[0][0].p, bx, c->geo_fact2_tmap[0], 128)) return r;
+                if (int r = pair_make_tmap(c->geo_fact_stream[0][1].p, bh, c->geo_fact2_tmap[1], 128)) return r;
+            }
         }
         c->geo_fact = true;
     }

@@ -189,8 +189,9 @@ int launch_pifu_pair_cols(const FieldDev& f, const TcMlp& geo, const void* tmap,
 int launch_pifu_pair_eval_small(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
                                 unsigned max_points, bool x3, cudaStream_t s);
 // k_fact2.cu: the same pass with activations as the A operand (M = 256 points), weights as B
+// x3: bf16x3 (the FACT x3 stream in 128-row hi / lo stages); else bf16 (the hi stream, 128-row stages)
 int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job, const float* records,
-                      const int* cmap, unsigned max_points, cudaStream_t s);
+                      const int* cmap, unsigned max_points, bool x3, cudaStream_t s);
 int launch_pifu_pair_fact(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,
                           const float* records, const int* cmap, unsigned max_points, bool x3, cudaStream_t s);
 int launch_pifu_pair_eval(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job,

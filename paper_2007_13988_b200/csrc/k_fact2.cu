@@ -39,10 +39,17 @@ namespace icg {
 namespace fact2 {
 
 constexpr uint32_t kHalf = 16384;                   // 128 x 64 bf16 tile
-constexpr uint32_t kStage = 16384;                  // half a weight item: hi or lo of 128 rows x 64 K
+constexpr uint32_t kStage = 16384;                  // a weight stage: 128 rows x 64 K (hi or lo of an item)
 constexpr int kStages = 5;                          // weight ring (80 KB in flight)
-constexpr int kA = 4;                               // activation chunk ring
-constexpr uint32_t kAChunk = 32768;                 // 128 points x 64 K, hi then lo
+constexpr uint32_t kARing = 131072;                 // activation chunk ring (128 KB)
+// bf16x3 (X3): chunks of 128 points x 64 K as hi then lo (32 KB, 4 slots); bf16: hi only (16 KB, 8 slots)
+template <bool X3>
+struct Prec {
+    static constexpr uint32_t kAChunk = X3 ? 32768u : 16384u;
+    static constexpr int kA = (int)(kARing / kAChunk);
+    static constexpr int kStagesPerItem = X3 ? 2 : 1;
+};
+constexpr int kAMax = 8;
 #ifndef FACT2_CQ
 #define FACT2_CQ 4
 #endif
@@ -58,14 +65,14 @@ constexpr int kSFinal = 1920;
 constexpr int kItems = 44;                          // FACT stream: L2 (kc, m) 32, L3 8, L4 4
 constexpr uint32_t kOffRing = 0;
 constexpr uint32_t kOffA = kOffRing + kStages * kStage;
-constexpr uint32_t kOffMisc = kOffA + kA * kAChunk;
+constexpr uint32_t kOffMisc = kOffA + kARing;
 constexpr uint32_t kMisc = 12288;
 constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
 static_assert(kTotal <= 232448, "shared memory");
 
 struct Misc {
     uint64_t full[kStages], empty[kStages];
-    uint64_t a_ready[kA], a_free[kA];
+    uint64_t a_ready[kAMax], a_free[kAMax];
     uint64_t d2a, d2done, d3done, d4done, tm_free;  // d2a: D2 columns 0-255 final
     uint32_t tmem_base;
     int ncaps;
@@ -100,8 +107,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+template <bool X3>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_fact2(const __grid_constant__ CUtensorMap tmapW, Params P) {
+    constexpr uint32_t kAChunk = Prec<X3>::kAChunk;
+    constexpr int kA = Prec<X3>::kA;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* ring = smem + kOffRing;
@@ -179,10 +189,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t ph = 0;
             const uint32_t ring0 = ptx::smem_u32(ring);
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
-                for (int i = 0; i < 2 * kItems; ++i) {  // stream [rank][item][hi, lo], 128 rows each
+                // stream [rank][item][hi, lo] (X3) or [rank][item] (bf16), 128-row stages
+                for (int i = 0; i < Prec<X3>::kStagesPerItem * kItems; ++i) {
                     ptx::mbar_wait(&ms.empty[s], ph ^ 1);
                     if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kStage);
-                    const int row0 = ((int)rank * kItems) * 256 + i * 128;
+                    const int row0 = ((int)rank * kItems * Prec<X3>::kStagesPerItem + i) * 128;
                     ptx::tma_load_2d_2sm(ring0 + s * kStage, &tmapW, full0 + s * 8, 0, row0);
                     if (++s == kStages) {
                         s = 0;
@@ -233,9 +244,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < 4; ++kk) {
                     const uint64_t ko = (uint64_t)(kk * 2);
                     ptx::mma_bf16_pair(tmem + dcol, ah + ko, bh + ko, idesc, (first && kk == 0) ? 0u : 1u);
-                    ptx::mma_bf16_pair(tmem + dcol, al + ko, bh + ko, idesc, 1u);
+                    if constexpr (X3) ptx::mma_bf16_pair(tmem + dcol, al + ko, bh + ko, idesc, 1u);
                 }
                 next_stage();
+                if constexpr (!X3) return;
                 wait_stage();
                 const uint64_t bl = ptx::sdesc_sw128(ring0 + s * kStage);
 #pragma unroll
@@ -322,11 +334,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 4; ++i) {
                     const float a = v[8 * j + 2 * i], b = v[8 * j + 2 * i + 1];
                     hp[i] = pack_bf16(a, b);
-                    lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                    if constexpr (X3)
+                        lp[i] = pack_bf16(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
                 }
                 const uint32_t off = ((((uint32_t)(cq * (kFW / 8) + j)) ^ sw) << 4);
                 ptx::st_shared_v4(base + off, hv);
-                ptx::st_shared_v4(base + kHalf + off, lv);
+                if constexpr (X3) ptx::st_shared_v4(base + kHalf + off, lv);
             }
         };
         auto begin_chunk = [&](uint32_t a) {
@@ -587,10 +600,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }  // namespace fact2
 
 int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& job, const float* records,
-                      const int* cmap, unsigned max_points, cudaStream_t s) {
+                      const int* cmap, unsigned max_points, bool x3, cudaStream_t s) {
     static PerDeviceOnce once;
     if (int r = once.run([] {
-            ICG_CUDA_TRY(cudaFuncSetAttribute(fact2::k_fact2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            ICG_CUDA_TRY(cudaFuncSetAttribute(fact2::k_fact2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)fact2::kTotal));
+            ICG_CUDA_TRY(cudaFuncSetAttribute(fact2::k_fact2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)fact2::kTotal));
             return ICG_OK;
         }))
@@ -617,7 +632,10 @@ int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, con
     }
     p.trace = tron ? trace : nullptr;
     if (p.trace) cudaMemsetAsync(p.trace, 0, 64 * 8, s);
-    fact2::k_fact2<<<2 * pairs, fact2::kThreads, fact2::kTotal, s>>>(tm, p);
+    if (x3)
+        fact2::k_fact2<true><<<2 * pairs, fact2::kThreads, fact2::kTotal, s>>>(tm, p);
+    else
+        fact2::k_fact2<false><<<2 * pairs, fact2::kThreads, fact2::kTotal, s>>>(tm, p);
     if (const cudaError_t e = cudaGetLastError()) {
         set_error(std::string("k_fact2: ") + cudaGetErrorString(e));
         return ICG_ERUNTIME;
