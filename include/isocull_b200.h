@@ -72,6 +72,20 @@ typedef struct icg_primitive {
     double inv_rotation[9];   /* row-major world->local (Primitive::inv_rotation) */
 } icg_primitive;
 
+/* TextureRule (scene.hpp:48-55, texture_color :105-127): the analytic field's T(P) */
+#define ICG_TEXTURE_NONE 0
+#define ICG_TEXTURE_CONSTANT 1      /* color */
+#define ICG_TEXTURE_GRADIENT 2      /* lerp(from, to, (P[axis] + 1) / 2) */
+#define ICG_TEXTURE_PER_PRIMITIVE 3 /* colors[nearest primitive] (first minimum) */
+
+typedef struct icg_texture_rule {
+    int32_t kind;              /* ICG_TEXTURE_* */
+    int32_t axis;              /* gradient: 0 = x, 1 = y, 2 = z */
+    double color[3];
+    double from[3], to[3];
+    const double* colors;      /* per primitive: n_prims x 3 (host memory) */
+} icg_texture_rule;
+
 /* Union-only CSG of primitives (the default tree of parse_scene,
  * scene.hpp:308-317; every bundled scene and the config-0 capsule figure use
  * it).  signed_distance = min over primitives (scene.hpp:130-146). */
@@ -79,7 +93,15 @@ typedef struct icg_scene {
     const icg_primitive* prims;
     int32_t n_prims;
     double tau; /* occupancy_from_distance(d, tau) = 1/(1+exp(d/tau)), field.hpp:81 */
+    icg_texture_rule texture;  /* analytic field: T(P) for render_view / texture_batch */
 } icg_scene;
+
+/* ---- camera: CameraSpec, render.hpp:19-46 -------------------------------- */
+typedef struct icg_camera {
+    double rotation[9];        /* row-major world->view */
+    double translation[3];
+    double scale;              /* weak-perspective x,y scale; 1 = orthographic */
+} icg_camera;
 
 /* ---- field descriptor: replaces FieldOracle (field.hpp:22-77) ------------ */
 #define ICG_FIELD_ANALYTIC 0 /* O(P) = 1/(1+exp(sdf(P)/tau)) on device (config 0) */
@@ -97,6 +119,12 @@ typedef struct icg_field {
     int32_t fmap_c, fmap_h, fmap_w;
     int32_t fmap_mem;          /* ICG_MEM_HOST (copied H2D inside the call) or ICG_MEM_DEVICE */
     int32_t precision;         /* ICG_PREC_* */
+    /* PIFu input view: Phi is sampled at q.xy and the depth feature is q.z,
+     * q = input_camera.world_to_view(P) = (s (R P + t).x, s (R P + t).y, (R P + t).z)
+     * (CameraSpec, render.hpp:19-46).  0 = orthographic identity (q = P, BASELINE configs 1-4;
+     * the column-factored fast path applies); otherwise every node takes the per-point path. */
+    int32_t has_input_camera;
+    icg_camera input_camera;
 } icg_field;
 
 /* ---- MLP weights (f_O / f_T; not in the reference) */
@@ -119,16 +147,19 @@ typedef struct icg_mlp_desc {
 
 /* ---- algorithm config: AlgoConfig, localize.hpp:36-45 -------------------- */
 #define ICG_VARIANT_BRUTE 0
+#define ICG_VARIANT_OCTREE_BINARIZED 1 /* extract_octree_binarized, localize.hpp:199-260 (Fig. 4 baseline) */
+#define ICG_VARIANT_OCTREE_THRESHOLD 2 /* extract_octree_threshold, localize.hpp:265-306 (Fig. 4 baseline) */
 #define ICG_VARIANT_PROGRESSIVE 3 /* Variant enum order, localize.hpp:16 */
 
 typedef struct icg_algo_config {
-    int32_t variant;           /* ICG_VARIANT_PROGRESSIVE or ICG_VARIANT_BRUTE */
+    int32_t variant;           /* ICG_VARIANT_* */
     int32_t coarsest_cells;    /* R_0 (>= 2) */
     int32_t target_level;      /* L; R_L = R_0 * 2^L <= 1024 */
     int32_t max_conflict_iters;/* 0 = one axis length per level (localize.hpp:339) */
     int32_t conflict_pass;     /* 0 = ablation (localize.hpp:42, 335-336) */
     int32_t keep_level_sets;   /* nonzero: keep every level's refined-cell and evaluated-node sets
                                   on the context for icg_level_set (one extra bitset pass per level) */
+    double threshold;          /* octree_threshold only, in (0, 0.5) (AlgoConfig::threshold) */
 } icg_algo_config;
 
 /* ---- extraction result: ExtractionResult, localize.hpp:57-64 ------------- */
@@ -150,13 +181,6 @@ typedef struct icg_extraction {
     double wall_seconds;       /* device time of the whole extraction */
 } icg_extraction;
 
-/* ---- camera: CameraSpec, render.hpp:19-46 -------------------------------- */
-typedef struct icg_camera {
-    double rotation[9];        /* row-major world->view */
-    double translation[3];
-    double scale;              /* weak-perspective x,y scale; 1 = orthographic */
-} icg_camera;
-
 /* ---- rendered image: RenderedImage, render.hpp:50-59 --------------------- */
 typedef struct icg_image {
     int32_t mem;               /* ICG_MEM_HOST or ICG_MEM_DEVICE for the arrays below */
@@ -170,6 +194,8 @@ typedef struct icg_image {
     uint64_t grazing_pixels;      /* fractional samples that never reach 0.5 */
     uint64_t texture_points;      /* texture-MLP evaluations (= covered pixels) */
     double wall_seconds;
+    uint64_t oracle_calls;        /* icg_render_view / icg_surface_depth_map: occupancy evaluations of
+                                     the depth pass (RenderedImage::oracle_calls, render.hpp:55) */
 } icg_image;
 
 /* ======================================================================== */
@@ -221,6 +247,24 @@ int icg_level_set(icg_context* ctx, int level, int which, int mem, uint32_t* out
 int icg_render_localized(icg_context* ctx, const icg_field* field, const icg_camera* camera,
                          int width, int height, const float* background, icg_image* out);
 
+/* render_view(oracle, camera, cfg, background, workers) -> RenderedImage (render.hpp:244-280):
+ * the reference's own mesh-free renderer.  The field is evaluated in view space
+ * (O(camera.view_to_world(p)), render.hpp:98-99): progressive localization to level L-1
+ * (cfg: progressive, target_level >= 1), then at level L shadow culling behind columns whose
+ * tentative maximum is 1, evaluation of the surviving fractional candidates and of the bracket
+ * nodes, and per-pixel depth 1 - 2 (k1 - 1 + s) / R (render.hpp:105-206); covered pixels take the
+ * texture at their surface point (clamp01), the rest the background.  The image is square,
+ * width = height = R_L + 1 (one pixel per grid column; row 0 = view y +1); the caller's buffers
+ * hold (R_L+1)^2 pixels.  Field: analytic with a texture rule, or PIFu with texture weights
+ * (else ICG_EINVAL, "render_view: scene has no texture"). */
+int icg_render_view(icg_context* ctx, const icg_field* field, const icg_camera* camera,
+                    const icg_algo_config* cfg, const float* background, icg_image* out);
+
+/* surface_depth_map(oracle, camera, cfg, workers) -> DepthMap (render.hpp:219-240): the same
+ * depth pass without texture; out->depth / mask / surface_k filled, out->rgb ignored. */
+int icg_surface_depth_map(icg_context* ctx, const icg_field* field, const icg_camera* camera,
+                          const icg_algo_config* cfg, icg_image* out);
+
 /* One frame = icg_extract + icg_render_localized in a single call
  * (BASELINE configs 2-4).  Either output may be NULL. */
 int icg_frame(icg_context* ctx, const icg_field* field, const icg_algo_config* cfg,
@@ -235,6 +279,12 @@ int icg_occupancy_batch(icg_context* ctx, const icg_field* field, const double* 
                         size_t n, int mem, float* out);
 int icg_texture_batch(icg_context* ctx, const icg_field* field, const double* points,
                       size_t n, int mem, float* out_rgb);
+
+/* composite (render.hpp:284-291): out[i] = mask[i] ? image_rgb[i] : backdrop[i], 3 floats per
+ * pixel; n_image != n_backdrop -> ICG_EINVAL ("composite: dimension mismatch").  Host arrays;
+ * out may alias backdrop. */
+int icg_composite(const float* image_rgb, const uint8_t* mask, size_t n_image, const float* backdrop,
+                  size_t n_backdrop, float* out);
 
 /* compare_iou (localize.hpp:377-387) on device or host arrays of n bytes. */
 int icg_compare_iou(icg_context* ctx, const uint8_t* a, const uint8_t* b, size_t n, int mem,

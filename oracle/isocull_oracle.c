@@ -224,6 +224,22 @@ void orc_sample_features(const orc_pifu* m, const double p[3], double* out) {
     }
 }
 
+/* CameraSpec::world_to_view (render.hpp:23-26) of the PIFu input view; identity without one */
+static void pifu_input(const orc_pifu* m, const double* P, double* q) {
+    if (!m->has_cam) {
+        q[0] = P[0];
+        q[1] = P[1];
+        q[2] = P[2];
+        return;
+    }
+    const double* R = m->cam_rot;
+    double v[3];
+    for (int r = 0; r < 3; ++r) v[r] = R[3 * r] * P[0] + R[3 * r + 1] * P[1] + R[3 * r + 2] * P[2] + m->cam_t[r];
+    q[0] = m->cam_scale * v[0];
+    q[1] = m->cam_scale * v[1];
+    q[2] = v[2];
+}
+
 #define PB 32 /* points per vector block; per-point arithmetic is independent of PB */
 
 /* One dense layer over a block of PB points: out[o][p] = b[o] + sum_k W[o][k] in[k][p]
@@ -356,13 +372,14 @@ static void pifu_range(void* c, size_t b, size_t e) {
         int np = (int)((e - p0) < PB ? (e - p0) : PB);
         /* skip features [Phi (C), z] per point (padding lanes repeat point 0) */
         for (int p = 0; p < PB; ++p) {
-            const double* P = a->pts + 3 * (p0 + (size_t)(p < np ? p : 0));
-            orc_sample_features(m, P, feat);
+            double q[3];
+            pifu_input(m, a->pts + 3 * (p0 + (size_t)(p < np ? p : 0)), q);
+            orc_sample_features(m, q, feat);
             for (int c = 0; c < C; ++c) gskip[(size_t)c * PB + p] = feat[c];
-            gskip[(size_t)C * PB + p] = P[2];
+            gskip[(size_t)C * PB + p] = q[2];
             if (tskip) {
                 for (int c = 0; c < C; ++c) tskip[(size_t)c * PB + p] = feat[c];
-                tskip[(size_t)(m->tex.skip_dim - 1) * PB + p] = P[2];
+                tskip[(size_t)(m->tex.skip_dim - 1) * PB + p] = q[2];
             }
         }
         if (a->mode == 2) {
@@ -397,13 +414,15 @@ static void pifu_range(void* c, size_t b, size_t e) {
 static void pifu_one(const orc_pifu* m, const double* P, double* out, int mode) {
     double gskip[257 + 8], tskip[513 + 8], bufA[1024], bufB[1024];
     int C = m->C;
-    orc_sample_features(m, P, gskip);
-    gskip[C] = P[2];
+    double q[3];
+    pifu_input(m, P, q);
+    orc_sample_features(m, q, gskip);
+    gskip[C] = q[2];
     if (mode == 2) {
         for (int c = 0; c < C; ++c) tskip[c] = gskip[c];
         const double* h3 = mlp_point(&m->geo, gskip, 3, bufA, bufB);
         for (int k = 0; k < m->geo.out_dims[2]; ++k) tskip[C + k] = h3[k];
-        tskip[m->tex.skip_dim - 1] = P[2];
+        tskip[m->tex.skip_dim - 1] = q[2];
         const double* o = mlp_point(&m->tex, tskip, m->tex.n_layers, bufA, bufB);
         for (int ch = 0; ch < 3; ++ch) out[ch] = sigmoid(o[ch]);
     } else {

@@ -75,6 +75,10 @@ typedef struct orc_pifu {
     orc_mlp geo;
     orc_mlp tex;
     int has_texture;
+    /* input view (icg_field.input_camera): Phi at q.xy, depth feature q.z with
+     * q = world_to_view(P) (render.hpp:23-26); has_cam = 0: q = P */
+    int has_cam;
+    double cam_rot[9], cam_t[3], cam_scale;
 } orc_pifu;
 
 /* Phi: bilinear sample of all C channels at P_xy (align corners,

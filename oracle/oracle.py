@@ -58,7 +58,8 @@ class orc_mlp(C.Structure):
 class orc_pifu(C.Structure):
     _fields_ = [("fmap", f32p), ("C", C.c_int), ("H", C.c_int), ("W", C.c_int),
                 ("prims", C.POINTER(icg_primitive)), ("n_prims", C.c_int), ("sdf_scale", C.c_double),
-                ("geo", orc_mlp), ("tex", orc_mlp), ("has_texture", C.c_int)]
+                ("geo", orc_mlp), ("tex", orc_mlp), ("has_texture", C.c_int), ("has_cam", C.c_int),
+                ("cam_rot", C.c_double * 9), ("cam_t", C.c_double * 3), ("cam_scale", C.c_double)]
 
 
 class orc_pifu_cb(C.Structure):
@@ -155,6 +156,11 @@ def ref() -> C.CDLL:
         lib.ref_scene_capsules.restype = C.c_void_p
         lib.ref_scene_capsules.argtypes = [C.POINTER(icg_primitive), C.c_int, C.c_double]
         lib.ref_scene_free.argtypes = [C.c_void_p]
+        lib.ref_scene_make.restype = C.c_void_p
+        lib.ref_scene_make.argtypes = [C.POINTER(icg_primitive), C.c_int, C.c_double, C.c_int, C.c_int, f64p, f64p,
+                                       f64p, f64p]
+        lib.ref_scene_texture.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), f64p, f64p, f64p,
+                                          f64p, C.c_int]
         lib.ref_scene_export.argtypes = [C.c_void_p, C.POINTER(icg_primitive), C.c_int, f64p, C.POINTER(C.c_int)]
         lib.ref_scene_occ.restype = C.c_double
         lib.ref_scene_occ.argtypes = [C.c_void_p, f64p]
@@ -207,7 +213,8 @@ class Pifu:
     """CPU restatement of the PIFu field: Phi + f_O (+ f_T), fp64."""
 
     def __init__(self, fmap: np.ndarray, caps, geo_w, geo_b, tex_w=None, tex_b=None, sdf_scale=50.0,
-                 threads: int = 1):
+                 threads: int = 1, input_camera=None):
+        """input_camera: (rotation 3x3, translation 3, scale) of the PIFu input view, or None."""
         self.keep = []
         self.fmap = np.ascontiguousarray(fmap, np.float32)
         self.prims = prim_array(caps)
@@ -221,6 +228,12 @@ class Pifu:
         if tex_w is not None:
             self._fill(m.tex, tex_w, tex_b, 513)
             m.has_texture = 1
+        if input_camera is not None:
+            rot, t, sc = input_camera
+            m.has_cam = 1
+            m.cam_rot[:] = [float(x) for x in np.asarray(rot, np.float64).reshape(9)]
+            m.cam_t[:] = [float(x) for x in np.asarray(t, np.float64).reshape(3)]
+            m.cam_scale = float(sc)
         self.m = m
         self.cb = orc_pifu_cb(C.pointer(self.m), threads)
         self.user = C.addressof(self.cb)
@@ -456,9 +469,23 @@ def ref_texture_batch(pt_fn: int, tex_fn: int, user: int, pts: np.ndarray, worke
 
 
 class RefScene:
-    def __init__(self, path: Optional[str] = None, capsules=None, tau: float = 0.02):
+    """A reference SceneSpec: loaded from a scene JSON by the reference's parser, built from capsules,
+    or built from (prims, tau, texture dict) data (ref_scene_make, validated by validate_scene)."""
+
+    def __init__(self, path: Optional[str] = None, capsules=None, tau: float = 0.02, prims=None, texture=None):
         if path is not None:
             self.h = ref().ref_scene_load(path.encode())
+            if not self.h:
+                raise ValueError(ref().ref_last_error().decode())
+        elif prims is not None:
+            arr = prim_array(prims)
+            t = texture or {"kind": 0}
+            vec = lambda k: np.ascontiguousarray(t.get(k, [0.0, 0.0, 0.0]), np.float64)
+            col, fr, to = vec("color"), vec("from"), vec("to")
+            cols = np.ascontiguousarray(t.get("colors", [[0.0] * 3] * max(1, len(prims))), np.float64)
+            self.h = ref().ref_scene_make(C.cast(arr, C.POINTER(icg_primitive)), len(prims), tau, int(t["kind"]),
+                                          int(t.get("axis", 2)), _p(col, C.c_double), _p(fr, C.c_double),
+                                          _p(to, C.c_double), _p(cols, C.c_double))
             if not self.h:
                 raise ValueError(ref().ref_last_error().decode())
         else:
@@ -476,6 +503,17 @@ class RefScene:
         if n < 0:
             raise ValueError("scene is not a plain union")
         return list(arr[:n]), tau.value, bool(has_tex.value)
+
+    def texture(self) -> dict:
+        """The scene's TextureRule as the reference parsed it: kind (ICG_TEXTURE_*), axis, color,
+        from, to, colors (per primitive)."""
+        kind, axis = C.c_int(), C.c_int()
+        col, fr, to = np.zeros(3), np.zeros(3), np.zeros(3)
+        cols = np.zeros(64 * 3)
+        n = ref().ref_scene_texture(self.h, C.byref(kind), C.byref(axis), _p(col, C.c_double), _p(fr, C.c_double),
+                                    _p(to, C.c_double), _p(cols, C.c_double), 64)
+        return {"kind": kind.value, "axis": axis.value, "color": col.tolist(), "from": fr.tolist(), "to": to.tolist(),
+                "colors": cols[:3 * n].reshape(n, 3).tolist()}
 
     def sdf(self, p):
         pp = np.ascontiguousarray(p, np.float64)
@@ -497,7 +535,9 @@ def ref_render_view(scene: RefScene, yaw, pitch, coarsest, level, bg=(0.0, 0.0, 
     calls = C.c_uint64()
     deg, graz, size = C.c_int(), C.c_int(), C.c_int()
     b = np.asarray(bg, np.float64)
-    rc = ref().ref_render_view(scene.pt_fn, scene.tex_fn, scene.user, yaw, pitch, dist, scale, coarsest, level,
+    # a RefScene (per-point occ / tex of the reference SceneSpec) or a Pifu model (per-point callbacks)
+    tex_fn = scene.pt_tex_fn if hasattr(scene, "pt_tex_fn") else scene.tex_fn
+    rc = ref().ref_render_view(scene.pt_fn, tex_fn, scene.user, yaw, pitch, dist, scale, coarsest, level,
                                _p(b, C.c_double), workers, _p(depth, C.c_double), _p(rgb, C.c_double),
                                _p(mask, C.c_uint8), C.byref(calls), C.byref(deg), C.byref(graz), C.byref(size))
     if rc:

@@ -195,6 +195,65 @@ void* ref_scene_capsules(const icg_primitive* prims, int n, double tau) {
     return s;
 }
 
+// A union scene built from C-ABI primitives and a texture rule (parse_scene's default union tree,
+// scene.hpp:302-321, with the fields parse_primitive / parse_texture fill), validated by the
+// reference's validate_scene: the GPU box rebuilds the bundled scenes from tests/golden/scenes.json.
+void* ref_scene_make(const icg_primitive* prims, int n, double tau, int tex_kind, int axis, const double* color,
+                     const double* from, const double* to, const double* colors) {
+    try {
+        auto* s = new RefScene;
+        for (int i = 0; i < n; ++i) {
+            const icg_primitive& q = prims[i];
+            Primitive p;
+            p.kind = static_cast<PrimitiveKind>(q.kind);
+            p.center = {q.center[0], q.center[1], q.center[2]};
+            p.capsule_a = {q.a[0], q.a[1], q.a[2]};
+            p.capsule_b = {q.b[0], q.b[1], q.b[2]};
+            p.radius = q.radius;
+            p.half = {q.half[0], q.half[1], q.half[2]};
+            p.major = q.major;
+            p.minor = q.minor;
+            p.rotated = q.rotated != 0;
+            for (int k = 0; k < 9; ++k) p.inv_rotation.m[k] = q.inv_rotation[k];
+            s->spec.primitives.push_back(p);
+            CsgNode leaf;
+            leaf.prim = i;
+            s->spec.csg.children.push_back(leaf);
+        }
+        s->spec.csg.op = CsgOp::union_op;
+        s->spec.tau = tau;
+        TextureRule& t = s->spec.texture;
+        t.kind = static_cast<TextureKind>(tex_kind);
+        if (color) t.color = {color[0], color[1], color[2]};
+        t.axis = axis;
+        if (from) t.from = {from[0], from[1], from[2]};
+        if (to) t.to = {to[0], to[1], to[2]};
+        if (tex_kind == static_cast<int>(TextureKind::per_primitive))
+            for (int i = 0; i < n; ++i) t.colors.push_back({colors[3 * i], colors[3 * i + 1], colors[3 * i + 2]});
+        validate_scene(s->spec);
+        return s;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// The scene's texture rule (after the reference's own JSON parsing): kind, axis, color, from, to,
+// per-primitive colors (room for max primitives).  Returns the number of per-primitive colors.
+int ref_scene_texture(void* handle, int* kind, int* axis, double* color, double* from, double* to, double* colors,
+                      int max) {
+    const TextureRule& t = static_cast<RefScene*>(handle)->spec.texture;
+    *kind = static_cast<int>(t.kind);
+    *axis = t.axis;
+    color[0] = t.color.x, color[1] = t.color.y, color[2] = t.color.z;
+    from[0] = t.from.x, from[1] = t.from.y, from[2] = t.from.z;
+    to[0] = t.to.x, to[1] = t.to.y, to[2] = t.to.z;
+    int n = static_cast<int>(t.colors.size());
+    for (int i = 0; i < n && i < max; ++i)
+        colors[3 * i] = t.colors[i].x, colors[3 * i + 1] = t.colors[i].y, colors[3 * i + 2] = t.colors[i].z;
+    return n;
+}
+
 void ref_scene_free(void* s) { delete static_cast<RefScene*>(s); }
 
 // Exports the (union-only) primitive list in the C ABI layout; returns -1 if

@@ -22,7 +22,7 @@ ICG_FIELD_ANALYTIC, ICG_FIELD_PIFU = 0, 1
 ICG_PREC_FP32, ICG_PREC_BF16, ICG_PREC_FP32_SIMT = 0, 1, 2
 ICG_MLP_GEOMETRY, ICG_MLP_TEXTURE = 0, 1
 ICG_MLP_LAYERS = 5
-ICG_VARIANT_BRUTE, ICG_VARIANT_PROGRESSIVE = 0, 3
+ICG_VARIANT_BRUTE, ICG_VARIANT_OCTREE_BINARIZED, ICG_VARIANT_OCTREE_THRESHOLD, ICG_VARIANT_PROGRESSIVE = 0, 1, 2, 3
 ICG_SET_EVALUATED_NODES, ICG_SET_REFINED_CELLS = 0, 1
 ICG_ABI_VERSION = 2
 
@@ -47,8 +47,21 @@ class icg_primitive(C.Structure):
     ]
 
 
+ICG_TEXTURE_NONE, ICG_TEXTURE_CONSTANT, ICG_TEXTURE_GRADIENT, ICG_TEXTURE_PER_PRIMITIVE = 0, 1, 2, 3
+
+
+class icg_texture_rule(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("axis", C.c_int32), ("color", C.c_double * 3), ("from_", C.c_double * 3),
+                ("to", C.c_double * 3), ("colors", C.POINTER(C.c_double))]
+
+
 class icg_scene(C.Structure):
-    _fields_ = [("prims", C.POINTER(icg_primitive)), ("n_prims", C.c_int32), ("tau", C.c_double)]
+    _fields_ = [("prims", C.POINTER(icg_primitive)), ("n_prims", C.c_int32), ("tau", C.c_double),
+                ("texture", icg_texture_rule)]
+
+
+class icg_camera(C.Structure):
+    _fields_ = [("rotation", C.c_double * 9), ("translation", C.c_double * 3), ("scale", C.c_double)]
 
 
 class icg_field(C.Structure):
@@ -62,6 +75,8 @@ class icg_field(C.Structure):
         ("fmap_w", C.c_int32),
         ("fmap_mem", C.c_int32),
         ("precision", C.c_int32),
+        ("has_input_camera", C.c_int32),
+        ("input_camera", icg_camera),
     ]
 
 
@@ -85,6 +100,7 @@ class icg_algo_config(C.Structure):
         ("max_conflict_iters", C.c_int32),
         ("conflict_pass", C.c_int32),
         ("keep_level_sets", C.c_int32),
+        ("threshold", C.c_double),
     ]
 
 
@@ -105,10 +121,6 @@ class icg_extraction(C.Structure):
     ]
 
 
-class icg_camera(C.Structure):
-    _fields_ = [("rotation", C.c_double * 9), ("translation", C.c_double * 3), ("scale", C.c_double)]
-
-
 class icg_image(C.Structure):
     _fields_ = [
         ("mem", C.c_int32),
@@ -121,6 +133,7 @@ class icg_image(C.Structure):
         ("grazing_pixels", C.c_uint64),
         ("texture_points", C.c_uint64),
         ("wall_seconds", C.c_double),
+        ("oracle_calls", C.c_uint64),
     ]
 
 
@@ -163,6 +176,10 @@ SIGNATURES = [
     ("icg_extract", C.c_int, [ctx_p, C.POINTER(icg_field), C.POINTER(icg_algo_config), C.POINTER(icg_extraction)]),
     ("icg_render_localized", C.c_int,
      [ctx_p, C.POINTER(icg_field), C.POINTER(icg_camera), C.c_int, C.c_int, f32p, C.POINTER(icg_image)]),
+    ("icg_render_view", C.c_int,
+     [ctx_p, C.POINTER(icg_field), C.POINTER(icg_camera), C.POINTER(icg_algo_config), f32p, C.POINTER(icg_image)]),
+    ("icg_surface_depth_map", C.c_int,
+     [ctx_p, C.POINTER(icg_field), C.POINTER(icg_camera), C.POINTER(icg_algo_config), C.POINTER(icg_image)]),
     ("icg_frame", C.c_int,
      [ctx_p, C.POINTER(icg_field), C.POINTER(icg_algo_config), C.POINTER(icg_camera), C.c_int, C.c_int, f32p,
       C.POINTER(icg_extraction), C.POINTER(icg_image)]),
@@ -171,6 +188,7 @@ SIGNATURES = [
     ("icg_occupancy_batch", C.c_int, [ctx_p, C.POINTER(icg_field), f64p, C.c_size_t, C.c_int, f32p]),
     ("icg_texture_batch", C.c_int, [ctx_p, C.POINTER(icg_field), f64p, C.c_size_t, C.c_int, f32p]),
     ("icg_compare_iou", C.c_int, [ctx_p, u8p, u8p, C.c_size_t, C.c_int, f64p]),
+    ("icg_composite", C.c_int, [f32p, u8p, C.c_size_t, f32p, C.c_size_t, f32p]),
     ("icg_profile_enable", C.c_int, [ctx_p, C.c_int]),
     ("icg_profile_reset", C.c_int, [ctx_p]),
     ("icg_profile_get", C.c_int, [ctx_p, C.POINTER(icg_profile)]),

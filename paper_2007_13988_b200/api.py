@@ -11,8 +11,12 @@ Mirrors the reference's operator surface (/root/reference/proj/include/isocull):
     extract_brute_force (localize:181-373)      extract_brute_force
   compare_iou, acceleration_factor            compare_iou, acceleration_factor
   CameraSpec::from_angles (render.hpp:36)     CameraSpec.from_angles
-  render_view -> RenderedImage (render:244)   render_view -> RenderedImage (first-crossing
-                                                through the localized world grid)
+  render_view -> RenderedImage (render:244)   render_view -> RenderedImage (the reference's
+                                                view-aligned renderer, icg_render_view)
+  surface_depth_map -> DepthMap (render:219)  surface_depth_map
+  composite (render.hpp:284)                  composite
+  (north-star renderer)     render_frame / Context.frame: localize + first-crossing
+                                                render through the localized world grid
 
 Errors follow the reference: std::invalid_argument -> ValueError,
 std::runtime_error -> RuntimeError.  All work runs in the sm_100a library.
@@ -77,12 +81,24 @@ class _Field:
 
 
 class AnalyticField(_Field):
-    """O(P) = 1/(1+exp(sdf(P)/tau)) over a union of primitives (build_oracle, field.hpp:83-91)."""
+    """O(P) = 1/(1+exp(sdf(P)/tau)) over a union of primitives (build_oracle, field.hpp:83-91), with
+    an optional TextureRule (scene.hpp:48-55): dict kind (ICG_TEXTURE_*), axis, color, from, to,
+    colors (per primitive) -- the layout of tests/golden/scenes.json."""
 
-    def __init__(self, prims: Sequence[abi.icg_primitive], tau: float):
+    def __init__(self, prims: Sequence[abi.icg_primitive], tau: float, texture: Optional[dict] = None):
         super().__init__()
         self.c.kind = abi.ICG_FIELD_ANALYTIC
         self._set_prims(prims, tau)
+        if texture and texture.get("kind", 0):
+            t = self.c.scene.texture
+            t.kind = int(texture["kind"])
+            t.axis = int(texture.get("axis", 2))
+            t.color[:] = [float(x) for x in texture.get("color", [1.0, 1.0, 1.0])]
+            t.from_[:] = [float(x) for x in texture.get("from", [0.0, 0.0, 0.0])]
+            t.to[:] = [float(x) for x in texture.get("to", [1.0, 1.0, 1.0])]
+            cols = np.ascontiguousarray(texture.get("colors") or [[0.0, 0.0, 0.0]], dtype=np.float64).reshape(-1)
+            self._colors = cols
+            t.colors = _ptr(cols, C.c_double)
 
 
 class PifuField(_Field):
@@ -90,8 +106,13 @@ class PifuField(_Field):
 
     def __init__(self, feature_map, capsules: Sequence[abi.icg_primitive], sdf_scale: float = 50.0,
                  precision: int = abi.ICG_PREC_FP32, device_ptr: Optional[int] = None,
-                 shape: Optional[tuple] = None):
+                 shape: Optional[tuple] = None, input_camera: Optional["CameraSpec"] = None):
+        """input_camera: the view the feature map was encoded from (Phi at its world_to_view x, y; depth
+        feature its z); None = orthographic identity."""
         super().__init__()
+        if input_camera is not None:
+            self.c.has_input_camera = 1
+            self.c.input_camera = input_camera.to_c()
         self.c.kind = abi.ICG_FIELD_PIFU
         self._set_prims(capsules, 0.02)
         self.c.sdf_scale = sdf_scale
@@ -112,6 +133,10 @@ class PifuField(_Field):
 # ---------------------------------------------------------------------------
 # Config / results
 # ---------------------------------------------------------------------------
+VARIANTS = {"brute": abi.ICG_VARIANT_BRUTE, "octree_binarized": abi.ICG_VARIANT_OCTREE_BINARIZED,
+            "octree_threshold": abi.ICG_VARIANT_OCTREE_THRESHOLD, "progressive": abi.ICG_VARIANT_PROGRESSIVE}
+
+
 @dataclass
 class AlgoConfig:
     variant: str = "progressive"
@@ -120,16 +145,18 @@ class AlgoConfig:
     max_conflict_iters: int = 0
     conflict_pass: bool = True
     keep_level_sets: bool = False  # keep per-level refined-cell / evaluated-node sets (Context.level_set)
+    threshold: float = 0.0  # octree_threshold only, in (0, 0.5)
 
     def target_cells(self) -> int:
         return self.coarsest_cells << self.target_level
 
     def to_c(self) -> abi.icg_algo_config:
-        v = {"progressive": abi.ICG_VARIANT_PROGRESSIVE, "brute": abi.ICG_VARIANT_BRUTE}.get(self.variant)
-        if v is None:
+        v = VARIANTS.get(self.variant)
+        if v is None:  # variant_from_name, localize.hpp:29-34
             raise ValueError(f"unknown variant '{self.variant}'")
         return abi.icg_algo_config(v, self.coarsest_cells, self.target_level, self.max_conflict_iters,
-                                   1 if self.conflict_pass else 0, 1 if self.keep_level_sets else 0)
+                                   1 if self.conflict_pass else 0, 1 if self.keep_level_sets else 0,
+                                   float(self.threshold))
 
 
 @dataclass
@@ -179,6 +206,7 @@ class RenderedImage:
     grazing_pixels: int
     texture_points: int
     wall_seconds: float
+    oracle_calls: int = 0  # render_view / surface_depth_map: occupancy evaluations of the depth pass
 
 
 # ---------------------------------------------------------------------------
@@ -284,6 +312,24 @@ class Context:
         if n.value:
             _check(self._lib.icg_level_set(self.h, level, w, abi.ICG_MEM_HOST, _ptr(out, C.c_uint32), n.value,
                                            C.byref(n)))
+        return out
+
+    def render_view(self, fld: _Field, camera: CameraSpec, cfg: AlgoConfig, background=(0.0, 0.0, 0.0),
+                    depth_only: bool = False) -> RenderedImage:
+        """render_view (render.hpp:244-280) / surface_depth_map (depth_only, :219-240): the reference's
+        view-aligned renderer, (R_L+1)^2 pixels."""
+        n = cfg.target_cells() + 1
+        img, bufs = _image_bufs(n, n)
+        cam = camera.to_c()
+        cc = cfg.to_c()
+        if depth_only:
+            _check(self._lib.icg_surface_depth_map(self.h, C.byref(fld.c), C.byref(cam), C.byref(cc), C.byref(img)))
+        else:
+            bg = np.asarray(background, dtype=np.float32)
+            _check(self._lib.icg_render_view(self.h, C.byref(fld.c), C.byref(cam), C.byref(cc), _ptr(bg, C.c_float),
+                                             C.byref(img)))
+        out = _image(img, n, n, bufs)
+        out.oracle_calls = int(img.oracle_calls)
         return out
 
     def occupancy_batch(self, fld: _Field, points: np.ndarray) -> np.ndarray:
@@ -410,9 +456,34 @@ def extract_brute_force(ctx: Context, fld: _Field, cfg: AlgoConfig) -> Extractio
     return ctx.extract(fld, cfg)
 
 
-def render_view(ctx: Context, fld: _Field, camera: CameraSpec, cfg: AlgoConfig, width: int, height: int,
+def extract_octree_binarized(ctx: Context, fld: _Field, cfg: AlgoConfig) -> ExtractionResult:
+    """extract_octree_binarized, localize.hpp:199-260 (Fig. 4 baseline)."""
+    cfg = AlgoConfig("octree_binarized", cfg.coarsest_cells, cfg.target_level, keep_level_sets=cfg.keep_level_sets)
+    return ctx.extract(fld, cfg)
+
+
+def extract_octree_threshold(ctx: Context, fld: _Field, cfg: AlgoConfig) -> ExtractionResult:
+    """extract_octree_threshold, localize.hpp:265-306 (Fig. 4 baseline); cfg.threshold in (0, 0.5)."""
+    cfg = AlgoConfig("octree_threshold", cfg.coarsest_cells, cfg.target_level, keep_level_sets=cfg.keep_level_sets,
+                     threshold=cfg.threshold)
+    return ctx.extract(fld, cfg)
+
+
+def render_view(ctx: Context, fld: _Field, camera: CameraSpec, cfg: AlgoConfig,
                 background=(0.0, 0.0, 0.0)) -> RenderedImage:
-    """Localize (progressive) then render through the localized grid (one icg_frame call)."""
+    """render_view(oracle, camera, cfg, background, workers), render.hpp:244-280 (icg_render_view)."""
+    return ctx.render_view(fld, camera, cfg, background)
+
+
+def surface_depth_map(ctx: Context, fld: _Field, camera: CameraSpec, cfg: AlgoConfig) -> RenderedImage:
+    """surface_depth_map(oracle, camera, cfg, workers), render.hpp:219-240 (depth + mask)."""
+    return ctx.render_view(fld, camera, cfg, depth_only=True)
+
+
+def render_frame(ctx: Context, fld: _Field, camera: CameraSpec, cfg: AlgoConfig, width: int, height: int,
+                 background=(0.0, 0.0, 0.0)) -> RenderedImage:
+    """North-star renderer: localize (progressive) then first-crossing render through the localized
+    grid (one icg_frame call)."""
     return ctx.frame(fld, cfg, camera, width, height, background)[1]
 
 
@@ -426,6 +497,20 @@ def compare_iou(a: np.ndarray, b: np.ndarray, ctx: Optional[Context] = None) -> 
     _check(abi.lib().icg_compare_iou(ctx.h if ctx else None, _ptr(a, C.c_uint8), _ptr(b, C.c_uint8), a.size,
                                      abi.ICG_MEM_HOST, C.byref(out)))
     return out.value
+
+
+def composite(image: RenderedImage, backdrop) -> np.ndarray:
+    """composite(image, backdrop), render.hpp:284-291: covered pixels from the image, the rest from
+    the backdrop ((H, W, 3) or (n, 3) floats; size mismatch -> ValueError)."""
+    rgb = np.ascontiguousarray(image.rgb, dtype=np.float32).reshape(-1)
+    mask = np.ascontiguousarray(image.mask, dtype=np.uint8).reshape(-1)
+    bd = np.ascontiguousarray(backdrop, dtype=np.float32)
+    shape = bd.shape
+    bd = bd.reshape(-1)
+    out = np.empty_like(bd)
+    _check(abi.lib().icg_composite(_ptr(rgb, C.c_float), _ptr(mask, C.c_uint8), mask.size, _ptr(bd, C.c_float),
+                                   bd.size // 3, _ptr(out, C.c_float)))
+    return out.reshape(shape)
 
 
 def acceleration_factor(result: ExtractionResult, brute: ExtractionResult) -> float:

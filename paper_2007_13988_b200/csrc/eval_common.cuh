@@ -47,6 +47,38 @@ __device__ __forceinline__ void job_point_d(const EvalJob& j, unsigned t, double
     }
 }
 
+// CameraSpec::view_to_world (render.hpp:29-32): R^T ({p.x / s, p.y / s, p.z} - t), Mat3::apply's
+// operation order (geom.hpp:64-68) with explicit roundings (bit-exact against the reference)
+__device__ __forceinline__ void view_to_world_d(const FieldDev& f, double* p) {
+    const double w0 = __dsub_rn(__ddiv_rn(p[0], f.vs), f.vt[0]);
+    const double w1 = __dsub_rn(__ddiv_rn(p[1], f.vs), f.vt[1]);
+    const double w2 = __dsub_rn(p[2], f.vt[2]);
+    const double* m = f.vr;
+    p[0] = __dadd_rn(__dadd_rn(__dmul_rn(m[0], w0), __dmul_rn(m[3], w1)), __dmul_rn(m[6], w2));
+    p[1] = __dadd_rn(__dadd_rn(__dmul_rn(m[1], w0), __dmul_rn(m[4], w1)), __dmul_rn(m[7], w2));
+    p[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[2], w0), __dmul_rn(m[5], w1)), __dmul_rn(m[8], w2));
+}
+
+// world position of point t of a job: grid nodes of a view-space field go through view_to_world
+// (the render_view wrap, render.hpp:98-99); explicit points are world points already
+__device__ __forceinline__ void field_point_d(const FieldDev& f, const EvalJob& j, unsigned t, double* p) {
+    job_point_d(j, t, p);
+    if (f.view && !j.points) view_to_world_d(f, p);
+}
+
+// input-camera coordinates of a world point: Phi is sampled at (q.x, q.y), the depth feature is
+// q.z (CameraSpec::world_to_view, render.hpp:23-26; identity without an input camera)
+__device__ __forceinline__ void input_coords(const FieldDev& f, const float* w, float* q) {
+    if (!f.icam) {
+        q[0] = w[0];
+        q[1] = w[1];
+        q[2] = w[2];
+        return;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) q[r] = f.ic[4 * r] * w[0] + f.ic[4 * r + 1] * w[1] + f.ic[4 * r + 2] * w[2] + f.ic[4 * r + 3];
+}
+
 // evaluate_nodes write-back (localize.hpp:86-88) + conflict detection
 // (localize.hpp:341-342): bin(oracle value) != bin(tentative value).
 __device__ __forceinline__ void grid_epilogue(const EvalJob& j, uint32_t idx, float v) {
@@ -128,6 +160,33 @@ __device__ __forceinline__ double scene_sdf(const DevScene& s, const double* p) 
         acc = (i == 0) ? d : (d < acc ? d : acc);
     }
     return acc;
+}
+
+// SceneSpec::texture_color (scene.hpp:105-127) in fp64, reference operation order (lerp:
+// a + t (b - a), geom.hpp:39; per primitive: the first primitive of minimum distance)
+__device__ __forceinline__ void scene_texture(const DevScene& s, const double* p, double* rgb) {
+    if (s.tex_kind == ICG_TEXTURE_CONSTANT) {
+        rgb[0] = s.tex_color[0];
+        rgb[1] = s.tex_color[1];
+        rgb[2] = s.tex_color[2];
+    } else if (s.tex_kind == ICG_TEXTURE_GRADIENT) {
+        const double c = p[s.tex_axis];
+        const double t = __dmul_rn(0.5, __dadd_rn(c, 1.0));
+        for (int d = 0; d < 3; ++d) rgb[d] = __dadd_rn(s.tex_from[d], __dmul_rn(t, __dsub_rn(s.tex_to[d], s.tex_from[d])));
+    } else {
+        double best = 1.0 / 0.0;
+        int bi = 0;
+        for (int i = 0; i < s.n_prims; ++i) {
+            const double d = prim_sdf(s.prims[i], p);
+            if (d < best) {
+                best = d;
+                bi = i;
+            }
+        }
+        rgb[0] = s.tex_colors[bi][0];
+        rgb[1] = s.tex_colors[bi][1];
+        rgb[2] = s.tex_colors[bi][2];
+    }
 }
 
 // fp32 union SDF (same formulas; the PIFu capsule bias is tolerance-bound)

@@ -258,12 +258,14 @@ int ensure_grid(icg_context* c, int cells) {
 int validate_algo(const icg_algo_config* cfg) {
     // validate_config, localize.hpp:47-55
     if (!cfg) return einval("config: null");
-    if (cfg->variant != ICG_VARIANT_PROGRESSIVE && cfg->variant != ICG_VARIANT_BRUTE)
-        return einval("config: variant must be progressive or brute");
+    if (cfg->variant < ICG_VARIANT_BRUTE || cfg->variant > ICG_VARIANT_PROGRESSIVE)
+        return einval("config: unknown variant");
     if (cfg->coarsest_cells < 2) return einval("config: coarsest cells must be >= 2");
     if (cfg->target_level < 0) return einval("config: target level must be >= 0");
     if (cfg->target_level > 10 || ((long)cfg->coarsest_cells << cfg->target_level) > ICG_MAX_TARGET_CELLS)
         return einval("config: target resolution exceeds 1024 cells per axis");
+    if (cfg->variant == ICG_VARIANT_OCTREE_THRESHOLD && !(cfg->threshold > 0.0 && cfg->threshold < 0.5))
+        return einval("config: threshold must lie in (0, 0.5)");
     return ICG_OK;
 }
 
@@ -299,6 +301,22 @@ int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
     h->n_prims = s.n_prims;
     h->tau = s.tau;
     h->sdf_scale = f->sdf_scale;
+    // TextureRule (scene.hpp:48-55; validate_scene's per-primitive rule, scene.hpp:199-201)
+    const icg_texture_rule& tr = s.texture;
+    if (tr.kind < ICG_TEXTURE_NONE || tr.kind > ICG_TEXTURE_PER_PRIMITIVE) return einval("scene: unknown texture kind");
+    if (tr.kind == ICG_TEXTURE_GRADIENT && (tr.axis < 0 || tr.axis > 2)) return einval("scene: gradient axis must be x, y or z");
+    if (tr.kind == ICG_TEXTURE_PER_PRIMITIVE && !tr.colors)
+        return einval("scene: per_primitive texture needs one color per primitive");
+    h->tex_kind = tr.kind;
+    h->tex_axis = tr.axis;
+    for (int k = 0; k < 3; ++k) {
+        h->tex_color[k] = tr.color[k];
+        h->tex_from[k] = tr.from[k];
+        h->tex_to[k] = tr.to[k];
+    }
+    if (tr.kind == ICG_TEXTURE_PER_PRIMITIVE)
+        for (int i = 0; i < s.n_prims; ++i)
+            for (int k = 0; k < 3; ++k) h->tex_colors[i][k] = tr.colors[3 * i + k];
     if (int r = c->scene.ensure(sizeof(DevScene))) return r;
     ICG_CUDA_TRY(cudaMemcpyAsync(c->scene.p, h, sizeof(DevScene), cudaMemcpyHostToDevice, c->stream));
     FScene* hf = c->h_fscene;
@@ -354,12 +372,30 @@ int prepare_field(icg_context* c, const icg_field* f, FieldDev& fd) {
         fd.C = f->fmap_c;
         fd.H = f->fmap_h;
         fd.W = f->fmap_w;
+        if (f->has_input_camera) {
+            const icg_camera& ic = f->input_camera;
+            if (!(ic.scale != 0.0) || !std::isfinite(ic.scale)) return einval("field: input camera scale must be nonzero");
+            fd.icam = 1;
+            for (int r = 0; r < 3; ++r) {
+                const double s = r < 2 ? ic.scale : 1.0;
+                for (int k = 0; k < 3; ++k) fd.ic[4 * r + k] = (float)(s * ic.rotation[3 * r + k]);
+                fd.ic[4 * r + 3] = (float)(s * ic.translation[r]);
+            }
+        }
     }
     return ICG_OK;
 }
 
+// column factoring: every node of a grid column shares Phi (orthographic identity input camera,
+// world-space grid)
+// FieldOracle::has_texture (field.hpp:50): a texture rule (analytic) or texture MLP weights (PIFu)
+bool field_has_texture(const icg_context* c, const FieldDev& fd) {
+    return fd.kind == ICG_FIELD_PIFU ? c->has_tex : c->h_scene->tex_kind != ICG_TEXTURE_NONE;
+}
+
 bool fact_ok(const icg_context* c, const FieldDev& fd) {
     return fd.kind == ICG_FIELD_PIFU && (fd.precision == ICG_PREC_FP32 || fd.precision == ICG_PREC_BF16) &&
+           !fd.icam && !fd.view &&
            c->geo_pair && c->geo_fact && c->use_fact;
 }
 
@@ -474,7 +510,9 @@ int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned ma
 int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
     int slot = prof_begin(c, 1);
     int r;
-    if (fd.precision == ICG_PREC_FP32_SIMT)
+    if (fd.kind == ICG_FIELD_ANALYTIC)
+        r = launch_analytic_texture(fd, job, max_points, c->stream);
+    else if (fd.precision == ICG_PREC_FP32_SIMT)
         r = launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
     else
         // one fp16 copy of every weight and operand, one MMA per K step, at every precision:
@@ -553,6 +591,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
         job.overflow = &ctr->overflow;
         if (int r = run_eval(c, fd, job, job.n_static)) return r;
     }
+    const bool octree = cfg->variant == ICG_VARIANT_OCTREE_BINARIZED || cfg->variant == ICG_VARIANT_OCTREE_THRESHOLD;
     for (int l = 1; l <= L; ++l) {
         const int fcells = 2 * cells;
         const size_t nf = nodes3(fcells);
@@ -569,6 +608,44 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
         lb.block_counts = c->block_counts.as<uint32_t>();
         lb.list = c->list_e0.as<uint32_t>();
         lb.rc = cells;
+        if (octree) {
+            // Fig. 4 baselines: mark cells, build the fine grid, evaluate the nodes of marked cells
+            const int mode = cfg->variant == ICG_VARIANT_OCTREE_BINARIZED ? 0 : 1;
+            {
+                int slot = prof_begin(c, 2);
+                int r = launch_octree_level(lb, lb.queued, mode, cfg->threshold, ctr, l, c->stream);
+                prof_end(c, slot);
+                c->launches += mode == 0 ? 4 : 2;
+                if (r) return r;
+            }
+            if (int r = c->set_scratch.ensure(bits_to_list_scratch_words(nf) * 4)) return r;
+            if (int r = launch_bits_to_list(lb.sel, nf, c->set_scratch.as<uint32_t>(), lb.list, &ctr->list_count,
+                                            c->stream))
+                return r;
+            c->launches += 3;
+            EvalJob job{};
+            job.list = lb.list;
+            job.count = &ctr->list_count;
+            job.cells = fcells;
+            job.values = lb.fv;
+            job.states = lb.fs;
+            job.evals = &ctr->evals[l];
+            job.overflow = &ctr->overflow;
+            if (int r = run_eval(c, fd, job, (unsigned)nf)) return r;
+            if (cfg->keep_level_sets) {
+                const size_t ncell = (size_t)cells * cells * cells;
+                if (int r = c->lvl_bits[0][l].ensure(words(nf) * 4 + 16)) return r;
+                if (int r = c->lvl_bits[1][l].ensure(words(ncell) * 4 + 16)) return r;
+                if (int r = launch_level_eval_bits(lb.fs, lb.cs, cells, c->lvl_bits[0][l].as<uint32_t>(), c->stream))
+                    return r;
+                ICG_CUDA_TRY(cudaMemcpyAsync(c->lvl_bits[1][l].p, c->mixed.p, words(ncell) * 4,
+                                             cudaMemcpyDeviceToDevice, c->stream));
+                c->launches += 1;
+            }
+            b ^= 1;
+            cells = fcells;
+            continue;
+        }
         {
             int slot = prof_begin(c, 2);
             int r = launch_level_classify(lb, ctr, l, c->stream);
@@ -695,6 +772,118 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
     }
     c->last_buf = b;
     c->last_cells = cells;
+    return ICG_OK;
+}
+
+// render_view's depth pass (render.hpp:89-215) on the context stream: view-space localization to
+// level L-1 (issue_extract with the view-field wrap), then the level-L passes of k_depth.cu;
+// `texture`: render_view (texture at covered pixels) else surface_depth_map.  Outputs in the
+// context's render buffers, (R_L+1)^2 pixels.
+int issue_depth_pass(icg_context* c, FieldDev fd, const icg_algo_config* cfg, const icg_camera* cam, const float* bg,
+                     bool texture) {
+    fd.view = 1;
+    for (int k = 0; k < 9; ++k) fd.vr[k] = cam->rotation[k];
+    for (int k = 0; k < 3; ++k) fd.vt[k] = cam->translation[k];
+    fd.vs = cam->scale;
+    icg_algo_config sub = *cfg;
+    sub.target_level = cfg->target_level - 1;
+    sub.keep_level_sets = 0;
+    if (int r = issue_extract(c, fd, &sub)) return r;
+    const int L = cfg->target_level, rc = c->last_cells, fcells = 2 * rc;
+    const int b = c->last_buf;
+    const size_t nf = nodes3(fcells), fn = (size_t)fcells + 1, npx = fn * fn;
+    DevCounters* ctr = c->ctr.as<DevCounters>();
+    LevelBufs lb{};
+    lb.cv = c->vals[b].as<float>();
+    lb.cs = c->sts[b].as<uint8_t>();
+    lb.fv = c->vals[b ^ 1].as<float>();
+    lb.fs = c->sts[b ^ 1].as<uint8_t>();
+    lb.cbin = c->cbin.as<uint32_t>();
+    lb.mixed = c->mixed.as<uint32_t>();
+    lb.tentbin = c->tentbin.as<uint32_t>();
+    lb.sel = c->sel.as<uint32_t>();
+    lb.queued = c->queued.as<uint32_t>();
+    lb.block_counts = c->block_counts.as<uint32_t>();
+    lb.list = c->list_e0.as<uint32_t>();
+    lb.rc = rc;
+    {
+        int slot = prof_begin(c, 2);
+        int r = launch_level_carry(lb, ctr, L, c->stream);
+        prof_end(c, slot);
+        c->launches += 3;
+        if (r) return r;
+    }
+    if (int r = c->set_scratch.ensure(bits_to_list_scratch_words(nf) * 4)) return r;
+    DepthJob dj{};
+    dj.cbin = lb.cbin;
+    dj.rc = rc;
+    dj.fv = lb.fv;
+    dj.fs = lb.fs;
+    dj.sel = lb.sel;
+    // evaluate the nodes of the sel bitset (ascending) into the level-L grid, counted at level L
+    auto eval_sel = [&]() -> int {
+        if (int r = launch_bits_to_list(lb.sel, nf, c->set_scratch.as<uint32_t>(), lb.list, &ctr->list_count,
+                                        c->stream))
+            return r;
+        c->launches += 3;
+        EvalJob job{};
+        job.list = lb.list;
+        job.count = &ctr->list_count;
+        job.cells = fcells;
+        job.values = lb.fv;
+        job.states = lb.fs;
+        job.evals = &ctr->evals[L];
+        job.overflow = &ctr->overflow;
+        return run_eval(c, fd, job, (unsigned)nf);
+    };
+    ICG_CUDA_TRY(cudaMemsetAsync(lb.sel, 0, (words(nf) + 1) * 4, c->stream));
+    if (int r = launch_depth_shadow(dj, c->stream)) return r;
+    if (int r = eval_sel()) return r;
+    ICG_CUDA_TRY(cudaMemsetAsync(lb.sel, 0, (words(nf) + 1) * 4, c->stream));
+    if (int r = launch_depth_bracket(dj, c->stream)) return r;
+    if (int r = eval_sel()) return r;
+    c->launches += 2;
+    // per-pixel depth + surface points
+    if (int r = c->depth.ensure(npx * 4)) return r;
+    if (int r = c->rgb.ensure(npx * 12)) return r;
+    if (int r = c->mask.ensure(npx)) return r;
+    if (int r = c->surfk.ensure(npx * 4)) return r;
+    if (int r = c->spts.ensure(npx * 24)) return r;
+    if (int r = c->spx.ensure(npx * 4)) return r;
+    ICG_CUDA_TRY(cudaMemsetAsync(&ctr->covered, 0, sizeof(DevCounters) - offsetof(DevCounters, covered), c->stream));
+    for (int k = 0; k < 9; ++k) dj.vr[k] = cam->rotation[k];
+    for (int k = 0; k < 3; ++k) {
+        dj.vt[k] = cam->translation[k];
+        dj.bg[k] = bg ? bg[k] : 0.0f;
+    }
+    dj.vs = cam->scale;
+    dj.depth = c->depth.as<float>();
+    dj.rgb = c->rgb.as<float>();
+    dj.mask = c->mask.as<uint8_t>();
+    dj.surface_k = c->surfk.as<int32_t>();
+    dj.surface_pts = c->spts.as<double>();
+    dj.surface_px = c->spx.as<uint32_t>();
+    dj.ctr = ctr;
+    {
+        int slot = prof_begin(c, 3);
+        int r = launch_depth_final(dj, c->stream);
+        prof_end(c, slot);
+        c->launches += 1;
+        if (r) return r;
+    }
+    if (texture) {
+        EvalJob tj{};
+        tj.points = c->spts.as<double>();
+        tj.count = &ctr->surface_count;
+        tj.out = c->rgb.as<float>();
+        tj.out_pixel = c->spx.as<uint32_t>();
+        tj.out_clamp = 1.0f;
+        FieldDev tf = fd;  // texture at world points: no view wrap
+        tf.view = 0;
+        if (int r = run_texture(c, tf, tj, (unsigned)npx)) return r;
+    }
+    c->last_buf = b ^ 1;
+    c->last_cells = fcells;
     return ICG_OK;
 }
 
@@ -1261,6 +1450,74 @@ int icg_render_localized(icg_context* c, const icg_field* field, const icg_camer
     return ICG_OK;
 }
 
+static int view_render(icg_context* c, const icg_field* field, const icg_camera* cam, const icg_algo_config* cfg,
+                       const float* bg, icg_image* out, bool texture) {
+    if (!c) return einval("render: null context");
+    if (int r = validate_algo(cfg)) return r;
+    // depth_pass's checks, render.hpp:91-94 / 247
+    if (cfg->variant != ICG_VARIANT_PROGRESSIVE) return einval("render: config variant must be progressive");
+    if (cfg->target_level < 1) return einval("render: target level must be >= 1");
+    if (!cam) return einval("render: null camera");
+    if (!(cam->scale != 0.0)) return einval("render: camera scale must be nonzero");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    FieldDev fd;
+    if (int r = prepare_field(c, field, fd)) return r;
+    if (texture && !field_has_texture(c, fd)) return einval("render_view: scene has no texture");
+    const int RL = cfg->coarsest_cells << cfg->target_level;
+    if (int r = ensure_grid(c, RL)) return r;
+    InflightGuard inflight(c->device);
+    c->tail_wide = inflight.alone;
+    prof_discard(c);
+    ICG_CUDA_TRY(cudaEventRecord(c->e0, c->stream));
+    for (int attempt = 0;; ++attempt) {
+        if (int r = issue_depth_pass(c, fd, cfg, cam, bg, texture)) return r;
+        if (int r = sync_counters(c)) return r;
+        if (c->h_ctr->overflow) {
+            set_error("render: device work list overflow");
+            return ICG_ECAPACITY;
+        }
+        icg_algo_config sub = *cfg;
+        sub.target_level -= 1;
+        if (!adapt_unroll(c, &sub)) break;  // the sub-extraction's conflict loop ran out: replay deeper
+        if (attempt > 12) {
+            set_error("render: conflict loop did not converge");
+            return ICG_ERUNTIME;
+        }
+    }
+    ICG_CUDA_TRY(cudaEventRecord(c->e1, c->stream));
+    const int n = RL + 1;
+    if (int r = finish_render_outputs(c, n, n, out)) return r;
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->kept_valid = false;
+    if (out) {
+        fill_image_scalars(c, out, elapsed(c));
+        uint64_t calls = 0;
+        for (int l = 0; l <= cfg->target_level; ++l) calls += c->h_ctr->evals[l];
+        out->oracle_calls = calls;
+    }
+    prof_collect(c);
+    return ICG_OK;
+}
+
+int icg_render_view(icg_context* c, const icg_field* field, const icg_camera* cam, const icg_algo_config* cfg,
+                    const float* bg, icg_image* out) {
+    return view_render(c, field, cam, cfg, bg, out, true);
+}
+
+int icg_surface_depth_map(icg_context* c, const icg_field* field, const icg_camera* cam, const icg_algo_config* cfg,
+                          icg_image* out) {
+    if (out) {
+        icg_image o = *out;
+        o.rgb = nullptr;  // no texture: depth / mask / surface_k only
+        int r = view_render(c, field, cam, cfg, nullptr, &o, false);
+        const float* keep_rgb = out->rgb;
+        *out = o;
+        out->rgb = const_cast<float*>(keep_rgb);
+        return r;
+    }
+    return view_render(c, field, cam, cfg, nullptr, out, false);
+}
+
 int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg, const icg_camera* cam, int W, int H,
               const float* bg, icg_extraction* ext, icg_image* img) {
     if (!c) return einval("frame: null context");
@@ -1411,7 +1668,7 @@ static int eval_points(icg_context* c, const icg_field* field, const double* poi
     ICG_CUDA_TRY(cudaSetDevice(c->device));
     FieldDev fd;
     if (int r = prepare_field(c, field, fd)) return r;
-    if (texture && (fd.kind != ICG_FIELD_PIFU || !c->has_tex)) return einval("FieldOracle: scene has no texture");
+    if (texture && !field_has_texture(c, fd)) return einval("FieldOracle: scene has no texture");
     const double* dpts = points;
     float* dout = out;
     size_t ob = n * 4 * (texture ? 3 : 1);
@@ -1447,6 +1704,21 @@ int icg_occupancy_batch(icg_context* c, const icg_field* f, const double* p, siz
 
 int icg_texture_batch(icg_context* c, const icg_field* f, const double* p, size_t n, int mem, float* out) {
     return eval_points(c, f, p, n, mem, out, true);
+}
+
+int icg_composite(const float* rgb, const uint8_t* mask, size_t n_image, const float* backdrop, size_t n_backdrop,
+                  float* out) {
+    if (n_image != n_backdrop) return einval("composite: dimension mismatch");
+    if (n_image == 0) return ICG_OK;
+    if (!rgb || !mask || !backdrop || !out) return einval("composite: null buffer");
+    for (size_t i = 0; i < n_image; ++i) {
+        const float* src = mask[i] ? rgb + 3 * i : backdrop + 3 * i;
+        const float r = src[0], g = src[1], b = src[2];
+        out[3 * i] = r;
+        out[3 * i + 1] = g;
+        out[3 * i + 2] = b;
+    }
+    return ICG_OK;
 }
 
 int icg_compare_iou(icg_context* c, const uint8_t* a, const uint8_t* b, size_t n, int mem, double* iou) {

@@ -104,6 +104,10 @@ struct DevScene {
     int n_prims;
     double tau;
     double sdf_scale;
+    // TextureRule (scene.hpp:48-55) of the analytic field
+    int tex_kind, tex_axis;
+    double tex_color[3], tex_from[3], tex_to[3];
+    double tex_colors[ICG_MAX_PRIMS][3];
 };
 
 // Fixed PIFu architecture (BASELINE.json configs[1-3]).
@@ -166,10 +170,19 @@ struct FieldDev {
     const FScene* fscene;     // device pointer, fp32 mirror
     const float* fmap_hwc;    // H x W x C fp32
     int C, H, W;
+    // view-space field of render_view (render.hpp:98-99): grid nodes are view points, evaluated at
+    // camera.view_to_world(p) (fp64, reference operation order); 0 = world grid
+    int view;
+    double vr[9], vt[3], vs;
+    // PIFu input camera (icg_field.input_camera): Phi sampled at world_to_view(P).xy, depth feature
+    // world_to_view(P).z; rows [s R0 | s t0], [s R1 | s t1], [R2 | t2]; 0 = orthographic identity
+    int icam;
+    float ic[12];
 };
 
 // ---- kernel launchers (k_*.cu) -------------------------------------------
 int launch_analytic_eval(const FieldDev& f, const EvalJob& job, unsigned int max_points, cudaStream_t s);
+int launch_analytic_texture(const FieldDev& f, const EvalJob& job, unsigned int max_points, cudaStream_t s);
 int launch_pifu_simt_eval(const FieldDev& f, const SimtMlp& geo, const EvalJob& job,
                           unsigned int max_points, cudaStream_t s);
 int launch_pifu_simt_texture(const FieldDev& f, const SimtMlp& geo, const SimtMlp& tex,
@@ -215,6 +228,34 @@ struct LevelBufs {
     int rc;                                 // coarse cells
 };
 int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s);
+int launch_level_carry(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s);
+// one level of the octree baselines (mode 0 binarized, 1 threshold): cell marks -> b.mixed (count
+// in ctr->refined[level]), fine values / states -> b.fv / b.fs, nodes to evaluate -> b.sel;
+// iface: scratch bitset over the coarse nodes (mode 0)
+int launch_octree_level(const LevelBufs& b, uint32_t* iface, int mode, double threshold, DevCounters* ctr, int level,
+                        cudaStream_t s);
+// render_view's view-space depth pass at level L (k_depth.cu, render.hpp:105-206)
+struct DepthJob {
+    const uint32_t* cbin;  // coarse (level L-1) binarized bits
+    int rc;                // coarse cells
+    float* fv;             // level-L values / states (carry of the coarse grid)
+    uint8_t* fs;
+    uint32_t* sel;         // fine bitset (cleared by the caller)
+    // final pass
+    const FieldDev* fd;    // (host copy; the kernels get the camera below)
+    double vr[9], vt[3], vs;  // CameraSpec (view_to_world of the surface points)
+    float bg[3];
+    float* depth;
+    float* rgb;
+    uint8_t* mask;
+    int32_t* surface_k;
+    double* surface_pts;
+    uint32_t* surface_px;
+    DevCounters* ctr;
+};
+int launch_depth_shadow(const DepthJob& j, cudaStream_t s);
+int launch_depth_bracket(const DepthJob& j, cudaStream_t s);
+int launch_depth_final(const DepthJob& j, cudaStream_t s);
 // size classes of a conflict batch: which evaluator takes n nodes (0: empty)
 struct ChainClasses {
     unsigned tail_max, mid_max;

@@ -315,6 +315,27 @@ k_write_words(const uint32_t* __restrict__ sel, unsigned long long nwords, const
     }
 }
 
+// binarize + mixed cells + upsample/carry of one level (fine values/states, tentbin, sel) without
+// the E0 compaction: the first half of launch_level_classify (also render_view's level-L pass)
+int launch_level_carry(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s) {
+    const int rc = b.rc, cn = rc + 1, fn = 2 * rc + 1;
+    if (cn + 32 > 32 * kRowWords) {
+        set_error("level classify: grid too large");
+        return ICG_ERUNTIME;
+    }
+    size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
+    const unsigned nwords = (unsigned)((nf + 31) / 32);
+    k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
+    k_mixed_cells<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(b.cbin, rc, b.mixed, &ctr->refined[level]);
+    ICG_CUDA_TRY(cudaMemsetAsync(b.tentbin, 0, ((size_t)nwords + 1) * 4, s));
+    ICG_CUDA_TRY(cudaMemsetAsync(b.sel, 0, ((size_t)nwords + 1) * 4, s));
+    const unsigned rows = (unsigned)fn * fn;
+    const unsigned fine_blocks = std::min<unsigned>((rows + kFineThreads / 32 - 1) / (kFineThreads / 32), 148u * 8u);
+    k_fine_rows<<<fine_blocks, kFineThreads, 0, s>>>(b.cv, b.cs, b.cbin, b.mixed, rc, b.fv, b.fs, b.tentbin, b.sel);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
 int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s) {
     const int rc = b.rc, cn = rc + 1, fn = 2 * rc + 1;
     if (cn + 32 > 32 * kRowWords) {
@@ -544,6 +565,139 @@ int launch_dense_column_list(int cells, uint32_t* list, cudaStream_t s) {
     const size_t total = ((size_t)cells + 1) * ((size_t)cells + 1) * ((size_t)cells + 1);
     const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 148 * 16);
     k_dense_column_list<<<blocks, 256, 0, s>>>(cells, list);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
+// ---- octree baselines (extract_octree_binarized / _threshold, localize.hpp:199-306) -----------
+// binarized octree: coarse nodes whose 6-neighbourhood crosses the binarized value (:214-228)
+__global__ void k_interface_nodes(const uint32_t* __restrict__ cbin, int rc, uint32_t* __restrict__ iface) {
+    const unsigned cn = rc + 1u;
+    const unsigned long long n = (unsigned long long)cn * cn * cn;
+    const unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool m = false;
+    if (idx < n) {
+        const unsigned jk = (unsigned)(idx / cn), i = (unsigned)(idx - (unsigned long long)jk * cn);
+        const unsigned k = jk / cn, j = jk - k * cn;
+        const bool b = test_bit(cbin, idx);
+        const int st[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+            const int ii = (int)i + st[s][0], jj = (int)j + st[s][1], kk = (int)k + st[s][2];
+            if (ii < 0 || jj < 0 || kk < 0 || ii >= (int)cn || jj >= (int)cn || kk >= (int)cn) continue;
+            if (test_bit(cbin, (unsigned)ii + (unsigned long long)cn * ((unsigned)jj + (unsigned long long)cn * (unsigned)kk)) != b) {
+                m = true;
+                break;
+            }
+        }
+    }
+    const unsigned w = __ballot_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && idx < n) iface[idx >> 5] = w;
+}
+
+// cell marks: mode 0 (binarized) any corner is an interface node (:230-242); mode 1 (threshold)
+// the spread of the corner values exceeds the threshold (:271-285)
+__global__ void k_octree_cells(const uint32_t* __restrict__ iface, const float* __restrict__ cv, int rc, double thr,
+                               int mode, uint32_t* __restrict__ marks, unsigned long long* refined) {
+    const unsigned long long ncell = (unsigned long long)rc * rc * rc;
+    const unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool m = false;
+    if (idx < ncell) {
+        const unsigned jk = (unsigned)(idx / rc), ci = (unsigned)(idx - (unsigned long long)jk * rc);
+        const unsigned ck = jk / rc, cj = jk - ck * rc, cn = rc + 1u;
+        float lo = 1.0f, hi = 0.0f;
+        for (int d = 0; d < 8; ++d) {
+            const unsigned long long o =
+                (ci + (d & 1)) + (unsigned long long)cn * ((cj + ((d >> 1) & 1)) + (unsigned long long)cn * (ck + (d >> 2)));
+            if (mode == 0) {
+                m = m || test_bit(iface, o);
+            } else {
+                const float v = cv[o];
+                lo = fminf(lo, v);
+                hi = fmaxf(hi, v);
+            }
+        }
+        if (mode == 1) m = (double)(hi - lo) > thr;
+    }
+    const unsigned w = __ballot_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) {
+        if (idx < ncell) marks[idx >> 5] = w;
+        if (w) atomicAdd(refined, (unsigned long long)__popc(w));
+    }
+}
+
+// the octree's fine grid and the nodes of marked cells to evaluate (cell_nodes_to_evaluate,
+// localize.hpp:131-151): mode 0 even nodes carry the coarse scalar and state, the rest take the
+// binarized interpolant of the binarized coarse grid (:244-246); mode 1 upsample_interpolate of the
+// continuous values (grid.hpp:87-120: double sum over the parents in (k, j, i) order / count)
+__global__ void k_octree_fine(const float* __restrict__ cv, const uint8_t* __restrict__ cs,
+                              const uint32_t* __restrict__ cbin, const uint32_t* __restrict__ marks, int rc, int mode,
+                              float* __restrict__ fv, uint8_t* __restrict__ fs, uint32_t* __restrict__ sel) {
+    const unsigned fn = 2u * rc + 1u, cn = rc + 1u;
+    const unsigned long long nf = (unsigned long long)fn * fn * fn;
+    const unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool pick = false;
+    if (idx < nf) {
+        const unsigned jk = (unsigned)(idx / fn), i = (unsigned)(idx - (unsigned long long)jk * fn);
+        const unsigned k = jk / fn, j = jk - k * fn;
+        const unsigned i0 = i >> 1, i1 = (i + 1) >> 1, j0 = j >> 1, j1 = (j + 1) >> 1, k0 = k >> 1, k1 = (k + 1) >> 1;
+        float v;
+        uint8_t st;
+        if (i0 == i1 && j0 == j1 && k0 == k1) {
+            const unsigned long long c = i0 + (unsigned long long)cn * (j0 + (unsigned long long)cn * k0);
+            v = cv[c];
+            st = cs[c];
+        } else {
+            st = ICG_STATE_INTERPOLATED;
+            if (mode == 0) {
+                int ones = 0, cnt = 0;
+                for (unsigned kk = k0; kk <= k1; ++kk)
+                    for (unsigned jj = j0; jj <= j1; ++jj)
+                        for (unsigned ii = i0; ii <= i1; ++ii) {
+                            ones += test_bit(cbin, ii + (unsigned long long)cn * (jj + (unsigned long long)cn * kk));
+                            ++cnt;
+                        }
+                v = 2 * ones >= cnt ? 1.0f : 0.0f;  // binarize_value(ones / cnt), exact for cnt in {2, 4, 8}
+            } else {
+                double sum = 0.0;
+                int cnt = 0;
+                for (unsigned kk = k0; kk <= k1; ++kk)
+                    for (unsigned jj = j0; jj <= j1; ++jj)
+                        for (unsigned ii = i0; ii <= i1; ++ii) {
+                            sum = __dadd_rn(sum, (double)cv[ii + (unsigned long long)cn * (jj + (unsigned long long)cn * kk)]);
+                            ++cnt;
+                        }
+                v = (float)__ddiv_rn(sum, (double)cnt);
+            }
+        }
+        fv[idx] = v;
+        fs[idx] = st;
+        if (st != ICG_STATE_EVALUATED) {
+            // coarse cells whose 3x3x3 fine nodes include (i, j, k): ci in [ceil((i-2)/2), floor(i/2)]
+            const int ca = i & 1 ? (int)i0 : (int)i0 - 1, cb = (int)i0 < rc ? (int)i0 : rc - 1;
+            const int ja = j & 1 ? (int)j0 : (int)j0 - 1, jb = (int)j0 < rc ? (int)j0 : rc - 1;
+            const int ka = k & 1 ? (int)k0 : (int)k0 - 1, kb = (int)k0 < rc ? (int)k0 : rc - 1;
+            for (int ck = ka < 0 ? 0 : ka; ck <= kb && !pick; ++ck)
+                for (int cj = ja < 0 ? 0 : ja; cj <= jb && !pick; ++cj)
+                    for (int ci = ca < 0 ? 0 : ca; ci <= cb && !pick; ++ci)
+                        pick = test_bit(marks, (unsigned)ci + (unsigned long long)rc * ((unsigned)cj + (unsigned long long)rc * (unsigned)ck));
+        }
+    }
+    const unsigned w = __ballot_sync(0xffffffffu, pick);
+    if ((threadIdx.x & 31) == 0 && idx < nf) sel[idx >> 5] = w;
+}
+
+int launch_octree_level(const LevelBufs& b, uint32_t* iface, int mode, double threshold, DevCounters* ctr, int level,
+                        cudaStream_t s) {
+    const int rc = b.rc, cn = rc + 1, fn = 2 * rc + 1;
+    const size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
+    if (mode == 0) {
+        k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
+        k_interface_nodes<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cbin, rc, iface);
+    }
+    k_octree_cells<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(iface, b.cv, rc, threshold, mode, b.mixed,
+                                                                     &ctr->refined[level]);
+    k_octree_fine<<<(unsigned)((nf + 255) / 256), 256, 0, s>>>(b.cv, b.cs, b.cbin, b.mixed, rc, mode, b.fv, b.fs, b.sel);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }

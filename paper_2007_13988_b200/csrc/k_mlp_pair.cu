@@ -984,7 +984,8 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     // list entry = a column i + n j of the level grid; its node at k = 0 gives (x, y)
                     if (idx < n) node_pos_d(job_node(job, jbase + idx), job.cells, pd);
                 } else {
-                    if (idx < n) job_point_d(job, idx, pd);
+                    // world point (view-space fields: view_to_world of the node, render.hpp:98-99)
+                    if (idx < n) field_point_d(f, job, idx, pd);
                 }
                 if constexpr (FACT) {
                     int sl = 0;
@@ -995,7 +996,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                     ms.slot[gb][et] = sl;
                 }
                 for (int d = 0; d < 3; ++d) ms.pos[gb][et][d] = (float)pd[d];
-                ms.z[gb][et] = (float)pd[2];
+                float q[3];
+                input_coords(f, ms.pos[gb][et], q);
+                ms.z[gb][et] = q[2];  // depth feature of the input camera
             }
             epi_bar();
             if constexpr (FACT) {
@@ -1036,8 +1039,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
                         const int p = (int)rank * NPC + ew * kPerWarp + it * 2 + j;
-                        float u = (ms.pos[gb][p][0] + 1.0f) * 0.5f * (float)(f.W - 1);
-                        float v = (1.0f - ms.pos[gb][p][1]) * 0.5f * (float)(f.H - 1);
+                        float q[3];
+                        input_coords(f, ms.pos[gb][p], q);  // Phi at the input camera's (x, y)
+                        float u = (q[0] + 1.0f) * 0.5f * (float)(f.W - 1);
+                        float v = (1.0f - q[1]) * 0.5f * (float)(f.H - 1);
                         u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
                         v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
                         const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);

@@ -148,10 +148,13 @@ __device__ void load_tile(const FieldDev& f, const EvalJob& job, unsigned base, 
     if (threadIdx.x < TP) {
         unsigned t = base + threadIdx.x;
         double p[3] = {0.0, 0.0, 0.0};
-        if (t < n) job_point_d(job, t, p);
+        if (t < n) field_point_d(f, job, t, p);
+        const float pw[3] = {(float)p[0], (float)p[1], (float)p[2]};
+        float q[3];
+        input_coords(f, pw, q);  // Phi at q.xy, depth feature q.z; the sdf bias at the world point
         for (int d = 0; d < 3; ++d) {
             sm.posd[threadIdx.x][d] = p[d];
-            sm.pos[threadIdx.x][d] = (float)p[d];
+            sm.pos[threadIdx.x][d] = q[d];
         }
     }
     __syncthreads();

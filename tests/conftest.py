@@ -37,6 +37,12 @@ def load_scenes():
     return out
 
 
+def load_scene_textures():
+    """Texture rules of the bundled scenes as the reference parsed them (scene.hpp:272-298)."""
+    data = json.load(open(os.path.join(GOLDEN, "scenes.json")))
+    return {name: sc.get("texture", {"kind": 0}) for name, sc in data.items()}
+
+
 @pytest.fixture(scope="session")
 def scenes():
     return load_scenes()

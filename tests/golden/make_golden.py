@@ -47,7 +47,8 @@ def main():
         name = os.path.splitext(os.path.basename(path))[0]
         sc = O.RefScene(path)
         prims, tau, has_tex = sc.export()
-        scenes[name] = dict(tau=tau, has_texture=has_tex, prims=[prim_to_dict(p) for p in prims])
+        scenes[name] = dict(tau=tau, has_texture=has_tex, prims=[prim_to_dict(p) for p in prims],
+                            texture=sc.texture())
     json.dump(scenes, open(os.path.join(OUT, "scenes.json"), "w"), indent=1)
 
     runs = {}

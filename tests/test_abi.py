@@ -33,7 +33,7 @@ def test_abi_version_and_struct_sizes():
     assert lib.icg_abi_version() == abi.ICG_ABI_VERSION == 2
     # spot-check layouts against the C compiler's view
     assert C.sizeof(abi.icg_primitive) == 8 + 8 * 24
-    assert C.sizeof(abi.icg_algo_config) == 24
+    assert C.sizeof(abi.icg_algo_config) == 32
     assert C.sizeof(abi.icg_camera) == 13 * 8
 
 

@@ -607,3 +607,32 @@ def test_frame_graph_survives_shape_changes(pifu_inputs):
         assert ext.cells == 64
         assert np.array_equal(ext.values, ref[0].values) and np.array_equal(ext.states, ref[0].states)
         assert np.array_equal(img.rgb, ref[1].rgb) and np.array_equal(img.surface_k, ref[1].surface_k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", PRECISIONS_FP32)
+def test_input_camera_phi_projection(gpu_ctx, pifu_inputs, precision):
+    """icg_field.input_camera: Phi sampled at the input view's world_to_view(P).xy,
+    depth feature its z, against the oracle with the same camera; the localization runs the
+    per-point path (no column sharing) and replays exactly through the reference."""
+    inp = pifu_inputs
+    gpu_ctx.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+    gpu_ctx.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+    cam = api.CameraSpec.from_angles(30, 20, 0.1, 0.9)
+    f = api.PifuField(inp["fmap"], inp["caps"], 50.0, precision, input_camera=cam)
+    m = O.Pifu(inp["fmap"], inp["caps"], inp["gw"], inp["gb"], inp["tw"], inp["tb"], threads=8,
+               input_camera=(cam.rotation, cam.translation, cam.scale))
+    rng = np.random.default_rng(3)
+    pts = rng.uniform(-1, 1, (2000, 3))
+    assert np.abs(gpu_ctx.occupancy_batch(f, pts) - m.occupancy(pts)).max() <= OCC_TOL_FP32
+    assert np.abs(gpu_ctx.texture_batch(f, pts[:500]) - m.texture(pts[:500])).max() <= RGB_TOL
+    # the camera changes the field (not the identity by accident)
+    m_id = _oracle_model(inp)
+    assert np.abs(m_id.occupancy(pts[:200]) - m.occupancy(pts[:200])).max() > 1e-2
+    g = gpu_ctx.extract(f, api.AlgoConfig("progressive", 16, 2))
+    replay_check(g, 16, 2)
+    ev = np.flatnonzero(g.states == abi.ICG_STATE_EVALUATED)
+    n = 65
+    i, j, k = ev % n, (ev // n) % n, ev // (n * n)
+    nodes = np.stack([-1 + 2 * i / 64.0, -1 + 2 * j / 64.0, 1 - 2 * k / 64.0], 1)
+    assert np.abs(g.values[ev] - m.occupancy(nodes)).max() <= OCC_TOL_FP32
