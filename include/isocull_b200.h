@@ -356,6 +356,20 @@ int icg_gen_mlp(uint64_t seed, int which, float* weights_out, float* biases_out)
 int icg_mlp_shape(int which, int32_t* out_dims, int32_t* in_dims, int32_t* skip_dim,
                   size_t* n_weights, size_t* n_biases);
 
+/* On-device feature producer (the encoder stand-in of a frame stream): n = c*h*w seeded N(0,1)
+ * values written to device (mem = ICG_MEM_DEVICE) or host memory, generated on the context's
+ * GPU.  Counter-based (Philox4x32-10 + the reference's Box-Muller form, random.hpp:32-37): a
+ * different stream from icg_gen_normals' host Rng. */
+int icg_gen_feature_map_device(icg_context* ctx, uint64_t seed, int c, int h, int w, int mem, float* out);
+
+/* Stream I/O, byte-identical to the reference writers: write_ppm (image.hpp:18-33, rgb w*h*3),
+ * write_float_map (image.hpp:37-48), dump_grid / load_grid_dump (grid.hpp:199-222; values may be
+ * NULL to read the header only).  Host buffers. */
+int icg_write_ppm(const char* path, int width, int height, const float* rgb);
+int icg_write_float_map(const char* path, int width, int height, const float* values);
+int icg_dump_grid(const char* path, int level, int cells, const float* values);
+int icg_load_grid_dump(const char* path, int* level, int* cells, float* values, size_t capacity);
+
 /* Camera from angles, CameraSpec::from_angles (render.hpp:36-45). */
 int icg_camera_from_angles(double yaw_deg, double pitch_deg, double dist, double scale,
                            icg_camera* out);

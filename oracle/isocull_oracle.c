@@ -853,6 +853,30 @@ int orc_extract_brute(orc_occ_batch_fn occ, void* user, int coarsest_cells, int 
     return ICG_OK;
 }
 
+static void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        c[1] = (uint32_t)p1;
+        c[3] = (uint32_t)p0;
+        c[0] = n0;
+        c[2] = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+void orc_feature_normals(uint64_t seed, size_t n, float* out) {
+    for (size_t e = 0; e < n; ++e) {
+        uint32_t c[4] = {(uint32_t)e, (uint32_t)(e >> 32), 0u, 0u};
+        philox10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+        double a = (double)((((uint64_t)c[0] << 32) | c[1]) >> 11) * 0x1.0p-53;
+        const double b = (double)((((uint64_t)c[2] << 32) | c[3]) >> 11) * 0x1.0p-53;
+        if (a <= 0.0) a = 0x1.0p-53;
+        out[e] = (float)(sqrt(-2.0 * log(a)) * cos(2.0 * 3.14159265358979323846 * b));
+    }
+}
+
 /* localize.hpp:377-387 */
 double orc_compare_iou(const uint8_t* a, const uint8_t* b, size_t n) {
     uint64_t inter = 0, uni = 0;

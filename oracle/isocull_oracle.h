@@ -180,6 +180,11 @@ int orc_render_first_crossing(const float* values, int cells, const icg_camera* 
 void orc_camera_from_angles(double yaw_deg, double pitch_deg, double dist, double scale,
                             icg_camera* out);
 
+/* The product's on-device feature producer (icg_gen_feature_map_device) restated: element e =
+ * Philox4x32-10 at counter (e, 0, 0, 0), key (seed lo, hi); 53-bit uniforms a, b from words
+ * (0, 1) and (2, 3); sqrt(-2 ln a) cos(2 pi b) (random.hpp:32-37) rounded to float. */
+void orc_feature_normals(uint64_t seed, size_t n, float* out);
+
 /* ---- seeded inputs (same draw order as the product's icg_gen_*) --------- */
 void orc_gen_capsules(uint64_t seed, int n, icg_primitive* out);
 void orc_gen_mlp(uint64_t seed, int which, float* w, float* b);

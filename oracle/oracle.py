@@ -100,6 +100,7 @@ def orc() -> C.CDLL:
         lib = C.CDLL(ORC_PATH)
         lib.orc_rng_uniforms.argtypes = [C.c_uint64, C.c_size_t, f64p]
         lib.orc_rng_normals.argtypes = [C.c_uint64, C.c_size_t, f64p]
+        lib.orc_feature_normals.argtypes = [C.c_uint64, C.c_size_t, f32p]
         lib.orc_scene_sdf.restype = C.c_double
         lib.orc_scene_sdf.argtypes = [C.POINTER(icg_primitive), C.c_int, f64p]
         lib.orc_analytic_occupancy_batch.argtypes = [C.POINTER(icg_primitive), C.c_int, C.c_double, f64p,
@@ -410,6 +411,13 @@ def gen_feature_map(seed: int, c: int = 256, h: int = 128, w: int = 128) -> np.n
     out = np.empty(c * h * w)
     orc().orc_rng_normals(seed, out.size, _p(out, C.c_double))
     return out.astype(np.float32).reshape(c, h, w)
+
+
+def feature_normals(seed: int, c: int, h: int, w: int) -> np.ndarray:
+    """Restatement of the product's on-device feature producer (icg_gen_feature_map_device)."""
+    out = np.empty(c * h * w, np.float32)
+    orc().orc_feature_normals(C.c_uint64(seed), C.c_size_t(out.size), _p(out, C.c_float))
+    return out.reshape(c, h, w)
 
 
 def gen_mlp(seed: int, which: int):

@@ -205,6 +205,11 @@ SIGNATURES = [
     ("icg_mlp_shape", C.c_int,
      [C.c_int, i32p, i32p, i32p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     ("icg_camera_from_angles", C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(icg_camera)]),
+    ("icg_gen_feature_map_device", C.c_int, [ctx_p, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, f32p]),
+    ("icg_write_ppm", C.c_int, [C.c_char_p, C.c_int, C.c_int, f32p]),
+    ("icg_write_float_map", C.c_int, [C.c_char_p, C.c_int, C.c_int, f32p]),
+    ("icg_dump_grid", C.c_int, [C.c_char_p, C.c_int, C.c_int, f32p]),
+    ("icg_load_grid_dump", C.c_int, [C.c_char_p, i32p, i32p, f32p, C.c_size_t]),
 ]
 
 

@@ -332,6 +332,17 @@ class Context:
         out.oracle_calls = int(img.oracle_calls)
         return out
 
+    def gen_feature_map(self, seed: int, c: int = 256, h: int = 128, w: int = 128, device_out: Optional[int] = None):
+        """On-device feature producer (icg_gen_feature_map_device): a seeded C x H x W N(0,1) map
+        generated on this GPU, into the device buffer `device_out` (returns it) or to the host."""
+        if device_out is not None:
+            _check(self._lib.icg_gen_feature_map_device(self.h, seed, c, h, w, abi.ICG_MEM_DEVICE,
+                                                        C.cast(C.c_void_p(device_out), abi.f32p)))
+            return device_out
+        out = np.empty((c, h, w), np.float32)
+        _check(self._lib.icg_gen_feature_map_device(self.h, seed, c, h, w, abi.ICG_MEM_HOST, _ptr(out, C.c_float)))
+        return out
+
     def occupancy_batch(self, fld: _Field, points: np.ndarray) -> np.ndarray:
         pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
         out = np.empty(len(pts), np.float32)

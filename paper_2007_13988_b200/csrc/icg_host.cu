@@ -820,6 +820,8 @@ int issue_depth_pass(icg_context* c, FieldDev fd, const icg_algo_config* cfg, co
     dj.fv = lb.fv;
     dj.fs = lb.fs;
     dj.sel = lb.sel;
+    if (int r = c->xext.ensure(npx * sizeof(int2))) return r;
+    dj.colk = reinterpret_cast<int*>(c->xext.p);
     // evaluate the nodes of the sel bitset (ascending) into the level-L grid, counted at level L
     auto eval_sel = [&]() -> int {
         if (int r = launch_bits_to_list(lb.sel, nf, c->set_scratch.as<uint32_t>(), lb.list, &ctr->list_count,
@@ -1869,6 +1871,24 @@ int icg_gen_normals(uint64_t seed, size_t n, float* out) {
     if (n && !out) return einval("gen_normals: null output");
     std::mt19937_64 g(seed);
     for (size_t i = 0; i < n; ++i) out[i] = (float)normal(g);
+    return ICG_OK;
+}
+
+int icg_gen_feature_map_device(icg_context* c, uint64_t seed, int C, int H, int W, int mem, float* out) {
+    if (!c || !out) return einval("gen_feature_map_device: null argument");
+    if (C < 1 || H < 1 || W < 1) return einval("gen_feature_map_device: bad shape");
+    if (mem != ICG_MEM_HOST && mem != ICG_MEM_DEVICE) return einval("gen_feature_map_device: bad mem");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    const size_t n = (size_t)C * H * W;
+    float* dst = out;
+    if (mem == ICG_MEM_HOST) {
+        if (int r = c->outv.ensure(n * 4)) return r;
+        dst = c->outv.as<float>();
+    }
+    if (int r = launch_feature_normals(seed, n, dst, c->stream)) return r;
+    c->launches += 1;
+    if (mem == ICG_MEM_HOST) ICG_CUDA_TRY(cudaMemcpyAsync(out, dst, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     return ICG_OK;
 }
 

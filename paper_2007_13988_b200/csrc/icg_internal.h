@@ -213,6 +213,7 @@ int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& t
                              const void* tmap_tex, const EvalJob& job, unsigned max_points, bool x3,
                              cudaStream_t s);
 int launch_fmap_chw_to_hwc(const float* chw, float* hwc, int C, int H, int W, cudaStream_t s);
+int launch_feature_normals(uint64_t seed, size_t n, float* out, cudaStream_t s);
 
 // grid kernels (k_grid.cu)
 struct LevelBufs {
@@ -241,6 +242,7 @@ struct DepthJob {
     float* fv;             // level-L values / states (carry of the coarse grid)
     uint8_t* fs;
     uint32_t* sel;         // fine bitset (cleared by the caller)
+    int* colk;             // per column: k1 of the binarized argmax before the bracket evaluation
     // final pass
     const FieldDev* fd;    // (host copy; the kernels get the camera below)
     double vr[9], vt[3], vs;  // CameraSpec (view_to_world of the surface points)

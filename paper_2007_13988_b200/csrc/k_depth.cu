@@ -69,13 +69,17 @@ __device__ __forceinline__ int first_inside(const float* fv, size_t col, size_t 
     return -1;
 }
 
+// k1 of every column is kept (colk): the per-pixel pass uses the argmax taken BEFORE the bracket
+// nodes are evaluated (final_pass, render.hpp:140-146), even if an evaluated bracket node k1-1
+// turns out inside (then s clamps to 0)
 __global__ void __launch_bounds__(256) k_depth_bracket(const float* __restrict__ fv, const uint8_t* __restrict__ fs,
-                                                       int rc, uint32_t* sel) {
+                                                       int rc, uint32_t* sel, int* __restrict__ colk) {
     const unsigned fn = 2u * rc + 1u;
     const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
     if (col >= fn * fn) return;
     const size_t plane = (size_t)fn * fn;
     const int k1 = first_inside(fv, col, plane, fn);
+    colk[col] = k1;
     if (k1 < 0) return;
     for (int k = k1 > 0 ? k1 - 1 : 0; k <= k1; ++k) {
         const size_t idx = col + plane * (size_t)k;
@@ -85,6 +89,7 @@ __global__ void __launch_bounds__(256) k_depth_bracket(const float* __restrict__
 
 struct FinalArgs {
     const float* fv;
+    const int* colk;
     int rc;
     double vr[9], vt[3], vs;
     float bg[3];
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(256) k_depth_final(FinalArgs a) {
     const size_t plane = (size_t)fn * fn;
     const unsigned i = col % fn, j = col / fn;
     const size_t px = i + (size_t)fn * (fn - 1 - j);  // image row = n-1-j, column = i
-    const int k1 = first_inside(a.fv, col, plane, fn);
+    const int k1 = a.colk[col];
     if (k1 < 0) {
         for (unsigned k = 0; k < fn; ++k) {
             const float v = a.fv[col + plane * k];
@@ -171,7 +176,7 @@ int launch_depth_shadow(const DepthJob& j, cudaStream_t s) {
 }
 
 int launch_depth_bracket(const DepthJob& j, cudaStream_t s) {
-    k_depth_bracket<<<column_blocks(j.rc), 256, 0, s>>>(j.fv, j.fs, j.rc, j.sel);
+    k_depth_bracket<<<column_blocks(j.rc), 256, 0, s>>>(j.fv, j.fs, j.rc, j.sel, j.colk);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }
@@ -179,6 +184,7 @@ int launch_depth_bracket(const DepthJob& j, cudaStream_t s) {
 int launch_depth_final(const DepthJob& j, cudaStream_t s) {
     FinalArgs a{};
     a.fv = j.fv;
+    a.colk = j.colk;
     a.rc = j.rc;
     for (int k = 0; k < 9; ++k) a.vr[k] = j.vr[k];
     for (int k = 0; k < 3; ++k) {

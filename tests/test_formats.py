@@ -68,3 +68,51 @@ def test_format_errors(tmp_path):
     p.write_bytes(b"\x00\x00")
     with pytest.raises(RuntimeError):
         api.load_grid_dump(str(p))
+
+
+@needs_ref
+def test_c_abi_writers_match_reference(tmp_path):
+    """The C-ABI stream writers (icg_write_ppm / icg_write_float_map / icg_dump_grid /
+    icg_load_grid_dump) on fp32 buffers: byte-identical to the reference writers fed the same
+    values; host-only, no GPU."""
+    import ctypes as C
+    from paper_2007_13988_b200 import abi
+    lib = abi.lib()
+    w, h = 29, 13
+    rgb = _rgb(w, h).astype(np.float32)
+    d64 = np.ascontiguousarray(rgb.astype(np.float64).reshape(-1))
+    a, b = str(tmp_path / "a.ppm"), str(tmp_path / "b.ppm")
+    assert lib.icg_write_ppm(a.encode(), w, h, np.ascontiguousarray(rgb).ctypes.data_as(abi.f32p)) == 0
+    assert O.ref().ref_write_ppm(b.encode(), w, h, d64.ctypes.data_as(O.f64p)) == 0
+    assert open(a, "rb").read() == open(b, "rb").read()
+    v = np.random.default_rng(2).normal(size=w * h).astype(np.float32)
+    a, b = str(tmp_path / "a.f32"), str(tmp_path / "b.f32")
+    assert lib.icg_write_float_map(a.encode(), w, h, v.ctypes.data_as(abi.f32p)) == 0
+    v64 = v.astype(np.float64)
+    assert O.ref().ref_write_float_map(b.encode(), w, h, v64.ctypes.data_as(O.f64p)) == 0
+    assert open(a, "rb").read() == open(b, "rb").read()
+    g = np.random.default_rng(4).uniform(0, 1, 9 ** 3).astype(np.float32)
+    a, b = str(tmp_path / "a.grid"), str(tmp_path / "b.grid")
+    assert lib.icg_dump_grid(a.encode(), 1, 8, g.ctypes.data_as(abi.f32p)) == 0
+    assert O.ref().ref_dump_grid(b.encode(), 1, 8, g.ctypes.data_as(C.POINTER(C.c_float))) == 0
+    assert open(a, "rb").read() == open(b, "rb").read()
+    lv, cells = C.c_int32(), C.c_int32()
+    back = np.empty(9 ** 3, np.float32)
+    small = np.empty(10, np.float32)
+    assert lib.icg_load_grid_dump(b.encode(), C.byref(lv), C.byref(cells), small.ctypes.data_as(abi.f32p), 10) == \
+        abi.ICG_ECAPACITY
+    assert lib.icg_load_grid_dump(b.encode(), C.byref(lv), C.byref(cells), back.ctypes.data_as(abi.f32p),
+                                  back.size) == 0
+    assert (lv.value, cells.value) == (1, 8) and np.array_equal(back, g)
+    assert lib.icg_load_grid_dump(str(tmp_path / "missing").encode(), C.byref(lv), C.byref(cells), None, 0) == \
+        abi.ICG_ERUNTIME
+
+
+def test_feature_producer_restatement_statistics():
+    """The oracle's restatement of the on-device feature producer: N(0,1) statistics, seed- and
+    index-determined (any prefix of a longer map is the shorter map)."""
+    a = O.feature_normals(1000, 4, 64, 64)
+    b = O.feature_normals(1000, 8, 64, 64)
+    assert np.array_equal(a.reshape(-1), b.reshape(-1)[: a.size])
+    assert abs(float(b.mean())) < 0.02 and abs(float(b.std()) - 1.0) < 0.02
+    assert not np.array_equal(a, O.feature_normals(1001, 4, 64, 64))

@@ -636,3 +636,26 @@ def test_input_camera_phi_projection(gpu_ctx, pifu_inputs, precision):
     i, j, k = ev % n, (ev // n) % n, ev // (n * n)
     nodes = np.stack([-1 + 2 * i / 64.0, -1 + 2 * j / 64.0, 1 - 2 * k / 64.0], 1)
     assert np.abs(g.values[ev] - m.occupancy(nodes)).max() <= OCC_TOL_FP32
+
+
+@pytest.mark.gpu
+def test_on_device_feature_producer(gpu_ctx, pifu_inputs):
+    """icg_gen_feature_map_device against the oracle restatement (fp64 Box-Muller rounded to fp32:
+    device and host libm may differ by an ulp), and a frame on the device-generated map equals the
+    frame on the same map uploaded from the host."""
+    m = gpu_ctx.gen_feature_map(1234, 256, 64, 64)
+    o = O.feature_normals(1234, 256, 64, 64)
+    assert np.abs(m - o).max() <= 1e-6 * max(1.0, float(np.abs(o).max()))
+    n = 256 * 64 * 64
+    dp = gpu_ctx.device_alloc(4 * n)
+    gpu_ctx.gen_feature_map(1234, 256, 64, 64, device_out=dp)
+    inp = pifu_inputs
+    gpu_ctx.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+    gpu_ctx.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+    fd = api.PifuField(None, inp["caps"], 50.0, abi.ICG_PREC_FP32, device_ptr=dp, shape=(256, 64, 64))
+    fh = api.PifuField(m, inp["caps"], 50.0, abi.ICG_PREC_FP32)
+    cfg, cam = api.AlgoConfig("progressive", 16, 2), api.CameraSpec.from_angles(90, 0)
+    e1, i1 = gpu_ctx.frame(fd, cfg, cam, 64, 64, want_grid=True)
+    e2, i2 = gpu_ctx.frame(fh, cfg, cam, 64, 64, want_grid=True)
+    gpu_ctx.device_free(dp)
+    assert np.array_equal(e1.values, e2.values) and np.array_equal(i1.rgb, i2.rgb)
