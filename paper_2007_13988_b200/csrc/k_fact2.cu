@@ -41,13 +41,19 @@ namespace fact2 {
 constexpr uint32_t kHalf = 16384;                   // 128 x 64 bf16 tile
 constexpr uint32_t kStage = 16384;                  // a weight stage: 128 rows x 64 K (hi or lo of an item)
 constexpr int kStages = 5;                          // weight ring (80 KB in flight)
-constexpr uint32_t kARing = 131072;                 // activation chunk ring (128 KB)
-// bf16x3 (X3): chunks of 128 points x 64 K as hi then lo (32 KB, 4 slots); bf16: hi only (16 KB, 8 slots)
+// bf16x3 (X3): chunks of 128 points x 64 K as hi then lo (32 KB), a 4-slot ring (128 KB);
+// bf16: hi only (16 KB), 4 slots (64 KB: the tensor cores drain a bf16 chunk faster than the
+// epilogue fills one, so a deeper ring would idle) -- the freed shared memory goes to L1, which
+// holds the record rows and biases the epilogue streams (its loads are latency-bound)
+// kG: chunks published per proxy fence (each fence stalls its warp until the stores land; the
+// bf16 tensor work per chunk is short, so bf16 publishes 4 at a time into a deeper ring)
 template <bool X3>
 struct Prec {
     static constexpr uint32_t kAChunk = X3 ? 32768u : 16384u;
-    static constexpr int kA = (int)(kARing / kAChunk);
+    static constexpr int kA = X3 ? 4 : 8;
+    static constexpr uint32_t kARing = kA * kAChunk;
     static constexpr int kStagesPerItem = X3 ? 2 : 1;
+    static constexpr int kG = X3 ? 2 : 4;
 };
 constexpr int kAMax = 8;
 #ifndef FACT2_CQ
@@ -65,10 +71,13 @@ constexpr int kSFinal = 1920;
 constexpr int kItems = 44;                          // FACT stream: L2 (kc, m) 32, L3 8, L4 4
 constexpr uint32_t kOffRing = 0;
 constexpr uint32_t kOffA = kOffRing + kStages * kStage;
-constexpr uint32_t kOffMisc = kOffA + kARing;
 constexpr uint32_t kMisc = 12288;
-constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
-static_assert(kTotal <= 232448, "shared memory");
+template <bool X3>
+struct Layout {
+    static constexpr uint32_t kOffMisc = kOffA + Prec<X3>::kARing;
+    static constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
+    static_assert(kTotal <= 232448, "shared memory");
+};
 
 struct Misc {
     uint64_t full[kStages], empty[kStages];
@@ -116,7 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* ring = smem + kOffRing;
     uint8_t* abuf = smem + kOffA;
-    Misc& ms = *reinterpret_cast<Misc*>(smem + kOffMisc);
+    Misc& ms = *reinterpret_cast<Misc*>(smem + Layout<X3>::kOffMisc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_rank();
     const bool leader = rank == 0;
@@ -402,17 +411,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             Pt q;
             q.idx = tg * NP + rank * NPC + (unsigned)row;
             q.valid = q.idx < n;
-            if (cq == 0) {  // position (fp64 node -> NDC, as the reference) and record slot
-                double pd[3] = {0.0, 0.0, 0.0};
-                if (q.valid) node_pos_d(pr.node, job.cells, pd);
-                ms.ppos[pb][row][0] = (float)pd[0];
-                ms.ppos[pb][row][1] = (float)pd[1];
-                ms.ppos[pb][row][2] = (float)pd[2];
+            if (cq == 0) {  // position (node -> NDC: dyadic, so fp32 equals the reference's fp64) and slot
+                float pf[3] = {0.0f, 0.0f, 0.0f};
+                if (q.valid) node_pos_f(pr.node, job.cells, pf);
+                ms.ppos[pb][row][0] = pf[0];
+                ms.ppos[pb][row][1] = pf[1];
+                ms.ppos[pb][row][2] = pf[2];
                 ms.pslot[pb][row] = pr.slot;
             }
             epi_bar();
             const float p3[3] = {ms.ppos[pb][row][0], ms.ppos[pb][row][1], ms.ppos[pb][row][2]};
             const int sl = ms.pslot[pb][row];
+            // the layer-1 record terms this thread will read for the tile, into L1 ahead of emit_h1
+            // (one 64-byte line per chunk: features c*64 + cq*kFW, kFW floats)
+            if (q.valid) {
+                const float* rp = P.s_in + (size_t)sl * kSRow + cq * kFW;
+#pragma unroll 4
+                for (int c = 0; c < 16; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + c * 64));
+            }
             float d = 3.0e38f;
             const int nc = ms.ncaps;
             if (nc >= 0) {
@@ -436,8 +452,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // layer 1 (no MMA): chunks [c0, c1) of act(S1 + w1z z + b1)
         // layer 1 in pairs of chunks [c0, c1) (c1 - c0 even)
         auto prefetch_l1 = [](const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); };
+        constexpr int kG = Prec<X3>::kG;
         auto emit_h1 = [&](const Pt& q, int c0, int c1) {
-            for (int kc = c0; kc < c1; kc += 2) {
+            for (int kg = c0; kg < c1; kg += kG) {
+              for (int kc = kg; kc < kg + kG; kc += 2) {
                 // the record terms and biases the drains of layers 2-4 read, into L1 ahead of time
                 // (pair kc: h2 chunk kc/2; pairs 0-3 also h3 chunk kc/2, pair 4 the layer-4 slice)
                 {
@@ -467,17 +485,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const float x = v[i] + fmaf(wz[i], q.z, bb[i]);
                         v[i] = x < 0.0f ? x * P.slope : x;
                     }
-                    begin_chunk(ac + u);
-                    store_chunk(v, ac + u);
+                    begin_chunk(ac + (kc - kg) + u);
+                    store_chunk(v, ac + (kc - kg) + u);
                 }
-                end_chunks(2);
+              }
+              end_chunks(kG);
             }
         };
         // hidden layers 2, 3: drain D (columns col0 + feature) into the next layer's chunks
         auto drain = [&](const Pt& q, int cbeg, int cend, uint32_t col0, const float* bl, int od, int soff) {
-            for (int c2 = cbeg; c2 < cend; c2 += 2) {
+            for (int c2 = cbeg; c2 < cend; c2 += kG) {
 #pragma unroll 1
-              for (int u = 0; u < 2; ++u) {
+              for (int u = 0; u < kG; ++u) {
                 const int c = c2 + u;
                 const int f0 = c * 64 + cq * kFW;
                 uint32_t r[kFW];
@@ -498,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 begin_chunk(ac + u);
                 store_chunk(v, ac + u);
               }
-              end_chunks(2);
+              end_chunks(kG);
             }
         };
         // layer 4 + output: this thread's 64 of the 128 layer-4 features, dot with w5
@@ -604,9 +623,9 @@ int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, con
     static PerDeviceOnce once;
     if (int r = once.run([] {
             ICG_CUDA_TRY(cudaFuncSetAttribute(fact2::k_fact2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)fact2::kTotal));
+                                              (int)fact2::Layout<true>::kTotal));
             ICG_CUDA_TRY(cudaFuncSetAttribute(fact2::k_fact2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)fact2::kTotal));
+                                              (int)fact2::Layout<false>::kTotal));
             return ICG_OK;
         }))
         return r;
@@ -633,9 +652,9 @@ int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, con
     p.trace = tron ? trace : nullptr;
     if (p.trace) cudaMemsetAsync(p.trace, 0, 64 * 8, s);
     if (x3)
-        fact2::k_fact2<true><<<2 * pairs, fact2::kThreads, fact2::kTotal, s>>>(tm, p);
+        fact2::k_fact2<true><<<2 * pairs, fact2::kThreads, fact2::Layout<true>::kTotal, s>>>(tm, p);
     else
-        fact2::k_fact2<false><<<2 * pairs, fact2::kThreads, fact2::kTotal, s>>>(tm, p);
+        fact2::k_fact2<false><<<2 * pairs, fact2::kThreads, fact2::Layout<false>::kTotal, s>>>(tm, p);
     if (const cudaError_t e = cudaGetLastError()) {
         set_error(std::string("k_fact2: ") + cudaGetErrorString(e));
         return ICG_ERUNTIME;
