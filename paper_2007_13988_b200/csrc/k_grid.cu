@@ -387,28 +387,45 @@ __global__ void k_conflict_expand(uint32_t* __restrict__ queued, const uint8_t* 
         if (ncf > 0 && iter >= max_iters) ctr->warning = 1;  // localize.hpp:343-346
     }
     if (ncf == 0 || iter >= max_iters) return;
-    const int fn = fcells + 1;
-    // one thread per (conflict, neighbour) pair, 26 neighbours in (dk, dj, di) order
-    size_t total = (size_t)ncf * 26;
-    for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-        unsigned c = (unsigned)(t / 26);
-        int r = (int)(t % 26);
-        if (r >= 13) ++r;  // skip the centre (di = dj = dk = 0)
-        int di = r % 3 - 1, dj = (r / 3) % 3 - 1, dk = r / 9 - 1;
-        size_t idx = conflicts[c];
-        int i = (int)(idx % fn), j = (int)((idx / fn) % fn), k = (int)(idx / ((size_t)fn * fn));
-        int ii = i + di, jj = j + dj, kk = k + dk;
-        if (ii < 0 || jj < 0 || kk < 0 || ii >= fn || jj >= fn || kk >= fn) continue;
-        size_t nb = (size_t)ii + (size_t)fn * ((size_t)jj + (size_t)fn * (size_t)kk);
-        if (fs[nb] == ICG_STATE_EVALUATED) continue;
-        unsigned bit = 1u << (nb & 31);
-        unsigned old = atomicOr(&queued[nb >> 5], bit);
-        if (old & bit) continue;
-        unsigned pos = atomicAdd(&ctr->nx_count[p], 1u);
-        if (pos < cap)
-            next_list[pos] = (uint32_t)nb;
-        else
-            ctr->overflow = 1;
+    const unsigned fn = (unsigned)fcells + 1u;  // fn^3 <= 1025^3 < 2^32: 32-bit node indices
+    // one thread per (conflict, neighbour) pair, 26 neighbours in (dk, dj, di) order; the new
+    // entries of a warp take one atomicAdd on the shared counter (warp-aggregated)
+    const unsigned long long total = (unsigned long long)ncf * 26u;
+    const unsigned lane = threadIdx.x & 31u;
+    for (unsigned long long t0 = (unsigned long long)blockIdx.x * blockDim.x; t0 < total;
+         t0 += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long t = t0 + threadIdx.x;
+        bool add = false;
+        uint32_t nb = 0;
+        if (t < total) {
+            const unsigned c = (unsigned)(t / 26u);
+            unsigned r = (unsigned)(t - (unsigned long long)c * 26u);
+            if (r >= 13u) ++r;  // skip the centre (di = dj = dk = 0)
+            const int di = (int)(r % 3u) - 1, dj = (int)((r / 3u) % 3u) - 1, dk = (int)(r / 9u) - 1;
+            const uint32_t idx = conflicts[c];
+            const unsigned jk = idx / fn, i = idx - jk * fn, k = jk / fn, j = jk - k * fn;
+            const int ii = (int)i + di, jj = (int)j + dj, kk = (int)k + dk;
+            if (ii >= 0 && jj >= 0 && kk >= 0 && ii < (int)fn && jj < (int)fn && kk < (int)fn) {
+                nb = (uint32_t)ii + fn * ((uint32_t)jj + fn * (uint32_t)kk);
+                if (fs[nb] != ICG_STATE_EVALUATED) {
+                    const unsigned bit = 1u << (nb & 31u);
+                    add = !(atomicOr(&queued[nb >> 5], bit) & bit);
+                }
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, add);
+        if (m) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&ctr->nx_count[p], (unsigned)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (add) {
+                const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+                if (pos < cap)
+                    next_list[pos] = nb;
+                else
+                    ctr->overflow = 1;
+            }
+        }
     }
 }
 
