@@ -490,6 +490,23 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
             "evals_per_frame": int(prof["geo_points"] / max(1, prof["frames"])),
         }
         line["gpu_launches"] = int(round(prof["kernel_launches"] / max(1, prof["frames"]) * args.steps))
+    if world == 1 and cfg_name == "config2" and args.config3 and not args.dry_run:
+        # BASELINE configs[3] beside the headline (512^3 bf16, 1024^2): its own bench.py run
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", "config3", "--steps", str(min(args.steps, 10)),
+               "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-config3"]
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=900).stdout
+            c3 = json.loads([l for l in out.splitlines() if l.startswith("{")][-1])
+            line["config3"] = {k: c3.get(k) for k in ("value", "unit", "ms_per_step", "steps", "dtype", "dtype_detail",
+                                                      "single_frame_latency_ms", "roofline", "gpu_launches", "clocks")}
+            line["config3"]["workload"] = c3["config"]["workload"]
+            s3 = c3.get("secondary", {})
+            line["config3"]["texture_mlp"] = s3.get("texture_mlp")
+            line["config3"]["conflict_chain_ms_per_frame"] = s3.get("conflict_chain", {}).get("ms_per_frame")
+            line["config3"]["bf16_target"] = {"target_frac_of_burst": 0.5,
+                                              "met": (c3.get("roofline") or {}).get("frac", 0.0) >= 0.5}
+        except Exception as e:  # noqa: BLE001 -- reported, never fatal for the headline
+            line["config3"] = {"error": str(e)[:200]}
     if world == 1 and not args.no_cpu_baseline and not args.dry_run:
         from oracle import oracle as O
         threads = os.cpu_count() or 1
@@ -515,6 +532,8 @@ def main():
                     help="frames in flight per GPU (one context + stream + host thread each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-config3", dest="config3", action="store_false",
+                    help="skip the BASELINE configs[3] (512^3 bf16) run reported beside the config-2 line")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)  # CPU tests of the rank loop
     args = ap.parse_args()
     if args.impl == "reference":

@@ -286,6 +286,31 @@ int icg_texture_batch(icg_context* ctx, const icg_field* field, const double* po
 int icg_composite(const float* image_rgb, const uint8_t* mask, size_t n_image, const float* backdrop,
                   size_t n_backdrop, float* out);
 
+/* marching_cubes(grid, iso) -> TriangleMesh (mesh.hpp:75-156) on the GPU: crossed edges, vertex
+ * interpolation, welding of bit-identical positions, degenerate-triangle removal and first-use
+ * vertex order as the reference; the triangulation of each cube case is generated (face-walk,
+ * see csrc/k_mc.cu), not the reference's Bourke table, so triangles may differ while the vertex
+ * set and the surface agree.  values: (cells+1)^3 fp32 (host or device per `mem`), or NULL for
+ * the grid the last extraction / frame on this context localized (cells ignored).  Outputs are
+ * host arrays; *_capacity too small -> ICG_ECAPACITY with n_vertices / n_triangles set (call
+ * again with room).  cells <= 1023. */
+typedef struct icg_mesh {
+    double* vertices;          /* n_vertices x 3 */
+    uint64_t vertex_capacity;
+    int32_t* triangles;        /* n_triangles x 3, 0-based vertex indices */
+    uint64_t triangle_capacity;
+    uint64_t n_vertices, n_triangles;
+} icg_mesh;
+int icg_marching_cubes(icg_context* ctx, const float* values, int cells, int mem, double iso, icg_mesh* out);
+
+/* The generated triangulation of one cube case (bit c set: Bourke corner c below iso): up to 5
+ * triangles as edge indices (Bourke edge numbering, mesh.hpp:42-46), -1 terminated.  Host only. */
+int icg_mc_case(int case_bits, int8_t* edges16, int* n_triangles);
+
+/* export_obj (mesh.hpp:159-172): "# isocull mesh: ..." header, "v %.9f %.9f %.9f", 1-based "f a b c". */
+int icg_write_obj(const char* path, const double* vertices, uint64_t n_vertices, const int32_t* triangles,
+                  uint64_t n_triangles);
+
 /* compare_iou (localize.hpp:377-387) on device or host arrays of n bytes. */
 int icg_compare_iou(icg_context* ctx, const uint8_t* a, const uint8_t* b, size_t n, int mem,
                     double* iou);

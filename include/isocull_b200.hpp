@@ -28,6 +28,7 @@
 #ifndef ISOCULL_B200_HPP
 #define ISOCULL_B200_HPP
 
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <stdexcept>
@@ -461,6 +462,40 @@ inline RenderedImage render_view(Context& ctx, const Field& field, const CameraS
 inline RenderedImage surface_depth_map(Context& ctx, const Field& field, const CameraSpec& camera,
                                        const AlgoConfig& cfg) {
     return detail::view_render(ctx, field, camera, cfg, {}, false);
+}
+
+struct TriangleMesh {  // mesh.hpp:22-27
+    std::vector<Vec3> vertices;
+    std::vector<std::array<int, 3>> triangles;
+    bool empty() const { return triangles.empty(); }
+};
+
+// marching_cubes(grid, iso), mesh.hpp:75-156, on the GPU (generated triangulation: the vertex set
+// is the reference's, the triangles of a cube may differ); grid = the result of extract()
+inline TriangleMesh marching_cubes(Context& ctx, const LevelGrid& grid, double iso = 0.5) {
+    icg_mesh m{};
+    int rc = icg_marching_cubes(ctx.get(), grid.values.data(), grid.cells, ICG_MEM_HOST, iso, &m);
+    if (rc != ICG_ECAPACITY) check(rc);
+    std::vector<double> v(3 * m.n_vertices);
+    std::vector<std::int32_t> t(3 * m.n_triangles);
+    m.vertices = v.data();
+    m.vertex_capacity = m.n_vertices;
+    m.triangles = t.data();
+    m.triangle_capacity = m.n_triangles;
+    check(icg_marching_cubes(ctx.get(), grid.values.data(), grid.cells, ICG_MEM_HOST, iso, &m));
+    TriangleMesh out;
+    for (std::uint64_t i = 0; i < m.n_vertices; ++i) out.vertices.push_back({v[3 * i], v[3 * i + 1], v[3 * i + 2]});
+    for (std::uint64_t i = 0; i < m.n_triangles; ++i) out.triangles.push_back({t[3 * i], t[3 * i + 1], t[3 * i + 2]});
+    return out;
+}
+
+// export_obj, mesh.hpp:159-172
+inline void export_obj(const TriangleMesh& mesh, const std::string& path) {
+    std::vector<double> v;
+    std::vector<std::int32_t> t;
+    for (const Vec3& p : mesh.vertices) v.insert(v.end(), {p.x, p.y, p.z});
+    for (const auto& tr : mesh.triangles) t.insert(t.end(), {tr[0], tr[1], tr[2]});
+    check(icg_write_obj(path.c_str(), v.data(), mesh.vertices.size(), t.data(), mesh.triangles.size()));
 }
 
 // composite, render.hpp:284-291

@@ -157,6 +157,9 @@ def ref() -> C.CDLL:
         lib.ref_scene_capsules.restype = C.c_void_p
         lib.ref_scene_capsules.argtypes = [C.POINTER(icg_primitive), C.c_int, C.c_double]
         lib.ref_scene_free.argtypes = [C.c_void_p]
+        lib.ref_marching_cubes.argtypes = [f32p, C.c_int, C.c_double, f64p, C.c_int, i32p, C.c_int,
+                                           C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        lib.ref_export_obj.argtypes = [C.c_char_p, f64p, C.c_int, i32p, C.c_int]
         lib.ref_scene_make.restype = C.c_void_p
         lib.ref_scene_make.argtypes = [C.POINTER(icg_primitive), C.c_int, C.c_double, C.c_int, C.c_int, f64p, f64p,
                                        f64p, f64p]
@@ -532,6 +535,20 @@ class RefScene:
             ref().ref_scene_free(self.h)
         except Exception:
             pass
+
+
+def ref_marching_cubes(values: np.ndarray, cells: int, iso: float = 0.5):
+    """The reference's marching_cubes (mesh.hpp:75-156): (vertices (n,3), triangles (m,3))."""
+    v = np.ascontiguousarray(values, np.float32).reshape(-1)
+    nv, nt = C.c_int(), C.c_int()
+    rc = ref().ref_marching_cubes(_p(v, C.c_float), cells, iso, None, 0, None, 0, C.byref(nv), C.byref(nt))
+    if rc:
+        raise ValueError(ref().ref_last_error().decode())
+    V = np.empty((nv.value, 3))
+    T = np.empty((nt.value, 3), np.int32)
+    ref().ref_marching_cubes(_p(v, C.c_float), cells, iso, _p(V, C.c_double), nv.value, _p(T, C.c_int32), nt.value,
+                             C.byref(nv), C.byref(nt))
+    return V, T
 
 
 def ref_render_view(scene: RefScene, yaw, pitch, coarsest, level, bg=(0.0, 0.0, 0.0), workers=1, dist=0.0,

@@ -24,6 +24,7 @@
 #include "isocull/grid.hpp"
 #include "isocull/image.hpp"
 #include "isocull/localize.hpp"
+#include "isocull/mesh.hpp"
 #include "isocull/random.hpp"
 #include "isocull/render.hpp"
 #include "isocull/scene.hpp"
@@ -255,6 +256,43 @@ int ref_scene_texture(void* handle, int* kind, int* axis, double* color, double*
 }
 
 void ref_scene_free(void* s) { delete static_cast<RefScene*>(s); }
+
+// marching_cubes(grid, iso) (mesh.hpp:75-156) on a (cells+1)^3 grid; outputs up to the capacities
+int ref_marching_cubes(const float* values, int cells, double iso, double* vertices, int vcap, int32_t* triangles,
+                       int tcap, int* nv, int* nt) {
+    try {
+        LevelGrid g = LevelGrid::make(0, cells, NodeState::evaluated);
+        std::memcpy(g.values.data(), values, g.values.size() * sizeof(float));
+        TriangleMesh m = marching_cubes(g, iso);
+        *nv = static_cast<int>(m.vertices.size());
+        *nt = static_cast<int>(m.triangles.size());
+        for (int i = 0; i < *nv && i < vcap; ++i) {
+            vertices[3 * i] = m.vertices[i].x;
+            vertices[3 * i + 1] = m.vertices[i].y;
+            vertices[3 * i + 2] = m.vertices[i].z;
+        }
+        for (int i = 0; i < *nt && i < tcap; ++i)
+            for (int c = 0; c < 3; ++c) triangles[3 * i + c] = m.triangles[i][c];
+        return ICG_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, ICG_EINVAL);
+    } catch (const std::exception& e) {
+        return fail(e, ICG_ERUNTIME);
+    }
+}
+
+// export_obj (mesh.hpp:159-172)
+int ref_export_obj(const char* path, const double* vertices, int nv, const int32_t* triangles, int nt) {
+    try {
+        TriangleMesh m;
+        for (int i = 0; i < nv; ++i) m.vertices.push_back({vertices[3 * i], vertices[3 * i + 1], vertices[3 * i + 2]});
+        for (int i = 0; i < nt; ++i) m.triangles.push_back({triangles[3 * i], triangles[3 * i + 1], triangles[3 * i + 2]});
+        export_obj(m, path);
+        return ICG_OK;
+    } catch (const std::exception& e) {
+        return fail(e, ICG_ERUNTIME);
+    }
+}
 
 // Exports the (union-only) primitive list in the C ABI layout; returns -1 if
 // the scene uses a non-union CSG tree.

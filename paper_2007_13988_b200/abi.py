@@ -137,6 +137,11 @@ class icg_image(C.Structure):
     ]
 
 
+class icg_mesh(C.Structure):
+    _fields_ = [("vertices", f64p), ("vertex_capacity", C.c_uint64), ("triangles", i32p),
+                ("triangle_capacity", C.c_uint64), ("n_vertices", C.c_uint64), ("n_triangles", C.c_uint64)]
+
+
 class icg_profile(C.Structure):
     _fields_ = [
         ("kernel_launches", C.c_uint64),
@@ -189,6 +194,9 @@ SIGNATURES = [
     ("icg_texture_batch", C.c_int, [ctx_p, C.POINTER(icg_field), f64p, C.c_size_t, C.c_int, f32p]),
     ("icg_compare_iou", C.c_int, [ctx_p, u8p, u8p, C.c_size_t, C.c_int, f64p]),
     ("icg_composite", C.c_int, [f32p, u8p, C.c_size_t, f32p, C.c_size_t, f32p]),
+    ("icg_marching_cubes", C.c_int, [ctx_p, f32p, C.c_int, C.c_int, C.c_double, C.POINTER(icg_mesh)]),
+    ("icg_mc_case", C.c_int, [C.c_int, C.POINTER(C.c_int8), C.POINTER(C.c_int)]),
+    ("icg_write_obj", C.c_int, [C.c_char_p, f64p, C.c_uint64, i32p, C.c_uint64]),
     ("icg_profile_enable", C.c_int, [ctx_p, C.c_int]),
     ("icg_profile_reset", C.c_int, [ctx_p]),
     ("icg_profile_get", C.c_int, [ctx_p, C.POINTER(icg_profile)]),

@@ -343,6 +343,29 @@ class Context:
         _check(self._lib.icg_gen_feature_map_device(self.h, seed, c, h, w, abi.ICG_MEM_HOST, _ptr(out, C.c_float)))
         return out
 
+    def marching_cubes(self, values: Optional[np.ndarray] = None, iso: float = 0.5):
+        """marching_cubes(grid, iso) (mesh.hpp:75-156) on the GPU: (vertices (n, 3) float64,
+        triangles (m, 3) int32).  values: a (R+1)^3 grid (host), or None for the grid the last
+        extraction on this context localized."""
+        cells = 0
+        vp = None
+        if values is not None:
+            vals = np.ascontiguousarray(values, dtype=np.float32).reshape(-1)
+            cells = int(round(vals.size ** (1.0 / 3.0))) - 1
+            if (cells + 1) ** 3 != vals.size:
+                raise ValueError("marching_cubes: values must hold (R+1)^3 nodes")
+            vp = _ptr(vals, C.c_float)
+        m = abi.icg_mesh()
+        rc = self._lib.icg_marching_cubes(self.h, vp, cells, abi.ICG_MEM_HOST, iso, C.byref(m))
+        if rc != abi.ICG_ECAPACITY:
+            _check(rc)
+        V = np.empty((m.n_vertices, 3), np.float64)
+        T = np.empty((m.n_triangles, 3), np.int32)
+        m.vertices, m.vertex_capacity = _ptr(V, C.c_double), m.n_vertices
+        m.triangles, m.triangle_capacity = _ptr(T, C.c_int32), m.n_triangles
+        _check(self._lib.icg_marching_cubes(self.h, vp, cells, abi.ICG_MEM_HOST, iso, C.byref(m)))
+        return V, T
+
     def occupancy_batch(self, fld: _Field, points: np.ndarray) -> np.ndarray:
         pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
         out = np.empty(len(pts), np.float32)
@@ -554,6 +577,21 @@ def write_float_map(path: str, width: int, height: int, values) -> None:
     with open(path, "wb") as f:
         f.write(np.array([width, height], dtype="<i4").tobytes())
         f.write(a.astype("<f4").tobytes())
+
+
+def write_obj(path: str, vertices, triangles) -> None:
+    """export_obj (mesh.hpp:159-172) through the C ABI (icg_write_obj)."""
+    V = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+    T = np.ascontiguousarray(triangles, dtype=np.int32).reshape(-1, 3)
+    _check(abi.lib().icg_write_obj(path.encode(), _ptr(V, C.c_double), len(V), _ptr(T, C.c_int32), len(T)))
+
+
+def mc_case(case_bits: int):
+    """The generated triangulation of one cube case: a list of (e0, e1, e2) edge triples."""
+    e = (C.c_int8 * 16)()
+    n = C.c_int()
+    _check(abi.lib().icg_mc_case(case_bits, e, C.byref(n)))
+    return [tuple(e[3 * t:3 * t + 3]) for t in range(n.value)]
 
 
 def dump_grid(path: str, level: int, cells: int, values) -> None:

@@ -11,10 +11,9 @@
 
 CSV schema (isocull_cli.cpp:52-59): scene,variant,threshold,R_L,total_evals,accel_factor,iou,wall_ms
 with %.6f doubles; `bench` writes DIR/bench.csv (one brute-force reference per scene and
-resolution, every variant and threshold, :134-172), `extract` appends to DIR/stats.csv (:82-119;
-the mesh is not written: marching cubes is outside this path, the localized grid can be dumped
-instead with --dump-grid), `render` writes DIR/render.ppm and optionally DIR/depth.f32
-(:188-218).  Exit codes: invalid_argument -> 2, other errors -> 1 (:358-364).
+resolution, every variant and threshold, :134-172), `extract` writes the GPU marching-cubes mesh
+DIR/<scene>_<variant>.obj and appends to DIR/stats.csv (:82-119; --dump-grid also dumps the
+localized grid), `render` writes DIR/render.ppm and optionally DIR/depth.f32 (:188-218).  Exit codes: invalid_argument -> 2, other errors -> 1 (:358-364).
 
 Scene files use the reference's JSON format (scene.hpp:204-321) for union scenes: primitives
 sphere / box / capsule / torus with optional center and rotation (yaw, pitch, roll degrees,
@@ -168,6 +167,9 @@ def cmd_extract(a, ctx: api.Context) -> int:
         accel = api.acceleration_factor(res, brute)
         iou = api.compare_iou(res.binarized, brute.binarized, ctx)
     os.makedirs(a.out, exist_ok=True)
+    V, T = ctx.marching_cubes(res.values)
+    obj = os.path.join(a.out, f"{name}_{a.variant}.obj")
+    api.write_obj(obj, V, T)
     path = os.path.join(a.out, "stats.csv")
     fresh = not os.path.exists(path)
     with open(path, "a") as fcsv:
@@ -178,7 +180,7 @@ def cmd_extract(a, ctx: api.Context) -> int:
     if a.dump_grid:
         api.dump_grid(os.path.join(a.out, f"{name}_{a.variant}.grid"), cfg.target_level, res.cells, res.values)
     print(f"extract: {name} ({a.variant}, {a.resolution}^3, tau={tau:g}): evals={res.total_evals} "
-          f"accel={csv_double(accel)} iou={csv_double(iou)}", file=sys.stderr)
+          f"accel={csv_double(accel)} iou={csv_double(iou)} -> {obj}", file=sys.stderr)
     if res.conflict_warning:
         print("extract: warning: conflict pass hit its iteration bound", file=sys.stderr)
     return 0

@@ -148,6 +148,9 @@ struct icg_context {
     bool kept_valid = false;
     icg_algo_config kept_cfg{};
     DBuf set_scratch, set_list, set_total, set_bits;
+    // marching cubes scratch (icg_marching_cubes)
+    DBuf mc_grid, mc_blocks, mc_total, mc_tri_keys, mc_key_bits, mc_keys, mc_tri_ids, mc_keep, mc_first, mc_slot_bits,
+        mc_slots, mc_tri_list, mc_new_id, mc_out_v, mc_out_t;
     // instrumentation
     struct Mark {
         int kind;  // 0 geo mlp, 1 tex mlp, 2 dense, 3 render
@@ -1180,7 +1183,10 @@ int icg_destroy(icg_context* c) {
                    &c->cbin, &c->mixed, &c->tentbin, &c->sel, &c->queued, &c->block_counts, &c->list_e0,
                    &c->cf[0], &c->cf[1], &c->nx[0], &c->nx[1], &c->ctr, &c->binar, &c->pts, &c->outv, &c->geo_pair_stream, &c->tex_pair_stream, &c->geo_pair_hi, &c->tex_pair_hi, &c->geo_pair_f16, &c->geo_pair_f16_hi,
                    &c->depth, &c->rgb, &c->mask, &c->surfk, &c->spts, &c->spx, &c->colrec, &c->cmap, &c->collist, &c->colcnt, &c->sorted, &c->tail_scratch,
-                   &c->set_scratch, &c->set_list, &c->set_total, &c->set_bits,
+                   &c->set_scratch, &c->set_list, &c->set_total, &c->set_bits, &c->mc_grid, &c->mc_blocks,
+                   &c->mc_total, &c->mc_tri_keys, &c->mc_key_bits, &c->mc_keys, &c->mc_tri_ids, &c->mc_keep,
+                   &c->mc_first, &c->mc_slot_bits, &c->mc_slots, &c->mc_tri_list, &c->mc_new_id, &c->mc_out_v,
+                   &c->mc_out_t,
                    &c->geo_fact_stream[0][0], &c->geo_fact_stream[0][1], &c->geo_fact_stream[1][0],
                    &c->geo_fact_stream[1][1]};
     for (DBuf* b : all) b->release();
@@ -1427,6 +1433,103 @@ int icg_level_set(icg_context* c, int level, int which, int mem, uint32_t* out, 
         return r;
     if (mem == ICG_MEM_HOST)
         ICG_CUDA_TRY(cudaMemcpyAsync(out, dst, (size_t)total * 4, cudaMemcpyDeviceToHost, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return ICG_OK;
+}
+
+int icg_marching_cubes(icg_context* c, const float* values, int cells, int mem, double iso, icg_mesh* out) {
+    if (!c || !out) return einval("marching_cubes: null argument");
+    if (mem != ICG_MEM_HOST && mem != ICG_MEM_DEVICE) return einval("marching_cubes: bad mem");
+    if (!values) {
+        if (c->last_buf < 0) return einval("marching_cubes: no localized grid on this context");
+        cells = c->last_cells;
+    }
+    if (cells < 1 || cells > 1023) return einval("marching_cubes: cells must lie in [1, 1023]");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    if (int r = mc_init_tables()) return r;
+    const size_t nn = nodes3(cells), ncell = (size_t)cells * cells * cells;
+    const float* v = values ? values : c->vals[c->last_buf].as<float>();
+    if (values && mem == ICG_MEM_HOST) {
+        if (int r = c->mc_grid.ensure(nn * 4)) return r;
+        ICG_CUDA_TRY(cudaMemcpyAsync(c->mc_grid.p, values, nn * 4, cudaMemcpyHostToDevice, c->stream));
+        v = c->mc_grid.as<float>();
+    }
+    auto read_total = [&](unsigned& x) -> int {
+        ICG_CUDA_TRY(cudaMemcpyAsync(&x, c->mc_total.p, 4, cudaMemcpyDeviceToHost, c->stream));
+        ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return ICG_OK;
+    };
+    // triangles per block of 1024 cells -> offsets -> emit (weld keys in cell order)
+    const unsigned nblocks = (unsigned)((ncell + 1023) / 1024);
+    if (int r = c->mc_blocks.ensure((size_t)nblocks * 4 + 16)) return r;
+    if (int r = c->mc_total.ensure(16)) return r;
+    if (int r = launch_mc_count(v, cells, iso, c->mc_blocks.as<uint32_t>(), nblocks, c->stream)) return r;
+    if (int r = launch_exclusive_scan(c->mc_blocks.as<uint32_t>(), nblocks, c->mc_total.as<unsigned>(), c->stream)) return r;
+    unsigned ntri = 0;
+    if (int r = read_total(ntri)) return r;
+    const size_t nkeybits = 4 * nn;
+    if (int r = c->mc_tri_keys.ensure((size_t)ntri * 12 + 16)) return r;
+    if (int r = c->mc_key_bits.ensure(words(nkeybits) * 4 + 16)) return r;
+    ICG_CUDA_TRY(cudaMemsetAsync(c->mc_key_bits.p, 0, words(nkeybits) * 4 + 16, c->stream));
+    if (int r = launch_mc_emit(v, cells, iso, c->mc_blocks.as<uint32_t>(), nblocks, c->mc_tri_keys.as<uint32_t>(),
+                               c->mc_key_bits.as<uint32_t>(), c->stream))
+        return r;
+    // the used weld keys, ascending (vertex ids before the first-use renumbering)
+    if (int r = c->set_scratch.ensure(bits_to_list_scratch_words(std::max(nkeybits, (size_t)ntri * 3)) * 4)) return r;
+    if (int r = launch_bits_to_list(c->mc_key_bits.as<uint32_t>(), nkeybits, c->set_scratch.as<uint32_t>(), nullptr,
+                                    c->mc_total.as<unsigned>(), c->stream))
+        return r;
+    unsigned nkeys = 0;
+    if (int r = read_total(nkeys)) return r;
+    if (int r = c->mc_keys.ensure((size_t)nkeys * 4 + 16)) return r;
+    if (int r = launch_bits_to_list(c->mc_key_bits.as<uint32_t>(), nkeybits, c->set_scratch.as<uint32_t>(),
+                                    c->mc_keys.as<uint32_t>(), c->mc_total.as<unsigned>(), c->stream))
+        return r;
+    // degenerate filter + first use, surviving vertices in first-use order, surviving triangles
+    if (int r = c->mc_tri_ids.ensure((size_t)ntri * 12 + 16)) return r;
+    if (int r = c->mc_keep.ensure(words(ntri) * 4 + 16)) return r;
+    if (int r = c->mc_first.ensure((size_t)nkeys * 4 + 16)) return r;
+    if (int r = c->mc_slot_bits.ensure(words((size_t)ntri * 3) * 4 + 16)) return r;
+    ICG_CUDA_TRY(cudaMemsetAsync(c->mc_keep.p, 0, words(ntri) * 4 + 16, c->stream));
+    ICG_CUDA_TRY(cudaMemsetAsync(c->mc_first.p, 0xFF, (size_t)nkeys * 4 + 16, c->stream));
+    ICG_CUDA_TRY(cudaMemsetAsync(c->mc_slot_bits.p, 0, words((size_t)ntri * 3) * 4 + 16, c->stream));
+    if (int r = launch_mc_filter(c->mc_tri_keys.as<uint32_t>(), ntri, c->mc_keys.as<uint32_t>(), nkeys, v, cells, iso,
+                                 c->mc_tri_ids.as<uint32_t>(), c->mc_keep.as<uint32_t>(), c->mc_first.as<uint32_t>(),
+                                 c->stream))
+        return r;
+    if (int r = launch_mc_mark_first(c->mc_first.as<uint32_t>(), nkeys, c->mc_slot_bits.as<uint32_t>(), c->stream))
+        return r;
+    if (int r = c->mc_slots.ensure((size_t)nkeys * 4 + 16)) return r;
+    if (int r = launch_bits_to_list(c->mc_slot_bits.as<uint32_t>(), (size_t)ntri * 3, c->set_scratch.as<uint32_t>(),
+                                    c->mc_slots.as<uint32_t>(), c->mc_total.as<unsigned>(), c->stream))
+        return r;
+    unsigned nv = 0;
+    if (int r = read_total(nv)) return r;
+    if (int r = c->mc_tri_list.ensure((size_t)ntri * 4 + 16)) return r;
+    if (int r = launch_bits_to_list(c->mc_keep.as<uint32_t>(), ntri, c->set_scratch.as<uint32_t>(),
+                                    c->mc_tri_list.as<uint32_t>(), c->mc_total.as<unsigned>(), c->stream))
+        return r;
+    unsigned nt = 0;
+    if (int r = read_total(nt)) return r;
+    out->n_vertices = nv;
+    out->n_triangles = nt;
+    c->launches += 12;
+    if ((nv && (!out->vertices || out->vertex_capacity < nv)) || (nt && (!out->triangles || out->triangle_capacity < nt))) {
+        set_error("marching_cubes: output capacity too small (" + std::to_string(nv) + " vertices, " +
+                  std::to_string(nt) + " triangles)");
+        return ICG_ECAPACITY;
+    }
+    if (int r = c->mc_new_id.ensure((size_t)nkeys * 4 + 16)) return r;
+    if (int r = c->mc_out_v.ensure((size_t)nv * 24 + 16)) return r;
+    if (int r = c->mc_out_t.ensure((size_t)nt * 12 + 16)) return r;
+    if (int r = launch_mc_vertices(c->mc_slots.as<uint32_t>(), nv, c->mc_tri_ids.as<uint32_t>(), c->mc_keys.as<uint32_t>(),
+                                   v, cells, iso, c->mc_new_id.as<uint32_t>(), c->mc_out_v.as<double>(), c->stream))
+        return r;
+    if (int r = launch_mc_triangles(c->mc_tri_list.as<uint32_t>(), nt, c->mc_tri_ids.as<uint32_t>(),
+                                    c->mc_new_id.as<uint32_t>(), c->mc_out_t.as<int32_t>(), c->stream))
+        return r;
+    if (nv) ICG_CUDA_TRY(cudaMemcpyAsync(out->vertices, c->mc_out_v.p, (size_t)nv * 24, cudaMemcpyDeviceToHost, c->stream));
+    if (nt) ICG_CUDA_TRY(cudaMemcpyAsync(out->triangles, c->mc_out_t.p, (size_t)nt * 12, cudaMemcpyDeviceToHost, c->stream));
     ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
     return ICG_OK;
 }

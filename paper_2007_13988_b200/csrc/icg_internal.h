@@ -214,6 +214,20 @@ int launch_pifu_pair_texture(const FieldDev& f, const TcMlp& geo, const TcMlp& t
                              cudaStream_t s);
 int launch_fmap_chw_to_hwc(const float* chw, float* hwc, int C, int H, int W, cudaStream_t s);
 int launch_feature_normals(uint64_t seed, size_t n, float* out, cudaStream_t s);
+// marching cubes (k_mc.cu): generated triangulation table, per-cell count / emit, weld, filter
+int mc_init_tables();
+int mc_table_row(int cs, int8_t* out16, int* ntri);
+int launch_mc_count(const float* v, int cells, double iso, uint32_t* block_tris, unsigned nblocks, cudaStream_t s);
+int launch_mc_emit(const float* v, int cells, double iso, const uint32_t* block_off, unsigned nblocks,
+                   uint32_t* tri_keys, uint32_t* key_bits, cudaStream_t s);
+int launch_mc_filter(const uint32_t* tri_keys, unsigned ntri, const uint32_t* keys, unsigned nkeys, const float* v,
+                     int cells, double iso, uint32_t* tri_ids, uint32_t* keep, uint32_t* first_use, cudaStream_t s);
+int launch_mc_mark_first(const uint32_t* first_use, unsigned nkeys, uint32_t* slot_bits, cudaStream_t s);
+int launch_mc_vertices(const uint32_t* slots, unsigned nv, const uint32_t* tri_ids, const uint32_t* keys,
+                       const float* v, int cells, double iso, uint32_t* new_id, double* out_v, cudaStream_t s);
+int launch_mc_triangles(const uint32_t* tri_list, unsigned nt, const uint32_t* tri_ids, const uint32_t* new_id,
+                        int32_t* out_t, cudaStream_t s);
+int launch_exclusive_scan(uint32_t* counts, unsigned n, unsigned* total, cudaStream_t s);
 
 // grid kernels (k_grid.cu)
 struct LevelBufs {

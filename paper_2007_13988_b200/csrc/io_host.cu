@@ -57,6 +57,18 @@ int icg_write_float_map(const char* path, int width, int height, const float* va
     return ICG_OK;
 }
 
+// export_obj (mesh.hpp:159-172)
+int icg_write_obj(const char* path, const double* v, uint64_t nv, const int32_t* t, uint64_t nt) {
+    if (!path || (nv && !v) || (nt && !t)) return io_fail("export_obj: bad arguments", ICG_EINVAL);
+    File out(path, "w");
+    if (!out.f) return io_fail(std::string("export_obj: cannot open ") + path, ICG_ERUNTIME);
+    std::fprintf(out.f, "# isocull mesh: %llu vertices, %llu triangles\n", (unsigned long long)nv, (unsigned long long)nt);
+    for (uint64_t i = 0; i < nv; ++i) std::fprintf(out.f, "v %.9f %.9f %.9f\n", v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    for (uint64_t i = 0; i < nt; ++i) std::fprintf(out.f, "f %d %d %d\n", t[3 * i] + 1, t[3 * i + 1] + 1, t[3 * i + 2] + 1);
+    if (std::ferror(out.f)) return io_fail(std::string("export_obj: write failed for ") + path, ICG_ERUNTIME);
+    return ICG_OK;
+}
+
 // dump_grid (grid.hpp:199-209): int32 level, int32 R, then (R+1)^3 float32 values x-fastest
 int icg_dump_grid(const char* path, int level, int cells, const float* values) {
     if (!path || cells < 0 || !values) return io_fail("dump_grid: bad arguments", ICG_EINVAL);

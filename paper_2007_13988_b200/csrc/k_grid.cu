@@ -760,6 +760,13 @@ int launch_all_bits(uint32_t* bits, size_t nbits, cudaStream_t s) {
     return ICG_OK;
 }
 
+// in-place exclusive scan of n counts (one block), *total = their sum
+int launch_exclusive_scan(uint32_t* counts, unsigned n, unsigned* total, cudaStream_t s) {
+    k_scan_total<<<1, 1024, 0, s>>>(counts, n, total);
+    ICG_CUDA_TRY(cudaGetLastError());
+    return ICG_OK;
+}
+
 size_t bits_to_list_scratch_words(size_t nbits) {
     const size_t nw = (nbits + 31) / 32;
     return (nw + kWordsPerCta - 1) / kWordsPerCta + 2;

@@ -132,6 +132,7 @@ static int gpu_mode() {
     oc.variant = ib::Variant::octree_threshold;
     oc.threshold = 0.12;
     ib::ExtractionResult ot = ib::extract(ctx, an, oc);
+    ib::TriangleMesh mesh = ib::marching_cubes(ctx, p.grid);
     // invalid config -> std::invalid_argument from the library itself
     bool threw = false;
     try {
@@ -146,13 +147,14 @@ static int gpu_mode() {
     std::printf("{\"mode\": \"gpu\", \"evals\": [%llu, %llu, %llu], \"total\": %llu, \"value_sum\": %.17g, "
                 "\"covered\": %d, \"rgb_sum\": %.17g, \"c0_evals\": [%llu, %llu, %llu, %llu], \"iou\": %.17g, "
                 "\"accel\": %.17g, \"invalid_threw\": %s, \"rv_covered\": %d, \"rv_calls\": %llu, "
-                "\"octree_evals\": %llu}\n",
+                "\"octree_evals\": %llu, \"mesh_vertices\": %zu, \"mesh_triangles\": %zu}\n",
                 (unsigned long long)r.evals_per_level[0], (unsigned long long)r.evals_per_level[1],
                 (unsigned long long)r.evals_per_level[2], (unsigned long long)r.total_evals, vsum, covered, rgbsum,
                 (unsigned long long)p.evals_per_level[0], (unsigned long long)p.evals_per_level[1],
                 (unsigned long long)p.evals_per_level[2], (unsigned long long)p.evals_per_level[3], iou,
                 ib::acceleration_factor(p, bt), threw ? "true" : "false", rv_cov,
-                (unsigned long long)rv.oracle_calls, (unsigned long long)ot.total_evals);
+                (unsigned long long)rv.oracle_calls, (unsigned long long)ot.total_evals, mesh.vertices.size(),
+                mesh.triangles.size());
     return 0;
 }
 

@@ -54,6 +54,7 @@ def test_adapter_frame_matches_python_face(demo):
         tan = api.AnalyticField(caps, 0.02, {"kind": abi.ICG_TEXTURE_CONSTANT, "color": [0.25, 0.5, 0.75]})
         rv = ctx.render_view(tan, api.CameraSpec.from_angles(30, 20), api.AlgoConfig("progressive", 8, 3))
         ot = ctx.extract(an, api.AlgoConfig("octree_threshold", 8, 3, threshold=0.12))
+        mv, mt = ctx.marching_cubes(p.values)
     assert d["evals"] == ext.evals_per_level and d["total"] == ext.total_evals
     assert d["value_sum"] == pytest.approx(float(np.sum(ext.values, dtype=np.float64)), rel=1e-12)
     assert d["covered"] == img.covered_pixels
@@ -64,3 +65,4 @@ def test_adapter_frame_matches_python_face(demo):
     assert d["invalid_threw"] is True
     assert d["rv_covered"] == rv.covered_pixels and d["rv_calls"] == rv.oracle_calls
     assert d["octree_evals"] == ot.total_evals
+    assert d["mesh_vertices"] == len(mv) and d["mesh_triangles"] == len(mt)

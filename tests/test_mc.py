@@ -1,0 +1,95 @@
+"""Marching cubes (mesh.hpp:75-172).  The GPU kernel uses a generated
+triangulation (face walk, csrc/k_mc.cu) instead of the reference's Bourke table, so the checks
+are: the table is a valid closed triangulation of every case; against the reference's own
+marching_cubes the vertex set is identical (same crossed edges, same fp64 interpolation, same
+welding) with the same triangle count, area and volume within 0.2 % at 64^3; the GPU output
+equals the numpy restatement (tests/mc_numpy.py) bit for bit; OBJ files match export_obj."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2007_13988_b200 import api
+
+from . import mc_numpy as M
+
+EDGE_ENDS = [(0, 1), (1, 2), (2, 3), (3, 0), (4, 5), (5, 6), (6, 7), (7, 4), (0, 4), (1, 5), (2, 6), (3, 7)]
+
+
+@pytest.fixture(scope="module")
+def table():
+    return [api.mc_case(c) for c in range(256)]
+
+
+def test_generated_table_is_a_closed_triangulation(table):
+    assert table[0] == [] and table[255] == []
+    for cs in range(256):
+        crossed = {e for e, (a, b) in enumerate(EDGE_ENDS) if ((cs >> a) & 1) != ((cs >> b) & 1)}
+        used = {e for t in table[cs] for e in t}
+        assert used == crossed, cs
+        # inside the cube every triangle edge between two crossed edges is shared by exactly two
+        # triangles, except the polygon boundary edges, which lie on cube faces (one use each)
+        cnt = {}
+        for t in table[cs]:
+            for x, y in ((t[0], t[1]), (t[1], t[2]), (t[2], t[0])):
+                cnt[(min(x, y), max(x, y))] = cnt.get((min(x, y), max(x, y)), 0) + 1
+        assert all(v in (1, 2) for v in cnt.values()), cs
+        assert len(table[cs]) <= 5
+    # complementary cases cut the same edges
+    for cs in range(256):
+        assert {e for t in table[cs] for e in t} == {e for t in table[255 - cs] for e in t}
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference shim not built")
+def test_numpy_restatement_against_reference_marching_cubes(table):
+    caps = O.gen_capsules(42)
+    r = O.extract_progressive(O.Analytic(caps, 0.02, threads=4), 16, 2)
+    V, T = M.marching_cubes(r["values"], 64, table)
+    RV, RT = O.ref_marching_cubes(r["values"], 64)
+    assert set(map(tuple, V)) == set(map(tuple, RV)) and len(T) == len(RT)
+    a, vol = M.area_and_volume(V, T)
+    ra, rvol = M.area_and_volume(RV, RT)
+    assert abs(a / ra - 1) < 2e-3 and abs(vol / rvol - 1) < 2e-3
+    assert all(c == 2 for c in M.edge_use_counts(T).values())  # closed 2-manifold
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference shim not built")
+def test_obj_writer_matches_reference(tmp_path, table):
+    V = np.random.default_rng(1).uniform(-1, 1, (7, 3))
+    T = np.array([[0, 1, 2], [2, 3, 4], [4, 5, 6]], np.int32)
+    a, b = str(tmp_path / "a.obj"), str(tmp_path / "b.obj")
+    api.write_obj(a, V, T)
+    Vc, Tc = np.ascontiguousarray(V), np.ascontiguousarray(T)
+    assert O.ref().ref_export_obj(b.encode(), Vc.ctypes.data_as(O.f64p), 7, Tc.ctypes.data_as(O.i32p), 3) == 0
+    assert open(a).read() == open(b).read()
+
+
+@pytest.mark.gpu
+def test_gpu_marching_cubes_equals_restatement(gpu_ctx, table):
+    caps = O.gen_capsules(42)
+    for r0, lv in ((16, 1), (16, 2)):
+        cells = r0 << lv
+        r = O.extract_progressive(O.Analytic(caps, 0.02, threads=4), r0, lv)
+        V, T = gpu_ctx.marching_cubes(r["values"])
+        NV, NT = M.marching_cubes(r["values"], cells, table)
+        assert np.array_equal(V, NV) and np.array_equal(T, NT)
+
+
+@pytest.mark.gpu
+def test_gpu_marching_cubes_config2_grid_against_reference(gpu_ctx, pifu_inputs):
+    """The config-2 grid (256^3, localized on the GPU and kept on the context) meshed on the
+    GPU, against the reference's marching_cubes of the same grid."""
+    from paper_2007_13988_b200 import abi
+    inp = pifu_inputs
+    gpu_ctx.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+    f = api.PifuField(inp["fmap"], inp["caps"], 50.0, abi.ICG_PREC_FP32)
+    ext = gpu_ctx.extract(f, api.AlgoConfig("progressive", 32, 3))
+    V, T = gpu_ctx.marching_cubes()  # the context's localized grid, no copy
+    RV, RT = O.ref_marching_cubes(ext.values, 256)
+    # the crossed edges are the reference's: the vertex sets agree up to vertices that only a
+    # degenerate triangle of one of the two triangulations used
+    sv, sr = set(map(tuple, V)), set(map(tuple, RV))
+    assert len(sv ^ sr) <= 1e-4 * len(sr), len(sv ^ sr)
+    assert abs(len(T) - len(RT)) <= 1e-4 * len(RT)
+    a, vol = M.area_and_volume(V, T)
+    ra, rvol = M.area_and_volume(RV, RT)
+    assert abs(a / ra - 1) < 2e-3 and abs(vol / rvol - 1) < 2e-3
