@@ -441,6 +441,16 @@ static int tail_setup(int sms) {
     return ICG_OK;
 }
 
+// CTAs of the tail when other frames share the device (ICG_TAIL_SHARED=32|64, default 32: the
+// cooperative kernel holds its SMs for the whole chain; 32 CTAs gave 375 vs 363 frames/s at 4 in flight)
+static int shared_width() {
+    static const int w = [] {
+        const char* e = getenv("ICG_TAIL_SHARED");
+        return e && atoi(e) == 64 ? 64 : 32;
+    }();
+    return w;
+}
+
 // wide: the frame is alone on the device (148-CTA grid, lower latency); otherwise 64 CTAs
 int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_new, unsigned max_cols, cudaStream_t s,
                 bool wide) {
@@ -449,6 +459,7 @@ int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_n
             int dev = 0, sms = 0;
             ICG_CUDA_TRY(cudaGetDevice(&dev));
             ICG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            if (int e = tail_setup<32>(sms)) return e;
             if (int e = tail_setup<64>(sms)) return e;
             return tail_setup<148>(sms);
         }))
@@ -486,6 +497,9 @@ int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_n
     if (wide)
         ICG_CUDA_TRY(cudaLaunchCooperativeKernel((void*)tail::k_tail<148>, 148, tail::kThreads, args,
                                                  sizeof(tail::TailCfg<148>::Smem), s));
+    else if (shared_width() == 32)
+        ICG_CUDA_TRY(cudaLaunchCooperativeKernel((void*)tail::k_tail<32>, 32, tail::kThreads, args,
+                                                 sizeof(tail::TailCfg<32>::Smem), s));
     else
         ICG_CUDA_TRY(cudaLaunchCooperativeKernel((void*)tail::k_tail<64>, 64, tail::kThreads, args,
                                                  sizeof(tail::TailCfg<64>::Smem), s));
