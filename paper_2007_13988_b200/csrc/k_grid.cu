@@ -140,6 +140,43 @@ k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const 
         const uint32_t rowbase = row * (uint32_t)fn;
         const bool even_jk = !((j | k) & 1);
         const uint32_t cbase = (uint32_t)cn * ((uint32_t)j0 + (uint32_t)cn * (uint32_t)k0);
+        // rows away from the surface (most of them): no adjacent mixed cell and a uniform parent box
+        // along the whole row -> every non-even node is the uniform value 0 or 1, nothing selected
+        {
+            const uint32_t valid = lane < cwords ? (lane == cwords - 1 && (cn & 31) ? (1u << (cn & 31)) - 1u : ~0u) : 0u;
+            const uint32_t p0 = lane < cwords ? pl[0][lane] & valid : 0u, p1 = lane < cwords ? pl[1][lane] & valid : 0u,
+                           p2 = lane < cwords ? pl[2][lane] & valid : 0u;
+            const uint32_t full = lgr == 0 ? p0 : lgr == 1 ? p1 : p2;  // count == 2^lgr (all parents inside)
+            const bool any_mixed = __any_sync(0xffffffffu, lane < mwords && mr[lane] != 0u);
+            const bool all0 = !__any_sync(0xffffffffu, (p0 | p1 | p2) != 0u);
+            const bool all1 = !__any_sync(0xffffffffu, lane < cwords && (full != valid || (lgr >= 1 && (p0 & valid)) ||
+                                                                          (lgr == 2 && (p1 & valid))));
+            if (!any_mixed && (all0 || all1)) {
+                const float u = all1 ? 1.0f : 0.0f;
+                for (int i0w = 0; i0w < fn; i0w += 32) {
+                    const int i = i0w + lane;
+                    if (i < fn) {
+                        float v = u;
+                        uint8_t st = ICG_STATE_INTERPOLATED;
+                        if (even_jk && !(i & 1)) {
+                            v = __ldg(&cv[cbase + (i >> 1)]);
+                            st = __ldg(&cs[cbase + (i >> 1)]);
+                        }
+                        fv[rowbase + i] = v;
+                        fs[rowbase + i] = st;
+                    }
+                    if (all1) {
+                        const unsigned tbw = __ballot_sync(0xffffffffu, i < fn);
+                        if (lane == 0) {
+                            const uint32_t first = rowbase + (uint32_t)i0w, sh = first & 31u, w = first >> 5;
+                            atomicOr(&tentbin[w], tbw << sh);
+                            if (sh && (tbw >> (32 - sh))) atomicOr(&tentbin[w + 1], tbw >> (32 - sh));
+                        }
+                    }
+                }
+                continue;
+            }
+        }
         auto count = [&](int x) -> int {
             const int w = x >> 5, sh = x & 31;
             return (int)((pl[0][w] >> sh) & 1u) + 2 * (int)((pl[1][w] >> sh) & 1u) + 4 * (int)((pl[2][w] >> sh) & 1u);
