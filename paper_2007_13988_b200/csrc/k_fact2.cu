@@ -222,10 +222,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t tfph = 0;
             const bool tr = P.trace && blockIdx.x == 0;
             unsigned long long w_chunk = 0, w_full = 0, w_tm = 0, t_begin = gtime();
+            unsigned long long w_ph[4] = {0, 0, 0, 0};  // chunk waits by phase: h1 first / h1 rest / h2 / h3
+            int wph = 0;
             auto wait_chunk = [&](uint32_t c) {
                 const unsigned long long t0 = tr ? gtime() : 0;
                 ptx::mbar_wait_cluster(&ms.a_ready[c % kA], (c / kA) & 1u);
-                if (tr) w_chunk += gtime() - t0;
+                if (tr) {
+                    w_chunk += gtime() - t0;
+                    w_ph[wph] += gtime() - t0;
+                }
                 ptx::tc_fence_after();
             };
             // one weight item (4 K steps) against activation chunk c into D columns dcol
@@ -271,6 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // (the previous tile's D3) are free once its h3 chunks were emitted, so the first
                 // item goes ahead; columns 256-511 (its D4) wait for the output layer to read them.
                 for (int kc = 0; kc < 16; ++kc) {
+                    wph = kc == 0 ? 0 : 1;
                     wait_chunk(ac);
                     item(ac, 0, kc == 0);
                     if (kc == 15) ptx::mma_commit_pair(&ms.d2a, both);  // h2 chunks 0-3 may be drained
@@ -288,6 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mma_commit_pair(&ms.d2done, both);
                 // layer 3 into D3 = columns 0-255: its first MMA needs h2 chunks 0-3 (D2 columns
                 // 0-255) read, i.e. all four of them emitted
+                wph = 2;
                 for (uint32_t c = ac; c < ac + 4; ++c) wait_chunk(c);
                 for (int kc = 0; kc < 8; ++kc) {
                     if (kc >= 4) wait_chunk(ac);
@@ -297,6 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 ptx::mma_commit_pair(&ms.d3done, both);
                 // layer 4 into D4 = columns 256-511 (D2's upper half was read as h2 chunks 4-7)
+                wph = 3;
                 for (int kc = 0; kc < 4; ++kc) {
                     wait_chunk(ac);
                     item(ac, 256, kc == 0);
@@ -310,6 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 P.trace[1] = w_chunk;
                 P.trace[2] = w_full;
                 P.trace[3] = w_tm;
+                for (int q = 0; q < 4; ++q) P.trace[10 + q] = w_ph[q];
             }
         }
     } else {
@@ -667,6 +676,8 @@ int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, con
                 "wait slot %.1f, wait acc %.1f, prep %.1f, h1 %.1f, final %.1f\n",
                 t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3, t[6] * 1e-3, t[7] * 1e-3,
                 t[8] * 1e-3, t[9] * 1e-3);
+        fprintf(stderr, "[fact2-trace] chunk waits by phase: h1 first %.1f, h1 rest %.1f, h2 %.1f, h3 %.1f us\n",
+                t[10] * 1e-3, t[11] * 1e-3, t[12] * 1e-3, t[13] * 1e-3);
     }
     return ICG_OK;
 }

@@ -584,29 +584,56 @@ def test_level_sets_config0_match_oracle(gpu_ctx):
 @pytest.mark.gpu
 def test_frame_graph_survives_shape_changes(pifu_inputs):
     """A captured frame graph must not be replayed after the context's work buffers moved
-    (a larger grid / image / feature map in between): frame(A) x3 (graph captured), then a larger
-    frame B and a larger extraction, then frame(A) again — every output equals a fresh context's."""
+    (a larger grid / image / feature map in between).  Frame A runs with FIXED pinned output
+    buffers (grid + image), so the second and later calls replay its CUDA graph; a larger frame B
+    and a larger extraction then grow the buffers; frame A again must equal a fresh context's."""
+    import ctypes as C
     inp = pifu_inputs
     ctx = api.Context(0)
     ctx.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
     ctx.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
-    fa = api.PifuField(inp["fmap"][:, :64, :64], inp["caps"], 50.0, abi.ICG_PREC_FP32)
+    fa = api.PifuField(np.ascontiguousarray(inp["fmap"][:, :64, :64]), inp["caps"], 50.0, abi.ICG_PREC_FP32)
     fb = api.PifuField(inp["fmap"], inp["caps"], 50.0, abi.ICG_PREC_FP32)
     cam = api.CameraSpec.from_angles(90, 0)
     ca, cb = api.AlgoConfig("progressive", 16, 2), api.AlgoConfig("progressive", 16, 3)
-    first = [ctx.frame(fa, ca, cam, 64, 64, want_grid=True) for _ in range(3)][-1]
-    ctx.frame(fb, cb, cam, 256, 256)
+    W = H = 64
+    n3 = 65 ** 3
+    sizes = {"depth": W * H * 4, "rgb": W * H * 12, "mask": W * H, "sk": W * H * 4, "v": n3 * 4, "s": n3}
+    ptrs = {k: api.host_alloc(b) for k, b in sizes.items()}
+    img = abi.icg_image()
+    img.mem = abi.ICG_MEM_HOST
+    img.depth = C.cast(C.c_void_p(ptrs["depth"]), abi.f32p)
+    img.rgb = C.cast(C.c_void_p(ptrs["rgb"]), abi.f32p)
+    img.mask = C.cast(C.c_void_p(ptrs["mask"]), abi.u8p)
+    img.surface_k = C.cast(C.c_void_p(ptrs["sk"]), abi.i32p)
+    ext = abi.icg_extraction()
+    ext.mem = abi.ICG_MEM_HOST
+    ext.values = C.cast(C.c_void_p(ptrs["v"]), abi.f32p)
+    ext.states = C.cast(C.c_void_p(ptrs["s"]), abi.u8p)
+
+    def view(k, dt, n):
+        return np.ctypeslib.as_array((C.c_uint8 * (n * np.dtype(dt).itemsize)).from_address(ptrs[k])).view(dt).copy()
+
+    def frame_a():
+        e, im = ctx.frame_raw(fa, ca, cam, W, H, img, ext)
+        return (e.cells, view("v", np.float32, n3), view("s", np.uint8, n3), view("rgb", np.float32, W * H * 3),
+                view("sk", np.int32, W * H))
+
+    outs = [frame_a() for _ in range(4)]  # eager, warm, captured, replayed
+    ctx.frame(fb, cb, cam, 256, 256)      # larger grid / image: buffers grow
     ctx.extract(fb, api.AlgoConfig("progressive", 32, 3))
-    again = [ctx.frame(fa, ca, cam, 64, 64, want_grid=True) for _ in range(3)]
+    outs += [frame_a() for _ in range(4)]
     ctx.close()
+    for p_ in ptrs.values():
+        api.host_free(p_)
     with api.Context(0) as fresh:
         fresh.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
         fresh.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
-        ref = fresh.frame(fa, ca, cam, 64, 64, want_grid=True)
-    for ext, img in [first] + again:
-        assert ext.cells == 64
-        assert np.array_equal(ext.values, ref[0].values) and np.array_equal(ext.states, ref[0].states)
-        assert np.array_equal(img.rgb, ref[1].rgb) and np.array_equal(img.surface_k, ref[1].surface_k)
+        ref_e, ref_i = fresh.frame(fa, ca, cam, W, H, want_grid=True)
+    for cells, v, st, rgb, sk in outs:
+        assert cells == 64
+        assert np.array_equal(v, ref_e.values) and np.array_equal(st, ref_e.states)
+        assert np.array_equal(rgb, ref_i.rgb.reshape(-1)) and np.array_equal(sk, ref_i.surface_k.reshape(-1))
 
 
 @pytest.mark.gpu
