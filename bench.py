@@ -405,16 +405,16 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
                 for _ in range(2):
                     ln.frame(host=True, flush=False)
             shard.barrier()
-            e2e_t = allmax(run_frames(args.steps, host=True, flush=False) / 1e3)
+            e2e_t = allmax(run_frames(args.steps, host=True, flush=True) / 1e3)
             e2e = {"value": world * args.steps / e2e_t, "unit": "frames/s", "h2d_bytes_per_step": fbytes,
                    "d2h_bytes_per_step": npx * (4 + 12 + 1 + 4),
-                   "note": "feature map H2D + depth/RGB/mask/first-crossing-index D2H in every timed call; the "
-                           "localized grid stays on the device (see e2e_with_grid)"}
+                   "note": "feature map H2D + depth/RGB/mask/first-crossing-index D2H in every timed call, L2 flushed "
+                           "before each; the localized grid stays on the device (see e2e_with_grid)"}
             for ln in lanes:
                 ln.frame(host=True, flush=False, grid=True)
             shard.barrier()
             n3 = ((r0 << lv) + 1) ** 3
-            eg_t = allmax(run_frames(args.steps, host=True, flush=False, grid=True) / 1e3)
+            eg_t = allmax(run_frames(args.steps, host=True, flush=True, grid=True) / 1e3)
             e2e_grid = {"value": world * args.steps / eg_t, "unit": "frames/s", "h2d_bytes_per_step": fbytes,
                         "d2h_bytes_per_step": npx * (4 + 12 + 1 + 4) + 5 * n3,
                         "note": "as e2e, plus the final grid (f32 values + u8 states) D2H every frame"}

@@ -226,7 +226,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int wph = 0;
             auto wait_chunk = [&](uint32_t c) {
                 const unsigned long long t0 = tr ? gtime() : 0;
-                ptx::mbar_wait_cluster(&ms.a_ready[c % kA], (c / kA) & 1u);
+                ptx::mbar_wait(&ms.a_ready[c % kA], (c / kA) & 1u);
                 if (tr) {
                     w_chunk += gtime() - t0;
                     w_ph[wph] += gtime() - t0;
@@ -282,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (kc == 15) ptx::mma_commit_pair(&ms.d2a, both);  // h2 chunks 0-3 may be drained
                     if (kc == 0 && t != pair_id) {
                         const unsigned long long t0 = tr ? gtime() : 0;
-                        ptx::mbar_wait_cluster(&ms.tm_free, tfph);
+                        ptx::mbar_wait(&ms.tm_free, tfph);
                         if (tr) w_tm += gtime() - t0;
                         tfph ^= 1;
                         ptx::tc_fence_after();
@@ -339,7 +339,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float w5z = __ldg(&P.wlast[128 + kGeoSkip - 1]);
         uint32_t ac = 0, d2aph = 0, d2ph = 0, d3ph = 0, d4ph = 0;
         const bool etr = P.trace && blockIdx.x == 0 && et == 0;
-        unsigned long long e_free = 0, e_d = 0, e_prep = 0, e_h1 = 0, e_fin = 0, e_begin = gtime();
+        unsigned long long e_free = 0, e_d = 0, e_prep = 0, e_h1 = 0, e_fin = 0, e_dr = 0, e_begin = gtime();
         // kFW activations of this thread (features cq kFW .. of the chunk) -> chunk slot, hi and lo
         auto store_chunk = [&](const float* v, uint32_t a) {
             const uint32_t base = arow + (a % kA) * kAChunk;
@@ -372,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0)
-                for (int i = 0; i < cnt; ++i) ptx::mbar_arrive_cluster(a_ready0 + 8u * ((ac + i) % kA));
+                for (int i = 0; i < cnt; ++i) ptx::mbar_arrive_remote(a_ready0 + 8u * ((ac + i) % kA));
             ac += cnt;
         };
         auto wait_d = [&](uint64_t* bar, uint32_t& par) {
@@ -555,7 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(tm_free0);  // D3 / D4 are free for the next tile
+            if (lane == 0) ptx::mbar_arrive_remote(tm_free0);  // D3 / D4 are free for the next tile
             ms.red[cq][row] = part;
             epi_bar();
             if (cq == 0 && q.valid) {
@@ -593,7 +593,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (has_next) nxt = prep(t + npairs, pb ^ 1, pre_next);
             if (etr) e_prep += gtime() - tq;
             wait_d(&ms.d2a, d2aph);
+            tq = etr ? gtime() : 0;
             drain(cur, 0, 4, 0, b2, 512, 1024);
+            if (etr) e_dr += gtime() - tq;
             wait_d(&ms.d2done, d2ph);
             drain(cur, 4, 8, 0, b2, 512, 1024);
             wait_d(&ms.d3done, d3ph);
@@ -615,6 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             P.trace[7] = e_prep;
             P.trace[8] = e_h1;
             P.trace[9] = e_fin;
+            P.trace[14] = e_dr;
         }
     }
     ptx::tc_fence_before();
@@ -676,8 +679,8 @@ int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, con
                 "wait slot %.1f, wait acc %.1f, prep %.1f, h1 %.1f, final %.1f\n",
                 t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3, t[6] * 1e-3, t[7] * 1e-3,
                 t[8] * 1e-3, t[9] * 1e-3);
-        fprintf(stderr, "[fact2-trace] chunk waits by phase: h1 first %.1f, h1 rest %.1f, h2 %.1f, h3 %.1f us\n",
-                t[10] * 1e-3, t[11] * 1e-3, t[12] * 1e-3, t[13] * 1e-3);
+        fprintf(stderr, "[fact2-trace] chunk waits by phase: h1 first %.1f, h1 rest %.1f, h2 %.1f, h3 %.1f us; drain h2 0-3 %.1f\n",
+                t[10] * 1e-3, t[11] * 1e-3, t[12] * 1e-3, t[13] * 1e-3, t[14] * 1e-3);
     }
     return ICG_OK;
 }

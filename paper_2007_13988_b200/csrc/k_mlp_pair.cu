@@ -541,7 +541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 ev(100 + 10 * buf + half);
                 const unsigned long long t0 = tr ? gtime() : 0;
                 const uint32_t bit = (uint32_t)(2 * buf + half);
-                ptx::mbar_wait_cluster(&ms.h_ready[buf][half], (hph_bits >> bit) & 1u);
+                ptx::mbar_wait(&ms.h_ready[buf][half], (hph_bits >> bit) & 1u);
                 if (tr) w_h += gtime() - t0;
                 hph_bits ^= 1u << bit;
                 ptx::tc_fence_after();
@@ -605,7 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             for (unsigned t = pair_id; t < ntiles; t += npairs) {
                 if constexpr (!FACT) {  // FACT: operands arrive through the h buffers only
                     const unsigned long long t0 = tr ? gtime() : 0;
-                    ptx::mbar_wait_cluster(&ms.f_ready, fph);
+                    ptx::mbar_wait(&ms.f_ready, fph);
                     if (tr) w_f += gtime() - t0;
                 }
                 fph ^= 1;
@@ -926,7 +926,14 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                 ptx::fence_proxy_async_cluster();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(h_ready0 + 16u * (uint32_t)buf);
+            if (lane == 0) {
+                // own shared memory only: CTA-scope release (no MEMBAR.ALL.GPU); DSMEM stores to the
+                // peer keep the cluster-scope release
+                if (local_dst)
+                    ptx::mbar_arrive_remote(h_ready0 + 16u * (uint32_t)buf);
+                else
+                    ptx::mbar_arrive_cluster(h_ready0 + 16u * (uint32_t)buf);
+            }
             if (etr) {
                 e_cyc[2] += clock64() - c0;
                 e_emit += gtime() - e_t0;
@@ -1123,7 +1130,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
             }
             ptx::fence_proxy_async_smem();  // the skip operand is this CTA's own shared memory
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(f_ready0);
+            if (lane == 0) ptx::mbar_arrive_remote(f_ready0);
         };
 
         // ---- final layer (CTA 0 holds layer-4 rows 0..127 for all points) ----
@@ -1240,7 +1247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(Cfg<MODE>::kMaxReg)
                         }
                     }
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive_cluster(acc_free0 + 8u * (uint32_t)a);
+                    ptx::mbar_arrive_remote(acc_free0 + 8u * (uint32_t)a);
                     ++cb;
                 }
                 if (t + npairs < ntiles) {

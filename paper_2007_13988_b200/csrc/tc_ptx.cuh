@@ -177,6 +177,16 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// arrive on a (possibly remote) cluster barrier with the default .release.cta semantics: the
+// .release.cluster form compiles to MEMBAR.ALL.GPU before the arrive.  For a producer whose data
+// reaches the consumer through the async proxy (its own shared memory, published by
+// fence.proxy.async, read by tcgen05.mma) the CTA-scope pair is enough -- the convention of
+// CUTLASS's ClusterBarrier (arrive(cta_id) / wait).
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// acquire.cluster: the SASS invalidates the SM's L1 (CCTL.IVALL) on every successful wait
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
