@@ -431,13 +431,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             epi_bar();
             const float p3[3] = {ms.ppos[pb][row][0], ms.ppos[pb][row][1], ms.ppos[pb][row][2]};
             const int sl = ms.pslot[pb][row];
-            // the layer-1 record terms this thread will read for the tile, into L1 ahead of emit_h1
-            // (one 64-byte line per chunk: features c*64 + cq*kFW, kFW floats)
-            if (q.valid) {
-                const float* rp = P.s_in + (size_t)sl * kSRow + cq * kFW;
-#pragma unroll 4
-                for (int c = 0; c < 16; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + c * 64));
-            }
+            // the tile's column records into L2 (one bulk prefetch per distinct column; the list is
+            // sorted by column): the records of a large level do not stay in L2 after the column
+            // pass, and the epilogue's loads would wait on DRAM one chunk at a time
+            if (cq == 0 && q.valid && (row == 0 || ms.pslot[pb][row - 1] != sl))
+                ptx::prefetch_l2_bulk(P.s_in + (size_t)sl * kSRow, kSRow * 4);
             float d = 3.0e38f;
             const int nc = ms.ncaps;
             if (nc >= 0) {
@@ -460,28 +458,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         };
         // layer 1 (no MMA): chunks [c0, c1) of act(S1 + w1z z + b1)
         // layer 1 in pairs of chunks [c0, c1) (c1 - c0 even)
-        auto prefetch_l1 = [](const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); };
         constexpr int kG = Prec<X3>::kG;
         auto emit_h1 = [&](const Pt& q, int c0, int c1) {
             for (int kg = c0; kg < c1; kg += kG) {
               for (int kc = kg; kc < kg + kG; kc += 2) {
-                // the record terms and biases the drains of layers 2-4 read, into L1 ahead of time
-                // (pair kc: h2 chunk kc/2; pairs 0-3 also h3 chunk kc/2, pair 4 the layer-4 slice)
-                {
-                    const int c = kc >> 1, fo = cq * kFW;
-                    prefetch_l1(q.rec + 1024 + c * 64 + fo);
-                    prefetch_l1(b2 + c * 64 + fo);
-                    prefetch_l1(b2 + 512 + c * 64 + fo);
-                    if (c < 4) {
-                        prefetch_l1(q.rec + 1536 + c * 64 + fo);
-                        prefetch_l1(b3 + c * 64 + fo);
-                        prefetch_l1(b3 + 256 + c * 64 + fo);
-                    } else if (c == 4) {
-                        prefetch_l1(q.rec + 1792 + cq * (128 / kCQ));
-                        prefetch_l1(b4 + cq * (128 / kCQ));
-                        prefetch_l1(b4 + 128 + cq * (128 / kCQ));
-                    }
-                }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                     const int f0 = (kc + u) * 64 + cq * kFW;

@@ -235,6 +235,11 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst_smem, const void* t
         : "memory");
 }
 
+// bulk prefetch of a contiguous global range into L2 (TMA unit; bytes a multiple of 16)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
