@@ -7,7 +7,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 # kernels whose arithmetic must match the CPU oracle bit-for-bit: no FMA contraction
 EXACT := $(CSRC)/k_analytic.cu $(CSRC)/k_render.cu $(CSRC)/k_depth.cu
-FAST := $(CSRC)/k_tail.cu $(CSRC)/k_grid.cu $(CSRC)/k_simt.cu $(CSRC)/mlp_pack.cu $(CSRC)/k_features.cu $(CSRC)/io_host.cu $(CSRC)/k_mc.cu $(CSRC)/k_mlp_pair.cu $(CSRC)/k_fact2.cu $(CSRC)/icg_host.cu
+FAST := $(CSRC)/k_tail.cu $(CSRC)/k_grid.cu $(CSRC)/k_simt.cu $(CSRC)/mlp_pack.cu $(CSRC)/k_features.cu $(CSRC)/io_host.cu $(CSRC)/k_mc.cu $(CSRC)/k_mlp_pair.cu $(CSRC)/k_fact2.cu $(CSRC)/k_texgemm.cu $(CSRC)/icg_host.cu
 OBJDIR := build/obj
 OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(EXACT) $(FAST))
 HDRS := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh) include/isocull_b200.h

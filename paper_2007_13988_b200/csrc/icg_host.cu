@@ -108,6 +108,17 @@ struct icg_context {
     DBuf geo_pair_f16, geo_pair_f16_hi;  // geometry stream with fp16 skip items (texture kernel prefix)
     alignas(64) unsigned char geo_pair_f16_tmap[2][128] = {};
     bool geo_pair = false, tex_pair = false;
+    // texture field as a per-layer GEMM chain (k_texgemm.cu): fp16 weights [g1 g2 g3 t1 t2 t3 t4],
+    // padded fp32 output layer, per-point activations (capacity tg_cap points)
+    std::vector<float> host_w[2][5];  // fp32 weights of each network as set (the chain packs both)
+    bool host_w_set[2] = {false, false};
+    DBuf tg_w, tg_w5, tg_skip, tg_h1, tg_h2, tg_h3, tg_z, tg_sdot;
+    size_t tg_off[7] = {};
+    unsigned tg_cap = 0;
+    bool tg_ready = false, use_tg = true;  // ICG_TEX_PAIR=1: the fused pair kernel instead
+    alignas(64) unsigned char tg_mapW[7][128] = {};
+    alignas(64) unsigned char tg_mapS[128] = {};
+    alignas(64) unsigned char tg_mapH[3][128] = {};  // h1 (1024 wide), h2 (512), h3 (256)
     // column-factored geometry field (FACT / COLS streams, [part][x3 ? 0 : 1])
     DBuf geo_fact_stream[2][2];
     alignas(64) unsigned char geo_fact_tmap[2][2][128] = {};
@@ -510,6 +521,106 @@ int run_eval(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned ma
     return r;
 }
 
+// The texture chain's weights: packed once both networks are set (icg_set_mlp).
+static int tg_upload(icg_context* c) {
+    c->tg_ready = false;
+    if (!c->host_w_set[0] || !c->host_w_set[1]) return ICG_OK;
+    const float* gw[5];
+    const float* tw[5];
+    for (int l = 0; l < 5; ++l) {
+        gw[l] = c->host_w[0][l].data();
+        tw[l] = c->host_w[1][l].data();
+    }
+    std::vector<__half> w(tg_weight_elems());
+    if (int r = tg_pack_weights(gw, tw, w.data(), c->tg_off)) return r;
+    if (int r = c->tg_w.ensure(w.size() * 2)) return r;
+    ICG_CUDA_TRY(cudaMemcpy(c->tg_w.p, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
+    const int nout[7] = {1024, 512, 256, 1024, 512, 256, 128};
+    const int kin[7] = {256, 1024 + 256, 512 + 256, 512, 1024 + 512, 512 + 512, 256 + 512};
+    for (int l = 0; l < 7; ++l) {
+        const unsigned box = nout[l] >= 256 ? 128u : (unsigned)nout[l] / 2;
+        if (int r = tg_make_tmap(c->tg_w.as<__half>() + c->tg_off[l], (size_t)nout[l], (size_t)kin[l], box, c->tg_mapW[l]))
+            return r;
+    }
+    std::vector<float> w5((size_t)3 * kTgW5Stride, 0.0f);
+    for (int o = 0; o < 3; ++o)
+        for (int k = 0; k < 128 + kTexSkip; ++k) w5[(size_t)o * kTgW5Stride + k] = tw[4][(size_t)o * (128 + kTexSkip) + k];
+    if (int r = c->tg_w5.ensure(w5.size() * 4)) return r;
+    ICG_CUDA_TRY(cudaMemcpy(c->tg_w5.p, w5.data(), w5.size() * 4, cudaMemcpyHostToDevice));
+    c->tg_ready = true;
+    return ICG_OK;
+}
+
+// per-point activations of up to `n` points (+ their TMA descriptors)
+static int tg_ensure(icg_context* c, unsigned n) {
+    if (n <= c->tg_cap) return ICG_OK;
+    const size_t cap = ((size_t)n + 255) / 256 * 256;
+    if (int r = c->tg_skip.ensure(cap * 512 * 2)) return r;
+    if (int r = c->tg_h1.ensure(cap * 1024 * 2)) return r;
+    if (int r = c->tg_h2.ensure(cap * 512 * 2)) return r;
+    if (int r = c->tg_h3.ensure(cap * 256 * 2)) return r;
+    if (int r = c->tg_z.ensure(cap * 4)) return r;
+    if (int r = c->tg_sdot.ensure(cap * 12)) return r;
+    if (int r = tg_make_tmap(c->tg_skip.p, cap, 512, 128, c->tg_mapS)) return r;
+    if (int r = tg_make_tmap(c->tg_h1.p, cap, 1024, 128, c->tg_mapH[0])) return r;
+    if (int r = tg_make_tmap(c->tg_h2.p, cap, 512, 128, c->tg_mapH[1])) return r;
+    if (int r = tg_make_tmap(c->tg_h3.p, cap, 256, 128, c->tg_mapH[2])) return r;
+    c->tg_cap = (unsigned)cap;
+    return ICG_OK;
+}
+
+// Texture field at `job`'s points as gather + 7 layer GEMMs (k_texgemm.cu).  Bias blocks per layer
+// l of the tc epilogue layout: [b (out), w_z (out)] at sum_{i<l} 2 out_i; final biases after.
+static int run_texture_chain(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
+    if (int r = tg_ensure(c, max_points)) return r;
+    __half* skip = c->tg_skip.as<__half>();
+    float* z = c->tg_z.as<float>();
+    float* sdot = c->tg_sdot.as<float>();
+    const float* w5 = c->tg_w5.as<float>();
+    const float* gb = c->geo_tc.bias;
+    const float* tb = c->tex_tc.bias;
+    if (int r = launch_tex_gather(fd, job, max_points, skip, z, sdot, w5, tb + 3840, c->stream)) return r;
+    struct L {
+        int w, hmap, n_out, hid, s1;
+        const float* bias;
+        __half* out;
+        int ldo, out_col, w5_off, fin;
+    };
+    const L ls[7] = {
+        {0, 0, 1024, 0, 4, gb + 0, c->tg_h1.as<__half>(), 1024, 0, -1, 0},
+        {1, 0, 512, 16, 4, gb + 2048, c->tg_h2.as<__half>(), 512, 0, -1, 0},
+        {2, 1, 256, 8, 4, gb + 3072, skip, 512, 256, 128 + 256, 0},  // h3 -> skip columns 256-511
+        {3, 0, 1024, 0, 8, tb + 0, c->tg_h1.as<__half>(), 1024, 0, -1, 0},
+        {4, 0, 512, 16, 8, tb + 2048, c->tg_h2.as<__half>(), 512, 0, -1, 0},
+        {5, 1, 256, 8, 8, tb + 3072, c->tg_h3.as<__half>(), 256, 0, -1, 0},
+        {6, 2, 128, 4, 8, tb + 3584, nullptr, 0, 0, 0, 1},
+    };
+    for (const L& l : ls) {
+        TgLayer t{};
+        t.count = job.count;
+        t.n_static = job.n_static;
+        t.n_out = l.n_out;
+        t.hid_chunks = l.hid;
+        t.skip_c0 = 0;
+        t.skip_c1 = l.s1;
+        t.bias = l.bias;
+        t.z = z;
+        t.slope = 0.02f;
+        t.out = l.out;
+        t.ldo = l.ldo;
+        t.out_col = l.out_col;
+        t.w5 = l.w5_off >= 0 ? w5 : nullptr;
+        t.w5_off = l.w5_off;
+        t.sdot = sdot;
+        t.final_layer = l.fin;
+        t.rgb = job.out;
+        t.out_pixel = job.out_pixel;
+        if (int r = launch_tex_layer(c->tg_mapH[l.hmap], c->tg_mapS, c->tg_mapW[l.w], t, max_points, c->stream)) return r;
+    }
+    c->launches += 7;  // + the gather (counted by the caller)
+    return ICG_OK;
+}
+
 int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned max_points) {
     int slot = prof_begin(c, 1);
     int r;
@@ -517,6 +628,8 @@ int run_texture(icg_context* c, const FieldDev& fd, const EvalJob& job, unsigned
         r = launch_analytic_texture(fd, job, max_points, c->stream);
     else if (fd.precision == ICG_PREC_FP32_SIMT)
         r = launch_pifu_simt_texture(fd, c->geo_simt, c->tex_simt, job, max_points, c->stream);
+    else if (c->tg_ready && c->use_tg)
+        r = run_texture_chain(c, fd, job, max_points);
     else
         // one fp16 copy of every weight and operand, one MMA per K step, at every precision:
         // colours within 5.2e-4 of fp64 (scripts/tex_precision.py; tolerance 1e-3)
@@ -1149,6 +1262,7 @@ int icg_create(int device, icg_context** out) {
     if (const char* e = getenv("ICG_NO_GRAPH")) c->use_graph = !(e[0] == '1');
     if (getenv("ICG_TC_TRACE") || getenv("ICG_TAIL_TRACE")) c->use_graph = false;  // traces synchronise
     if (const char* e = getenv("ICG_FACT2")) c->use_fact2 = e[0] == '1';
+    if (const char* e = getenv("ICG_TEX_PAIR")) c->use_tg = !(e[0] == '1');
     if (const char* e = getenv("ICG_CHAIN_FACT")) c->chain_fact = e[0] == '1';
     if (const char* e = getenv("ICG_CHAIN_FACT_MIN")) c->chain_fact_min = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_NO_XEXT")) c->use_xext = !(e[0] == '1');
@@ -1188,7 +1302,8 @@ int icg_destroy(icg_context* c) {
                    &c->mc_first, &c->mc_slot_bits, &c->mc_slots, &c->mc_tri_list, &c->mc_new_id, &c->mc_out_v,
                    &c->mc_out_t,
                    &c->geo_fact_stream[0][0], &c->geo_fact_stream[0][1], &c->geo_fact_stream[1][0],
-                   &c->geo_fact_stream[1][1]};
+                   &c->geo_fact_stream[1][1], &c->tg_w, &c->tg_w5, &c->tg_skip, &c->tg_h1, &c->tg_h2, &c->tg_h3,
+                   &c->tg_z, &c->tg_sdot};
     for (DBuf* b : all) b->release();
     for (auto& lv : c->lvl_bits)
         for (DBuf& b : lv) b.release();
@@ -1346,6 +1461,12 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
             }
         }
         c->geo_fact = true;
+    }
+    {
+        const int w = geo ? 0 : 1;
+        for (int l = 0; l < 5; ++l) c->host_w[w][l].assign(d->weights[l], d->weights[l] + (size_t)outs[l] * ins[l]);
+        c->host_w_set[w] = true;
+        if (int r = tg_upload(c)) return r;
     }
     if (geo)
         c->has_geo = true;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include <atomic>
@@ -137,6 +138,27 @@ struct TcMlp {
 };
 
 // Where the evaluated points come from and where results go.
+// One layer of the texture-field GEMM chain (k_texgemm.cu): A = `hid_chunks` 64-wide chunks of the
+// hidden input, then skip chunks [skip_c0, skip_c1); fused epilogue acc + b + w_z z, leaky-ReLU.
+constexpr int kTgW5Stride = 644;  // padded row of the fp32 texture output layer [h4 | Phi | h3 | z]
+struct TgLayer {
+    const unsigned* count;
+    unsigned n_static;
+    int n_out;
+    int hid_chunks, skip_c0, skip_c1;
+    const float* bias;  // [b (n_out), w_z (n_out)]
+    const float* z;
+    float slope;
+    __half* out;        // fp16 activations (nullptr: no store)
+    int ldo, out_col;
+    const float* w5;    // output-layer terms of this layer's features (nullptr: none)
+    int w5_off;
+    float* sdot;
+    int final_layer;
+    float* rgb;
+    const uint32_t* out_pixel;
+};
+
 struct EvalJob {
     // source: node list of a level grid, or explicit points
     const uint32_t* list;         // node indices (nullptr with list_count==nullptr: dense 0..n^3-1)
@@ -196,6 +218,15 @@ int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out, unsigne
 constexpr int kColRecord = 1936;  // floats per column record
 size_t pair_fact_stream_bytes(int part, bool x3);
 int pair_pack_factored(const float* const* w, int part, uint8_t* stream_x3, uint8_t* stream_hi);
+// texture-field GEMM chain (k_texgemm.cu)
+int tg_make_tmap(const void* base, size_t rows, size_t cols, unsigned box_rows, void* out);
+size_t tg_weight_elems();
+int tg_pack_weights(const float* const* gw, const float* const* tw, __half* dst, size_t* off);
+int launch_tex_gather(const FieldDev& f, const EvalJob& job, unsigned max_points, __half* skip, float* z, float* sdot,
+                      const float* w5, const float* b5, cudaStream_t s);
+int launch_tex_layer(const void* mapH, const void* mapS, const void* mapW, const TgLayer& L, unsigned max_points,
+                     cudaStream_t s);
+
 int launch_pifu_pair_cols(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& cols, float* records,
                           unsigned max_cols, bool x3, cudaStream_t s);
 // geometry field with 64-point pair tiles (twice the pairs busy on mid-size batches)
