@@ -362,6 +362,10 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
     for ln in lanes:
         for _ in range(max(args.warmup, 1 if args.dry_run else len(ln.dev_maps))):
             ln.frame()
+    # ... and with every lane in flight: a frame that shares its device runs the conflict-loop tail
+    # on fewer SMs, a different frame graph than the frames above (one eager run, then the capture)
+    if S > 1:
+        run_frames(3 * S)
     # ---- single-frame latency: one lane, frames back to back (device time per frame) ----
     lat_lane = lanes[0]
     lat_lane.lat = []

@@ -119,6 +119,7 @@ struct icg_context {
     alignas(64) unsigned char tg_mapW[7][128] = {};
     alignas(64) unsigned char tg_mapS[128] = {};
     alignas(64) unsigned char tg_mapH[3][128] = {};  // h1 (1024 wide), h2 (512), h3 (256)
+    alignas(64) unsigned char tg_mapO[4][128] = {};  // output boxes (64 x 32): h1, h2, h3, skip
     // column-factored geometry field (FACT / COLS streams, [part][x3 ? 0 : 1])
     DBuf geo_fact_stream[2][2];
     alignas(64) unsigned char geo_fact_tmap[2][2][128] = {};
@@ -565,6 +566,10 @@ static int tg_ensure(icg_context* c, unsigned n) {
     if (int r = tg_make_tmap(c->tg_h1.p, cap, 1024, 128, c->tg_mapH[0])) return r;
     if (int r = tg_make_tmap(c->tg_h2.p, cap, 512, 128, c->tg_mapH[1])) return r;
     if (int r = tg_make_tmap(c->tg_h3.p, cap, 256, 128, c->tg_mapH[2])) return r;
+    if (int r = tg_make_tmap(c->tg_h1.p, cap, 1024, 32, c->tg_mapO[0])) return r;
+    if (int r = tg_make_tmap(c->tg_h2.p, cap, 512, 32, c->tg_mapO[1])) return r;
+    if (int r = tg_make_tmap(c->tg_h3.p, cap, 256, 32, c->tg_mapO[2])) return r;
+    if (int r = tg_make_tmap(c->tg_skip.p, cap, 512, 32, c->tg_mapO[3])) return r;
     c->tg_cap = (unsigned)cap;
     return ICG_OK;
 }
@@ -581,19 +586,19 @@ static int run_texture_chain(icg_context* c, const FieldDev& fd, const EvalJob& 
     const float* tb = c->tex_tc.bias;
     if (int r = launch_tex_gather(fd, job, max_points, skip, z, sdot, w5, tb + 3840, c->stream)) return r;
     struct L {
-        int w, hmap, n_out, hid, s1;
+        int w, hmap, omap, n_out, hid, s1;
         const float* bias;
         __half* out;
         int ldo, out_col, w5_off, fin;
     };
     const L ls[7] = {
-        {0, 0, 1024, 0, 4, gb + 0, c->tg_h1.as<__half>(), 1024, 0, -1, 0},
-        {1, 0, 512, 16, 4, gb + 2048, c->tg_h2.as<__half>(), 512, 0, -1, 0},
-        {2, 1, 256, 8, 4, gb + 3072, skip, 512, 256, 128 + 256, 0},  // h3 -> skip columns 256-511
-        {3, 0, 1024, 0, 8, tb + 0, c->tg_h1.as<__half>(), 1024, 0, -1, 0},
-        {4, 0, 512, 16, 8, tb + 2048, c->tg_h2.as<__half>(), 512, 0, -1, 0},
-        {5, 1, 256, 8, 8, tb + 3072, c->tg_h3.as<__half>(), 256, 0, -1, 0},
-        {6, 2, 128, 4, 8, tb + 3584, nullptr, 0, 0, 0, 1},
+        {0, 0, 0, 1024, 0, 4, gb + 0, c->tg_h1.as<__half>(), 1024, 0, -1, 0},
+        {1, 0, 1, 512, 16, 4, gb + 2048, c->tg_h2.as<__half>(), 512, 0, -1, 0},
+        {2, 1, 3, 256, 8, 4, gb + 3072, skip, 512, 256, 128 + 256, 0},  // h3 -> skip columns 256-511
+        {3, 0, 0, 1024, 0, 8, tb + 0, c->tg_h1.as<__half>(), 1024, 0, -1, 0},
+        {4, 0, 1, 512, 16, 8, tb + 2048, c->tg_h2.as<__half>(), 512, 0, -1, 0},
+        {5, 1, 2, 256, 8, 8, tb + 3072, c->tg_h3.as<__half>(), 256, 0, -1, 0},
+        {6, 2, 2, 128, 4, 8, tb + 3584, nullptr, 0, 0, 0, 1},
     };
     for (const L& l : ls) {
         TgLayer t{};
@@ -615,7 +620,9 @@ static int run_texture_chain(icg_context* c, const FieldDev& fd, const EvalJob& 
         t.final_layer = l.fin;
         t.rgb = job.out;
         t.out_pixel = job.out_pixel;
-        if (int r = launch_tex_layer(c->tg_mapH[l.hmap], c->tg_mapS, c->tg_mapW[l.w], t, max_points, c->stream)) return r;
+        if (int r = launch_tex_layer(c->tg_mapH[l.hmap], c->tg_mapS, c->tg_mapW[l.w], c->tg_mapO[l.omap], t, max_points,
+                                     c->stream))
+            return r;
     }
     c->launches += 7;  // + the gather (counted by the caller)
     return ICG_OK;

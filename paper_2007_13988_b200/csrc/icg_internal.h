@@ -224,8 +224,8 @@ size_t tg_weight_elems();
 int tg_pack_weights(const float* const* gw, const float* const* tw, __half* dst, size_t* off);
 int launch_tex_gather(const FieldDev& f, const EvalJob& job, unsigned max_points, __half* skip, float* z, float* sdot,
                       const float* w5, const float* b5, cudaStream_t s);
-int launch_tex_layer(const void* mapH, const void* mapS, const void* mapW, const TgLayer& L, unsigned max_points,
-                     cudaStream_t s);
+int launch_tex_layer(const void* mapH, const void* mapS, const void* mapW, const void* mapO, const TgLayer& L,
+                     unsigned max_points, cudaStream_t s);
 
 int launch_pifu_pair_cols(const FieldDev& f, const TcMlp& geo, const void* tmap, const EvalJob& cols, float* records,
                           unsigned max_cols, bool x3, cudaStream_t s);

@@ -44,19 +44,27 @@ constexpr int kStages = 5;
 constexpr uint32_t kATile = 16384;  // 128 rows x 64 fp16
 constexpr uint32_t kBTile = 16384;  // up to 128 weight rows x 64 fp16
 constexpr uint32_t kStage = kATile + kBTile;
-constexpr int kEpiWarps = 8;
+#ifndef TG_EPI_WARPS
+#define TG_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = TG_EPI_WARPS;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kMaxChunks = 32;
-constexpr uint32_t kSmem = kStages * kStage + 4096 + 1024;
+constexpr int kMaxOut = 1024;
+// stages | Misc | the layer's epilogue constants (b, w_z, and the output-layer rows of its features)
+constexpr uint32_t kMisc = 8192;
+constexpr uint32_t kConsts = (2 * kMaxOut + 3 * 256) * 4;  // 11 KB, keeps 1 KB alignment
+constexpr uint32_t kStaging = 4096;                           // per epilogue warp: 32 rows x 128 B
+constexpr uint32_t kSmem = kStages * kStage + kMisc + kConsts + kEpiWarps * kStaging + 1024;
 constexpr int kW5S = kTgW5Stride;  // padded row stride of the fp32 output-layer weights
 
 struct Misc {
     uint64_t full[kStages], empty[kStages];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem_base;
-    float red[2][128][3];
+    float red[kEpiWarps / 4][128][3];
 };
-static_assert(sizeof(Misc) <= 4096, "misc");
+static_assert(sizeof(Misc) <= kMisc, "misc");
 
 struct Params {
     const unsigned* count;  // points (device counter) or nullptr -> n_static
@@ -87,9 +95,11 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_layer(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapS,
-            const __grid_constant__ CUtensorMap mapW, const __grid_constant__ Params P) {
+            const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapO,
+            const __grid_constant__ Params P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KB-aligned base, kept as smem_raw + offset so the compiler sees shared-space accesses
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     Misc& ms = *reinterpret_cast<Misc*>(smem + kStages * kStage);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_rank();
@@ -110,10 +120,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         ptx::fence_mbar_init();
     }
+    // epilogue constants into shared memory (every epilogue thread reads all of them: broadcast)
+    float* cb = reinterpret_cast<float*>(smem + kStages * kStage + kMisc);  // [b | w_z] of the layer
+    float* cw5 = cb + 2 * kMaxOut;                                         // [3][256] output-layer terms
+    for (int i = threadIdx.x; i < 2 * P.n_out; i += kThreads) cb[i] = __ldg(&P.bias[i]);
+    if (P.w5)
+        for (int i = threadIdx.x; i < 3 * P.n_out && i < 3 * 256; i += kThreads)
+            cw5[i] = __ldg(&P.w5[(i / P.n_out) * kW5S + P.w5_off + i % P.n_out]);
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&mapH);
         ptx::prefetch_tmap(&mapS);
         ptx::prefetch_tmap(&mapW);
+        ptx::prefetch_tmap(&mapO);
     }
     if (warp == 1) ptx::tmem_alloc2<512>(&ms.tmem_base);
     ptx::tc_fence_before();
@@ -184,10 +202,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else {
         // ===================== epilogue: thread = (point row, column half) =====================
-        const int quarter = warp & 3, half = (warp - 2) >> 2;
+        const int quarter = warp & 3, half = (warp - 2) >> 2;  // half: column slice (kEpiWarps / 4 of them)
         const int row = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-        const int cols = bn / 2;  // this thread's features of the tile
+        const int cols = bn / (kEpiWarps / 4);  // this thread's features of the tile
+        // output staging of this warp: 32 rows (its TMEM lanes) x 64 features, 128-byte swizzled,
+        // written to HBM by one TMA store per 64 features (full 128-byte lines)
+        uint8_t* stg = smem + kStages * kStage + kMisc + kConsts + (uint32_t)(warp - 2) * kStaging;
+        const uint32_t stg_s = ptx::smem_u32(stg);
+        bool stg_busy = false;
         uint32_t k = 0;
         for (unsigned t = pair_id; t < ntiles; t += npairs, ++k) {
             const uint32_t a = k & 1u;
@@ -207,8 +230,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const float4 b = __ldg(reinterpret_cast<const float4*>(P.bias + f) + q);
-                    const float4 w = __ldg(reinterpret_cast<const float4*>(P.bias + P.n_out + f) + q);
+                    const float4 b = reinterpret_cast<const float4*>(cb + f)[q];
+                    const float4 w = reinterpret_cast<const float4*>(cb + P.n_out + f)[q];
                     v[4 * q + 0] = fmaf(w.x, z, b.x);
                     v[4 * q + 1] = fmaf(w.y, z, b.y);
                     v[4 * q + 2] = fmaf(w.z, z, b.z);
@@ -218,15 +241,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const float x = __uint_as_float(r[i]) + v[i];
-                    v[i] = x < 0.0f ? x * P.slope : x;
+                    v[i] = fmaxf(x, x * P.slope);  // leaky-ReLU (0 < slope < 1)
                 }
                 if (dot) {
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        const float* wr = P.w5 + c * kW5S + P.w5_off + f;
+                        const float* wr = cw5 + c * P.n_out + f;
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            const float4 w = __ldg(reinterpret_cast<const float4*>(wr) + q);
+                            const float4 w = reinterpret_cast<const float4*>(wr)[q];
                             part[c] = fmaf(w.x, v[4 * q], part[c]);
                             part[c] = fmaf(w.y, v[4 * q + 1], part[c]);
                             part[c] = fmaf(w.z, v[4 * q + 2], part[c]);
@@ -234,12 +257,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
-                if (P.out && valid) {
-                    uint4* o = reinterpret_cast<uint4*>(P.out + (size_t)idx * P.ldo + P.out_col + f);
+                if (P.out) {
+                    if ((g & 63) == 0 && stg_busy) {  // the previous store has read the staging rows
+                        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        __syncwarp();
+                    }
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        o[q] = make_uint4(pack_h2(v[8 * q], v[8 * q + 1]), pack_h2(v[8 * q + 2], v[8 * q + 3]),
-                                          pack_h2(v[8 * q + 4], v[8 * q + 5]), pack_h2(v[8 * q + 6], v[8 * q + 7]));
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t c16 = (uint32_t)(((g & 63) >> 3) + q);
+                        ptx::st_shared_v4(stg_s + (uint32_t)lane * 128u + ((c16 ^ ((uint32_t)lane & 7u)) << 4),
+                                          make_uint4(pack_h2(v[8 * q], v[8 * q + 1]), pack_h2(v[8 * q + 2], v[8 * q + 3]),
+                                                     pack_h2(v[8 * q + 4], v[8 * q + 5]),
+                                                     pack_h2(v[8 * q + 6], v[8 * q + 7])));
+                    }
+                    if ((g & 63) == 32) {
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            const int x = P.out_col + f - 32, y = (int)(idx - (unsigned)lane);
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n\t"
+                                "cp.async.bulk.commit_group;" ::"l"(&mapO),
+                                "r"(x), "r"(y), "r"(stg_s)
+                                : "memory");
+                        }
+                        stg_busy = true;
+                    }
                 }
             }
             ptx::tc_fence_before();
@@ -253,7 +296,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (half == 0 && valid) {
                     float s3[3];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) s3[c] = (ms.red[0][row][c] + ms.red[1][row][c]) + P.sdot[3 * (size_t)idx + c];
+                    for (int c = 0; c < 3; ++c) {
+                        float acc = ms.red[0][row][c];
+                        for (int h = 1; h < kEpiWarps / 4; ++h) acc += ms.red[h][row][c];
+                        s3[c] = acc + P.sdot[3 * (size_t)idx + c];
+                    }
                     if (P.final_layer) {
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
@@ -274,6 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     }
+    if (warp >= 2 && lane == 0 && P.out) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     ptx::tc_fence_before();
     ptx::cluster_sync();
     if (warp == 1) {
@@ -417,8 +465,8 @@ int launch_tex_gather(const FieldDev& f, const EvalJob& job, unsigned max_points
 }
 
 // one layer: A chunks = `hid` chunks of the hidden map, then skip chunks [s0, s1) of the skip map
-int launch_tex_layer(const void* mapH, const void* mapS, const void* mapW, const TgLayer& L, unsigned max_points,
-                     cudaStream_t s) {
+int launch_tex_layer(const void* mapH, const void* mapS, const void* mapW, const void* mapO, const TgLayer& L,
+                     unsigned max_points, cudaStream_t s) {
     static PerDeviceOnce once;
     if (int r = once.run([] {
             ICG_CUDA_TRY(cudaFuncSetAttribute(tg::k_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tg::kSmem));
@@ -459,11 +507,12 @@ int launch_tex_layer(const void* mapH, const void* mapS, const void* mapW, const
     const unsigned tiles = (max_points + 255) / 256 * (unsigned)(L.n_out / p.bn);
     unsigned pairs = tiles < 74 ? tiles : 74;
     if (pairs == 0) pairs = 1;
-    CUtensorMap h, sk, w;
+    CUtensorMap h, sk, w, o;
     std::memcpy(&h, mapH, sizeof(CUtensorMap));
     std::memcpy(&sk, mapS, sizeof(CUtensorMap));
     std::memcpy(&w, mapW, sizeof(CUtensorMap));
-    tg::k_layer<<<2 * pairs, tg::kThreads, tg::kSmem, s>>>(h, sk, w, p);
+    std::memcpy(&o, mapO, sizeof(CUtensorMap));
+    tg::k_layer<<<2 * pairs, tg::kThreads, tg::kSmem, s>>>(h, sk, w, o, p);
     if (const cudaError_t e = cudaGetLastError()) {
         set_error(std::string("k_layer (texture GEMM): ") + cudaGetErrorString(e));
         return ICG_ERUNTIME;
