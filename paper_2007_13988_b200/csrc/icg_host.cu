@@ -116,6 +116,7 @@ struct icg_context {
     size_t tg_off[7] = {};
     unsigned tg_cap = 0;
     bool tg_ready = false, use_tg = true;  // ICG_TEX_PAIR=1: the fused pair kernel instead
+    bool tg_pdl = true;                    // ICG_TG_PDL=0: layers launched without programmatic dependence
     alignas(64) unsigned char tg_mapW[7][128] = {};
     alignas(64) unsigned char tg_mapS[128] = {};
     alignas(64) unsigned char tg_mapH[3][128] = {};  // h1 (1024 wide), h2 (512), h3 (256)
@@ -620,6 +621,7 @@ static int run_texture_chain(icg_context* c, const FieldDev& fd, const EvalJob& 
         t.final_layer = l.fin;
         t.rgb = job.out;
         t.out_pixel = job.out_pixel;
+        t.pdl = c->tg_pdl && &l != &ls[0];  // g1 follows the gather (a plain launch)
         if (int r = launch_tex_layer(c->tg_mapH[l.hmap], c->tg_mapS, c->tg_mapW[l.w], c->tg_mapO[l.omap], t, max_points,
                                      c->stream))
             return r;
@@ -1270,6 +1272,7 @@ int icg_create(int device, icg_context** out) {
     if (getenv("ICG_TC_TRACE") || getenv("ICG_TAIL_TRACE")) c->use_graph = false;  // traces synchronise
     if (const char* e = getenv("ICG_FACT2")) c->use_fact2 = e[0] == '1';
     if (const char* e = getenv("ICG_TEX_PAIR")) c->use_tg = !(e[0] == '1');
+    if (const char* e = getenv("ICG_TG_PDL")) c->tg_pdl = e[0] == '1';
     if (const char* e = getenv("ICG_CHAIN_FACT")) c->chain_fact = e[0] == '1';
     if (const char* e = getenv("ICG_CHAIN_FACT_MIN")) c->chain_fact_min = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_NO_XEXT")) c->use_xext = !(e[0] == '1');

@@ -157,6 +157,7 @@ struct TgLayer {
     int final_layer;
     float* rgb;
     const uint32_t* out_pixel;
+    int pdl;  // launched as a programmatic dependent of the previous layer
 };
 
 struct EvalJob {

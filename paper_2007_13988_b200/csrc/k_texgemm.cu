@@ -137,6 +137,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     ptx::cluster_sync();
     ptx::tc_fence_after();
+    // programmatic dependent launch: everything above overlaps the previous layer's tail; its
+    // outputs (this layer's A operand, z, sdot) are read only after it has completed
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t tmem = ms.tmem_base;
     const uint32_t full0 = ptx::mapa(ptx::smem_u32(&ms.full[0]), 0);
     const uint32_t acc_empty0 = ptx::mapa(ptx::smem_u32(&ms.acc_empty[0]), 0);
@@ -512,7 +516,17 @@ int launch_tex_layer(const void* mapH, const void* mapS, const void* mapW, const
     std::memcpy(&sk, mapS, sizeof(CUtensorMap));
     std::memcpy(&w, mapW, sizeof(CUtensorMap));
     std::memcpy(&o, mapO, sizeof(CUtensorMap));
-    tg::k_layer<<<2 * pairs, tg::kThreads, tg::kSmem, s>>>(h, sk, w, o, p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(tg::kThreads);
+    cfg.dynamicSmemBytes = tg::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = L.pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ICG_CUDA_TRY(cudaLaunchKernelEx(&cfg, tg::k_layer, h, sk, w, o, p));
     if (const cudaError_t e = cudaGetLastError()) {
         set_error(std::string("k_layer (texture GEMM): ") + cudaGetErrorString(e));
         return ICG_ERUNTIME;
