@@ -459,9 +459,9 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
             pass
         line["roofline"] = {
             "bound": "tensor",
-            "kernel": "geometry field, bulk batches (dense level 0 + each level's E0 list): column pass "
-                      "k_mlp_pair<COLS> + factored pass k_fact2 (CTA-pair tcgen05, M = 256 points x N = 256 "
-                      "features), incl. list sorting",
+            "kernel": "geometry field, bulk batches (dense level 0 + each level's E0 list): column gather + "
+                      "column GEMM k_cols (M = 256 columns x N = 256 outputs) + factored pass k_fact2 (CTA-pair "
+                      "tcgen05, M = 256 points x N = 256 features), incl. list sorting",
             "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
             "traffic": traffic, "traffic_note": traffic_note,
             "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: each launch is timed alone by CUDA events)"

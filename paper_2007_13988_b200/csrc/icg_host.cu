@@ -121,6 +121,15 @@ struct icg_context {
     alignas(64) unsigned char tg_mapS[128] = {};
     alignas(64) unsigned char tg_mapH[3][128] = {};  // h1 (1024 wide), h2 (512), h3 (256)
     alignas(64) unsigned char tg_mapO[4][128] = {};  // output boxes (64 x 32): h1, h2, h3, skip
+    // column pass as one GEMM: bf16 Phi rows (hi, lo) of up to cg_cap columns, W_Phi (hi, lo)
+    DBuf cg_ah, cg_al, cg_w;
+    size_t cg_cap = 0;
+    const void* cg_rec = nullptr;  // the records buffer cg_mapR describes (pointer, bytes)
+    size_t cg_rec_n = 0;
+    bool cg_ready = false, use_cg = true;  // ICG_COLS_PAIR=1: k_mlp_pair<COLS> instead
+    alignas(64) unsigned char cg_mapA[2][128] = {};
+    alignas(64) unsigned char cg_mapW[2][128] = {};
+    alignas(64) unsigned char cg_mapR[128] = {};
     // column-factored geometry field (FACT / COLS streams, [part][x3 ? 0 : 1])
     DBuf geo_fact_stream[2][2];
     alignas(64) unsigned char geo_fact_tmap[2][2][128] = {};
@@ -415,6 +424,31 @@ bool fact_ok(const icg_context* c, const FieldDev& fd) {
            c->geo_pair && c->geo_fact && c->use_fact;
 }
 
+// Column records of `cj`'s list window: the column GEMM (k_cols) or the pair kernel.
+static int run_cols(icg_context* c, const FieldDev& fd, const EvalJob& cj, unsigned max_cols, int xi) {
+    if (!(c->cg_ready && c->use_cg))
+        return launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][xi], cj, c->colrec.as<float>(), max_cols,
+                                     xi == 0, c->stream);
+    const size_t n1 = (size_t)cj.cells + 1, plane = n1 * n1;
+    if (plane > c->cg_cap) {
+        const size_t cap = (plane + 255) / 256 * 256;
+        if (int r = c->cg_ah.ensure(cap * 512)) return r;
+        if (int r = c->cg_al.ensure(cap * 512)) return r;
+        if (int r = cg_make_tmap(c->cg_ah.p, cap, 256, 512, 64, 128, false, c->cg_mapA[0])) return r;
+        if (int r = cg_make_tmap(c->cg_al.p, cap, 256, 512, 64, 128, false, c->cg_mapA[1])) return r;
+        c->cg_cap = cap;
+    }
+    if (c->cg_rec != c->colrec.p || c->cg_rec_n != c->colrec.n) {
+        const size_t rows = c->colrec.n / (kColRecord * sizeof(float));
+        if (int r = cg_make_tmap(c->colrec.p, rows, kColRecord, kColRecord * 4, 32, 32, true, c->cg_mapR)) return r;
+        c->cg_rec = c->colrec.p;
+        c->cg_rec_n = c->colrec.n;
+    }
+    return launch_cols_gemm(fd, cj, c->geo_tc.w_last, c->cg_ah.as<__nv_bfloat16>(), c->cg_al.as<__nv_bfloat16>(),
+                            c->colrec.as<float>(), c->cg_mapA[0], c->cg_mapA[1], c->cg_mapW[0], c->cg_mapW[1], c->cg_mapR,
+                            max_cols, xi == 0, c->stream);
+}
+
 // Column-factored evaluation of a grid job (a level's node list, or all nodes of a dense grid):
 // the orthographic projection gives every node of a column (i, j) the same Phi, so the Phi part
 // of every layer is computed once per distinct column (COLS pass, k_mlp_pair.cu) and the per-node
@@ -457,8 +491,7 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
         if (int r = launch_dense_column_list(job.cells, c->sorted.as<uint32_t>(), c->stream)) return r;
         c->launches += 1;
     }
-    if (int r = launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][xi], cj, c->colrec.as<float>(), max_cols,
-                                      xi == 0, c->stream))
+    if (int r = run_cols(c, fd, cj, max_cols, xi))
         return r;
     int r = c->use_fact2
                 ? launch_pifu_fact2(fd, c->geo_tc, c->geo_fact2_tmap[xi], pj, c->colrec.as<float>(), cm, max_points,
@@ -491,8 +524,7 @@ int run_chain_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsig
     cj.count = &ctr->ncols;
     cj.base = &ctr->ncols_base;
     const unsigned max_cols = (unsigned)std::min<size_t>(plane, max_points);
-    if (int r = launch_pifu_pair_cols(fd, c->geo_tc, c->geo_fact_tmap[1][xi], cj, c->colrec.as<float>(), max_cols,
-                                      xi == 0, c->stream))
+    if (int r = run_cols(c, fd, cj, max_cols, xi))
         return r;
     EvalJob pj = job;
     pj.list = c->sorted.as<uint32_t>();
@@ -1273,6 +1305,7 @@ int icg_create(int device, icg_context** out) {
     if (const char* e = getenv("ICG_FACT2")) c->use_fact2 = e[0] == '1';
     if (const char* e = getenv("ICG_TEX_PAIR")) c->use_tg = !(e[0] == '1');
     if (const char* e = getenv("ICG_TG_PDL")) c->tg_pdl = e[0] == '1';
+    if (const char* e = getenv("ICG_COLS_PAIR")) c->use_cg = !(e[0] == '1');
     if (const char* e = getenv("ICG_CHAIN_FACT")) c->chain_fact = e[0] == '1';
     if (const char* e = getenv("ICG_CHAIN_FACT_MIN")) c->chain_fact_min = (unsigned)atoi(e);
     if (const char* e = getenv("ICG_NO_XEXT")) c->use_xext = !(e[0] == '1');
@@ -1313,7 +1346,7 @@ int icg_destroy(icg_context* c) {
                    &c->mc_out_t,
                    &c->geo_fact_stream[0][0], &c->geo_fact_stream[0][1], &c->geo_fact_stream[1][0],
                    &c->geo_fact_stream[1][1], &c->tg_w, &c->tg_w5, &c->tg_skip, &c->tg_h1, &c->tg_h2, &c->tg_h3,
-                   &c->tg_z, &c->tg_sdot};
+                   &c->tg_z, &c->tg_sdot, &c->cg_ah, &c->cg_al, &c->cg_w};
     for (DBuf* b : all) b->release();
     for (auto& lv : c->lvl_bits)
         for (DBuf& b : lv) b.release();
@@ -1477,6 +1510,20 @@ int icg_set_mlp(icg_context* c, const icg_mlp_desc* d) {
         for (int l = 0; l < 5; ++l) c->host_w[w][l].assign(d->weights[l], d->weights[l] + (size_t)outs[l] * ins[l]);
         c->host_w_set[w] = true;
         if (int r = tg_upload(c)) return r;
+    }
+    if (geo) {  // the column GEMM's W_Phi (hi, lo)
+        c->cg_ready = false;
+        const float* ws[5];
+        for (int l = 0; l < 5; ++l) ws[l] = d->weights[l];
+        std::vector<__nv_bfloat16> wh((size_t)2048 * 256), wl((size_t)2048 * 256);
+        if (int r = cg_pack_weights(ws, wh.data(), wl.data())) return r;
+        if (int r = c->cg_w.ensure(wh.size() * 4)) return r;
+        ICG_CUDA_TRY(cudaMemcpy(c->cg_w.p, wh.data(), wh.size() * 2, cudaMemcpyHostToDevice));
+        __nv_bfloat16* lo = c->cg_w.as<__nv_bfloat16>() + wh.size();
+        ICG_CUDA_TRY(cudaMemcpy(lo, wl.data(), wl.size() * 2, cudaMemcpyHostToDevice));
+        if (int r = cg_make_tmap(c->cg_w.p, 2048, 256, 512, 64, 128, false, c->cg_mapW[0])) return r;
+        if (int r = cg_make_tmap(lo, 2048, 256, 512, 64, 128, false, c->cg_mapW[1])) return r;
+        c->cg_ready = true;
     }
     if (geo)
         c->has_geo = true;

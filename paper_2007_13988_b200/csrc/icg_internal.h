@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
 
@@ -219,6 +220,13 @@ int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out, unsigne
 constexpr int kColRecord = 1936;  // floats per column record
 size_t pair_fact_stream_bytes(int part, bool x3);
 int pair_pack_factored(const float* const* w, int part, uint8_t* stream_x3, uint8_t* stream_hi);
+// column pass as one GEMM (k_texgemm.cu, namespace cg)
+int cg_pack_weights(const float* const* w, __nv_bfloat16* hi, __nv_bfloat16* lo);
+int cg_make_tmap(const void* base, size_t rows, size_t cols, size_t row_bytes, unsigned box_cols, unsigned box_rows,
+                 bool f32, void* out);
+int launch_cols_gemm(const FieldDev& f, const EvalJob& cj, const float* wlast, __nv_bfloat16* ah, __nv_bfloat16* al,
+                     float* records, const void* mapAh, const void* mapAl, const void* mapWh, const void* mapWl,
+                     const void* mapR, unsigned max_cols, bool x3, cudaStream_t s);
 // texture-field GEMM chain (k_texgemm.cu)
 int tg_make_tmap(const void* base, size_t rows, size_t cols, unsigned box_rows, void* out);
 size_t tg_weight_elems();

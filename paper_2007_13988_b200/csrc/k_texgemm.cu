@@ -26,6 +26,7 @@
 // (warp - 2) / 4).  Two TMEM accumulators (2 x 256 columns): a tile's epilogue overlaps the next
 // tile's main loop.  Tiles run M-major (consecutive tiles share their A rows in L2).
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
@@ -529,6 +530,374 @@ int launch_tex_layer(const void* mapH, const void* mapS, const void* mapW, const
     ICG_CUDA_TRY(cudaLaunchKernelEx(&cfg, tg::k_layer, h, sk, w, o, p));
     if (const cudaError_t e = cudaGetLastError()) {
         set_error(std::string("k_layer (texture GEMM): ") + cudaGetErrorString(e));
+        return ICG_ERUNTIME;
+    }
+    return ICG_OK;
+}
+
+
+// ============================================================================================
+// Column pass of the column-factored geometry field as one GEMM (replaces k_mlp_pair<COLS>):
+// records[slot] = W_Phi . Phi(column) for the Phi columns of layers 1-4 (1920 outputs), with
+// M = 256 columns x N = 256 outputs per CTA-pair tile, K = the 256 Phi channels, bf16x3 (A and
+// B as bf16 hi + lo, three MMAs per K step: fp32-accurate) or bf16.  The output layer's Phi dot
+// (record column 1920) is an fp32 dot in the gather.  Records are written by TMA bulk stores of
+// 32 x 32 fp32 boxes from per-warp swizzled staging.
+// ============================================================================================
+namespace cg {
+
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr uint32_t kTile = 16384;  // 128 rows x 64 bf16
+constexpr int kNOut = 1920;        // record columns computed by the GEMM (layers 1-4)
+constexpr int kNTiles = 8;         // 2048 weight rows (the last 128 zero)
+constexpr uint32_t kStaging = 4096;  // per epilogue warp: 32 rows x 32 fp32
+template <bool X3>
+struct Cfg {
+    static constexpr int kStages = X3 ? 3 : 5;
+    static constexpr uint32_t kStage = (X3 ? 4 : 2) * kTile;  // A hi (lo), B hi (lo)
+    static constexpr uint32_t kSmem = kStages * kStage + 1024 + kEpiWarps * kStaging + 1024;
+};
+
+struct Misc {
+    uint64_t full[5], empty[5];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem_base;
+};
+
+struct Params {
+    const unsigned* count;  // list entries [*base, *count) (count null: n_static)
+    const unsigned* base;
+    unsigned n_static;
+};
+
+template <bool X3>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_cols(const __grid_constant__ CUtensorMap mapAh, const __grid_constant__ CUtensorMap mapAl,
+           const __grid_constant__ CUtensorMap mapWh, const __grid_constant__ CUtensorMap mapWl,
+           const __grid_constant__ CUtensorMap mapR, const __grid_constant__ Params P) {
+    using C = Cfg<X3>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    Misc& ms = *reinterpret_cast<Misc*>(smem + C::kStages * C::kStage);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_rank();
+    const bool leader = rank == 0;
+    const unsigned pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const unsigned base = P.base ? *P.base : 0u;
+    const unsigned cnt = P.count ? *P.count : P.n_static;
+    const unsigned n = cnt > base ? cnt - base : 0u;
+    const unsigned mt = (n + 255) / 256, ntiles = mt * kNTiles;
+    if (pair_id >= ntiles) return;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            ptx::mbar_init(&ms.full[s], 1);
+            ptx::mbar_init(&ms.empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&ms.acc_full[a], 1);
+            ptx::mbar_init(&ms.acc_empty[a], 2 * kEpiWarps);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&mapAh);
+        ptx::prefetch_tmap(&mapWh);
+        ptx::prefetch_tmap(&mapR);
+        if (X3) {
+            ptx::prefetch_tmap(&mapAl);
+            ptx::prefetch_tmap(&mapWl);
+        }
+    }
+    if (warp == 1) ptx::tmem_alloc2<512>(&ms.tmem_base);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = ms.tmem_base;
+    const uint32_t full0 = ptx::mapa(ptx::smem_u32(&ms.full[0]), 0);
+    const uint32_t acc_empty0 = ptx::mapa(ptx::smem_u32(&ms.acc_empty[0]), 0);
+    const uint16_t both = 0x3;
+
+    if (warp == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t sbase = ptx::smem_u32(smem);
+            for (unsigned t = pair_id; t < ntiles; t += npairs) {
+                const int row0 = (int)((t / kNTiles) * 256 + rank * 128);
+                const int wrow0 = (int)((t % kNTiles) * 256 + rank * 128);
+                for (int j = 0; j < 4; ++j) {
+                    ptx::mbar_wait(&ms.empty[s], ph ^ 1);
+                    if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * C::kStage);
+                    const uint32_t st = sbase + (uint32_t)s * C::kStage;
+                    ptx::tma_load_2d_2sm(st, &mapAh, full0 + s * 8, j * 64, row0);
+                    ptx::tma_load_2d_2sm(st + kTile, &mapWh, full0 + s * 8, j * 64, wrow0);
+                    if (X3) {
+                        ptx::tma_load_2d_2sm(st + 2 * kTile, &mapAl, full0 + s * 8, j * 64, row0);
+                        ptx::tma_load_2d_2sm(st + 3 * kTile, &mapWl, full0 + s * 8, j * 64, wrow0);
+                    }
+                    if (++s == C::kStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader only) =====================
+        if (leader && lane == 0) {
+            const uint32_t idesc = ptx::idesc_bf16_f32(256, 256);
+            const uint32_t sbase = ptx::smem_u32(smem);
+            int s = 0;
+            uint32_t ph = 0, k = 0;
+            for (unsigned t = pair_id; t < ntiles; t += npairs, ++k) {
+                const uint32_t a = k & 1u;
+                if (k >= 2) {
+                    ptx::mbar_wait(&ms.acc_empty[a], ((k >> 1) - 1) & 1u);
+                    ptx::tc_fence_after();
+                }
+                const uint32_t d = tmem + a * 256u;
+                for (int j = 0; j < 4; ++j) {
+                    ptx::mbar_wait(&ms.full[s], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t st = sbase + (uint32_t)s * C::kStage;
+                    const uint64_t ah = ptx::sdesc_sw128(st), bh = ptx::sdesc_sw128(st + kTile);
+                    const uint64_t al = ptx::sdesc_sw128(st + 2 * kTile), bl = ptx::sdesc_sw128(st + 3 * kTile);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t ko = (uint64_t)(kk * 2);
+                        ptx::mma_bf16_pair(d, ah + ko, bh + ko, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+                        if (X3) {
+                            ptx::mma_bf16_pair(d, al + ko, bh + ko, idesc, 1u);
+                            ptx::mma_bf16_pair(d, ah + ko, bl + ko, idesc, 1u);
+                        }
+                    }
+                    ptx::mma_commit_pair(&ms.empty[s], both);
+                    if (++s == C::kStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                ptx::mma_commit_pair(&ms.acc_full[a], both);
+            }
+        }
+    } else {
+        // ===================== epilogue: raw fp32 records through TMA stores =====================
+        const int quarter = warp & 3, half = (warp - 2) >> 2;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        uint8_t* stg = smem + C::kStages * C::kStage + 1024 + (uint32_t)(warp - 2) * kStaging;
+        const uint32_t stg_s = ptx::smem_u32(stg);
+        bool busy = false;
+        uint32_t k = 0;
+        for (unsigned t = pair_id; t < ntiles; t += npairs, ++k) {
+            const uint32_t a = k & 1u;
+            const int y = (int)(base + (t / kNTiles) * 256 + rank * 128 + (unsigned)quarter * 32);
+            const int f_tile = (int)(t % kNTiles) * 256;
+            ptx::mbar_wait(&ms.acc_full[a], (k >> 1) & 1u);
+            ptx::tc_fence_after();
+            for (int g = 0; g < 128; g += 32) {
+                const int fl = half * 128 + g, f = f_tile + fl;
+                uint32_t r[32];
+                ptx::tmem_ld32(lane_base + a * 256u + (uint32_t)fl, r);
+                if (busy) {  // the previous box has been read out of the staging rows
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+                }
+                ptx::tmem_ld_wait();
+                if (f < kNOut) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        ptx::st_shared_v4(stg_s + (uint32_t)lane * 128u + ((((uint32_t)q) ^ ((uint32_t)lane & 7u)) << 4),
+                                          make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]));
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n\t"
+                            "cp.async.bulk.commit_group;" ::"l"(&mapR),
+                            "r"(f), "r"(y), "r"(stg_s)
+                            : "memory");
+                    busy = true;
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_remote(acc_empty0 + 8u * a);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc2<512>(tmem);
+    }
+}
+
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Per column (one warp): Phi at the column's (x, y), bf16 hi (+ lo) rows of the GEMM's A operand,
+// and the output layer's Phi dot (fp32) into the record (same arithmetic as k_mlp_pair<COLS>).
+template <bool X3>
+__global__ void __launch_bounds__(256) k_cols_gather(FieldDev f, EvalJob cj, __nv_bfloat16* ah, __nv_bfloat16* al,
+                                                     float* records, const float* wlast) {
+    const unsigned base = cj.base ? *cj.base : 0u;
+    const unsigned cnt = job_count(cj);
+    const unsigned n = cnt > base ? cnt - base : 0u;
+    const int lane = threadIdx.x & 31;
+    const unsigned warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int c0 = 8 * lane;
+    const size_t rowW = (size_t)f.W * f.C;
+    float w5s[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w5s[i] = __ldg(&wlast[128 + c0 + i]);
+    for (unsigned idx = warp_g; idx < n; idx += nwarps) {
+        double pd[3];
+        node_pos_d(job_node(cj, base + idx), cj.cells, pd);
+        const float pw[3] = {(float)pd[0], (float)pd[1], (float)pd[2]};
+        float q[3];
+        input_coords(f, pw, q);
+        float u = (q[0] + 1.0f) * 0.5f * (float)(f.W - 1);
+        float v = (1.0f - q[1]) * 0.5f * (float)(f.H - 1);
+        u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
+        v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
+        const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
+        const float ax = u - (float)x0, ay = v - (float)y0;
+        const float w00 = (1.0f - ax) * (1.0f - ay), w01 = ax * (1.0f - ay), w10 = (1.0f - ax) * ay, w11 = ax * ay;
+        const float* m00 = f.fmap_hwc + ((size_t)y0 * f.W + x0) * (size_t)f.C + c0;
+        const float* taps[4] = {m00, m00 + f.C, m00 + rowW, m00 + rowW + f.C};
+        float4 tv[8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            tv[2 * t] = __ldg(reinterpret_cast<const float4*>(taps[t]));
+            tv[2 * t + 1] = __ldg(reinterpret_cast<const float4*>(taps[t] + 4));
+        }
+        float val[8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float4 a0 = tv[h], a1 = tv[2 + h], a2 = tv[4 + h], a3 = tv[6 + h];
+            val[4 * h + 0] = w00 * a0.x + w01 * a1.x + w10 * a2.x + w11 * a3.x;
+            val[4 * h + 1] = w00 * a0.y + w01 * a1.y + w10 * a2.y + w11 * a3.y;
+            val[4 * h + 2] = w00 * a0.z + w01 * a1.z + w10 * a2.z + w11 * a3.z;
+            val[4 * h + 3] = w00 * a0.w + w01 * a1.w + w10 * a2.w + w11 * a3.w;
+        }
+        uint32_t hp[4], lp[4];
+        float dot = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float a = val[2 * i], b = val[2 * i + 1];
+            hp[i] = pack_bf2(a, b);
+            lp[i] = pack_bf2(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+            dot = fmaf(w5s[2 * i], a, dot);
+            dot = fmaf(w5s[2 * i + 1], b, dot);
+        }
+        *reinterpret_cast<uint4*>(ah + (size_t)idx * 256 + c0) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+        if (X3) *reinterpret_cast<uint4*>(al + (size_t)idx * 256 + c0) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == 0) records[(size_t)(base + idx) * kColRecord + 1920] = dot;
+    }
+}
+
+}  // namespace cg
+
+// bf16 weights of the column GEMM: rows [layer-1 Phi part (1024) | layer 2 (512) | layer 3 (256) |
+// layer 4 (128) | zero (128)] x the 256 Phi channels, as hi and lo
+int cg_pack_weights(const float* const* w, __nv_bfloat16* hi, __nv_bfloat16* lo) {
+    const int outs[4] = {1024, 512, 256, 128};
+    int row = 0;
+    for (int l = 0; l < 4; ++l) {
+        const int prev = l ? outs[l - 1] : 0, in = prev + kGeoSkip;
+        for (int o = 0; o < outs[l]; ++o, ++row)
+            for (int k = 0; k < 256; ++k) {
+                const float v = w[l][(size_t)o * in + prev + k];
+                const __nv_bfloat16 h = __float2bfloat16_rn(v);
+                hi[(size_t)row * 256 + k] = h;
+                lo[(size_t)row * 256 + k] = __float2bfloat16_rn(v - __bfloat162float(h));
+            }
+    }
+    for (; row < 2048; ++row)
+        for (int k = 0; k < 256; ++k) {
+            hi[(size_t)row * 256 + k] = __float2bfloat16_rn(0.0f);
+            lo[(size_t)row * 256 + k] = __float2bfloat16_rn(0.0f);
+        }
+    return ICG_OK;
+}
+
+// 2D tensor map of `elem`-byte elements, boxes of box_cols x box_rows, 128-byte swizzle
+int cg_make_tmap(const void* base, size_t rows, size_t cols, size_t row_bytes, unsigned box_cols, unsigned box_rows,
+                 bool f32, void* out) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        ICG_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) {
+            set_error("cuTensorMapEncodeTiled not available");
+            return ICG_ERUNTIME;
+        }
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap*>(out),
+                        f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (column GEMM) failed: " + std::to_string((int)r));
+        return ICG_ERUNTIME;
+    }
+    return ICG_OK;
+}
+
+// column records of the list window of `cj` (max_cols entries at most): gather + GEMM
+int launch_cols_gemm(const FieldDev& f, const EvalJob& cj, const float* wlast, __nv_bfloat16* ah, __nv_bfloat16* al,
+                     float* records, const void* mapAh, const void* mapAl, const void* mapWh, const void* mapWl,
+                     const void* mapR, unsigned max_cols, bool x3, cudaStream_t s) {
+    static PerDeviceOnce once;
+    if (int r = once.run([] {
+            ICG_CUDA_TRY(cudaFuncSetAttribute(cg::k_cols<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)cg::Cfg<true>::kSmem));
+            ICG_CUDA_TRY(cudaFuncSetAttribute(cg::k_cols<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)cg::Cfg<false>::kSmem));
+            return ICG_OK;
+        }))
+        return r;
+    unsigned blocks = (max_cols + 7) / 8;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks == 0) blocks = 1;
+    if (x3)
+        cg::k_cols_gather<true><<<blocks, 256, 0, s>>>(f, cj, ah, al, records, wlast);
+    else
+        cg::k_cols_gather<false><<<blocks, 256, 0, s>>>(f, cj, ah, al, records, wlast);
+    ICG_CUDA_TRY(cudaGetLastError());
+    cg::Params p{};
+    p.count = cj.count;
+    p.base = cj.base;
+    p.n_static = cj.n_static;
+    const unsigned tiles = (max_cols + 255) / 256 * cg::kNTiles;
+    unsigned pairs = tiles < 74 ? tiles : 74;
+    if (pairs == 0) pairs = 1;
+    CUtensorMap a0, a1, w0, w1, rr;
+    std::memcpy(&a0, mapAh, sizeof(CUtensorMap));
+    std::memcpy(&a1, mapAl, sizeof(CUtensorMap));
+    std::memcpy(&w0, mapWh, sizeof(CUtensorMap));
+    std::memcpy(&w1, mapWl, sizeof(CUtensorMap));
+    std::memcpy(&rr, mapR, sizeof(CUtensorMap));
+    if (x3)
+        cg::k_cols<true><<<2 * pairs, cg::kThreads, cg::Cfg<true>::kSmem, s>>>(a0, a1, w0, w1, rr, p);
+    else
+        cg::k_cols<false><<<2 * pairs, cg::kThreads, cg::Cfg<false>::kSmem, s>>>(a0, a1, w0, w1, rr, p);
+    if (const cudaError_t e = cudaGetLastError()) {
+        set_error(std::string("k_cols: ") + cudaGetErrorString(e));
         return ICG_ERUNTIME;
     }
     return ICG_OK;
