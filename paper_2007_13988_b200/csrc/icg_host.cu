@@ -136,7 +136,7 @@ struct icg_context {
     alignas(64) unsigned char geo_fact2_tmap[2][128] = {};  // k_fact2: the FACT [x3, hi] streams in 16 KB boxes
     bool geo_fact = false, use_fact = true;
     bool fact_used = false;  // the last extraction ran its bulk batches column-factored
-    DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch;
+    DBuf colrec, cmap, collist, colcnt, sorted, tail_scratch, scan_bsum;
     DBuf xext;  // render: nonzero extent of every grid x-line
     DBuf rtab;  // render: per-column / per-row / per-sample view_to_world terms
     bool use_xext = true;  // ICG_NO_XEXT=1: rays along grid x walk every sample
@@ -461,6 +461,7 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
     if (int r = c->collist.ensure(plane * sizeof(uint32_t))) return r;
     if (int r = c->colcnt.ensure(plane * sizeof(uint32_t))) return r;
     if (int r = c->sorted.ensure(nodes3(job.cells) * sizeof(uint32_t))) return r;
+    if (int r = c->scan_bsum.ensure((plane + 8191) / 8192 * sizeof(unsigned))) return r;
     DevCounters* ctr = c->ctr.as<DevCounters>();
     int slot = prof_begin(c, 4);
     c->fact_used = true;
@@ -477,7 +478,7 @@ int run_eval_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsign
                                      ctr, max_points, c->stream))
             return r;
         if (int r = launch_sort_by_column(job.list, job.count, job.cells, c->cmap.as<int>(), c->colcnt.as<uint32_t>(),
-                                          ctr, c->sorted.as<uint32_t>(), max_points, c->stream))
+                                          ctr, c->sorted.as<uint32_t>(), c->scan_bsum.as<unsigned>(), max_points, c->stream))
             return r;
         cj.list = c->collist.as<uint32_t>();
         cj.count = &ctr->ncols;
@@ -512,11 +513,12 @@ int run_chain_fact(icg_context* c, const FieldDev& fd, const EvalJob& job, unsig
     const int xi = fd.precision == ICG_PREC_FP32 ? 0 : 1;
     const size_t n1 = (size_t)job.cells + 1, plane = n1 * n1;
     DevCounters* ctr = c->ctr.as<DevCounters>();
+    if (int r = c->scan_bsum.ensure((plane + 8191) / 8192 * sizeof(unsigned))) return r;
     if (int r = launch_col_claim(job.list, job.count, job.cells, c->cmap.as<int>(), c->collist.as<uint32_t>(), ctr,
                                  max_points, c->stream, job.min_count))
         return r;
     if (int r = launch_sort_by_column(job.list, job.count, job.cells, c->cmap.as<int>(), c->colcnt.as<uint32_t>(), ctr,
-                                      c->sorted.as<uint32_t>(), max_points, c->stream, job.min_count))
+                                      c->sorted.as<uint32_t>(), c->scan_bsum.as<unsigned>(), max_points, c->stream, job.min_count))
         return r;
     EvalJob cj{};
     cj.cells = job.cells;

@@ -365,8 +365,9 @@ int launch_col_claim(const uint32_t* list, const unsigned* count, int cells, int
                      DevCounters* ctr, unsigned max_points, cudaStream_t s, unsigned min_count = 0);
 // counting sort of a node list by column record (so a point tile spans few columns); cnt holds
 // one u32 per possible column and is cleared here
+// bsum: (plane + 8191) / 8192 scratch words (chunk sums of the slot scan)
 int launch_sort_by_column(const uint32_t* list, const unsigned* count, int cells, const int* cmap, uint32_t* cnt,
-                          DevCounters* ctr, uint32_t* sorted, unsigned max_points, cudaStream_t s,
+                          DevCounters* ctr, uint32_t* sorted, unsigned* bsum, unsigned max_points, cudaStream_t s,
                           unsigned min_count = 0);
 // node list of a dense (cells+1)^3 grid in column order: t -> node (t / n1) + plane * (t % n1)
 int launch_dense_column_list(int cells, uint32_t* list, cudaStream_t s);

@@ -523,65 +523,100 @@ __global__ void k_slot_count(const uint32_t* __restrict__ list, const unsigned* 
         atomicAdd(&cnt[cmap[list[t] % plane]], 1u);
 }
 
-// exclusive scan of cnt[0 .. *ncols) in place (one block; each thread scans 8 consecutive
-// entries of an 8 K pass staged in shared memory with coalesced loads and stores)
-__global__ void __launch_bounds__(1024) k_scan_slots(uint32_t* __restrict__ cnt, const unsigned* __restrict__ ncols) {
-    constexpr int kPer = 8;
-    __shared__ unsigned warp_sums[32];
-    __shared__ unsigned carry;
-    __shared__ unsigned stage[1024 * kPer];  // coalesced loads, scanned per thread from shared memory
-    const unsigned n = *ncols;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
+// exclusive scan of cnt[0 .. *ncols) in place, in chunks of 8 K entries (1024 threads x 8): pass 1
+// sums each chunk, pass 2 rescans it from the sum of the chunks before it (every block adds up the
+// few chunk sums itself).  Both passes skip a batch below its size class (count < min_count).
+constexpr unsigned kScanChunk = 8192;
+
+__device__ __forceinline__ unsigned block_sum_1024(unsigned v, unsigned* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (unsigned base = 0; base < n; base += 1024u * kPer) {
-        const unsigned i0 = base + threadIdx.x * kPer;
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const unsigned i = base + q * 1024u + threadIdx.x;
-            stage[q * 1024 + threadIdx.x] = i < n ? cnt[i] : 0u;
-        }
-        __syncthreads();
-        unsigned v[kPer], sum = 0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    unsigned t = lane < 32 ? red[lane] : 0u;
+    if (warp == 0) {
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            v[q] = stage[threadIdx.x * kPer + q];
-            sum += v[q];
-        }
-        unsigned x = sum;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+__global__ void __launch_bounds__(1024) k_scan_part(const uint32_t* __restrict__ cnt, const unsigned* __restrict__ ncols,
+                                                    const unsigned* __restrict__ count, unsigned min_count,
+                                                    unsigned* __restrict__ bsum) {
+    __shared__ unsigned red[33];
+    if (count && *count < min_count) return;
+    const unsigned n = *ncols, b0 = blockIdx.x * kScanChunk;
+    if (b0 >= n) return;
+    unsigned v = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const unsigned i = b0 + q * 1024u + threadIdx.x;
+        v += i < n ? cnt[i] : 0u;
+    }
+    v = block_sum_1024(v, red);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = v;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_slots(uint32_t* __restrict__ cnt, const unsigned* __restrict__ ncols,
+                                                     const unsigned* __restrict__ count, unsigned min_count,
+                                                     const unsigned* __restrict__ bsum) {
+    constexpr int kPer = 8;
+    __shared__ unsigned warp_sums[33];
+    __shared__ unsigned stage[1024 * kPer];  // coalesced loads, scanned per thread from shared memory
+    if (count && *count < min_count) return;
+    const unsigned n = *ncols, base = blockIdx.x * kScanChunk;
+    if (base >= n) return;
+    // the sum of the chunks before this one
+    unsigned pre = 0;
+    for (unsigned c = threadIdx.x; c < blockIdx.x; c += 1024u) pre += bsum[c];
+    const unsigned carry = block_sum_1024(pre, warp_sums);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const unsigned i = base + q * 1024u + threadIdx.x;
+        stage[q * 1024 + threadIdx.x] = i < n ? cnt[i] : 0u;
+    }
+    __syncthreads();
+    unsigned v[kPer], sum = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        v[q] = stage[threadIdx.x * kPer + q];
+        sum += v[q];
+    }
+    unsigned x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned w = warp_sums[lane];
+        unsigned ws = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const unsigned y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += y;
         }
-        if (lane == 31) warp_sums[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            const unsigned w = warp_sums[lane];
-            unsigned ws = w;
+        warp_sums[lane] = ws - w;
+    }
+    __syncthreads();
+    unsigned run = carry + warp_sums[warp] + x - sum;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(0xffffffffu, ws, o);
-                if (lane >= o) ws += y;
-            }
-            warp_sums[lane] = ws - w;
-        }
-        __syncthreads();
-        unsigned run = carry + warp_sums[warp] + x - sum;
+    for (int q = 0; q < kPer; ++q) {
+        stage[threadIdx.x * kPer + q] = run;
+        run += v[q];
+    }
+    __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            stage[threadIdx.x * kPer + q] = run;
-            run += v[q];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const unsigned i = base + q * 1024u + threadIdx.x;
-            if (i < n) cnt[i] = stage[q * 1024 + threadIdx.x];
-        }
-        (void)i0;
-        if (threadIdx.x == 1023) carry = run;
-        __syncthreads();
+    for (int q = 0; q < kPer; ++q) {
+        const unsigned i = base + q * 1024u + threadIdx.x;
+        if (i < n) cnt[i] = stage[q * 1024 + threadIdx.x];
     }
 }
 
@@ -598,12 +633,15 @@ __global__ void k_slot_scatter(const uint32_t* __restrict__ list, const unsigned
 }
 
 int launch_sort_by_column(const uint32_t* list, const unsigned* count, int cells, const int* cmap, uint32_t* cnt,
-                          DevCounters* ctr, uint32_t* sorted, unsigned max_points, cudaStream_t s, unsigned min_count) {
+                          DevCounters* ctr, uint32_t* sorted, unsigned* bsum, unsigned max_points, cudaStream_t s,
+                          unsigned min_count) {
     const size_t plane = ((size_t)cells + 1) * ((size_t)cells + 1);
     ICG_CUDA_TRY(cudaMemsetAsync(cnt, 0, plane * 4, s));
     const unsigned blocks = std::max(1u, std::min<unsigned>((max_points + 255) / 256, 148u * 8u));
     k_slot_count<<<blocks, 256, 0, s>>>(list, count, cells, cmap, cnt, min_count);
-    k_scan_slots<<<1, 1024, 0, s>>>(cnt, &ctr->ncols);
+    const unsigned chunks = (unsigned)((plane + kScanChunk - 1) / kScanChunk);
+    k_scan_part<<<chunks, 1024, 0, s>>>(cnt, &ctr->ncols, count, min_count, bsum);
+    k_scan_slots<<<chunks, 1024, 0, s>>>(cnt, &ctr->ncols, count, min_count, bsum);
     k_slot_scatter<<<blocks, 256, 0, s>>>(list, count, cells, cmap, cnt, sorted, min_count);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
