@@ -143,7 +143,9 @@ struct icg_context {
     bool use_tail = true;
     bool chain_trace = false;  // ICG_CHAIN_TRACE=1
     bool chain_fact = true;    // large conflict-loop batches column-factored (ICG_CHAIN_FACT=0: CTA-pair GEO)
-    unsigned chain_fact_min = 74u * 128u;  // ... above this many nodes (ICG_CHAIN_FACT_MIN)
+    // ... above this many nodes (ICG_CHAIN_FACT_MIN; 0 = by precision: bf16x3 74 x 64 -- the 128-point
+    // pair class then never runs, 427 vs 411 frames/s at 4 in flight -- bf16 74 x 128)
+    unsigned chain_fact_min = 0;
     bool use_fact2 = true;     // bulk factored pass with swapped operands (k_fact2.cu); ICG_FACT2=0: k_mlp_pair<FACT>
     bool tail_wide = true;  // this frame is alone on its device: the tail kernel takes every SM
     unsigned tail_max = 128;  // conflict batches up to this size start the persistent tail kernel
@@ -838,7 +840,8 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
             const unsigned mid_max = 74u * 64u;
             // batches beyond one wave of 128-point pair tiles: column-factored (k_fact2, 256-point tiles)
             const bool x3c = fd.precision == ICG_PREC_FP32;
-            const unsigned big_max = (c->chain_fact && c->use_fact2) ? c->chain_fact_min : 0u;
+            const unsigned cfm = c->chain_fact_min ? c->chain_fact_min : (x3c ? 74u * 64u : 74u * 128u);
+            const unsigned big_max = (c->chain_fact && c->use_fact2) ? cfm : 0u;
             int prev_mask = -1;
             for (int it = 0; it < unroll; ++it) {
                 int p = it & 1;
