@@ -40,17 +40,22 @@ namespace fact2 {
 
 constexpr uint32_t kHalf = 16384;                   // 128 x 64 bf16 tile
 constexpr uint32_t kStage = 16384;                  // a weight stage: 128 rows x 64 K (hi or lo of an item)
-constexpr int kStages = 5;                          // weight ring (80 KB in flight)
+constexpr int kStagesMax = 5;
 // bf16x3 (X3): chunks of 128 points x 64 K as hi then lo (32 KB), a 4-slot ring (128 KB);
 // bf16: hi only (16 KB), 4 slots (64 KB: the tensor cores drain a bf16 chunk faster than the
 // epilogue fills one, so a deeper ring would idle) -- the freed shared memory goes to L1, which
 // holds the record rows and biases the epilogue streams (its loads are latency-bound)
 // kG: chunks published per proxy fence (each fence stalls its warp until the stores land; the
 // bf16 tensor work per chunk is short, so bf16 publishes 4 at a time into a deeper ring)
+// kWS: weight-ring stages (5 x 16 KB).  The epilogue's bias and z-weight rows sit in shared memory
+// (broadcast loads instead of global ones): bf16 all of layers 1-4 (15 KB, the activation ring
+// one slot shorter), bf16x3 those of layers 2-4 (7 KB: the drains; layer 1 is paced by the MMA)
 template <bool X3>
 struct Prec {
+    static constexpr int kWS = 5;
+    static constexpr bool kBiasL1 = !X3;  // layer-1 rows in shared memory too
     static constexpr uint32_t kAChunk = X3 ? 32768u : 16384u;
-    static constexpr int kA = X3 ? 4 : 8;
+    static constexpr int kA = X3 ? 4 : 7;
     static constexpr uint32_t kARing = kA * kAChunk;
     static constexpr int kStagesPerItem = X3 ? 2 : 1;
     static constexpr int kG = X3 ? 2 : 4;
@@ -70,17 +75,21 @@ constexpr int kSRow = 1936;
 constexpr int kSFinal = 1920;
 constexpr int kItems = 44;                          // FACT stream: L2 (kc, m) 32, L3 8, L4 4
 constexpr uint32_t kOffRing = 0;
-constexpr uint32_t kOffA = kOffRing + kStages * kStage;
-constexpr uint32_t kMisc = 12288;
+constexpr uint32_t kMisc = 11264;
+constexpr int kBiasFloats = 2 * (1024 + 512 + 256 + 128);  // [b, w_z] of layers 1-4
+constexpr int kBiasL1Floats = 2 * 1024;
 template <bool X3>
 struct Layout {
-    static constexpr uint32_t kOffMisc = kOffA + Prec<X3>::kARing;
+    static constexpr int kSBias = Prec<X3>::kBiasL1 ? kBiasFloats : kBiasFloats - kBiasL1Floats;
+    static constexpr uint32_t kOffA = kOffRing + Prec<X3>::kWS * kStage;
+    static constexpr uint32_t kOffBias = kOffA + Prec<X3>::kARing;
+    static constexpr uint32_t kOffMisc = kOffBias + kSBias * 4;
     static constexpr uint32_t kTotal = kOffMisc + kMisc + 1024;
     static_assert(kTotal <= 232448, "shared memory");
 };
 
 struct Misc {
-    uint64_t full[kStages], empty[kStages];
+    uint64_t full[kStagesMax], empty[kStagesMax];
     uint64_t a_ready[kAMax], a_free[kAMax];
     uint64_t d2a, d2done, d3done, d4done, tm_free;  // d2a: D2 columns 0-255 final
     uint32_t tmem_base;
@@ -89,7 +98,6 @@ struct Misc {
     float dmin[2][kCQ][NPC];  // capsule distance, split over the column groups (tile parity)
     float ppos[2][NPC][3];  // the tile's point positions (tile parity)
     int pslot[2][NPC];
-    float sfinal[2][NPC];   // the record's output-layer term (tile parity)
     float red[kCQ][NPC];
 };
 static_assert(sizeof(Misc) <= kMisc, "misc");
@@ -121,10 +129,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_fact2(const __grid_constant__ CUtensorMap tmapW, Params P) {
     constexpr uint32_t kAChunk = Prec<X3>::kAChunk;
     constexpr int kA = Prec<X3>::kA;
+    constexpr int kStages = Prec<X3>::kWS;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KB-aligned base kept as smem_raw + offset (shared-space loads for the bias rows)
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* ring = smem + kOffRing;
-    uint8_t* abuf = smem + kOffA;
+    uint8_t* abuf = smem + Layout<X3>::kOffA;
+    float* sbias = reinterpret_cast<float*>(smem + Layout<X3>::kOffBias);
+    {
+        const float* src = P.bias + (Prec<X3>::kBiasL1 ? 0 : kBiasL1Floats);
+        for (int i = threadIdx.x; i < Layout<X3>::kSBias; i += kThreads) sbias[i] = __ldg(&src[i]);
+    }
     Misc& ms = *reinterpret_cast<Misc*>(smem + Layout<X3>::kOffMisc);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_rank();
@@ -331,11 +346,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t arow = ptx::smem_u32(abuf) + (uint32_t)row * 128u;
         const uint32_t sw = (uint32_t)row & 7u;
         auto epi_bar = [] { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); };
-        const float* b1 = P.bias;
-        const float* b2 = b1 + 2 * 1024;
+        const float* b1 = Prec<X3>::kBiasL1 ? sbias : P.bias;  // [b, w_z] per layer (shared memory, see Prec)
+        const float* b2 = Prec<X3>::kBiasL1 ? sbias + kBiasL1Floats : sbias;
         const float* b3 = b2 + 2 * 512;
         const float* b4 = b3 + 2 * 256;
-        const float* b5 = b4 + 2 * 128;
+        const float* b5 = P.bias + kBiasFloats;
         const float w5z = __ldg(&P.wlast[128 + kGeoSkip - 1]);
         uint32_t ac = 0, d2aph = 0, d2ph = 0, d3ph = 0, d4ph = 0;
         const bool etr = P.trace && blockIdx.x == 0 && et == 0;
@@ -383,6 +398,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
         };
         // kFW consecutive floats at p (16-byte aligned) into v as float4 loads
+        auto loads = [](const float* p, float* v) {  // shared memory (bias rows)
+#pragma unroll
+            for (int q = 0; q < kFW / 4; ++q) {
+                const float4 x = reinterpret_cast<const float4*>(p)[q];
+                v[4 * q + 0] = x.x;
+                v[4 * q + 1] = x.y;
+                v[4 * q + 2] = x.z;
+                v[4 * q + 3] = x.w;
+            }
+        };
         auto loadw = [](const float* p, float* v) {
 #pragma unroll
             for (int q = 0; q < kFW / 4; ++q) {
@@ -467,8 +492,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int f0 = (kc + u) * 64 + cq * kFW;
                     float v[kFW], bb[kFW], wz[kFW];
                     loadw(q.rec + f0, v);
-                    loadw(b1 + f0, bb);
-                    loadw(b1 + 1024 + f0, wz);
+                    loads(b1 + f0, bb);
+                    loads(b1 + 1024 + f0, wz);
 #pragma unroll
                     for (int i = 0; i < kFW; ++i) {
                         const float x = v[i] + fmaf(wz[i], q.z, bb[i]);
@@ -495,8 +520,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::tmem_ld16(lane_base + col0 + (uint32_t)f0, r);
                 float v[kFW], bb[kFW], wz[kFW];
                 loadw(q.rec + soff + f0, v);
-                loadw(bl + f0, bb);
-                loadw(bl + od + f0, wz);
+                loads(bl + f0, bb);
+                loads(bl + od + f0, wz);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < kFW; ++i) {
@@ -523,8 +548,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::tmem_ld16(lane_base + 256u + (uint32_t)f0, r);
                 float v[kFW], bb[kFW], wz[kFW];
                 loadw(q.rec + 1792 + f0, v);
-                loadw(b4 + f0, bb);
-                loadw(b4 + 128 + f0, wz);
+                loads(b4 + f0, bb);
+                loads(b4 + 128 + f0, wz);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < kFW; ++i) {
