@@ -124,6 +124,18 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// FACT stream item consumed at MMA position p.  The stream holds layer 2 as (kc, m) pairs, kc =
+// h1 chunk, m = feature half; the issuer takes the last four chunks' m = 0 items first, so D2
+// columns 0-255 are final four items before the end of layer 2 and h2 chunks 0-3 drain while the
+// m = 1 items run (each into the slot its h1 chunk frees)
+__device__ __forceinline__ int mma_item(int p) {
+    if (p >= 24 && p < 32) {
+        const int q = p - 24;
+        return 2 * (12 + (q & 3)) + (q >> 2);
+    }
+    return p;
+}
+
 template <bool X3>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_fact2(const __grid_constant__ CUtensorMap tmapW, Params P) {
@@ -217,7 +229,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < Prec<X3>::kStagesPerItem * kItems; ++i) {
                     ptx::mbar_wait(&ms.empty[s], ph ^ 1);
                     if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kStage);
-                    const int row0 = ((int)rank * kItems * Prec<X3>::kStagesPerItem + i) * 128;
+                    constexpr int kSPI = Prec<X3>::kStagesPerItem;
+                    const int row0 = (((int)rank * kItems + mma_item(i / kSPI)) * kSPI + i % kSPI) * 128;
                     ptx::tma_load_2d_2sm(ring0 + s * kStage, &tmapW, full0 + s * 8, 0, row0);
                     if (++s == kStages) {
                         s = 0;
@@ -290,11 +303,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // layer 2: 16 h1 chunks x 2 feature halves into D2 (columns 0-511).  Columns 0-255
                 // (the previous tile's D3) are free once its h3 chunks were emitted, so the first
                 // item goes ahead; columns 256-511 (its D4) wait for the output layer to read them.
-                for (int kc = 0; kc < 16; ++kc) {
+                for (int kc = 0; kc < 12; ++kc) {
                     wph = kc == 0 ? 0 : 1;
                     wait_chunk(ac);
                     item(ac, 0, kc == 0);
-                    if (kc == 15) ptx::mma_commit_pair(&ms.d2a, both);  // h2 chunks 0-3 may be drained
                     if (kc == 0 && t != pair_id) {
                         const unsigned long long t0 = tr ? gtime() : 0;
                         ptx::mbar_wait(&ms.tm_free, tfph);
@@ -306,6 +318,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::mma_commit_pair(&ms.a_free[ac % kA], both);
                     ++ac;
                 }
+                // chunks 12-15 (resident together: kA >= 4): their m = 0 items, then their m = 1 items
+                // (mma_item), each chunk's slot freed after its second item
+                for (int q = 0; q < 4; ++q) {
+                    wait_chunk(ac + q);
+                    item(ac + q, 0, false);
+                }
+                ptx::mma_commit_pair(&ms.d2a, both);  // D2 columns 0-255 final: h2 chunks 0-3 may be drained
+                for (int q = 0; q < 4; ++q) {
+                    item(ac + q, 256, false);
+                    ptx::mma_commit_pair(&ms.a_free[(ac + q) % kA], both);
+                }
+                ac += 4;
                 ptx::mma_commit_pair(&ms.d2done, both);
                 // layer 3 into D3 = columns 0-255: its first MMA needs h2 chunks 0-3 (D2 columns
                 // 0-255) read, i.e. all four of them emitted
@@ -507,29 +531,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         };
         // hidden layers 2, 3: drain D (columns col0 + feature) into the next layer's chunks
+        // two chunks per step: both TMEM loads and both record loads in flight before either is used
+        // (the drain is latency-bound: one chunk at a time left the tensor pipe waiting ~1 us per chunk)
         auto drain = [&](const Pt& q, int cbeg, int cend, uint32_t col0, const float* bl, int od, int soff) {
+            static_assert(kFW == 16, "drain: 16 features per thread and chunk");
             for (int c2 = cbeg; c2 < cend; c2 += kG) {
 #pragma unroll 1
-              for (int u = 0; u < kG; ++u) {
-                const int c = c2 + u;
-                const int f0 = c * 64 + cq * kFW;
-                uint32_t r[kFW];
-                if constexpr (kFW == 32)
-                    ptx::tmem_ld32(lane_base + col0 + (uint32_t)f0, r);
-                else
-                    ptx::tmem_ld16(lane_base + col0 + (uint32_t)f0, r);
-                float v[kFW], bb[kFW], wz[kFW];
-                loadw(q.rec + soff + f0, v);
-                loads(bl + f0, bb);
-                loads(bl + od + f0, wz);
+              for (int u = 0; u < kG; u += 2) {
+                const int f0 = (c2 + u) * 64 + cq * kFW, f1 = f0 + 64;
+                uint32_t r0[kFW], r1[kFW];
+                ptx::tmem_ld16(lane_base + col0 + (uint32_t)f0, r0);
+                ptx::tmem_ld16(lane_base + col0 + (uint32_t)f1, r1);
+                float v0[kFW], v1[kFW];
+                loadw(q.rec + soff + f0, v0);
+                loadw(q.rec + soff + f1, v1);
                 ptx::tmem_ld_wait();
+                {
+                    float bb[kFW], wz[kFW];
+                    loads(bl + f0, bb);
+                    loads(bl + od + f0, wz);
 #pragma unroll
-                for (int i = 0; i < kFW; ++i) {
-                    const float x = (__uint_as_float(r[i]) + v[i]) + fmaf(wz[i], q.z, bb[i]);
-                    v[i] = x < 0.0f ? x * P.slope : x;
+                    for (int i = 0; i < kFW; ++i) {
+                        const float x = (__uint_as_float(r0[i]) + v0[i]) + fmaf(wz[i], q.z, bb[i]);
+                        v0[i] = x < 0.0f ? x * P.slope : x;
+                    }
                 }
                 begin_chunk(ac + u);
-                store_chunk(v, ac + u);
+                store_chunk(v0, ac + u);
+                {
+                    float bb[kFW], wz[kFW];
+                    loads(bl + f1, bb);
+                    loads(bl + od + f1, wz);
+#pragma unroll
+                    for (int i = 0; i < kFW; ++i) {
+                        const float x = (__uint_as_float(r1[i]) + v1[i]) + fmaf(wz[i], q.z, bb[i]);
+                        v1[i] = x < 0.0f ? x * P.slope : x;
+                    }
+                }
+                begin_chunk(ac + u + 1);
+                store_chunk(v1, ac + u + 1);
               }
               end_chunks(kG);
             }
