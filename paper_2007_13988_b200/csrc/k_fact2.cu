@@ -125,13 +125,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 
 // FACT stream item consumed at MMA position p.  The stream holds layer 2 as (kc, m) pairs, kc =
-// h1 chunk, m = feature half; the issuer takes the last four chunks' m = 0 items first, so D2
-// columns 0-255 are final four items before the end of layer 2 and h2 chunks 0-3 drain while the
-// m = 1 items run (each into the slot its h1 chunk frees)
+// h1 chunk, m = feature half; the issuer takes the last R chunks' m = 0 items first (R = the
+// activation ring depth: those chunks are resident together), so D2 columns 0-255 are final R
+// items before the end of layer 2 and h2 chunks 0-3 drain while the m = 1 items run
+template <int R>  // R = chunks reordered (the activation ring depth, <= 16)
 __device__ __forceinline__ int mma_item(int p) {
-    if (p >= 24 && p < 32) {
-        const int q = p - 24;
-        return 2 * (12 + (q & 3)) + (q >> 2);
+    if (p >= 32 - 2 * R && p < 32) {
+        const int q = p - (32 - 2 * R);
+        return 2 * (16 - R + q % R) + q / R;
     }
     return p;
 }
@@ -230,7 +231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&ms.empty[s], ph ^ 1);
                     if (leader) ptx::mbar_arrive_expect_tx(&ms.full[s], 2 * kStage);
                     constexpr int kSPI = Prec<X3>::kStagesPerItem;
-                    const int row0 = (((int)rank * kItems + mma_item(i / kSPI)) * kSPI + i % kSPI) * 128;
+                    const int row0 = (((int)rank * kItems + mma_item<Prec<X3>::kA>(i / kSPI)) * kSPI + i % kSPI) * 128;
                     ptx::tma_load_2d_2sm(ring0 + s * kStage, &tmapW, full0 + s * 8, 0, row0);
                     if (++s == kStages) {
                         s = 0;
@@ -303,7 +304,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // layer 2: 16 h1 chunks x 2 feature halves into D2 (columns 0-511).  Columns 0-255
                 // (the previous tile's D3) are free once its h3 chunks were emitted, so the first
                 // item goes ahead; columns 256-511 (its D4) wait for the output layer to read them.
-                for (int kc = 0; kc < 12; ++kc) {
+                constexpr int kR = kA;  // chunks whose feature halves are issued apart (mma_item)
+                for (int kc = 0; kc < 16 - kR; ++kc) {
                     wph = kc == 0 ? 0 : 1;
                     wait_chunk(ac);
                     item(ac, 0, kc == 0);
@@ -318,18 +320,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     ptx::mma_commit_pair(&ms.a_free[ac % kA], both);
                     ++ac;
                 }
-                // chunks 12-15 (resident together: kA >= 4): their m = 0 items, then their m = 1 items
+                // the last kR chunks (resident together): their m = 0 items, then their m = 1 items
                 // (mma_item), each chunk's slot freed after its second item
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kR; ++q) {
                     wait_chunk(ac + q);
                     item(ac + q, 0, false);
                 }
                 ptx::mma_commit_pair(&ms.d2a, both);  // D2 columns 0-255 final: h2 chunks 0-3 may be drained
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kR; ++q) {
                     item(ac + q, 256, false);
                     ptx::mma_commit_pair(&ms.a_free[(ac + q) % kA], both);
                 }
-                ac += 4;
+                ac += kR;
                 ptx::mma_commit_pair(&ms.d2done, both);
                 // layer 3 into D3 = columns 0-255: its first MMA needs h2 chunks 0-3 (D2 columns
                 // 0-255) read, i.e. all four of them emitted
