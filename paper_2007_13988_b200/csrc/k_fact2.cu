@@ -523,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < kFW; ++i) {
                         const float x = v[i] + fmaf(wz[i], q.z, bb[i]);
-                        v[i] = x < 0.0f ? x * P.slope : x;
+                        v[i] = fmaxf(x, x * P.slope);  // leaky-ReLU (0 < slope < 1)
                     }
                     begin_chunk(ac + (kc - kg) + u);
                     store_chunk(v, ac + (kc - kg) + u);
@@ -555,7 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < kFW; ++i) {
                         const float x = (__uint_as_float(r0[i]) + v0[i]) + fmaf(wz[i], q.z, bb[i]);
-                        v0[i] = x < 0.0f ? x * P.slope : x;
+                        v0[i] = fmaxf(x, x * P.slope);
                     }
                 }
                 begin_chunk(ac + u);
@@ -567,7 +567,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < kFW; ++i) {
                         const float x = (__uint_as_float(r1[i]) + v1[i]) + fmaf(wz[i], q.z, bb[i]);
-                        v1[i] = x < 0.0f ? x * P.slope : x;
+                        v1[i] = fmaxf(x, x * P.slope);
                     }
                 }
                 begin_chunk(ac + u + 1);
@@ -596,7 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int i = 0; i < kFW; ++i) {
                     const float x = (__uint_as_float(r[i]) + v[i]) + fmaf(wz[i], q.z, bb[i]);
-                    const float h = x < 0.0f ? x * P.slope : x;
+                    const float h = fmaxf(x, x * P.slope);
                     part = fmaf(__ldg(&P.wlast[f0 + i]), h, part);
                 }
             }
