@@ -41,7 +41,10 @@ namespace icg {
 
 namespace tg {
 
-constexpr int kStages = 5;
+#ifndef TG_STAGES
+#define TG_STAGES 5
+#endif
+constexpr int kStages = TG_STAGES;
 constexpr uint32_t kATile = 16384;  // 128 rows x 64 fp16
 constexpr uint32_t kBTile = 16384;  // up to 128 weight rows x 64 fp16
 constexpr uint32_t kStage = kATile + kBTile;
