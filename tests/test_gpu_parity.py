@@ -686,3 +686,32 @@ def test_on_device_feature_producer(gpu_ctx, pifu_inputs):
     e2, i2 = gpu_ctx.frame(fh, cfg, cam, 64, 64, want_grid=True)
     gpu_ctx.device_free(dp)
     assert np.array_equal(e1.values, e2.values) and np.array_equal(i1.rgb, i2.rgb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("switch", ["ICG_TEX_PAIR", "ICG_COLS_PAIR"])
+def test_alternate_kernels_match_default(pifu_inputs, monkeypatch, switch):
+    """The reference paths kept behind switches -- the fused pair texture kernel (ICG_TEX_PAIR=1)
+    and the pair kernel's column pass (ICG_COLS_PAIR=1) -- against the default texture GEMM chain
+    and column GEMM on a config-2 frame (256^3, 512^2): identical geometry and first crossings,
+    grid values within 1e-5, colours within 1e-3 of each other."""
+    inp = pifu_inputs
+    cfg = api.AlgoConfig("progressive", 32, 3)
+    cam = api.CameraSpec.from_angles(90, 0)
+    out = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv(switch, v)
+        c = api.Context(0)
+        c.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+        c.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+        f = api.PifuField(inp["fmap"], inp["caps"], 50.0, abi.ICG_PREC_FP32)
+        out[v] = c.frame(f, cfg, cam, 512, 512, want_grid=True)
+        c.close()
+    (ea, ia), (eb, ib) = out["0"], out["1"]
+    assert np.array_equal(ea.states, eb.states)
+    assert np.abs(ea.values - eb.values).max() <= 1e-5
+    assert np.array_equal(ia.mask, ib.mask) and np.array_equal(ia.surface_k, ib.surface_k)
+    assert np.array_equal(ia.depth, ib.depth)
+    cov = ia.mask.astype(bool)
+    assert cov.sum() > 1000
+    assert np.abs(ia.rgb[cov] - ib.rgb[cov]).max() <= RGB_TOL
