@@ -1,5 +1,5 @@
 """Summaries of the round-2 ncu outputs for profiles/ (dev tool):
-python scripts/summarize_r02.py gpurun_out profiles"""
+python scripts/summarize_r02.py gpurun_out profiles [tag]"""
 import csv
 import json
 import os
@@ -38,16 +38,17 @@ def full(path, top=3):
     return out
 
 
-def main(src, dst):
+def main(src, dst, tag="r02"):
     for c in ("config2", "config3"):
-        p = os.path.join(src, f"r02_launches_{c}.csv")
+        p = os.path.join(src, f"{tag}_launches_{c}.csv")
         if os.path.exists(p):
-            json.dump(launch_summary(p), open(os.path.join(dst, f"r02_launch_summary_{c}.json"), "w"), indent=1)
-        for k in ("k_fact2", "k_mlp_pair", "k_tail", "k_fine_rows", "k_render", "k_conflict_expand"):
-            p = os.path.join(src, f"r02_raw_{k}_{c}.csv")
+            json.dump(launch_summary(p), open(os.path.join(dst, f"{tag}_launch_summary_{c}.json"), "w"), indent=1)
+        for k in ("k_fact2", "k_mlp_pair", "k_tail", "k_fine_rows", "k_render", "k_conflict_expand", "k_layer",
+                  "k_cols", "k_gather"):
+            p = os.path.join(src, f"{tag}_raw_{k}_{c}.csv")
             if os.path.exists(p):
-                json.dump(full(p), open(os.path.join(dst, f"r02_ncu_full_{k}_{c}.json"), "w"), indent=1)
+                json.dump(full(p), open(os.path.join(dst, f"{tag}_ncu_full_{k}_{c}.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], *(sys.argv[3:4]))
