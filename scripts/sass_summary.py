@@ -7,7 +7,7 @@ import re
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEYS = ["UTCHMMA", "UTCBAR", "UTMALDG", "UBLKCP", "LDTM", "STTM", "UTCATOMSWS", "SYNCS", "MEMBAR", "HMMA", "DFMA",
+KEYS = ["UTCHMMA", "UTCBAR", "UTMALDG", "UTMASTG", "UTMAPF", "UBLKCP", "UBLKPF", "LDTM", "STTM", "UTCATOMSWS", "SYNCS", "MEMBAR", "HMMA", "DFMA",
         "FFMA", "LDG", "STG", "LDS", "STS", "ATOMG", "RED", "SHFL"]
 
 txt = subprocess.run(["cuobjdump", "-sass", os.path.join(ROOT, "paper_2007_13988_b200", "libisocull_b200.so")],
