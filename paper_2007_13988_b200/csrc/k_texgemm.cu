@@ -338,67 +338,98 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
 }
 
-// Per point (one warp): world point -> input coordinates, Phi bilinear in fp32 (lane = 8 channels),
-// fp16 into the skip row [Phi | h3], z, and the output layer's Phi and z terms + b5 (fp32).
+// Bilinear taps of one point: input coordinates -> the four tap rows of the H x W x C map and weights.
+__device__ __forceinline__ void tap_rows(const FieldDev& f, const float* q, const float*& m00, float* w) {
+    float u = (q[0] + 1.0f) * 0.5f * (float)(f.W - 1);
+    float v = (1.0f - q[1]) * 0.5f * (float)(f.H - 1);
+    u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
+    v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
+    const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
+    const float ax = u - (float)x0, ay = v - (float)y0;
+    w[0] = (1.0f - ax) * (1.0f - ay);
+    w[1] = ax * (1.0f - ay);
+    w[2] = (1.0f - ax) * ay;
+    w[3] = ax * ay;
+    m00 = f.fmap_hwc + ((size_t)y0 * f.W + x0) * (size_t)f.C;
+}
+
+// lane L's 8 channels {4L..4L+3, 128+4L..128+4L+3}: every 16-byte load of a warp is one contiguous
+// 512-byte run of a tap row; both points' 16 loads are issued before either is used
+__device__ __forceinline__ void tap_loads(const FieldDev& f, const float* m00, int c0, float4* tv) {
+    const size_t rowW = (size_t)f.W * f.C;
+    const float* taps[4] = {m00, m00 + f.C, m00 + rowW, m00 + rowW + f.C};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        tv[2 * t] = __ldg(reinterpret_cast<const float4*>(taps[t] + c0));
+        tv[2 * t + 1] = __ldg(reinterpret_cast<const float4*>(taps[t] + c0 + 128));
+    }
+}
+
+__device__ __forceinline__ void tap_blend(const float4* tv, const float* w, float* val) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float4 a0 = tv[h], a1 = tv[2 + h], a2 = tv[4 + h], a3 = tv[6 + h];
+        val[4 * h + 0] = w[0] * a0.x + w[1] * a1.x + w[2] * a2.x + w[3] * a3.x;
+        val[4 * h + 1] = w[0] * a0.y + w[1] * a1.y + w[2] * a2.y + w[3] * a3.y;
+        val[4 * h + 2] = w[0] * a0.z + w[1] * a1.z + w[2] * a2.z + w[3] * a3.z;
+        val[4 * h + 3] = w[0] * a0.w + w[1] * a1.w + w[2] * a2.w + w[3] * a3.w;
+    }
+}
+
+// Per point (one warp, two points per step): world point -> input coordinates, Phi bilinear in
+// fp32 (lane = 8 channels), fp16 into the skip row [Phi | h3], z, and the output layer's Phi and z
+// terms + b5 (fp32).
 __global__ void __launch_bounds__(256) k_gather(FieldDev f, EvalJob job, __half* skip, float* zbuf, float* sdot,
                                                 const float* w5, const float* b5) {
     const unsigned n = job_count(job);
     if (blockIdx.x == 0 && threadIdx.x == 0) job_account(job);
     const int lane = threadIdx.x & 31;
     const unsigned warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int c0 = 8 * lane;
-    const size_t rowW = (size_t)f.W * f.C;
+    const int c0 = 4 * lane;
     float w5s[3][8];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) w5s[c][i] = __ldg(&w5[c * kW5S + 128 + c0 + i]);
-    for (unsigned idx = warp_g; idx < n; idx += nwarps) {
-        double pd[3];
-        field_point_d(f, job, idx, pd);
-        const float pw[3] = {(float)pd[0], (float)pd[1], (float)pd[2]};
-        float q[3];
-        input_coords(f, pw, q);
-        float u = (q[0] + 1.0f) * 0.5f * (float)(f.W - 1);
-        float v = (1.0f - q[1]) * 0.5f * (float)(f.H - 1);
-        u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
-        v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
-        const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
-        const float ax = u - (float)x0, ay = v - (float)y0;
-        const float w00 = (1.0f - ax) * (1.0f - ay), w01 = ax * (1.0f - ay), w10 = (1.0f - ax) * ay, w11 = ax * ay;
-        const float* m00 = f.fmap_hwc + ((size_t)y0 * f.W + x0) * (size_t)f.C + c0;
-        const float* taps[4] = {m00, m00 + f.C, m00 + rowW, m00 + rowW + f.C};
-        float4 tv[8];
+        for (int i = 0; i < 8; ++i) w5s[c][i] = __ldg(&w5[c * kW5S + 128 + c0 + (i & 3) + (i >> 2) * 128]);
+    for (unsigned i0 = warp_g; i0 < n; i0 += 2 * nwarps) {
+        unsigned idx[2] = {i0, i0 + nwarps};
+        float q[2][3], w[2][4];
+        float4 tv[2][8];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            tv[2 * t] = __ldg(reinterpret_cast<const float4*>(taps[t]));
-            tv[2 * t + 1] = __ldg(reinterpret_cast<const float4*>(taps[t] + 4));
+        for (int p = 0; p < 2; ++p) {
+            if (idx[p] >= n) continue;
+            double pd[3];
+            field_point_d(f, job, idx[p], pd);
+            const float pw[3] = {(float)pd[0], (float)pd[1], (float)pd[2]};
+            input_coords(f, pw, q[p]);
+            const float* m00;
+            tap_rows(f, q[p], m00, w[p]);
+            tap_loads(f, m00, c0, tv[p]);
         }
-        float val[8];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float4 a0 = tv[h], a1 = tv[2 + h], a2 = tv[4 + h], a3 = tv[6 + h];
-            val[4 * h + 0] = w00 * a0.x + w01 * a1.x + w10 * a2.x + w11 * a3.x;
-            val[4 * h + 1] = w00 * a0.y + w01 * a1.y + w10 * a2.y + w11 * a3.y;
-            val[4 * h + 2] = w00 * a0.z + w01 * a1.z + w10 * a2.z + w11 * a3.z;
-            val[4 * h + 3] = w00 * a0.w + w01 * a1.w + w10 * a2.w + w11 * a3.w;
-        }
-        *reinterpret_cast<uint4*>(skip + (size_t)idx * 512 + c0) =
-            make_uint4(pack_h2(val[0], val[1]), pack_h2(val[2], val[3]), pack_h2(val[4], val[5]), pack_h2(val[6], val[7]));
-        float dot[3];
+        for (int p = 0; p < 2; ++p) {
+            if (idx[p] >= n) continue;
+            float val[8];
+            tap_blend(tv[p], w[p], val);
+            __half* row = skip + (size_t)idx[p] * 512;
+            *reinterpret_cast<uint2*>(row + c0) = make_uint2(pack_h2(val[0], val[1]), pack_h2(val[2], val[3]));
+            *reinterpret_cast<uint2*>(row + 128 + c0) = make_uint2(pack_h2(val[4], val[5]), pack_h2(val[6], val[7]));
+            float dot[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            dot[c] = 0.0f;
+            for (int c = 0; c < 3; ++c) {
+                dot[c] = 0.0f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) dot[c] = fmaf(w5s[c][i], val[i], dot[c]);
+                for (int i = 0; i < 8; ++i) dot[c] = fmaf(w5s[c][i], val[i], dot[c]);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) dot[c] += __shfl_xor_sync(0xffffffffu, dot[c], o);
-        }
-        if (lane == 0) {
-            zbuf[idx] = q[2];
+                for (int o = 16; o > 0; o >>= 1) dot[c] += __shfl_xor_sync(0xffffffffu, dot[c], o);
+            }
+            if (lane == 0) {
+                zbuf[idx[p]] = q[p][2];
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-                sdot[3 * (size_t)idx + c] = dot[c] + fmaf(__ldg(&w5[c * kW5S + 128 + kTexSkip - 1]), q[2], __ldg(&b5[c]));
+                for (int c = 0; c < 3; ++c)
+                    sdot[3 * (size_t)idx[p] + c] =
+                        dot[c] + fmaf(__ldg(&w5[c * kW5S + 128 + kTexSkip - 1]), q[p][2], __ldg(&b5[c]));
+            }
         }
     }
 }
@@ -754,56 +785,53 @@ __global__ void __launch_bounds__(256) k_cols_gather(FieldDev f, EvalJob cj, __n
     const unsigned n = cnt > base ? cnt - base : 0u;
     const int lane = threadIdx.x & 31;
     const unsigned warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int c0 = 8 * lane;
-    const size_t rowW = (size_t)f.W * f.C;
+    const int c0 = 4 * lane;  // channels {c0..c0+3, 128+c0..128+c0+3} (tg::tap_loads)
     float w5s[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) w5s[i] = __ldg(&wlast[128 + c0 + i]);
-    for (unsigned idx = warp_g; idx < n; idx += nwarps) {
-        double pd[3];
-        node_pos_d(job_node(cj, base + idx), cj.cells, pd);
-        const float pw[3] = {(float)pd[0], (float)pd[1], (float)pd[2]};
-        float q[3];
-        input_coords(f, pw, q);
-        float u = (q[0] + 1.0f) * 0.5f * (float)(f.W - 1);
-        float v = (1.0f - q[1]) * 0.5f * (float)(f.H - 1);
-        u = fminf(fmaxf(u, 0.0f), (float)(f.W - 1));
-        v = fminf(fmaxf(v, 0.0f), (float)(f.H - 1));
-        const int x0 = min((int)floorf(u), f.W - 2), y0 = min((int)floorf(v), f.H - 2);
-        const float ax = u - (float)x0, ay = v - (float)y0;
-        const float w00 = (1.0f - ax) * (1.0f - ay), w01 = ax * (1.0f - ay), w10 = (1.0f - ax) * ay, w11 = ax * ay;
-        const float* m00 = f.fmap_hwc + ((size_t)y0 * f.W + x0) * (size_t)f.C + c0;
-        const float* taps[4] = {m00, m00 + f.C, m00 + rowW, m00 + rowW + f.C};
-        float4 tv[8];
+    for (int i = 0; i < 8; ++i) w5s[i] = __ldg(&wlast[128 + c0 + (i & 3) + (i >> 2) * 128]);
+    for (unsigned i0 = warp_g; i0 < n; i0 += 2 * nwarps) {
+        const unsigned idx[2] = {i0, i0 + nwarps};
+        float w[2][4];
+        float4 tv[2][8];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            tv[2 * t] = __ldg(reinterpret_cast<const float4*>(taps[t]));
-            tv[2 * t + 1] = __ldg(reinterpret_cast<const float4*>(taps[t] + 4));
+        for (int p = 0; p < 2; ++p) {
+            if (idx[p] >= n) continue;
+            double pd[3];
+            node_pos_d(job_node(cj, base + idx[p]), cj.cells, pd);
+            const float pw[3] = {(float)pd[0], (float)pd[1], (float)pd[2]};
+            float q[3];
+            input_coords(f, pw, q);
+            const float* m00;
+            tg::tap_rows(f, q, m00, w[p]);
+            tg::tap_loads(f, m00, c0, tv[p]);
         }
-        float val[8];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float4 a0 = tv[h], a1 = tv[2 + h], a2 = tv[4 + h], a3 = tv[6 + h];
-            val[4 * h + 0] = w00 * a0.x + w01 * a1.x + w10 * a2.x + w11 * a3.x;
-            val[4 * h + 1] = w00 * a0.y + w01 * a1.y + w10 * a2.y + w11 * a3.y;
-            val[4 * h + 2] = w00 * a0.z + w01 * a1.z + w10 * a2.z + w11 * a3.z;
-            val[4 * h + 3] = w00 * a0.w + w01 * a1.w + w10 * a2.w + w11 * a3.w;
+        for (int p = 0; p < 2; ++p) {
+            if (idx[p] >= n) continue;
+            float val[8];
+            tg::tap_blend(tv[p], w[p], val);
+            uint32_t hp[4], lp[4];
+            float dot = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float a = val[2 * i], b = val[2 * i + 1];
+                hp[i] = pack_bf2(a, b);
+                lp[i] = pack_bf2(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
+                dot = fmaf(w5s[2 * i], a, dot);
+                dot = fmaf(w5s[2 * i + 1], b, dot);
+            }
+            __nv_bfloat16* rh = ah + (size_t)idx[p] * 256;
+            *reinterpret_cast<uint2*>(rh + c0) = make_uint2(hp[0], hp[1]);
+            *reinterpret_cast<uint2*>(rh + 128 + c0) = make_uint2(hp[2], hp[3]);
+            if (X3) {
+                __nv_bfloat16* rl = al + (size_t)idx[p] * 256;
+                *reinterpret_cast<uint2*>(rl + c0) = make_uint2(lp[0], lp[1]);
+                *reinterpret_cast<uint2*>(rl + 128 + c0) = make_uint2(lp[2], lp[3]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+            if (lane == 0) records[(size_t)(base + idx[p]) * kColRecord + 1920] = dot;
         }
-        uint32_t hp[4], lp[4];
-        float dot = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float a = val[2 * i], b = val[2 * i + 1];
-            hp[i] = pack_bf2(a, b);
-            lp[i] = pack_bf2(a - __uint_as_float(hp[i] << 16), b - __uint_as_float(hp[i] & 0xFFFF0000u));
-            dot = fmaf(w5s[2 * i], a, dot);
-            dot = fmaf(w5s[2 * i + 1], b, dot);
-        }
-        *reinterpret_cast<uint4*>(ah + (size_t)idx * 256 + c0) = make_uint4(hp[0], hp[1], hp[2], hp[3]);
-        if (X3) *reinterpret_cast<uint4*>(al + (size_t)idx * 256 + c0) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        if (lane == 0) records[(size_t)(base + idx) * kColRecord + 1920] = dot;
     }
 }
 

@@ -694,7 +694,7 @@ def test_alternate_kernels_match_default(pifu_inputs, monkeypatch, switch):
     """The reference paths kept behind switches -- the fused pair texture kernel (ICG_TEX_PAIR=1)
     and the pair kernel's column pass (ICG_COLS_PAIR=1) -- against the default texture GEMM chain
     and column GEMM on a config-2 frame (256^3, 512^2): identical geometry and first crossings,
-    grid values within 1e-5, colours within 1e-3 of each other."""
+    grid values within 1e-5 (so bracket depths within 1e-5), colours within 1e-3 of each other."""
     inp = pifu_inputs
     cfg = api.AlgoConfig("progressive", 32, 3)
     cam = api.CameraSpec.from_angles(90, 0)
@@ -711,7 +711,8 @@ def test_alternate_kernels_match_default(pifu_inputs, monkeypatch, switch):
     assert np.array_equal(ea.states, eb.states)
     assert np.abs(ea.values - eb.values).max() <= 1e-5
     assert np.array_equal(ia.mask, ib.mask) and np.array_equal(ia.surface_k, ib.surface_k)
-    assert np.array_equal(ia.depth, ib.depth)
     cov = ia.mask.astype(bool)
+    assert np.array_equal(ia.depth[~cov], ib.depth[~cov])
+    assert np.abs(ia.depth[cov] - ib.depth[cov]).max() <= 1e-5
     assert cov.sum() > 1000
     assert np.abs(ia.rgb[cov] - ib.rgb[cov]).max() <= RGB_TOL
