@@ -57,6 +57,8 @@ struct Prec {
     static constexpr uint32_t kAChunk = X3 ? 32768u : 16384u;
     static constexpr int kA = X3 ? 4 : 7;
     static constexpr uint32_t kARing = kA * kAChunk;
+    // layer 3 reuses D2 columns 0-255: it starts once h2 chunks 0-3 are all in the ring
+    static_assert(kA >= 4 && kA <= 8, "activation ring: 4..8 slots");
     static constexpr int kStagesPerItem = X3 ? 2 : 1;
     static constexpr int kG = X3 ? 2 : 4;
 };
