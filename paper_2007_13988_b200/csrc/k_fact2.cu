@@ -537,11 +537,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // hidden layers 2, 3: drain D (columns col0 + feature) into the next layer's chunks
         // two chunks per step: both TMEM loads and both record loads in flight before either is used
         // (the drain is latency-bound: one chunk at a time left the tensor pipe waiting ~1 us per chunk)
-        auto drain = [&](const Pt& q, int cbeg, int cend, uint32_t col0, const float* bl, int od, int soff) {
+        // g: chunks published per proxy fence (kG; 2 for h3, whose chunks layer 4 takes one by one)
+        auto drain = [&](const Pt& q, int cbeg, int cend, uint32_t col0, const float* bl, int od, int soff, int g) {
             static_assert(kFW == 16, "drain: 16 features per thread and chunk");
-            for (int c2 = cbeg; c2 < cend; c2 += kG) {
+            for (int c2 = cbeg; c2 < cend; c2 += g) {
 #pragma unroll 1
-              for (int u = 0; u < kG; u += 2) {
+              for (int u = 0; u < g; u += 2) {
                 const int f0 = (c2 + u) * 64 + cq * kFW, f1 = f0 + 64;
                 uint32_t r0[kFW], r1[kFW];
                 ptx::tmem_ld16(lane_base + col0 + (uint32_t)f0, r0);
@@ -575,7 +576,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 begin_chunk(ac + u + 1);
                 store_chunk(v1, ac + u + 1);
               }
-              end_chunks(kG);
+              end_chunks(g);
             }
         };
         // layer 4 + output: this thread's 64 of the 128 layer-4 features, dot with w5
@@ -643,12 +644,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (etr) e_prep += gtime() - tq;
             wait_d(&ms.d2a, d2aph);
             tq = etr ? gtime() : 0;
-            drain(cur, 0, 4, 0, b2, 512, 1024);
+            drain(cur, 0, 4, 0, b2, 512, 1024, kG);
             if (etr) e_dr += gtime() - tq;
             wait_d(&ms.d2done, d2ph);
-            drain(cur, 4, 8, 0, b2, 512, 1024);
+            drain(cur, 4, 8, 0, b2, 512, 1024, kG);
             wait_d(&ms.d3done, d3ph);
-            drain(cur, 0, 4, 0, b3, 256, 1536);
+            drain(cur, 0, 4, 0, b3, 256, 1536, 2);
             tq = etr ? gtime() : 0;
             if (has_next) emit_h1(nxt, 0, 4);
             if (etr) e_h1 += gtime() - tq;
