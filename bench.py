@@ -447,14 +447,14 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
         achieved = fact_pts * GEO_FLOP_PER_POINT / fact_s / 1e12 if fact_s > 0 else 0.0
         executed = fact_pts * FACT_MMA_FLOP_PER_POINT * exec_mult / fact_s / 1e12 if fact_s > 0 else 0.0
         traffic, traffic_note = None, None
-        try:  # DRAM bytes of the factored pass's level-3 launch, from the committed ncu --set full capture
-            cap = "r02_ncu_full_fact2_L3.json" if os.path.exists(
-                os.path.join(ROOT, "profiles", "r02_ncu_full_fact2_L3.json")) else "r01e_ncu_full_fact2_L3.json"
+        try:  # DRAM bytes of the longest k_fact2 launch of a frame, from the committed ncu --set full capture
+            cap = f"r02b_ncu_full_k_fact2_{cfg_name}.json"
             rec = json.load(open(os.path.join(ROOT, "profiles", cap)))[0]
             mb = lambda v: float(v.split()[0]) * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}[v.split()[1]]
             traffic = (mb(rec["dram__bytes_read.sum"]) + mb(rec["dram__bytes_write.sum"])) * 1e6
-            traffic_note = (f"dram__bytes_read.sum + dram__bytes_write.sum of one level-3 k_fact2 launch "
-                            f"(profiles/{cap}): weights, column records and lists")
+            traffic_note = (f"dram__bytes_read.sum + dram__bytes_write.sum of the frame's longest k_fact2 launch "
+                            f"(the last level's E0 list, profiles/{cap}): column records (bulk-prefetched into L2), "
+                            f"weights and lists")
         except Exception:
             pass
         line["roofline"] = {
