@@ -540,10 +540,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // g: chunks published per proxy fence (kG; 2 for h3, whose chunks layer 4 takes one by one)
         auto drain = [&](const Pt& q, int cbeg, int cend, uint32_t col0, const float* bl, int od, int soff, int g) {
             static_assert(kFW == 16, "drain: 16 features per thread and chunk");
-            for (int c2 = cbeg; c2 < cend; c2 += g) {
+            int pend = 0;  // chunks stored since the last publish (chunk index = ac + pend)
+            auto one = [&](const uint32_t* r, float* v, int f) {
+                float bb[kFW], wz[kFW];
+                loads(bl + f, bb);
+                loads(bl + od + f, wz);
+#pragma unroll
+                for (int i = 0; i < kFW; ++i) {
+                    const float x = (__uint_as_float(r[i]) + v[i]) + fmaf(wz[i], q.z, bb[i]);
+                    v[i] = fmaxf(x, x * P.slope);
+                }
+                begin_chunk(ac + pend);
+                store_chunk(v, ac + pend);
+                if (++pend == g) {
+                    end_chunks(pend);
+                    pend = 0;
+                }
+            };
 #pragma unroll 1
-              for (int u = 0; u < g; u += 2) {
-                const int f0 = (c2 + u) * 64 + cq * kFW, f1 = f0 + 64;
+            for (int c = cbeg; c < cend; c += 2) {
+                const int f0 = c * 64 + cq * kFW, f1 = f0 + 64;
                 uint32_t r0[kFW], r1[kFW];
                 ptx::tmem_ld16(lane_base + col0 + (uint32_t)f0, r0);
                 ptx::tmem_ld16(lane_base + col0 + (uint32_t)f1, r1);
@@ -551,33 +567,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 loadw(q.rec + soff + f0, v0);
                 loadw(q.rec + soff + f1, v1);
                 ptx::tmem_ld_wait();
-                {
-                    float bb[kFW], wz[kFW];
-                    loads(bl + f0, bb);
-                    loads(bl + od + f0, wz);
-#pragma unroll
-                    for (int i = 0; i < kFW; ++i) {
-                        const float x = (__uint_as_float(r0[i]) + v0[i]) + fmaf(wz[i], q.z, bb[i]);
-                        v0[i] = fmaxf(x, x * P.slope);
-                    }
-                }
-                begin_chunk(ac + u);
-                store_chunk(v0, ac + u);
-                {
-                    float bb[kFW], wz[kFW];
-                    loads(bl + f1, bb);
-                    loads(bl + od + f1, wz);
-#pragma unroll
-                    for (int i = 0; i < kFW; ++i) {
-                        const float x = (__uint_as_float(r1[i]) + v1[i]) + fmaf(wz[i], q.z, bb[i]);
-                        v1[i] = fmaxf(x, x * P.slope);
-                    }
-                }
-                begin_chunk(ac + u + 1);
-                store_chunk(v1, ac + u + 1);
-              }
-              end_chunks(g);
+                one(r0, v0, f0);
+                one(r1, v1, f1);
             }
+            if (pend) end_chunks(pend);
         };
         // layer 4 + output: this thread's 64 of the 128 layer-4 features, dot with w5
         auto final_layer = [&](const Pt& q, int pb) {
@@ -649,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             wait_d(&ms.d2done, d2ph);
             drain(cur, 4, 8, 0, b2, 512, 1024, kG);
             wait_d(&ms.d3done, d3ph);
-            drain(cur, 0, 4, 0, b3, 256, 1536, 2);
+            drain(cur, 0, 4, 0, b3, 256, 1536, 1);  // layer 4 takes h3 chunk by chunk
             tq = etr ? gtime() : 0;
             if (has_next) emit_h1(nxt, 0, 4);
             if (etr) e_h1 += gtime() - tq;
