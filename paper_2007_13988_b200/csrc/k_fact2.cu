@@ -254,6 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const bool tr = P.trace && blockIdx.x == 0;
             unsigned long long w_chunk = 0, w_full = 0, w_tm = 0, t_begin = gtime();
             unsigned long long w_ph[4] = {0, 0, 0, 0};  // chunk waits by phase: h1 first / h1 rest / h2 / h3
+            unsigned long long w_wph[4] = {0, 0, 0, 0};  // weight waits by the same phases
             int wph = 0;
             auto wait_chunk = [&](uint32_t c) {
                 const unsigned long long t0 = tr ? gtime() : 0;
@@ -275,7 +276,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             auto wait_stage = [&]() {
                 const unsigned long long t0 = tr ? gtime() : 0;
                 ptx::mbar_wait(&ms.full[s], ph);
-                if (tr) w_full += gtime() - t0;
+                if (tr) {
+                    w_full += gtime() - t0;
+                    w_wph[wph] += gtime() - t0;
+                }
                 ptx::tc_fence_after();
             };
             // one weight item (4 K steps) against activation chunk c into D columns dcol: the weights'
@@ -362,6 +366,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 P.trace[2] = w_full;
                 P.trace[3] = w_tm;
                 for (int q = 0; q < 4; ++q) P.trace[10 + q] = w_ph[q];
+                for (int q = 0; q < 4; ++q) P.trace[20 + q] = w_wph[q];
             }
         }
     } else {
@@ -722,6 +727,8 @@ int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, con
                 "wait slot %.1f, wait acc %.1f, prep %.1f, h1 %.1f, final %.1f\n",
                 t[0] * 1e-3, t[1] * 1e-3, t[2] * 1e-3, t[3] * 1e-3, t[4] * 1e-3, t[5] * 1e-3, t[6] * 1e-3, t[7] * 1e-3,
                 t[8] * 1e-3, t[9] * 1e-3);
+        fprintf(stderr, "[fact2-trace] weight waits by phase: L2 first %.1f, L2 rest %.1f, L3 %.1f, L4 %.1f us\n",
+                t[20] * 1e-3, t[21] * 1e-3, t[22] * 1e-3, t[23] * 1e-3);
         fprintf(stderr, "[fact2-trace] chunk waits by phase: h1 first %.1f, h1 rest %.1f, h2 %.1f, h3 %.1f us; drain h2 0-3 %.1f\n",
                 t[10] * 1e-3, t[11] * 1e-3, t[12] * 1e-3, t[13] * 1e-3, t[14] * 1e-3);
     }
