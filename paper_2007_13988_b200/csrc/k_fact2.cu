@@ -415,12 +415,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         };
         // publish chunks ac .. ac+cnt-1: ONE proxy fence for all of this thread's stores (the fence
         // waits for them to land, so it is paid per batch, not per chunk)
-        auto end_chunks = [&](int cnt) {
+        auto publish = [&](uint32_t first, int cnt) {
             ptx::fence_proxy_async_smem();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0)
-                for (int i = 0; i < cnt; ++i) ptx::mbar_arrive_remote(a_ready0 + 8u * ((ac + i) % kA));
+                for (int i = 0; i < cnt; ++i) ptx::mbar_arrive_remote(a_ready0 + 8u * ((first + i) % kA));
+        };
+        auto end_chunks = [&](int cnt) {
+            publish(ac, cnt);
             ac += cnt;
         };
         auto wait_d = [&](uint64_t* bar, uint32_t& par) {
@@ -517,27 +520,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // layer 1 (no MMA): chunks [c0, c1) of act(S1 + w1z z + b1)
         // layer 1 in pairs of chunks [c0, c1) (c1 - c0 even)
         constexpr int kG = Prec<X3>::kG;
-        auto emit_h1 = [&](const Pt& q, int c0, int c1) {
-            for (int kg = c0; kg < c1; kg += kG) {
-              for (int kc = kg; kc < kg + kG; kc += 2) {
+        // layer-1 chunk c of point q (act(S1 + w1z z + b1)) into ring slot a
+        auto h1_chunk = [&](const Pt& q, int c, uint32_t a) {
+            const int f0 = c * 64 + cq * kFW;
+            float v[kFW], bb[kFW], wz[kFW];
+            loadw(q.rec + f0, v);
+            loads(b1 + f0, bb);
+            loads(b1 + 1024 + f0, wz);
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int f0 = (kc + u) * 64 + cq * kFW;
-                    float v[kFW], bb[kFW], wz[kFW];
-                    loadw(q.rec + f0, v);
-                    loads(b1 + f0, bb);
-                    loads(b1 + 1024 + f0, wz);
-#pragma unroll
-                    for (int i = 0; i < kFW; ++i) {
-                        const float x = v[i] + fmaf(wz[i], q.z, bb[i]);
-                        v[i] = fmaxf(x, x * P.slope);  // leaky-ReLU (0 < slope < 1)
-                    }
-                    begin_chunk(ac + (kc - kg) + u);
-                    store_chunk(v, ac + (kc - kg) + u);
-                }
-              }
-              end_chunks(kG);
+            for (int i = 0; i < kFW; ++i) {
+                const float x = v[i] + fmaf(wz[i], q.z, bb[i]);
+                v[i] = fmaxf(x, x * P.slope);  // leaky-ReLU (0 < slope < 1)
             }
+            begin_chunk(a);
+            store_chunk(v, a);
+        };
+        // layer 1, chunks [c0, c1) in ring order, published kG at a time
+        auto emit_h1 = [&](const Pt& q, int c0, int c1) {  // (c1 - c0 even)
+            int pend = 0;
+#pragma unroll 1
+            for (int c = c0; c < c1; c += 2) {
+                // two chunks per step, unrolled: both chunks' record loads in flight together
+#pragma unroll
+                for (int u = 0; u < 2; ++u) h1_chunk(q, c + u, ac + pend + u);
+                pend += 2;
+                if (pend == kG) {
+                    end_chunks(pend);
+                    pend = 0;
+                }
+            }
+            if (pend) end_chunks(pend);
+        };
+        // bf16: the next tile's first layer-1 chunks, written `off` ring slots ahead of ac while the
+        // epilogue would otherwise wait for layer 3 (their slots' previous chunks, h2 5-6, are layer-3
+        // operands: freed without the epilogue); published out of ring order, ac not advanced
+        auto emit_h1_ahead = [&](const Pt& q, int c0, int c1, uint32_t off) {
+#pragma unroll 1
+            for (int c = c0; c < c1; ++c) h1_chunk(q, c, ac + off + (uint32_t)(c - c0));
+            publish(ac + off, c1 - c0);
         };
         // hidden layers 2, 3: drain D (columns col0 + feature) into the next layer's chunks
         // two chunks per step: both TMEM loads and both record loads in flight before either is used
@@ -646,10 +666,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (etr) e_dr += gtime() - tq;
             wait_d(&ms.d2done, d2ph);
             drain(cur, 4, 8, 0, b2, 512, 1024, kG);
+            // bf16 (7-slot ring): next tile's h1 chunks 0-1 go to the slots after the 4 h3 chunks
+            constexpr int kAhead = X3 ? 0 : 2;
+            static_assert(X3 || kA >= 4 + kAhead + 1, "ring: h3 chunks + the early h1 chunks + one");
+            if (kAhead && has_next) emit_h1_ahead(nxt, 0, kAhead, 4);
             wait_d(&ms.d3done, d3ph);
             drain(cur, 0, 4, 0, b3, 256, 1536, 1);  // layer 4 takes h3 chunk by chunk
             tq = etr ? gtime() : 0;
-            if (has_next) emit_h1(nxt, 0, 4);
+            if (has_next) {
+                ac += kAhead;  // (already written and published)
+                emit_h1(nxt, kAhead, 4);
+            }
             if (etr) e_h1 += gtime() - tq;
             wait_d(&ms.d4done, d4ph);
             tq = etr ? gtime() : 0;
