@@ -490,6 +490,10 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
                              "peak_gbs": pk.get("hbm_gbs")},
             "render": {"bytes": prof["render_bytes"], "ms": prof["render_ms"],
                        "achieved_gbs": prof["render_bytes"] / max(1e-9, prof["render_ms"] / 1e3) / 1e9},
+            # the texture field's Phi gather: 4 bilinear taps x C x 4 B per surface point (L2-resident map)
+            "texture_gather": {"points": prof.get("gather_points", 0), "bytes": prof.get("gather_bytes", 0),
+                               "ms": prof.get("gather_ms", 0.0),
+                               "achieved_gbs": prof.get("gather_bytes", 0) / max(1e-9, prof.get("gather_ms", 0.0) / 1e3) / 1e9},
             "profiled_frames": prof["frames"], "profiled_frame_ms": prof["frame_ms"] / max(1, prof["frames"]),
             "evals_per_frame": int(prof["geo_points"] / max(1, prof["frames"])),
         }

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ICG_ABI_VERSION 2
+#define ICG_ABI_VERSION 3
 
 /* ---- status codes ------------------------------------------------------ */
 #define ICG_OK 0
@@ -342,6 +342,12 @@ typedef struct icg_profile {
     uint64_t chain_launches;       /* conflict-loop batches (CTA-pair kernels + persistent tail) */
     uint64_t chain_points;
     double chain_ms;
+    /* the texture field's Phi gather (bilinear taps of the H x W x C map at the surface points;
+       part of tex_mlp_ms above): algorithmic bytes = 4 taps x C x 4 B per point (ABI 3) */
+    uint64_t gather_launches;
+    uint64_t gather_points;
+    double gather_ms;
+    uint64_t gather_bytes;
 } icg_profile;
 
 int icg_profile_enable(icg_context* ctx, int on);

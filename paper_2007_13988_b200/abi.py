@@ -24,7 +24,7 @@ ICG_MLP_GEOMETRY, ICG_MLP_TEXTURE = 0, 1
 ICG_MLP_LAYERS = 5
 ICG_VARIANT_BRUTE, ICG_VARIANT_OCTREE_BINARIZED, ICG_VARIANT_OCTREE_THRESHOLD, ICG_VARIANT_PROGRESSIVE = 0, 1, 2, 3
 ICG_SET_EVALUATED_NODES, ICG_SET_REFINED_CELLS = 0, 1
-ICG_ABI_VERSION = 2
+ICG_ABI_VERSION = 3
 
 f32p = C.POINTER(C.c_float)
 u8p = C.POINTER(C.c_uint8)
@@ -165,6 +165,10 @@ class icg_profile(C.Structure):
         ("chain_launches", C.c_uint64),
         ("chain_points", C.c_uint64),
         ("chain_ms", C.c_double),
+        ("gather_launches", C.c_uint64),
+        ("gather_points", C.c_uint64),
+        ("gather_ms", C.c_double),
+        ("gather_bytes", C.c_uint64),
     ]
 
 

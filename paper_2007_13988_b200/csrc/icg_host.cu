@@ -115,6 +115,7 @@ struct icg_context {
     DBuf tg_w, tg_w5, tg_skip, tg_h1, tg_h2, tg_h3, tg_z, tg_sdot;
     size_t tg_off[7] = {};
     unsigned tg_cap = 0;
+    int tg_C = 0;  // channels of the last texture gather (profile bytes)
     bool tg_ready = false, use_tg = true;  // ICG_TEX_PAIR=1: the fused pair kernel instead
     bool tg_pdl = true;                    // ICG_TG_PDL=0: layers launched without programmatic dependence
     alignas(64) unsigned char tg_mapW[7][128] = {};
@@ -256,6 +257,7 @@ void prof_collect(icg_context* c) {
             case 1: c->prof.tex_mlp_ms += ms; c->prof.tex_mlp_launches++; break;
             case 2: c->prof.dense_ms += ms; c->prof.dense_launches++; break;
             case 3: c->prof.render_ms += ms; c->prof.render_launches++; break;
+            case 6: c->prof.gather_ms += ms; c->prof.gather_launches++; break;  // (inside a kind-1 interval)
         }
     }
     prof_discard(c);
@@ -621,7 +623,13 @@ static int run_texture_chain(icg_context* c, const FieldDev& fd, const EvalJob& 
     const float* w5 = c->tg_w5.as<float>();
     const float* gb = c->geo_tc.bias;
     const float* tb = c->tex_tc.bias;
-    if (int r = launch_tex_gather(fd, job, max_points, skip, z, sdot, w5, tb + 3840, c->stream)) return r;
+    c->tg_C = fd.C;
+    {
+        const int gs = prof_begin(c, 6);
+        const int r = launch_tex_gather(fd, job, max_points, skip, z, sdot, w5, tb + 3840, c->stream);
+        prof_end(c, gs);
+        if (r) return r;
+    }
     struct L {
         int w, hmap, omap, n_out, hid, s1;
         const float* bias;
@@ -1204,6 +1212,10 @@ void prof_extract_done(icg_context* c, const icg_algo_config* cfg) {
 void prof_render_done(icg_context* c, int W, int H) {
     if (!c->prof_on) return;
     c->prof.tex_points += c->h_ctr->surface_count;
+    if (c->tg_ready && c->use_tg) {
+        c->prof.gather_points += c->h_ctr->surface_count;
+        c->prof.gather_bytes += 16ull * (uint64_t)c->tg_C * c->h_ctr->surface_count;
+    }
     c->prof.render_bytes += 4 * nodes3(c->last_cells) + 17ull * (uint64_t)W * (uint64_t)H;
 }
 
