@@ -220,6 +220,9 @@ int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out, unsigne
 constexpr int kColRecord = 1936;  // floats per column record
 size_t pair_fact_stream_bytes(int part, bool x3);
 int pair_pack_factored(const float* const* w, int part, uint8_t* stream_x3, uint8_t* stream_hi);
+// 2D tiled tensor map (k_texgemm.cu): dtype = CUtensorMapDataType, swizzle = CUtensorMapSwizzle
+int make_tmap_2d(const void* base, int dtype, size_t rows, size_t cols, size_t row_bytes, unsigned box_cols,
+                 unsigned box_rows, int swizzle, void* out);
 // column pass as one GEMM (k_texgemm.cu, namespace cg)
 int cg_pack_weights(const float* const* w, __nv_bfloat16* hi, __nv_bfloat16* lo);
 int cg_make_tmap(const void* base, size_t rows, size_t cols, size_t row_bytes, unsigned box_cols, unsigned box_rows,

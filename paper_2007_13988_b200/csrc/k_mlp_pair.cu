@@ -1564,30 +1564,9 @@ int pair_pack_factored(const float* const* w, int part, uint8_t* stream_x3, uint
 }
 
 int pair_make_tmap(const void* dev_stream, size_t bytes, void* tmap_out /* 128-byte CUtensorMap */, unsigned box_rows) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q;
-        void* fn = nullptr;
-        ICG_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) {
-            set_error("cuTensorMapEncodeTiled not available");
-            return ICG_ERUNTIME;
-        }
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    cuuint64_t dims[2] = {128, (cuuint64_t)(bytes / 128)};
-    cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {128, box_rows};  // one stage: 256 rows = 32 KB (hi + lo of an item)
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
-                        const_cast<void*>(dev_stream), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-        return ICG_ERUNTIME;
-    }
-    return ICG_OK;
+    // the pre-swizzled stream as bytes: rows of 128 B, one stage = box_rows rows
+    return make_tmap_2d(dev_stream, CU_TENSOR_MAP_DATA_TYPE_UINT8, bytes / 128, 128, 128, 128, box_rows,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, tmap_out);
 }
 
 template <int MODE>

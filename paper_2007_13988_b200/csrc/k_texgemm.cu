@@ -32,6 +32,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "eval_common.cuh"
@@ -436,31 +437,41 @@ __global__ void __launch_bounds__(256) k_gather(FieldDev f, EvalJob job, __half*
 
 }  // namespace tg
 
-// fp16 row-major [rows][cols] tensor map, boxes of 64 columns x box_rows rows, 128-byte swizzle
-int tg_make_tmap(const void* base, size_t rows, size_t cols, unsigned box_rows, void* out) {
+// 2D tiled tensor map (one encoder for every TMA descriptor of the library): element type `dtype`
+// (CUtensorMapDataType), row pitch row_bytes, boxes of box_cols x box_rows, swizzle (CUtensorMapSwizzle)
+int make_tmap_2d(const void* base, int dtype, size_t rows, size_t cols, size_t row_bytes, unsigned box_cols,
+                 unsigned box_rows, int swizzle, void* out) {
+    static std::once_flag once;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
+    std::call_once(once, [] {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
-        ICG_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) {
-            set_error("cuTensorMapEncodeTiled not available");
-            return ICG_ERUNTIME;
-        }
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    if (!encode) {
+        set_error("cuTensorMapEncodeTiled not available");
+        return ICG_ERUNTIME;
     }
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-    cuuint32_t box[2] = {64, box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+    cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base),
-                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    CUresult r = encode(reinterpret_cast<CUtensorMap*>(out), (CUtensorMapDataType)dtype, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, (CUtensorMapSwizzle)swizzle,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled (texture GEMM) failed: " + std::to_string((int)r));
+        set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
         return ICG_ERUNTIME;
     }
     return ICG_OK;
+}
+
+// fp16 row-major [rows][cols] tensor map, boxes of 64 columns x box_rows rows, 128-byte swizzle
+int tg_make_tmap(const void* base, size_t rows, size_t cols, unsigned box_rows, void* out) {
+    return make_tmap_2d(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, cols, cols * 2, 64, box_rows,
+                        CU_TENSOR_MAP_SWIZZLE_128B, out);
 }
 
 // fp16 weights of the texture chain, row-major [n_out][K] with K ordered like the layer's A chunks:
@@ -860,33 +871,11 @@ int cg_pack_weights(const float* const* w, __nv_bfloat16* hi, __nv_bfloat16* lo)
     return ICG_OK;
 }
 
-// 2D tensor map of `elem`-byte elements, boxes of box_cols x box_rows, 128-byte swizzle
+// bf16 (or fp32) row-major tensor map, boxes of box_cols x box_rows, 128-byte swizzle
 int cg_make_tmap(const void* base, size_t rows, size_t cols, size_t row_bytes, unsigned box_cols, unsigned box_rows,
                  bool f32, void* out) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q;
-        void* fn = nullptr;
-        ICG_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) {
-            set_error("cuTensorMapEncodeTiled not available");
-            return ICG_ERUNTIME;
-        }
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
-    cuuint32_t box[2] = {box_cols, box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(reinterpret_cast<CUtensorMap*>(out),
-                        f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled (column GEMM) failed: " + std::to_string((int)r));
-        return ICG_ERUNTIME;
-    }
-    return ICG_OK;
+    return make_tmap_2d(base, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rows, cols,
+                        row_bytes, box_cols, box_rows, CU_TENSOR_MAP_SWIZZLE_128B, out);
 }
 
 // column records of the list window of `cj` (max_cols entries at most): gather + GEMM
