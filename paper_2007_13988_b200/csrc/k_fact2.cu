@@ -729,14 +729,14 @@ int launch_pifu_fact2(const FieldDev& f, const TcMlp& geo, const void* tmap, con
     if (pairs == 0) pairs = 1;
     CUtensorMap tm;
     std::memcpy(&tm, tmap, sizeof(CUtensorMap));
-    static unsigned long long* trace = nullptr;
-    static int tron = -1;
-    if (tron < 0) {
+    // dev trace buffer (ICG_TC_TRACE=1), created once (thread-safe static initialisation)
+    static unsigned long long* const trace = [] {
         const char* e = getenv("ICG_TC_TRACE");
-        tron = e && e[0] == '1';
-        if (tron) cudaMallocManaged(&trace, 64 * sizeof(unsigned long long));
-    }
-    p.trace = tron ? trace : nullptr;
+        unsigned long long* t = nullptr;
+        if (e && e[0] == '1' && cudaMallocManaged(&t, 64 * sizeof(unsigned long long)) != cudaSuccess) t = nullptr;
+        return t;
+    }();
+    p.trace = trace;
     if (p.trace) cudaMemsetAsync(p.trace, 0, 64 * 8, s);
     if (x3)
         fact2::k_fact2<true><<<2 * pairs, fact2::kThreads, fact2::Layout<true>::kTotal, s>>>(tm, p);

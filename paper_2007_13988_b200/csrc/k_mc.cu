@@ -312,8 +312,7 @@ int mc_init_tables() {
     static PerDeviceOnce once;
     return once.run([] {
         static mc::Tables host;
-        static int built = -1;
-        if (built < 0) built = mc::build_tables(host);
+        static const int built = mc::build_tables(host);  // once per process (thread-safe)
         if (built != ICG_OK) {
             set_error("marching cubes: triangulation table generation failed");
             return ICG_ERUNTIME;

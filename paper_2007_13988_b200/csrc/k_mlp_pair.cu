@@ -1580,14 +1580,14 @@ static int launch_pair(pair::Params p, const void* tmapA, const void* tmapB, uns
             return ICG_OK;
         }))
         return r;
-    static unsigned long long* trace = nullptr;
-    static int tron = -1;
-    if (tron < 0) {
+    // dev trace buffer (ICG_TC_TRACE=1), created once (thread-safe static initialisation)
+    static unsigned long long* const trace = [] {
         const char* e = getenv("ICG_TC_TRACE");
-        tron = e && e[0] == '1';
-        if (tron) cudaMallocManaged(&trace, 2048 * sizeof(unsigned long long));
-    }
-    p.trace = tron ? trace : nullptr;
+        unsigned long long* t = nullptr;
+        if (e && e[0] == '1' && cudaMallocManaged(&t, 2048 * sizeof(unsigned long long)) != cudaSuccess) t = nullptr;
+        return t;
+    }();
+    p.trace = trace;
     if (p.trace) cudaMemsetAsync(p.trace, 0, 2048 * 8, s);
     unsigned pairs = (max_points + C::NP - 1) / C::NP;
     if (pairs > 74) pairs = 74;

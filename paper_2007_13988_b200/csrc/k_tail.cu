@@ -484,14 +484,14 @@ int launch_tail(TailParams p, uint8_t* scratch, unsigned cap_pts, unsigned cap_n
     p.nnew = reinterpret_cast<unsigned*>(q);
     p.cap_pts = cap_pts;
     p.cap_new = cap_new;
-    static unsigned long long* trace = nullptr;
-    static int tron = -1;
-    if (tron < 0) {
+    // dev trace buffer (ICG_TAIL_TRACE=1), created once (thread-safe static initialisation)
+    static unsigned long long* const trace = [] {
         const char* e = getenv("ICG_TAIL_TRACE");
-        tron = e && e[0] == '1';
-        if (tron) cudaMallocManaged(&trace, 2000 * sizeof(unsigned long long));
-    }
-    p.trace = tron ? trace : nullptr;
+        unsigned long long* t = nullptr;
+        if (e && e[0] == '1' && cudaMallocManaged(&t, 2000 * sizeof(unsigned long long)) != cudaSuccess) t = nullptr;
+        return t;
+    }();
+    p.trace = trace;
     if (p.trace) cudaMemsetAsync(p.trace, 0, 2000 * 8, s);
     void* args[] = {&p};
     if (wide)
