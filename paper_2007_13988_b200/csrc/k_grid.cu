@@ -466,11 +466,18 @@ __global__ void k_conflict_expand(uint32_t* __restrict__ queued, const uint8_t* 
     }
 }
 
+#ifndef EXPAND_BLOCKS
+#define EXPAND_BLOCKS (148 * 8)
+#endif
+// 8 blocks per SM: a thread's (conflict, neighbour) chain is a few dependent random accesses, so
+// the big expansions (tens of thousands of conflicts) want many of them in flight
+constexpr unsigned kExpandBlocks = EXPAND_BLOCKS;
+
 int launch_conflict_expand(uint32_t* queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
                            DevCounters* ctr, int iter, int max_iters, uint32_t* next_list, unsigned cap,
                            cudaStream_t s) {
     ChainClasses cc{0, 0, 0, -1};
-    k_conflict_expand<<<148, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap, cc);
+    k_conflict_expand<<<kExpandBlocks, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap, cc);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }
@@ -478,7 +485,7 @@ int launch_conflict_expand(uint32_t* queued, const uint8_t* fs, int fcells, cons
 int launch_conflict_expand_cls(uint32_t* queued, const uint8_t* fs, int fcells, const uint32_t* conflicts,
                                DevCounters* ctr, int iter, int max_iters, uint32_t* next_list, unsigned cap,
                                const ChainClasses& cc, cudaStream_t s) {
-    k_conflict_expand<<<148, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap, cc);
+    k_conflict_expand<<<kExpandBlocks, 256, 0, s>>>(queued, fs, fcells, conflicts, ctr, iter, max_iters, next_list, cap, cc);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }
