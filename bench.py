@@ -30,6 +30,7 @@ import socket
 import statistics
 import subprocess
 import sys
+import itertools
 import threading
 import time
 
@@ -339,7 +340,7 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
         return shard.allmax(x, device=dev)
 
     def run_frames(nframes: int, **kw) -> float:
-        """nframes frames round-robin over the lanes (one host thread per lane); returns the
+        """nframes frames over the lanes (one host thread per lane, dynamic hand-out); returns the
         device-timed span in ms (CUDA events: common start event, last stream's end event)."""
         counts = [nframes // S + (1 if i < nframes % S else 0) for i in range(S)]
         if args.dry_run:
@@ -349,9 +350,16 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
                     ln.frame(**kw)
             return 1e3 * (time.perf_counter() - t0)
         from paper_2007_13988_b200 import api as _api
+        # frames are handed out dynamically (the next frame goes to the first lane that is free), so no
+        # lane idles at the end of the span while another still has a queue
+        ticket = itertools.count()
+
+        def lane_loop(ln):
+            while next(ticket) < nframes:
+                ln.frame(**kw)
+
         _api.span_begin(ctxs)
-        ths = [threading.Thread(target=lambda ln=ln, c=c: [ln.frame(**kw) for _ in range(c)])
-               for ln, c in zip(lanes, counts)]
+        ths = [threading.Thread(target=lane_loop, args=(ln,)) for ln in lanes]
         for t in ths:
             t.start()
         for t in ths:
