@@ -372,6 +372,8 @@ int icg_host_free(void* ptr);
 int icg_device_alloc(icg_context* ctx, size_t bytes, void** ptr);
 int icg_device_free(icg_context* ctx, void* ptr);
 int icg_memcpy(icg_context* ctx, void* dst, const void* src, size_t bytes, int dst_mem, int src_mem);
+/* bytes of device memory set to `value` on the context's stream (returns when done; e.g. an L2 flush) */
+int icg_memset(icg_context* ctx, void* dst, int value, size_t bytes);
 
 /* Seeded synthetic inputs; Rng = mt19937_64 with the
  * reference's hand-rolled uniform / Box-Muller (random.hpp:16-43). */

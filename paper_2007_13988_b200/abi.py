@@ -211,6 +211,7 @@ SIGNATURES = [
     ("icg_device_alloc", C.c_int, [ctx_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     ("icg_device_free", C.c_int, [ctx_p, C.c_void_p]),
     ("icg_memcpy", C.c_int, [ctx_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int]),
+    ("icg_memset", C.c_int, [ctx_p, C.c_void_p, C.c_int, C.c_size_t]),
     ("icg_gen_capsules", C.c_int, [C.c_uint64, C.c_int, C.POINTER(icg_primitive)]),
     ("icg_gen_normals", C.c_int, [C.c_uint64, C.c_size_t, f32p]),
     ("icg_gen_mlp", C.c_int, [C.c_uint64, C.c_int, f32p, f32p]),

@@ -406,6 +406,10 @@ class Context:
     def memcpy(self, dst: int, src: int, nbytes: int, dst_mem: int, src_mem: int):
         _check(self._lib.icg_memcpy(self.h, C.c_void_p(dst), C.c_void_p(src), nbytes, dst_mem, src_mem))
 
+    def memset(self, dst: int, value: int, nbytes: int):
+        """Device bytes set on the context's stream (returns when done)."""
+        _check(self._lib.icg_memset(self.h, C.c_void_p(dst), value, nbytes))
+
     def frame_raw(self, fld: "_Field", cfg: AlgoConfig, camera: CameraSpec, width: int, height: int,
                   img: "abi.icg_image", ext: Optional["abi.icg_extraction"] = None, background=(0.0, 0.0, 0.0)):
         """icg_frame with caller-owned output structs (host or device buffers)."""

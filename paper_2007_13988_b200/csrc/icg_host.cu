@@ -2141,6 +2141,16 @@ int icg_memcpy(icg_context* c, void* dst, const void* src, size_t bytes, int dst
     return ICG_OK;
 }
 
+int icg_memset(icg_context* c, void* dst, int value, size_t bytes) {
+    if (!c) return einval("null context");
+    if (bytes == 0) return ICG_OK;
+    if (!dst) return einval("memset: null pointer");
+    ICG_CUDA_TRY(cudaSetDevice(c->device));
+    ICG_CUDA_TRY(cudaMemsetAsync(dst, value, bytes, c->stream));
+    ICG_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return ICG_OK;
+}
+
 // ---- seeded inputs: std::mt19937_64 + random.hpp:22-38 transforms ----------
 static double u01(std::mt19937_64& g) { return (double)(g() >> 11) * 0x1.0p-53; }
 static double urange(std::mt19937_64& g, double lo, double hi) { return lo + (hi - lo) * u01(g); }
