@@ -92,22 +92,22 @@ __device__ __forceinline__ uint32_t row_word(const uint32_t* __restrict__ g, uin
     return r ? __funnelshift_r(lo, __ldg(&g[q + 1]), r) : lo;
 }
 
-__device__ __forceinline__ uint32_t sbit(const uint32_t* row, int i) { return (row[i >> 5] >> (i & 31)) & 1u; }
 
-__global__ void __launch_bounds__(kFineThreads)
+__global__ void __launch_bounds__(kFineThreads, 8)
 k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const uint32_t* __restrict__ cbin,
             const uint32_t* __restrict__ mixed, int rc, float* __restrict__ fv, uint8_t* __restrict__ fs,
             uint32_t* __restrict__ tentbin, uint32_t* __restrict__ sel) {
-    // per warp: the parent rows' binarised bits summed per coarse node, as 3 bit planes
-    // (count = p0 + 2 p1 + 4 p2, count <= 4), and the OR of the adjacent mixed-cell rows
-    __shared__ uint32_t plane[kFineThreads / 32][3][kRowWords];
-    __shared__ uint32_t mrow[kFineThreads / 32][kRowWords];
+    // per warp: one byte per coarse x of the row, (number of binarised parents set, bits 0-2) |
+    // (coarse cell x mixed in an adjacent cell row, bit 4); built only for rows near the surface
+    __shared__ uint8_t info_s[kFineThreads / 32][32 * kRowWords];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int fn = 2 * rc + 1, cn = rc + 1;
     const uint32_t nrows_total = (uint32_t)fn * (uint32_t)fn;
     const int cwords = (cn + 31) >> 5, mwords = (rc + 31) >> 5;
-    uint32_t(*pl)[kRowWords] = plane[wl];
-    uint32_t* mr = mrow[wl];
+    uint8_t* inf = info_s[wl];
+    // valid bits of this lane's word of a coarse node row (cn bits) and of a cell row (rc bits)
+    const uint32_t valid = lane < cwords ? (lane == cwords - 1 && (cn & 31) ? (1u << (cn & 31)) - 1u : ~0u) : 0u;
+    const uint32_t mvalid = lane < mwords ? (lane == mwords - 1 && (rc & 31) ? (1u << (rc & 31)) - 1u : ~0u) : 0u;
     for (uint32_t row = blockIdx.x * (kFineThreads / 32) + wl; row < nrows_total; row += gridDim.x * (kFineThreads / 32)) {
         const int k = (int)(row / (uint32_t)fn), j = (int)(row - (uint32_t)k * fn);
         const int j0 = j >> 1, j1 = (j + 1) >> 1, k0 = k >> 1, k1 = (k + 1) >> 1;
@@ -116,109 +116,155 @@ k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const 
         int yl, yh, zl, zh;
         adjacent_cells(j, rc, yl, yh);
         adjacent_cells(k, rc, zl, zh);
-        __syncwarp();
+        // lane w < cwords: word w of the bit-sliced sum of the (1, 2 or 4) parent bit rows
+        // (upsample_interpolate, grid.hpp:106-115): count = p0 + 2 p1 + 4 p2 <= 4
+        uint32_t p0 = 0u, p1 = 0u, p2 = 0u, m = 0u;
         if (lane < cwords) {
-            // bit-sliced sum of the (1, 2 or 4) parent bit rows (upsample_interpolate, grid.hpp:106-115)
             const uint32_t a = row_word(cbin, (uint32_t)cn * ((uint32_t)j0 + (uint32_t)cn * (uint32_t)k0), lane);
             const uint32_t b = jy ? row_word(cbin, (uint32_t)cn * ((uint32_t)j1 + (uint32_t)cn * (uint32_t)k0), lane) : 0u;
             const uint32_t c = kz ? row_word(cbin, (uint32_t)cn * ((uint32_t)j0 + (uint32_t)cn * (uint32_t)k1), lane) : 0u;
             const uint32_t d = (jy && kz) ? row_word(cbin, (uint32_t)cn * ((uint32_t)j1 + (uint32_t)cn * (uint32_t)k1), lane) : 0u;
             const uint32_t ab0 = a ^ b, ab1 = a & b, cd0 = c ^ d, cd1 = c & d;
             const uint32_t carry = ab0 & cd0, t = ab1 ^ cd1;
-            pl[0][lane] = ab0 ^ cd0;
-            pl[1][lane] = t ^ carry;
-            pl[2][lane] = (ab1 & cd1) | (t & carry);
+            p0 = (ab0 ^ cd0) & valid;
+            p1 = (t ^ carry) & valid;
+            p2 = ((ab1 & cd1) | (t & carry)) & valid;
         }
-        if (lane < mwords) {
-            uint32_t m = 0;
-            for (int cz = zl; cz <= zh; ++cz)
-                for (int cy = yl; cy <= yh; ++cy)
-                    m |= row_word(mixed, (uint32_t)rc * ((uint32_t)cy + (uint32_t)rc * (uint32_t)cz), lane);
-            mr[lane] = m;
+        // lane w < mwords: word w of the OR of the adjacent mixed-cell rows (dilate_1ring of
+        // boundary_candidates, as cells)
+        if (lane < mwords) {  // (at most 2 x 2 rows: all loads issued before the ORs)
+            const uint32_t r00 = (uint32_t)rc * ((uint32_t)yl + (uint32_t)rc * (uint32_t)zl);
+            const uint32_t r10 = (uint32_t)rc * ((uint32_t)yh + (uint32_t)rc * (uint32_t)zl);
+            const uint32_t r01 = (uint32_t)rc * ((uint32_t)yl + (uint32_t)rc * (uint32_t)zh);
+            const uint32_t r11 = (uint32_t)rc * ((uint32_t)yh + (uint32_t)rc * (uint32_t)zh);
+            const bool dy = yh != yl, dz = zh != zl;
+            const uint32_t m00 = row_word(mixed, r00, lane);
+            const uint32_t m10 = dy ? row_word(mixed, r10, lane) : 0u;
+            const uint32_t m01 = dz ? row_word(mixed, r01, lane) : 0u;
+            const uint32_t m11 = (dy && dz) ? row_word(mixed, r11, lane) : 0u;
+            m = (m00 | m10 | m01 | m11) & mvalid;
         }
-        __syncwarp();
         const uint32_t rowbase = row * (uint32_t)fn;
         const bool even_jk = !((j | k) & 1);
         const uint32_t cbase = (uint32_t)cn * ((uint32_t)j0 + (uint32_t)cn * (uint32_t)k0);
         // rows away from the surface (most of them): no adjacent mixed cell and a uniform parent box
         // along the whole row -> every non-even node is the uniform value 0 or 1, nothing selected
         {
-            const uint32_t valid = lane < cwords ? (lane == cwords - 1 && (cn & 31) ? (1u << (cn & 31)) - 1u : ~0u) : 0u;
-            const uint32_t p0 = lane < cwords ? pl[0][lane] & valid : 0u, p1 = lane < cwords ? pl[1][lane] & valid : 0u,
-                           p2 = lane < cwords ? pl[2][lane] & valid : 0u;
             const uint32_t full = lgr == 0 ? p0 : lgr == 1 ? p1 : p2;  // count == 2^lgr (all parents inside)
-            const bool any_mixed = __any_sync(0xffffffffu, lane < mwords && mr[lane] != 0u);
+            const bool any_mixed = __any_sync(0xffffffffu, m != 0u);
             const bool all0 = !__any_sync(0xffffffffu, (p0 | p1 | p2) != 0u);
-            const bool all1 = !__any_sync(0xffffffffu, lane < cwords && (full != valid || (lgr >= 1 && (p0 & valid)) ||
-                                                                          (lgr == 2 && (p1 & valid))));
+            const bool all1 = !__any_sync(0xffffffffu, lane < cwords && (full != valid || (lgr >= 1 && p0) ||
+                                                                          (lgr == 2 && p1)));
             if (!any_mixed && (all0 || all1)) {
                 const float u = all1 ? 1.0f : 0.0f;
-                for (int i0w = 0; i0w < fn; i0w += 32) {
-                    const int i = i0w + lane;
-                    if (i < fn) {
+                if (!even_jk) {
+                    // every node is u / interpolated: 16-byte stores between a scalar head and tail
+                    float* vrow = fv + rowbase;
+                    const int hv = min((int)(((16u - ((uint32_t)(uintptr_t)vrow & 15u)) & 15u) >> 2), fn);
+                    const int nv = (fn - hv) >> 2, tv = hv + 4 * nv;
+                    if (lane < hv) vrow[lane] = u;
+                    float4* v4 = reinterpret_cast<float4*>(vrow + hv);
+                    for (int q = lane; q < nv; q += 32) v4[q] = make_float4(u, u, u, u);
+                    if (tv + lane < fn) vrow[tv + lane] = u;
+                    uint8_t* srow = fs + rowbase;
+                    const int hs = min((int)((16u - ((uint32_t)(uintptr_t)srow & 15u)) & 15u), fn);
+                    const int ns = (fn - hs) >> 4, ts = hs + 16 * ns;
+                    constexpr uint32_t i4 = 0x01010101u * ICG_STATE_INTERPOLATED;
+                    if (lane < hs) srow[lane] = ICG_STATE_INTERPOLATED;
+                    uint4* s16 = reinterpret_cast<uint4*>(srow + hs);
+                    for (int q = lane; q < ns; q += 32) s16[q] = make_uint4(i4, i4, i4, i4);
+                    if (ts + lane < fn) srow[ts + lane] = ICG_STATE_INTERPOLATED;
+                } else {
+                    // even nodes carry the coarse row, odd ones are u: 4 nodes per lane (float4 +
+                    // 4-byte state stores; the launcher checks fv 16-byte / fs 4-byte base alignment)
+                    const int hv = min((int)((4u - (rowbase & 3u)) & 3u), fn);
+                    const int nq = (fn - hv) >> 2, tq = hv + 4 * nq;
+                    auto one = [&](int i) {
                         float v = u;
                         uint8_t st = ICG_STATE_INTERPOLATED;
-                        if (even_jk && !(i & 1)) {
+                        if (!(i & 1)) {
                             v = __ldg(&cv[cbase + (i >> 1)]);
                             st = __ldg(&cs[cbase + (i >> 1)]);
                         }
                         fv[rowbase + i] = v;
                         fs[rowbase + i] = st;
-                    }
-                    if (all1) {
-                        const unsigned tbw = __ballot_sync(0xffffffffu, i < fn);
-                        if (lane == 0) {
-                            const uint32_t first = rowbase + (uint32_t)i0w, sh = first & 31u, w = first >> 5;
-                            atomicOr(&tentbin[w], tbw << sh);
-                            if (sh && (tbw >> (32 - sh))) atomicOr(&tentbin[w + 1], tbw >> (32 - sh));
+                    };
+                    if (lane < hv) one(lane);
+                    if (tq + lane < fn) one(tq + lane);
+                    const int par = hv & 1;  // group node e is even iff e == par (mod 2)
+                    float4* v4 = reinterpret_cast<float4*>(fv + rowbase + hv);
+                    uint32_t* s4 = reinterpret_cast<uint32_t*>(fs + rowbase + hv);
+                    for (int q = lane; q < nq; q += 32) {
+                        const uint32_t x0 = cbase + (uint32_t)((hv + par) >> 1) + 2u * (uint32_t)q;
+                        const float c0 = __ldg(&cv[x0]), c1 = __ldg(&cv[x0 + 1]);
+                        const uint32_t t0 = __ldg(&cs[x0]), t1 = __ldg(&cs[x0 + 1]);
+                        constexpr uint32_t I = ICG_STATE_INTERPOLATED;
+                        if (par == 0) {
+                            v4[q] = make_float4(c0, u, c1, u);
+                            s4[q] = t0 | (I << 8) | (t1 << 16) | (I << 24);
+                        } else {
+                            v4[q] = make_float4(u, c0, u, c1);
+                            s4[q] = I | (t0 << 8) | (I << 16) | (t1 << 24);
                         }
+                    }
+                }
+                if (all1) {  // every tentative bit of the row is set: one OR per word
+                    const uint32_t last = rowbase + (uint32_t)fn - 1u, w0 = rowbase >> 5, w1 = last >> 5;
+                    for (uint32_t w = w0 + (uint32_t)lane; w <= w1; w += 32u) {
+                        uint32_t mk = ~0u;
+                        if (w == w0) mk &= ~0u << (rowbase & 31u);
+                        if (w == w1) mk &= ~0u >> (31u - (last & 31u));
+                        atomicOr(&tentbin[w], mk);
                     }
                 }
                 continue;
             }
         }
-        auto count = [&](int x) -> int {
-            const int w = x >> 5, sh = x & 31;
-            return (int)((pl[0][w] >> sh) & 1u) + 2 * (int)((pl[1][w] >> sh) & 1u) + 4 * (int)((pl[2][w] >> sh) & 1u);
-        };
+        // the per-x info bytes of this row (word t of the planes / mixed row from lane t)
+        __syncwarp();  // the previous row's readers are done
+        for (int t = 0; t < cwords; ++t) {
+            const uint32_t q0 = __shfl_sync(0xffffffffu, p0, t), q1 = __shfl_sync(0xffffffffu, p1, t),
+                           q2 = __shfl_sync(0xffffffffu, p2, t), qm = __shfl_sync(0xffffffffu, m, t);
+            inf[32 * t + lane] = (uint8_t)(((q0 >> lane) & 1u) | (((q1 >> lane) & 1u) << 1) |
+                                           (((q2 >> lane) & 1u) << 2) | (((qm >> lane) & 1u) << 4));
+        }
+        __syncwarp();
         for (int i0w = 0; i0w < fn; i0w += 32) {
             const int i = i0w + lane;
             bool tb = false, sl = false;
             if (i < fn) {
                 const int odd = i & 1, x0 = i >> 1;
-                const int ones = count(x0) + (odd ? count(x0 + 1) : 0);
+                // node i interpolates coarse nodes x0 (and x0 + 1 if odd); its adjacent cells are x0
+                // (odd) or x0 - 1 and x0, clamped to the grid (an unused x0 = rc cell bit is 0)
+                const uint32_t ia = inf[x0], ib = inf[odd ? x0 + 1 : (x0 > 0 ? x0 - 1 : 0)];
+                const int ones = (int)(ia & 7u) + (odd ? (int)(ib & 7u) : 0);
+                const bool flagged = (((odd ? ia : (ia | ib)) >> 4) & 1u) != 0u;  // dilate_1ring(boundary_candidates)
+                const int lg = lgr + odd;
                 float v;
                 uint8_t st;
                 if (even_jk && !odd) {
                     // even node: carry the coarse scalar and state (carry_scalars, localize.hpp:116-119)
                     v = __ldg(&cv[cbase + x0]);
                     st = __ldg(&cs[cbase + x0]);
-                    tb = ones != 0;  // its tentative value is the binarised coarse value
                 } else {
                     // mean of the binarised parents: exact dyadic ones / 2^lg
-                    const int lg = lgr + odd;
                     v = (float)ones * __int_as_float((127 - lg) << 23);
                     st = ICG_STATE_INTERPOLATED;
-                    tb = 2 * ones >= (1 << lg);  // tent >= 0.5f
                 }
+                // tent >= 0.5f (for an even node: its binarised coarse value)
+                tb = 2 * ones >= (1 << lg);
                 fv[rowbase + i] = v;
                 fs[rowbase + i] = st;
-                int xl, xh;
-                adjacent_cells(i, rc, xl, xh);
-                const bool flagged = sbit(mr, xl) | sbit(mr, xh);  // dilate_1ring(boundary_candidates)
-                sl = flagged && st != ICG_STATE_EVALUATED;          // mask_to_unevaluated_list
+                sl = flagged && st != ICG_STATE_EVALUATED;  // mask_to_unevaluated_list
             }
             const unsigned tbw = __ballot_sync(0xffffffffu, tb), sw = __ballot_sync(0xffffffffu, sl);
-            if (lane == 0) {
+            // lane 0 merges the tentative bits, lane 1 the selection bits (one code path)
+            const unsigned bits = lane == 0 ? tbw : sw;
+            if (lane < 2 && bits) {
+                uint32_t* dst = lane == 0 ? tentbin : sel;
                 const uint32_t first = rowbase + (uint32_t)i0w, sh = first & 31u, w = first >> 5;
-                if (tbw) {
-                    atomicOr(&tentbin[w], tbw << sh);
-                    if (sh && (tbw >> (32 - sh))) atomicOr(&tentbin[w + 1], tbw >> (32 - sh));
-                }
-                if (sw) {
-                    atomicOr(&sel[w], sw << sh);
-                    if (sh && (sw >> (32 - sh))) atomicOr(&sel[w + 1], sw >> (32 - sh));
-                }
+                atomicOr(&dst[w], bits << sh);
+                if (sh && (bits >> (32 - sh))) atomicOr(&dst[w + 1], bits >> (32 - sh));
             }
         }
     }
@@ -360,6 +406,10 @@ int launch_level_carry(const LevelBufs& b, DevCounters* ctr, int level, cudaStre
         set_error("level classify: grid too large");
         return ICG_ERUNTIME;
     }
+    if (((uintptr_t)b.fv & 15u) || ((uintptr_t)b.fs & 3u)) {  // k_fine_rows' vector stores
+        set_error("level classify: fine grid buffers not 16-byte (values) / 4-byte (states) aligned");
+        return ICG_ERUNTIME;
+    }
     size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
     const unsigned nwords = (unsigned)((nf + 31) / 32);
     k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
@@ -377,6 +427,10 @@ int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaS
     const int rc = b.rc, cn = rc + 1, fn = 2 * rc + 1;
     if (cn + 32 > 32 * kRowWords) {
         set_error("level classify: grid too large");
+        return ICG_ERUNTIME;
+    }
+    if (((uintptr_t)b.fv & 15u) || ((uintptr_t)b.fs & 3u)) {  // k_fine_rows' vector stores
+        set_error("level classify: fine grid buffers not 16-byte (values) / 4-byte (states) aligned");
         return ICG_ERUNTIME;
     }
     size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
