@@ -92,6 +92,47 @@ __device__ __forceinline__ uint32_t row_word(const uint32_t* __restrict__ g, uin
     return r ? __funnelshift_r(lo, __ldg(&g[q + 1]), r) : lo;
 }
 
+// ---- the same cells 32 at a time (rc a multiple of 32: a word of the cell bitset is 32 cells of
+// one cell row): per corner node row, the word of corners x and its shift by one (corners x + 1);
+// a cell is mixed when the OR of its 8 corners is set and their AND is not
+__global__ void k_mixed_words(const uint32_t* __restrict__ cbin, int rc, uint32_t* __restrict__ mixed,
+                              unsigned long long* refined) {
+    const unsigned wpr = (unsigned)rc >> 5, nw = (unsigned)rc * (unsigned)rc * wpr;
+    const unsigned w = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned cnt = 0;
+    if (w < nw) {
+        const unsigned row = w / wpr, ci0 = (w - row * wpr) << 5;
+        const unsigned ck = row / (unsigned)rc, cj = row - ck * (unsigned)rc, cn = (unsigned)rc + 1u;
+        uint32_t any = 0u, all = ~0u;
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t base = cn * ((cj + (d & 1)) + cn * (ck + (d >> 1))) + ci0;
+            const uint32_t lo = row_word(cbin, base, 0);
+            const uint32_t b32 = (__ldg(&cbin[(base + 32u) >> 5]) >> ((base + 32u) & 31u)) & 1u;
+            const uint32_t x1 = (lo >> 1) | (b32 << 31);
+            any |= lo | x1;
+            all &= lo & x1;
+        }
+        const uint32_t mw = any & ~all;
+        mixed[w] = mw;
+        cnt = __popc(mw);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(refined, (unsigned long long)cnt);
+}
+
+static void launch_mixed(const uint32_t* cbin, int rc, uint32_t* mixed, unsigned long long* refined, cudaStream_t s) {
+    if ((rc & 31) == 0) {
+        const unsigned nw = (unsigned)rc * (unsigned)rc * ((unsigned)rc >> 5);
+        k_mixed_words<<<(nw + 255) / 256, 256, 0, s>>>(cbin, rc, mixed, refined);
+    } else {
+        const size_t ncell = (size_t)rc * rc * rc;
+        k_mixed_cells<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(cbin, rc, mixed, refined);
+    }
+}
+
+
 
 __global__ void __launch_bounds__(kFineThreads, 8)
 k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const uint32_t* __restrict__ cbin,
@@ -413,7 +454,7 @@ int launch_level_carry(const LevelBufs& b, DevCounters* ctr, int level, cudaStre
     size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
     const unsigned nwords = (unsigned)((nf + 31) / 32);
     k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
-    k_mixed_cells<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(b.cbin, rc, b.mixed, &ctr->refined[level]);
+    launch_mixed(b.cbin, rc, b.mixed, &ctr->refined[level], s);
     ICG_CUDA_TRY(cudaMemsetAsync(b.tentbin, 0, ((size_t)nwords + 1) * 4, s));
     ICG_CUDA_TRY(cudaMemsetAsync(b.sel, 0, ((size_t)nwords + 1) * 4, s));
     const unsigned rows = (unsigned)fn * fn;
@@ -437,7 +478,7 @@ int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaS
     const unsigned nwords = (unsigned)((nf + 31) / 32);
     const unsigned nblocks = (nwords + kWordsPerCta - 1) / kWordsPerCta;
     k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
-    k_mixed_cells<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(b.cbin, rc, b.mixed, &ctr->refined[level]);
+    launch_mixed(b.cbin, rc, b.mixed, &ctr->refined[level], s);
     ICG_CUDA_TRY(cudaMemsetAsync(b.tentbin, 0, ((size_t)nwords + 1) * 4, s));
     ICG_CUDA_TRY(cudaMemsetAsync(b.sel, 0, ((size_t)nwords + 1) * 4, s));
     const unsigned rows = (unsigned)fn * fn;
