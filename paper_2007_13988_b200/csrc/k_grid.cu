@@ -38,6 +38,39 @@ __global__ void k_coarse_bits(const float* __restrict__ cv, size_t n, uint32_t* 
     if ((threadIdx.x & 31) == 0 && idx < n) bits[idx >> 5] = m;
 }
 
+// the same, 128 nodes per warp step: lane l loads nodes 4l..4l+3 as one float4 (cv 16-byte aligned,
+// the launcher checks), its 4 bits are OR-merged over groups of 8 lanes into the step's 4 words
+__global__ void k_coarse_bits4(const float* __restrict__ cv, size_t n, uint32_t* __restrict__ bits) {
+    const unsigned lane = threadIdx.x & 31u;
+    const size_t nwarps = (size_t)gridDim.x * (blockDim.x >> 5);
+    for (size_t q = (size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); 128 * q < n; q += nwarps) {
+        const size_t i0 = 128 * q + 4 * lane;
+        uint32_t nib = 0u;
+        if (i0 + 3 < n) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(cv + i0));
+            nib = (v.x >= 0.5f ? 1u : 0u) | (v.y >= 0.5f ? 2u : 0u) | (v.z >= 0.5f ? 4u : 0u) | (v.w >= 0.5f ? 8u : 0u);
+        } else {
+            for (int e = 0; e < 4; ++e)
+                if (i0 + e < n && __ldg(&cv[i0 + e]) >= 0.5f) nib |= 1u << e;  // binarize_value, grid.hpp:122
+        }
+        uint32_t w = nib << (4u * (lane & 7u));
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((lane & 7u) == 0 && 128 * q + 4 * lane < n) bits[4 * q + (lane >> 3)] = w;
+    }
+}
+
+static void launch_coarse_bits(const float* cv, size_t n, uint32_t* bits, cudaStream_t s) {
+    if (((uintptr_t)cv & 15u) == 0) {
+        const size_t steps = (n + 127) / 128;  // one per warp, 8 warps per block
+        const unsigned blocks = (unsigned)std::min<size_t>((steps + 7) / 8, 148u * 16u);
+        k_coarse_bits4<<<blocks, 256, 0, s>>>(cv, n, bits);
+    } else {
+        k_coarse_bits<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cv, n, bits);
+    }
+}
+
 // ---- coarse cells with mixed binarised corners (refined-cell set) ---------
 __global__ void k_mixed_cells(const uint32_t* __restrict__ cbin, int rc, uint32_t* __restrict__ mixed,
                               unsigned long long* refined) {
@@ -453,7 +486,7 @@ int launch_level_carry(const LevelBufs& b, DevCounters* ctr, int level, cudaStre
     }
     size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
     const unsigned nwords = (unsigned)((nf + 31) / 32);
-    k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
+    launch_coarse_bits(b.cv, ncoarse, b.cbin, s);
     launch_mixed(b.cbin, rc, b.mixed, &ctr->refined[level], s);
     ICG_CUDA_TRY(cudaMemsetAsync(b.tentbin, 0, ((size_t)nwords + 1) * 4, s));
     ICG_CUDA_TRY(cudaMemsetAsync(b.sel, 0, ((size_t)nwords + 1) * 4, s));
@@ -477,7 +510,7 @@ int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaS
     size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
     const unsigned nwords = (unsigned)((nf + 31) / 32);
     const unsigned nblocks = (nwords + kWordsPerCta - 1) / kWordsPerCta;
-    k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
+    launch_coarse_bits(b.cv, ncoarse, b.cbin, s);
     launch_mixed(b.cbin, rc, b.mixed, &ctr->refined[level], s);
     ICG_CUDA_TRY(cudaMemsetAsync(b.tentbin, 0, ((size_t)nwords + 1) * 4, s));
     ICG_CUDA_TRY(cudaMemsetAsync(b.sel, 0, ((size_t)nwords + 1) * 4, s));
@@ -886,7 +919,7 @@ int launch_octree_level(const LevelBufs& b, uint32_t* iface, int mode, double th
     const int rc = b.rc, cn = rc + 1, fn = 2 * rc + 1;
     const size_t ncoarse = (size_t)cn * cn * cn, ncell = (size_t)rc * rc * rc, nf = (size_t)fn * fn * fn;
     if (mode == 0) {
-        k_coarse_bits<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cv, ncoarse, b.cbin);
+        launch_coarse_bits(b.cv, ncoarse, b.cbin, s);
         k_interface_nodes<<<(unsigned)((ncoarse + 255) / 256), 256, 0, s>>>(b.cbin, rc, iface);
     }
     k_octree_cells<<<(unsigned)((ncell + 255) / 256), 256, 0, s>>>(iface, b.cv, rc, threshold, mode, b.mixed,

@@ -32,8 +32,31 @@ __global__ void k_chw_to_hwc(const float* __restrict__ chw, float* __restrict__ 
     }
 }
 
+// 64 x 64 tiles, 8-byte loads and stores (C and H*W multiples of 64, 8-byte aligned maps)
+__global__ void __launch_bounds__(256) k_chw_to_hwc64(const float* __restrict__ chw, float* __restrict__ hwc, int C,
+                                                      int HW) {
+    __shared__ float tile[64][65];
+    const int p0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+#pragma unroll
+    for (int r = ty; r < 64; r += 8) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(chw + (size_t)(c0 + r) * HW + p0 + 2 * tx));
+        tile[r][2 * tx] = v.x;
+        tile[r][2 * tx + 1] = v.y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = ty; r < 64; r += 8)
+        *reinterpret_cast<float2*>(hwc + (size_t)(p0 + r) * C + c0 + 2 * tx) = make_float2(tile[2 * tx][r], tile[2 * tx + 1][r]);
+}
+
 int launch_fmap_chw_to_hwc(const float* chw, float* hwc, int C, int H, int W, cudaStream_t s) {
     int HW = H * W;
+    if (C % 64 == 0 && HW % 64 == 0 && !((uintptr_t)chw & 7u) && !((uintptr_t)hwc & 7u)) {
+        k_chw_to_hwc64<<<dim3(HW / 64, C / 64), dim3(32, 8), 0, s>>>(chw, hwc, C, HW);
+        ICG_CUDA_TRY(cudaGetLastError());
+        return ICG_OK;
+    }
     dim3 grid((HW + 31) / 32, (C + 31) / 32), block(32, 8);
     k_chw_to_hwc<<<grid, block, 0, s>>>(chw, hwc, C, HW);
     ICG_CUDA_TRY(cudaGetLastError());
