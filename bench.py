@@ -493,9 +493,19 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
                             / max(1e-9, prof["tex_mlp_ms"] / 1e3) / 1e12,
                             "frac_of_burst": prof["tex_points"] * TEX_FLOP_PER_POINT
                             / max(1e-9, prof["tex_mlp_ms"] / 1e3) / 1e12 / peak_t},
+            # every level's dense pass (binarize, mixed cells, upsample / carry / candidates, E0
+            # compaction), the coarse levels being a few us each; the target level alone beside it
             "dense_passes": {"bytes": prof["dense_bytes"], "ms": prof["dense_ms"],
+                             "launch_groups": prof["dense_launches"],
                              "achieved_gbs": prof["dense_bytes"] / max(1e-9, prof["dense_ms"] / 1e3) / 1e9,
                              "peak_gbs": pk.get("hbm_gbs")},
+            "last_level_pass": {"bytes": prof["last_level_bytes"], "ms": prof["last_level_ms"],
+                                "achieved_gbs": prof["last_level_bytes"] / max(1e-9, prof["last_level_ms"] / 1e3) / 1e9,
+                                "frac_of_hbm": prof["last_level_bytes"] / max(1e-9, prof["last_level_ms"] / 1e3) / 1e9
+                                / max(1e-9, pk.get("hbm_gbs") or 1e-9)},
+            # the conflict loop's neighbour expansions (latency-bound chain links, not a dense pass)
+            "conflict_expand": {"launches": prof["expand_launches"], "ms": prof["expand_ms"],
+                                "ms_per_frame": prof["expand_ms"] / max(1, prof["frames"])},
             "render": {"bytes": prof["render_bytes"], "ms": prof["render_ms"],
                        "achieved_gbs": prof["render_bytes"] / max(1e-9, prof["render_ms"] / 1e3) / 1e9},
             # the texture field's Phi gather: 4 bilinear taps x C x 4 B per surface point (L2-resident map)

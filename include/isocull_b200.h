@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ICG_ABI_VERSION 3
+#define ICG_ABI_VERSION 4
 
 /* ---- status codes ------------------------------------------------------ */
 #define ICG_OK 0
@@ -327,7 +327,7 @@ typedef struct icg_profile {
     uint64_t tex_mlp_launches;
     uint64_t tex_points;
     double tex_mlp_ms;
-    uint64_t dense_launches;       /* per-level dense passes + compaction + conflict expansion */
+    uint64_t dense_launches;       /* per-level dense passes + compaction (conflict expansion: ABI 4, below) */
     double dense_ms;
     uint64_t dense_bytes;          /* algorithmic bytes of the dense passes */
     uint64_t render_launches;
@@ -348,6 +348,14 @@ typedef struct icg_profile {
     uint64_t gather_points;
     double gather_ms;
     uint64_t gather_bytes;
+    /* ABI 4: the conflict loop's neighbour expansions (k_conflict_expand; counted in dense_* before
+       ABI 4), and the target level's dense pass alone (also in dense_*): binarize + mixed cells +
+       upsample / carry / candidates + E0 compaction at full size, its SURVEY §8(d) bytes */
+    uint64_t expand_launches;
+    double expand_ms;
+    uint64_t last_level_launches;
+    double last_level_ms;
+    uint64_t last_level_bytes;
 } icg_profile;
 
 int icg_profile_enable(icg_context* ctx, int on);

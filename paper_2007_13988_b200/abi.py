@@ -24,7 +24,7 @@ ICG_MLP_GEOMETRY, ICG_MLP_TEXTURE = 0, 1
 ICG_MLP_LAYERS = 5
 ICG_VARIANT_BRUTE, ICG_VARIANT_OCTREE_BINARIZED, ICG_VARIANT_OCTREE_THRESHOLD, ICG_VARIANT_PROGRESSIVE = 0, 1, 2, 3
 ICG_SET_EVALUATED_NODES, ICG_SET_REFINED_CELLS = 0, 1
-ICG_ABI_VERSION = 3
+ICG_ABI_VERSION = 4
 
 f32p = C.POINTER(C.c_float)
 u8p = C.POINTER(C.c_uint8)
@@ -169,6 +169,11 @@ class icg_profile(C.Structure):
         ("gather_points", C.c_uint64),
         ("gather_ms", C.c_double),
         ("gather_bytes", C.c_uint64),
+        ("expand_launches", C.c_uint64),
+        ("expand_ms", C.c_double),
+        ("last_level_launches", C.c_uint64),
+        ("last_level_ms", C.c_double),
+        ("last_level_bytes", C.c_uint64),
     ]
 
 

@@ -258,6 +258,11 @@ void prof_collect(icg_context* c) {
             case 2: c->prof.dense_ms += ms; c->prof.dense_launches++; break;
             case 3: c->prof.render_ms += ms; c->prof.render_launches++; break;
             case 6: c->prof.gather_ms += ms; c->prof.gather_launches++; break;  // (inside a kind-1 interval)
+            case 7: c->prof.expand_ms += ms; c->prof.expand_launches++; break;
+            case 8:  // the target level's dense pass (also a dense pass)
+                c->prof.dense_ms += ms; c->prof.dense_launches++;
+                c->prof.last_level_ms += ms; c->prof.last_level_launches++;
+                break;
         }
     }
     prof_discard(c);
@@ -816,7 +821,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
             continue;
         }
         {
-            int slot = prof_begin(c, 2);
+            int slot = prof_begin(c, l == cfg->target_level ? 8 : 2);
             int r = launch_level_classify(lb, ctr, l, c->stream);
             prof_end(c, slot);
             c->launches += 5;
@@ -856,7 +861,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                 const int pm =
                     (chain_pred && c->pred_valid[l] && !c->pred_all[l] && it < kPredIters) ? c->pred[l][it] : 15;
                 {
-                    int slot = prof_begin(c, 2);
+                    int slot = prof_begin(c, 7);
                     ChainClasses cc{c->tail_max, mid_max, l, chain_pred ? prev_mask : -1, big_max};
                     int r = launch_conflict_expand_cls(c->queued.as<uint32_t>(), lb.fs, fcells,
                                                        c->cf[p].as<uint32_t>(), ctr, it, max_iters,
@@ -1204,8 +1209,10 @@ void prof_extract_done(icg_context* c, const icg_algo_config* cfg) {
     if (cfg->variant == ICG_VARIANT_PROGRESSIVE) {
         for (int l = 1; l <= cfg->target_level; ++l) {
             // level pass: fine value+state written, coarse read, index list
-            c->prof.dense_bytes += 5 * nodes3(cfg->coarsest_cells << l) + 5 * nodes3(cfg->coarsest_cells << (l - 1)) +
-                                   4 * h.evals[l];
+            const uint64_t b = 5 * nodes3(cfg->coarsest_cells << l) + 5 * nodes3(cfg->coarsest_cells << (l - 1)) +
+                               4 * h.evals[l];
+            c->prof.dense_bytes += b;
+            if (l == cfg->target_level) c->prof.last_level_bytes += b;
         }
     }
 }

@@ -30,12 +30,12 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_struct_sizes():
     lib = abi.lib()
-    assert lib.icg_abi_version() == abi.ICG_ABI_VERSION == 3
+    assert lib.icg_abi_version() == abi.ICG_ABI_VERSION == 4
     # spot-check layouts against the C compiler's view
     assert C.sizeof(abi.icg_primitive) == 8 + 8 * 24
     assert C.sizeof(abi.icg_algo_config) == 32
     assert C.sizeof(abi.icg_camera) == 13 * 8
-    assert C.sizeof(abi.icg_profile) == 25 * 8
+    assert C.sizeof(abi.icg_profile) == 30 * 8
 
 
 def test_no_device_is_reported_not_faked():
