@@ -51,6 +51,7 @@ __device__ __forceinline__ float sample_grid(const float* __restrict__ V, int R,
 
 constexpr int kMaxRenderCells = 1024;
 constexpr int kRenderThreads = 256;
+constexpr int kLaneSamples = 8;  // samples each lane walks of its own ray before the warp walk
 
 // The ray-independent double terms of view_to_world, each computed once per frame with the
 // operations (and roundings) of the per-sample formulation:
@@ -153,11 +154,85 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderJob r) {
                 }
             }
         }
-        // ---------------- the rays, one at a time across the warp ----------------
+        // ---------------- first samples of every ray, lane-parallel ----------------
+        // Most rays cross within a few samples of their window start: each lane walks the first
+        // kLaneSamples samples of its own ray (independent loads in flight), with the same per-
+        // sample arithmetic and the same scan order as the warp walk below, which takes over
+        // (from sample k_lo + kLaneSamples, carrying the last value and the grazing flag) only for
+        // the rays still unresolved.
         int my_k1 = -1;
         float my_vhit = 0.0f, my_vprev = 0.0f;
         bool my_graz = false;
-        unsigned todo = __ballot_sync(0xffffffffu, valid && k_lo <= k_hi);
+        float my_last = 0.0f;  // the sample before the warp walk's start (the one before k_lo is exactly 0)
+        int k_lo2 = k_lo;
+        if (valid && k_lo <= k_hi) {
+            const size_t byz = nn * ((size_t)j0 + nn * (size_t)kk0);
+            auto sample_own = [&](int k) -> float {
+                float v = 0.0f;
+                const double w0 = __dadd_rn(c0, mv_tab[0][k]);
+                const float gx = (float)__dmul_rn(__dadd_rn(w0, 1.0), hr);
+                if (xray) {
+                    if (yz_in && gx >= 0.0f && gx <= fR) {
+                        const int i0 = min((int)floorf(gx), R - 1);
+                        const float fx = __fsub_rn(gx, (float)i0);
+                        const float* V = r.values + byz + (size_t)i0;
+                        const size_t sj = nn, sk = nn * nn;
+                        float c00, c10, c01, c11;
+                        if (fx == 0.0f) {
+                            c00 = __ldg(&V[0]);
+                            c10 = __ldg(&V[sj]);
+                            c01 = __ldg(&V[sk]);
+                            c11 = __ldg(&V[sj + sk]);
+                        } else {
+                            c00 = lerp_rn(__ldg(&V[0]), __ldg(&V[1]), fx);
+                            c10 = lerp_rn(__ldg(&V[sj]), __ldg(&V[sj + 1]), fx);
+                            c01 = lerp_rn(__ldg(&V[sk]), __ldg(&V[sk + 1]), fx);
+                            c11 = lerp_rn(__ldg(&V[sj + sk]), __ldg(&V[sj + sk + 1]), fx);
+                        }
+                        const float cy0 = lerp_rn(c00, c10, fy);
+                        const float cy1 = lerp_rn(c01, c11, fy);
+                        v = lerp_rn(cy0, cy1, fk);
+                    }
+                } else {
+                    const double w1 = __dadd_rn(c1, mv_tab[1][k]);
+                    const double w2 = __dadd_rn(c2, mv_tab[2][k]);
+                    const float gy = (float)__dmul_rn(__dadd_rn(w1, 1.0), hr);
+                    const float gk = (float)__dmul_rn(__dsub_rn(1.0, w2), hr);
+                    v = sample_grid(r.values, R, gx, gy, gk);
+                }
+                return v;
+            };
+            bool done = false;
+#pragma unroll
+            for (int g = 0; g < kLaneSamples; g += 4) {
+                if (!done) {
+                    float v[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int k = k_lo + g + e;
+                        v[e] = k <= k_hi ? sample_own(k) : 0.0f;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int k = k_lo + g + e;
+                        if (!done && k <= k_hi) {
+                            if (v[e] >= 0.5f) {
+                                my_k1 = k;
+                                my_vhit = v[e];
+                                my_vprev = my_last;
+                                done = true;
+                            } else {
+                                my_graz |= v[e] > 0.0f && v[e] < 1.0f;  // render.hpp:180-188
+                                my_last = v[e];
+                            }
+                        }
+                    }
+                }
+            }
+            k_lo2 = done ? k_hi + 1 : k_lo + kLaneSamples;
+        }
+        // ---------------- the remaining rays, one at a time across the warp ----------------
+        unsigned todo = __ballot_sync(0xffffffffu, valid && k_lo2 <= k_hi);
         while (todo) {
             const int p = __ffs(todo) - 1;
             todo &= todo - 1;
@@ -168,7 +243,9 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderJob r) {
             const bool pyz_in = __shfl_sync(0xffffffffu, (int)yz_in, p) != 0;
             const int pj0 = __shfl_sync(0xffffffffu, j0, p), pkk0 = __shfl_sync(0xffffffffu, kk0, p);
             const float pfy = __shfl_sync(0xffffffffu, fy, p), pfk = __shfl_sync(0xffffffffu, fk, p);
-            const int plo = __shfl_sync(0xffffffffu, k_lo, p), phi = __shfl_sync(0xffffffffu, k_hi, p);
+            const int plo = __shfl_sync(0xffffffffu, k_lo2, p), phi = __shfl_sync(0xffffffffu, k_hi, p);
+            const float plast = __shfl_sync(0xffffffffu, my_last, p);
+            const bool pgraz = __shfl_sync(0xffffffffu, (int)my_graz, p) != 0;
             const size_t byz = nn * ((size_t)pj0 + nn * (size_t)pkk0);
             auto sample_at = [&](int k) -> float {
                 float v = 0.0f;
@@ -206,8 +283,8 @@ __global__ void __launch_bounds__(kRenderThreads, 4) k_render(RenderJob r) {
                 return v;
             };
             int k1 = -1;
-            float vprev = 0.0f, vhit = 0.0f, last = 0.0f;  // the sample before k_lo is exactly 0
-            bool grazing = false;
+            float vprev = 0.0f, vhit = 0.0f, last = plast;  // the lane-parallel samples' last value
+            bool grazing = pgraz;
             for (int kb = plo; kb <= phi; kb += 32) {
                 const int k = kb + lane;
                 const float v = k <= phi ? sample_at(k) : 0.0f;
@@ -341,7 +418,10 @@ int launch_render_first_crossing(const RenderJob& r, cudaStream_t s) {
     const int nt = r.width + r.height + r.cells + 1;
     k_render_setup<<<(nt + 255) / 256, 256, 0, s>>>(r);
     const size_t warps = (npx + 31) / 32;  // 32 pixels per warp
-    const size_t blocks = std::min<size_t>((warps + kRenderThreads / 32 - 1) / (kRenderThreads / 32), 148 * 4);
+    // one 32-pixel group per warp (up to 64 blocks per SM): the hardware block scheduler balances the
+    // groups' very different ray walks (a grid-stride loop over one resident wave left ~half of the
+    // warps idle at the end)
+    const size_t blocks = std::min<size_t>((warps + kRenderThreads / 32 - 1) / (kRenderThreads / 32), 148 * 64);
     k_render<<<(unsigned)blocks, kRenderThreads, 0, s>>>(r);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
