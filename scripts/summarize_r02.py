@@ -44,7 +44,7 @@ def main(src, dst, tag="r02"):
         if os.path.exists(p):
             json.dump(launch_summary(p), open(os.path.join(dst, f"{tag}_launch_summary_{c}.json"), "w"), indent=1)
         for k in ("k_fact2", "k_mlp_pair", "k_tail", "k_fine_rows", "k_render", "k_conflict_expand", "k_layer",
-                  "k_cols", "k_gather"):
+                  "k_cols", "k_gather", "k_mixed_words", "k_coarse_bits4", "k_xline_extents", "k_chw_to_hwc64"):
             p = os.path.join(src, f"{tag}_raw_{k}_{c}.csv")
             if os.path.exists(p):
                 json.dump(full(p), open(os.path.join(dst, f"{tag}_ncu_full_{k}_{c}.json"), "w"), indent=1)

@@ -716,3 +716,23 @@ def test_alternate_kernels_match_default(pifu_inputs, monkeypatch, switch):
     assert np.abs(ia.depth[cov] - ib.depth[cov]).max() <= 1e-5
     assert cov.sum() > 1000
     assert np.abs(ia.rgb[cov] - ib.rgb[cov]).max() <= RGB_TOL
+
+
+@pytest.mark.gpu
+def test_odd_feature_map_shape(gpu_ctx, pifu_inputs):
+    """A feature map whose H x W is not a multiple of 64 (the 32 x 32-tile transpose instead of the
+    64 x 64 one) through the per-point and the column-factored paths, against the oracle."""
+    inp = pifu_inputs
+    gpu_ctx.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+    gpu_ctx.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+    fmap = api.gen_feature_map(77, 256, 20, 21)
+    f = api.PifuField(fmap, inp["caps"], 50.0, abi.ICG_PREC_FP32)
+    m = O.Pifu(fmap, inp["caps"], inp["gw"], inp["gb"], inp["tw"], inp["tb"], threads=8)
+    pts = np.random.default_rng(11).uniform(-1, 1, (1500, 3))
+    assert np.abs(gpu_ctx.occupancy_batch(f, pts) - m.occupancy(pts)).max() <= OCC_TOL_FP32
+    g = gpu_ctx.extract(f, api.AlgoConfig("progressive", 16, 2))
+    ev = np.flatnonzero(g.states == abi.ICG_STATE_EVALUATED)
+    n = 65
+    i, j, k = ev % n, (ev // n) % n, ev // (n * n)
+    node_pts = np.stack([-1 + 2 * i / 64.0, -1 + 2 * j / 64.0, 1 - 2 * k / 64.0], 1)
+    assert np.abs(g.values[ev] - m.occupancy(node_pts)).max() <= OCC_TOL_FP32
