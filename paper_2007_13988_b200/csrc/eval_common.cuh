@@ -84,6 +84,12 @@ __device__ __forceinline__ void input_coords(const FieldDev& f, const float* w, 
 __device__ __forceinline__ void grid_epilogue(const EvalJob& j, uint32_t idx, float v) {
     j.values[idx] = v;
     j.states[idx] = ICG_STATE_EVALUATED;
+    if (j.xext && v != 0.0f) {  // (a superset of the final extent is still exact for the renderer)
+        const uint32_t fn = (uint32_t)j.cells + 1u, line = idx / fn;
+        const int i = (int)(idx - line * fn);
+        atomicMin(&j.xext[line].x, i);
+        atomicMax(&j.xext[line].y, i);
+    }
     if (j.tentbin) {
         bool tb = (j.tentbin[idx >> 5] >> (idx & 31)) & 1u;
         bool vb = v >= 0.5f;

@@ -705,6 +705,7 @@ int issue_tail(icg_context* c, const FieldDev& fd, const LevelBufs& lb, int leve
     if (int r = c->tail_scratch.ensure(tail_scratch_bytes(cap_pts, cap_new, (unsigned)plane))) return r;
     TailParams tp{};
     tp.f = fd;
+    tp.xext = lb.xext;
     tp.cells = fcells;
     tp.level = level;
     tp.it0 = it;
@@ -731,7 +732,9 @@ int issue_tail(icg_context* c, const FieldDev& fd, const LevelBufs& lb, int leve
 }
 
 // Issues one whole extraction on the context stream (no host sync).
-int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg) {
+// keep_xext: the target level's x-line extents are kept in c->xext by the level pass and every
+// evaluation epilogue (icg_frame's renderer then skips k_xline_extents; progressive variant only)
+int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg, bool keep_xext = false) {
     prof_discard(c);
     c->fact_used = false;
     DevCounters* ctr = c->ctr.as<DevCounters>();
@@ -782,6 +785,10 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
         lb.block_counts = c->block_counts.as<uint32_t>();
         lb.list = c->list_e0.as<uint32_t>();
         lb.rc = cells;
+        if (keep_xext && !octree && l == L) {
+            if (int r = c->xext.ensure(((size_t)fcells + 1) * ((size_t)fcells + 1) * sizeof(int2))) return r;
+            lb.xext = c->xext.as<int2>();
+        }
         if (octree) {
             // Fig. 4 baselines: mark cells, build the fine grid, evaluate the nodes of marked cells
             const int mode = cfg->variant == ICG_VARIANT_OCTREE_BINARIZED ? 0 : 1;
@@ -836,6 +843,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
         job.values = lb.fv;
         job.states = lb.fs;
         job.overflow = &ctr->overflow;
+        job.xext = lb.xext;
         if (cfg->conflict_pass) {
             job.tentbin = lb.tentbin;
             job.conflicts = c->cf[0].as<uint32_t>();
@@ -884,6 +892,7 @@ int issue_extract(icg_context* c, const FieldDev& fd, const icg_algo_config* cfg
                 cj.evals = &ctr->evals[l];
                 cj.iters = &ctr->conflict_iters[l];
                 cj.overflow = &ctr->overflow;
+                cj.xext = lb.xext;
                 if (chain_pred) {
                     // large batches: the CTA-pair kernel; the first small one starts the persistent tail,
                     // which finishes the level's chain (k_tail.cu)
@@ -1109,7 +1118,9 @@ int sync_counters(icg_context* c) {
     return ICG_OK;
 }
 
-int issue_render(icg_context* c, const FieldDev& fd, const icg_camera* cam, int W, int H, const float* bg) {
+// xext_ready: c->xext already holds the rendered grid's x-line extents (issue_extract keep_xext)
+int issue_render(icg_context* c, const FieldDev& fd, const icg_camera* cam, int W, int H, const float* bg,
+                 bool xext_ready = false) {
     size_t npx = (size_t)W * H;
     if (int r = c->depth.ensure(npx * 4)) return r;
     if (int r = c->rgb.ensure(npx * 12)) return r;
@@ -1142,11 +1153,13 @@ int issue_render(icg_context* c, const FieldDev& fd, const icg_camera* cam, int 
         int slot = prof_begin(c, 3);
         // rays along world x (the view direction R^T e_z has no y / z part): empty-space skipping
         if (c->use_xext && std::fabs(cam->rotation[7]) < 1e-9 && std::fabs(cam->rotation[8]) < 1e-9) {
-            const size_t lines = ((size_t)rj.cells + 1) * ((size_t)rj.cells + 1);
-            if (int r = c->xext.ensure(lines * sizeof(int2))) return r;
-            if (int r = launch_xline_extents(rj.values, rj.cells, c->xext.as<int2>(), c->stream)) return r;
+            if (!xext_ready) {
+                const size_t lines = ((size_t)rj.cells + 1) * ((size_t)rj.cells + 1);
+                if (int r = c->xext.ensure(lines * sizeof(int2))) return r;
+                if (int r = launch_xline_extents(rj.values, rj.cells, c->xext.as<int2>(), c->stream)) return r;
+                c->launches += 1;
+            }
             rj.xext = c->xext.as<int2>();
-            c->launches += 1;
         }
         int r = launch_render_first_crossing(rj, c->stream);
         prof_end(c, slot);
@@ -1838,9 +1851,12 @@ int icg_frame(icg_context* c, const icg_field* field, const icg_algo_config* cfg
     InflightGuard inflight(c->device);
     c->tail_wide = inflight.alone;
     // the frame's device work: extraction, render + texture, output copies, counters back to the host
+    // rays along grid x: the extraction keeps the final grid's x-line extents for the renderer
+    const bool keep_xext = c->use_xext && cfg->variant == ICG_VARIANT_PROGRESSIVE && cfg->target_level >= 1 &&
+                           std::fabs(cam->rotation[7]) < 1e-9 && std::fabs(cam->rotation[8]) < 1e-9;
     auto body = [&]() -> int {
-        if (int r = issue_extract(c, fd, cfg)) return r;
-        if (int r = issue_render(c, fd, cam, W, H, bg)) return r;
+        if (int r = issue_extract(c, fd, cfg, keep_xext)) return r;
+        if (int r = issue_render(c, fd, cam, W, H, bg, keep_xext)) return r;
         if (int r = finish_render_outputs(c, W, H, img)) return r;
         ICG_CUDA_TRY(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->stream));
         return ICG_OK;

@@ -185,6 +185,9 @@ struct EvalJob {
     float* out;                   // occupancy per point (or rgb x3 for texture)
     const uint32_t* out_pixel;    // texture: pixel index per point (out = rgb image)
     float out_clamp;              // texture: clamp01 when nonzero
+    // nonzero extents of the grid's x-lines kept by the grid epilogue (the frame path's renderer
+    // skips k_xline_extents; nullptr: none): an evaluated nonzero value widens its line's extent
+    int2* xext;
 };
 
 struct FieldDev {
@@ -284,6 +287,7 @@ struct LevelBufs {
     uint32_t* block_counts;                 // per 1024-node block
     uint32_t* list;                         // E0 output
     int rc;                                 // coarse cells
+    int2* xext;                             // k_fine_rows: each fine x-line's nonzero extent (nullptr: none)
 };
 int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s);
 int launch_level_carry(const LevelBufs& b, DevCounters* ctr, int level, cudaStream_t s);
@@ -356,6 +360,7 @@ struct TailParams {
     unsigned *newcols, *nnew;
     unsigned cap_pts, cap_new;
     unsigned long long* trace;  // ICG_TAIL_TRACE=1: phase times of block 0
+    int2* xext;                 // x-line extents kept by the grid epilogue (EvalJob::xext)
 };
 size_t tail_smem_bytes();
 size_t tail_scratch_bytes(unsigned cap_pts, unsigned cap_new, unsigned max_cols);

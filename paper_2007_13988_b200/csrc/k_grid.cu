@@ -170,7 +170,7 @@ static void launch_mixed(const uint32_t* cbin, int rc, uint32_t* mixed, unsigned
 __global__ void __launch_bounds__(kFineThreads, 8)
 k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const uint32_t* __restrict__ cbin,
             const uint32_t* __restrict__ mixed, int rc, float* __restrict__ fv, uint8_t* __restrict__ fs,
-            uint32_t* __restrict__ tentbin, uint32_t* __restrict__ sel) {
+            uint32_t* __restrict__ tentbin, uint32_t* __restrict__ sel, int2* __restrict__ xext) {
     // per warp: one byte per coarse x of the row, (number of binarised parents set, bits 0-2) |
     // (coarse cell x mixed in an adjacent cell row, bit 4); built only for rows near the surface
     __shared__ uint8_t info_s[kFineThreads / 32][32 * kRowWords];
@@ -282,6 +282,22 @@ k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const 
                         }
                     }
                 }
+                if (xext) {  // the row's nonzero extent: u everywhere, or the carried even nodes
+                    int first = fn, last = -1;
+                    if (all1) {
+                        first = (even_jk && __ldg(&cv[cbase]) == 0.0f) ? 1 : 0;
+                        last = (even_jk && __ldg(&cv[cbase + (uint32_t)rc]) == 0.0f) ? fn - 2 : fn - 1;
+                    } else if (even_jk) {
+                        for (int x = lane; x <= rc; x += 32)
+                            if (__ldg(&cv[cbase + (uint32_t)x]) != 0.0f) {
+                                first = min(first, 2 * x);
+                                last = max(last, 2 * x);
+                            }
+                        first = __reduce_min_sync(0xffffffffu, first);
+                        last = __reduce_max_sync(0xffffffffu, last);
+                    }
+                    if (lane == 0) xext[row] = make_int2(first, last);
+                }
                 if (all1) {  // every tentative bit of the row is set: one OR per word
                     const uint32_t last = rowbase + (uint32_t)fn - 1u, w0 = rowbase >> 5, w1 = last >> 5;
                     for (uint32_t w = w0 + (uint32_t)lane; w <= w1; w += 32u) {
@@ -303,9 +319,10 @@ k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const 
                                            (((q2 >> lane) & 1u) << 2) | (((qm >> lane) & 1u) << 4));
         }
         __syncwarp();
+        int nz_first = fn, nz_last = -1;  // the row's nonzero extent (xext)
         for (int i0w = 0; i0w < fn; i0w += 32) {
             const int i = i0w + lane;
-            bool tb = false, sl = false;
+            bool tb = false, sl = false, nz = false;
             if (i < fn) {
                 const int odd = i & 1, x0 = i >> 1;
                 // node i interpolates coarse nodes x0 (and x0 + 1 if odd); its adjacent cells are x0
@@ -330,6 +347,14 @@ k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const 
                 fv[rowbase + i] = v;
                 fs[rowbase + i] = st;
                 sl = flagged && st != ICG_STATE_EVALUATED;  // mask_to_unevaluated_list
+                nz = v != 0.0f;
+            }
+            if (xext) {
+                const unsigned nzw = __ballot_sync(0xffffffffu, nz);
+                if (nzw) {
+                    if (nz_first == fn) nz_first = i0w + __ffs(nzw) - 1;
+                    nz_last = i0w + 31 - __clz(nzw);
+                }
             }
             const unsigned tbw = __ballot_sync(0xffffffffu, tb), sw = __ballot_sync(0xffffffffu, sl);
             // lane 0 merges the tentative bits, lane 1 the selection bits (one code path)
@@ -341,6 +366,7 @@ k_fine_rows(const float* __restrict__ cv, const uint8_t* __restrict__ cs, const 
                 if (sh && (bits >> (32 - sh))) atomicOr(&dst[w + 1], bits >> (32 - sh));
             }
         }
+        if (xext && lane == 0) xext[row] = make_int2(nz_first, nz_last);
     }
 }
 
@@ -492,7 +518,7 @@ int launch_level_carry(const LevelBufs& b, DevCounters* ctr, int level, cudaStre
     ICG_CUDA_TRY(cudaMemsetAsync(b.sel, 0, ((size_t)nwords + 1) * 4, s));
     const unsigned rows = (unsigned)fn * fn;
     const unsigned fine_blocks = std::min<unsigned>((rows + kFineThreads / 32 - 1) / (kFineThreads / 32), 148u * 8u);
-    k_fine_rows<<<fine_blocks, kFineThreads, 0, s>>>(b.cv, b.cs, b.cbin, b.mixed, rc, b.fv, b.fs, b.tentbin, b.sel);
+    k_fine_rows<<<fine_blocks, kFineThreads, 0, s>>>(b.cv, b.cs, b.cbin, b.mixed, rc, b.fv, b.fs, b.tentbin, b.sel, b.xext);
     ICG_CUDA_TRY(cudaGetLastError());
     return ICG_OK;
 }
@@ -516,7 +542,7 @@ int launch_level_classify(const LevelBufs& b, DevCounters* ctr, int level, cudaS
     ICG_CUDA_TRY(cudaMemsetAsync(b.sel, 0, ((size_t)nwords + 1) * 4, s));
     const unsigned rows = (unsigned)fn * fn;
     const unsigned fine_blocks = std::min<unsigned>((rows + kFineThreads / 32 - 1) / (kFineThreads / 32), 148u * 8u);
-    k_fine_rows<<<fine_blocks, kFineThreads, 0, s>>>(b.cv, b.cs, b.cbin, b.mixed, rc, b.fv, b.fs, b.tentbin, b.sel);
+    k_fine_rows<<<fine_blocks, kFineThreads, 0, s>>>(b.cv, b.cs, b.cbin, b.mixed, rc, b.fv, b.fs, b.tentbin, b.sel, b.xext);
     k_count_words<<<nblocks, kWriteThreads, 0, s>>>(b.sel, nwords, b.block_counts);
     k_scan_blocks<<<1, 1024, 0, s>>>(b.block_counts, nblocks, ctr, level);
     k_write_words<<<nblocks, kWriteThreads, 0, s>>>(b.sel, nwords, b.block_counts, b.list);

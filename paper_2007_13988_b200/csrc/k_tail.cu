@@ -356,6 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tail(TailParams P) {
                                     (__ldg(&b5[0]) + w5z * __ldcg(&P.pz[t]) - __ldg(&P.f.fscene->sdf_scale) * sdf);
                     const float v = 1.0f / (1.0f + expf(-s));
                     EvalJob j{};
+                    j.cells = P.cells;
+                    j.xext = P.xext;
                     j.values = P.fv;
                     j.states = P.fs;
                     j.tentbin = P.tentbin;
