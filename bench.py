@@ -456,7 +456,7 @@ def gpu_arm(args, cfg_name: str, rank: int, world: int, local_rank: int, dist):
         executed = fact_pts * FACT_MMA_FLOP_PER_POINT * exec_mult / fact_s / 1e12 if fact_s > 0 else 0.0
         traffic, traffic_note = None, None
         try:  # DRAM bytes of the longest k_fact2 launch of a frame, from the committed ncu --set full capture
-            cap = f"r02b_ncu_full_k_fact2_{cfg_name}.json"
+            cap = f"r02d_ncu_full_k_fact2_{cfg_name}.json"
             rec = json.load(open(os.path.join(ROOT, "profiles", cap)))[0]
             mb = lambda v: float(v.split()[0]) * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}[v.split()[1]]
             traffic = (mb(rec["dram__bytes_read.sum"]) + mb(rec["dram__bytes_write.sum"])) * 1e6
