@@ -736,3 +736,24 @@ def test_odd_feature_map_shape(gpu_ctx, pifu_inputs):
     i, j, k = ev % n, (ev // n) % n, ev // (n * n)
     node_pts = np.stack([-1 + 2 * i / 64.0, -1 + 2 * j / 64.0, 1 - 2 * k / 64.0], 1)
     assert np.abs(g.values[ev] - m.occupancy(node_pts)).max() <= OCC_TOL_FP32
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg_args", [(32, 2), (16, 3)])
+def test_frame_kept_extents_equal_render_of_grid(gpu_ctx, pifu_inputs, cfg_args):
+    """icg_frame keeps the final grid's x-line extents during the extraction (level pass + every
+    evaluation epilogue); rendering the same extracted grid afterwards recomputes them with
+    k_xline_extents.  Both must give identical images, crossing indices and counters."""
+    inp = pifu_inputs
+    gpu_ctx.set_mlp(abi.ICG_MLP_GEOMETRY, inp["gw"], inp["gb"])
+    gpu_ctx.set_mlp(abi.ICG_MLP_TEXTURE, inp["tw"], inp["tb"])
+    f = api.PifuField(inp["fmap"], inp["caps"], 50.0, abi.ICG_PREC_FP32)
+    cfg = api.AlgoConfig("progressive", *cfg_args)
+    cam = api.CameraSpec.from_angles(90, 0)
+    ext, img = gpu_ctx.frame(f, cfg, cam, 192, 160, want_grid=True)
+    img2 = gpu_ctx.render_localized(f, cam, 192, 160)
+    assert img.covered_pixels == img2.covered_pixels > 0
+    assert np.array_equal(img.surface_k, img2.surface_k)
+    assert np.array_equal(img.mask, img2.mask)
+    assert np.array_equal(img.depth, img2.depth)
+    assert np.array_equal(img.rgb, img2.rgb)
